@@ -1,0 +1,279 @@
+#!/usr/bin/env python
+"""Faster-MoA tree request benchmark on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--impl b200|reference]
+
+One *step* = one tree-MoA request (run_query, orchestrator.cpp:130-295) of the
+configured workload, sample index = step % 24 (the preset's 24 repetitions,
+config.cpp:230).  `value` = agent tokens/s = output tokens of invoked,
+unpruned agents / device-event time (first tick -> last completion), summed
+over the K timed requests; L2 is flushed (256 MiB write) between requests,
+outside each request's events.  `e2e` = the same metric through the C-ABI call
+with host buffers (prompt synthesis, row upload, result read-back) on the host
+wall clock.  Multi-GPU (torchrun): each rank serves its own requests
+(replicas), value = all ranks' tokens / max rank time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "tree_moa_agent_tokens_per_s"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C1")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-baseline-s", type=float, default=15.0, help="CPU sample budget (seconds)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="run steps without JSON (for ncu)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.rows, self.stop = device, [], threading.Event()
+
+    def _loop(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 7:
+                    self.rows.append(vals)
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._loop, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return j["hbm_gbs"], j["bf16_tflops"], "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def cpu_baseline(cfg, budget_s):
+    """The oracle (numpy transformer + reference-semantics orchestration) on
+    a bounded sample of the same workload, all host cores."""
+    import numpy as np  # noqa: F401
+
+    from oracle.configs import models_of, run_config
+    from oracle.orchestrator import run_query
+    rc = run_config(cfg)
+    ms = models_of(cfg, 1024)
+    t0, toks, n = time.perf_counter(), 0, 0
+    while True:
+        r = run_query(rc, ms, n % 24)
+        toks += r["tokens"]
+        n += 1
+        if time.perf_counter() - t0 > budget_s or n >= 24:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": toks / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{n} {cfg['name']} requests (samples 0..{n - 1}), oracle/orchestrator.py + numpy fp32 "
+                      f"transformer, {os.cpu_count()} host threads", "seconds": dt, "tokens": toks}
+
+
+def reference_simulator_time(cfg, reps=24):
+    """Wall time of the reference's own run_repetitions (the virtual-time
+    simulator, oracle/_ref) on the same tree shape -- context only."""
+    lib = ROOT / "oracle" / "_ref" / "libmoaref.so"
+    if not lib.exists():
+        return None
+    import ctypes
+    L = ctypes.CDLL(str(lib))
+    L.moaref_call.restype = ctypes.c_char_p
+    t = cfg["topology"]
+    req = {"cmd": "time_run_query", "topology": t, "reps": reps,
+           "profiles": {tag: {"output_len": cfg["out_len"][0] if isinstance(cfg["out_len"][0], int) else 64}
+                        for tag in cfg["models"]},
+           "assign": cfg["assign"], "mode": cfg["mode"], "early_exit": cfg["early_exit"],
+           "chunk_size": cfg["chunk_size"], "seed": cfg["seed"]}
+    r = json.loads(L.moaref_call(json.dumps(req).encode()))
+    if "seconds" not in r:
+        return None
+    return {"seconds_per_request": r["seconds"] / reps, "reps": reps, "cores": 1,
+            "note": "reference SimWorld (virtual-time, no model compute), orchestrator.cpp:297-302"}
+
+
+def run_reference_arm(args, cfg, rank, world):
+    if rank != 0:
+        return
+    steps = []
+    from oracle.configs import models_of, run_config
+    from oracle.orchestrator import run_query
+    rc, ms = run_config(cfg), models_of(cfg, 1024)
+    for i in range(args.warmup):
+        run_query(rc, ms, i % 24)
+    t_all = time.perf_counter()
+    toks = 0
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        r = run_query(rc, ms, i % 24)
+        steps.append(time.perf_counter() - t0)
+        toks += r["tokens"]
+    dt = time.perf_counter() - t_all
+    value = toks / dt
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "p50_ms_per_request": 1e3 * statistics.median(steps), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "name": cfg["name"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"{args.steps} {cfg['name']} requests through oracle/ (numpy fp32 "
+                                       f"transformer agents + reference-semantics orchestration)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    sim = reference_simulator_time(cfg)
+    if sim:
+        line["reference_simulator"] = sim
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    from paper_2512_18126_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    from paper_2512_18126_b200 import capi
+
+    eng, qc = capi.engine_for(cfg, device=local)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
+
+    def one(i, detail=False):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        return eng.run_query(qc, sample=(rank * 1000 + i) % 24, resolve=detail, detail=detail)
+
+    for i in range(args.warmup):
+        one(i)
+    if args.profile_only:
+        for i in range(args.steps):
+            one(i)
+        return
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    dev_ms, toks, per_req, rows, fwd, wbytes = 0.0, 0, [], 0, 0, 0.0
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            s = one(i)
+            dev_ms += s["e2e_ms"]
+            per_req.append(s["e2e_ms"])
+            toks += s["tokens"]
+            rows += s["rows"]
+            fwd += s["forwards"]
+            wbytes += s["weight_bytes"]
+    torch.cuda.synchronize()
+    # e2e: through the C-ABI with host buffers (resolve = copy results back)
+    e2e_wall, e2e_toks, h2d, d2h = 0.0, 0, 0, 0
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = eng.run_query(qc, sample=(rank * 1000 + i) % 24, resolve=True, detail=True)
+        e2e_wall += time.perf_counter() - t0
+        e2e_toks += r["tokens"]
+        h2d += r["rows"] * 16
+        d2h += sum(4 * len(a["prompt"]) + 12 * len(a["output"]) for a in r["agents"].values())
+    if pg:
+        t = torch.tensor([dev_ms, e2e_wall * 1e3, toks, e2e_toks], dtype=torch.float64, device="cuda")
+        mx = t.clone()
+        pg.all_reduce(mx, op=pg.ReduceOp.MAX)
+        sm = t.clone()
+        pg.all_reduce(sm, op=pg.ReduceOp.SUM)
+        dev_ms_max, e2e_ms_max, toks_all, e2e_toks_all = mx[0].item(), mx[1].item(), sm[2].item(), sm[3].item()
+    else:
+        dev_ms_max, e2e_ms_max, toks_all, e2e_toks_all = dev_ms, e2e_wall * 1e3, toks, e2e_toks
+    if rank != 0:
+        if pg:
+            pg.destroy_process_group()
+        return
+    hbm, tf, src = peaks()
+    value = toks_all / (dev_ms_max / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps,
+        "p50_ms_per_request": statistics.median(per_req), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "name": cfg["name"], "l2": "flushed (256 MiB write) between requests",
+                   "models": {t: m["shape"] for t, m in cfg["models"].items()}, "parallelism": f"replicas{world}"},
+        "e2e": {"value": e2e_toks_all / (e2e_ms_max / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps},
+        "gpu_launches": None,
+        "clocks": clk.summary(),
+        "peaks": {"hbm_gbs": hbm, "bf16_tflops": tf, "source": src},
+        "engine": {"rows_per_request": rows / args.steps, "forwards_per_request": fwd / args.steps,
+                   "weight_gb_per_request": wbytes / args.steps / 1e9,
+                   "weight_stream_gbs": wbytes / (dev_ms / 1e3) / 1e9},
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_baseline_s)
+    print(json.dumps(line), flush=True)
+    eng.close()
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

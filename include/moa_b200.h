@@ -1,0 +1,209 @@
+/*
+ * moa_b200.h -- C-ABI of the B200 Faster-MoA agent-execution hot path.
+ *
+ * Drop-in boundary for the reference's proj/core path (arXiv 2512.18126,
+ * "moaserve").  Plain C types only: caller-owned host buffers in, results
+ * copied into caller buffers out; the engine owns weights, KV caches and
+ * generated tokens on the GPU.  Every function returns a status code
+ * (MOA_OK on success); moa_last_error() returns the thread-local message of
+ * the last failure.  Status codes map onto the reference's error types
+ * (errors.hpp:10-33): MOA_ERR_VALIDATION = ValidationError (CLI exit 2),
+ * MOA_ERR_RUNTIME = RunError (CLI exit 3).
+ *
+ * Reference interfaces replaced (file:line under /root/reference/proj):
+ *   engine protocol   SimWorld            core/include/moaserve/pdsim.hpp:61-156
+ *   request entry     run_query           core/include/moaserve/orchestrator.hpp:57
+ *   early-exit        MetricQEvaluator    core/include/moaserve/metricq.hpp:25-122
+ *   embedding plugin  EmbeddingProvider   core/include/moaserve/embedding.hpp:38-44
+ *   routing           Topology / SlotPlan core/include/moaserve/topology.hpp:28-80,
+ *                                         core/include/moaserve/router.hpp:36-90
+ * INTEGRATION.md shows the C++ adapter a maintainer adds on the reference side.
+ */
+#ifndef MOA_B200_H
+#define MOA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOA_OK 0
+#define MOA_ERR_VALIDATION 2 /* ValidationError (errors.hpp:10-13)            */
+#define MOA_ERR_RUNTIME 3    /* RunError        (errors.hpp:17-20)            */
+#define MOA_ERR_DEVICE 4     /* CUDA failure (a RunError on the reference side) */
+#define MOA_ERR_UNSUPPORTED 5
+
+typedef struct moa_engine moa_engine;
+typedef struct moa_query moa_query;
+typedef struct moa_slotplan moa_slotplan;
+
+const char* moa_last_error(void);
+const char* moa_version(void);
+int moa_device_count(int* n);
+
+/* ---- engine lifecycle ------------------------------------------------- */
+
+/* One agent model (builder-chosen Llama-style shape; random uniform-hash
+ * init from (seed, tag) -- bit-identical with oracle/model.py). */
+typedef struct {
+  char tag[32];
+  int d, n_layers, n_heads, n_kv_heads, head_dim, ffn, vocab;
+  double rope_theta, norm_eps, lm_gain;
+  uint64_t seed;
+  int max_agents; /* agents that may bind this model at once */
+} moa_model_spec;
+
+typedef struct {
+  int max_ctx;     /* KV positions per agent                 */
+  int max_out;     /* output tokens per agent                */
+  int max_rows;    /* rows per tick (prefill budget)         */
+  int device;      /* CUDA device ordinal                    */
+  int keep_logits; /* debug: retain fp32 logits per token    */
+} moa_engine_opts;
+
+int moa_engine_create(const moa_model_spec* models, int n_models, const moa_engine_opts* opts,
+                      moa_engine** out);
+int moa_engine_destroy(moa_engine* eng);
+/* Drops every request; weights and buffers stay resident. */
+int moa_engine_reset(moa_engine* eng);
+
+/* ---- SimWorld engine protocol (pdsim.hpp:61-156) ------------------------
+ * Agents are (layer, position) = AgentId (agent.hpp:16-37).  Tokens passed
+ * in are literal ids in [0, vocab).  Time advances by moa_step ticks.      */
+int moa_add_agent(moa_engine* eng, int layer, int position, int model);
+/* submit_prefill_only (pdsim.cpp:155-174): start must equal the scheduled
+ * prompt length (contiguity) or MOA_ERR_RUNTIME. */
+int moa_prefill_only(moa_engine* eng, int layer, int position, int start, const int32_t* tokens,
+                     int n);
+/* submit_generate (pdsim.cpp:176-214): prompt must extend the scheduled
+ * prefix; the engine decodes max_new greedy tokens and announces them every
+ * apc_chunk tokens.  prefill_chunk > 0 splits the remainder (DpChunkedPrefill). */
+int moa_generate(moa_engine* eng, int layer, int position, const int32_t* prompt, int n, int max_new,
+                 int apc_chunk, int prefill_chunk);
+int moa_cancel(moa_engine* eng, int layer, int position);            /* pdsim.cpp:374-398 */
+int moa_reclaim(moa_engine* eng, int layer, int position, int keep); /* pdsim.cpp:400-418 */
+
+#define MOA_EV_CHUNK 1      /* a = begin, b = end (output offsets)   */
+#define MOA_EV_DECODE_END 2 /* a = output tokens                     */
+#define MOA_EV_CANCEL 3     /* a = tokens emitted before the cancel  */
+#define MOA_EV_RECLAIM 4    /* a = keep point                        */
+typedef struct {
+  int kind, tick, layer, position, a, b;
+} moa_event;
+
+/* Runs one engine tick; returns the tick's events (chunk/decode_end/...) and
+ * whether work remains.  Chunk tokens are read with moa_read_output. */
+int moa_step(moa_engine* eng, moa_event* events, int cap, int* n_events, int* busy);
+int moa_busy(moa_engine* eng, int* busy);
+/* First n outputs of an agent (tokens, fp32 logprob of the greedy token,
+ * fp32 softmax entropy).  Any pointer may be NULL. */
+int moa_read_output(moa_engine* eng, int layer, int position, int n, int32_t* tokens, float* logprobs,
+                    float* entropy);
+int moa_read_logits(moa_engine* eng, int layer, int position, int k, float* logits /* [vocab] */);
+int moa_agent_state(moa_engine* eng, int layer, int position, int* scheduled, int* decoded,
+                    int* finished, int* cancelled);
+
+/* ---- run_query (orchestrator.cpp:130-295) ------------------------------ */
+#define MOA_TOPO_TREE 0
+#define MOA_TOPO_ALL_TO_ALL 1
+#define MOA_MODE_SEQUENTIAL_PD 0
+#define MOA_MODE_DP_ONLY 1
+#define MOA_MODE_DP_CHUNKED_PREFILL 2
+#define MOA_MODE_INCREMENTAL_OVERLAP 3
+#define MOA_SCOPE_CLUSTER 0
+#define MOA_SCOPE_LAYER 1
+
+typedef struct {
+  int topo_kind;
+  int n_layers;
+  const int* widths;        /* [n_layers]                                        */
+  const int* cluster_sizes; /* tree: sum(widths[1:]) sizes, layer by layer; NULL = all-to-all */
+  const int* model_cycle;   /* concatenated per-layer model-index cycles (config.cpp:252-265) */
+  const int* cycle_len;     /* [n_layers]                                        */
+  const int* out_lo;        /* [n_layers] output length: fixed (lo == hi) or U(lo, hi) */
+  const int* out_hi;
+  int mode, early_exit, exit_scope;
+  double tau;
+  int include_diagonal;
+  int use_force_q;
+  double force_q;
+  int chunk_size;
+  uint64_t seed;
+  int query_tokens, leaf_prefix_tokens, agg_prefix_tokens, separator_tokens, suffix_tokens;
+  int hidden; /* mock embedding width (ProviderSpec::hidden) */
+  uint64_t provider_seed;
+} moa_run_config;
+
+typedef struct {
+  int ticks;
+  int n_agents;
+  int n_evals;
+  int forwards;
+  long long tokens;         /* output tokens of invoked, unpruned agents */
+  long long decoded_tokens; /* every token decoded (incl. pruned partials) */
+  long long rows;
+  double e2e_ms;       /* device events: first tick -> last completion */
+  double wall_ms;      /* host wall clock of the whole call            */
+  double weight_bytes; /* weight bytes the forwards had to read        */
+} moa_run_summary;
+
+typedef struct {
+  int layer, position, model;
+  int invoked, pruned, empty_input;
+  int prompt_tokens, output_tokens;
+  int prefill_only_calls, recomputed_tokens, reclaimed_tokens;
+  int decode_start, decode_end, complete, precursor_ready;
+} moa_agent_record;
+
+typedef struct {
+  int tick, group, eval_index, layer, position, evaluated, exited, n_pruned, outputs;
+  double q, draw, c, c_bar, weight_sum, weighted, calibrated;
+  int pruned_layer[16], pruned_position[16];
+} moa_eval_record;
+
+/* resolve != 0 copies literal prompts/outputs back (needed by moa_query_*). */
+int moa_run_query(moa_engine* eng, const moa_run_config* cfg, int sample, int resolve,
+                  moa_run_summary* summary, moa_query** out /* may be NULL */);
+int moa_query_agent(const moa_query* q, int i, moa_agent_record* rec);
+/* which: 0 = prompt, 1 = output. */
+int moa_query_tokens(const moa_query* q, int i, int which, int32_t* dst, int cap, int* n);
+int moa_query_logprobs(const moa_query* q, int i, float* logprobs, float* entropy, int cap, int* n);
+int moa_query_eval(const moa_query* q, int i, moa_eval_record* rec, double* sim_row, int cap);
+int moa_query_free(moa_query* q);
+
+/* ---- early-exit signals (metricq.hpp:25-122, embedding.cpp:86-120) ------ */
+/* MockProvider::embed on the GPU: out[n][hidden] fp64, bit-exact. */
+int moa_mock_embed(const int32_t* tokens, int n, int hidden, uint64_t seed, double* out, int device);
+/* Incremental MetricQ over m completions (lengths lens[i], concatenated
+ * tokens / logprobs), exit draws from RngStream::derive(master, label).
+ * Per completion i: out6[i] = {c, c_bar, W, P, B, q}, draw[i], exited[i];
+ * sim_out = final m x m similarity matrix (row-major). */
+int moa_metricq_run(const int32_t* tokens, const float* logprobs, const int* lens, int m, int hidden,
+                    uint64_t seed, double tau, int include_diagonal, uint64_t master, const char* label,
+                    double* out6, double* draw, int* exited, double* sim_out, int device);
+
+/* ---- routing (topology.cpp:43-196, router.cpp:9-184) ------------------- */
+/* precursor lists: for agent k (layer-major order) pre_off[k]..pre_off[k+1]
+ * index into pre (as layer-major agent indices). */
+int moa_topology(int kind, int n_layers, const int* widths, const int* cluster_sizes, int* pre_off,
+                 int* pre, int cap);
+int moa_slotplan_create(int self_layer, int self_position, const int32_t* prefix, int n_prefix,
+                        const int* slot_layer, const int* slot_position, const int32_t* sep_tokens,
+                        const int* sep_lens, int n_slots, const int32_t* suffix, int n_suffix,
+                        int incremental, moa_slotplan** out);
+/* op: 0 start, 1 chunk, 2 done, 3 cancelled.  Actions are serialised into
+ * buf as [kind, start, n, tokens...]* (kind 0 prefill_only, 1 generate,
+ * 2 reclaim); *n_words receives the length. */
+int moa_slotplan_event(moa_slotplan* p, int op, int layer, int position, const int32_t* tokens, int n,
+                       int32_t* buf, int cap, int* n_words);
+int moa_slotplan_free(moa_slotplan* p);
+
+/* ---- kernel entry points (device pointers; tests and profiling) -------- */
+int moa_k_gemm_skinny(uintptr_t A, int R, uintptr_t W, int N, int K, int S, uintptr_t P, uintptr_t stream);
+int moa_k_init_uniform(uintptr_t dst, long long n, uint64_t base, float scale, uintptr_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOA_B200_H */

@@ -1,0 +1,219 @@
+"""CPU transformer agent -- TEST INFRASTRUCTURE (the checker for the B200 path).
+
+The reference has no model (it synthesises outputs, orchestrator.cpp:87-116),
+so this is a restatement of OUR engine's numerics contract:
+Llama-style decoder (RMSNorm, RoPE rotate-half, GQA, SwiGLU), bf16 weights,
+fp32 math, with the activations rounded to bf16 at exactly the points the CUDA
+kernels round them:
+
+  rp1  h  = bf16(rmsnorm(x) * g)            (GEMM A operand)
+  rp2  q,k = bf16(rope(fp32 acc)); v = bf16(acc)   (KV cache is bf16)
+  rp3  o  = bf16(softmax(q k^T / sqrt(hd)) v)
+  rp4  a  = bf16(silu(g_acc) * u_acc)
+  residual stream x stays fp32; logits fp32.
+
+Weights: uniform hash init, bit-identical with the device init kernel:
+bits_i = mix64(base_T + i), base_T = hash_combine(hash_combine(seed,
+fnv1a(tag)), fnv1a(T)); w = bf16(fp32((bits>>40) * 2^-23 - 1) * scale_T).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .rng import fnv1a, hash_combine, mix64_np
+
+VOCAB = 50000
+
+
+@dataclass(frozen=True)
+class ModelSpec:
+    tag: str
+    d: int
+    n_layers: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    ffn: int
+    vocab: int = VOCAB
+    rope_theta: float = 10000.0
+    norm_eps: float = 1e-5
+    lm_gain: float = 4.0
+    seed: int = 0
+
+
+# Shapes from SURVEY.md §8 (builder's choice; the reference has none).
+SHAPES = {
+    "tiny": dict(d=256, n_layers=4, n_heads=4, n_kv_heads=4, head_dim=64, ffn=1024),
+    "1b": dict(d=2048, n_layers=16, n_heads=32, n_kv_heads=8, head_dim=64, ffn=8192),
+    "8b": dict(d=4096, n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, ffn=14336),
+}
+
+
+def make_spec(tag: str, shape: str, seed: int = 0, **kw) -> ModelSpec:
+    return ModelSpec(tag=tag, seed=seed, **{**SHAPES[shape], **kw})
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """fp32 -> bf16 (round to nearest even) -> fp32, like __float2bfloat16_rn."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    b = x.view(np.uint32).astype(np.uint64)
+    r = ((b + 0x7FFF + ((b >> 16) & 1)) >> 16) << 16
+    out = r.astype(np.uint32).view(np.float32)
+    nan = np.isnan(x)
+    if nan.any():
+        out = np.where(nan, x, out)
+    return out
+
+
+def tensor_scale(spec: ModelSpec, name: str) -> np.float32:
+    """Per-tensor uniform half-width; fp64 formula then one cast to fp32."""
+    if name == "emb":
+        s = 1.0
+    elif name == "lm":
+        s = math.sqrt(3.0 / spec.d) * spec.lm_gain
+    else:
+        k = {"wq": spec.d, "wk": spec.d, "wv": spec.d, "wg": spec.d, "wu": spec.d,
+             "wo": spec.n_heads * spec.head_dim, "wd": spec.ffn}[name.split(".")[-1]]
+        s = math.sqrt(3.0 / k)
+    return np.float32(s)
+
+
+def init_tensor(spec: ModelSpec, name: str, rows: int, cols: int) -> np.ndarray:
+    """Hash-uniform bf16 weights (as fp32 values), logical [rows, cols]."""
+    base = hash_combine(hash_combine(spec.seed, fnv1a(spec.tag)), fnv1a(name))
+    n = rows * cols
+    out = np.empty(n, dtype=np.float32)
+    scale = tensor_scale(spec, name)
+    step = 1 << 24
+    with np.errstate(over="ignore"):
+        for s0 in range(0, n, step):
+            idx = np.arange(s0, min(n, s0 + step), dtype=np.uint64)
+            bits = mix64_np(idx + np.uint64(base))
+            u = (bits >> np.uint64(40)).astype(np.float32) * np.float32(2.0 ** -23) - np.float32(1.0)
+            out[s0:s0 + len(idx)] = u * scale
+    return bf16_round(out).reshape(rows, cols)
+
+
+class Weights:
+    def __init__(self, spec: ModelSpec):
+        self.spec = spec
+        d, hd, nh, nkv, f, V = spec.d, spec.head_dim, spec.n_heads, spec.n_kv_heads, spec.ffn, spec.vocab
+        self.emb = init_tensor(spec, "emb", V, d)
+        self.layers = []
+        for l in range(spec.n_layers):
+            p = f"L{l}."
+            self.layers.append(dict(
+                wq=init_tensor(spec, p + "wq", nh * hd, d),
+                wk=init_tensor(spec, p + "wk", nkv * hd, d),
+                wv=init_tensor(spec, p + "wv", nkv * hd, d),
+                wo=init_tensor(spec, p + "wo", d, nh * hd),
+                wg=init_tensor(spec, p + "wg", f, d),
+                wu=init_tensor(spec, p + "wu", f, d),
+                wd=init_tensor(spec, p + "wd", d, f),
+            ))
+        self.lm = init_tensor(spec, "lm", V, d)
+
+
+def rope_table(spec: ModelSpec, max_pos: int):
+    """cos/sin [max_pos, hd/2] in fp64 (libm) then cast to fp32 -- the device
+    uses the identical table computed by the host library."""
+    half = spec.head_dim // 2
+    cos = np.empty((max_pos, half), dtype=np.float32)
+    sin = np.empty((max_pos, half), dtype=np.float32)
+    inv = [spec.rope_theta ** (-2.0 * i / spec.head_dim) for i in range(half)]
+    for p in range(max_pos):
+        for i in range(half):
+            a = p * inv[i]
+            cos[p, i] = math.cos(a)
+            sin[p, i] = math.sin(a)
+    return cos, sin
+
+
+def rmsnorm(x: np.ndarray, eps: float) -> np.ndarray:
+    ms = np.mean(x * x, axis=-1, keepdims=True, dtype=np.float32)
+    return x * (np.float32(1.0) / np.sqrt(ms + np.float32(eps)))
+
+
+def logit_stats(logits: np.ndarray):
+    """argmax (lowest index on ties), logprob(argmax) = -log S, entropy
+    H = log S - T/S with S = sum e^(l-m), T = sum (l-m) e^(l-m)."""
+    tok = np.argmax(logits, axis=-1)
+    m = logits.max(axis=-1, keepdims=True)
+    z = logits - m
+    e = np.exp(z)
+    S = e.sum(axis=-1)
+    T = (z * e).sum(axis=-1)
+    lp = -np.log(S)
+    ent = np.log(S) - T / S
+    return tok.astype(np.int32), lp.astype(np.float32), ent.astype(np.float32)
+
+
+class AgentKV:
+    def __init__(self, spec: ModelSpec, max_ctx: int):
+        self.k = np.zeros((spec.n_layers, spec.n_kv_heads, max_ctx, spec.head_dim), np.float32)
+        self.v = np.zeros_like(self.k)
+
+
+class CpuModel:
+    """Batched ragged forward over rows (agent kv, position, token)."""
+
+    def __init__(self, spec: ModelSpec, max_ctx: int = 4096):
+        self.spec = spec
+        self.w = Weights(spec)
+        self.cos, self.sin = rope_table(spec, max_ctx)
+        self.max_ctx = max_ctx
+
+    def new_kv(self) -> AgentKV:
+        return AgentKV(self.spec, self.max_ctx)
+
+    def forward(self, rows, want_logits):
+        """rows: list of (kv: AgentKV, pos, token); rows of one agent appear in
+        ascending position order.  Returns (logits[n_out, V]) for rows whose
+        want_logits flag is set."""
+        sp, w = self.spec, self.w
+        R = len(rows)
+        hd, nh, nkv = sp.head_dim, sp.n_heads, sp.n_kv_heads
+        half = hd // 2
+        grp = nh // nkv
+        pos = np.array([r[1] for r in rows])
+        x = w.emb[np.array([r[2] for r in rows])].astype(np.float32)
+        cos, sin = self.cos[pos][:, None, :], self.sin[pos][:, None, :]
+        scale = np.float32(1.0 / math.sqrt(hd))
+        for l, L in enumerate(w.layers):
+            h = bf16_round(rmsnorm(x, sp.norm_eps))
+            q = (h @ L["wq"].T).reshape(R, nh, hd)
+            k = (h @ L["wk"].T).reshape(R, nkv, hd)
+            v = bf16_round(h @ L["wv"].T).reshape(R, nkv, hd)
+
+            def rope(t):
+                a, b = t[..., :half], t[..., half:]
+                return np.concatenate([a * cos - b * sin, b * cos + a * sin], axis=-1)
+
+            q, k = bf16_round(rope(q)), bf16_round(rope(k))
+            for i, (kv, p, _) in enumerate(rows):
+                kv.k[l, :, p] = k[i]
+                kv.v[l, :, p] = v[i]
+            o = np.empty((R, nh, hd), np.float32)
+            for i, (kv, p, _) in enumerate(rows):
+                K = kv.k[l, :, : p + 1]  # [nkv, p+1, hd]
+                V = kv.v[l, :, : p + 1]
+                qi = q[i].reshape(nkv, grp, hd)
+                s = np.einsum("kgd,ktd->kgt", qi, K) * scale
+                s = s - s.max(axis=-1, keepdims=True)
+                e = np.exp(s)
+                o[i] = (np.einsum("kgt,ktd->kgd", e, V) / e.sum(axis=-1, keepdims=True)).reshape(nh, hd)
+            o = bf16_round(o.reshape(R, nh * hd))
+            x = x + o @ L["wo"].T
+            h2 = bf16_round(rmsnorm(x, sp.norm_eps))
+            g = h2 @ L["wg"].T
+            u = h2 @ L["wu"].T
+            a = bf16_round(g / (np.float32(1.0) + np.exp(-g)) * u)
+            x = x + a @ L["wd"].T
+        sel = np.nonzero(np.asarray(want_logits, bool))[0]
+        if len(sel) == 0:
+            return np.zeros((0, sp.vocab), np.float32)
+        hf = bf16_round(rmsnorm(x[sel], sp.norm_eps))
+        return hf @ w.lm.T

@@ -1,0 +1,364 @@
+"""ctypes binding of include/moa_b200.h (the reference-facing C-ABI).
+
+This is the same binding a Python caller of the reference path would add
+(INTEGRATION.md); the tests and bench.py drive the B200 path only through it.
+There is no fallback: if libmoa_b200.so is missing or the GPU is absent the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+from . import configs as _configs
+
+LIB_PATH = Path(__file__).resolve().parent / "libmoa_b200.so"
+
+MOA_OK, MOA_ERR_VALIDATION, MOA_ERR_RUNTIME, MOA_ERR_DEVICE, MOA_ERR_UNSUPPORTED = 0, 2, 3, 4, 5
+MODES = {"sequential-pd": 0, "dp-only": 1, "dp-chunked-prefill": 2, "incremental-overlap": 3}
+EVENT_KINDS = {1: "chunk", 2: "decode_end", 3: "cancel", 4: "reclaim"}
+
+
+class ValidationError(Exception):
+    """MOA_ERR_VALIDATION -- the reference's ValidationError (errors.hpp:10-13)."""
+
+
+class RunError(Exception):
+    """MOA_ERR_RUNTIME -- the reference's RunError (errors.hpp:17-20)."""
+
+
+class DeviceError(RunError):
+    """MOA_ERR_DEVICE -- CUDA failure."""
+
+
+class ModelSpec(C.Structure):
+    _fields_ = [("tag", C.c_char * 32), ("d", C.c_int), ("n_layers", C.c_int), ("n_heads", C.c_int),
+                ("n_kv_heads", C.c_int), ("head_dim", C.c_int), ("ffn", C.c_int), ("vocab", C.c_int),
+                ("rope_theta", C.c_double), ("norm_eps", C.c_double), ("lm_gain", C.c_double),
+                ("seed", C.c_uint64), ("max_agents", C.c_int)]
+
+
+class EngineOpts(C.Structure):
+    _fields_ = [("max_ctx", C.c_int), ("max_out", C.c_int), ("max_rows", C.c_int), ("device", C.c_int),
+                ("keep_logits", C.c_int)]
+
+
+class Event(C.Structure):
+    _fields_ = [("kind", C.c_int), ("tick", C.c_int), ("layer", C.c_int), ("position", C.c_int),
+                ("a", C.c_int), ("b", C.c_int)]
+
+
+_P = C.POINTER
+
+
+class RunConfigC(C.Structure):
+    _fields_ = [("topo_kind", C.c_int), ("n_layers", C.c_int), ("widths", _P(C.c_int)),
+                ("cluster_sizes", _P(C.c_int)), ("model_cycle", _P(C.c_int)), ("cycle_len", _P(C.c_int)),
+                ("out_lo", _P(C.c_int)), ("out_hi", _P(C.c_int)), ("mode", C.c_int), ("early_exit", C.c_int),
+                ("exit_scope", C.c_int), ("tau", C.c_double), ("include_diagonal", C.c_int),
+                ("use_force_q", C.c_int), ("force_q", C.c_double), ("chunk_size", C.c_int),
+                ("seed", C.c_uint64), ("query_tokens", C.c_int), ("leaf_prefix_tokens", C.c_int),
+                ("agg_prefix_tokens", C.c_int), ("separator_tokens", C.c_int), ("suffix_tokens", C.c_int),
+                ("hidden", C.c_int), ("provider_seed", C.c_uint64)]
+
+
+class RunSummary(C.Structure):
+    _fields_ = [("ticks", C.c_int), ("n_agents", C.c_int), ("n_evals", C.c_int), ("forwards", C.c_int),
+                ("tokens", C.c_longlong), ("decoded_tokens", C.c_longlong), ("rows", C.c_longlong),
+                ("e2e_ms", C.c_double), ("wall_ms", C.c_double), ("weight_bytes", C.c_double)]
+
+
+class AgentRecordC(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("layer", "position", "model", "invoked", "pruned", "empty_input",
+                                       "prompt_tokens", "output_tokens", "prefill_only_calls",
+                                       "recomputed_tokens", "reclaimed_tokens", "decode_start", "decode_end",
+                                       "complete", "precursor_ready")]
+
+
+class EvalRecordC(C.Structure):
+    _fields_ = ([(n, C.c_int) for n in ("tick", "group", "eval_index", "layer", "position", "evaluated", "exited",
+                                        "n_pruned", "outputs")]
+                + [(n, C.c_double) for n in ("q", "draw", "c", "c_bar", "weight_sum", "weighted", "calibrated")]
+                + [("pruned_layer", C.c_int * 16), ("pruned_position", C.c_int * 16)])
+
+
+_lib = None
+
+_SIGS = {
+    "moa_last_error": ([], C.c_char_p),
+    "moa_version": ([], C.c_char_p),
+    "moa_device_count": ([_P(C.c_int)], C.c_int),
+    "moa_engine_create": ([_P(ModelSpec), C.c_int, _P(EngineOpts), _P(C.c_void_p)], C.c_int),
+    "moa_engine_destroy": ([C.c_void_p], C.c_int),
+    "moa_engine_reset": ([C.c_void_p], C.c_int),
+    "moa_add_agent": ([C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
+    "moa_prefill_only": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_int32), C.c_int], C.c_int),
+    "moa_generate": ([C.c_void_p, C.c_int, C.c_int, _P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
+    "moa_cancel": ([C.c_void_p, C.c_int, C.c_int], C.c_int),
+    "moa_reclaim": ([C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
+    "moa_step": ([C.c_void_p, _P(Event), C.c_int, _P(C.c_int), _P(C.c_int)], C.c_int),
+    "moa_busy": ([C.c_void_p, _P(C.c_int)], C.c_int),
+    "moa_read_output": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_int32), _P(C.c_float), _P(C.c_float)],
+                        C.c_int),
+    "moa_read_logits": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_float)], C.c_int),
+    "moa_agent_state": ([C.c_void_p, C.c_int, C.c_int] + [_P(C.c_int)] * 4, C.c_int),
+    "moa_run_query": ([C.c_void_p, _P(RunConfigC), C.c_int, C.c_int, _P(RunSummary), _P(C.c_void_p)], C.c_int),
+    "moa_query_agent": ([C.c_void_p, C.c_int, _P(AgentRecordC)], C.c_int),
+    "moa_query_tokens": ([C.c_void_p, C.c_int, C.c_int, _P(C.c_int32), C.c_int, _P(C.c_int)], C.c_int),
+    "moa_query_logprobs": ([C.c_void_p, C.c_int, _P(C.c_float), _P(C.c_float), C.c_int, _P(C.c_int)], C.c_int),
+    "moa_query_eval": ([C.c_void_p, C.c_int, _P(EvalRecordC), _P(C.c_double), C.c_int], C.c_int),
+    "moa_query_free": ([C.c_void_p], C.c_int),
+    "moa_mock_embed": ([_P(C.c_int32), C.c_int, C.c_int, C.c_uint64, _P(C.c_double), C.c_int], C.c_int),
+    "moa_metricq_run": ([_P(C.c_int32), _P(C.c_float), _P(C.c_int), C.c_int, C.c_int, C.c_uint64, C.c_double,
+                         C.c_int, C.c_uint64, C.c_char_p, _P(C.c_double), _P(C.c_double), _P(C.c_int),
+                         _P(C.c_double), C.c_int], C.c_int),
+    "moa_topology": ([C.c_int, C.c_int, _P(C.c_int), _P(C.c_int), _P(C.c_int), _P(C.c_int), C.c_int], C.c_int),
+    "moa_slotplan_create": ([C.c_int, C.c_int, _P(C.c_int32), C.c_int, _P(C.c_int), _P(C.c_int), _P(C.c_int32),
+                             _P(C.c_int), C.c_int, _P(C.c_int32), C.c_int, C.c_int, _P(C.c_void_p)], C.c_int),
+    "moa_slotplan_event": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_int32), C.c_int, _P(C.c_int32), C.c_int,
+                            _P(C.c_int)], C.c_int),
+    "moa_slotplan_free": ([C.c_void_p], C.c_int),
+    "moa_k_gemm_skinny": ([C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_size_t, C.c_size_t],
+                          C.c_int),
+    "moa_k_init_uniform": ([C.c_size_t, C.c_longlong, C.c_uint64, C.c_float, C.c_size_t], C.c_int),
+}
+
+EXPORTED = tuple(_SIGS)
+
+
+def lib():
+    """Load libmoa_b200.so (fails loudly when it was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2512_18126_b200.build`")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (args, res) in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes, f.restype = args, res
+        _lib = L
+    return _lib
+
+
+def check(rc: int):
+    if rc == MOA_OK:
+        return
+    msg = lib().moa_last_error().decode(errors="replace")
+    if rc == MOA_ERR_VALIDATION:
+        raise ValidationError(msg)
+    if rc == MOA_ERR_DEVICE:
+        raise DeviceError(msg)
+    raise RunError(msg)
+
+
+def _ints(v):
+    v = [int(x) for x in v]
+    return (C.c_int32 * max(1, len(v)))(*v), len(v)
+
+
+SHAPES = {
+    "tiny": dict(d=256, n_layers=4, n_heads=4, n_kv_heads=4, head_dim=64, ffn=1024),
+    "1b": dict(d=2048, n_layers=16, n_heads=32, n_kv_heads=8, head_dim=64, ffn=8192),
+    "8b": dict(d=4096, n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, ffn=14336),
+}
+
+
+def model_spec(tag: str, shape: str, seed: int = 0, max_agents: int = 16, vocab: int = 50000,
+               lm_gain: float = 4.0) -> ModelSpec:
+    s = SHAPES[shape]
+    return ModelSpec(tag=tag.encode()[:31], vocab=vocab, rope_theta=10000.0, norm_eps=1e-5, lm_gain=lm_gain,
+                     seed=seed, max_agents=max_agents, **s)
+
+
+class Engine:
+    """Owns one moa_engine (one GPU)."""
+
+    def __init__(self, models, max_ctx=1024, max_out=1024, max_rows=16384, device=0, keep_logits=False):
+        self.models = list(models)
+        arr = (ModelSpec * len(self.models))(*self.models)
+        opts = EngineOpts(max_ctx, max_out, max_rows, device, int(keep_logits))
+        h = C.c_void_p()
+        check(lib().moa_engine_create(arr, len(self.models), C.byref(opts), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            check(lib().moa_engine_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # --- SimWorld protocol ---
+    def add_agent(self, a, model):
+        check(lib().moa_add_agent(self.h, a[0], a[1], model))
+
+    def prefill_only(self, a, start, tokens):
+        buf, n = _ints(tokens)
+        check(lib().moa_prefill_only(self.h, a[0], a[1], start, buf, n))
+
+    def generate(self, a, prompt, max_new, apc_chunk, prefill_chunk=0):
+        buf, n = _ints(prompt)
+        check(lib().moa_generate(self.h, a[0], a[1], buf, n, max_new, apc_chunk, prefill_chunk))
+
+    def cancel(self, a):
+        check(lib().moa_cancel(self.h, a[0], a[1]))
+
+    def reclaim(self, a, keep):
+        check(lib().moa_reclaim(self.h, a[0], a[1], keep))
+
+    def step(self):
+        ev = (Event * 256)()
+        n, busy = C.c_int(), C.c_int()
+        check(lib().moa_step(self.h, ev, 256, C.byref(n), C.byref(busy)))
+        out = [(EVENT_KINDS[e.kind], e.tick, (e.layer, e.position), e.a, e.b) for e in ev[: min(n.value, 256)]]
+        return out, bool(busy.value)
+
+    def busy(self):
+        b = C.c_int()
+        check(lib().moa_busy(self.h, C.byref(b)))
+        return bool(b.value)
+
+    def read_output(self, a, n):
+        tok, lp, ent = (C.c_int32 * max(n, 1))(), (C.c_float * max(n, 1))(), (C.c_float * max(n, 1))()
+        check(lib().moa_read_output(self.h, a[0], a[1], n, tok, lp, ent))
+        return list(tok[:n]), list(lp[:n]), list(ent[:n])
+
+    def read_logits(self, a, k, vocab=50000):
+        buf = (C.c_float * vocab)()
+        check(lib().moa_read_logits(self.h, a[0], a[1], k, buf))
+        import numpy as np
+        return np.ctypeslib.as_array(buf).copy()
+
+    def state(self, a):
+        v = [C.c_int() for _ in range(4)]
+        check(lib().moa_agent_state(self.h, a[0], a[1], *[C.byref(x) for x in v]))
+        return dict(zip(("scheduled", "decoded", "finished", "cancelled"), (x.value for x in v)))
+
+    def reset(self):
+        check(lib().moa_engine_reset(self.h))
+
+    # --- run_query ---
+    def run_query(self, cfg: "QueryConfig", sample=0, resolve=True, detail=True):
+        s = RunSummary()
+        q = C.c_void_p()
+        check(lib().moa_run_query(self.h, C.byref(cfg.c), sample, int(resolve), C.byref(s),
+                                  C.byref(q) if detail else None))
+        res = {k: getattr(s, k) for k, _ in RunSummary._fields_}
+        if detail:
+            try:
+                res.update(_query_detail(q, s, resolve))
+            finally:
+                lib().moa_query_free(q)
+        return res
+
+
+def _query_detail(q, s, resolve):
+    agents, evals = {}, []
+    for i in range(s.n_agents):
+        r = AgentRecordC()
+        check(lib().moa_query_agent(q, i, C.byref(r)))
+        d = {k: getattr(r, k) for k, _ in AgentRecordC._fields_}
+        if resolve:
+            for which, key in ((0, "prompt"), (1, "output")):
+                n = C.c_int()
+                check(lib().moa_query_tokens(q, i, which, None, 0, C.byref(n)))
+                buf = (C.c_int32 * max(1, n.value))()
+                check(lib().moa_query_tokens(q, i, which, buf, n.value, C.byref(n)))
+                d[key] = list(buf[: n.value])
+            n = C.c_int()
+            cap = max(1, len(d["output"]))
+            lp, ent = (C.c_float * cap)(), (C.c_float * cap)()
+            check(lib().moa_query_logprobs(q, i, lp, ent, cap, C.byref(n)))
+            d["logprobs"], d["entropy"] = list(lp[: n.value]), list(ent[: n.value])
+        agents[f"{r.layer}:{r.position}"] = d
+    for i in range(s.n_evals):
+        e = EvalRecordC()
+        row = (C.c_double * 64)()
+        check(lib().moa_query_eval(q, i, C.byref(e), row, 64))
+        d = {k: getattr(e, k) for k, _ in EvalRecordC._fields_ if not k.startswith("pruned_")}
+        d["completed"] = f"{e.layer}:{e.position}"
+        d["pruned"] = [f"{e.pruned_layer[k]}:{e.pruned_position[k]}" for k in range(e.n_pruned)]
+        d["sim_row"] = list(row[: e.outputs])
+        evals.append(d)
+    return dict(agents=agents, metricq=evals)
+
+
+class QueryConfig:
+    """moa_run_config built from a plain config dict (configs.py)."""
+
+    def __init__(self, cfg: dict, model_index: dict):
+        t = cfg["topology"]
+        widths = list(t["widths"])
+        L = len(widths)
+        self._keep = []
+
+        def arr(v, ty=C.c_int):
+            a = (ty * max(1, len(v)))(*v)
+            self._keep.append(a)
+            return C.cast(a, _P(ty))
+
+        if t["kind"] == "all_to_all":
+            kind, cs = 1, None
+        else:
+            kind = 0
+            if "cluster_sizes" in t:
+                sizes = [s for layer in t["cluster_sizes"] for s in layer]
+            else:
+                sizes = [b for l, b in enumerate(t["branching"]) for _ in range(widths[l + 1])]
+            cs = arr(sizes)
+        cyc, clen, lo, hi = [], [], [], []
+        for l in range(L):
+            c = cfg["assign"][min(l, len(cfg["assign"]) - 1)]
+            cyc += [model_index[x] for x in c]
+            clen.append(len(c))
+            ol = cfg["out_len"][min(l, len(cfg["out_len"]) - 1)]
+            a, b = (ol, ol) if isinstance(ol, int) else tuple(ol)
+            lo.append(a)
+            hi.append(b)
+        fq = cfg.get("force_q")
+        self.c = RunConfigC(
+            topo_kind=kind, n_layers=L, widths=arr(widths), cluster_sizes=cs, model_cycle=arr(cyc),
+            cycle_len=arr(clen), out_lo=arr(lo), out_hi=arr(hi), mode=MODES[cfg["mode"]],
+            early_exit=int(cfg["early_exit"]), exit_scope=0 if cfg.get("exit_scope", "cluster") == "cluster" else 1,
+            tau=cfg.get("tau", 0.7), include_diagonal=int(cfg.get("include_diagonal", True)),
+            use_force_q=int(fq is not None), force_q=fq or 0.0, chunk_size=cfg["chunk_size"], seed=cfg["seed"],
+            query_tokens=cfg["query_tokens"], leaf_prefix_tokens=cfg["leaf_prefix_tokens"],
+            agg_prefix_tokens=cfg["agg_prefix_tokens"], separator_tokens=cfg["separator_tokens"],
+            suffix_tokens=cfg["suffix_tokens"], hidden=cfg.get("hidden", 64),
+            provider_seed=cfg.get("provider_seed", 0))
+
+
+def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16384):
+    """Engine holding every model the config names, sized for its agents."""
+    from collections import Counter
+    counts = Counter()
+    t = cfg["topology"]
+    for l, w in enumerate(t["widths"]):
+        for p in range(w):
+            counts[_configs.agent_tag(cfg, l + 1, p)] += 1
+    tags = list(cfg["models"])
+    specs = [model_spec(tag, cfg["models"][tag]["shape"], cfg["models"][tag].get("seed", 0),
+                        max_agents=max(1, counts[tag])) for tag in tags]
+    out_max = max(x if isinstance(x, int) else x[1] for x in cfg["out_len"])
+    if max_ctx is None:
+        prompt_max = max(cfg["query_tokens"] + cfg["leaf_prefix_tokens"],
+                         cfg["agg_prefix_tokens"] + cfg["suffix_tokens"]
+                         + max(t["widths"]) * (out_max + cfg["separator_tokens"]))
+        max_ctx = ((prompt_max + out_max + 255) // 256) * 256
+    eng = Engine(specs, max_ctx=max_ctx, max_out=out_max, max_rows=max_rows, device=device, keep_logits=keep_logits)
+    return eng, QueryConfig(cfg, {t: i for i, t in enumerate(tags)})
+
+
+def device_count() -> int:
+    n = C.c_int()
+    check(lib().moa_device_count(C.byref(n)))
+    return n.value
+
+
+if os.environ.get("MOA_B200_EAGER_LOAD"):
+    lib()

@@ -1,0 +1,549 @@
+// extern "C" boundary (include/moa_b200.h).  Exceptions never cross it: they
+// become status codes plus a thread-local message.
+#include "../../../include/moa_b200.h"
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../kernels/kernels.cuh"
+#include "engine.hpp"
+#include "graph.hpp"
+#include "metricq.hpp"
+#include "orchestrator.hpp"
+
+struct moa_engine {
+  std::unique_ptr<moa::GpuEngine> eng;
+};
+
+struct moa_query {
+  moa::QueryResult r;
+};
+
+struct moa_slotplan {
+  moa::SlotPlan plan;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return MOA_OK;
+  } catch (const moa::ValidationError& e) {
+    g_err = e.what();
+    return MOA_ERR_VALIDATION;
+  } catch (const moa::DeviceError& e) {
+    g_err = e.what();
+    return MOA_ERR_DEVICE;
+  } catch (const moa::RunError& e) {
+    g_err = e.what();
+    return MOA_ERR_RUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MOA_ERR_RUNTIME;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw moa::ValidationError(std::string(what) + ": null pointer");
+}
+
+moa::GpuEngine& E(moa_engine* e) {
+  need(e, "engine");
+  return *e->eng;
+}
+
+moa::TokenSeq seq(const int32_t* t, int n) {
+  if (n < 0) throw moa::ValidationError("token count must be >= 0");
+  if (n > 0) need(t, "tokens");
+  moa::TokenSeq s(t, t + n);
+  for (auto v : s)
+    if (v < 0) throw moa::ValidationError("tokens must be >= 0");
+  return s;
+}
+
+moa::Topology topology_of(int kind, int n_layers, const int* widths, const int* cluster_sizes) {
+  need(widths, "widths");
+  if (n_layers <= 0) throw moa::ValidationError("topology: widths must be non-empty");
+  std::vector<int> w(widths, widths + n_layers);
+  if (kind == MOA_TOPO_ALL_TO_ALL) return moa::Topology::all_to_all(w);
+  need(cluster_sizes, "cluster_sizes");
+  std::vector<std::vector<int>> cs;
+  int off = 0;
+  for (int l = 1; l < n_layers; ++l) {
+    if (w[static_cast<std::size_t>(l)] <= 0)
+      throw moa::ValidationError("topology: layer " + std::to_string(l + 1) + " has non-positive width");
+    cs.emplace_back(cluster_sizes + off, cluster_sizes + off + w[static_cast<std::size_t>(l)]);
+    off += w[static_cast<std::size_t>(l)];
+  }
+  return moa::Topology::tree_custom(w, cs);
+}
+
+moa::RunConfig run_config_of(const moa_run_config* c) {
+  need(c, "config");
+  moa::RunConfig cfg;
+  cfg.topology = topology_of(c->topo_kind, c->n_layers, c->widths, c->cluster_sizes);
+  need(c->model_cycle, "model_cycle");
+  need(c->cycle_len, "cycle_len");
+  need(c->out_lo, "out_lo");
+  need(c->out_hi, "out_hi");
+  std::vector<int> off(static_cast<std::size_t>(c->n_layers) + 1, 0);
+  for (int l = 0; l < c->n_layers; ++l) {
+    if (c->cycle_len[l] <= 0) throw moa::ValidationError("config: assignment cycle must not be empty");
+    off[static_cast<std::size_t>(l) + 1] = off[static_cast<std::size_t>(l)] + c->cycle_len[l];
+  }
+  for (const auto& layer : cfg.topology.layers())
+    for (const auto& a : layer) {
+      const int l = a.layer - 1;
+      cfg.model_of[a] = c->model_cycle[off[static_cast<std::size_t>(l)] + a.position % c->cycle_len[l]];
+      cfg.out_len[a] = moa::OutLen{c->out_lo[l], c->out_hi[l]};
+    }
+  switch (c->mode) {
+    case MOA_MODE_SEQUENTIAL_PD: cfg.mode = moa::ScheduleMode::SequentialPd; break;
+    case MOA_MODE_DP_ONLY: cfg.mode = moa::ScheduleMode::DpOnly; break;
+    case MOA_MODE_DP_CHUNKED_PREFILL: cfg.mode = moa::ScheduleMode::DpChunkedPrefill; break;
+    case MOA_MODE_INCREMENTAL_OVERLAP: cfg.mode = moa::ScheduleMode::IncrementalOverlap; break;
+    default: throw moa::ValidationError("mode: unknown schedule mode");
+  }
+  cfg.early_exit = c->early_exit != 0;
+  cfg.exit_scope = c->exit_scope == MOA_SCOPE_LAYER ? moa::ExitScope::Layer : moa::ExitScope::Cluster;
+  cfg.tau = c->tau;
+  cfg.include_diagonal = c->include_diagonal != 0;
+  if (c->use_force_q) cfg.force_q = c->force_q;
+  cfg.chunk_size = c->chunk_size;
+  cfg.seed = c->seed;
+  cfg.query_tokens = c->query_tokens;
+  cfg.leaf_prefix_tokens = c->leaf_prefix_tokens;
+  cfg.agg_prefix_tokens = c->agg_prefix_tokens;
+  cfg.separator_tokens = c->separator_tokens;
+  cfg.suffix_tokens = c->suffix_tokens;
+  cfg.hidden = c->hidden;
+  cfg.provider_seed = c->provider_seed;
+  return cfg;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* moa_last_error(void) { return g_err.c_str(); }
+const char* moa_version(void) { return "moa_b200 0.1 (sm_100a)"; }
+
+int moa_device_count(int* n) {
+  return guard([&] {
+    need(n, "n");
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+    *n = c;
+  });
+}
+
+int moa_engine_create(const moa_model_spec* models, int n_models, const moa_engine_opts* opts, moa_engine** out) {
+  return guard([&] {
+    need(models, "models");
+    need(out, "out");
+    if (n_models <= 0) throw moa::ValidationError("engine: at least one model is required");
+    std::vector<moa::ModelSpec> specs;
+    std::vector<int> caps;
+    for (int i = 0; i < n_models; ++i) {
+      const moa_model_spec& m = models[i];
+      moa::ModelSpec s;
+      s.tag = std::string(m.tag, strnlen(m.tag, sizeof(m.tag)));
+      s.d = m.d;
+      s.n_layers = m.n_layers;
+      s.n_heads = m.n_heads;
+      s.n_kv_heads = m.n_kv_heads;
+      s.head_dim = m.head_dim;
+      s.ffn = m.ffn;
+      s.vocab = m.vocab;
+      s.rope_theta = m.rope_theta;
+      s.norm_eps = m.norm_eps;
+      s.lm_gain = m.lm_gain;
+      s.seed = m.seed;
+      specs.push_back(s);
+      caps.push_back(m.max_agents);
+    }
+    moa::EngineOptions o;
+    if (opts) {
+      o.max_ctx = opts->max_ctx;
+      o.max_out = opts->max_out;
+      o.max_rows = opts->max_rows;
+      o.device = opts->device;
+      o.keep_logits = opts->keep_logits != 0;
+    }
+    auto e = std::make_unique<moa_engine>();
+    e->eng = std::make_unique<moa::GpuEngine>(specs, caps, o);
+    *out = e.release();
+  });
+}
+
+int moa_engine_destroy(moa_engine* eng) {
+  return guard([&] { delete eng; });
+}
+
+int moa_engine_reset(moa_engine* eng) {
+  return guard([&] { E(eng).reset(); });
+}
+
+int moa_add_agent(moa_engine* eng, int layer, int position, int model) {
+  return guard([&] { E(eng).add_agent(moa::AgentId{layer, position}, model); });
+}
+
+int moa_prefill_only(moa_engine* eng, int layer, int position, int start, const int32_t* tokens, int n) {
+  return guard([&] { E(eng).submit_prefill_only(moa::AgentId{layer, position}, start, seq(tokens, n)); });
+}
+
+int moa_generate(moa_engine* eng, int layer, int position, const int32_t* prompt, int n, int max_new, int apc_chunk,
+                 int prefill_chunk) {
+  return guard([&] {
+    E(eng).submit_generate(moa::AgentId{layer, position}, seq(prompt, n), max_new, apc_chunk, prefill_chunk);
+  });
+}
+
+int moa_cancel(moa_engine* eng, int layer, int position) {
+  return guard([&] { E(eng).cancel(moa::AgentId{layer, position}); });
+}
+
+int moa_reclaim(moa_engine* eng, int layer, int position, int keep) {
+  return guard([&] { E(eng).reclaim(moa::AgentId{layer, position}, keep); });
+}
+
+int moa_step(moa_engine* eng, moa_event* events, int cap, int* n_events, int* busy) {
+  return guard([&] {
+    moa::GpuEngine& g = E(eng);
+    g.clear_events();
+    g.step();
+    const auto& ev = g.events();
+    int n = 0;
+    for (const auto& e : ev) {
+      if (events && n < cap) events[n] = moa_event{e.kind, e.tick, e.agent.layer, e.agent.position, e.a, e.b};
+      ++n;
+    }
+    if (n_events) *n_events = n;
+    if (busy) *busy = g.busy() ? 1 : 0;
+  });
+}
+
+int moa_busy(moa_engine* eng, int* busy) {
+  return guard([&] {
+    need(busy, "busy");
+    *busy = E(eng).busy() ? 1 : 0;
+  });
+}
+
+int moa_read_output(moa_engine* eng, int layer, int position, int n, int32_t* tokens, float* logprobs,
+                    float* entropy) {
+  return guard([&] {
+    moa::GpuEngine& g = E(eng);
+    const moa::AgentId id{layer, position};
+    if (n > g.decoded(id)) throw moa::ValidationError("read_output: only " + std::to_string(g.decoded(id)) +
+                                                      " tokens decoded");
+    g.read_outputs(id, n, tokens, logprobs, entropy);
+  });
+}
+
+int moa_read_logits(moa_engine* eng, int layer, int position, int k, float* logits) {
+  return guard([&] {
+    need(logits, "logits");
+    moa::GpuEngine& g = E(eng);
+    const moa::AgentId id{layer, position};
+    if (k < 0 || k >= g.decoded(id)) throw moa::ValidationError("read_logits: token index out of range");
+    g.read_logits(id, k, logits);
+  });
+}
+
+int moa_agent_state(moa_engine* eng, int layer, int position, int* scheduled, int* decoded, int* finished,
+                    int* cancelled) {
+  return guard([&] {
+    moa::GpuEngine& g = E(eng);
+    const moa::AgentId id{layer, position};
+    if (scheduled) *scheduled = static_cast<int>(g.prompt(id).size());
+    if (decoded) *decoded = g.decoded(id);
+    if (finished) *finished = g.finished(id) ? 1 : 0;
+    if (cancelled) *cancelled = g.cancelled(id) ? 1 : 0;
+  });
+}
+
+int moa_run_query(moa_engine* eng, const moa_run_config* cfg, int sample, int resolve, moa_run_summary* summary,
+                  moa_query** out) {
+  return guard([&] {
+    moa::GpuEngine& g = E(eng);
+    auto q = std::make_unique<moa_query>();
+    q->r = moa::run_query(g, run_config_of(cfg), sample, resolve != 0);
+    if (summary) {
+      const auto& r = q->r;
+      summary->ticks = r.ticks;
+      summary->n_agents = static_cast<int>(r.agents.size());
+      summary->n_evals = static_cast<int>(r.metricq.size());
+      summary->forwards = r.forwards;
+      summary->tokens = r.tokens;
+      summary->decoded_tokens = r.decoded_tokens;
+      summary->rows = r.rows;
+      summary->e2e_ms = r.e2e_ms;
+      summary->wall_ms = r.wall_ms;
+      summary->weight_bytes = r.weight_bytes;
+    }
+    if (out) *out = q.release();
+  });
+}
+
+int moa_query_agent(const moa_query* q, int i, moa_agent_record* rec) {
+  return guard([&] {
+    need(q, "query");
+    need(rec, "rec");
+    if (i < 0 || i >= static_cast<int>(q->r.agents.size())) throw moa::ValidationError("agent index out of range");
+    const auto& a = q->r.agents[static_cast<std::size_t>(i)];
+    const auto& r = q->r.records.at(a);
+    *rec = moa_agent_record{a.layer,
+                            a.position,
+                            r.model,
+                            r.invoked,
+                            r.pruned,
+                            r.empty_input,
+                            r.prompt_tokens,
+                            r.output_tokens,
+                            r.prefill_only_calls,
+                            r.recomputed_tokens,
+                            r.reclaimed_tokens,
+                            r.decode_start,
+                            r.decode_end,
+                            r.complete,
+                            r.precursor_ready_tick};
+  });
+}
+
+int moa_query_tokens(const moa_query* q, int i, int which, int32_t* dst, int cap, int* n) {
+  return guard([&] {
+    need(q, "query");
+    if (i < 0 || i >= static_cast<int>(q->r.agents.size())) throw moa::ValidationError("agent index out of range");
+    const auto& a = q->r.agents[static_cast<std::size_t>(i)];
+    const auto& m = which == 0 ? q->r.prompts : q->r.outputs;
+    auto it = m.find(a);
+    if (it == m.end()) throw moa::ValidationError("query: tokens were not resolved (resolve = 0)");
+    const int len = static_cast<int>(it->second.size());
+    if (n) *n = len;
+    if (dst) std::memcpy(dst, it->second.data(), sizeof(int32_t) * std::min(cap, len));
+  });
+}
+
+int moa_query_logprobs(const moa_query* q, int i, float* logprobs, float* entropy, int cap, int* n) {
+  return guard([&] {
+    need(q, "query");
+    if (i < 0 || i >= static_cast<int>(q->r.agents.size())) throw moa::ValidationError("agent index out of range");
+    const auto& a = q->r.agents[static_cast<std::size_t>(i)];
+    auto it = q->r.logprobs.find(a);
+    if (it == q->r.logprobs.end()) throw moa::ValidationError("query: outputs were not resolved");
+    const int len = static_cast<int>(it->second.size());
+    if (n) *n = len;
+    if (logprobs) std::memcpy(logprobs, it->second.data(), sizeof(float) * std::min(cap, len));
+    if (entropy) std::memcpy(entropy, q->r.entropy.at(a).data(), sizeof(float) * std::min(cap, len));
+  });
+}
+
+int moa_query_eval(const moa_query* q, int i, moa_eval_record* rec, double* sim_row, int cap) {
+  return guard([&] {
+    need(q, "query");
+    need(rec, "rec");
+    if (i < 0 || i >= static_cast<int>(q->r.metricq.size())) throw moa::ValidationError("eval index out of range");
+    const auto& m = q->r.metricq[static_cast<std::size_t>(i)];
+    moa_eval_record r{};
+    r.tick = m.tick;
+    r.group = m.group;
+    r.eval_index = m.eval_index;
+    r.layer = m.completed.layer;
+    r.position = m.completed.position;
+    r.evaluated = m.evaluated;
+    r.exited = m.decision.exited;
+    r.n_pruned = static_cast<int>(m.pruned.size());
+    r.outputs = m.score.outputs;
+    r.q = m.decision.q;
+    r.draw = m.decision.draw;
+    r.c = m.score.confidences.empty() ? 0.0 : m.score.confidences.back();
+    r.c_bar = m.score.c_bar;
+    r.weight_sum = m.score.weight_sum;
+    r.weighted = m.score.weighted;
+    r.calibrated = m.score.calibrated;
+    for (int k = 0; k < r.n_pruned && k < 16; ++k) {
+      r.pruned_layer[k] = m.pruned[static_cast<std::size_t>(k)].layer;
+      r.pruned_position[k] = m.pruned[static_cast<std::size_t>(k)].position;
+    }
+    *rec = r;
+    if (sim_row && m.score.outputs > 0) {
+      const int n = m.score.outputs;
+      for (int j = 0; j < n && j < cap; ++j) sim_row[j] = m.score.sim[static_cast<std::size_t>(n - 1) * n + j];
+    }
+  });
+}
+
+int moa_query_free(moa_query* q) {
+  return guard([&] { delete q; });
+}
+
+int moa_mock_embed(const int32_t* tokens, int n, int hidden, uint64_t seed, double* out, int device) {
+  return guard([&] {
+    if (n <= 0) return;
+    need(tokens, "tokens");
+    need(out, "out");
+    if (hidden <= 0) throw moa::ValidationError("provider.hidden: must be > 0");
+    MOA_CUDA(cudaSetDevice(device));
+    int* d_tok = nullptr;
+    double* d_emb = nullptr;
+    MOA_CUDA(cudaMalloc(&d_tok, sizeof(int) * n));
+    MOA_CUDA(cudaMalloc(&d_emb, sizeof(double) * n * hidden));
+    MOA_CUDA(cudaMemcpy(d_tok, tokens, sizeof(int) * n, cudaMemcpyHostToDevice));
+    moa::k::ee_mock_embed(d_tok, 0, n, hidden, seed, d_emb, nullptr);
+    MOA_CUDA(cudaGetLastError());
+    MOA_CUDA(cudaMemcpy(out, d_emb, sizeof(double) * n * hidden, cudaMemcpyDeviceToHost));
+    cudaFree(d_tok);
+    cudaFree(d_emb);
+  });
+}
+
+int moa_metricq_run(const int32_t* tokens, const float* logprobs, const int* lens, int m, int hidden, uint64_t seed,
+                    double tau, int include_diagonal, uint64_t master, const char* label, double* out6,
+                    double* draw, int* exited, double* sim_out, int device) {
+  return guard([&] {
+    need(lens, "lens");
+    need(label, "label");
+    if (m <= 0) throw moa::ValidationError("metricq: need at least one completion");
+    long long total = 0;
+    int maxn = 0;
+    for (int i = 0; i < m; ++i) {
+      if (lens[i] <= 0) throw moa::ValidationError("logprobs: need at least one token");
+      total += lens[i];
+      maxn = std::max(maxn, lens[i]);
+    }
+    need(tokens, "tokens");
+    need(logprobs, "logprobs");
+    MOA_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    MOA_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int* d_tok = nullptr;
+    float* d_lp = nullptr;
+    MOA_CUDA(cudaMalloc(&d_tok, sizeof(int) * total));
+    MOA_CUDA(cudaMalloc(&d_lp, sizeof(float) * total));
+    MOA_CUDA(cudaMemcpy(d_tok, tokens, sizeof(int) * total, cudaMemcpyHostToDevice));
+    MOA_CUDA(cudaMemcpy(d_lp, logprobs, sizeof(float) * total, cudaMemcpyHostToDevice));
+    {
+      moa::GpuMetricQ ev(hidden, seed, tau, include_diagonal != 0, m, maxn, st);
+      moa::rng::Stream s = moa::rng::Stream::derive(master, label);
+      long long base = 0;
+      moa::QualityScore qs;
+      for (int i = 0; i < m; ++i) {
+        qs = ev.add_completion(d_tok, d_lp, base, lens[i]);
+        base += lens[i];
+        const moa::ExitDecision d = moa::decide_exit(qs.q, s);
+        if (out6) {
+          double* o = out6 + 6 * i;
+          o[0] = qs.confidences.back();
+          o[1] = qs.c_bar;
+          o[2] = qs.weight_sum;
+          o[3] = qs.weighted;
+          o[4] = qs.calibrated;
+          o[5] = qs.q;
+        }
+        if (draw) draw[i] = d.draw;
+        if (exited) exited[i] = d.exited ? 1 : 0;
+      }
+      if (sim_out) std::memcpy(sim_out, qs.sim.data(), sizeof(double) * qs.sim.size());
+    }
+    cudaFree(d_tok);
+    cudaFree(d_lp);
+    cudaStreamDestroy(st);
+  });
+}
+
+int moa_topology(int kind, int n_layers, const int* widths, const int* cluster_sizes, int* pre_off, int* pre,
+                 int cap) {
+  return guard([&] {
+    moa::Topology t = topology_of(kind, n_layers, widths, cluster_sizes);
+    std::map<moa::AgentId, int> index;
+    int k = 0;
+    for (const auto& layer : t.layers())
+      for (const auto& a : layer) index[a] = k++;
+    int n = 0, i = 0;
+    for (const auto& layer : t.layers())
+      for (const auto& a : layer) {
+        if (pre_off) pre_off[i] = n;
+        for (const auto& p : t.precursors(a)) {
+          if (pre && n < cap) pre[n] = index.at(p);
+          ++n;
+        }
+        ++i;
+      }
+    if (pre_off) pre_off[i] = n;
+  });
+}
+
+int moa_slotplan_create(int self_layer, int self_position, const int32_t* prefix, int n_prefix, const int* slot_layer,
+                        const int* slot_position, const int32_t* sep_tokens, const int* sep_lens, int n_slots,
+                        const int32_t* suffix, int n_suffix, int incremental, moa_slotplan** out) {
+  return guard([&] {
+    need(out, "out");
+    std::vector<moa::Slot> slots;
+    int off = 0;
+    for (int i = 0; i < n_slots; ++i) {
+      const int len = sep_lens ? sep_lens[i] : 0;
+      slots.push_back(moa::Slot{moa::AgentId{slot_layer[i], slot_position[i]},
+                                moa::TokenSeq(sep_tokens + off, sep_tokens + off + len)});
+      off += len;
+    }
+    moa::PromptTemplate t(moa::TokenSeq(prefix, prefix + n_prefix), slots, moa::TokenSeq(suffix, suffix + n_suffix));
+    *out = new moa_slotplan{moa::SlotPlan(moa::AgentId{self_layer, self_position}, t, incremental != 0)};
+  });
+}
+
+int moa_slotplan_event(moa_slotplan* p, int op, int layer, int position, const int32_t* tokens, int n, int32_t* buf,
+                       int cap, int* n_words) {
+  return guard([&] {
+    need(p, "plan");
+    std::vector<moa::RouteAction> acts;
+    const moa::AgentId who{layer, position};
+    switch (op) {
+      case 0: acts = p->plan.start(); break;
+      case 1: acts = p->plan.on_chunk(who, moa::TokenSeq(tokens, tokens + n)); break;
+      case 2: acts = p->plan.on_precursor_done(who); break;
+      case 3: acts = p->plan.on_precursor_cancelled(who); break;
+      default: throw moa::ValidationError("slotplan: unknown op");
+    }
+    int w = 0;
+    auto put = [&](int32_t v) {
+      if (buf && w < cap) buf[w] = v;
+      ++w;
+    };
+    for (const auto& a : acts) {
+      put(a.kind == moa::RouteAction::Kind::PrefillOnly ? 0 : a.kind == moa::RouteAction::Kind::Generate ? 1 : 2);
+      put(a.start);
+      put(static_cast<int32_t>(a.tokens.size()));
+      for (auto t : a.tokens) put(t);
+    }
+    if (n_words) *n_words = w;
+  });
+}
+
+int moa_slotplan_free(moa_slotplan* p) {
+  return guard([&] { delete p; });
+}
+
+int moa_k_gemm_skinny(uintptr_t A, int R, uintptr_t W, int N, int K, int S, uintptr_t P, uintptr_t stream) {
+  return guard([&] {
+    if (S <= 0 || K % (256 * S)) throw moa::ValidationError("gemm_skinny: K must split into multiples of 256");
+    moa::k::gemm_skinny(reinterpret_cast<const moa::k::bf16*>(A), R, reinterpret_cast<const moa::k::bf16*>(W), N, K,
+                        S, reinterpret_cast<float*>(P), reinterpret_cast<cudaStream_t>(stream));
+    MOA_CUDA(cudaGetLastError());
+  });
+}
+
+int moa_k_init_uniform(uintptr_t dst, long long n, uint64_t base, float scale, uintptr_t stream) {
+  return guard([&] {
+    moa::k::init_uniform(reinterpret_cast<moa::k::bf16*>(dst), n, base, scale,
+                         reinterpret_cast<cudaStream_t>(stream));
+    MOA_CUDA(cudaGetLastError());
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,441 @@
+// Tick engine over the device models.  Protocol checks follow pdsim.cpp
+// (cited per method); the tick schedule is the contract in oracle/engine.py.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace moa {
+
+namespace {
+constexpr int kRing = 64;
+}
+
+GpuEngine::GpuEngine(std::vector<ModelSpec> models, std::vector<int> agents_per_model, EngineOptions opt)
+    : opt_(opt) {
+  if (models.empty()) throw ValidationError("engine: at least one model is required");
+  if (agents_per_model.size() != models.size())
+    throw ValidationError("engine: one agent capacity per model is required");
+  if (opt_.max_ctx <= 0 || opt_.max_out <= 0 || opt_.max_rows <= 0)
+    throw ValidationError("engine: max_ctx, max_out and max_rows must be > 0");
+  MOA_CUDA(cudaSetDevice(opt_.device));
+  MOA_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  for (int c : agents_per_model) max_slots_ += c;
+  if (static_cast<long long>(max_slots_) * opt_.max_out >= (1LL << 31))
+    throw ValidationError("engine: agents x max_out exceeds the symbolic token range");
+  for (std::size_t m = 0; m < models.size(); ++m) {
+    const int cap = std::max(1, agents_per_model[m]);
+    models_.push_back(std::make_unique<DeviceModel>(models[m], cap, opt_.max_ctx, opt_.max_rows + max_slots_,
+                                                    max_slots_, stream_));
+    logits_v_ = std::max(logits_v_, models[m].vocab);
+  }
+  const long long nout = static_cast<long long>(max_slots_) * opt_.max_out;
+  MOA_CUDA(cudaMalloc(&out_tok_, sizeof(int) * nout));
+  MOA_CUDA(cudaMalloc(&out_lp_, sizeof(float) * nout));
+  MOA_CUDA(cudaMalloc(&out_ent_, sizeof(float) * nout));
+  MOA_CUDA(cudaMemsetAsync(out_tok_, 0, sizeof(int) * nout, stream_));
+  if (opt_.keep_logits) {
+    MOA_CUDA(cudaMalloc(&logits_, sizeof(float) * nout * logits_v_));
+    MOA_CUDA(cudaMalloc(&logits_scratch_, sizeof(float) * static_cast<long long>(max_slots_) * logits_v_));
+  }
+  ring_bytes_ = sizeof(k::RowDesc) * (opt_.max_rows + max_slots_) + sizeof(int) * 2 * max_slots_;
+  for (int i = 0; i < kRing; ++i) {
+    Staging s;
+    MOA_CUDA(cudaMallocHost(&s.host, ring_bytes_));
+    MOA_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    ring_.push_back(s);
+  }
+  MOA_CUDA(cudaEventCreate(&start_ev_));
+  MOA_CUDA(cudaStreamSynchronize(stream_));
+}
+
+GpuEngine::~GpuEngine() {
+  cudaSetDevice(opt_.device);
+  if (stream_) cudaStreamSynchronize(stream_);
+  ee_pool_.clear();
+  models_.clear();
+  for (auto& s : ring_) {
+    cudaFreeHost(s.host);
+    cudaEventDestroy(s.done);
+  }
+  for (auto e : tick_ev_) cudaEventDestroy(e);
+  if (start_ev_) cudaEventDestroy(start_ev_);
+  for (void* p : {static_cast<void*>(out_tok_), static_cast<void*>(out_lp_), static_cast<void*>(out_ent_),
+                  static_cast<void*>(logits_), static_cast<void*>(logits_scratch_)})
+    if (p) cudaFree(p);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+GpuEngine::Req& GpuEngine::req(const AgentId& id) {
+  auto it = reqs_.find(id);
+  if (it == reqs_.end()) throw RunError("sim: unknown agent " + id.str());
+  return it->second;
+}
+
+const GpuEngine::Req& GpuEngine::req(const AgentId& id) const {
+  auto it = reqs_.find(id);
+  if (it == reqs_.end()) throw RunError("sim: unknown agent " + id.str());
+  return it->second;
+}
+
+void GpuEngine::add_agent(const AgentId& id, int model) {
+  if (reqs_.count(id)) throw ValidationError("sim: agent " + id.str() + " added twice");
+  if (model < 0 || model >= n_models()) throw ValidationError("engine: unknown model index for " + id.str());
+  if (slots_ >= max_slots_) throw ValidationError("engine: agent capacity exhausted");
+  Req r;
+  r.id = id;
+  r.model = model;
+  r.kv = models_[static_cast<std::size_t>(model)]->bind_agent();
+  r.slot = slots_++;
+  r.rec.id = id;
+  r.rec.model = model;
+  r.rec.submit_tick = tick_;
+  reqs_.emplace(id, std::move(r));
+  order_.push_back(id);
+}
+
+// pdsim.cpp:155-174
+void GpuEngine::submit_prefill_only(const AgentId& id, int expected_start, const TokenSeq& tokens) {
+  Req& r = req(id);
+  if (r.cancelled) return;
+  if (r.gen_pending || r.dec_started) throw RunError("sim: prefill_only after generate for agent " + id.str());
+  const int sched = static_cast<int>(r.prompt.size());
+  if (expected_start != sched)
+    throw RunError("sim: contiguity violation for agent " + id.str() + ": prefill starts at " +
+                   std::to_string(expected_start) + " but " + std::to_string(sched) +
+                   " tokens are scheduled");
+  if (tokens.empty()) return;
+  if (sched + static_cast<int>(tokens.size()) > opt_.max_ctx)
+    throw ValidationError("engine: prompt of " + id.str() + " exceeds max_ctx");
+  r.prompt.insert(r.prompt.end(), tokens.begin(), tokens.end());
+  r.rec.prefill_only_calls += 1;
+  r.queue.push_back(Job{sched, sched + static_cast<int>(tokens.size())});
+}
+
+// pdsim.cpp:176-214 (max_new replaces the planned output)
+void GpuEngine::submit_generate(const AgentId& id, const TokenSeq& full, int max_new, int apc_chunk,
+                                int prefill_chunk) {
+  Req& r = req(id);
+  if (r.cancelled) return;
+  if (r.gen_pending || r.dec_started) throw RunError("sim: generate submitted twice for agent " + id.str());
+  const int sched = static_cast<int>(r.prompt.size());
+  if (static_cast<int>(full.size()) < sched || !std::equal(r.prompt.begin(), r.prompt.end(), full.begin()))
+    throw RunError("sim: generate prompt for agent " + id.str() + " does not extend the prefilled prefix");
+  if (apc_chunk <= 0) throw ValidationError("sim: apc_chunk must be > 0");
+  if (max_new < 0) throw ValidationError("sim: max_new must be >= 0");
+  if (max_new > opt_.max_out) throw ValidationError("engine: max_new exceeds max_out");
+  if (static_cast<int>(full.size()) + max_new > opt_.max_ctx)
+    throw ValidationError("engine: prompt + output of " + id.str() + " exceeds max_ctx");
+  r.prompt = full;
+  r.max_new = max_new;
+  r.apc = apc_chunk;
+  r.gen_pending = true;
+  r.rec.prompt_tokens = static_cast<int>(full.size());
+  r.rec.invoked = true;
+  const int n = static_cast<int>(full.size());
+  const int step = prefill_chunk > 0 ? prefill_chunk : n - sched;
+  for (int b = sched; b < n; b += step) r.queue.push_back(Job{b, std::min(b + step, n)});
+}
+
+// pdsim.cpp:374-398: output truncated to the tokens already decoded
+void GpuEngine::cancel(const AgentId& id) {
+  Req& r = req(id);
+  if (r.finished) throw RunError("sim: cancel after completion for agent " + id.str());
+  if (r.cancelled) return;
+  r.cancelled = true;
+  r.rec.pruned = true;
+  r.gen += 1;
+  r.queue.clear();
+  r.gen_pending = false;
+  r.rec.output_tokens = r.dec_started ? r.n_out : 0;
+  events_.push_back(EngineEvent{EngineEvent::Cancel, tick_, id, r.rec.output_tokens, 0});
+}
+
+// pdsim.cpp:400-418, except that jobs below `keep` survive (truncated at
+// keep): between ticks nothing is in flight, so the rewind is exact.
+void GpuEngine::reclaim(const AgentId& id, int keep) {
+  Req& r = req(id);
+  if (r.gen_pending || r.dec_started) throw RunError("sim: reclaim after generate for agent " + id.str());
+  const int sched = static_cast<int>(r.prompt.size());
+  if (keep < 0 || keep > sched)
+    throw RunError("sim: reclaim point " + std::to_string(keep) + " outside scheduled prompt of " +
+                   std::to_string(sched) + " tokens");
+  r.gen += 1;
+  std::deque<Job> kept;
+  for (const Job& j : r.queue)
+    if (j.b < keep) kept.push_back(Job{j.b, std::min(j.e, keep)});
+  r.queue.swap(kept);
+  r.prompt.resize(static_cast<std::size_t>(keep));
+  if (r.prefilled > keep) {
+    r.rec.reclaimed_tokens += r.prefilled - keep;
+    r.prefilled = keep;
+  }
+  events_.push_back(EngineEvent{EngineEvent::Reclaim, tick_, id, keep, 0});
+}
+
+void GpuEngine::on_chunk(const AgentId& id, ChunkFn fn) { req(id).chunk_fns.push_back(std::move(fn)); }
+void GpuEngine::on_decode_end(const AgentId& id, EndFn fn) { req(id).end_fns.push_back(std::move(fn)); }
+
+void GpuEngine::note_precursor_ready(const AgentId& id) {
+  Req& r = req(id);
+  r.rec.precursor_ready_tick = std::max(r.rec.precursor_ready_tick, tick_);
+}
+
+void GpuEngine::mark_empty_input(const AgentId& id) { req(id).rec.empty_input = true; }
+
+bool GpuEngine::busy() const {
+  for (const auto& [id, r] : reqs_) {
+    if (r.cancelled || r.finished) continue;
+    if (!r.queue.empty() || r.gen_pending || r.dec_started) return true;
+  }
+  return false;
+}
+
+void GpuEngine::start_decode(Req& r, int n_out) {
+  r.gen_pending = false;
+  r.dec_started = true;
+  r.rec.decode_start = tick_;
+  r.n_out = n_out;
+}
+
+void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, const std::vector<int>& lsel,
+                                   const std::vector<int>& lout) {
+  DeviceModel& dm = *models_[static_cast<std::size_t>(m)];
+  Staging& s = ring_[ring_next_];
+  ring_next_ = (ring_next_ + 1) % ring_.size();
+  MOA_CUDA(cudaEventSynchronize(s.done));  // the copy that last used this slot has consumed it
+  const std::size_t rb = sizeof(k::RowDesc) * rows.size();
+  std::memcpy(s.host, rows.data(), rb);
+  const int L = dm.max_logit_rows();
+  int* sel = reinterpret_cast<int*>(s.host + rb);
+  std::memcpy(sel, lsel.data(), sizeof(int) * lsel.size());
+  std::memcpy(sel + L, lout.data(), sizeof(int) * lout.size());
+  MOA_CUDA(cudaMemcpyAsync(dm.buffers().rows, s.host, rb, cudaMemcpyHostToDevice, stream_));
+  if (!lsel.empty())
+    MOA_CUDA(cudaMemcpyAsync(dm.buffers().sel, sel, sizeof(int) * 2 * L, cudaMemcpyHostToDevice, stream_));
+  MOA_CUDA(cudaEventRecord(s.done, stream_));
+  float* logits = (opt_.keep_logits && !lsel.empty()) ? logits_scratch_ : nullptr;
+  dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), out_tok_, out_tok_, out_lp_,
+             out_ent_, logits, stream_);
+  if (logits) {  // debug path: scatter each logits row to its (slot, k) home
+    const long long V = dm.spec().vocab;
+    for (std::size_t i = 0; i < lsel.size(); ++i)
+      MOA_CUDA(cudaMemcpyAsync(logits_ + static_cast<long long>(lout[i]) * logits_v_,
+                               logits_scratch_ + static_cast<long long>(i) * V, sizeof(float) * V,
+                               cudaMemcpyDeviceToDevice, stream_));
+  }
+  rows_total_ += static_cast<long long>(rows.size());
+  weight_bytes_ += dm.weight_bytes();
+  forwards_ += 1;
+}
+
+void GpuEngine::step() {
+  enum Kind { Decode, Prefill, Bootstrap, Empty };
+  struct Plan {
+    Req* r;
+    Kind kind;
+    Job job;
+    bool yields;
+  };
+  std::vector<Plan> plan;
+  const std::size_t nm = models_.size();
+  std::vector<std::vector<k::RowDesc>> rows(nm);
+  std::vector<std::vector<int>> lsel(nm), lout(nm);
+  int budget = opt_.max_rows;
+  auto add_row = [&](Req& r, int pos, Token tok, int out_k) {
+    auto& rv = rows[static_cast<std::size_t>(r.model)];
+    int oi = -1;
+    if (out_k >= 0) {
+      oi = r.slot * opt_.max_out + out_k;
+      lsel[static_cast<std::size_t>(r.model)].push_back(static_cast<int>(rv.size()));
+      lout[static_cast<std::size_t>(r.model)].push_back(oi);
+    }
+    rv.push_back(k::RowDesc{r.kv, pos, tok, oi});
+  };
+  for (const AgentId& id : order_) {
+    Req& r = reqs_.at(id);
+    if (r.cancelled || r.finished) continue;
+    if (r.dec_started) {
+      if (r.n_out < r.max_new) {
+        add_row(r, static_cast<int>(r.prompt.size()) + r.n_out - 1, ref(r.slot, r.n_out - 1), r.n_out);
+        plan.push_back(Plan{&r, Decode, {}, false});
+        budget -= 1;
+      }
+      continue;
+    }
+    if (!r.queue.empty()) {
+      const Job j = r.queue.front();
+      if (j.e - j.b > budget) continue;
+      r.queue.pop_front();
+      budget -= j.e - j.b;
+      const bool yields = r.gen_pending && j.e == static_cast<int>(r.prompt.size()) && r.max_new > 0;
+      for (int p = j.b; p < j.e; ++p) add_row(r, p, r.prompt[static_cast<std::size_t>(p)], (yields && p == j.e - 1) ? 0 : -1);
+      plan.push_back(Plan{&r, Prefill, j, yields});
+      continue;
+    }
+    if (r.gen_pending && r.prefilled == static_cast<int>(r.prompt.size())) {
+      if (r.max_new == 0) {
+        plan.push_back(Plan{&r, Empty, {}, false});
+      } else {
+        const int P = static_cast<int>(r.prompt.size());
+        add_row(r, std::max(P - 1, 0), P > 0 ? r.prompt[static_cast<std::size_t>(P - 1)] : 0, 0);
+        plan.push_back(Plan{&r, Bootstrap, {}, false});
+        budget -= 1;
+      }
+    }
+  }
+  for (std::size_t m = 0; m < nm; ++m)
+    if (!rows[m].empty()) upload_and_forward(static_cast<int>(m), rows[m], lsel[m], lout[m]);
+  if (opt_.time_ticks) {
+    if (static_cast<int>(tick_ev_.size()) <= tick_) {
+      cudaEvent_t e;
+      MOA_CUDA(cudaEventCreate(&e));
+      tick_ev_.push_back(e);
+    }
+    MOA_CUDA(cudaEventRecord(tick_ev_[static_cast<std::size_t>(tick_)], stream_));
+  }
+  // state update
+  for (Plan& p : plan) {
+    Req& r = *p.r;
+    switch (p.kind) {
+      case Decode:
+        r.n_out += 1;
+        break;
+      case Prefill: {
+        const int recomputed = std::max(0, std::min(p.job.e, r.max_computed) - p.job.b);
+        r.max_computed = std::max(r.max_computed, p.job.e);
+        r.rec.prefill.push_back(PrefillInterval{tick_, p.job.b, p.job.e});
+        r.rec.recomputed_tokens += recomputed;
+        if (p.job.b != r.prefilled) throw RunError("sim: internal contiguity breach for agent " + r.id.str());
+        r.prefilled = p.job.e;
+        if (p.yields)
+          start_decode(r, 1);
+        else if (r.gen_pending && r.prefilled == static_cast<int>(r.prompt.size()) && r.max_new == 0)
+          start_decode(r, 0);
+        break;
+      }
+      case Bootstrap:
+        start_decode(r, 1);
+        break;
+      case Empty:
+        start_decode(r, 0);
+        break;
+    }
+  }
+  const int t = tick_;
+  tick_ += 1;
+  // phase A: chunk emission (pdsim.cpp:339-362)
+  std::vector<Req*> done;
+  for (const AgentId& id : order_) {
+    Req& r = reqs_.at(id);
+    if (r.cancelled || r.finished || !r.dec_started) continue;
+    const int n = r.n_out;
+    if (n > r.chunk_begin && (n - r.chunk_begin >= r.apc || n == r.max_new)) {
+      const int b = r.chunk_begin;
+      r.chunk_begin = n;
+      const std::uint64_t gen = r.gen;
+      TokenSeq toks;
+      toks.reserve(static_cast<std::size_t>(n - b));
+      for (int q = b; q < n; ++q) toks.push_back(ref(r.slot, q));
+      events_.push_back(EngineEvent{EngineEvent::Chunk, t, id, b, n});
+      const auto fns = r.chunk_fns;
+      for (const auto& fn : fns) {
+        fn(b, n, toks);
+        if (r.gen != gen) break;  // a callback cancelled this request
+      }
+    }
+    if (r.n_out == r.max_new && !r.cancelled) done.push_back(&r);
+  }
+  // phase B: completions
+  for (Req* r : done) {
+    if (r->cancelled || r->finished) continue;
+    r->finished = true;
+    r->rec.decode_end = t;
+    r->rec.complete = t;
+    r->rec.output_tokens = r->max_new;
+    events_.push_back(EngineEvent{EngineEvent::DecodeEnd, t, r->id, r->max_new, 0});
+    const auto fns = r->end_fns;
+    for (const auto& fn : fns) fn(t);
+  }
+  // phase C: deferred work (early-exit evaluations), FIFO
+  while (!deferred_.empty()) {
+    auto fn = std::move(deferred_.front());
+    deferred_.pop_front();
+    fn();
+  }
+}
+
+void GpuEngine::run(int max_ticks) {
+  while (busy()) {
+    step();
+    if (tick_ > max_ticks) throw RunError("engine: tick limit exceeded");
+  }
+}
+
+TokenSeq GpuEngine::resolve(const TokenSeq& seq) {
+  bool any = false;
+  for (Token t : seq) any |= t < 0;
+  if (!any) return seq;
+  std::vector<int> host(static_cast<std::size_t>(slots_) * opt_.max_out);
+  MOA_CUDA(cudaMemcpyAsync(host.data(), out_tok_, sizeof(int) * host.size(), cudaMemcpyDeviceToHost, stream_));
+  MOA_CUDA(cudaStreamSynchronize(stream_));
+  TokenSeq out(seq);
+  for (Token& t : out)
+    if (t < 0) t = host[static_cast<std::size_t>(-1 - t)];
+  return out;
+}
+
+void GpuEngine::read_outputs(const AgentId& id, int n, int* tok, float* lp, float* ent) {
+  const Req& r = req(id);
+  if (n < 0 || n > opt_.max_out) throw ValidationError("engine: read_outputs count out of range");
+  const long long off = static_cast<long long>(r.slot) * opt_.max_out;
+  if (tok) MOA_CUDA(cudaMemcpyAsync(tok, out_tok_ + off, sizeof(int) * n, cudaMemcpyDeviceToHost, stream_));
+  if (lp) MOA_CUDA(cudaMemcpyAsync(lp, out_lp_ + off, sizeof(float) * n, cudaMemcpyDeviceToHost, stream_));
+  if (ent) MOA_CUDA(cudaMemcpyAsync(ent, out_ent_ + off, sizeof(float) * n, cudaMemcpyDeviceToHost, stream_));
+  MOA_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void GpuEngine::read_logits(const AgentId& id, int kk, float* dst) {
+  if (!logits_) throw ValidationError("engine: keep_logits is off");
+  const Req& r = req(id);
+  const int V = models_[static_cast<std::size_t>(r.model)]->spec().vocab;
+  const long long home = (static_cast<long long>(r.slot) * opt_.max_out + kk) * logits_v_;
+  MOA_CUDA(cudaMemcpyAsync(dst, logits_ + home, sizeof(float) * V, cudaMemcpyDeviceToHost, stream_));
+  MOA_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void GpuEngine::reset() {
+  MOA_CUDA(cudaStreamSynchronize(stream_));
+  reqs_.clear();
+  order_.clear();
+  deferred_.clear();
+  events_.clear();
+  tick_ = 0;
+  slots_ = 0;
+  rows_total_ = 0;
+  weight_bytes_ = 0.0;
+  forwards_ = 0;
+  for (auto& m : models_) m->reset_bindings();
+}
+
+GpuMetricQ& GpuEngine::ee_evaluator(int i, int hidden, std::uint64_t seed, double tau, bool diag, int members,
+                                     int max_tokens) {
+  if (static_cast<int>(ee_pool_.size()) <= i) ee_pool_.resize(static_cast<std::size_t>(i) + 1);
+  auto& e = ee_pool_[static_cast<std::size_t>(i)];
+  if (!e || !e->fits(hidden, members, max_tokens))
+    e = std::make_unique<GpuMetricQ>(hidden, seed, tau, diag, std::max(members, 8), std::max(max_tokens, 512), stream_);
+  e->reset(seed, tau, diag);
+  return *e;
+}
+
+void GpuEngine::mark_start() { MOA_CUDA(cudaEventRecord(start_ev_, stream_)); }
+
+double GpuEngine::ms_since_start(int t) {
+  if (t < 0 || t >= static_cast<int>(tick_ev_.size())) return 0.0;
+  MOA_CUDA(cudaEventSynchronize(tick_ev_[static_cast<std::size_t>(t)]));
+  float ms = 0.f;
+  MOA_CUDA(cudaEventElapsedTime(&ms, start_ev_, tick_ev_[static_cast<std::size_t>(t)]));
+  return ms;
+}
+
+}  // namespace moa

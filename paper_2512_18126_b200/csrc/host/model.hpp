@@ -1,0 +1,94 @@
+// One agent model resident on the device: bf16 weights (hash-uniform init,
+// bit-identical with oracle/model.py), the RoPE table, a KV pool for the
+// agents bound to it, and the per-tick workspace.  `forward` runs one ragged
+// batch of rows (decode rows + incremental-prefill rows of any agents of this
+// model) through all layers and writes greedy token / logprob / entropy for
+// the rows that need logits.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../kernels/kernels.cuh"
+#include "common.hpp"
+
+namespace moa {
+
+void cuda_check(cudaError_t e, const char* what);
+#define MOA_CUDA(x) ::moa::cuda_check((x), #x)
+
+struct ModelSpec {
+  std::string tag;
+  int d = 256, n_layers = 4, n_heads = 4, n_kv_heads = 4, head_dim = 64, ffn = 1024;
+  int vocab = 50000;
+  double rope_theta = 10000.0, norm_eps = 1e-5, lm_gain = 4.0;
+  std::uint64_t seed = 0;
+
+  int qkv_cols() const { return (n_heads + 2 * n_kv_heads) * head_dim; }
+  long long weight_elems() const;
+  double weight_bytes() const { return 2.0 * static_cast<double>(weight_elems()); }
+  void validate() const;
+};
+
+struct ForwardBuffers {
+  k::RowDesc* rows = nullptr;  // [max_rows]
+  int* sel = nullptr;          // [2][max_logit_rows]: logits row index, flat output index
+};
+
+class DeviceModel {
+ public:
+  DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int max_rows, int max_logit_rows,
+              cudaStream_t st);
+  ~DeviceModel();
+  DeviceModel(const DeviceModel&) = delete;
+  DeviceModel& operator=(const DeviceModel&) = delete;
+
+  const ModelSpec& spec() const { return spec_; }
+  int bind_agent();  // next free KV slot
+  void reset_bindings() { bound_ = 0; }
+  int max_rows() const { return max_rows_; }
+  int max_logit_rows() const { return max_lrows_; }
+  const ForwardBuffers& buffers() const { return buf_; }
+
+  // R rows / Rl logits rows already resident in buffers(); out_* are the
+  // engine's flat per-agent output arrays; logits (optional) [Rl][V] fp32.
+  void forward(int R, int Rl, const int* out_tok_read, int* out_tok, float* out_lp, float* out_ent,
+               float* logits, cudaStream_t st);
+
+  // Algorithmic bytes one forward must move for weights (every tick reads the
+  // full weight set once) -- the roofline basis.
+  double weight_bytes() const { return spec_.weight_bytes(); }
+
+ private:
+  int split_k(int N, int K, int R) const;
+
+  ModelSpec spec_;
+  int max_agents_, max_ctx_, max_rows_, max_lrows_;
+  int bound_ = 0;
+  // weights
+  k::bf16* wbase_ = nullptr;
+  k::bf16* emb_ = nullptr;
+  k::bf16* lm_ = nullptr;
+  struct Layer {
+    k::bf16 *wqkv, *wo, *wgu, *wd;
+  };
+  std::vector<Layer> layers_;
+  float* ones_ = nullptr;  // RMSNorm gains (all 1.0)
+  float2* rope_ = nullptr;
+  // KV pools [agents][L][nkv][max_ctx][hd]
+  k::bf16* kpool_ = nullptr;
+  k::bf16* vpool_ = nullptr;
+  long long kv_stride_ = 0, layer_stride_ = 0;
+  // workspace
+  float* x_ = nullptr;
+  k::bf16* h_ = nullptr;
+  k::bf16* q_ = nullptr;
+  float* P_ = nullptr;
+  long long P_cap_ = 0;
+  k::LmStat* part_ = nullptr;
+  ForwardBuffers buf_;
+};
+
+}  // namespace moa

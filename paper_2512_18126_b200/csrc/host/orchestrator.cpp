@@ -1,0 +1,265 @@
+#include "orchestrator.hpp"
+
+#include <chrono>
+
+namespace moa {
+
+void RunConfig::validate() const {  // orchestrator.cpp:21-62
+  if (topology.layers().back().size() != 1)
+    throw ValidationError("run: last layer must hold a single aggregator");
+  if (!(tau > 0.0 && tau <= 1.0)) throw ValidationError("run.tau: must be in (0, 1]");
+  if (chunk_size <= 0) throw ValidationError("run.chunk_size: must be > 0");
+  if (force_q && !(*force_q >= 0.0 && *force_q <= 1.0)) throw ValidationError("run.force_q: must be in [0, 1]");
+  if (query_tokens < 0 || leaf_prefix_tokens < 0 || agg_prefix_tokens < 0 || separator_tokens < 0 ||
+      suffix_tokens < 0)
+    throw ValidationError("run: token counts must be >= 0");
+  if (hidden <= 0) throw ValidationError("provider.hidden: must be > 0");
+  for (const auto& layer : topology.layers())
+    for (const auto& a : layer) {
+      if (!model_of.count(a)) throw ValidationError("run: no model assigned to agent " + a.str());
+      auto it = out_len.find(a);
+      if (it == out_len.end()) throw ValidationError("run: no output length for agent " + a.str());
+      if (it->second.lo < 0 || it->second.hi < it->second.lo)
+        throw ValidationError("run: output length needs 0 <= min <= max for agent " + a.str());
+    }
+}
+
+namespace {
+
+bool incremental(ScheduleMode m) { return m == ScheduleMode::IncrementalOverlap; }
+
+// SimDriver (scenario.cpp:10-116) over the GPU engine.
+class Driver {
+ public:
+  Driver(GpuEngine& eng, ScheduleMode mode, int chunk) : eng_(eng), mode_(mode), chunk_(chunk) {}
+
+  void add_source(const AgentId& a, int model, TokenSeq prompt, int n) {
+    eng_.add_agent(a, model);
+    order_.push_back(a);
+    dependent_[a] = false;
+    out_len_[a] = n;
+    plans_.emplace(a, SlotPlan(a, PromptTemplate(std::move(prompt), {}, {}), false));
+  }
+
+  void add_plan(const AgentId& a, int model, PromptTemplate tmpl, int n) {
+    eng_.add_agent(a, model);
+    order_.push_back(a);
+    dependent_[a] = !tmpl.slots().empty();
+    out_len_[a] = n;
+    for (const auto& s : tmpl.slots()) consumers_[s.precursor].push_back(a);
+    plans_.emplace(a, SlotPlan(a, std::move(tmpl), incremental(mode_)));
+  }
+
+  void start() {
+    for (const auto& [dep, cs] : consumers_)
+      for (const AgentId& c : cs) {
+        const AgentId d = dep, cc = c;
+        eng_.on_chunk(d, [this, d, cc](int, int, const TokenSeq& toks) { apply(cc, plans_.at(cc).on_chunk(d, toks)); });
+      }
+    for (const AgentId& a : order_) eng_.on_decode_end(a, [this, a](int) { completed(a); });
+    for (const AgentId& a : order_) apply(a, plans_.at(a).start());
+  }
+
+  void apply(const AgentId& a, const std::vector<RouteAction>& acts) {
+    for (const RouteAction& x : acts) {
+      switch (x.kind) {
+        case RouteAction::Kind::PrefillOnly:
+          eng_.submit_prefill_only(a, x.start, x.tokens);
+          break;
+        case RouteAction::Kind::Generate: {
+          const int pc = (mode_ == ScheduleMode::DpChunkedPrefill && dependent_.at(a)) ? chunk_ : 0;
+          eng_.submit_generate(a, x.tokens, out_len_.at(a), chunk_, pc);
+          break;
+        }
+        case RouteAction::Kind::Reclaim:
+          eng_.reclaim(a, x.start);
+          break;
+      }
+    }
+  }
+
+  void release(const AgentId& p) {
+    auto it = consumers_.find(p);
+    if (it == consumers_.end()) return;
+    for (const AgentId& c : it->second) {
+      eng_.note_precursor_ready(c);
+      apply(c, plans_.at(c).on_precursor_done(p));
+    }
+  }
+
+  void prune(const AgentId& p) {
+    eng_.cancel(p);
+    auto it = consumers_.find(p);
+    if (it == consumers_.end()) return;
+    for (const AgentId& c : it->second) {
+      SlotPlan& plan = plans_.at(c);
+      apply(c, plan.on_precursor_cancelled(p));
+      if (plan.all_inputs_pruned()) eng_.mark_empty_input(c);
+    }
+  }
+
+  std::function<void(const AgentId&)> gate;
+  const std::vector<AgentId>& order() const { return order_; }
+
+ private:
+  void completed(const AgentId& a) {
+    if (gate)
+      gate(a);
+    else
+      release(a);
+  }
+
+  GpuEngine& eng_;
+  ScheduleMode mode_;
+  int chunk_;
+  std::vector<AgentId> order_;
+  std::map<AgentId, SlotPlan> plans_;
+  std::map<AgentId, int> out_len_;
+  std::map<AgentId, std::vector<AgentId>> consumers_;
+  std::map<AgentId, bool> dependent_;
+};
+
+struct ExitGroup {
+  int index = 0;
+  std::vector<AgentId> members;
+  GpuMetricQ* eval = nullptr;
+  rng::Stream stream{0};
+  bool exited = false;
+  int evals = 0;
+};
+
+}  // namespace
+
+QueryResult run_query(GpuEngine& eng, const RunConfig& cfg, int sample, bool resolve) {
+  const auto t0 = std::chrono::steady_clock::now();
+  cfg.validate();
+  const Topology& topo = cfg.topology;
+  const std::uint64_t ss = rng::hash_combine(cfg.seed, static_cast<std::uint64_t>(sample));
+  eng.reset();
+  Driver drv(eng, cfg.mode, cfg.chunk_size);
+
+  // prompt synthesis + registration (orchestrator.cpp:151-191)
+  const TokenSeq query = rng::synth_tokens(ss, "query", cfg.query_tokens);
+  int max_out = 0;
+  for (const auto& layer : topo.layers())
+    for (const AgentId& a : layer) {
+      const OutLen ol = cfg.out_len.at(a);
+      int n = ol.lo;
+      if (ol.hi != ol.lo) {
+        rng::Stream s = rng::Stream::derive(ss, "outlen:" + a.str());
+        n = static_cast<int>(s.next_int(ol.lo, ol.hi));
+      }
+      max_out = std::max(max_out, n);
+      if (topo.precursors(a).empty()) {
+        TokenSeq prompt = rng::synth_tokens(ss, "leaf_prefix:" + a.str(), cfg.leaf_prefix_tokens);
+        prompt.insert(prompt.end(), query.begin(), query.end());
+        drv.add_source(a, cfg.model_of.at(a), std::move(prompt), n);
+      } else {
+        std::vector<Slot> slots;
+        const auto& pre = topo.precursors(a);
+        for (std::size_t k = 0; k < pre.size(); ++k)
+          slots.push_back(Slot{pre[k], rng::synth_tokens(ss, "sep:" + a.str() + ":" + std::to_string(k),
+                                                         cfg.separator_tokens)});
+        PromptTemplate tmpl(rng::synth_tokens(ss, "agg_prefix:" + a.str(), cfg.agg_prefix_tokens), std::move(slots),
+                            rng::synth_tokens(ss, "suffix:" + a.str(), cfg.suffix_tokens));
+        drv.add_plan(a, cfg.model_of.at(a), std::move(tmpl), n);
+      }
+    }
+
+  // exit groups (orchestrator.cpp:193-220)
+  QueryResult res;
+  std::vector<std::unique_ptr<ExitGroup>> groups;
+  std::map<AgentId, ExitGroup*> group_of;
+  if (cfg.early_exit && topo.depth() > 1) {
+    std::vector<std::vector<AgentId>> sets;
+    if (cfg.exit_scope == ExitScope::Layer || topo.kind() == TopologyKind::AllToAll) {
+      for (int l = 1; l < topo.depth(); ++l) sets.push_back(topo.layer(l));
+    } else {
+      for (int l = 2; l <= topo.depth(); ++l)
+        for (auto& c : topo.clusters_of_layer(l)) sets.push_back(c);
+    }
+    for (std::size_t g = 0; g < sets.size(); ++g) {
+      auto grp = std::make_unique<ExitGroup>();
+      grp->index = static_cast<int>(g);
+      grp->members = sets[g];
+      grp->eval = &eng.ee_evaluator(static_cast<int>(g), cfg.hidden, cfg.provider_seed, cfg.tau,
+                                    cfg.include_diagonal, static_cast<int>(sets[g].size()), std::max(1, max_out));
+      grp->stream = rng::Stream::derive(ss, "ee:" + std::to_string(g));
+      for (const AgentId& m : grp->members) group_of[m] = grp.get();
+      groups.push_back(std::move(grp));
+    }
+    // completion gate (orchestrator.cpp:222-276); evaluations run between ticks
+    drv.gate = [&](const AgentId& producer) {
+      auto it = group_of.find(producer);
+      if (it == group_of.end() || it->second->exited) {
+        drv.release(producer);
+        return;
+      }
+      ExitGroup* grp = it->second;
+      eng.defer([&, producer, grp]() {
+        MetricQRecord rec;
+        rec.tick = eng.tick();
+        rec.group = grp->index;
+        rec.eval_index = grp->evals;
+        rec.completed = producer;
+        if (grp->exited) {
+          res.metricq.push_back(rec);
+          drv.release(producer);
+          return;
+        }
+        grp->evals += 1;
+        rec.evaluated = true;
+        const int n = eng.record(producer).output_tokens;
+        rec.score = grp->eval->add_completion(eng.d_out_tok(), eng.d_out_lp(), eng.out_offset(producer), n);
+        const double q = cfg.force_q ? *cfg.force_q : rec.score.q;
+        rec.decision = decide_exit(q, grp->stream);
+        if (rec.decision.exited) {
+          grp->exited = true;
+          for (const AgentId& m : grp->members) {
+            if (m == producer || eng.finished(m) || eng.cancelled(m)) continue;
+            rec.pruned.push_back(m);
+          }
+        }
+        for (const AgentId& m : rec.pruned) drv.prune(m);
+        res.metricq.push_back(rec);
+        drv.release(producer);
+      });
+    };
+  }
+
+  eng.mark_start();
+  drv.start();
+  eng.run();
+
+  // roll-up
+  res.agents = drv.order();
+  int last = -1;
+  for (const AgentId& a : res.agents) {
+    const AgentRecord& r = eng.record(a);
+    res.records[a] = r;
+    last = std::max(last, r.complete);
+    if (r.invoked && !r.pruned) res.tokens += r.output_tokens;
+    res.decoded_tokens += eng.decoded(a);
+  }
+  res.ticks = last + 1;
+  res.e2e_ms = eng.ms_since_start(last);
+  res.weight_bytes = eng.bytes_moved();
+  res.rows = eng.rows_processed();
+  res.forwards = eng.kernel_forwards();
+  if (resolve) {
+    for (const AgentId& a : res.agents) {
+      res.prompts[a] = eng.resolve(eng.prompt(a));
+      const int n = eng.record(a).output_tokens;
+      TokenSeq out(static_cast<std::size_t>(n));
+      std::vector<float> lp(static_cast<std::size_t>(n)), ent(static_cast<std::size_t>(n));
+      if (n > 0) eng.read_outputs(a, n, out.data(), lp.data(), ent.data());
+      res.outputs[a] = std::move(out);
+      res.logprobs[a] = std::move(lp);
+      res.entropy[a] = std::move(ent);
+    }
+  }
+  res.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return res;
+}
+
+}  // namespace moa

@@ -1,0 +1,78 @@
+// run_query over the GPU engine: prompt synthesis, source/plan registration,
+// slot-filling driver, exit groups and the completion gate, exactly as the
+// reference wires them (orchestrator.cpp:130-295, scenario.cpp:10-116), with
+// agent outputs produced by greedy decode on the device.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "graph.hpp"
+#include "metricq.hpp"
+
+namespace moa {
+
+enum class ScheduleMode { SequentialPd, DpOnly, DpChunkedPrefill, IncrementalOverlap };  // pdsim.hpp:38
+enum class ExitScope { Cluster, Layer };                                                   // orchestrator.hpp:17
+
+struct OutLen {
+  int lo = 64, hi = 64;  // fixed when lo == hi, else uniform (agent.hpp:40-103)
+};
+
+struct RunConfig {  // orchestrator.hpp:23-53 (+ model per agent, which replaces rates)
+  Topology topology = Topology::tree({1}, {});
+  std::map<AgentId, int> model_of;
+  std::map<AgentId, OutLen> out_len;
+  ScheduleMode mode = ScheduleMode::IncrementalOverlap;
+  bool early_exit = false;
+  ExitScope exit_scope = ExitScope::Cluster;
+  double tau = kDefaultTau;
+  bool include_diagonal = true;
+  std::optional<double> force_q;
+  int chunk_size = 32;
+  std::uint64_t seed = 0;
+  int query_tokens = 256, leaf_prefix_tokens = 64, agg_prefix_tokens = 96, separator_tokens = 0,
+      suffix_tokens = 32;
+  int hidden = 64;
+  std::uint64_t provider_seed = 0;
+
+  void validate() const;
+};
+
+struct MetricQRecord {  // trace.hpp:69-78
+  int tick = 0;
+  int group = 0;
+  int eval_index = 0;
+  AgentId completed;
+  bool evaluated = false;
+  QualityScore score;
+  ExitDecision decision;
+  std::vector<AgentId> pruned;
+};
+
+struct QueryResult {
+  std::vector<AgentId> agents;  // registration order
+  std::map<AgentId, AgentRecord> records;
+  std::map<AgentId, TokenSeq> prompts;  // literal tokens
+  std::map<AgentId, TokenSeq> outputs;  // literal tokens (emitted prefix for pruned agents)
+  std::map<AgentId, std::vector<float>> logprobs, entropy;
+  std::vector<MetricQRecord> metricq;
+  int ticks = 0;
+  long long tokens = 0;          // output tokens of invoked, unpruned agents
+  long long decoded_tokens = 0;  // every token the GPU produced (incl. pruned)
+  double e2e_ms = 0.0;           // first tick -> last completion (device events)
+  double wall_ms = 0.0;          // host wall clock around the whole call
+  double weight_bytes = 0.0;     // sum of per-forward weight reads
+  long long rows = 0;
+  int forwards = 0;
+};
+
+// One orchestrated request on `eng` (which must hold every model the config
+// names).  `resolve` = copy literal prompts/outputs back to the host.
+QueryResult run_query(GpuEngine& eng, const RunConfig& cfg, int sample, bool resolve = true);
+
+}  // namespace moa

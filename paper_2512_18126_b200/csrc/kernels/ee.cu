@@ -1,0 +1,153 @@
+// Early-exit signal kernels (fp64 on B200's FP64 pipe):
+//   confidence  C = exp(mean logprob)            metricq.cpp:18-23
+//   mock embed  hash rows, row-centred           embedding.cpp:91-113 (bit-exact)
+//   corr        cosine-normalised Gram t^T t     metricq.cpp:32-53, :157
+//   FCS         Frobenius cosine of two corrs    metricq.cpp:55-64
+// The h x h formulation is used (h = 64 for the preset provider, h <= n);
+// DESIGN.md §6 gives the n x n cross-Gram route for hidden-state widths.
+#include "kernels.cuh"
+
+namespace moa::k {
+
+namespace {
+
+__device__ __forceinline__ std::uint64_t mix64(std::uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ std::uint64_t hash_combine(std::uint64_t a, std::uint64_t b) {
+  return mix64(a ^ (b + 0x9e3779b97f4a7c15ULL + (a << 6) + (a >> 2)));
+}
+
+__global__ void confidence_kernel(const float* __restrict__ lp, int n, double* __restrict__ c) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += static_cast<double>(lp[i]);  // sequential, as the reference
+    *c = exp(s / static_cast<double>(n));
+  }
+}
+
+__global__ void mock_embed_kernel(const int* __restrict__ out_tok, long long base, int h,
+                                  std::uint64_t seed, double* __restrict__ emb) {
+  extern __shared__ double row[];
+  const int r = blockIdx.x;
+  const std::uint64_t tok = static_cast<std::uint64_t>(static_cast<std::int64_t>(out_tok[base + r]));
+  const std::uint64_t row_seed = hash_combine(hash_combine(seed, tok), static_cast<std::uint64_t>(r));
+  for (int c = threadIdx.x; c < h; c += blockDim.x) {
+    const std::uint64_t bits = mix64(hash_combine(row_seed, static_cast<std::uint64_t>(c)));
+    const double u = static_cast<double>(bits >> 11) * 0x1.0p-53;
+    row[c] = __dsub_rn(__dmul_rn(2.0, u), 1.0);
+  }
+  __syncthreads();
+  __shared__ double mean;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int c = 0; c < h; ++c) s += row[c];  // sequential row mean (embedding.cpp:104-108)
+    mean = s / static_cast<double>(h);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < h; c += blockDim.x)
+    emb[static_cast<long long>(r) * h + c] = row[c] - mean;
+}
+
+// gram[i][j] = sum_r emb[r][i] * emb[r][j], sequential in r; mirrored so the
+// matrix is exactly symmetric.
+__global__ void gram_kernel(const double* __restrict__ emb, int n, int h, double* __restrict__ gram) {
+  const long long total = static_cast<long long>(h) * h;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = static_cast<int>(t / h), j = static_cast<int>(t % h);
+    if (j < i) continue;
+    double s = 0.0;
+    for (int r = 0; r < n; ++r) s = __dadd_rn(s, __dmul_rn(emb[r * h + i], emb[r * h + j]));
+    gram[static_cast<long long>(i) * h + j] = s;
+    gram[static_cast<long long>(j) * h + i] = s;
+  }
+}
+
+__global__ void corr_kernel(const double* __restrict__ gram, int h, double eps, double* __restrict__ corr) {
+  const long long total = static_cast<long long>(h) * h;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = static_cast<int>(t / h), j = static_cast<int>(t % h);
+    const double gi = gram[static_cast<long long>(i) * h + i], gj = gram[static_cast<long long>(j) * h + j];
+    double v = 0.0;
+    if (gi > eps && gj > eps) {
+      if (i == j) {
+        v = 1.0;
+      } else {
+        const int a = i < j ? i : j, b = i < j ? j : i;  // reference computes the upper triangle
+        v = gram[static_cast<long long>(a) * h + b] / sqrt(gram[static_cast<long long>(a) * h + a] *
+                                                           gram[static_cast<long long>(b) * h + b]);
+      }
+    }
+    corr[t] = v;
+  }
+}
+
+__global__ void fcs_kernel(const double* __restrict__ cu, const double* __restrict__ corrs, int h,
+                           double* __restrict__ sim) {
+  __shared__ double red[3][32];
+  const int j = blockIdx.x;
+  const double* cv = corrs + static_cast<long long>(j) * h * h;
+  double dot = 0.0, nu = 0.0, nv = 0.0;
+  const long long total = static_cast<long long>(h) * h;
+  for (long long t = threadIdx.x; t < total; t += blockDim.x) {
+    const double a = cu[t], b = cv[t];
+    dot = fma(a, b, dot);
+    nu = fma(a, a, nu);
+    nv = fma(b, b, nv);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    nu += __shfl_xor_sync(0xffffffffu, nu, o);
+    nv += __shfl_xor_sync(0xffffffffu, nv, o);
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    red[0][w] = dot;
+    red[1][w] = nu;
+    red[2][w] = nv;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double d = 0, a = 0, b = 0;
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) {
+      d += red[0][i];
+      a += red[1][i];
+      b += red[2][i];
+    }
+    const double su = sqrt(a), sv = sqrt(b);
+    sim[j] = (su == 0.0 || sv == 0.0) ? 0.0 : d / (su * sv);
+  }
+}
+
+}  // namespace
+
+void ee_confidence(const float* lp, int n, double* c, cudaStream_t st) {
+  confidence_kernel<<<1, 32, 0, st>>>(lp, n, c);
+}
+
+void ee_mock_embed(const int* out_tok, long long base, int n, int h, std::uint64_t seed, double* emb,
+                   cudaStream_t st) {
+  if (n > 0)
+    mock_embed_kernel<<<n, h < 256 ? ((h + 31) / 32) * 32 : 256, h * sizeof(double), st>>>(out_tok, base, h,
+                                                                                          seed, emb);
+}
+
+void ee_corr(const double* emb, int n, int h, double eps, double* gram, double* corr, cudaStream_t st) {
+  const long long total = static_cast<long long>(h) * h;
+  const int blocks = static_cast<int>((total + 255) / 256 < 592 ? (total + 255) / 256 : 592);
+  gram_kernel<<<blocks, 256, 0, st>>>(emb, n, h, gram);
+  corr_kernel<<<blocks, 256, 0, st>>>(gram, h, eps, corr);
+}
+
+void ee_fcs(const double* corr_new, const double* corrs, int m, int h, double* sim, cudaStream_t st) {
+  if (m > 0) fcs_kernel<<<m, 256, 0, st>>>(corr_new, corrs, h, sim);
+}
+
+}  // namespace moa::k
