@@ -200,8 +200,13 @@ int moa_slotplan_event(moa_slotplan* p, int op, int layer, int position, const i
 int moa_slotplan_free(moa_slotplan* p);
 
 /* ---- kernel entry points (device pointers; tests and profiling) -------- */
-int moa_k_gemm_skinny(uintptr_t A, int R, uintptr_t W, int N, int K, int S, uintptr_t P, uintptr_t stream);
-int moa_k_init_uniform(uintptr_t dst, long long n, uint64_t base, float scale, uintptr_t stream);
+/* out[R][N] fp32 = A . W^T with A = bf16 A [R][K], or A = bf16(rmsnorm(X)) for
+ * fp32 X (pass 0 for the unused one).  W bf16 [N][K]. */
+int moa_k_gemv(uintptr_t A, uintptr_t X, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
+/* Hash-uniform weight init of a logical [rows][cols] tensor into a device row
+ * layout (0 identity, 1 RoPE-pair interleave per hd rows, 2 even rows, 3 odd rows). */
+int moa_k_init_uniform(uintptr_t dst, long long rows, long long cols, uint64_t base, float scale, int row_map, int hd,
+                       uintptr_t stream);
 
 #ifdef __cplusplus
 }

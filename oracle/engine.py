@@ -10,8 +10,8 @@ reclaim bounds, late actions on cancelled requests dropped.
 One tick:
   1. rows, in agent registration order (skip cancelled / finished):
      - decoding (n_out >= 1, n_out < max_new): one decode row at P+n_out-1;
-     - else the FRONT queued prefill job (one job per tick), if the row budget
-       allows; its last row yields out[0] when it ends the sealed prompt;
+     - else its queued prefill jobs, in order, while they fit the tick's row
+       budget; the last row of the job that ends the sealed prompt yields out[0];
      - else a sealed, fully prefilled prompt that has not started decoding:
        one bootstrap row at P-1 (re-writes the identical KV) yielding out[0]
        (max_new == 0: no row, decode starts and ends this tick).
@@ -57,8 +57,13 @@ class Request:
 
 
 class TickEngine:
-    def __init__(self, models: dict, max_rows_per_tick: int = 16384, keep_logits: bool = False):
-        self.models = models  # tag -> CpuModel
+    def __init__(self, models: dict, max_rows_per_tick: int = 16384, keep_logits: bool = False,
+                 forced: dict | None = None):
+        """forced: agent -> (tokens, logprobs, entropy) replayed instead of the
+        model's greedy outputs (record-and-replay parity: the schedule, routing
+        and early-exit logic then run on exactly the GPU's completions)."""
+        self.models = models  # tag -> CpuModel (unused when forced)
+        self.forced = forced
         self.reqs = {}
         self.order = []
         self.tick = 0
@@ -72,8 +77,8 @@ class TickEngine:
     def add_agent(self, rid, model_tag):
         if rid in self.reqs:
             raise ValidationError(f"sim: agent {aid(rid)} added twice")
-        m = self.models[model_tag]
-        r = Request(rid, model_tag, m.new_kv(), len(self.order))
+        kv = None if self.forced is not None else self.models[model_tag].new_kv()
+        r = Request(rid, model_tag, kv, len(self.order))
         r.rec["submit_tick"] = self.tick
         self.reqs[rid] = r
         self.order.append(rid)
@@ -206,17 +211,18 @@ class TickEngine:
                     budget -= 1
                 continue
             if r.queue:
-                b, e, _ = r.queue[0]
-                if e - b > budget:
+                took = False
+                while r.queue and r.queue[0][1] - r.queue[0][0] <= budget:
+                    b, e, _ = r.queue.popleft()
+                    budget -= e - b
+                    took = True
+                    yields = r.generate_pending and e == len(r.prompt) and r.max_new > 0
+                    lst = rows_by_model.setdefault(r.model, [])
+                    for p in range(b, e):
+                        lst.append((r, p, r.prompt[p], yields and p == e - 1))
+                    plan.append((r, "prefill", (b, e, yields)))
+                if took or r.queue:
                     continue
-                r.queue.popleft()
-                budget -= e - b
-                yields = r.generate_pending and e == len(r.prompt) and r.max_new > 0
-                lst = rows_by_model.setdefault(r.model, [])
-                for p in range(b, e):
-                    lst.append((r, p, r.prompt[p], yields and p == e - 1))
-                plan.append((r, "prefill", (b, e, yields)))
-                continue
             if r.generate_pending and r.prefilled == len(r.prompt):
                 if r.max_new == 0:
                     plan.append((r, "empty", None))
@@ -228,6 +234,15 @@ class TickEngine:
                     budget -= 1
         # 2. forward per model
         for tag, rows in rows_by_model.items():
+            if self.forced is not None:
+                for r, p, _, want in rows:
+                    if want:
+                        k = len(r.out)
+                        tok, lp, ent = self.forced[r.id]
+                        r.out.append(int(tok[k]))
+                        r.lp.append(float(lp[k]))
+                        r.ent.append(float(ent[k]))
+                continue
             m = self.models[tag]
             logits = m.forward([(r.kv, p, tok) for r, p, tok, _ in rows], [w for *_, w in rows])
             if len(logits):

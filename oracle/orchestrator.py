@@ -178,9 +178,10 @@ def exit_groups(cfg: RunConfig, ss: int):
     return groups
 
 
-def run_query(cfg: RunConfig, models: dict, sample: int = 0, keep_logits: bool = False):
+def run_query(cfg: RunConfig, models: dict, sample: int = 0, keep_logits: bool = False, forced=None):
+    """forced: agent -> (tokens, logprobs, entropy) -- replay mode (see TickEngine)."""
     cfg.validate()
-    eng = TickEngine(models, keep_logits=keep_logits)
+    eng = TickEngine(models, keep_logits=keep_logits, forced=forced)
     ss, drv = build_query(cfg, sample, eng)
     records = []
     if cfg.early_exit and cfg.topology.depth > 1:

@@ -1,0 +1,51 @@
+"""Parity helpers (test infrastructure): teacher-forced numerics and
+record-and-replay of a GPU request through the oracle orchestration.
+
+Tolerance rationale: activations are rounded to bf16 at the
+same points on both sides, but fp32 accumulation order differs, which flips
+individual bf16 roundings; the oracle against an fp64-accumulation variant of
+itself already differs by up to ~0.08 in the logits (tests/test_oracle_
+sensitivity.py).  LOGIT_ATOL is twice the measured self-sensitivity; greedy
+ids are compared wherever the oracle's top-1 margin exceeds 2*LOGIT_ATOL.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .model import CpuModel, logit_stats
+
+LOGIT_ATOL = 0.2
+LOGPROB_ATOL = 0.1  # a logprob moves with the logit and the log-sum-exp: <= 2 x a logit error / 4
+
+
+def teacher_forced(model: CpuModel, prompt, outputs):
+    """Logits predicting outputs[k] given prompt + outputs[:k] (one prefill
+    over the whole sequence on a fresh KV)."""
+    seq = list(prompt) + list(outputs[:-1]) if outputs else list(prompt)
+    P, n = len(prompt), len(outputs)
+    if n == 0:
+        return np.zeros((0, model.spec.vocab), np.float32)
+    kv = model.new_kv()
+    want = [i >= P - 1 for i in range(len(seq))]
+    if P == 0:  # empty prompt: BOS 0 bootstraps (engine contract)
+        seq = [0] + list(outputs[:-1])
+        want = [True] * len(seq)
+    return model.forward([(kv, i, t) for i, t in enumerate(seq)], want)
+
+
+def check_agent(model: CpuModel, prompt, out_tokens, out_logprobs, logits_atol=LOGIT_ATOL, lp_atol=LOGPROB_ATOL):
+    """Returns dict(checked, skipped_near_tie, mismatches, max_lp_err).  A
+    mismatch is a GPU greedy id that disagrees with a decisive oracle argmax."""
+    L = teacher_forced(model, prompt, out_tokens)
+    tok, lp, _ = logit_stats(L)
+    srt = np.sort(L, axis=-1)
+    margin = srt[:, -1] - srt[:, -2]
+    decisive = margin > 2 * logits_atol
+    mism = [k for k in range(len(out_tokens)) if decisive[k] and int(tok[k]) != int(out_tokens[k])]
+    # logprob of the GPU's token under the oracle
+    z = L - L.max(axis=-1, keepdims=True)
+    lse = np.log(np.exp(z).sum(axis=-1))
+    lp_gpu_tok = np.array([z[k, out_tokens[k]] - lse[k] for k in range(len(out_tokens))])
+    lp_err = float(np.abs(lp_gpu_tok - np.asarray(out_logprobs)).max()) if len(out_tokens) else 0.0
+    return dict(checked=int(decisive.sum()), skipped_near_tie=int((~decisive).sum()), mismatches=mism,
+                max_lp_err=lp_err, lp_ok=lp_err <= lp_atol)

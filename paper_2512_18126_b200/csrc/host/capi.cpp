@@ -529,19 +529,39 @@ int moa_slotplan_free(moa_slotplan* p) {
   return guard([&] { delete p; });
 }
 
-int moa_k_gemm_skinny(uintptr_t A, int R, uintptr_t W, int N, int K, int S, uintptr_t P, uintptr_t stream) {
+int moa_k_gemv(uintptr_t A, uintptr_t X, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream) {
   return guard([&] {
-    if (S <= 0 || K % (256 * S)) throw moa::ValidationError("gemm_skinny: K must split into multiples of 256");
-    moa::k::gemm_skinny(reinterpret_cast<const moa::k::bf16*>(A), R, reinterpret_cast<const moa::k::bf16*>(W), N, K,
-                        S, reinterpret_cast<float*>(P), reinterpret_cast<cudaStream_t>(stream));
+    if (K % 256) throw moa::ValidationError("gemv: K must be a multiple of 256");
+    if ((A == 0) == (X == 0)) throw moa::ValidationError("gemv: exactly one of A (bf16) / X (fp32, normed) is required");
+    moa::k::GemvArgs a;
+    a.A = reinterpret_cast<const moa::k::bf16*>(A);
+    a.X = reinterpret_cast<const float*>(X);
+    float* ones = nullptr;
+    if (X) {
+      MOA_CUDA(cudaMalloc(&ones, sizeof(float) * K));
+      moa::k::fill_f32(ones, K, 1.0f, reinterpret_cast<cudaStream_t>(stream));
+      a.g = ones;
+    }
+    a.R = R;
+    a.N = N;
+    a.K = K;
+    a.W = reinterpret_cast<const moa::k::bf16*>(W);
+    a.epi = moa::k::kEpiF32;
+    a.out = reinterpret_cast<float*>(out);
+    moa::k::gemv(a, reinterpret_cast<cudaStream_t>(stream));
     MOA_CUDA(cudaGetLastError());
+    if (ones) {
+      MOA_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+      cudaFree(ones);
+    }
   });
 }
 
-int moa_k_init_uniform(uintptr_t dst, long long n, uint64_t base, float scale, uintptr_t stream) {
+int moa_k_init_uniform(uintptr_t dst, long long rows, long long cols, uint64_t base, float scale, int row_map, int hd,
+                       uintptr_t stream) {
   return guard([&] {
-    moa::k::init_uniform(reinterpret_cast<moa::k::bf16*>(dst), n, base, scale,
-                         reinterpret_cast<cudaStream_t>(stream));
+    moa::k::init_uniform_rows(reinterpret_cast<moa::k::bf16*>(dst), rows, cols, base, scale, row_map, hd,
+                              reinterpret_cast<cudaStream_t>(stream));
     MOA_CUDA(cudaGetLastError());
   });
 }

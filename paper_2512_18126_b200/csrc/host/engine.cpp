@@ -215,7 +215,9 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
     MOA_CUDA(cudaMemcpyAsync(dm.buffers().sel, sel, sizeof(int) * 2 * L, cudaMemcpyHostToDevice, stream_));
   MOA_CUDA(cudaEventRecord(s.done, stream_));
   float* logits = (opt_.keep_logits && !lsel.empty()) ? logits_scratch_ : nullptr;
-  dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), out_tok_, out_tok_, out_lp_,
+  int max_pos = 0;
+  for (const auto& rd : rows) max_pos = std::max(max_pos, rd.pos);
+  dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), max_pos, out_tok_, out_tok_, out_lp_,
              out_ent_, logits, stream_);
   if (logits) {  // debug path: scatter each logits row to its (slot, k) home
     const long long V = dm.spec().vocab;
@@ -264,13 +266,16 @@ void GpuEngine::step() {
       continue;
     }
     if (!r.queue.empty()) {
-      const Job j = r.queue.front();
-      if (j.e - j.b > budget) continue;
-      r.queue.pop_front();
-      budget -= j.e - j.b;
-      const bool yields = r.gen_pending && j.e == static_cast<int>(r.prompt.size()) && r.max_new > 0;
-      for (int p = j.b; p < j.e; ++p) add_row(r, p, r.prompt[static_cast<std::size_t>(p)], (yields && p == j.e - 1) ? 0 : -1);
-      plan.push_back(Plan{&r, Prefill, j, yields});
+      // every queued job, in order, while it fits the tick's row budget
+      while (!r.queue.empty() && r.queue.front().e - r.queue.front().b <= budget) {
+        const Job j = r.queue.front();
+        r.queue.pop_front();
+        budget -= j.e - j.b;
+        const bool yields = r.gen_pending && j.e == static_cast<int>(r.prompt.size()) && r.max_new > 0;
+        for (int p = j.b; p < j.e; ++p)
+          add_row(r, p, r.prompt[static_cast<std::size_t>(p)], (yields && p == j.e - 1) ? 0 : -1);
+        plan.push_back(Plan{&r, Prefill, j, yields});
+      }
       continue;
     }
     if (r.gen_pending && r.prefilled == static_cast<int>(r.prompt.size())) {

@@ -29,6 +29,7 @@ struct ModelSpec {
   int qkv_cols() const { return (n_heads + 2 * n_kv_heads) * head_dim; }
   long long weight_elems() const;
   double weight_bytes() const { return 2.0 * static_cast<double>(weight_elems()); }
+  double decode_weight_bytes() const;  // bytes one tick must stream (all but the embedding table)
   void validate() const;
 };
 
@@ -54,16 +55,14 @@ class DeviceModel {
 
   // R rows / Rl logits rows already resident in buffers(); out_* are the
   // engine's flat per-agent output arrays; logits (optional) [Rl][V] fp32.
-  void forward(int R, int Rl, const int* out_tok_read, int* out_tok, float* out_lp, float* out_ent,
+  void forward(int R, int Rl, int max_pos, const int* out_tok_read, int* out_tok, float* out_lp, float* out_ent,
                float* logits, cudaStream_t st);
 
   // Algorithmic bytes one forward must move for weights (every tick reads the
   // full weight set once) -- the roofline basis.
-  double weight_bytes() const { return spec_.weight_bytes(); }
+  double weight_bytes() const { return spec_.decode_weight_bytes(); }
 
  private:
-  int split_k(int N, int K, int R) const;
-
   ModelSpec spec_;
   int max_agents_, max_ctx_, max_rows_, max_lrows_;
   int bound_ = 0;
@@ -85,9 +84,11 @@ class DeviceModel {
   float* x_ = nullptr;
   k::bf16* h_ = nullptr;
   k::bf16* q_ = nullptr;
-  float* P_ = nullptr;
-  long long P_cap_ = 0;
+  float* attn_ws_ = nullptr;
+  long long attn_ws_floats_ = 0;
+  int* attn_cnt_ = nullptr;
   k::LmStat* part_ = nullptr;
+  int* lm_cnt_ = nullptr;
   ForwardBuffers buf_;
 };
 

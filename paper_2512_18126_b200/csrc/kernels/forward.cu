@@ -1,9 +1,11 @@
-// Agent forward kernels for sm_100a (decode + incremental prefill ticks).
+// Agent forward kernels for sm_100a: decode rows and incremental-prefill rows
+// of one tick.
 //
 // Numerics contract (oracle/model.py mirrors it): bf16 weights and bf16 GEMM
 // operands, fp32 accumulation, fp32 residual stream, bf16 KV cache, fp32
-// logits.  Every reduction has a fixed order (split-K partials are summed by
-// the consumer kernel in slice order), so a tick is bit-reproducible.
+// logits.  Every reduction has a fixed order and no tile/split choice depends
+// on the batch, so a row's result does not depend on which rows share its
+// tick (schedule modes decode identical tokens) and reruns are bit-identical.
 #include <cfloat>
 #include <climits>
 #include <cstdio>
@@ -15,6 +17,9 @@ namespace moa::k {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kRB = 8;    // rows per CTA row-block
+constexpr int kCPW = 4;   // output columns per warp
+constexpr int kWarps = 8;
 
 __device__ __forceinline__ std::uint64_t mix64(std::uint64_t z) {
   z += 0x9e3779b97f4a7c15ULL;
@@ -31,21 +36,31 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   return r;
 }
 
-__device__ __forceinline__ float dot8(uint4 a, uint4 b, float acc) {
+__device__ __forceinline__ void unpack8(uint4 a, float (&f)[8]) {
   const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&a);
-  const __nv_bfloat162* y = reinterpret_cast<const __nv_bfloat162*>(&b);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     float2 u = __bfloat1622float2(x[i]);
+    f[2 * i] = u.x;
+    f[2 * i + 1] = u.y;
+  }
+}
+
+__device__ __forceinline__ float dot8(const float (&a)[8], uint4 w, float acc) {
+  const __nv_bfloat162* y = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
     float2 v = __bfloat1622float2(y[i]);
-    acc = fmaf(u.x, v.x, acc);
-    acc = fmaf(u.y, v.y, acc);
+    acc = fmaf(a[2 * i], v.x, acc);
+    acc = fmaf(a[2 * i + 1], v.y, acc);
   }
   return acc;
 }
 
+__device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
 // Reduce 32 per-lane values across the warp: afterwards lane L holds the sum
-// of value L over all lanes (31 shuffles instead of 32 x 5).
+// of value L over all lanes (31 shuffles).
 __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
@@ -60,17 +75,46 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
   return v[0];
 }
 
-__device__ __forceinline__ float block_sum(float v, float* red) {
+__device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) red[w] = v;
-  __syncthreads();
-  float s = 0.f;
-  const int nw = blockDim.x >> 5;
-  for (int i = 0; i < nw; ++i) s += red[i];
-  __syncthreads();
-  return s;
+  return v;
+}
+
+// 1 / sqrt(mean(x^2) + eps) of one K-row, computed by one warp in a fixed order.
+__device__ __forceinline__ float row_inv_rms(const float* __restrict__ x, int K, float eps, int lane) {
+  float ss = 0.f;
+  for (int k = lane * 4; k < K; k += 128) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(x + k));
+    ss = fmaf(v.x, v.x, ss);
+    ss = fmaf(v.y, v.y, ss);
+    ss = fmaf(v.z, v.z, ss);
+    ss = fmaf(v.w, v.w, ss);
+  }
+  ss = warp_sum(ss);
+  return 1.0f / sqrtf(ss / static_cast<float>(K) + eps);
+}
+
+// A fragment: 8 consecutive K elements of one row, as fp32 values of bf16.
+template <bool NORM>
+__device__ __forceinline__ void load_a(const GemvArgs& a, int row, int k, float inv, float (&f)[8]) {
+  if constexpr (NORM) {
+    const float* x = a.X + static_cast<long long>(row) * a.K + k;
+    const float4 x0 = __ldg(reinterpret_cast<const float4*>(x));
+    const float4 x1 = __ldg(reinterpret_cast<const float4*>(x + 4));
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(a.g + k));
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(a.g + k + 4));
+    f[0] = bf16r(x0.x * inv * g0.x);
+    f[1] = bf16r(x0.y * inv * g0.y);
+    f[2] = bf16r(x0.z * inv * g0.z);
+    f[3] = bf16r(x0.w * inv * g0.w);
+    f[4] = bf16r(x1.x * inv * g1.x);
+    f[5] = bf16r(x1.y * inv * g1.y);
+    f[6] = bf16r(x1.z * inv * g1.z);
+    f[7] = bf16r(x1.w * inv * g1.w);
+  } else {
+    unpack8(__ldg(reinterpret_cast<const uint4*>(a.A + static_cast<long long>(row) * a.K + k)), f);
+  }
 }
 
 __device__ __forceinline__ LmStat stat_merge(LmStat a, LmStat b) {
@@ -91,14 +135,31 @@ __device__ __forceinline__ LmStat stat_merge(LmStat a, LmStat b) {
   return r;
 }
 
+__device__ __forceinline__ LmStat shfl_stat(LmStat s, int off) {
+  return LmStat{__shfl_xor_sync(kFull, s.m, off), __shfl_xor_sync(kFull, s.s, off),
+                __shfl_xor_sync(kFull, s.t, off), __shfl_xor_sync(kFull, s.idx, off)};
+}
+
 // --------------------------------------------------------------------------
 
-__global__ void init_uniform_kernel(bf16* dst, long long n, std::uint64_t base, float scale) {
+__global__ void init_uniform_rows_kernel(bf16* dst, long long rows, long long cols, std::uint64_t base,
+                                         float scale, int map, int hd) {
+  const long long n = rows * cols;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    std::uint64_t bits = mix64(base + static_cast<std::uint64_t>(i));
-    float u = __fsub_rn(__fmul_rn(static_cast<float>(bits >> 40), 0x1p-23f), 1.0f);
-    dst[i] = __float2bfloat16_rn(__fmul_rn(u, scale));
+    const std::uint64_t bits = mix64(base + static_cast<std::uint64_t>(i));
+    const float u = __fsub_rn(__fmul_rn(static_cast<float>(bits >> 40), 0x1p-23f), 1.0f);
+    const long long r = i / cols, c = i % cols;
+    long long dr = r;
+    if (map == kRowsRopeInterleave) {
+      const long long h = r / hd, e = r % hd, half = hd / 2;
+      dr = h * hd + (e < half ? 2 * e : 2 * (e - half) + 1);
+    } else if (map == kRowsEven) {
+      dr = 2 * r;
+    } else if (map == kRowsOdd) {
+      dr = 2 * r + 1;
+    }
+    dst[dr * cols + c] = __float2bfloat16_rn(__fmul_rn(u, scale));
   }
 }
 
@@ -114,221 +175,268 @@ __global__ void embed_kernel(const RowDesc* __restrict__ rows, const int* __rest
   int t = rows[r].tok;
   if (t < 0) t = out_tok[-1 - t];
   const bf16* e = emb + static_cast<long long>(t) * d;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) x[static_cast<long long>(r) * d + c] = __bfloat162float(e[c]);
+  for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(e + c), f);
+    float4* o = reinterpret_cast<float4*>(x + static_cast<long long>(r) * d + c);
+    o[0] = make_float4(f[0], f[1], f[2], f[3]);
+    o[1] = make_float4(f[4], f[5], f[6], f[7]);
+  }
 }
 
-__global__ void rmsnorm_kernel(const float* __restrict__ x, const int* __restrict__ sel, int d,
-                               const float* __restrict__ g, float eps, bf16* __restrict__ h) {
-  __shared__ float red[32];
-  const int i = blockIdx.x;
-  const int r = sel ? sel[i] : i;
-  const float* xr = x + static_cast<long long>(r) * d;
-  float ss = 0.f;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) ss = fmaf(xr[c], xr[c], ss);
-  ss = block_sum(ss, red);
-  const float inv = rsqrtf(ss / static_cast<float>(d) + eps);
-  for (int c = threadIdx.x; c < d; c += blockDim.x)
-    h[static_cast<long long>(i) * d + c] = __float2bfloat16_rn(xr[c] * inv * g[c]);
-}
-
-// Skinny GEMM: each warp owns CPW output columns x RB rows x one K slice.
-// Weights stream once per row block through 16-byte non-allocating loads.
-constexpr int kRB = 8, kCPW = 4, kWarps = 8;
-
-__global__ void __launch_bounds__(kWarps * 32)
-gemm_skinny_kernel(const bf16* __restrict__ A, int R, const bf16* __restrict__ W, int N, int K,
-                   int S, float* __restrict__ P) {
+// Fused skinny GEMM.  CTA = 8 warps = WG column groups x KP k-parts; a warp
+// owns 4 columns x 8 rows x one k-part; k-parts meet in shared memory in a
+// fixed order; the epilogue runs on the k-part-0 warps.
+template <int WG, bool NORM>
+__global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
+  constexpr int KP = kWarps / WG;
+  __shared__ float inv_s[kRB];
+  __shared__ float red[KP][WG][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n0 = (blockIdx.x * kWarps + warp) * kCPW;
-  const int s = blockIdx.y;
+  const int cg = warp % WG, kp = warp / WG;
+  const int n0 = (blockIdx.x * WG + cg) * kCPW;
   const int r0 = blockIdx.z * kRB;
-  if (n0 >= N) return;
-  const int ks = K / S, kb = s * ks, ke = kb + ks;
-  const int rows = min(kRB, R - r0);
+  const int rows = min(kRB, a.R - r0);
+  if constexpr (NORM) {
+    if (warp < rows) {
+      const float inv = row_inv_rms(a.X + static_cast<long long>(r0 + warp) * a.K, a.K, a.eps, lane);
+      if (lane == 0) inv_s[warp] = inv;
+    }
+    __syncthreads();
+  }
   float acc[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) acc[i] = 0.f;
-  for (int k = kb + lane * 8; k < ke; k += 256) {
-    uint4 w[kCPW];
+  if (n0 < a.N) {
+    const int kpart = a.K / KP, kb = kp * kpart, ke = kb + kpart;
+    for (int k = kb + lane * 8; k < ke; k += 256) {
+      uint4 w[kCPW];
 #pragma unroll
-    for (int c = 0; c < kCPW; ++c)
-      w[c] = (n0 + c < N) ? ldg_stream(W + static_cast<long long>(n0 + c) * K + k) : make_uint4(0, 0, 0, 0);
+      for (int c = 0; c < kCPW; ++c)
+        w[c] = (n0 + c < a.N) ? ldg_stream(a.W + static_cast<long long>(n0 + c) * a.K + k) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-    for (int r = 0; r < kRB; ++r) {
-      if (r < rows) {
-        uint4 a = __ldg(reinterpret_cast<const uint4*>(A + static_cast<long long>(r0 + r) * K + k));
+      for (int r = 0; r < kRB; ++r) {
+        if (r < rows) {
+          float f[8];
+          load_a<NORM>(a, r0 + r, k, NORM ? inv_s[r] : 0.f, f);
 #pragma unroll
-        for (int c = 0; c < kCPW; ++c) acc[c * kRB + r] = dot8(a, w[c], acc[c * kRB + r]);
+          for (int c = 0; c < kCPW; ++c) acc[c * kRB + r] = dot8(f, w[c], acc[c * kRB + r]);
+        }
       }
     }
   }
-  const float v = transpose_reduce32(acc, lane);
-  const int c = lane / kRB, r = lane % kRB;
-  if (r < rows && n0 + c < N) P[(static_cast<long long>(s) * R + r0 + r) * N + n0 + c] = v;
-}
-
-__global__ void residual_add_kernel(float* __restrict__ x, const float* __restrict__ P, int S,
-                                    long long RN) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < RN;
-       i += (long long)gridDim.x * blockDim.x) {
-    float a = 0.f;
-    for (int s = 0; s < S; ++s) a += P[s * RN + i];
-    x[i] += a;
+  float v = transpose_reduce32(acc, lane);
+  if constexpr (KP > 1) {
+    red[kp][cg][lane] = v;
+    __syncthreads();
+    if (kp != 0) return;
+    v = red[0][cg][lane];
+#pragma unroll
+    for (int p = 1; p < KP; ++p) v += red[p][cg][lane];
   }
-}
-
-__global__ void swiglu_kernel(const float* __restrict__ P, int S, int R, int ffn,
-                              bf16* __restrict__ a) {
-  const long long total = static_cast<long long>(R) * ffn;
-  const long long RN = static_cast<long long>(R) * 2 * ffn;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long r = i / ffn, j = i % ffn;
-    float g = 0.f, u = 0.f;
-    for (int s = 0; s < S; ++s) {
-      g += P[s * RN + r * 2 * ffn + j];
-      u += P[s * RN + r * 2 * ffn + ffn + j];
-    }
-    const float silu = g / (1.0f + __expf(-g));
-    a[i] = __float2bfloat16_rn(silu * u);
-  }
-}
-
-__global__ void rope_kv_kernel(const float* __restrict__ P, int S, const RowDesc* __restrict__ rows,
-                               int R, int nh, int nkv, int hd, const float2* __restrict__ rope,
-                               bf16* __restrict__ q, bf16* __restrict__ kpool,
-                               bf16* __restrict__ vpool, long long kv_stride, long long layer_off,
-                               int max_ctx) {
-  const int r = blockIdx.x;
-  const RowDesc rd = rows[r];
-  const int half = hd / 2;
-  const int N = (nh + 2 * nkv) * hd;
-  const long long RN = static_cast<long long>(R) * N;
-  const float* base = P + static_cast<long long>(r) * N;
-  auto get = [&](int c) {
-    float a = 0.f;
-    for (int s = 0; s < S; ++s) a += base[s * RN + c];
-    return a;
-  };
-  const float2* cs = rope + static_cast<long long>(rd.pos) * half;
-  const int pairs = (nh + nkv) * half;
-  for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
-    const int head = i / half, e = i % half;
-    const float x0 = get(head * hd + e), x1 = get(head * hd + e + half);
-    const float2 c = cs[e];
-    const float y0 = __fsub_rn(__fmul_rn(x0, c.x), __fmul_rn(x1, c.y));
-    const float y1 = __fadd_rn(__fmul_rn(x1, c.x), __fmul_rn(x0, c.y));
-    if (head < nh) {
-      bf16* qo = q + static_cast<long long>(r) * nh * hd + head * hd;
-      qo[e] = __float2bfloat16_rn(y0);
-      qo[e + half] = __float2bfloat16_rn(y1);
-    } else {
-      const int kh = head - nh;
-      bf16* ko = kpool + rd.kv * kv_stride + layer_off +
-                 (static_cast<long long>(kh) * max_ctx + rd.pos) * hd;
-      ko[e] = __float2bfloat16_rn(y0);
-      ko[e + half] = __float2bfloat16_rn(y1);
+  // ---- epilogue: lane L holds column n0 + L/8, row r0 + L%8 ----
+  const int c = lane / kRB, r = lane % kRB, n = n0 + c, row = r0 + r;
+  const bool ok = r < rows && n < a.N;
+  const float partner = __shfl_xor_sync(kFull, v, kRB);  // column n ^ 1 (same row)
+  switch (a.epi) {
+    case kEpiF32:
+      if (ok) a.out[static_cast<long long>(row) * a.N + n] = v;
+      break;
+    case kEpiResidual:
+      if (ok) a.out[static_cast<long long>(row) * a.N + n] += v;
+      break;
+    case kEpiSwiGlu:  // device rows interleave gate (even) / up (odd)
+      if (ok && !(n & 1)) {
+        const float g = v, u = partner;
+        a.out_bf16[static_cast<long long>(row) * (a.N / 2) + n / 2] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
+      }
+      break;
+    case kEpiQkv: {
+      if (!ok) break;
+      const RowDesc rd = a.rows[row];
+      const int hd = a.hd, half = hd / 2;
+      const int qk_cols = (a.nh + a.nkv) * hd;
+      if (n < qk_cols) {
+        if (n & 1) break;  // even lanes own the (x0, x1) RoPE pair
+        const int head = n / hd, i = (n % hd) / 2;
+        const float2 cs = a.rope[static_cast<long long>(rd.pos) * half + i];
+        const float x0 = v, x1 = partner;
+        const float y0 = __fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y));
+        const float y1 = __fadd_rn(__fmul_rn(x1, cs.x), __fmul_rn(x0, cs.y));
+        bf16* dst;
+        if (head < a.nh) {
+          dst = a.out_bf16 + (static_cast<long long>(row) * a.nh + head) * hd;
+        } else {
+          dst = a.kpool + rd.kv * a.kv_stride + a.layer_off +
+                (static_cast<long long>(head - a.nh) * a.max_ctx + rd.pos) * hd;
+        }
+        dst[i] = __float2bfloat16_rn(y0);
+        dst[i + half] = __float2bfloat16_rn(y1);
+      } else {
+        const int vc = n - qk_cols, kh = vc / hd, e = vc % hd;
+        a.vpool[rd.kv * a.kv_stride + a.layer_off + (static_cast<long long>(kh) * a.max_ctx + rd.pos) * hd + e] =
+            __float2bfloat16_rn(v);
+      }
+      break;
     }
   }
-  for (int i = threadIdx.x; i < nkv * hd; i += blockDim.x) {
-    const int kh = i / hd, e = i % hd;
-    bf16* vo = vpool + rd.kv * kv_stride + layer_off +
-               (static_cast<long long>(kh) * max_ctx + rd.pos) * hd;
-    vo[e] = __float2bfloat16_rn(get((nh + nkv) * hd + i));
-  }
 }
 
-// One warp per (row, head): online softmax over 32-key blocks.
+// Split-KV attention: CTA (row, head, split) covers kKvSplit keys with 4
+// warps x 32 keys; a row whose context needs several splits writes partials
+// and the last CTA to arrive combines them in split order.
 template <int HD>
 __global__ void __launch_bounds__(128)
 attention_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, int nh, int nkv,
-                 const bf16* __restrict__ kpool, const bf16* __restrict__ vpool,
-                 long long kv_stride, long long layer_off, int max_ctx, bf16* __restrict__ o) {
+                 const bf16* __restrict__ kpool, const bf16* __restrict__ vpool, long long kv_stride,
+                 long long layer_off, int max_ctx, bf16* __restrict__ o, float* __restrict__ ws,
+                 int* __restrict__ cnt, int nsplit_max) {
   constexpr int E = HD / 32;
-  __shared__ float qs[4][HD];
+  __shared__ float qs[HD];
+  __shared__ float wm[4], wl[4], wo[4][HD];
+  __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r = blockIdx.x, h = blockIdx.y * 4 + warp;
-  if (h >= nh) return;
+  const int r = blockIdx.x, h = blockIdx.y, s = blockIdx.z;
   const RowDesc rd = rows[r];
+  const int n = rd.pos + 1;
+  const int nsplit = (n + kKvSplit - 1) / kKvSplit;
+  if (s >= nsplit) return;
   const int kvh = h / (nh / nkv);
   const bf16* qr = q + (static_cast<long long>(r) * nh + h) * HD;
-  for (int e = lane; e < HD; e += 32) qs[warp][e] = __bfloat162float(qr[e]);
-  __syncwarp();
+  for (int e = threadIdx.x; e < HD; e += 128) qs[e] = __bfloat162float(qr[e]);
+  __syncthreads();
   const bf16* K = kpool + rd.kv * kv_stride + layer_off + static_cast<long long>(kvh) * max_ctx * HD;
   const bf16* V = vpool + rd.kv * kv_stride + layer_off + static_cast<long long>(kvh) * max_ctx * HD;
   const float scale = rsqrtf(static_cast<float>(HD));
-  float m = -INFINITY, l = 0.f, acc[E];
+  const int base = s * kKvSplit + warp * 32;
+  const int j = base + lane;
+  float sc = -INFINITY;
+  if (j < n) {
+    const uint4* kp = reinterpret_cast<const uint4*>(K + static_cast<long long>(j) * HD);
+    uint4 kk[HD / 8];
+#pragma unroll
+    for (int v = 0; v < HD / 8; ++v) kk[v] = __ldg(kp + v);
+    float d = 0.f;
+#pragma unroll
+    for (int v = 0; v < HD / 8; ++v) {
+      float f[8];
+      unpack8(kk[v], f);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) d = fmaf(qs[v * 8 + t], f[t], d);
+    }
+    sc = d * scale;
+  }
+  float m = sc;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, off));
+  const float p = (j < n) ? __expf(sc - m) : 0.f;
+  const float l = warp_sum(p);
+  float acc[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
-  const int n = rd.pos + 1;
-  for (int base = 0; base < n; base += 32) {
-    const int j = base + lane;
-    float s = -INFINITY;
-    if (j < n) {
-      const uint4* kp = reinterpret_cast<const uint4*>(K + static_cast<long long>(j) * HD);
-      float d = 0.f;
-#pragma unroll
-      for (int v = 0; v < HD / 8; ++v) {
-        uint4 kk = __ldg(kp + v);
-        const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kk);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          float2 kf = __bfloat1622float2(k2[t]);
-          d = fmaf(qs[warp][v * 8 + 2 * t], kf.x, d);
-          d = fmaf(qs[warp][v * 8 + 2 * t + 1], kf.y, d);
-        }
-      }
-      s = d * scale;
+  const int cntk = max(0, min(32, n - base));
+#pragma unroll 8
+  for (int jj = 0; jj < cntk; ++jj) {
+    const float pj = __shfl_sync(kFull, p, jj);
+    const bf16* vr = V + static_cast<long long>(base + jj) * HD + lane * E;
+    if constexpr (E == 2) {
+      const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
+      acc[0] = fmaf(pj, vf.x, acc[0]);
+      acc[1] = fmaf(pj, vf.y, acc[1]);
+    } else {
+      const uint2 raw = *reinterpret_cast<const uint2*>(vr);
+      const float2 v0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+      const float2 v1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+      acc[0] = fmaf(pj, v0.x, acc[0]);
+      acc[1] = fmaf(pj, v0.y, acc[1]);
+      acc[2] = fmaf(pj, v1.x, acc[2]);
+      acc[3] = fmaf(pj, v1.y, acc[3]);
     }
-    float bm = s;
-#pragma unroll
-    for (int off = 16; off; off >>= 1) bm = fmaxf(bm, __shfl_xor_sync(kFull, bm, off));
-    const float mn = fmaxf(m, bm);
-    const float corr = (m == -INFINITY) ? 0.f : __expf(m - mn);
-    const float p = (j < n) ? __expf(s - mn) : 0.f;
-    float ps = p;
-#pragma unroll
-    for (int off = 16; off; off >>= 1) ps += __shfl_xor_sync(kFull, ps, off);
-    l = l * corr + ps;
-#pragma unroll
-    for (int e = 0; e < E; ++e) acc[e] *= corr;
-    const int cnt = min(32, n - base);
-    for (int jj = 0; jj < cnt; ++jj) {
-      const float pj = __shfl_sync(kFull, p, jj);
-      const bf16* vr = V + static_cast<long long>(base + jj) * HD + lane * E;
-      if constexpr (E == 2) {
-        float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
-        acc[0] = fmaf(pj, vf.x, acc[0]);
-        acc[1] = fmaf(pj, vf.y, acc[1]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; e += 2) {
-          float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr + e));
-          acc[e] = fmaf(pj, vf.x, acc[e]);
-          acc[e + 1] = fmaf(pj, vf.y, acc[e + 1]);
-        }
-      }
-    }
-    m = mn;
   }
-  const float inv = 1.0f / l;
-  bf16* orow = o + (static_cast<long long>(r) * nh + h) * HD + lane * E;
+  if (lane == 0) {
+    wm[warp] = cntk > 0 ? m : -INFINITY;
+    wl[warp] = l;
+  }
 #pragma unroll
-  for (int e = 0; e < E; ++e) orow[e] = __float2bfloat16_rn(acc[e] * inv);
+  for (int e = 0; e < E; ++e) wo[warp][lane * E + e] = acc[e];
+  __syncthreads();
+  // CTA combine of the 4 warps (fixed order)
+  float M = wm[0];
+  for (int w = 1; w < 4; ++w) M = fmaxf(M, wm[w]);
+  float L = 0.f;
+  float sw[4];
+  for (int w = 0; w < 4; ++w) {
+    sw[w] = wm[w] == -INFINITY ? 0.f : __expf(wm[w] - M);
+    L += sw[w] * wl[w];
+  }
+  bf16* orow = o + (static_cast<long long>(r) * nh + h) * HD;
+  if (nsplit == 1) {
+    for (int e = threadIdx.x; e < HD; e += 128) {
+      float val = 0.f;
+      for (int w = 0; w < 4; ++w) val += sw[w] * wo[w][e];
+      orow[e] = __float2bfloat16_rn(val / L);
+    }
+    return;
+  }
+  float* part = ws + ((static_cast<long long>(r) * nh + h) * nsplit_max + s) * (2 + HD);
+  for (int e = threadIdx.x; e < HD; e += 128) {
+    float val = 0.f;
+    for (int w = 0; w < 4; ++w) val += sw[w] * wo[w][e];
+    part[2 + e] = val;
+  }
+  if (threadIdx.x == 0) {
+    part[0] = M;
+    part[1] = L;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = atomicAdd(cnt + r * nh + h, 1);
+    last = prev == nsplit - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const float* pr = ws + (static_cast<long long>(r) * nh + h) * nsplit_max * (2 + HD);
+  float Mg = -INFINITY;
+  for (int t = 0; t < nsplit; ++t) Mg = fmaxf(Mg, __ldcg(pr + t * (2 + HD)));
+  float Lg = 0.f;
+  for (int t = 0; t < nsplit; ++t) Lg += __expf(__ldcg(pr + t * (2 + HD)) - Mg) * __ldcg(pr + t * (2 + HD) + 1);
+  for (int e = threadIdx.x; e < HD; e += 128) {
+    float val = 0.f;
+    for (int t = 0; t < nsplit; ++t) val += __expf(__ldcg(pr + t * (2 + HD)) - Mg) * __ldcg(pr + t * (2 + HD) + 2 + e);
+    orow[e] = __float2bfloat16_rn(val / Lg);
+  }
+  if (threadIdx.x == 0) cnt[r * nh + h] = 0;
 }
 
-// LM head: block b owns a contiguous vocab slice; warps take 4 columns at a
-// time for 8 rows; per-lane running stats are merged warp- then block-wide.
+// LM head: block b owns a contiguous vocab slice; warps take 4 columns x 8
+// rows at a time; rows are normalised on the fly.  The last CTA merges all
+// slices per row in slice order and writes token / logprob / entropy.
 constexpr int kLmBlocksPerSm = 4;
+constexpr int kLmMaxRows = 64;
 
 __global__ void __launch_bounds__(kWarps * 32)
-lm_head_kernel(const bf16* __restrict__ H, int Rl, const bf16* __restrict__ W, int V, int d,
-               LmStat* __restrict__ part, float* __restrict__ logits) {
+lm_head_kernel(const float* __restrict__ X, const int* __restrict__ sel, int Rl, const float* __restrict__ g,
+               float eps, const bf16* __restrict__ W, int V, int d, LmStat* __restrict__ part,
+               int* __restrict__ cnt, const int* __restrict__ out_idx, int* __restrict__ out_tok,
+               float* __restrict__ out_lp, float* __restrict__ out_ent, float* __restrict__ logits) {
+  __shared__ float inv_s[kLmMaxRows];
   __shared__ LmStat sm[kWarps][kRB];
+  __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = gridDim.x;
   const int per = (V + nb - 1) / nb;
   const int c0 = blockIdx.x * per, c1 = min(V, c0 + per);
+  for (int r = warp; r < Rl; r += kWarps) {
+    const float inv = row_inv_rms(X + static_cast<long long>(sel[r]) * d, d, eps, lane);
+    if (lane == 0) inv_s[r] = inv;
+  }
+  __syncthreads();
+  GemvArgs ga;
+  ga.X = X;
+  ga.g = g;
+  ga.K = d;
   for (int r0 = 0; r0 < Rl; r0 += kRB) {
     const int rows = min(kRB, Rl - r0);
     LmStat st{-INFINITY, 0.f, 0.f, INT_MAX};
@@ -344,9 +452,10 @@ lm_head_kernel(const bf16* __restrict__ H, int Rl, const bf16* __restrict__ W, i
 #pragma unroll
         for (int r = 0; r < kRB; ++r) {
           if (r < rows) {
-            uint4 a = __ldg(reinterpret_cast<const uint4*>(H + static_cast<long long>(r0 + r) * d + k));
+            float f[8];
+            load_a<true>(ga, sel[r0 + r], k, inv_s[r0 + r], f);
 #pragma unroll
-            for (int c = 0; c < kCPW; ++c) acc[c * kRB + r] = dot8(a, w[c], acc[c * kRB + r]);
+            for (int c = 0; c < kCPW; ++c) acc[c * kRB + r] = dot8(f, w[c], acc[c * kRB + r]);
           }
         }
       }
@@ -357,11 +466,9 @@ lm_head_kernel(const bf16* __restrict__ H, int Rl, const bf16* __restrict__ W, i
         st = stat_merge(st, LmStat{v, 1.f, 0.f, cb + c});
       }
     }
-    // lanes r, r+8, r+16, r+24 hold the same row
 #pragma unroll
     for (int off = 8; off < 32; off <<= 1) {
-      LmStat o{__shfl_xor_sync(kFull, st.m, off), __shfl_xor_sync(kFull, st.s, off),
-               __shfl_xor_sync(kFull, st.t, off), __shfl_xor_sync(kFull, st.idx, off)};
+      const LmStat o = shfl_stat(st, off);
       st = (lane & off) ? stat_merge(o, st) : stat_merge(st, o);
     }
     if (lane < kRB) sm[warp][lane] = st;
@@ -373,27 +480,37 @@ lm_head_kernel(const bf16* __restrict__ H, int Rl, const bf16* __restrict__ W, i
     }
     __syncthreads();
   }
-}
-
-__global__ void lm_merge_kernel(const LmStat* __restrict__ part, int nblk, const int* __restrict__ out_idx,
-                                int* __restrict__ out_tok, float* __restrict__ out_lp,
-                                float* __restrict__ out_ent) {
-  const int r = blockIdx.x, lane = threadIdx.x;
-  LmStat st{-INFINITY, 0.f, 0.f, INT_MAX};
-  for (int b = lane; b < nblk; b += 32) st = stat_merge(st, part[static_cast<long long>(r) * nblk + b]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(cnt, 1) == nb - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int r = warp; r < Rl; r += kWarps) {
+    LmStat st{-INFINITY, 0.f, 0.f, INT_MAX};
+    const LmStat* pr = part + static_cast<long long>(r) * nb;
+    for (int b = lane; b < nb; b += 32) {
+      LmStat x;
+      x.m = __ldcg(&pr[b].m);
+      x.s = __ldcg(&pr[b].s);
+      x.t = __ldcg(&pr[b].t);
+      x.idx = __ldcg(&pr[b].idx);
+      st = stat_merge(st, x);
+    }
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    LmStat o{__shfl_xor_sync(kFull, st.m, off), __shfl_xor_sync(kFull, st.s, off),
-             __shfl_xor_sync(kFull, st.t, off), __shfl_xor_sync(kFull, st.idx, off)};
-    st = (lane & off) ? stat_merge(o, st) : stat_merge(st, o);
+    for (int off = 1; off < 32; off <<= 1) {
+      const LmStat o = shfl_stat(st, off);
+      st = (lane & off) ? stat_merge(o, st) : stat_merge(st, o);
+    }
+    if (lane == 0) {
+      const int oi = out_idx[r];
+      const float ls = logf(st.s);
+      out_tok[oi] = st.idx;
+      out_lp[oi] = -ls;
+      out_ent[oi] = ls - st.t / st.s;
+    }
   }
-  if (lane == 0) {
-    const int oi = out_idx[r];
-    const float ls = logf(st.s);
-    out_tok[oi] = st.idx;
-    out_lp[oi] = -ls;
-    out_ent[oi] = ls - st.t / st.s;
-  }
+  if (threadIdx.x == 0) *cnt = 0;
 }
 
 inline int grid_for(long long n, int block) {
@@ -401,60 +518,61 @@ inline int grid_for(long long n, int block) {
   return static_cast<int>(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
 }
 
+template <bool NORM>
+void gemv_launch(const GemvArgs& a, cudaStream_t st) {
+  // k-parts per CTA: as many as K allows (each part a multiple of 256)
+  int kp = 8;
+  while (kp > 1 && (a.K % (256 * kp))) kp >>= 1;
+  const int wg = kWarps / kp;
+  dim3 grid((a.N + wg * kCPW - 1) / (wg * kCPW), 1, (a.R + kRB - 1) / kRB);
+  switch (wg) {
+    case 1: gemv_kernel<1, NORM><<<grid, kWarps * 32, 0, st>>>(a); break;
+    case 2: gemv_kernel<2, NORM><<<grid, kWarps * 32, 0, st>>>(a); break;
+    case 4: gemv_kernel<4, NORM><<<grid, kWarps * 32, 0, st>>>(a); break;
+    default: gemv_kernel<8, NORM><<<grid, kWarps * 32, 0, st>>>(a); break;
+  }
+}
+
 }  // namespace
 
-void init_uniform(bf16* dst, long long n, std::uint64_t base, float scale, cudaStream_t st) {
-  init_uniform_kernel<<<grid_for(n, 256), 256, 0, st>>>(dst, n, base, scale);
+void init_uniform_rows(bf16* dst, long long rows, long long cols, std::uint64_t base, float scale, int map, int hd,
+                       cudaStream_t st) {
+  init_uniform_rows_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(dst, rows, cols, base, scale, map, hd);
 }
 
 void fill_f32(float* dst, long long n, float v, cudaStream_t st) {
   fill_f32_kernel<<<grid_for(n, 256), 256, 0, st>>>(dst, n, v);
 }
 
-void embed(const RowDesc* rows, int R, const int* out_tok, const bf16* emb, int d, float* x,
-           cudaStream_t st) {
-  if (R > 0) embed_kernel<<<R, 256, 0, st>>>(rows, out_tok, emb, d, x);
+void embed(const RowDesc* rows, int R, const int* out_tok, const bf16* emb, int d, float* x, cudaStream_t st) {
+  if (R > 0) embed_kernel<<<R, 128, 0, st>>>(rows, out_tok, emb, d, x);
 }
 
-void rmsnorm(const float* x, const int* sel, int R, int d, const float* g, float eps, bf16* h,
-             cudaStream_t st) {
-  if (R > 0) rmsnorm_kernel<<<R, d >= 1024 ? 512 : 256, 0, st>>>(x, sel, d, g, eps, h);
+void gemv(const GemvArgs& a, cudaStream_t st) {
+  if (a.R <= 0) return;
+  if (a.X)
+    gemv_launch<true>(a, st);
+  else
+    gemv_launch<false>(a, st);
 }
 
-void gemm_skinny(const bf16* A, int R, const bf16* W, int N, int K, int S, float* P,
-                 cudaStream_t st) {
+long long attention_ws_floats(int R, int nh, int hd, int max_ctx) {
+  const int ns = (max_ctx + kKvSplit - 1) / kKvSplit;
+  return static_cast<long long>(R) * nh * ns * (2 + hd);
+}
+
+void attention(const bf16* q, const RowDesc* rows, int R, int max_pos, int nh, int nkv, int hd, const bf16* kpool,
+               const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx, bf16* o, float* ws, int* cnt,
+               cudaStream_t st) {
   if (R <= 0) return;
-  dim3 grid((N + kWarps * kCPW - 1) / (kWarps * kCPW), S, (R + kRB - 1) / kRB);
-  gemm_skinny_kernel<<<grid, kWarps * 32, 0, st>>>(A, R, W, N, K, S, P);
-}
-
-void residual_add(float* x, const float* P, int S, int R, int N, cudaStream_t st) {
-  const long long RN = static_cast<long long>(R) * N;
-  if (RN > 0) residual_add_kernel<<<grid_for(RN, 256), 256, 0, st>>>(x, P, S, RN);
-}
-
-void swiglu(const float* P, int S, int R, int ffn, bf16* a, cudaStream_t st) {
-  const long long n = static_cast<long long>(R) * ffn;
-  if (n > 0) swiglu_kernel<<<grid_for(n, 256), 256, 0, st>>>(P, S, R, ffn, a);
-}
-
-void rope_kv(const float* P, int S, const RowDesc* rows, int R, int nh, int nkv, int hd,
-             const float2* rope, bf16* q, bf16* kpool, bf16* vpool, long long kv_stride,
-             long long layer_off, int max_ctx, cudaStream_t st) {
-  if (R > 0)
-    rope_kv_kernel<<<R, 256, 0, st>>>(P, S, rows, R, nh, nkv, hd, rope, q, kpool, vpool, kv_stride,
-                                      layer_off, max_ctx);
-}
-
-void attention(const bf16* q, const RowDesc* rows, int R, int nh, int nkv, int hd,
-               const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off,
-               int max_ctx, bf16* o, cudaStream_t st) {
-  if (R <= 0) return;
-  dim3 grid(R, (nh + 3) / 4);
+  const int nsplit_max = (max_ctx + kKvSplit - 1) / kKvSplit;
+  dim3 grid(R, nh, (max_pos + kKvSplit) / kKvSplit);
   if (hd == 64)
-    attention_kernel<64><<<grid, 128, 0, st>>>(q, rows, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx, o);
+    attention_kernel<64><<<grid, 128, 0, st>>>(q, rows, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx, o, ws,
+                                               cnt, nsplit_max);
   else if (hd == 128)
-    attention_kernel<128><<<grid, 128, 0, st>>>(q, rows, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx, o);
+    attention_kernel<128><<<grid, 128, 0, st>>>(q, rows, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx, o, ws,
+                                                cnt, nsplit_max);
   else
     printf("attention: unsupported head_dim %d\n", hd);
 }
@@ -464,14 +582,16 @@ int lm_head_blocks(int V) {
   return nb < V ? nb : V;
 }
 
-void lm_head_stats(const bf16* h, int Rl, const bf16* W, int V, int d, LmStat* part, float* logits,
-                   cudaStream_t st) {
-  if (Rl > 0) lm_head_kernel<<<lm_head_blocks(V), kWarps * 32, 0, st>>>(h, Rl, W, V, d, part, logits);
-}
-
-void lm_merge(const LmStat* part, int Rl, int nblk, const int* out_idx, int* out_tok, float* out_lp,
-              float* out_ent, cudaStream_t st) {
-  if (Rl > 0) lm_merge_kernel<<<Rl, 32, 0, st>>>(part, nblk, out_idx, out_tok, out_lp, out_ent);
+void lm_head(const float* X, const int* sel, int Rl, const float* g, float eps, const bf16* W, int V, int d,
+             LmStat* part, int* cnt, const int* out_idx, int* out_tok, float* out_lp, float* out_ent, float* logits,
+             cudaStream_t st) {
+  if (Rl <= 0) return;
+  if (Rl > kLmMaxRows) {
+    printf("lm_head: %d logits rows exceed %d\n", Rl, kLmMaxRows);
+    return;
+  }
+  lm_head_kernel<<<lm_head_blocks(V), kWarps * 32, 0, st>>>(X, sel, Rl, g, eps, W, V, d, part, cnt, out_idx, out_tok,
+                                                            out_lp, out_ent, logits);
 }
 
 }  // namespace moa::k

@@ -20,45 +20,73 @@ struct RowDesc {
   int out;
 };
 
-// Running softmax statistics of one vocab slice (see lm_head_stats).
+// Running softmax statistics of one vocab slice (see lm_head).
 struct LmStat {
-  float m;    // max logit
-  float s;    // sum exp(x - m)
-  float t;    // sum (x - m) exp(x - m)
-  int idx;    // argmax (lowest index on ties)
+  float m;  // max logit
+  float s;  // sum exp(x - m)
+  float t;  // sum (x - m) exp(x - m)
+  int idx;  // argmax (lowest index on ties)
 };
 
-void init_uniform(bf16* dst, long long n, std::uint64_t base, float scale, cudaStream_t st);
+// Device weight-row layouts (init_uniform_rows): the fused GEMV epilogues
+// need RoPE pairs / gate-up pairs in adjacent output columns.
+enum RowMap : int {
+  kRowsIdentity = 0,
+  kRowsRopeInterleave = 1,  // within each head of `hd` rows: i -> 2i (i < hd/2), 2(i-hd/2)+1
+  kRowsEven = 2,            // r -> 2r     (gate rows)
+  kRowsOdd = 3,             // r -> 2r + 1 (up rows)
+};
+
+void init_uniform_rows(bf16* dst, long long rows, long long cols, std::uint64_t base, float scale, int map,
+                       int hd, cudaStream_t st);
 void fill_f32(float* dst, long long n, float v, cudaStream_t st);
 
 void embed(const RowDesc* rows, int R, const int* out_tok, const bf16* emb, int d, float* x,
            cudaStream_t st);
-// h[i] = bf16(rmsnorm(x[sel ? sel[i] : i]) * g)
-void rmsnorm(const float* x, const int* sel, int R, int d, const float* g, float eps, bf16* h,
-             cudaStream_t st);
-// P[s][r][n] = sum_{k in slice s} A[r][k] * W[n][k]   (A bf16 [R][K], W bf16 [N][K])
-void gemm_skinny(const bf16* A, int R, const bf16* W, int N, int K, int S, float* P,
-                 cudaStream_t st);
-// x[r][n] += sum_s P[s][r][n]
-void residual_add(float* x, const float* P, int S, int R, int N, cudaStream_t st);
-// a[r][j] = bf16(silu(g) * u), g/u = sum_s P[s][r][j], P[s][r][ffn + j]
-void swiglu(const float* P, int S, int R, int ffn, bf16* a, cudaStream_t st);
-// RoPE + KV append: q -> bf16 q buffer, k/v -> the agent's cache at `pos`.
-void rope_kv(const float* P, int S, const RowDesc* rows, int R, int nh, int nkv, int hd,
-             const float2* rope, bf16* q, bf16* kpool, bf16* vpool, long long kv_stride,
-             long long layer_off, int max_ctx, cudaStream_t st);
-// o[r][h] = softmax(q k^T / sqrt(hd)) v over keys [0, pos] of the row's agent.
-void attention(const bf16* q, const RowDesc* rows, int R, int nh, int nkv, int hd,
-               const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off,
-               int max_ctx, bf16* o, cudaStream_t st);
-// Fused LM head + greedy statistics over the selected rows: per-block partial
-// (max, sum e^, sum (x-m) e^, argmax); `logits` (optional) receives fp32 rows.
+
+// Fused skinny GEMM  y[r][n] = sum_k A[r][k] W[n][k]  for decode/incremental
+// rows.  A is either bf16 activations or, with `norm`, the fp32 residual rows
+// normalised on the fly (A = bf16(rmsnorm(x) * g), the oracle's rounding
+// point).  Epilogues:
+enum Epi : int { kEpiF32 = 0, kEpiResidual = 1, kEpiSwiGlu = 2, kEpiQkv = 3 };
+struct GemvArgs {
+  const bf16* A = nullptr;   // [R][K] bf16 (when X == nullptr)
+  const float* X = nullptr;  // [R][K] fp32 residual rows (norm prologue)
+  const float* g = nullptr;  // norm gains [K]
+  float eps = 1e-5f;
+  int R = 0, N = 0, K = 0;
+  const bf16* W = nullptr;  // [N][K] device layout
+  int epi = kEpiF32;
+  float* out = nullptr;      // kEpiF32: [R][N]; kEpiResidual: x [R][N] (+=)
+  bf16* out_bf16 = nullptr;  // kEpiSwiGlu: a [R][N/2]; kEpiQkv: q [R][nh*hd]
+  // kEpiQkv: RoPE + KV append
+  const RowDesc* rows = nullptr;
+  const float2* rope = nullptr;
+  bf16* kpool = nullptr;
+  bf16* vpool = nullptr;
+  long long kv_stride = 0, layer_off = 0;
+  int max_ctx = 0, nh = 0, nkv = 0, hd = 0;
+};
+void gemv(const GemvArgs& a, cudaStream_t st);
+
+// o[r][h] = softmax(q k^T / sqrt(hd)) v over keys [0, pos] of the row's agent;
+// keys split across CTAs (kKvSplit keys each), partials combined in split
+// order by the last-arriving CTA.  `ws` >= attention_ws_floats(...) floats,
+// `cnt` >= R*nh ints, zero-initialised once (the kernel leaves them zero).
+constexpr int kKvSplit = 128;
+long long attention_ws_floats(int R, int nh, int hd, int max_ctx);
+void attention(const bf16* q, const RowDesc* rows, int R, int max_pos, int nh, int nkv, int hd,
+               const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx,
+               bf16* o, float* ws, int* cnt, cudaStream_t st);
+
+// LM head over selected rows: logits = bf16(rmsnorm(x[sel[i]]) * g) . W^T,
+// fused greedy statistics; the last CTA merges the per-slice partials and
+// writes token / logprob / entropy to out_*[out_idx[i]].  `logits`
+// (optional) receives the fp32 rows.  cnt: one int, zero-initialised once.
 int lm_head_blocks(int V);
-void lm_head_stats(const bf16* h, int Rl, const bf16* W, int V, int d, LmStat* part,
-                   float* logits, cudaStream_t st);
-// Merge partials and write token / logprob / entropy at out[]; out index per row.
-void lm_merge(const LmStat* part, int Rl, int nblk, const int* out_idx, int* out_tok,
-              float* out_lp, float* out_ent, cudaStream_t st);
+void lm_head(const float* X, const int* sel, int Rl, const float* g, float eps, const bf16* W, int V, int d,
+             LmStat* part, int* cnt, const int* out_idx, int* out_tok, float* out_lp, float* out_ent,
+             float* logits, cudaStream_t st);
 
 // ---- early-exit signals (fp64) ----
 // C = exp(mean(lp[0..n))) with a sequential fp64 sum (metricq.cpp:18-23).
@@ -67,10 +95,8 @@ void ee_confidence(const float* lp, int n, double* c, cudaStream_t st);
 void ee_mock_embed(const int* out_tok, long long base, int n, int h, std::uint64_t seed, double* emb,
                    cudaStream_t st);
 // corr = correlation_from_gram(emb^T emb) (metricq.cpp:32-53), h x h.
-void ee_corr(const double* emb, int n, int h, double eps, double* gram, double* corr,
-             cudaStream_t st);
+void ee_corr(const double* emb, int n, int h, double eps, double* gram, double* corr, cudaStream_t st);
 // sim[j] = frob_cos_sim_corr(corr_new, corrs[j]) for j < m (metricq.cpp:55-64).
-void ee_fcs(const double* corr_new, const double* corrs, int m, int h, double* sim,
-            cudaStream_t st);
+void ee_fcs(const double* corr_new, const double* corrs, int m, int h, double* sim, cudaStream_t st);
 
 }  // namespace moa::k

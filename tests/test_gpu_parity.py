@@ -2,9 +2,13 @@
 
 Tolerances (stated here):
   * weights, mock embeddings, token routing, exit draws: bit-exact;
-  * logits: |gpu - oracle| <= LOGIT_ATOL (fp32 accumulation order differs;
-    bf16 rounding points are identical on both sides);
-  * greedy ids: identical wherever the oracle's top-1 margin > 2*LOGIT_ATOL;
+  * logits: |gpu - oracle| <= LOGIT_ATOL = 0.2 (oracle/parity.py: fp32
+    accumulation order differs, bf16 rounding points are identical; the
+    oracle's own fp64-vs-fp32 spread is ~0.08, tests/test_oracle_sensitivity.py);
+  * greedy ids: teacher-forced, identical wherever the oracle's top-1
+    margin > 2*LOGIT_ATOL; logprob of the GPU's token within 0.05;
+  * orchestration (prompts, schedule, EE q/draw/exit/pruned): bit-exact when
+    the oracle replays the GPU's own completions (record-and-replay);
   * EE quality q: <= 1e-9 vs the oracle replayed on the GPU's own outputs
     (fp64 on both sides); exit decisions identical when |q - draw| > 1e-6.
 """
@@ -19,12 +23,12 @@ from oracle.configs import models_of, run_config
 from oracle.engine import TickEngine
 from oracle.model import CpuModel, init_tensor, make_spec
 from oracle.orchestrator import run_query as oracle_run_query
+from oracle.parity import LOGIT_ATOL, check_agent, teacher_forced
 from paper_2512_18126_b200 import capi
 from paper_2512_18126_b200.configs import C0, C1, C1U, CONFIGS
 
 pytestmark = pytest.mark.gpu
 
-LOGIT_ATOL = 0.05
 
 
 @pytest.fixture(scope="module")
@@ -38,30 +42,43 @@ def torch_cuda():
 def test_weight_init_bit_exact(torch_cuda):
     torch = torch_cuda
     spec = make_spec("leaf", "tiny", seed=1)
-    for name, rows, cols in (("emb", 64, 256), ("L0.wq", 256, 256), ("L3.wd", 256, 1024), ("lm", 128, 256)):
+    from oracle.model import tensor_scale
+    half = spec.head_dim // 2
+    rope_perm = np.array([(r // 64) * 64 + (2 * (r % 64) if r % 64 < half else 2 * (r % 64 - half) + 1)
+                          for r in range(256)])
+    for name, rows, cols, rmap in (("emb", 64, 256, 0), ("L0.wq", 256, 256, 1), ("L3.wd", 256, 1024, 0),
+                                   ("L1.wg", 64, 256, 2), ("L1.wu", 64, 256, 3), ("lm", 128, 256, 0)):
         ref = init_tensor(spec, name, rows, cols)
         base = orng.hash_combine(orng.hash_combine(spec.seed, orng.fnv1a(spec.tag)), orng.fnv1a(name))
-        from oracle.model import tensor_scale
-        dst = torch.empty(rows * cols, dtype=torch.bfloat16, device="cuda")
-        capi.check(capi.lib().moa_k_init_uniform(dst.data_ptr(), rows * cols, base, float(tensor_scale(spec, name)), 0))
+        dev_rows = 2 * rows if rmap in (2, 3) else rows
+        dst = torch.zeros(dev_rows * cols, dtype=torch.bfloat16, device="cuda")
+        capi.check(capi.lib().moa_k_init_uniform(dst.data_ptr(), rows, cols, base, float(tensor_scale(spec, name)),
+                                                 rmap, spec.head_dim, 0))
         torch.cuda.synchronize()
-        got = dst.float().cpu().numpy().reshape(rows, cols)
-        assert np.array_equal(got, ref), name
+        got = dst.float().cpu().numpy().reshape(dev_rows, cols)
+        idx = {0: np.arange(rows), 1: rope_perm[:rows], 2: 2 * np.arange(rows), 3: 2 * np.arange(rows) + 1}[rmap]
+        assert np.array_equal(got[idx], ref), name
 
 
-@pytest.mark.parametrize("R,N,K,S", [(1, 768, 256, 1), (4, 256, 1024, 4), (8, 3072, 2048, 4), (13, 2048, 8192, 8),
-                                     (37, 16384, 2048, 1), (300, 1024, 256, 1)])
-def test_gemm_skinny_vs_torch_fp32(torch_cuda, R, N, K, S):
+@pytest.mark.parametrize("R,N,K", [(1, 768, 256), (4, 256, 1024), (8, 3072, 2048), (13, 2048, 8192),
+                                   (37, 16384, 2048), (300, 1024, 256)])
+def test_gemv_vs_torch_fp32(torch_cuda, R, N, K):
     torch = torch_cuda
     g = torch.Generator(device="cuda").manual_seed(R * 7 + N)
     A = torch.randn(R, K, device="cuda", generator=g).to(torch.bfloat16)
     W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
-    P = torch.zeros(S, R, N, device="cuda")
-    capi.check(capi.lib().moa_k_gemm_skinny(A.data_ptr(), R, W.data_ptr(), N, K, S, P.data_ptr(), 0))
+    out = torch.zeros(R, N, device="cuda")
+    capi.check(capi.lib().moa_k_gemv(A.data_ptr(), 0, R, W.data_ptr(), N, K, out.data_ptr(), 0))
     torch.cuda.synchronize()
     ref = A.float() @ W.float().T
-    got = P.sum(0)
-    assert torch.allclose(got, ref, atol=1e-3 * math.sqrt(K / 256), rtol=1e-4), (got - ref).abs().max()
+    assert torch.allclose(out, ref, atol=1e-3 * math.sqrt(K / 256), rtol=1e-4), (out - ref).abs().max()
+    # rmsnorm prologue: A = bf16(x / rms(x)) rounded exactly where the oracle rounds
+    X = torch.randn(R, K, device="cuda", generator=g) * 3.0
+    capi.check(capi.lib().moa_k_gemv(0, X.data_ptr(), R, W.data_ptr(), N, K, out.data_ptr(), 0))
+    torch.cuda.synchronize()
+    h = (X / torch.sqrt((X * X).mean(-1, keepdim=True) + 1e-5)).to(torch.bfloat16).float()
+    ref = h @ W.float().T
+    assert torch.allclose(out, ref, atol=2e-2, rtol=1e-3), (out - ref).abs().max()
 
 
 def test_mock_embed_bit_exact_on_gpu(golden):
@@ -109,31 +126,18 @@ def test_metricq_kernels_vs_reference(golden):
 
 
 # ---------------------------------------------------------------- engine
-def _oracle_single(prompt, max_new, apc, spec):
-    m = CpuModel(spec, 1024)
-    eng = TickEngine({"m": m}, keep_logits=True)
-    a = (1, 0)
-    eng.add_agent(a, "m")
-    eng.submit_generate(a, prompt, max_new, apc)
-    eng.run()
-    r = eng.reqs[a]
-    return r.out, r.lp, r.ent, [eng.logits[(a, k)] for k in range(max_new)]
+_MODELS = {}
 
 
-def _check_logits(gpu_logits, ora_logits, gpu_tok, ora_tok):
-    worst = 0.0
-    for k, (g, o) in enumerate(zip(gpu_logits, ora_logits)):
-        worst = max(worst, float(np.abs(g - o).max()))
-        top2 = np.sort(o)[-2:]
-        if top2[1] - top2[0] > 2 * LOGIT_ATOL:
-            assert gpu_tok[k] == ora_tok[k], k
-        if gpu_tok[k] != ora_tok[k]:
-            return worst, k  # trajectories diverged legitimately at a near-tie
-    return worst, None
+def _cpu_model(tag, shape, seed):
+    key = (tag, shape, seed)
+    if key not in _MODELS:
+        _MODELS[key] = CpuModel(make_spec(tag, shape, seed=seed), 1024)
+    return _MODELS[key]
 
 
 def test_single_agent_decode_matches_oracle():
-    spec = make_spec("leaf", "tiny", seed=1)
+    model = _cpu_model("leaf", "tiny", 1)
     eng = capi.Engine([capi.model_spec("leaf", "tiny", 1, max_agents=2)], max_ctx=1024, max_out=64, keep_logits=True)
     prompt = orng.synth_tokens(3, "p", 40)
     a = (1, 0)
@@ -146,14 +150,13 @@ def test_single_agent_decode_matches_oracle():
         events += ev
         ticks += 1
     tok, lp, ent = eng.read_output(a, 24)
-    logits = [eng.read_logits(a, k) for k in range(24)]
-    otok, olp, oent, ologits = _oracle_single(prompt, 24, 8, spec)
-    worst, div = _check_logits(logits, ologits, tok, otok)
-    assert worst < LOGIT_ATOL, worst
-    n = 24 if div is None else div
-    assert tok[:n] == otok[:n]
-    assert np.allclose(lp[:n], olp[:n], atol=1e-3)
-    assert np.allclose(ent[:n], oent[:n], atol=2e-3)
+    logits = np.stack([eng.read_logits(a, k) for k in range(24)])
+    ref = teacher_forced(model, prompt, tok)
+    err = float(np.abs(logits - ref).max())
+    assert err < LOGIT_ATOL, err
+    chk = check_agent(model, prompt, tok, lp)
+    assert chk["mismatches"] == [] and chk["lp_ok"], chk
+    assert chk["checked"] >= 12
     chunks = [(e[3], e[4]) for e in events if e[0] == "chunk"]
     assert chunks == [(0, 8), (8, 16), (16, 24)]
     assert ticks == 24  # 1 prefill tick (yields out[0]) + 23 decode ticks
@@ -236,45 +239,51 @@ def _gpu_query(cfg, sample=0):
         eng.close()
 
 
-def _compare_query(cfg, sample=0):
+def _replay(cfg, g, sample):
+    """The oracle orchestration re-run on exactly the GPU's completions."""
+    forced = {tuple(int(x) for x in k.split(":")): (a["output"], a["logprobs"], a["entropy"])
+              for k, a in g["agents"].items()}
+    return oracle_run_query(run_config(cfg), {}, sample, forced=forced)
+
+
+@pytest.mark.parametrize("cfg,sample", [(C0, 0), (C1, 0), (C1, 5), (C1U, 0), (C1U, 3)],
+                         ids=lambda v: v["name"] if isinstance(v, dict) else str(v))
+def test_run_query_replay_and_numerics(cfg, sample):
     g = _gpu_query(cfg, sample)
-    o = oracle_run_query(run_config(cfg), models_of(cfg, 1024), sample)
-    diverged = []
-    for name, oa in o["agents"].items():
-        ga = g["agents"][name]
-        if ga["output"] != oa["output"]:
-            diverged.append(name)
-    return g, o, diverged
-
-
-@pytest.mark.parametrize("cfg", [C0, C1, C1U], ids=lambda c: c["name"])
-def test_run_query_matches_oracle(cfg):
-    g, o, diverged = _compare_query(cfg)
-    # A greedy near-tie may legitimately fork a trajectory; everything
-    # upstream of the fork must agree and forks must be rare.
-    assert len(diverged) <= 1, diverged
-    if diverged:
-        pytest.skip(f"greedy near-tie forked {diverged}; upstream agents matched")
+    o = _replay(cfg, g, sample)
+    # 1. orchestration parity, bit-exact: prompts, schedule, EE decisions
     for name, oa in o["agents"].items():
         ga = g["agents"][name]
         assert ga["prompt"] == oa["prompt"], name
         assert ga["output"] == oa["output"], name
         for k in ("invoked", "pruned", "empty_input", "prompt_tokens", "output_tokens", "prefill_only_calls",
                   "recomputed_tokens", "reclaimed_tokens", "decode_start", "complete"):
-            assert ga[k] == int(oa[k]) if isinstance(oa[k], bool) else ga[k] == oa[k], (name, k)
-        assert np.allclose(ga["logprobs"], oa["logprobs"], atol=1e-3)
+            assert ga[k] == int(oa[k]), (name, k, ga[k], oa[k])
     assert g["ticks"] == o["e2e_ticks"]
     assert g["tokens"] == o["tokens"]
     assert len(g["metricq"]) == len(o["metricq"])
     for ge, oe in zip(g["metricq"], o["metricq"]):
-        assert ge["completed"] == oe["completed"]
-        assert bool(ge["evaluated"]) == oe["evaluated"]
+        assert ge["completed"] == oe["completed"] and bool(ge["evaluated"]) == oe["evaluated"]
+        assert ge["tick"] == oe["tick"]
         if oe["evaluated"]:
-            assert ge["q"] == pytest.approx(oe["q"], abs=1e-5)
+            assert ge["q"] == pytest.approx(oe["q"], rel=1e-9, abs=1e-12)
             assert ge["draw"] == oe["draw"]
-            if abs(oe["q"] - oe["draw"]) > 1e-5:
-                assert bool(ge["exited"]) == oe["exited"]
+            assert bool(ge["exited"]) == oe["exited"]
             assert ge["pruned"] == oe["pruned"]
+            assert ge["sim_row"] == pytest.approx(oe["sim_row"], rel=1e-9, abs=1e-12)
+    # 2. numerics: every agent's greedy stream against teacher-forced oracle logits
+    checked = 0
+    for name, ga in g["agents"].items():
+        if not ga["output"]:
+            continue
+        tag = cfg["assign"][min(int(name[0]) - 1, len(cfg["assign"]) - 1)]
+        tag = tag[int(name.split(":")[1]) % len(tag)]
+        mm = cfg["models"][tag]
+        chk = check_agent(_cpu_model(tag, mm["shape"], mm["seed"]), ga["prompt"], ga["output"], ga["logprobs"])
+        assert chk["mismatches"] == [], (name, chk)
+        assert chk["lp_ok"], (name, chk)
+        checked += chk["checked"]
+    assert checked > 0.5 * g["decoded_tokens"]
 
 
 @pytest.mark.parametrize("sample", [0, 1, 2, 3])
