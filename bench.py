@@ -102,6 +102,25 @@ def peaks():
     return 6650.0, 1590.0, "fallback"
 
 
+def roofline(probes, hbm_gbs, src):
+    """Dominant kernel (largest share of probed time): algorithmic bytes per
+    launch / average launch duration, against the measured HBM copy peak.
+    `traffic` = DRAM bytes per launch from the committed ncu --set full
+    capture (profiles/ncu_traffic.json) when present."""
+    kind, v = max(probes.items(), key=lambda kv: kv[1]["ms"])
+    if v["launches"] == 0:
+        return None
+    achieved = v["bytes"] / (v["ms"] / 1e3) / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get(kind)
+    return {"kernel": kind, "bound": "hbm", "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s",
+            "frac": achieved / hbm_gbs, "traffic": traffic, "peak_source": src,
+            "bytes_per_launch": v["bytes"] / v["launches"], "avg_us": 1e3 * v["ms"] / v["launches"],
+            "share_of_probed_time": v["ms"] / max(1e-12, sum(p["ms"] for p in probes.values()))}
+
+
 def cpu_baseline(cfg, budget_s):
     """The oracle (numpy transformer + reference-semantics orchestration) on
     a bounded sample of the same workload, all host cores."""
@@ -214,10 +233,11 @@ def main():
     if pg:
         pg.barrier()
     torch.cuda.synchronize()
-    dev_ms, toks, per_req, rows, fwd, wbytes = 0.0, 0, [], 0, 0, 0.0
+    dev_ms, toks, per_req, rows, fwd, wbytes, host_ms = 0.0, 0, [], 0, 0, 0.0, 0.0
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             s = one(i)
+            host_ms += s["host_ms"]
             dev_ms += s["e2e_ms"]
             per_req.append(s["e2e_ms"])
             toks += s["tokens"]
@@ -236,6 +256,15 @@ def main():
         e2e_toks += r["tokens"]
         h2d += r["rows"] * 16
         d2h += sum(4 * len(a["prompt"]) + 12 * len(a["output"]) for a in r["agents"].values())
+    # kernel probes: CUDA events around every forward kernel while the same
+    # K requests replay (graphs bypassed during this pass only)
+    eng.probe(True)
+    n_ee_launches = 0
+    for i in range(args.steps):
+        r = one(i, detail=True)
+        n_ee_launches += sum(4 + (e["outputs"] > 1) for e in r["metricq"] if e["evaluated"])
+    probes = eng.probe_stats()
+    eng.probe(False)
     if pg:
         t = torch.tensor([dev_ms, e2e_wall * 1e3, toks, e2e_toks], dtype=torch.float64, device="cuda")
         mx = t.clone()
@@ -260,10 +289,15 @@ def main():
                    "models": {t: m["shape"] for t, m in cfg["models"].items()}, "parallelism": f"replicas{world}"},
         "e2e": {"value": e2e_toks_all / (e2e_ms_max / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps},
-        "gpu_launches": None,
+        "gpu_launches": int(sum(v["launches"] for v in probes.values()) + n_ee_launches),
+        "roofline": roofline(probes, hbm, src),
+        "kernels": {k: {"launches": v["launches"], "ms_per_request": v["ms"] / args.steps,
+                        "avg_us": 1e3 * v["ms"] / max(1, v["launches"]),
+                        "gbs": v["bytes"] / max(1e-12, v["ms"] / 1e3) / 1e9} for k, v in probes.items()},
         "clocks": clk.summary(),
         "peaks": {"hbm_gbs": hbm, "bf16_tflops": tf, "source": src},
         "engine": {"rows_per_request": rows / args.steps, "forwards_per_request": fwd / args.steps,
+                   "host_ms_per_request": host_ms / args.steps,
                    "weight_gb_per_request": wbytes / args.steps / 1e9,
                    "weight_stream_gbs": wbytes / (dev_ms / 1e3) / 1e9},
     }

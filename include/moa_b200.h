@@ -67,6 +67,11 @@ int moa_engine_create(const moa_model_spec* models, int n_models, const moa_engi
 int moa_engine_destroy(moa_engine* eng);
 /* Drops every request; weights and buffers stay resident. */
 int moa_engine_reset(moa_engine* eng);
+/* Kernel probes: CUDA events around every forward kernel (graphs bypassed)
+ * with each launch's algorithmic bytes.  kind: 0 embed, 1 qkv, 2 attention,
+ * 3 o-proj, 4 gate/up, 5 down, 6 lm-head. */
+int moa_engine_probe(moa_engine* eng, int enable);
+int moa_engine_probe_stats(moa_engine* eng, int kind, int* launches, double* ms, double* bytes);
 
 /* ---- SimWorld engine protocol (pdsim.hpp:61-156) ------------------------
  * Agents are (layer, position) = AgentId (agent.hpp:16-37).  Tokens passed
@@ -146,6 +151,7 @@ typedef struct {
   double e2e_ms;       /* device events: first tick -> last completion */
   double wall_ms;      /* host wall clock of the whole call            */
   double weight_bytes; /* weight bytes the forwards had to read        */
+  double host_ms;      /* host time spent inside engine ticks          */
 } moa_run_summary;
 
 typedef struct {

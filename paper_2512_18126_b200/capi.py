@@ -66,7 +66,8 @@ class RunConfigC(C.Structure):
 class RunSummary(C.Structure):
     _fields_ = [("ticks", C.c_int), ("n_agents", C.c_int), ("n_evals", C.c_int), ("forwards", C.c_int),
                 ("tokens", C.c_longlong), ("decoded_tokens", C.c_longlong), ("rows", C.c_longlong),
-                ("e2e_ms", C.c_double), ("wall_ms", C.c_double), ("weight_bytes", C.c_double)]
+                ("e2e_ms", C.c_double), ("wall_ms", C.c_double), ("weight_bytes", C.c_double),
+                ("host_ms", C.c_double)]
 
 
 class AgentRecordC(C.Structure):
@@ -92,6 +93,8 @@ _SIGS = {
     "moa_engine_create": ([_P(ModelSpec), C.c_int, _P(EngineOpts), _P(C.c_void_p)], C.c_int),
     "moa_engine_destroy": ([C.c_void_p], C.c_int),
     "moa_engine_reset": ([C.c_void_p], C.c_int),
+    "moa_engine_probe": ([C.c_void_p, C.c_int], C.c_int),
+    "moa_engine_probe_stats": ([C.c_void_p, C.c_int, _P(C.c_int), _P(C.c_double), _P(C.c_double)], C.c_int),
     "moa_add_agent": ([C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
     "moa_prefill_only": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_int32), C.c_int], C.c_int),
     "moa_generate": ([C.c_void_p, C.c_int, C.c_int, _P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
@@ -241,6 +244,19 @@ class Engine:
 
     def reset(self):
         check(lib().moa_engine_reset(self.h))
+
+    PROBE_KINDS = ("embed", "qkv", "attention", "o_proj", "gate_up", "down", "lm_head")
+
+    def probe(self, enable: bool):
+        check(lib().moa_engine_probe(self.h, int(enable)))
+
+    def probe_stats(self):
+        out = {}
+        for k, name in enumerate(self.PROBE_KINDS):
+            n, ms, b = C.c_int(), C.c_double(), C.c_double()
+            check(lib().moa_engine_probe_stats(self.h, k, C.byref(n), C.byref(ms), C.byref(b)))
+            out[name] = {"launches": n.value, "ms": ms.value, "bytes": b.value}
+        return out
 
     # --- run_query ---
     def run_query(self, cfg: "QueryConfig", sample=0, resolve=True, detail=True):

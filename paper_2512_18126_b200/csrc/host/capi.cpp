@@ -189,6 +189,19 @@ int moa_engine_reset(moa_engine* eng) {
   return guard([&] { E(eng).reset(); });
 }
 
+int moa_engine_probe(moa_engine* eng, int enable) {
+  return guard([&] { E(eng).set_probing(enable != 0); });
+}
+
+int moa_engine_probe_stats(moa_engine* eng, int kind, int* launches, double* ms, double* bytes) {
+  return guard([&] {
+    need(launches, "launches");
+    need(ms, "ms");
+    need(bytes, "bytes");
+    E(eng).probe_stats(kind, launches, ms, bytes);
+  });
+}
+
 int moa_add_agent(moa_engine* eng, int layer, int position, int model) {
   return guard([&] { E(eng).add_agent(moa::AgentId{layer, position}, model); });
 }
@@ -286,6 +299,7 @@ int moa_run_query(moa_engine* eng, const moa_run_config* cfg, int sample, int re
       summary->e2e_ms = r.e2e_ms;
       summary->wall_ms = r.wall_ms;
       summary->weight_bytes = r.weight_bytes;
+      summary->host_ms = r.host_ms;
     }
     if (out) *out = q.release();
   });

@@ -3,6 +3,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 
 namespace moa {
@@ -38,7 +39,7 @@ GpuEngine::GpuEngine(std::vector<ModelSpec> models, std::vector<int> agents_per_
     MOA_CUDA(cudaMalloc(&logits_, sizeof(float) * nout * logits_v_));
     MOA_CUDA(cudaMalloc(&logits_scratch_, sizeof(float) * static_cast<long long>(max_slots_) * logits_v_));
   }
-  ring_bytes_ = sizeof(k::RowDesc) * (opt_.max_rows + max_slots_) + sizeof(int) * 2 * max_slots_;
+  ring_bytes_ = sizeof(k::RowDesc) * (opt_.max_rows + max_slots_) + sizeof(int) * (2 * max_slots_ + 3);
   for (int i = 0; i < kRing; ++i) {
     Staging s;
     MOA_CUDA(cudaMallocHost(&s.host, ring_bytes_));
@@ -207,18 +208,25 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   const std::size_t rb = sizeof(k::RowDesc) * rows.size();
   std::memcpy(s.host, rows.data(), rb);
   const int L = dm.max_logit_rows();
+  int max_pos = 0;
+  long long keys = 0;
+  for (const auto& rd : rows) {
+    max_pos = std::max(max_pos, rd.pos);
+    keys += rd.pos + 1;
+  }
+  // [lsel (L)][lout (L)][meta: R, Rl, max_pos] -- the graph's kernels read meta
   int* sel = reinterpret_cast<int*>(s.host + rb);
   std::memcpy(sel, lsel.data(), sizeof(int) * lsel.size());
   std::memcpy(sel + L, lout.data(), sizeof(int) * lout.size());
+  sel[2 * L] = static_cast<int>(rows.size());
+  sel[2 * L + 1] = static_cast<int>(lsel.size());
+  sel[2 * L + 2] = max_pos;
   MOA_CUDA(cudaMemcpyAsync(dm.buffers().rows, s.host, rb, cudaMemcpyHostToDevice, stream_));
-  if (!lsel.empty())
-    MOA_CUDA(cudaMemcpyAsync(dm.buffers().sel, sel, sizeof(int) * 2 * L, cudaMemcpyHostToDevice, stream_));
+  MOA_CUDA(cudaMemcpyAsync(dm.buffers().sel, sel, sizeof(int) * (2 * L + 3), cudaMemcpyHostToDevice, stream_));
   MOA_CUDA(cudaEventRecord(s.done, stream_));
   float* logits = (opt_.keep_logits && !lsel.empty()) ? logits_scratch_ : nullptr;
-  int max_pos = 0;
-  for (const auto& rd : rows) max_pos = std::max(max_pos, rd.pos);
-  dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), max_pos, out_tok_, out_tok_, out_lp_,
-             out_ent_, logits, stream_);
+  dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), max_pos, keys, out_tok_, out_tok_,
+             out_lp_, out_ent_, logits, stream_);
   if (logits) {  // debug path: scatter each logits row to its (slot, k) home
     const long long V = dm.spec().vocab;
     for (std::size_t i = 0; i < lsel.size(); ++i)
@@ -232,6 +240,12 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
 }
 
 void GpuEngine::step() {
+  const auto host_t0 = std::chrono::steady_clock::now();
+  struct HostTimer {
+    std::chrono::steady_clock::time_point t0;
+    double* acc;
+    ~HostTimer() { *acc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
+  } host_timer{host_t0, &host_ms_};
   enum Kind { Decode, Prefill, Bootstrap, Empty };
   struct Plan {
     Req* r;
@@ -420,6 +434,7 @@ void GpuEngine::reset() {
   rows_total_ = 0;
   weight_bytes_ = 0.0;
   forwards_ = 0;
+  host_ms_ = 0.0;
   for (auto& m : models_) m->reset_bindings();
 }
 
@@ -431,6 +446,30 @@ GpuMetricQ& GpuEngine::ee_evaluator(int i, int hidden, std::uint64_t seed, doubl
     e = std::make_unique<GpuMetricQ>(hidden, seed, tau, diag, std::max(members, 8), std::max(max_tokens, 512), stream_);
   e->reset(seed, tau, diag);
   return *e;
+}
+
+void GpuEngine::set_probing(bool on) {
+  MOA_CUDA(cudaStreamSynchronize(stream_));
+  probing_ = on;
+  probes_.reset();
+  for (auto& m : models_) m->attach_probes(on ? &probes_ : nullptr);
+}
+
+void GpuEngine::probe_stats(int kind, int* count, double* ms, double* bytes) {
+  MOA_CUDA(cudaStreamSynchronize(stream_));
+  int n = 0;
+  double t = 0.0, b = 0.0;
+  for (const auto& r : probes_.recs) {
+    if (r.kind != kind) continue;
+    float e = 0.f;
+    MOA_CUDA(cudaEventElapsedTime(&e, r.a, r.b));
+    ++n;
+    t += e;
+    b += r.bytes;
+  }
+  *count = n;
+  *ms = t;
+  *bytes = b;
 }
 
 void GpuEngine::mark_start() { MOA_CUDA(cudaEventRecord(start_ev_, stream_)); }

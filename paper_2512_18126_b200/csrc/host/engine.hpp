@@ -113,6 +113,9 @@ class GpuEngine {
   const EngineOptions& options() const { return opt_; }
   DeviceModel& model(int m) { return *models_[static_cast<std::size_t>(m)]; }
   int n_models() const { return static_cast<int>(models_.size()); }
+  // Kernel probes (bench roofline): attach to every model; stats after a run.
+  void set_probing(bool on);
+  void probe_stats(int kind, int* count, double* ms, double* bytes);
   // Pooled early-exit evaluator #i (device buffers reused across requests).
   GpuMetricQ& ee_evaluator(int i, int hidden, std::uint64_t seed, double tau, bool diag, int members,
                            int max_tokens);
@@ -123,6 +126,7 @@ class GpuEngine {
   double bytes_moved() const { return weight_bytes_; }
   long long rows_processed() const { return rows_total_; }
   int kernel_forwards() const { return forwards_; }
+  double host_ms() const { return host_ms_; }  // host time spent inside step() (incl. EE syncs)
 
  private:
   struct Job {
@@ -170,6 +174,8 @@ class GpuEngine {
   };
   std::vector<Staging> ring_;
   std::vector<std::unique_ptr<GpuMetricQ>> ee_pool_;
+  KernelProbes probes_;
+  bool probing_ = false;
   std::size_t ring_next_ = 0, ring_bytes_ = 0;
   // timing
   cudaEvent_t start_ev_ = nullptr;
@@ -177,6 +183,7 @@ class GpuEngine {
   double weight_bytes_ = 0.0;
   long long rows_total_ = 0;
   int forwards_ = 0;
+  double host_ms_ = 0.0;
 };
 
 }  // namespace moa

@@ -52,8 +52,9 @@ void dev_alloc(T** p, long long n) {
 }  // namespace
 
 DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int max_rows, int max_logit_rows,
-                         cudaStream_t st)
-    : spec_(spec), max_agents_(max_agents), max_ctx_(max_ctx), max_rows_(max_rows), max_lrows_(max_logit_rows) {
+                         cudaStream_t st, bool use_graphs)
+    : spec_(spec), max_agents_(max_agents), max_ctx_(max_ctx), max_rows_(max_rows), max_lrows_(max_logit_rows),
+      use_graphs_(use_graphs) {
   spec_.validate();
   const ModelSpec& s = spec_;
   const long long D = s.d, hd = s.head_dim, V = s.vocab;
@@ -124,11 +125,12 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   dev_alloc(&lm_cnt_, 1);
   MOA_CUDA(cudaMemsetAsync(lm_cnt_, 0, sizeof(int), st));
   dev_alloc(&buf_.rows, max_rows);
-  dev_alloc(&buf_.sel, 2LL * max_logit_rows);
+  dev_alloc(&buf_.sel, 2LL * max_logit_rows + 3);
   MOA_CUDA(cudaGetLastError());
 }
 
 DeviceModel::~DeviceModel() {
+  for (auto& [key, exec] : graphs_) cudaGraphExecDestroy(exec);
   for (void* ptr : {static_cast<void*>(wbase_), static_cast<void*>(ones_), static_cast<void*>(rope_),
                     static_cast<void*>(kpool_), static_cast<void*>(vpool_), static_cast<void*>(x_),
                     static_cast<void*>(h_), static_cast<void*>(q_), static_cast<void*>(attn_ws_),
@@ -143,15 +145,81 @@ int DeviceModel::bind_agent() {
   return bound_++;
 }
 
-void DeviceModel::forward(int R, int Rl, int max_pos, const int* out_tok_read, int* out_tok, float* out_lp,
-                          float* out_ent, float* logits, cudaStream_t st) {
+cudaEvent_t KernelProbes::event() {
+  if (next == pool.size()) {
+    cudaEvent_t e;
+    MOA_CUDA(cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+  return pool[next++];
+}
+
+void KernelProbes::begin(int kind, double bytes, cudaStream_t st) {
+  Rec r{kind, bytes, event(), event()};
+  MOA_CUDA(cudaEventRecord(r.a, st));
+  recs.push_back(r);
+}
+
+void KernelProbes::end(cudaStream_t st) { MOA_CUDA(cudaEventRecord(recs.back().b, st)); }
+
+KernelProbes::~KernelProbes() {
+  for (auto e : pool) cudaEventDestroy(e);
+}
+
+namespace {
+int pow2_at_least(int v, int lo) {
+  int p = lo;
+  while (p < v) p <<= 1;
+  return p;
+}
+}  // namespace
+
+void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int* out_tok_read, int* out_tok,
+                          float* out_lp, float* out_ent, float* logits, cudaStream_t st) {
   if (R <= 0) return;
   if (R > max_rows_) throw RunError("model " + spec_.tag + ": tick rows exceed workspace");
+  if (Rl > max_lrows_ || Rl > k::kLmMaxRows) throw RunError("model " + spec_.tag + ": logits rows exceed workspace");
   if (max_pos >= max_ctx_) throw RunError("model " + spec_.tag + ": position exceeds max_ctx");
+  // bucket caps: one graph serves every tick whose live counts fit them
+  const int rcap = std::min(pow2_at_least(R, 8), max_rows_);
+  const int nsplit = pow2_at_least((max_pos + k::kKvSplit) / k::kKvSplit, 1);
+  if (!use_graphs_ || probes_) {
+    live_R_ = R;
+    live_Rl_ = Rl;
+    live_keys_ = keys;
+    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st);
+    return;
+  }
+  const auto key = std::make_tuple(rcap, nsplit, Rl > 0 ? 1 : 0, logits ? 1 : 0);
+  auto it = graphs_.find(key);
+  if (it == graphs_.end()) {
+    cudaGraph_t g = nullptr;
+    MOA_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st);
+    MOA_CUDA(cudaStreamEndCapture(st, &g));
+    cudaGraphExec_t exec = nullptr;
+    MOA_CUDA(cudaGraphInstantiate(&exec, g, 0));
+    MOA_CUDA(cudaGraphDestroy(g));
+    it = graphs_.emplace(key, exec).first;
+  }
+  MOA_CUDA(cudaGraphLaunch(it->second, st));
+}
+
+void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_tok_read, int* out_tok,
+                         float* out_lp, float* out_ent, float* logits, cudaStream_t st) {
   const ModelSpec& s = spec_;
   const int D = s.d, hd = s.head_dim, nh = s.n_heads, nkv = s.n_kv_heads;
   const float eps = static_cast<float>(s.norm_eps);
-  k::embed(buf_.rows, R, out_tok_read, emb_, D, x_, st);
+  const int* meta = buf_.sel + 2 * max_lrows_;
+  auto probe_begin = [&](int kind, double bytes) {
+    if (probes_) probes_->begin(kind, bytes, st);
+  };
+  auto probe_end = [&]() {
+    if (probes_) probes_->end(st);
+  };
+  probe_begin(KernelProbes::Embed, 6.0 * live_R_ * D);
+  k::embed(buf_.rows, rcap, meta, out_tok_read, emb_, D, x_, st);
+  probe_end();
   for (int l = 0; l < s.n_layers; ++l) {
     const Layer& L = layers_[static_cast<std::size_t>(l)];
     const long long loff = layer_stride_ * l;
@@ -160,7 +228,8 @@ void DeviceModel::forward(int R, int Rl, int max_pos, const int* out_tok_read, i
     qkv.X = x_;
     qkv.g = ones_;
     qkv.eps = eps;
-    qkv.R = R;
+    qkv.R = rcap;
+    qkv.meta = meta;
     qkv.N = s.qkv_cols();
     qkv.K = D;
     qkv.W = L.wqkv;
@@ -176,46 +245,60 @@ void DeviceModel::forward(int R, int Rl, int max_pos, const int* out_tok_read, i
     qkv.nh = nh;
     qkv.nkv = nkv;
     qkv.hd = hd;
+    probe_begin(KernelProbes::Qkv, 2.0 * qkv.N * qkv.K + 4.0 * live_R_ * D + 2.0 * live_R_ * qkv.N);
     k::gemv(qkv, st);
-    k::attention(q_, buf_.rows, R, max_pos, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_, attn_ws_,
-                 attn_cnt_, st);
+    probe_end();
+    probe_begin(KernelProbes::Attention, 4.0 * live_keys_ * nkv * hd + 4.0 * live_R_ * nh * hd);
+    k::attention(q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_,
+                 attn_ws_, attn_cnt_, st);
+    probe_end();
     // x += o . Wo^T
     k::GemvArgs o;
     o.A = h_;
-    o.R = R;
+    o.R = rcap;
+    o.meta = meta;
     o.N = D;
     o.K = nh * hd;
     o.W = L.wo;
     o.epi = k::kEpiResidual;
     o.out = x_;
+    probe_begin(KernelProbes::OProj, 2.0 * o.N * o.K + 2.0 * live_R_ * o.K + 8.0 * live_R_ * D);
     k::gemv(o, st);
+    probe_end();
     // a = silu(gate) * up over rmsnorm(x)
     k::GemvArgs gu;
     gu.X = x_;
     gu.g = ones_;
     gu.eps = eps;
-    gu.R = R;
+    gu.R = rcap;
+    gu.meta = meta;
     gu.N = 2 * s.ffn;
     gu.K = D;
     gu.W = L.wgu;
     gu.epi = k::kEpiSwiGlu;
     gu.out_bf16 = h_;
+    probe_begin(KernelProbes::GateUp, 2.0 * gu.N * gu.K + 4.0 * live_R_ * D + 2.0 * live_R_ * s.ffn);
     k::gemv(gu, st);
+    probe_end();
     // x += a . Wd^T
     k::GemvArgs dn;
     dn.A = h_;
-    dn.R = R;
+    dn.R = rcap;
+    dn.meta = meta;
     dn.N = D;
     dn.K = s.ffn;
     dn.W = L.wd;
     dn.epi = k::kEpiResidual;
     dn.out = x_;
+    probe_begin(KernelProbes::Down, 2.0 * dn.N * dn.K + 2.0 * live_R_ * dn.K + 8.0 * live_R_ * D);
     k::gemv(dn, st);
+    probe_end();
   }
-  if (Rl > 0) {
-    if (Rl > max_lrows_) throw RunError("model " + spec_.tag + ": logits rows exceed workspace");
-    k::lm_head(x_, buf_.sel, Rl, ones_, eps, lm_, s.vocab, D, part_, lm_cnt_, buf_.sel + max_lrows_, out_tok, out_lp,
-               out_ent, logits, st);
+  if (with_logits) {
+    probe_begin(KernelProbes::LmHead, 2.0 * s.vocab * D + 4.0 * live_Rl_ * D);
+    k::lm_head(x_, buf_.sel, meta, ones_, eps, lm_, s.vocab, D, part_, lm_cnt_, buf_.sel + max_lrows_, out_tok,
+               out_lp, out_ent, logits, st);
+    probe_end();
   }
   MOA_CUDA(cudaGetLastError());
 }

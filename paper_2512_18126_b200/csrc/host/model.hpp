@@ -8,7 +8,9 @@
 
 #include <cuda_runtime.h>
 
+#include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../kernels/kernels.cuh"
@@ -35,13 +37,37 @@ struct ModelSpec {
 
 struct ForwardBuffers {
   k::RowDesc* rows = nullptr;  // [max_rows]
-  int* sel = nullptr;          // [2][max_logit_rows]: logits row index, flat output index
+  int* sel = nullptr;  // [2 * max_logit_rows + 3]: logits row index, flat output index, meta {R, Rl, max_pos}
+};
+
+// Per-kernel CUDA-event probes (bench roofline): when attached, forwards run
+// without graphs and every launch is bracketed by an event pair together with
+// its algorithmic bytes.
+struct KernelProbes {
+  enum Kind { Embed = 0, Qkv, Attention, OProj, GateUp, Down, LmHead, kKinds };
+  struct Rec {
+    int kind;
+    double bytes;
+    cudaEvent_t a, b;
+  };
+  std::vector<cudaEvent_t> pool;
+  std::size_t next = 0;
+  std::vector<Rec> recs;
+  cudaEvent_t event();
+  void begin(int kind, double bytes, cudaStream_t st);
+  void end(cudaStream_t st);
+  void reset() {
+    next = 0;
+    recs.clear();
+  }
+  ~KernelProbes();
 };
 
 class DeviceModel {
  public:
+  void attach_probes(KernelProbes* p) { probes_ = p; }
   DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int max_rows, int max_logit_rows,
-              cudaStream_t st);
+              cudaStream_t st, bool use_graphs = true);
   ~DeviceModel();
   DeviceModel(const DeviceModel&) = delete;
   DeviceModel& operator=(const DeviceModel&) = delete;
@@ -55,16 +81,25 @@ class DeviceModel {
 
   // R rows / Rl logits rows already resident in buffers(); out_* are the
   // engine's flat per-agent output arrays; logits (optional) [Rl][V] fp32.
-  void forward(int R, int Rl, int max_pos, const int* out_tok_read, int* out_tok, float* out_lp, float* out_ent,
+  void forward(int R, int Rl, int max_pos, long long keys, const int* out_tok_read, int* out_tok, float* out_lp,
+               float* out_ent,
                float* logits, cudaStream_t st);
 
   // Algorithmic bytes one forward must move for weights (every tick reads the
   // full weight set once) -- the roofline basis.
   double weight_bytes() const { return spec_.decode_weight_bytes(); }
+  int graphs() const { return static_cast<int>(graphs_.size()); }
 
  private:
+  void launch(int rcap, int nsplit, bool with_logits, const int* out_tok_read, int* out_tok, float* out_lp,
+              float* out_ent, float* logits, cudaStream_t st);
+  std::map<std::tuple<int, int, int, int>, cudaGraphExec_t> graphs_;
   ModelSpec spec_;
   int max_agents_, max_ctx_, max_rows_, max_lrows_;
+  bool use_graphs_ = true;
+  KernelProbes* probes_ = nullptr;
+  int live_R_ = 0, live_Rl_ = 0;
+  long long live_keys_ = 0;  // sum over rows of (pos + 1): attention K/V reads
   int bound_ = 0;
   // weights
   k::bf16* wbase_ = nullptr;

@@ -246,6 +246,7 @@ QueryResult run_query(GpuEngine& eng, const RunConfig& cfg, int sample, bool res
   res.weight_bytes = eng.bytes_moved();
   res.rows = eng.rows_processed();
   res.forwards = eng.kernel_forwards();
+  res.host_ms = eng.host_ms();
   if (resolve) {
     for (const AgentId& a : res.agents) {
       res.prompts[a] = eng.resolve(eng.prompt(a));

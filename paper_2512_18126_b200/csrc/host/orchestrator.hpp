@@ -69,6 +69,7 @@ struct QueryResult {
   double weight_bytes = 0.0;     // sum of per-forward weight reads
   long long rows = 0;
   int forwards = 0;
+  double host_ms = 0.0;  // host time inside engine ticks
 };
 
 // One orchestrated request on `eng` (which must hold every model the config

@@ -169,9 +169,11 @@ __global__ void fill_f32_kernel(float* dst, long long n, float v) {
     dst[i] = v;
 }
 
-__global__ void embed_kernel(const RowDesc* __restrict__ rows, const int* __restrict__ out_tok,
-                             const bf16* __restrict__ emb, int d, float* __restrict__ x) {
+__global__ void embed_kernel(const RowDesc* __restrict__ rows, const int* __restrict__ meta,
+                             const int* __restrict__ out_tok, const bf16* __restrict__ emb, int d,
+                             float* __restrict__ x) {
   const int r = blockIdx.x;
+  if (r >= meta[0]) return;
   int t = rows[r].tok;
   if (t < 0) t = out_tok[-1 - t];
   const bf16* e = emb + static_cast<long long>(t) * d;
@@ -196,7 +198,9 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
   const int cg = warp % WG, kp = warp / WG;
   const int n0 = (blockIdx.x * WG + cg) * kCPW;
   const int r0 = blockIdx.z * kRB;
-  const int rows = min(kRB, a.R - r0);
+  const int live = a.meta ? __ldg(a.meta) : a.R;
+  if (r0 >= live) return;  // uniform across the CTA
+  const int rows = min(kRB, live - r0);
   if constexpr (NORM) {
     if (warp < rows) {
       const float inv = row_inv_rms(a.X + static_cast<long long>(r0 + warp) * a.K, a.K, a.eps, lane);
@@ -287,70 +291,77 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
 // and the last CTA to arrive combines them in split order.
 template <int HD>
 __global__ void __launch_bounds__(128)
-attention_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, int nh, int nkv,
-                 const bf16* __restrict__ kpool, const bf16* __restrict__ vpool, long long kv_stride,
+attention_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, const int* __restrict__ meta, int nh,
+                 int nkv, const bf16* __restrict__ kpool, const bf16* __restrict__ vpool, long long kv_stride,
                  long long layer_off, int max_ctx, bf16* __restrict__ o, float* __restrict__ ws,
                  int* __restrict__ cnt, int nsplit_max) {
   constexpr int E = HD / 32;
+  constexpr int V8 = HD / 8;  // 16-byte vectors per K/V row
   __shared__ float qs[HD];
   __shared__ float wm[4], wl[4], wo[4][HD];
+  __shared__ __align__(16) bf16 vs[4][32][HD];  // V rows of each warp's 32 keys
+  __shared__ float ps[4][32];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.x, h = blockIdx.y, s = blockIdx.z;
+  if (r >= __ldg(meta)) return;
   const RowDesc rd = rows[r];
   const int n = rd.pos + 1;
   const int nsplit = (n + kKvSplit - 1) / kKvSplit;
   if (s >= nsplit) return;
   const int kvh = h / (nh / nkv);
+  const bf16* K = kpool + rd.kv * kv_stride + layer_off + static_cast<long long>(kvh) * max_ctx * HD;
+  const bf16* V = vpool + rd.kv * kv_stride + layer_off + static_cast<long long>(kvh) * max_ctx * HD;
+  const int base = s * kKvSplit + warp * 32;
+  const int j = base + lane;
+  // every lane issues its key's K and V rows at once (2 x HD bf16 in flight)
+  uint4 kk[V8], vv[V8];
+  if (j < n) {
+    const uint4* kp = reinterpret_cast<const uint4*>(K + static_cast<long long>(j) * HD);
+    const uint4* vp = reinterpret_cast<const uint4*>(V + static_cast<long long>(j) * HD);
+#pragma unroll
+    for (int v = 0; v < V8; ++v) kk[v] = __ldg(kp + v);
+#pragma unroll
+    for (int v = 0; v < V8; ++v) vv[v] = __ldg(vp + v);
+  }
   const bf16* qr = q + (static_cast<long long>(r) * nh + h) * HD;
   for (int e = threadIdx.x; e < HD; e += 128) qs[e] = __bfloat162float(qr[e]);
   __syncthreads();
-  const bf16* K = kpool + rd.kv * kv_stride + layer_off + static_cast<long long>(kvh) * max_ctx * HD;
-  const bf16* V = vpool + rd.kv * kv_stride + layer_off + static_cast<long long>(kvh) * max_ctx * HD;
   const float scale = rsqrtf(static_cast<float>(HD));
-  const int base = s * kKvSplit + warp * 32;
-  const int j = base + lane;
   float sc = -INFINITY;
   if (j < n) {
-    const uint4* kp = reinterpret_cast<const uint4*>(K + static_cast<long long>(j) * HD);
-    uint4 kk[HD / 8];
-#pragma unroll
-    for (int v = 0; v < HD / 8; ++v) kk[v] = __ldg(kp + v);
     float d = 0.f;
 #pragma unroll
-    for (int v = 0; v < HD / 8; ++v) {
+    for (int v = 0; v < V8; ++v) {
       float f[8];
       unpack8(kk[v], f);
 #pragma unroll
       for (int t = 0; t < 8; ++t) d = fmaf(qs[v * 8 + t], f[t], d);
     }
     sc = d * scale;
+    uint4* dst = reinterpret_cast<uint4*>(&vs[warp][lane][0]);
+#pragma unroll
+    for (int v = 0; v < V8; ++v) dst[v] = vv[v];
   }
   float m = sc;
 #pragma unroll
   for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, off));
   const float p = (j < n) ? __expf(sc - m) : 0.f;
   const float l = warp_sum(p);
+  ps[warp][lane] = p;
+  __syncwarp();
   float acc[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
   const int cntk = max(0, min(32, n - base));
-#pragma unroll 8
   for (int jj = 0; jj < cntk; ++jj) {
-    const float pj = __shfl_sync(kFull, p, jj);
-    const bf16* vr = V + static_cast<long long>(base + jj) * HD + lane * E;
-    if constexpr (E == 2) {
-      const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
-      acc[0] = fmaf(pj, vf.x, acc[0]);
-      acc[1] = fmaf(pj, vf.y, acc[1]);
-    } else {
-      const uint2 raw = *reinterpret_cast<const uint2*>(vr);
-      const float2 v0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
-      const float2 v1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
-      acc[0] = fmaf(pj, v0.x, acc[0]);
-      acc[1] = fmaf(pj, v0.y, acc[1]);
-      acc[2] = fmaf(pj, v1.x, acc[2]);
-      acc[3] = fmaf(pj, v1.y, acc[3]);
+    const float pj = ps[warp][jj];
+    const bf16* vr = &vs[warp][jj][lane * E];
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+      const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr + e));
+      acc[e] = fmaf(pj, vf.x, acc[e]);
+      acc[e + 1] = fmaf(pj, vf.y, acc[e + 1]);
     }
   }
   if (lane == 0) {
@@ -414,10 +425,10 @@ attention_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, i
 // rows at a time; rows are normalised on the fly.  The last CTA merges all
 // slices per row in slice order and writes token / logprob / entropy.
 constexpr int kLmBlocksPerSm = 4;
-constexpr int kLmMaxRows = 64;
 
 __global__ void __launch_bounds__(kWarps * 32)
-lm_head_kernel(const float* __restrict__ X, const int* __restrict__ sel, int Rl, const float* __restrict__ g,
+lm_head_kernel(const float* __restrict__ X, const int* __restrict__ sel, const int* __restrict__ meta,
+               const float* __restrict__ g,
                float eps, const bf16* __restrict__ W, int V, int d, LmStat* __restrict__ part,
                int* __restrict__ cnt, const int* __restrict__ out_idx, int* __restrict__ out_tok,
                float* __restrict__ out_lp, float* __restrict__ out_ent, float* __restrict__ logits) {
@@ -428,6 +439,8 @@ lm_head_kernel(const float* __restrict__ X, const int* __restrict__ sel, int Rl,
   const int nb = gridDim.x;
   const int per = (V + nb - 1) / nb;
   const int c0 = blockIdx.x * per, c1 = min(V, c0 + per);
+  const int Rl = __ldg(meta + 1);
+  if (Rl <= 0) return;
   for (int r = warp; r < Rl; r += kWarps) {
     const float inv = row_inv_rms(X + static_cast<long long>(sel[r]) * d, d, eps, lane);
     if (lane == 0) inv_s[r] = inv;
@@ -488,14 +501,17 @@ lm_head_kernel(const float* __restrict__ X, const int* __restrict__ sel, int Rl,
   __threadfence();
   for (int r = warp; r < Rl; r += kWarps) {
     LmStat st{-INFINITY, 0.f, 0.f, INT_MAX};
-    const LmStat* pr = part + static_cast<long long>(r) * nb;
-    for (int b = lane; b < nb; b += 32) {
-      LmStat x;
-      x.m = __ldcg(&pr[b].m);
-      x.s = __ldcg(&pr[b].s);
-      x.t = __ldcg(&pr[b].t);
-      x.idx = __ldcg(&pr[b].idx);
-      st = stat_merge(st, x);
+    const float4* pr = reinterpret_cast<const float4*>(part + static_cast<long long>(r) * nb);
+    // issue the lane's partial loads in batches of 8 before merging them
+    for (int b0 = lane; b0 < nb; b0 += 32 * 8) {
+      float4 raw[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int b = b0 + 32 * u;
+        raw[u] = b < nb ? __ldcg(pr + b) : make_float4(-INFINITY, 0.f, 0.f, __int_as_float(INT_MAX));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) st = stat_merge(st, LmStat{raw[u].x, raw[u].y, raw[u].z, __float_as_int(raw[u].w)});
     }
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -544,8 +560,9 @@ void fill_f32(float* dst, long long n, float v, cudaStream_t st) {
   fill_f32_kernel<<<grid_for(n, 256), 256, 0, st>>>(dst, n, v);
 }
 
-void embed(const RowDesc* rows, int R, const int* out_tok, const bf16* emb, int d, float* x, cudaStream_t st) {
-  if (R > 0) embed_kernel<<<R, 128, 0, st>>>(rows, out_tok, emb, d, x);
+void embed(const RowDesc* rows, int R_cap, const int* meta, const int* out_tok, const bf16* emb, int d, float* x,
+           cudaStream_t st) {
+  if (R_cap > 0) embed_kernel<<<R_cap, 128, 0, st>>>(rows, meta, out_tok, emb, d, x);
 }
 
 void gemv(const GemvArgs& a, cudaStream_t st) {
@@ -561,18 +578,18 @@ long long attention_ws_floats(int R, int nh, int hd, int max_ctx) {
   return static_cast<long long>(R) * nh * ns * (2 + hd);
 }
 
-void attention(const bf16* q, const RowDesc* rows, int R, int max_pos, int nh, int nkv, int hd, const bf16* kpool,
-               const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx, bf16* o, float* ws, int* cnt,
-               cudaStream_t st) {
-  if (R <= 0) return;
+void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, const int* meta, int nh, int nkv, int hd,
+               const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx, bf16* o,
+               float* ws, int* cnt, cudaStream_t st) {
+  if (R_cap <= 0) return;
   const int nsplit_max = (max_ctx + kKvSplit - 1) / kKvSplit;
-  dim3 grid(R, nh, (max_pos + kKvSplit) / kKvSplit);
+  dim3 grid(R_cap, nh, nsplit_cap);
   if (hd == 64)
-    attention_kernel<64><<<grid, 128, 0, st>>>(q, rows, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx, o, ws,
-                                               cnt, nsplit_max);
+    attention_kernel<64><<<grid, 128, 0, st>>>(q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx,
+                                               o, ws, cnt, nsplit_max);
   else if (hd == 128)
-    attention_kernel<128><<<grid, 128, 0, st>>>(q, rows, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx, o, ws,
-                                                cnt, nsplit_max);
+    attention_kernel<128><<<grid, 128, 0, st>>>(q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx,
+                                                o, ws, cnt, nsplit_max);
   else
     printf("attention: unsupported head_dim %d\n", hd);
 }
@@ -582,15 +599,10 @@ int lm_head_blocks(int V) {
   return nb < V ? nb : V;
 }
 
-void lm_head(const float* X, const int* sel, int Rl, const float* g, float eps, const bf16* W, int V, int d,
+void lm_head(const float* X, const int* sel, const int* meta, const float* g, float eps, const bf16* W, int V, int d,
              LmStat* part, int* cnt, const int* out_idx, int* out_tok, float* out_lp, float* out_ent, float* logits,
              cudaStream_t st) {
-  if (Rl <= 0) return;
-  if (Rl > kLmMaxRows) {
-    printf("lm_head: %d logits rows exceed %d\n", Rl, kLmMaxRows);
-    return;
-  }
-  lm_head_kernel<<<lm_head_blocks(V), kWarps * 32, 0, st>>>(X, sel, Rl, g, eps, W, V, d, part, cnt, out_idx, out_tok,
+  lm_head_kernel<<<lm_head_blocks(V), kWarps * 32, 0, st>>>(X, sel, meta, g, eps, W, V, d, part, cnt, out_idx, out_tok,
                                                             out_lp, out_ent, logits);
 }
 

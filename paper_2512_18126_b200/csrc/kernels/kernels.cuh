@@ -41,7 +41,11 @@ void init_uniform_rows(bf16* dst, long long rows, long long cols, std::uint64_t 
                        int hd, cudaStream_t st);
 void fill_f32(float* dst, long long n, float v, cudaStream_t st);
 
-void embed(const RowDesc* rows, int R, const int* out_tok, const bf16* emb, int d, float* x,
+// Tick metadata in device memory, read by every kernel of a forward so one
+// captured CUDA graph per (rows, context) bucket serves every tick:
+// meta[0] = live rows R, meta[1] = logits rows Rl, meta[2] = max position.
+// Grids are sized for the bucket caps; CTAs past the live counts exit.
+void embed(const RowDesc* rows, int R_cap, const int* meta, const int* out_tok, const bf16* emb, int d, float* x,
            cudaStream_t st);
 
 // Fused skinny GEMM  y[r][n] = sum_k A[r][k] W[n][k]  for decode/incremental
@@ -54,7 +58,8 @@ struct GemvArgs {
   const float* X = nullptr;  // [R][K] fp32 residual rows (norm prologue)
   const float* g = nullptr;  // norm gains [K]
   float eps = 1e-5f;
-  int R = 0, N = 0, K = 0;
+  int R = 0, N = 0, K = 0;    // R: row cap (grid); live rows = meta ? meta[0] : R
+  const int* meta = nullptr;
   const bf16* W = nullptr;  // [N][K] device layout
   int epi = kEpiF32;
   float* out = nullptr;      // kEpiF32: [R][N]; kEpiResidual: x [R][N] (+=)
@@ -75,8 +80,8 @@ void gemv(const GemvArgs& a, cudaStream_t st);
 // `cnt` >= R*nh ints, zero-initialised once (the kernel leaves them zero).
 constexpr int kKvSplit = 128;
 long long attention_ws_floats(int R, int nh, int hd, int max_ctx);
-void attention(const bf16* q, const RowDesc* rows, int R, int max_pos, int nh, int nkv, int hd,
-               const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx,
+void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, const int* meta, int nh, int nkv,
+               int hd, const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx,
                bf16* o, float* ws, int* cnt, cudaStream_t st);
 
 // LM head over selected rows: logits = bf16(rmsnorm(x[sel[i]]) * g) . W^T,
@@ -84,7 +89,8 @@ void attention(const bf16* q, const RowDesc* rows, int R, int max_pos, int nh, i
 // writes token / logprob / entropy to out_*[out_idx[i]].  `logits`
 // (optional) receives the fp32 rows.  cnt: one int, zero-initialised once.
 int lm_head_blocks(int V);
-void lm_head(const float* X, const int* sel, int Rl, const float* g, float eps, const bf16* W, int V, int d,
+constexpr int kLmMaxRows = 64;
+void lm_head(const float* X, const int* sel, const int* meta, const float* g, float eps, const bf16* W, int V, int d,
              LmStat* part, int* cnt, const int* out_idx, int* out_tok, float* out_lp, float* out_ent,
              float* logits, cudaStream_t st);
 
