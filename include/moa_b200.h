@@ -60,6 +60,7 @@ typedef struct {
   int max_rows;    /* rows per tick (prefill budget)         */
   int device;      /* CUDA device ordinal                    */
   int keep_logits; /* debug: retain fp32 logits per token    */
+  int gemv_only;   /* 1: never use the tcgen05 prefill GEMM  */
 } moa_engine_opts;
 
 int moa_engine_create(const moa_model_spec* models, int n_models, const moa_engine_opts* opts,
@@ -209,6 +210,9 @@ int moa_slotplan_free(moa_slotplan* p);
 /* out[R][N] fp32 = A . W^T with A = bf16 A [R][K], or A = bf16(rmsnorm(X)) for
  * fp32 X (pass 0 for the unused one).  W bf16 [N][K]. */
 int moa_k_gemv(uintptr_t A, uintptr_t X, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
+/* out[M][N] fp32 = A[M][K] . W[N][K]^T on the tcgen05 tensor cores (TMA, TMEM);
+ * N % 128 == 0, K % 64 == 0. */
+int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
 /* Hash-uniform weight init of a logical [rows][cols] tensor into a device row
  * layout (0 identity, 1 RoPE-pair interleave per hd rows, 2 even rows, 3 odd rows). */
 int moa_k_init_uniform(uintptr_t dst, long long rows, long long cols, uint64_t base, float scale, int row_map, int hd,

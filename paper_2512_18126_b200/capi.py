@@ -41,7 +41,7 @@ class ModelSpec(C.Structure):
 
 class EngineOpts(C.Structure):
     _fields_ = [("max_ctx", C.c_int), ("max_out", C.c_int), ("max_rows", C.c_int), ("device", C.c_int),
-                ("keep_logits", C.c_int)]
+                ("keep_logits", C.c_int), ("gemv_only", C.c_int)]
 
 
 class Event(C.Structure):
@@ -123,6 +123,7 @@ _SIGS = {
                             _P(C.c_int)], C.c_int),
     "moa_slotplan_free": ([C.c_void_p], C.c_int),
     "moa_k_gemv": ([C.c_size_t, C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_size_t], C.c_int),
+    "moa_k_gemm_tc": ([C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_size_t], C.c_int),
     "moa_k_init_uniform": ([C.c_size_t, C.c_longlong, C.c_longlong, C.c_uint64, C.c_float, C.c_int, C.c_int,
                             C.c_size_t], C.c_int),
 }
@@ -177,10 +178,11 @@ def model_spec(tag: str, shape: str, seed: int = 0, max_agents: int = 16, vocab:
 class Engine:
     """Owns one moa_engine (one GPU)."""
 
-    def __init__(self, models, max_ctx=1024, max_out=1024, max_rows=16384, device=0, keep_logits=False):
+    def __init__(self, models, max_ctx=1024, max_out=1024, max_rows=16384, device=0, keep_logits=False,
+                 gemv_only=False):
         self.models = list(models)
         arr = (ModelSpec * len(self.models))(*self.models)
-        opts = EngineOpts(max_ctx, max_out, max_rows, device, int(keep_logits))
+        opts = EngineOpts(max_ctx, max_out, max_rows, device, int(keep_logits), int(gemv_only))
         h = C.c_void_p()
         check(lib().moa_engine_create(arr, len(self.models), C.byref(opts), C.byref(h)))
         self.h = h
@@ -349,7 +351,7 @@ class QueryConfig:
             provider_seed=cfg.get("provider_seed", 0))
 
 
-def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16384):
+def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16384, gemv_only=False):
     """Engine holding every model the config names, sized for its agents."""
     from collections import Counter
     counts = Counter()
@@ -366,7 +368,8 @@ def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16
                          cfg["agg_prefix_tokens"] + cfg["suffix_tokens"]
                          + max(t["widths"]) * (out_max + cfg["separator_tokens"]))
         max_ctx = ((prompt_max + out_max + 255) // 256) * 256
-    eng = Engine(specs, max_ctx=max_ctx, max_out=out_max, max_rows=max_rows, device=device, keep_logits=keep_logits)
+    eng = Engine(specs, max_ctx=max_ctx, max_out=out_max, max_rows=max_rows, device=device, keep_logits=keep_logits,
+                 gemv_only=gemv_only)
     return eng, QueryConfig(cfg, {t: i for i, t in enumerate(tags)})
 
 

@@ -174,6 +174,7 @@ int moa_engine_create(const moa_model_spec* models, int n_models, const moa_engi
       o.max_rows = opts->max_rows;
       o.device = opts->device;
       o.keep_logits = opts->keep_logits != 0;
+      o.tensor_cores = opts->gemv_only == 0;
     }
     auto e = std::make_unique<moa_engine>();
     e->eng = std::make_unique<moa::GpuEngine>(specs, caps, o);
@@ -568,6 +569,25 @@ int moa_k_gemv(uintptr_t A, uintptr_t X, int R, uintptr_t W, int N, int K, uintp
       MOA_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
       cudaFree(ones);
     }
+  });
+}
+
+int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream) {
+  return guard([&] {
+    if (!moa::k::gemm_tc_supported(N, K)) throw moa::ValidationError("gemm_tc: needs N % 128 == 0 and K % 64 == 0");
+    if (M <= 0) return;
+    moa::k::TmaMap ma, mw;
+    if (!moa::k::make_tmap_bf16(&ma, reinterpret_cast<const moa::k::bf16*>(A), M, K, 128) ||
+        !moa::k::make_tmap_bf16(&mw, reinterpret_cast<const moa::k::bf16*>(W), N, K, 128))
+      throw moa::DeviceError("gemm_tc: cuTensorMapEncodeTiled failed");
+    moa::k::GemvArgs a;
+    a.R = M;
+    a.N = N;
+    a.K = K;
+    a.epi = moa::k::kEpiF32;
+    a.out = reinterpret_cast<float*>(out);
+    moa::k::gemm_tc(ma, mw, a, reinterpret_cast<cudaStream_t>(stream));
+    MOA_CUDA(cudaGetLastError());
   });
 }
 

@@ -29,6 +29,7 @@ GpuEngine::GpuEngine(std::vector<ModelSpec> models, std::vector<int> agents_per_
     models_.push_back(std::make_unique<DeviceModel>(models[m], cap, opt_.max_ctx, opt_.max_rows + max_slots_,
                                                     max_slots_, stream_));
     logits_v_ = std::max(logits_v_, models[m].vocab);
+    models_.back()->set_tensor_cores(opt_.tensor_cores);
   }
   const long long nout = static_cast<long long>(max_slots_) * opt_.max_out;
   MOA_CUDA(cudaMalloc(&out_tok_, sizeof(int) * nout));

@@ -31,6 +31,7 @@ struct EngineOptions {
   int device = 0;
   bool keep_logits = false;  // debug: keep fp32 logits of every produced token
   bool time_ticks = true;    // record a CUDA event after every tick
+  bool tensor_cores = true;  // tcgen05 GEMMs for ticks with >= 128 rows of a model (else GEMV only)
 };
 
 struct PrefillInterval {

@@ -126,6 +126,20 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   MOA_CUDA(cudaMemsetAsync(lm_cnt_, 0, sizeof(int), st));
   dev_alloc(&buf_.rows, max_rows);
   dev_alloc(&buf_.sel, 2LL * max_logit_rows + 3);
+  dev_alloc(&hn_, static_cast<long long>(max_rows) * D);
+  // TMA descriptors for the tensor-core prefill path (weights: 128-row boxes)
+  tc_ok_ = k::gemm_tc_supported(s.qkv_cols(), D) && k::gemm_tc_supported(D, s.n_heads * s.head_dim) &&
+           k::gemm_tc_supported(2 * s.ffn, D) && k::gemm_tc_supported(D, s.ffn);
+  for (const Layer& L : layers_) {
+    LayerMaps m{};
+    tc_ok_ = tc_ok_ && k::make_tmap_bf16(&m.wqkv, L.wqkv, s.qkv_cols(), D, 128) &&
+             k::make_tmap_bf16(&m.wo, L.wo, D, static_cast<long long>(s.n_heads) * hd, 128) &&
+             k::make_tmap_bf16(&m.wgu, L.wgu, 2LL * s.ffn, D, 128) && k::make_tmap_bf16(&m.wd, L.wd, D, s.ffn, 128);
+    wmaps_.push_back(m);
+  }
+  tc_ok_ = tc_ok_ && k::make_tmap_bf16(&map_hn_, hn_, max_rows, D, 128) &&
+           k::make_tmap_bf16(&map_h_attn_, h_, max_rows, static_cast<long long>(s.n_heads) * hd, 128) &&
+           k::make_tmap_bf16(&map_h_ffn_, h_, max_rows, s.ffn, 128);
   MOA_CUDA(cudaGetLastError());
 }
 
@@ -135,7 +149,7 @@ DeviceModel::~DeviceModel() {
                     static_cast<void*>(kpool_), static_cast<void*>(vpool_), static_cast<void*>(x_),
                     static_cast<void*>(h_), static_cast<void*>(q_), static_cast<void*>(attn_ws_),
                     static_cast<void*>(attn_cnt_), static_cast<void*>(part_), static_cast<void*>(lm_cnt_),
-                    static_cast<void*>(buf_.rows), static_cast<void*>(buf_.sel)})
+                    static_cast<void*>(buf_.rows), static_cast<void*>(buf_.sel), static_cast<void*>(hn_)})
     if (ptr) cudaFree(ptr);
 }
 
@@ -190,7 +204,7 @@ void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int*
     launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st);
     return;
   }
-  const auto key = std::make_tuple(rcap, nsplit, Rl > 0 ? 1 : 0, logits ? 1 : 0);
+  const auto key = std::make_tuple(rcap, nsplit, (Rl > 0 ? 1 : 0) | (use_tc_ ? 2 : 0), logits ? 1 : 0);
   auto it = graphs_.find(key);
   if (it == graphs_.end()) {
     cudaGraph_t g = nullptr;
@@ -211,6 +225,21 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   const int D = s.d, hd = s.head_dim, nh = s.n_heads, nkv = s.n_kv_heads;
   const float eps = static_cast<float>(s.norm_eps);
   const int* meta = buf_.sel + 2 * max_lrows_;
+  // tensor-core path for row buckets >= kTcMinRows (prefill-heavy ticks)
+  const bool tc = use_tc_ && tc_ok_ && rcap >= k::kTcMinRows;
+  auto run_gemm = [&](k::GemvArgs& g, const k::TmaMap* map_a, const k::TmaMap& map_w) {
+    if (!tc) {
+      k::gemv(g, st);
+      return;
+    }
+    if (g.X) {  // materialise bf16(rmsnorm(x)) once, then TMA-load it
+      k::rmsnorm_rows(g.X, rcap, meta, g.K, g.g, g.eps, hn_, st);
+      g.X = nullptr;
+      g.A = hn_;
+      map_a = &map_hn_;
+    }
+    k::gemm_tc(*map_a, map_w, g, st);
+  };
   auto probe_begin = [&](int kind, double bytes) {
     if (probes_) probes_->begin(kind, bytes, st);
   };
@@ -246,7 +275,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     qkv.nkv = nkv;
     qkv.hd = hd;
     probe_begin(KernelProbes::Qkv, 2.0 * qkv.N * qkv.K + 4.0 * live_R_ * D + 2.0 * live_R_ * qkv.N);
-    k::gemv(qkv, st);
+    run_gemm(qkv, nullptr, wmaps_[static_cast<std::size_t>(l)].wqkv);
     probe_end();
     probe_begin(KernelProbes::Attention, 4.0 * live_keys_ * nkv * hd + 4.0 * live_R_ * nh * hd);
     k::attention(q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_,
@@ -263,7 +292,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     o.epi = k::kEpiResidual;
     o.out = x_;
     probe_begin(KernelProbes::OProj, 2.0 * o.N * o.K + 2.0 * live_R_ * o.K + 8.0 * live_R_ * D);
-    k::gemv(o, st);
+    run_gemm(o, &map_h_attn_, wmaps_[static_cast<std::size_t>(l)].wo);
     probe_end();
     // a = silu(gate) * up over rmsnorm(x)
     k::GemvArgs gu;
@@ -278,7 +307,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     gu.epi = k::kEpiSwiGlu;
     gu.out_bf16 = h_;
     probe_begin(KernelProbes::GateUp, 2.0 * gu.N * gu.K + 4.0 * live_R_ * D + 2.0 * live_R_ * s.ffn);
-    k::gemv(gu, st);
+    run_gemm(gu, nullptr, wmaps_[static_cast<std::size_t>(l)].wgu);
     probe_end();
     // x += a . Wd^T
     k::GemvArgs dn;
@@ -291,7 +320,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     dn.epi = k::kEpiResidual;
     dn.out = x_;
     probe_begin(KernelProbes::Down, 2.0 * dn.N * dn.K + 2.0 * live_R_ * dn.K + 8.0 * live_R_ * D);
-    k::gemv(dn, st);
+    run_gemm(dn, &map_h_ffn_, wmaps_[static_cast<std::size_t>(l)].wd);
     probe_end();
   }
   if (with_logits) {

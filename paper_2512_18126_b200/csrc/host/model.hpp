@@ -66,6 +66,8 @@ struct KernelProbes {
 class DeviceModel {
  public:
   void attach_probes(KernelProbes* p) { probes_ = p; }
+  void set_tensor_cores(bool on) { use_tc_ = on; }
+  bool tensor_cores_ready() const { return tc_ok_; }
   DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int max_rows, int max_logit_rows,
               cudaStream_t st, bool use_graphs = true);
   ~DeviceModel();
@@ -97,6 +99,14 @@ class DeviceModel {
   ModelSpec spec_;
   int max_agents_, max_ctx_, max_rows_, max_lrows_;
   bool use_graphs_ = true;
+  bool use_tc_ = true;  // tensor-core path for ticks with >= kTcMinRows rows
+  bool tc_ok_ = false;
+  struct LayerMaps {
+    k::TmaMap wqkv, wo, wgu, wd;
+  };
+  std::vector<LayerMaps> wmaps_;
+  k::TmaMap map_hn_, map_h_attn_, map_h_ffn_;  // A operands
+  k::bf16* hn_ = nullptr;                      // normalised rows for the tensor-core path
   KernelProbes* probes_ = nullptr;
   int live_R_ = 0, live_Rl_ = 0;
   long long live_keys_ = 0;  // sum over rows of (pos + 1): attention K/V reads

@@ -1,0 +1,314 @@
+// Prefill GEMM on the 5th-generation tensor cores (sm_100a):
+//   Y[M][N] = A[M][K] . W[N][K]^T, bf16 operands, fp32 accumulation in TMEM.
+//
+// One CTA per 128 x 128 output tile, 4 warps:
+//   warp 0 / lane 0  TMA producer: A and W k-tiles (64 x 128, SWIZZLE_128B)
+//                    into a 4-stage shared-memory ring, mbarrier complete_tx;
+//   warp 1 / lane 0  MMA issuer: tcgen05.mma.cta_group::1.kind::f16
+//                    (M=128, N=128, K=16) x 4 per k-tile, tcgen05.commit
+//                    frees the stage;
+//   all 4 warps      epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
+//                    32w..32w+31 = rows), then the same epilogues as the GEMV
+//                    path (RoPE + KV append, residual add, SwiGLU, fp32 store).
+// With N along TMEM columns each thread holds consecutive columns of its row,
+// so RoPE pairs and gate/up pairs (adjacent device columns) sit in one thread.
+#include <cuda.h>
+
+#include <cstdio>
+
+#include "kernels.cuh"
+
+namespace moa::k {
+
+namespace {
+
+constexpr int kBM = 128, kBN = 128, kBK = 64, kStages = 4;
+constexpr int kTileA = kBM * kBK * 2;  // 16 KB
+constexpr int kTileB = kBN * kBK * 2;  // 16 KB
+constexpr int kSmem = kStages * (kTileA + kTileB) + 1024 /*align*/ + 256 /*barriers*/;
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+// K-major, SWIZZLE_128B shared-memory matrix descriptor: 8-row groups of
+// 128-byte rows, SBO = 1024 B, LBO unused (1), version 1 (sm100), layout 2.
+__device__ __forceinline__ std::uint64_t umma_desc(std::uint32_t saddr) {
+  std::uint64_t d = 0;
+  d |= static_cast<std::uint64_t>((saddr & 0x3FFFF) >> 4);
+  d |= static_cast<std::uint64_t>(1) << 16;
+  d |= static_cast<std::uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<std::uint64_t>(1) << 46;
+  d |= static_cast<std::uint64_t>(2) << 61;
+  return d;
+}
+
+// kind::f16 instruction descriptor: F32 accumulate, BF16 A/B, K-major both.
+constexpr std::uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<std::uint32_t>(kBN >> 3) << 17) |
+                                 (static_cast<std::uint32_t>(kBM >> 4) << 24);
+
+__device__ __forceinline__ void umma_f16(std::uint32_t tmem_d, std::uint64_t da, std::uint64_t db, std::uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(std::uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, float (&v)[16]) {
+  std::uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__global__ void __launch_bounds__(128, 1)
+gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_w, const GemvArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  unsigned char* sa = smem;
+  unsigned char* sb = smem + kStages * kTileA;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sb + kStages * kTileB);
+  std::uint64_t* empty = full + kStages;
+  std::uint64_t* done = empty + kStages;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * kBN;
+  const int live = a.meta ? __ldg(a.meta) : a.R;
+  if (m0 >= live) return;  // uniform: the whole tile is past the live rows
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(kBN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const std::uint32_t tmem = *tmem_slot;
+  const int kt_n = a.K / kBK;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    for (int kt = 0; kt < kt_n; ++kt) {
+      const int s = kt % kStages;
+      if (kt >= kStages) mbar_wait(&empty[s], ((kt / kStages) - 1) & 1);
+      mbar_expect_tx(&full[s], kTileA + kTileB);
+      tma_load_2d(sa + s * kTileA, &map_a, &full[s], kt * kBK, m0);
+      tma_load_2d(sb + s * kTileB, &map_w, &full[s], kt * kBK, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer ----
+    for (int kt = 0; kt < kt_n; ++kt) {
+      const int s = kt % kStages;
+      mbar_wait(&full[s], (kt / kStages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const std::uint32_t a0 = smem_u32(sa + s * kTileA), b0 = smem_u32(sb + s * kTileB);
+#pragma unroll
+      for (int k = 0; k < kBK / 16; ++k)  // K advance inside the 128-byte swizzle atom: +32 bytes
+        umma_f16(tmem, umma_desc(a0 + k * 32), umma_desc(b0 + k * 32), (kt | k) ? 1u : 0u);
+      umma_commit(&empty[s]);
+    }
+    umma_commit(done);
+  }
+  __syncwarp();
+  mbar_wait(done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  // ---- epilogue: thread = row m0 + 32*warp + lane; 16 columns per tcgen05.ld ----
+  const int row = m0 + warp * 32 + lane;
+  const bool row_ok = row < live;
+  const std::uint32_t lane_base = static_cast<std::uint32_t>(warp * 32) << 16;
+  RowDesc rd{};
+  if (row_ok && a.epi == kEpiQkv) rd = a.rows[row];
+  for (int c0 = 0; c0 < kBN; c0 += 16) {
+    float v[16];
+    tmem_ld16(tmem + lane_base + static_cast<std::uint32_t>(c0), v);
+    if (!row_ok) continue;
+    const int nb = n0 + c0;
+    if (nb >= a.N) break;
+    switch (a.epi) {
+      case kEpiF32: {
+        float4* o = reinterpret_cast<float4*>(a.out + static_cast<long long>(row) * a.N + nb);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        break;
+      }
+      case kEpiResidual: {
+        float4* o = reinterpret_cast<float4*>(a.out + static_cast<long long>(row) * a.N + nb);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float4 x = o[i];
+          x.x += v[4 * i];
+          x.y += v[4 * i + 1];
+          x.z += v[4 * i + 2];
+          x.w += v[4 * i + 3];
+          o[i] = x;
+        }
+        break;
+      }
+      case kEpiSwiGlu: {
+        bf16* o = a.out_bf16 + static_cast<long long>(row) * (a.N / 2) + nb / 2;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float g = v[2 * i], u = v[2 * i + 1];
+          o[i] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
+        }
+        break;
+      }
+      case kEpiQkv: {
+        const int hd = a.hd, half = hd / 2;
+        const int qk_cols = (a.nh + a.nkv) * hd;
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const int n = nb + i;
+          if (n < qk_cols) {
+            const int head = n / hd, e = (n % hd) / 2;
+            const float2 cs = a.rope[static_cast<long long>(rd.pos) * half + e];
+            const float x0 = v[i], x1 = v[i + 1];
+            const float y0 = __fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y));
+            const float y1 = __fadd_rn(__fmul_rn(x1, cs.x), __fmul_rn(x0, cs.y));
+            bf16* dst = head < a.nh ? a.out_bf16 + (static_cast<long long>(row) * a.nh + head) * hd
+                                    : a.kpool + rd.kv * a.kv_stride + a.layer_off +
+                                          (static_cast<long long>(head - a.nh) * a.max_ctx + rd.pos) * hd;
+            dst[e] = __float2bfloat16_rn(y0);
+            dst[e + half] = __float2bfloat16_rn(y1);
+          } else {
+            const int vc = n - qk_cols, kh = vc / hd, e = vc % hd;
+            bf16* dst = a.vpool + rd.kv * a.kv_stride + a.layer_off +
+                        (static_cast<long long>(kh) * a.max_ctx + rd.pos) * hd + e;
+            dst[0] = __float2bfloat16_rn(v[i]);
+            dst[1] = __float2bfloat16_rn(v[i + 1]);
+          }
+        }
+        break;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kBN));
+}
+
+__global__ void rmsnorm_rows_kernel(const float* __restrict__ x, const int* __restrict__ meta, int K,
+                                    const float* __restrict__ g, float eps, bf16* __restrict__ h) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (r >= __ldg(meta)) return;
+  const float* xr = x + static_cast<long long>(r) * K;
+  float ss = 0.f;
+  for (int k = lane * 4; k < K; k += 128) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(xr + k));
+    ss = fmaf(v.x, v.x, ss);
+    ss = fmaf(v.y, v.y, ss);
+    ss = fmaf(v.z, v.z, ss);
+    ss = fmaf(v.w, v.w, ss);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float inv = 1.0f / sqrtf(ss / static_cast<float>(K) + eps);  // == row_inv_rms (forward.cu)
+  for (int k = lane; k < K; k += 32)
+    h[static_cast<long long>(r) * K + k] = __float2bfloat16_rn(xr[k] * inv * g[k]);
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+bool make_tmap_bf16(TmaMap* out, const bf16* base, long long rows, long long cols, int box_rows) {
+  static_assert(sizeof(TmaMap) == sizeof(CUtensorMap), "TmaMap must mirror CUtensorMap");
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(base),
+                        dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool gemm_tc_supported(int N, int K) { return N % kBN == 0 && K % kBK == 0; }
+
+void gemm_tc(const TmaMap& map_a, const TmaMap& map_w, const GemvArgs& a, cudaStream_t st) {
+  if (a.R <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    attr = true;
+  }
+  dim3 grid(a.N / kBN, (a.R + kBM - 1) / kBM);
+  gemm_tc_kernel<<<grid, 128, kSmem, st>>>(*reinterpret_cast<const CUtensorMap*>(&map_a),
+                                           *reinterpret_cast<const CUtensorMap*>(&map_w), a);
+}
+
+void rmsnorm_rows(const float* x, int R_cap, const int* meta, int K, const float* g, float eps, bf16* h,
+                  cudaStream_t st) {
+  if (R_cap > 0) rmsnorm_rows_kernel<<<(R_cap + 7) / 8, 256, 0, st>>>(x, meta, K, g, eps, h);
+}
+
+}  // namespace moa::k

@@ -74,6 +74,21 @@ struct GemvArgs {
 };
 void gemv(const GemvArgs& a, cudaStream_t st);
 
+// ---- tensor-core prefill GEMM (gemm_tc.cu): tcgen05 + TMEM + TMA ----
+// Opaque mirror of CUtensorMap (2-D bf16, K-major, SWIZZLE_128B, box 64 x rows).
+struct alignas(64) TmaMap {
+  unsigned char raw[128];
+};
+bool make_tmap_bf16(TmaMap* out, const bf16* base, long long rows, long long cols, int box_rows);
+bool gemm_tc_supported(int N, int K);
+// Same epilogues as gemv; A comes from map_a (bf16 rows, already normalised
+// where the GEMV path would normalise on the fly).
+void gemm_tc(const TmaMap& map_a, const TmaMap& map_w, const GemvArgs& a, cudaStream_t st);
+// h[r] = bf16(rmsnorm(x[r]) * g) for the live rows (same rounding as the gemv prologue).
+void rmsnorm_rows(const float* x, int R_cap, const int* meta, int K, const float* g, float eps, bf16* h,
+                  cudaStream_t st);
+constexpr int kTcMinRows = 128;  // ticks with at least this many rows of a model use the tensor cores
+
 // o[r][h] = softmax(q k^T / sqrt(hd)) v over keys [0, pos] of the row's agent;
 // keys split across CTAs (kKvSplit keys each), partials combined in split
 // order by the last-arriving CTA.  `ws` >= attention_ws_floats(...) floats,
