@@ -567,6 +567,10 @@ void embed(const RowDesc* rows, int R_cap, const int* meta, const int* out_tok, 
 
 void gemv(const GemvArgs& a, cudaStream_t st) {
   if (a.R <= 0) return;
+  if (gemv_stream_supported(a)) {
+    gemv_stream(a, st);
+    return;
+  }
   if (a.X)
     gemv_launch<true>(a, st);
   else

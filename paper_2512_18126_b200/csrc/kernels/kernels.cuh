@@ -72,7 +72,10 @@ struct GemvArgs {
   long long kv_stride = 0, layer_off = 0;
   int max_ctx = 0, nh = 0, nkv = 0, hd = 0;
 };
-void gemv(const GemvArgs& a, cudaStream_t st);
+void gemv(const GemvArgs& a, cudaStream_t st);  // dispatches to gemv_stream for large matrices
+// HBM-streaming variant (gemv_stream.cu): persistent CTAs, cp.async.bulk ring.
+bool gemv_stream_supported(const GemvArgs& a);
+void gemv_stream(const GemvArgs& a, cudaStream_t st);
 
 // ---- tensor-core prefill GEMM (gemm_tc.cu): tcgen05 + TMEM + TMA ----
 // Opaque mirror of CUtensorMap (2-D bf16, K-major, SWIZZLE_128B, box 64 x rows).

@@ -61,7 +61,9 @@ def test_weight_init_bit_exact(torch_cuda):
 
 
 @pytest.mark.parametrize("R,N,K", [(1, 768, 256), (4, 256, 1024), (8, 3072, 2048), (13, 2048, 8192),
-                                   (37, 16384, 2048), (300, 1024, 256)])
+                                   (37, 16384, 2048), (300, 1024, 256),
+                                   # HBM-streaming path (R <= 8, >= 4M weights): staged / unstaged A, K > 2048
+                                   (1, 16384, 2048), (3, 2056, 2048), (8, 2048, 8192), (2, 4096, 14336)])
 def test_gemv_vs_torch_fp32(torch_cuda, R, N, K):
     torch = torch_cuda
     g = torch.Generator(device="cuda").manual_seed(R * 7 + N)
