@@ -213,6 +213,9 @@ int moa_k_gemv(uintptr_t A, uintptr_t X, int R, uintptr_t W, int N, int K, uintp
 /* out[M][N] fp32 = A[M][K] . W[N][K]^T on the tcgen05 tensor cores (TMA, TMEM);
  * N % 128 == 0, K % 64 == 0. */
 int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
+/* Decode GEMV on the tensor cores (swap-AB, split-K): out[R][N] fp32 =
+ * A[R][K] . W[N][K]^T for R <= 16; A must have >= 16 allocated rows. */
+int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
 /* Hash-uniform weight init of a logical [rows][cols] tensor into a device row
  * layout (0 identity, 1 RoPE-pair interleave per hd rows, 2 even rows, 3 odd rows). */
 int moa_k_init_uniform(uintptr_t dst, long long rows, long long cols, uint64_t base, float scale, int row_map, int hd,

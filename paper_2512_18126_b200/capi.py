@@ -124,6 +124,7 @@ _SIGS = {
     "moa_slotplan_free": ([C.c_void_p], C.c_int),
     "moa_k_gemv": ([C.c_size_t, C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_size_t], C.c_int),
     "moa_k_gemm_tc": ([C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_size_t], C.c_int),
+    "moa_k_gemv_tc": ([C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_size_t], C.c_int),
     "moa_k_init_uniform": ([C.c_size_t, C.c_longlong, C.c_longlong, C.c_uint64, C.c_float, C.c_int, C.c_int,
                             C.c_size_t], C.c_int),
 }

@@ -591,6 +591,41 @@ int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, 
   });
 }
 
+int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream) {
+  return guard([&] {
+    moa::k::GemvArgs a;
+    a.R = R;
+    a.N = N;
+    a.K = K;
+    a.epi = moa::k::kEpiF32;
+    a.out = reinterpret_cast<float*>(out);
+    if (R <= 0 || R > moa::k::kGemvTcRows || K % 64 || N % 2)
+      throw moa::ValidationError("gemv_tc: needs 1 <= R <= 16, K % 64 == 0, even N");
+    moa::k::TmaMap mw, mx;
+    if (!moa::k::make_tmap_bf16(&mw, reinterpret_cast<const moa::k::bf16*>(W), N, K, 128) ||
+        !moa::k::make_tmap_bf16(&mx, reinterpret_cast<const moa::k::bf16*>(A), moa::k::kGemvTcRows, K,
+                                moa::k::kGemvTcRows))
+      throw moa::DeviceError("gemv_tc: cuTensorMapEncodeTiled failed");
+    static float* ws = nullptr;
+    static int* cnt = nullptr;
+    static long long ws_cap = 0, cnt_cap = 0;
+    const long long need = moa::k::gemv_tc_ws_floats(N, K), tiles = (N + 127) / 128;
+    if (need > ws_cap) {
+      if (ws) cudaFree(ws);
+      MOA_CUDA(cudaMalloc(&ws, sizeof(float) * need));
+      ws_cap = need;
+    }
+    if (tiles > cnt_cap) {
+      if (cnt) cudaFree(cnt);
+      MOA_CUDA(cudaMalloc(&cnt, sizeof(int) * tiles));
+      MOA_CUDA(cudaMemset(cnt, 0, sizeof(int) * tiles));
+      cnt_cap = tiles;
+    }
+    moa::k::gemv_tc(mw, mx, a, ws, cnt, reinterpret_cast<cudaStream_t>(stream));
+    MOA_CUDA(cudaGetLastError());
+  });
+}
+
 int moa_k_init_uniform(uintptr_t dst, long long rows, long long cols, uint64_t base, float scale, int row_map, int hd,
                        uintptr_t stream) {
   return guard([&] {

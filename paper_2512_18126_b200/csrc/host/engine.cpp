@@ -4,6 +4,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 namespace moa {
@@ -205,7 +207,11 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   DeviceModel& dm = *models_[static_cast<std::size_t>(m)];
   Staging& s = ring_[ring_next_];
   ring_next_ = (ring_next_ + 1) % ring_.size();
-  MOA_CUDA(cudaEventSynchronize(s.done));  // the copy that last used this slot has consumed it
+  {
+    const auto t_wait = std::chrono::steady_clock::now();
+    MOA_CUDA(cudaEventSynchronize(s.done));  // the copy that last used this slot has consumed it
+    host_wait_ms_ += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wait).count();
+  }
   const std::size_t rb = sizeof(k::RowDesc) * rows.size();
   std::memcpy(s.host, rows.data(), rb);
   const int L = dm.max_logit_rows();
@@ -305,7 +311,11 @@ void GpuEngine::step() {
     }
   }
   for (std::size_t m = 0; m < nm; ++m)
-    if (!rows[m].empty()) upload_and_forward(static_cast<int>(m), rows[m], lsel[m], lout[m]);
+    if (!rows[m].empty()) {
+      const auto t_api = std::chrono::steady_clock::now();
+      upload_and_forward(static_cast<int>(m), rows[m], lsel[m], lout[m]);
+      host_api_ms_ += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_api).count();
+    }
   if (opt_.time_ticks) {
     if (static_cast<int>(tick_ev_.size()) <= tick_) {
       cudaEvent_t e;
@@ -390,6 +400,9 @@ void GpuEngine::run(int max_ticks) {
     step();
     if (tick_ > max_ticks) throw RunError("engine: tick limit exceeded");
   }
+  if (std::getenv("MOA_HOST_PROFILE"))
+    std::fprintf(stderr, "[moa] ticks %d host %.3f ms (api %.3f ms, ring wait %.3f ms, forwards %d)\n", tick_,
+                 host_ms_, host_api_ms_, host_wait_ms_, forwards_);
 }
 
 TokenSeq GpuEngine::resolve(const TokenSeq& seq) {
@@ -435,7 +448,7 @@ void GpuEngine::reset() {
   rows_total_ = 0;
   weight_bytes_ = 0.0;
   forwards_ = 0;
-  host_ms_ = 0.0;
+  host_ms_ = host_api_ms_ = host_wait_ms_ = 0.0;
   for (auto& m : models_) m->reset_bindings();
 }
 

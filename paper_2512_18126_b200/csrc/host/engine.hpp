@@ -128,6 +128,8 @@ class GpuEngine {
   long long rows_processed() const { return rows_total_; }
   int kernel_forwards() const { return forwards_; }
   double host_ms() const { return host_ms_; }  // host time spent inside step() (incl. EE syncs)
+  double host_api_ms() const { return host_api_ms_; }    // of which: uploads + graph launches
+  double host_wait_ms() const { return host_wait_ms_; }  // of which: blocked on the staging ring (GPU behind)
 
  private:
   struct Job {
@@ -184,7 +186,7 @@ class GpuEngine {
   double weight_bytes_ = 0.0;
   long long rows_total_ = 0;
   int forwards_ = 0;
-  double host_ms_ = 0.0;
+  double host_ms_ = 0.0, host_api_ms_ = 0.0, host_wait_ms_ = 0.0;
 };
 
 }  // namespace moa

@@ -137,9 +137,19 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
              k::make_tmap_bf16(&m.wgu, L.wgu, 2LL * s.ffn, D, 128) && k::make_tmap_bf16(&m.wd, L.wd, D, s.ffn, 128);
     wmaps_.push_back(m);
   }
-  tc_ok_ = tc_ok_ && k::make_tmap_bf16(&map_hn_, hn_, max_rows, D, 128) &&
+  tc_ok_ = tc_ok_ && k::make_tmap_bf16(&wmap_lm_, lm_, V, D, 128) && k::make_tmap_bf16(&map_hn_, hn_, max_rows, D, 128) &&
            k::make_tmap_bf16(&map_h_attn_, h_, max_rows, static_cast<long long>(s.n_heads) * hd, 128) &&
-           k::make_tmap_bf16(&map_h_ffn_, h_, max_rows, s.ffn, 128);
+           k::make_tmap_bf16(&map_h_ffn_, h_, max_rows, s.ffn, 128) &&
+           k::make_tmap_bf16(&map_hn16_, hn_, max_rows, D, k::kGemvTcRows) &&
+           k::make_tmap_bf16(&map_h_attn16_, h_, max_rows, static_cast<long long>(s.n_heads) * hd, k::kGemvTcRows) &&
+           k::make_tmap_bf16(&map_h_ffn16_, h_, max_rows, s.ffn, k::kGemvTcRows);
+  long long ws = 0;
+  for (auto [n, kk] : {std::pair<int, int>{s.qkv_cols(), s.d}, {s.d, s.n_heads * s.head_dim}, {2 * s.ffn, s.d},
+                       {s.d, s.ffn}})
+    ws = std::max(ws, k::gemv_tc_ws_floats(n, kk));
+  dev_alloc(&gv_ws_, ws);
+  dev_alloc(&gv_cnt_, (std::max({s.qkv_cols(), 2 * s.ffn, s.d}) + 127) / 128);
+  MOA_CUDA(cudaMemsetAsync(gv_cnt_, 0, sizeof(int) * ((std::max({s.qkv_cols(), 2 * s.ffn, s.d}) + 127) / 128), st));
   MOA_CUDA(cudaGetLastError());
 }
 
@@ -149,7 +159,8 @@ DeviceModel::~DeviceModel() {
                     static_cast<void*>(kpool_), static_cast<void*>(vpool_), static_cast<void*>(x_),
                     static_cast<void*>(h_), static_cast<void*>(q_), static_cast<void*>(attn_ws_),
                     static_cast<void*>(attn_cnt_), static_cast<void*>(part_), static_cast<void*>(lm_cnt_),
-                    static_cast<void*>(buf_.rows), static_cast<void*>(buf_.sel), static_cast<void*>(hn_)})
+                    static_cast<void*>(buf_.rows), static_cast<void*>(buf_.sel), static_cast<void*>(hn_),
+                    static_cast<void*>(gv_ws_), static_cast<void*>(gv_cnt_)})
     if (ptr) cudaFree(ptr);
 }
 
@@ -196,7 +207,8 @@ void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int*
   if (max_pos >= max_ctx_) throw RunError("model " + spec_.tag + ": position exceeds max_ctx");
   // bucket caps: one graph serves every tick whose live counts fit them
   const int rcap = std::min(pow2_at_least(R, 8), max_rows_);
-  const int nsplit = pow2_at_least((max_pos + k::kKvSplit) / k::kKvSplit, 1);
+  const int ks = k::kv_split(spec_.head_dim);
+  const int nsplit = pow2_at_least((max_pos + ks) / ks, 1);
   if (!use_graphs_ || probes_) {
     live_R_ = R;
     live_Rl_ = Rl;
@@ -227,8 +239,11 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   const int* meta = buf_.sel + 2 * max_lrows_;
   // tensor-core path for row buckets >= kTcMinRows (prefill-heavy ticks)
   const bool tc = use_tc_ && tc_ok_ && rcap >= k::kTcMinRows;
-  auto run_gemm = [&](k::GemvArgs& g, const k::TmaMap* map_a, const k::TmaMap& map_w) {
-    if (!tc) {
+  // decode ticks of large models: swap-AB tensor-core GEMV (pure weight stream)
+  const bool swap_ab = use_tc_ && tc_ok_ && rcap <= k::kGemvTcRows;
+  auto run_gemm = [&](k::GemvArgs& g, const k::TmaMap* map_a, const k::TmaMap* map_a16, const k::TmaMap& map_w) {
+    const bool dec_tc = swap_ab && k::gemv_tc_supported(g);
+    if (!tc && !dec_tc) {
       k::gemv(g, st);
       return;
     }
@@ -237,8 +252,12 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       g.X = nullptr;
       g.A = hn_;
       map_a = &map_hn_;
+      map_a16 = &map_hn16_;
     }
-    k::gemm_tc(*map_a, map_w, g, st);
+    if (dec_tc)
+      k::gemv_tc(map_w, *map_a16, g, gv_ws_, gv_cnt_, st);
+    else
+      k::gemm_tc(*map_a, map_w, g, st);
   };
   auto probe_begin = [&](int kind, double bytes) {
     if (probes_) probes_->begin(kind, bytes, st);
@@ -275,7 +294,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     qkv.nkv = nkv;
     qkv.hd = hd;
     probe_begin(KernelProbes::Qkv, 2.0 * qkv.N * qkv.K + 4.0 * live_R_ * D + 2.0 * live_R_ * qkv.N);
-    run_gemm(qkv, nullptr, wmaps_[static_cast<std::size_t>(l)].wqkv);
+    run_gemm(qkv, nullptr, nullptr, wmaps_[static_cast<std::size_t>(l)].wqkv);
     probe_end();
     probe_begin(KernelProbes::Attention, 4.0 * live_keys_ * nkv * hd + 4.0 * live_R_ * nh * hd);
     k::attention(q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_,
@@ -292,7 +311,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     o.epi = k::kEpiResidual;
     o.out = x_;
     probe_begin(KernelProbes::OProj, 2.0 * o.N * o.K + 2.0 * live_R_ * o.K + 8.0 * live_R_ * D);
-    run_gemm(o, &map_h_attn_, wmaps_[static_cast<std::size_t>(l)].wo);
+    run_gemm(o, &map_h_attn_, &map_h_attn16_, wmaps_[static_cast<std::size_t>(l)].wo);
     probe_end();
     // a = silu(gate) * up over rmsnorm(x)
     k::GemvArgs gu;
@@ -307,7 +326,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     gu.epi = k::kEpiSwiGlu;
     gu.out_bf16 = h_;
     probe_begin(KernelProbes::GateUp, 2.0 * gu.N * gu.K + 4.0 * live_R_ * D + 2.0 * live_R_ * s.ffn);
-    run_gemm(gu, nullptr, wmaps_[static_cast<std::size_t>(l)].wgu);
+    run_gemm(gu, nullptr, nullptr, wmaps_[static_cast<std::size_t>(l)].wgu);
     probe_end();
     // x += a . Wd^T
     k::GemvArgs dn;
@@ -320,13 +339,35 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     dn.epi = k::kEpiResidual;
     dn.out = x_;
     probe_begin(KernelProbes::Down, 2.0 * dn.N * dn.K + 2.0 * live_R_ * dn.K + 8.0 * live_R_ * D);
-    run_gemm(dn, &map_h_ffn_, wmaps_[static_cast<std::size_t>(l)].wd);
+    run_gemm(dn, &map_h_ffn_, &map_h_ffn16_, wmaps_[static_cast<std::size_t>(l)].wd);
     probe_end();
   }
   if (with_logits) {
     probe_begin(KernelProbes::LmHead, 2.0 * s.vocab * D + 4.0 * live_Rl_ * D);
-    k::lm_head(x_, buf_.sel, meta, ones_, eps, lm_, s.vocab, D, part_, lm_cnt_, buf_.sel + max_lrows_, out_tok,
-               out_lp, out_ent, logits, st);
+    if (use_tc_ && tc_ok_ && max_lrows_ <= k::kGemvTcRows) {
+      // normalise the selected rows, then the swap-AB tensor-core GEMV with
+      // the fused greedy-statistics epilogue (LM head = one weight stream)
+      k::rmsnorm_rows(x_, max_lrows_, meta, D, ones_, eps, hn_, st, buf_.sel, 1);
+      k::GemvArgs lm;
+      lm.A = hn_;
+      lm.R = k::kGemvTcRows;
+      lm.meta = meta + 1;  // live logits rows
+      lm.N = s.vocab;
+      lm.K = D;
+      lm.W = lm_;
+      lm.epi = k::kEpiLmStats;
+      lm.lm_part = part_;
+      lm.lm_cnt = lm_cnt_;
+      lm.out_idx = buf_.sel + max_lrows_;
+      lm.out_tok = out_tok;
+      lm.out_lp = out_lp;
+      lm.out_ent = out_ent;
+      lm.logits = logits;
+      k::gemv_tc(wmap_lm_, map_hn16_, lm, gv_ws_, gv_cnt_, st);
+    } else {
+      k::lm_head(x_, buf_.sel, meta, ones_, eps, lm_, s.vocab, D, part_, lm_cnt_, buf_.sel + max_lrows_, out_tok,
+                 out_lp, out_ent, logits, st);
+    }
     probe_end();
   }
   MOA_CUDA(cudaGetLastError());

@@ -105,7 +105,11 @@ class DeviceModel {
     k::TmaMap wqkv, wo, wgu, wd;
   };
   std::vector<LayerMaps> wmaps_;
-  k::TmaMap map_hn_, map_h_attn_, map_h_ffn_;  // A operands
+  k::TmaMap wmap_lm_;  // LM head [V][d], 128-row boxes
+  k::TmaMap map_hn_, map_h_attn_, map_h_ffn_;        // A operands, 128-row boxes (prefill)
+  k::TmaMap map_hn16_, map_h_attn16_, map_h_ffn16_;  // 16-row boxes (decode, swap-AB)
+  float* gv_ws_ = nullptr;                           // gemv_tc split-K partials
+  int* gv_cnt_ = nullptr;
   k::bf16* hn_ = nullptr;                      // normalised rows for the tensor-core path
   KernelProbes* probes_ = nullptr;
   int live_R_ = 0, live_Rl_ = 0;

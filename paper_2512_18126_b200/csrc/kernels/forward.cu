@@ -17,6 +17,31 @@ namespace moa::k {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+
+// Programmatic dependent launch: every forward kernel is launched with
+// programmatic stream serialisation; it waits for its predecessor's memory
+// before touching anything, then immediately lets its successor start
+// launching (the successor waits in turn), so launch latency overlaps work.
+#define MOA_PDL_ENTRY()                                     \
+  do {                                                      \
+    asm volatile("griddepcontrol.wait;" ::: "memory");      \
+    asm volatile("griddepcontrol.launch_dependents;" :::); \
+  } while (0)
+
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 constexpr int kRB = 8;    // rows per CTA row-block
 constexpr int kCPW = 4;   // output columns per warp
 constexpr int kWarps = 8;
@@ -172,6 +197,7 @@ __global__ void fill_f32_kernel(float* dst, long long n, float v) {
 __global__ void embed_kernel(const RowDesc* __restrict__ rows, const int* __restrict__ meta,
                              const int* __restrict__ out_tok, const bf16* __restrict__ emb, int d,
                              float* __restrict__ x) {
+  MOA_PDL_ENTRY();
   const int r = blockIdx.x;
   if (r >= meta[0]) return;
   int t = rows[r].tok;
@@ -198,6 +224,16 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
   const int cg = warp % WG, kp = warp / WG;
   const int n0 = (blockIdx.x * WG + cg) * kCPW;
   const int r0 = blockIdx.z * kRB;
+  const int kpart = a.K / KP, kb = kp * kpart, ke = kb + kpart;
+  // Weights never depend on the previous kernel: the first k-step's weight
+  // vectors are in flight before waiting on it (PDL).
+  uint4 w_first[kCPW];
+#pragma unroll
+  for (int c = 0; c < kCPW; ++c)
+    w_first[c] = (n0 + c < a.N && kb + lane * 8 < ke)
+                     ? ldg_stream(a.W + static_cast<long long>(n0 + c) * a.K + kb + lane * 8)
+                     : make_uint4(0, 0, 0, 0);
+  MOA_PDL_ENTRY();
   const int live = a.meta ? __ldg(a.meta) : a.R;
   if (r0 >= live) return;  // uniform across the CTA
   const int rows = min(kRB, live - r0);
@@ -212,12 +248,13 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) acc[i] = 0.f;
   if (n0 < a.N) {
-    const int kpart = a.K / KP, kb = kp * kpart, ke = kb + kpart;
     for (int k = kb + lane * 8; k < ke; k += 256) {
       uint4 w[kCPW];
 #pragma unroll
       for (int c = 0; c < kCPW; ++c)
-        w[c] = (n0 + c < a.N) ? ldg_stream(a.W + static_cast<long long>(n0 + c) * a.K + k) : make_uint4(0, 0, 0, 0);
+        w[c] = (k == kb + lane * 8) ? w_first[c]
+               : (n0 + c < a.N)     ? ldg_stream(a.W + static_cast<long long>(n0 + c) * a.K + k)
+                                    : make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int r = 0; r < kRB; ++r) {
         if (r < rows) {
@@ -286,33 +323,34 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
   }
 }
 
-// Split-KV attention: CTA (row, head, split) covers kKvSplit keys with 4
+// Split-KV attention: CTA (row, head, split) covers kv_split(hd) keys with NW
 // warps x 32 keys; a row whose context needs several splits writes partials
 // and the last CTA to arrive combines them in split order.
-template <int HD>
-__global__ void __launch_bounds__(128)
+template <int HD, int NW>
+__global__ void __launch_bounds__(NW * 32)
 attention_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, const int* __restrict__ meta, int nh,
                  int nkv, const bf16* __restrict__ kpool, const bf16* __restrict__ vpool, long long kv_stride,
                  long long layer_off, int max_ctx, bf16* __restrict__ o, float* __restrict__ ws,
                  int* __restrict__ cnt, int nsplit_max) {
+  MOA_PDL_ENTRY();
   constexpr int E = HD / 32;
   constexpr int V8 = HD / 8;  // 16-byte vectors per K/V row
   __shared__ float qs[HD];
-  __shared__ float wm[4], wl[4], wo[4][HD];
-  __shared__ __align__(16) bf16 vs[4][32][HD];  // V rows of each warp's 32 keys
-  __shared__ float ps[4][32];
+  __shared__ float wm[NW], wl[NW], wo[NW][HD];
+  __shared__ __align__(16) bf16 vs[NW][32][HD];  // V rows of each warp's 32 keys
+  __shared__ float ps[NW][32];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.x, h = blockIdx.y, s = blockIdx.z;
   if (r >= __ldg(meta)) return;
   const RowDesc rd = rows[r];
   const int n = rd.pos + 1;
-  const int nsplit = (n + kKvSplit - 1) / kKvSplit;
+  const int nsplit = (n + (NW * 32) - 1) / (NW * 32);
   if (s >= nsplit) return;
   const int kvh = h / (nh / nkv);
   const bf16* K = kpool + rd.kv * kv_stride + layer_off + static_cast<long long>(kvh) * max_ctx * HD;
   const bf16* V = vpool + rd.kv * kv_stride + layer_off + static_cast<long long>(kvh) * max_ctx * HD;
-  const int base = s * kKvSplit + warp * 32;
+  const int base = s * (NW * 32) + warp * 32;
   const int j = base + lane;
   // every lane issues its key's K and V rows at once (2 x HD bf16 in flight)
   uint4 kk[V8], vv[V8];
@@ -325,7 +363,7 @@ attention_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, c
     for (int v = 0; v < V8; ++v) vv[v] = __ldg(vp + v);
   }
   const bf16* qr = q + (static_cast<long long>(r) * nh + h) * HD;
-  for (int e = threadIdx.x; e < HD; e += 128) qs[e] = __bfloat162float(qr[e]);
+  for (int e = threadIdx.x; e < HD; e += NW * 32) qs[e] = __bfloat162float(qr[e]);
   __syncthreads();
   const float scale = rsqrtf(static_cast<float>(HD));
   float sc = -INFINITY;
@@ -373,26 +411,26 @@ attention_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, c
   __syncthreads();
   // CTA combine of the 4 warps (fixed order)
   float M = wm[0];
-  for (int w = 1; w < 4; ++w) M = fmaxf(M, wm[w]);
+  for (int w = 1; w < NW; ++w) M = fmaxf(M, wm[w]);
   float L = 0.f;
-  float sw[4];
-  for (int w = 0; w < 4; ++w) {
+  float sw[NW];
+  for (int w = 0; w < NW; ++w) {
     sw[w] = wm[w] == -INFINITY ? 0.f : __expf(wm[w] - M);
     L += sw[w] * wl[w];
   }
   bf16* orow = o + (static_cast<long long>(r) * nh + h) * HD;
   if (nsplit == 1) {
-    for (int e = threadIdx.x; e < HD; e += 128) {
+    for (int e = threadIdx.x; e < HD; e += NW * 32) {
       float val = 0.f;
-      for (int w = 0; w < 4; ++w) val += sw[w] * wo[w][e];
+      for (int w = 0; w < NW; ++w) val += sw[w] * wo[w][e];
       orow[e] = __float2bfloat16_rn(val / L);
     }
     return;
   }
   float* part = ws + ((static_cast<long long>(r) * nh + h) * nsplit_max + s) * (2 + HD);
-  for (int e = threadIdx.x; e < HD; e += 128) {
+  for (int e = threadIdx.x; e < HD; e += NW * 32) {
     float val = 0.f;
-    for (int w = 0; w < 4; ++w) val += sw[w] * wo[w][e];
+    for (int w = 0; w < NW; ++w) val += sw[w] * wo[w][e];
     part[2 + e] = val;
   }
   if (threadIdx.x == 0) {
@@ -413,7 +451,7 @@ attention_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, c
   for (int t = 0; t < nsplit; ++t) Mg = fmaxf(Mg, __ldcg(pr + t * (2 + HD)));
   float Lg = 0.f;
   for (int t = 0; t < nsplit; ++t) Lg += __expf(__ldcg(pr + t * (2 + HD)) - Mg) * __ldcg(pr + t * (2 + HD) + 1);
-  for (int e = threadIdx.x; e < HD; e += 128) {
+  for (int e = threadIdx.x; e < HD; e += NW * 32) {
     float val = 0.f;
     for (int t = 0; t < nsplit; ++t) val += __expf(__ldcg(pr + t * (2 + HD)) - Mg) * __ldcg(pr + t * (2 + HD) + 2 + e);
     orow[e] = __float2bfloat16_rn(val / Lg);
@@ -432,6 +470,7 @@ lm_head_kernel(const float* __restrict__ X, const int* __restrict__ sel, const i
                float eps, const bf16* __restrict__ W, int V, int d, LmStat* __restrict__ part,
                int* __restrict__ cnt, const int* __restrict__ out_idx, int* __restrict__ out_tok,
                float* __restrict__ out_lp, float* __restrict__ out_ent, float* __restrict__ logits) {
+  MOA_PDL_ENTRY();
   __shared__ float inv_s[kLmMaxRows];
   __shared__ LmStat sm[kWarps][kRB];
   __shared__ bool last;
@@ -542,10 +581,10 @@ void gemv_launch(const GemvArgs& a, cudaStream_t st) {
   const int wg = kWarps / kp;
   dim3 grid((a.N + wg * kCPW - 1) / (wg * kCPW), 1, (a.R + kRB - 1) / kRB);
   switch (wg) {
-    case 1: gemv_kernel<1, NORM><<<grid, kWarps * 32, 0, st>>>(a); break;
-    case 2: gemv_kernel<2, NORM><<<grid, kWarps * 32, 0, st>>>(a); break;
-    case 4: gemv_kernel<4, NORM><<<grid, kWarps * 32, 0, st>>>(a); break;
-    default: gemv_kernel<8, NORM><<<grid, kWarps * 32, 0, st>>>(a); break;
+    case 1: launch_pdl(gemv_kernel<1, NORM>, grid, dim3(kWarps * 32), st, a); break;
+    case 2: launch_pdl(gemv_kernel<2, NORM>, grid, dim3(kWarps * 32), st, a); break;
+    case 4: launch_pdl(gemv_kernel<4, NORM>, grid, dim3(kWarps * 32), st, a); break;
+    default: launch_pdl(gemv_kernel<8, NORM>, grid, dim3(kWarps * 32), st, a); break;
   }
 }
 
@@ -562,7 +601,7 @@ void fill_f32(float* dst, long long n, float v, cudaStream_t st) {
 
 void embed(const RowDesc* rows, int R_cap, const int* meta, const int* out_tok, const bf16* emb, int d, float* x,
            cudaStream_t st) {
-  if (R_cap > 0) embed_kernel<<<R_cap, 128, 0, st>>>(rows, meta, out_tok, emb, d, x);
+  if (R_cap > 0) launch_pdl(embed_kernel, dim3(R_cap), dim3(128), st, rows, meta, out_tok, emb, d, x);
 }
 
 void gemv(const GemvArgs& a, cudaStream_t st) {
@@ -589,10 +628,10 @@ void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, co
   const int nsplit_max = (max_ctx + kKvSplit - 1) / kKvSplit;
   dim3 grid(R_cap, nh, nsplit_cap);
   if (hd == 64)
-    attention_kernel<64><<<grid, 128, 0, st>>>(q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx,
+    launch_pdl(attention_kernel<64, 8>, grid, dim3(256), st, q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx,
                                                o, ws, cnt, nsplit_max);
   else if (hd == 128)
-    attention_kernel<128><<<grid, 128, 0, st>>>(q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx,
+    launch_pdl(attention_kernel<128, 4>, grid, dim3(128), st, q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx,
                                                 o, ws, cnt, nsplit_max);
   else
     printf("attention: unsupported head_dim %d\n", hd);
@@ -606,7 +645,7 @@ int lm_head_blocks(int V) {
 void lm_head(const float* X, const int* sel, const int* meta, const float* g, float eps, const bf16* W, int V, int d,
              LmStat* part, int* cnt, const int* out_idx, int* out_tok, float* out_lp, float* out_ent, float* logits,
              cudaStream_t st) {
-  lm_head_kernel<<<lm_head_blocks(V), kWarps * 32, 0, st>>>(X, sel, meta, g, eps, W, V, d, part, cnt, out_idx, out_tok,
+  launch_pdl(lm_head_kernel, dim3(lm_head_blocks(V)), dim3(kWarps * 32), st, X, sel, meta, g, eps, W, V, d, part, cnt, out_idx, out_tok,
                                                             out_lp, out_ent, logits);
 }
 

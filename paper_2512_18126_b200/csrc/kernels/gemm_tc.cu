@@ -238,25 +238,47 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kBN));
 }
 
-__global__ void rmsnorm_rows_kernel(const float* __restrict__ x, const int* __restrict__ meta, int K,
-                                    const float* __restrict__ g, float eps, bf16* __restrict__ h) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (r >= __ldg(meta)) return;
-  const float* xr = x + static_cast<long long>(r) * K;
+// One CTA per row: 16-byte vector loads, block reduction in a fixed order.
+__global__ void __launch_bounds__(128) rmsnorm_rows_kernel(const float* __restrict__ x, const int* __restrict__ sel,
+                                                           const int* __restrict__ meta, int meta_idx, int K,
+                                                           const float* __restrict__ g, float eps,
+                                                           bf16* __restrict__ h) {
+  __shared__ float red[4];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int i = blockIdx.x;
+  if (i >= meta[meta_idx]) return;
+  const int r = sel ? sel[i] : i;
+  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long long>(r) * K);
   float ss = 0.f;
-  for (int k = lane * 4; k < K; k += 128) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(xr + k));
-    ss = fmaf(v.x, v.x, ss);
-    ss = fmaf(v.y, v.y, ss);
-    ss = fmaf(v.z, v.z, ss);
-    ss = fmaf(v.w, v.w, ss);
+  for (int v = threadIdx.x; v < K / 4; v += 128) {
+    const float4 t = xr[v];
+    ss = fmaf(t.x, t.x, ss);
+    ss = fmaf(t.y, t.y, ss);
+    ss = fmaf(t.z, t.z, ss);
+    ss = fmaf(t.w, t.w, ss);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  const float inv = 1.0f / sqrtf(ss / static_cast<float>(K) + eps);  // == row_inv_rms (forward.cu)
-  for (int k = lane; k < K; k += 32)
-    h[static_cast<long long>(r) * K + k] = __float2bfloat16_rn(xr[k] * inv * g[k]);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  const float tot = red[0] + red[1] + red[2] + red[3];
+  const float inv = 1.0f / sqrtf(tot / static_cast<float>(K) + eps);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const float4* gr = reinterpret_cast<const float4*>(g);
+  for (int v = threadIdx.x; v < K / 8; v += 128) {
+    const float4 a = xr[2 * v], b = xr[2 * v + 1];
+    const float4 ga = gr[2 * v], gb = gr[2 * v + 1];
+    __align__(16) bf16 o[8];
+    o[0] = __float2bfloat16_rn(a.x * inv * ga.x);
+    o[1] = __float2bfloat16_rn(a.y * inv * ga.y);
+    o[2] = __float2bfloat16_rn(a.z * inv * ga.z);
+    o[3] = __float2bfloat16_rn(a.w * inv * ga.w);
+    o[4] = __float2bfloat16_rn(b.x * inv * gb.x);
+    o[5] = __float2bfloat16_rn(b.y * inv * gb.y);
+    o[6] = __float2bfloat16_rn(b.z * inv * gb.z);
+    o[7] = __float2bfloat16_rn(b.w * inv * gb.w);
+    reinterpret_cast<uint4*>(h + static_cast<long long>(i) * K)[v] = *reinterpret_cast<const uint4*>(o);
+  }
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
@@ -307,8 +329,18 @@ void gemm_tc(const TmaMap& map_a, const TmaMap& map_w, const GemvArgs& a, cudaSt
 }
 
 void rmsnorm_rows(const float* x, int R_cap, const int* meta, int K, const float* g, float eps, bf16* h,
-                  cudaStream_t st) {
-  if (R_cap > 0) rmsnorm_rows_kernel<<<(R_cap + 7) / 8, 256, 0, st>>>(x, meta, K, g, eps, h);
+                  cudaStream_t st, const int* sel, int meta_idx) {
+  if (R_cap <= 0) return;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(R_cap);
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, rmsnorm_rows_kernel, x, sel, meta, meta_idx, K, g, eps, h);
 }
 
 }  // namespace moa::k

@@ -1,0 +1,308 @@
+// Decode GEMV on the tensor cores ("swap AB"): for R <= 16 activation rows
+//   D[128 weight rows][16] = W_tile[128][K] . X[16][K]^T     (tcgen05, TMEM)
+// so the weight tile is the M = 128 operand and the few decode rows are
+// N = 16: the tensor pipe does the dot products for free and the kernel is a
+// pure HBM stream of weights.  Work item = (128-row weight tile, K split);
+// weights and activations arrive by TMA (SWIZZLE_128B) through a 6-stage
+// mbarrier ring, one elected thread issues tcgen05.mma, 4 warps read the
+// 128 x 16 fp32 accumulator back with tcgen05.ld (thread = weight row, 16
+// registers = activation rows).  With K split over S CTAs, each writes a
+// partial tile and the last CTA to arrive sums the S partials in split order
+// and runs the epilogue (deterministic; S depends on (N, K) only).
+// Epilogues: the GEMV path's (RoPE + KV append, residual, SwiGLU, fp32);
+// RoPE / gate-up partners are adjacent weight rows = adjacent lanes.
+#include <cstdio>
+
+#include "kernels.cuh"
+#include "tc_common.cuh"
+
+namespace moa::k {
+
+namespace {
+
+using namespace tc;
+
+constexpr int kM = 128, kN = 16, kBK = 64, kStages = 6;
+constexpr int kTileW = kM * kBK * 2;  // 16 KB
+constexpr int kTileX = kN * kBK * 2;  // 2 KB
+constexpr int kSmem = kStages * (kTileW + kTileX) + 1024 + 256;
+constexpr std::uint32_t kIdesc = idesc_bf16(kM, kN);
+
+__device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const float (&v)[16]) {
+  const int lane = threadIdx.x & 31;
+  (void)lane;
+#pragma unroll
+  for (int r = 0; r < kN; ++r) {
+    const float x = v[r];
+    const float partner = __shfl_xor_sync(0xffffffffu, x, 1);  // weight row n ^ 1
+    if (r >= R || n >= a.N) continue;
+    switch (a.epi) {
+      case kEpiF32:
+        a.out[static_cast<long long>(r) * a.N + n] = x;
+        break;
+      case kEpiResidual:
+        a.out[static_cast<long long>(r) * a.N + n] += x;
+        break;
+      case kEpiSwiGlu:
+        if (!(n & 1))
+          a.out_bf16[static_cast<long long>(r) * (a.N / 2) + n / 2] = __float2bfloat16_rn(x / (1.0f + __expf(-x)) * partner);
+        break;
+      case kEpiQkv: {
+        const RowDesc rd = a.rows[r];
+        const int hd = a.hd, half = hd / 2, qk_cols = (a.nh + a.nkv) * hd;
+        if (n < qk_cols) {
+          if (n & 1) break;
+          const int head = n / hd, e = (n % hd) / 2;
+          const float2 cs = a.rope[static_cast<long long>(rd.pos) * half + e];
+          const float y0 = __fsub_rn(__fmul_rn(x, cs.x), __fmul_rn(partner, cs.y));
+          const float y1 = __fadd_rn(__fmul_rn(partner, cs.x), __fmul_rn(x, cs.y));
+          bf16* dst = head < a.nh ? a.out_bf16 + (static_cast<long long>(r) * a.nh + head) * hd
+                                  : a.kpool + rd.kv * a.kv_stride + a.layer_off +
+                                        (static_cast<long long>(head - a.nh) * a.max_ctx + rd.pos) * hd;
+          dst[e] = __float2bfloat16_rn(y0);
+          dst[e + half] = __float2bfloat16_rn(y1);
+        } else {
+          const int vc = n - qk_cols, kh = vc / hd, e = vc % hd;
+          a.vpool[rd.kv * a.kv_stride + a.layer_off + (static_cast<long long>(kh) * a.max_ctx + rd.pos) * hd + e] =
+              __float2bfloat16_rn(x);
+        }
+        break;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ LmStat stat_merge(LmStat a, LmStat b) {
+  if (b.s == 0.f) return a;
+  if (a.s == 0.f) return b;
+  LmStat r;
+  if (b.m > a.m || (b.m == a.m && b.idx < a.idx)) {
+    r.m = b.m;
+    r.idx = b.idx;
+  } else {
+    r.m = a.m;
+    r.idx = a.idx;
+  }
+  const float da = a.m - r.m, db = b.m - r.m;
+  const float ea = __expf(da), eb = __expf(db);
+  r.s = ea * a.s + eb * b.s;
+  r.t = ea * (a.t + da * a.s) + eb * (b.t + db * b.s);
+  return r;
+}
+
+__device__ __forceinline__ LmStat shfl_stat(LmStat s, int off) {
+  return LmStat{__shfl_xor_sync(0xffffffffu, s.m, off), __shfl_xor_sync(0xffffffffu, s.s, off),
+                __shfl_xor_sync(0xffffffffu, s.t, off), __shfl_xor_sync(0xffffffffu, s.idx, off)};
+}
+
+// LM head epilogue: per logits row, greedy statistics over this tile's 128
+// vocab entries (warp then CTA merge, fixed order), then the last CTA merges
+// all tiles and writes token / logprob / entropy.
+__device__ void lm_stats_epilogue(const GemvArgs& a, int n, int R, const float (&v)[16], int tile, int ntiles) {
+  __shared__ LmStat sm[4][kN];
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const LmStat none{-INFINITY, 0.f, 0.f, 0x7fffffff};
+#pragma unroll
+  for (int r = 0; r < kN; ++r) {
+    const bool ok = r < R && n < a.N;
+    if (ok && a.logits) a.logits[static_cast<long long>(r) * a.N + n] = v[r];
+    LmStat st = ok ? LmStat{v[r], 1.f, 0.f, n} : none;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const LmStat o = shfl_stat(st, off);
+      st = (lane & off) ? stat_merge(o, st) : stat_merge(st, o);
+    }
+    if (lane == 0) sm[warp][r] = st;
+  }
+  __syncthreads();
+  if (threadIdx.x < R) {
+    LmStat st = sm[0][threadIdx.x];
+    for (int w = 1; w < 4; ++w) st = stat_merge(st, sm[w][threadIdx.x]);
+    a.lm_part[static_cast<long long>(threadIdx.x) * ntiles + tile] = st;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(a.lm_cnt, 1) == ntiles - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int r = warp; r < R; r += 4) {
+    LmStat st = none;
+    const float4* pr = reinterpret_cast<const float4*>(a.lm_part + static_cast<long long>(r) * ntiles);
+    for (int b0 = lane; b0 < ntiles; b0 += 32 * 8) {
+      float4 raw[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int b = b0 + 32 * u;
+        raw[u] = b < ntiles ? __ldcg(pr + b) : make_float4(-INFINITY, 0.f, 0.f, __int_as_float(0x7fffffff));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) st = stat_merge(st, LmStat{raw[u].x, raw[u].y, raw[u].z, __float_as_int(raw[u].w)});
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const LmStat o = shfl_stat(st, off);
+      st = (lane & off) ? stat_merge(o, st) : stat_merge(st, o);
+    }
+    if (lane == 0) {
+      const int oi = a.out_idx[r];
+      const float ls = logf(st.s);
+      a.out_tok[oi] = st.idx;
+      a.out_lp[oi] = -ls;
+      a.out_ent[oi] = ls - st.t / st.s;
+    }
+  }
+  if (threadIdx.x == 0) *a.lm_cnt = 0;
+}
+
+__global__ void __launch_bounds__(128)
+gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, const GemvArgs a,
+               int S, float* __restrict__ ws, int* __restrict__ cnt) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  unsigned char* sw = smem;
+  unsigned char* sx = smem + kStages * kTileW;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sx + kStages * kTileX);
+  std::uint64_t* empty = full + kStages;
+  std::uint64_t* done = empty + kStages;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
+  __shared__ bool last;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x, split = blockIdx.y;
+  const int m0 = tile * kM;
+  const int kt_n = a.K / kBK / S, kt0 = split * kt_n;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&map_w);
+    prefetch_tmap(&map_x);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    mbar_fence_init();
+  }
+  if (warp == 0) tmem_alloc<32>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // TMA producer.  Weight tiles do not depend on the previous kernel, so
+    // the first ring's worth is issued before waiting on it (PDL).
+    int kt = 0;
+    for (; kt < kt_n && kt < kStages; ++kt) {
+      mbar_expect_tx(&full[kt], kTileW + kTileX);
+      tma_load_2d(sw + kt * kTileW, &map_w, &full[kt], (kt0 + kt) * kBK, m0);
+    }
+    pdl_wait();
+    for (int j = 0; j < kt; ++j) tma_load_2d(sx + j * kTileX, &map_x, &full[j], (kt0 + j) * kBK, 0);
+    for (; kt < kt_n; ++kt) {
+      const int s = kt % kStages;
+      mbar_wait(&empty[s], ((kt / kStages) - 1) & 1);
+      mbar_expect_tx(&full[s], kTileW + kTileX);
+      tma_load_2d(sw + s * kTileW, &map_w, &full[s], (kt0 + kt) * kBK, m0);
+      tma_load_2d(sx + s * kTileX, &map_x, &full[s], (kt0 + kt) * kBK, 0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    for (int kt = 0; kt < kt_n; ++kt) {
+      const int s = kt % kStages;
+      mbar_wait(&full[s], (kt / kStages) & 1);
+      tc_fence_after();
+      const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + s * kTileX);
+#pragma unroll
+      for (int k = 0; k < kBK / 16; ++k) umma_bf16(tmem, umma_desc(w0 + k * 32), umma_desc(x0 + k * 32), kIdesc, (kt | k) ? 1u : 0u);
+      umma_commit(&empty[s]);
+    }
+    umma_commit(done);
+  }
+  __syncwarp();
+  pdl_wait();  // every epilogue thread reads the previous kernel's outputs (rows, residual)
+  mbar_wait(done, 0);
+  tc_fence_after();
+  pdl_launch_dependents();
+
+  const int R = a.meta ? __ldcg(a.meta) : a.R;
+  const int row = warp * 32 + lane, n = m0 + row;
+  float v[16];
+  tmem_ld16(tmem + (static_cast<std::uint32_t>(warp * 32) << 16), v);
+  if (a.epi == kEpiLmStats) {
+    lm_stats_epilogue(a, n, R, v, tile, gridDim.x);  // S == 1 for the LM head
+  } else if (S == 1) {
+    epilogue(a, n, R, v);
+  } else {
+    float4* p = reinterpret_cast<float4*>(ws + ((static_cast<long long>(tile) * S + split) * kM + row) * kN);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) p[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(cnt + tile, 1) == S - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      for (int s = 0; s < S; ++s) {
+        const float4* q = reinterpret_cast<const float4*>(ws + ((static_cast<long long>(tile) * S + s) * kM + row) * kN);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 t = __ldcg(q + i);
+          v[4 * i] += t.x;
+          v[4 * i + 1] += t.y;
+          v[4 * i + 2] += t.z;
+          v[4 * i + 3] += t.w;
+        }
+      }
+      epilogue(a, n, R, v);
+      if (threadIdx.x == 0) cnt[tile] = 0;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<32>(tmem);
+}
+
+}  // namespace
+
+int gemv_tc_splits(int N, int K, int epi) {
+  const int tiles = (N + kM - 1) / kM, kts = K / kBK;
+  int S = 1;
+  if (epi == kEpiLmStats) return 1;
+  while (tiles * S * 2 <= 2 * 148 && kts % (S * 2) == 0 && S < 16) S *= 2;
+  return S;
+}
+
+long long gemv_tc_ws_floats(int N, int K) {
+  return static_cast<long long>((N + kM - 1) / kM) * gemv_tc_splits(N, K, kEpiF32) * kM * kN;
+}
+
+bool gemv_tc_supported(const GemvArgs& a) {
+  return a.R <= kN && a.K % kBK == 0 && a.N % 2 == 0 && static_cast<long long>(a.N) * a.K >= (2LL << 20);
+}
+
+void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float* ws, int* cnt, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    attr = true;
+  }
+  const int S = gemv_tc_splits(a.N, a.K, a.epi);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((a.N + kM - 1) / kM, S);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr_pdl[1];
+  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr_pdl;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, gemv_tc_kernel, *reinterpret_cast<const CUtensorMap*>(&map_w),
+                     *reinterpret_cast<const CUtensorMap*>(&map_x), a, S, ws, cnt);
+}
+
+}  // namespace moa::k

@@ -52,7 +52,8 @@ void embed(const RowDesc* rows, int R_cap, const int* meta, const int* out_tok, 
 // rows.  A is either bf16 activations or, with `norm`, the fp32 residual rows
 // normalised on the fly (A = bf16(rmsnorm(x) * g), the oracle's rounding
 // point).  Epilogues:
-enum Epi : int { kEpiF32 = 0, kEpiResidual = 1, kEpiSwiGlu = 2, kEpiQkv = 3 };
+enum Epi : int { kEpiF32 = 0, kEpiResidual = 1, kEpiSwiGlu = 2, kEpiQkv = 3, kEpiLmStats = 4 };
+struct LmStat;
 struct GemvArgs {
   const bf16* A = nullptr;   // [R][K] bf16 (when X == nullptr)
   const float* X = nullptr;  // [R][K] fp32 residual rows (norm prologue)
@@ -71,6 +72,14 @@ struct GemvArgs {
   bf16* vpool = nullptr;
   long long kv_stride = 0, layer_off = 0;
   int max_ctx = 0, nh = 0, nkv = 0, hd = 0;
+  // kEpiLmStats (tensor-core LM head): greedy statistics per logits row
+  LmStat* lm_part = nullptr;  // [rows][tiles]
+  int* lm_cnt = nullptr;      // one int, zero-initialised once
+  const int* out_idx = nullptr;
+  int* out_tok = nullptr;
+  float* out_lp = nullptr;
+  float* out_ent = nullptr;
+  float* logits = nullptr;  // optional fp32 [rows][N]
 };
 void gemv(const GemvArgs& a, cudaStream_t st);  // dispatches to gemv_stream for large matrices
 // HBM-streaming variant (gemv_stream.cu): persistent CTAs, cp.async.bulk ring.
@@ -87,16 +96,31 @@ bool gemm_tc_supported(int N, int K);
 // Same epilogues as gemv; A comes from map_a (bf16 rows, already normalised
 // where the GEMV path would normalise on the fly).
 void gemm_tc(const TmaMap& map_a, const TmaMap& map_w, const GemvArgs& a, cudaStream_t st);
-// h[r] = bf16(rmsnorm(x[r]) * g) for the live rows (same rounding as the gemv prologue).
+// h[i] = bf16(rmsnorm(x[sel ? sel[i] : i]) * g) for i < meta[meta_idx] (same
+// rounding as the gemv prologue); one CTA per row, 16-byte vectors.
 void rmsnorm_rows(const float* x, int R_cap, const int* meta, int K, const float* g, float eps, bf16* h,
-                  cudaStream_t st);
+                  cudaStream_t st, const int* sel = nullptr, int meta_idx = 0);
 constexpr int kTcMinRows = 128;  // ticks with at least this many rows of a model use the tensor cores
+
+// ---- decode GEMV on the tensor cores, swap-AB (gemv_tc.cu) ----
+// Weight map: box 64 x 128 rows (the gemm_tc weight maps); activation map:
+// box 64 x 16 rows.  ws / cnt: split-K partials and per-tile counters
+// (cnt zero-initialised once; the kernel leaves it zero).  Launched with
+// programmatic dependent launch: weight tiles stream before the previous
+// kernel has finished.
+constexpr int kGemvTcRows = 16;
+bool gemv_tc_supported(const GemvArgs& a);
+int gemv_tc_splits(int N, int K, int epi);
+long long gemv_tc_ws_floats(int N, int K);
+void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float* ws, int* cnt, cudaStream_t st);
 
 // o[r][h] = softmax(q k^T / sqrt(hd)) v over keys [0, pos] of the row's agent;
 // keys split across CTAs (kKvSplit keys each), partials combined in split
 // order by the last-arriving CTA.  `ws` >= attention_ws_floats(...) floats,
 // `cnt` >= R*nh ints, zero-initialised once (the kernel leaves them zero).
-constexpr int kKvSplit = 128;
+constexpr int kKvSplit = 128;  // smallest split (sizes the partial workspace)
+// keys per attention CTA: 8 warps x 32 for hd 64, 4 warps x 32 for hd 128
+inline int kv_split(int hd) { return hd == 64 ? 256 : 128; }
 long long attention_ws_floats(int R, int nh, int hd, int max_ctx);
 void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, const int* meta, int nh, int nkv,
                int hd, const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx,

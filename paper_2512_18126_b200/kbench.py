@@ -45,19 +45,22 @@ def _time(fn, iters):
     return e0.elapsed_time(e1) / iters  # ms per launch
 
 
-def gemv_case(name, R, N, K, copies):
+def gemv_case(name, R, N, K, copies, kernel="gemv"):
     g = torch.Generator(device="cuda").manual_seed(N + K)
     Ws = [(torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16) for _ in range(copies)]
-    A = torch.randn(R, K, device="cuda", generator=g).to(torch.bfloat16)
+    A = torch.randn(16, K, device="cuda", generator=g).to(torch.bfloat16)
     out = torch.empty(R, N, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
 
     def fn(i):
-        capi.check(capi.lib().moa_k_gemv(A.data_ptr(), 0, R, Ws[i % copies].data_ptr(), N, K, out.data_ptr(), st))
+        if kernel == "gemv_tc":
+            capi.check(capi.lib().moa_k_gemv_tc(A.data_ptr(), R, Ws[i % copies].data_ptr(), N, K, out.data_ptr(), st))
+        else:
+            capi.check(capi.lib().moa_k_gemv(A.data_ptr(), 0, R, Ws[i % copies].data_ptr(), N, K, out.data_ptr(), st))
 
     ms = _time(fn, 40)
     bytes_ = 2.0 * N * K + 2.0 * R * K + 4.0 * R * N
-    return {"kernel": "gemv", "case": name, "rows": R, "N": N, "K": K, "us": ms * 1e3,
+    return {"kernel": kernel, "case": name, "rows": R, "N": N, "K": K, "us": ms * 1e3,
             "gbs": bytes_ / (ms / 1e3) / 1e9, "bytes": bytes_}
 
 
@@ -81,11 +84,13 @@ def gemm_case(name, M, N, K):
 def run():
     hbm, tf, src = peaks()
     rows = []
-    for R in (1, 4, 8):
-        rows.append(gemv_case("1b.qkv", R, 3072, 2048, 48))
-        rows.append(gemv_case("1b.gate_up", R, 16384, 2048, 16))
-        rows.append(gemv_case("1b.down", R, 2048, 8192, 16))
-        rows.append(gemv_case("1b.lm_head", R, 50000, 2048, 4))
+    for kernel in ("gemv_tc", "gemv"):
+        for R in (1, 8):
+            rows.append(gemv_case("1b.qkv", R, 3072, 2048, 48, kernel))
+            rows.append(gemv_case("1b.gate_up", R, 16384, 2048, 16, kernel))
+            rows.append(gemv_case("1b.down", R, 2048, 8192, 16, kernel))
+            rows.append(gemv_case("1b.lm_head", R, 50000, 2048, 4, kernel))
+            rows.append(gemv_case("8b.gate_up", R, 28672, 4096, 4, kernel))
     for M in (512, 2048):
         rows.append(gemm_case("1b.gate_up", M, 16384, 2048))
         rows.append(gemm_case("1b.qkv", M, 3072, 2048))

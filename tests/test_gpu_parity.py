@@ -99,6 +99,23 @@ def test_gemm_tc_vs_torch_fp32(torch_cuda, M, N, K):
     assert torch.allclose(out, ref, atol=1e-3 * math.sqrt(K / 256), rtol=1e-4), (out - ref).abs().max()
 
 
+@pytest.mark.parametrize("R,N,K", [(1, 3072, 2048), (8, 16384, 2048), (16, 2048, 8192), (3, 50000, 2048),
+                                   (5, 6144, 4096)])
+def test_gemv_tc_vs_torch_fp32(torch_cuda, R, N, K):
+    """Swap-AB tensor-core decode GEMV (split-K, last-arriver epilogue)."""
+    torch = torch_cuda
+    g = torch.Generator(device="cuda").manual_seed(R + N + K)
+    A = torch.randn(16, K, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    out = torch.full((R, N), float("nan"), device="cuda")
+    for _ in range(2):  # second call re-uses the zeroed split counters
+        capi.check(capi.lib().moa_k_gemv_tc(A.data_ptr(), R, W.data_ptr(), N, K, out.data_ptr(), 0))
+    torch.cuda.synchronize()
+    ref = A[:R].float() @ W.float().T
+    assert torch.isfinite(out).all()
+    assert torch.allclose(out, ref, atol=1e-3 * math.sqrt(K / 256), rtol=1e-4), (out - ref).abs().max()
+
+
 def test_mock_embed_bit_exact_on_gpu(golden):
     import ctypes as C
     for c in golden("mock_embed.json"):
