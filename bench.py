@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-baseline-s", type=float, default=15.0, help="CPU sample budget (seconds)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--placement", default="replicas", choices=["replicas", "tree"],
+                    help="N>1: independent replicas (weak scaling) or one request tree-partitioned over the ranks")
     ap.add_argument("--profile-only", action="store_true", help="run steps without JSON (for ncu)")
     return ap.parse_args()
 
@@ -186,7 +188,7 @@ def run_reference_arm(args, cfg, rank, world):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "p50_ms_per_request": 1e3 * statistics.median(steps), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "scaling": "strong" if tree else "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
             "config": {"workload": cfg["workload"], "name": cfg["name"]},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                              "sample": f"{args.steps} {cfg['name']} requests through oracle/ (numpy fp32 "
@@ -217,12 +219,22 @@ def main():
     from paper_2512_18126_b200 import capi
 
     eng, qc = capi.engine_for(cfg, device=local)
+    tree = world > 1 and args.placement == "tree"
+    if tree:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(capi.nccl_unique_id()), dtype=torch.uint8))
+        pg.broadcast(uid, 0)
+        eng.attach_comm(bytes(uid.cpu().numpy()), rank, world)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
+
+    def sample_of(i):  # tree mode: every rank serves the same request
+        return (i if tree else rank * 1000 + i) % 24
 
     def one(i, detail=False):
         flush.fill_(float(i))
         torch.cuda.synchronize()
-        return eng.run_query(qc, sample=(rank * 1000 + i) % 24, resolve=detail, detail=detail)
+        return eng.run_query(qc, sample=sample_of(i), resolve=detail, detail=detail)
 
     for i in range(args.warmup):
         one(i)
@@ -251,7 +263,7 @@ def main():
         flush.fill_(float(i))
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r = eng.run_query(qc, sample=(rank * 1000 + i) % 24, resolve=True, detail=True)
+        r = eng.run_query(qc, sample=sample_of(i), resolve=True, detail=True)
         e2e_wall += time.perf_counter() - t0
         e2e_toks += r["tokens"]
         h2d += r["rows"] * 16
@@ -272,6 +284,8 @@ def main():
         sm = t.clone()
         pg.all_reduce(sm, op=pg.ReduceOp.SUM)
         dev_ms_max, e2e_ms_max, toks_all, e2e_toks_all = mx[0].item(), mx[1].item(), sm[2].item(), sm[3].item()
+        if tree:  # one request shared by all ranks: count its tokens once
+            toks_all, e2e_toks_all = toks, e2e_toks
     else:
         dev_ms_max, e2e_ms_max, toks_all, e2e_toks_all = dev_ms, e2e_wall * 1e3, toks, e2e_toks
     if rank != 0:
@@ -284,9 +298,9 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps,
         "p50_ms_per_request": statistics.median(per_req), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "scaling": "strong" if tree else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": cfg["workload"], "name": cfg["name"], "l2": "flushed (256 MiB write) between requests",
-                   "models": {t: m["shape"] for t, m in cfg["models"].items()}, "parallelism": f"replicas{world}"},
+                   "models": {t: m["shape"] for t, m in cfg["models"].items()}, "parallelism": f"tree{world}" if tree else f"replicas{world}"},
         "e2e": {"value": e2e_toks_all / (e2e_ms_max / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps},
         "gpu_launches": int(sum(v["launches"] for v in probes.values()) + n_ee_launches),

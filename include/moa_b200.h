@@ -74,6 +74,17 @@ int moa_engine_reset(moa_engine* eng);
 int moa_engine_probe(moa_engine* eng, int enable);
 int moa_engine_probe_stats(moa_engine* eng, int kind, int* launches, double* ms, double* bytes);
 
+/* ---- tree-partitioned serving over several GPUs (one process per GPU) ----
+ * Rank 0 creates the id, the caller broadcasts it (e.g. torch.distributed),
+ * every rank attaches before its first request.  run_query then places the
+ * agents along the tree (moa_placement), every rank runs the same tick
+ * schedule, computes only its own agents, and moves each output chunk from its
+ * owner to the other ranks with NCCL P2P. */
+int moa_nccl_unique_id(uint8_t* out /* 128 bytes */);
+int moa_engine_attach_comm(moa_engine* eng, const uint8_t* id /* 128 bytes */, int rank, int world);
+/* ranks[k] = owning rank of agent k (layer-major order) for `world` GPUs. */
+int moa_placement(int kind, int n_layers, const int* widths, const int* cluster_sizes, int world, int* ranks);
+
 /* ---- SimWorld engine protocol (pdsim.hpp:61-156) ------------------------
  * Agents are (layer, position) = AgentId (agent.hpp:16-37).  Tokens passed
  * in are literal ids in [0, vocab).  Time advances by moa_step ticks.      */

@@ -58,12 +58,19 @@ class Request:
 
 class TickEngine:
     def __init__(self, models: dict, max_rows_per_tick: int = 16384, keep_logits: bool = False,
-                 forced: dict | None = None):
+                 forced: dict | None = None, owner: dict | None = None, rank: int = 0, exchange=None):
         """forced: agent -> (tokens, logprobs, entropy) replayed instead of the
         model's greedy outputs (record-and-replay parity: the schedule, routing
-        and early-exit logic then run on exactly the GPU's completions)."""
+        and early-exit logic then run on exactly the GPU's completions).
+
+        owner / rank / exchange: tree-partitioned mode (the C++ engine's
+        replicated control plane): every rank runs this schedule for all
+        agents but computes rows only for agents it owns; at each chunk,
+        exchange(agent, owner, payload) returns the chunk's (tokens, logprobs,
+        entropies) -- the owner passes its payload, the others receive it."""
         self.models = models  # tag -> CpuModel (unused when forced)
         self.forced = forced
+        self.owner, self.rank, self.exchange = owner, rank, exchange
         self.reqs = {}
         self.order = []
         self.tick = 0
@@ -186,6 +193,9 @@ class TickEngine:
         self.req(rid).rec["empty_input"] = True
 
     # ---- ticks ----
+    def _computes(self, r):
+        return self.owner is None or self.owner[r.id] == self.rank
+
     def busy(self):
         for r in self.reqs.values():
             if r.cancelled or r.finished:
@@ -206,7 +216,8 @@ class TickEngine:
             if r.decode_started:
                 if r.n_out < r.max_new:
                     p = len(r.prompt) + r.n_out - 1
-                    rows_by_model.setdefault(r.model, []).append((r, p, r.out[r.n_out - 1], True))
+                    if self._computes(r):
+                        rows_by_model.setdefault(r.model, []).append((r, p, r.out[r.n_out - 1], True))
                     plan.append((r, "decode", None))
                     budget -= 1
                 continue
@@ -217,9 +228,10 @@ class TickEngine:
                     budget -= e - b
                     took = True
                     yields = r.generate_pending and e == len(r.prompt) and r.max_new > 0
-                    lst = rows_by_model.setdefault(r.model, [])
-                    for p in range(b, e):
-                        lst.append((r, p, r.prompt[p], yields and p == e - 1))
+                    if self._computes(r):
+                        lst = rows_by_model.setdefault(r.model, [])
+                        for p in range(b, e):
+                            lst.append((r, p, r.prompt[p], yields and p == e - 1))
                     plan.append((r, "prefill", (b, e, yields)))
                 if took or r.queue:
                     continue
@@ -229,7 +241,8 @@ class TickEngine:
                 else:
                     P = len(r.prompt)
                     tok = r.prompt[P - 1] if P > 0 else 0
-                    rows_by_model.setdefault(r.model, []).append((r, max(P - 1, 0), tok, True))
+                    if self._computes(r):
+                        rows_by_model.setdefault(r.model, []).append((r, max(P - 1, 0), tok, True))
                     plan.append((r, "bootstrap", None))
                     budget -= 1
         # 2. forward per model
@@ -278,7 +291,22 @@ class TickEngine:
             elif kind == "empty":
                 self._start_decode(r, t, 0)
         self.tick += 1
-        # 4. phase A: chunks
+        # 4. phase A: chunks (partitioned mode: owner -> every rank first)
+        if self.exchange is not None:
+            for rid in self.order:
+                r = self.reqs[rid]
+                if r.cancelled or r.finished or not r.decode_started:
+                    continue
+                n = r.n_out
+                if n > r.chunk_begin and (n - r.chunk_begin >= r.apc_chunk or n == r.max_new):
+                    b = r.chunk_begin
+                    mine = self._computes(r)
+                    payload = (r.out[b:n], r.lp[b:n], r.ent[b:n]) if mine else None
+                    toks, lps, ents = self.exchange(rid, self.owner[rid], n - b, payload)
+                    if not mine:
+                        r.out += [int(x) for x in toks]
+                        r.lp += [float(x) for x in lps]
+                        r.ent += [float(x) for x in ents]
         done = []
         for rid in self.order:
             r = self.reqs[rid]

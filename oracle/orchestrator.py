@@ -178,10 +178,26 @@ def exit_groups(cfg: RunConfig, ss: int):
     return groups
 
 
-def run_query(cfg: RunConfig, models: dict, sample: int = 0, keep_logits: bool = False, forced=None):
-    """forced: agent -> (tokens, logprobs, entropy) -- replay mode (see TickEngine)."""
+def tree_placement(topo: Topology, world: int) -> dict:
+    """Owning rank per agent (mirrors csrc/host/orchestrator.cpp
+    tree_placement): leaves in contiguous blocks over the ranks, every
+    dependent agent on the rank of its first precursor."""
+    leaves = topo.layers[0]
+    at = {a: (i * world) // len(leaves) for i, a in enumerate(leaves)}
+    for layer in topo.layers[1:]:
+        for a in layer:
+            at[a] = at[topo.precursors(a)[0]]
+    return at
+
+
+def run_query(cfg: RunConfig, models: dict, sample: int = 0, keep_logits: bool = False, forced=None,
+              world: int = 1, rank: int = 0, exchange=None):
+    """forced: agent -> (tokens, logprobs, entropy) -- replay mode (see TickEngine).
+    world > 1: tree-partitioned mode -- this rank computes only the agents
+    tree_placement gives it; `exchange` moves chunk payloads between ranks."""
     cfg.validate()
-    eng = TickEngine(models, keep_logits=keep_logits, forced=forced)
+    owner = tree_placement(cfg.topology, world) if world > 1 else None
+    eng = TickEngine(models, keep_logits=keep_logits, forced=forced, owner=owner, rank=rank, exchange=exchange)
     ss, drv = build_query(cfg, sample, eng)
     records = []
     if cfg.early_exit and cfg.topology.depth > 1:

@@ -93,6 +93,9 @@ _SIGS = {
     "moa_engine_create": ([_P(ModelSpec), C.c_int, _P(EngineOpts), _P(C.c_void_p)], C.c_int),
     "moa_engine_destroy": ([C.c_void_p], C.c_int),
     "moa_engine_reset": ([C.c_void_p], C.c_int),
+    "moa_nccl_unique_id": ([_P(C.c_uint8)], C.c_int),
+    "moa_engine_attach_comm": ([C.c_void_p, _P(C.c_uint8), C.c_int, C.c_int], C.c_int),
+    "moa_placement": ([C.c_int, C.c_int, _P(C.c_int), _P(C.c_int), C.c_int, _P(C.c_int)], C.c_int),
     "moa_engine_probe": ([C.c_void_p, C.c_int], C.c_int),
     "moa_engine_probe_stats": ([C.c_void_p, C.c_int, _P(C.c_int), _P(C.c_double), _P(C.c_double)], C.c_int),
     "moa_add_agent": ([C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
@@ -248,6 +251,11 @@ class Engine:
     def reset(self):
         check(lib().moa_engine_reset(self.h))
 
+    def attach_comm(self, nccl_id: bytes, rank: int, world: int):
+        """Join a tree-partitioned serving group (call before the first request)."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        check(lib().moa_engine_attach_comm(self.h, buf, rank, world))
+
     PROBE_KINDS = ("embed", "qkv", "attention", "o_proj", "gate_up", "down", "lm_head")
 
     def probe(self, enable: bool):
@@ -382,3 +390,27 @@ def device_count() -> int:
 
 if os.environ.get("MOA_B200_EAGER_LOAD"):
     lib()
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(lib().moa_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def placement(topology: dict, world: int) -> dict:
+    """Owning rank per agent ("l:p") for tree-partitioned serving."""
+    widths = list(topology["widths"])
+    kind = 1 if topology["kind"] == "all_to_all" else 0
+    cs = None
+    if kind == 0:
+        if "cluster_sizes" in topology:
+            sizes = [s for layer in topology["cluster_sizes"] for s in layer]
+        else:
+            sizes = [b for l, b in enumerate(topology["branching"]) for _ in range(widths[l + 1])]
+        cs = (C.c_int * max(1, len(sizes)))(*sizes)
+    w = (C.c_int * len(widths))(*widths)
+    out = (C.c_int * sum(widths))()
+    check(lib().moa_placement(kind, len(widths), w, cs, world, out))
+    names = [f"{l + 1}:{p}" for l, n in enumerate(widths) for p in range(n)]
+    return dict(zip(names, list(out)))

@@ -190,6 +190,34 @@ int moa_engine_reset(moa_engine* eng) {
   return guard([&] { E(eng).reset(); });
 }
 
+int moa_nccl_unique_id(uint8_t* out) {
+  return guard([&] {
+    need(out, "out");
+    moa::PeerComm::unique_id(out);
+  });
+}
+
+int moa_engine_attach_comm(moa_engine* eng, const uint8_t* id, int rank, int world) {
+  return guard([&] {
+    need(id, "id");
+    moa::GpuEngine& g = E(eng);
+    MOA_CUDA(cudaSetDevice(g.device()));
+    g.attach_comm(std::make_unique<moa::PeerComm>(id, rank, world));
+  });
+}
+
+int moa_placement(int kind, int n_layers, const int* widths, const int* cluster_sizes, int world, int* ranks) {
+  return guard([&] {
+    need(ranks, "ranks");
+    if (world < 1) throw moa::ValidationError("placement: world must be >= 1");
+    moa::Topology t = topology_of(kind, n_layers, widths, cluster_sizes);
+    const auto at = moa::tree_placement(t, world);
+    int k = 0;
+    for (const auto& layer : t.layers())
+      for (const auto& a : layer) ranks[k++] = at.at(a);
+  });
+}
+
 int moa_engine_probe(moa_engine* eng, int enable) {
   return guard([&] { E(eng).set_probing(enable != 0); });
 }

@@ -82,14 +82,17 @@ const GpuEngine::Req& GpuEngine::req(const AgentId& id) const {
   return it->second;
 }
 
-void GpuEngine::add_agent(const AgentId& id, int model) {
+void GpuEngine::add_agent(const AgentId& id, int model, int owner) {
   if (reqs_.count(id)) throw ValidationError("sim: agent " + id.str() + " added twice");
   if (model < 0 || model >= n_models()) throw ValidationError("engine: unknown model index for " + id.str());
   if (slots_ >= max_slots_) throw ValidationError("engine: agent capacity exhausted");
+  if (owner >= world()) throw ValidationError("engine: owner rank out of range for " + id.str());
   Req r;
   r.id = id;
   r.model = model;
-  r.kv = models_[static_cast<std::size_t>(model)]->bind_agent();
+  r.owner = owner < 0 ? rank() : owner;
+  r.local = r.owner == rank();
+  r.kv = r.local ? models_[static_cast<std::size_t>(model)]->bind_agent() : -1;
   r.slot = slots_++;
   r.rec.id = id;
   r.rec.model = model;
@@ -266,6 +269,7 @@ void GpuEngine::step() {
   std::vector<std::vector<int>> lsel(nm), lout(nm);
   int budget = opt_.max_rows;
   auto add_row = [&](Req& r, int pos, Token tok, int out_k) {
+    if (!r.local) return;  // another rank computes it; the schedule advances identically here
     auto& rv = rows[static_cast<std::size_t>(r.model)];
     int oi = -1;
     if (out_k >= 0) {
@@ -354,7 +358,36 @@ void GpuEngine::step() {
   }
   const int t = tick_;
   tick_ += 1;
-  // phase A: chunk emission (pdsim.cpp:339-362)
+  // phase A: chunk emission (pdsim.cpp:339-362).  With several ranks the
+  // chunk's tokens / logprobs / entropies first move from the owner to every
+  // other rank (grouped NCCL P2P on the engine stream, so they land before
+  // the next tick's forward and before this tick's early-exit evaluations).
+  if (world() > 1) {
+    bool any = false;
+    for (const AgentId& id : order_) {
+      Req& r = reqs_.at(id);
+      if (r.cancelled || r.finished || !r.dec_started) continue;
+      const int n = r.n_out;
+      if (!(n > r.chunk_begin && (n - r.chunk_begin >= r.apc || n == r.max_new))) continue;
+      if (!any) comm_->begin();
+      any = true;
+      const long long off = static_cast<long long>(r.slot) * opt_.max_out + r.chunk_begin;
+      const long long cnt = n - r.chunk_begin;
+      for (int p = 0; p < world(); ++p) {
+        if (p == rank()) continue;
+        if (r.local) {
+          comm_->send_i32(out_tok_ + off, cnt, p, stream_);
+          comm_->send_f32(out_lp_ + off, cnt, p, stream_);
+          comm_->send_f32(out_ent_ + off, cnt, p, stream_);
+        } else if (p == r.owner) {
+          comm_->recv_i32(out_tok_ + off, cnt, p, stream_);
+          comm_->recv_f32(out_lp_ + off, cnt, p, stream_);
+          comm_->recv_f32(out_ent_ + off, cnt, p, stream_);
+        }
+      }
+    }
+    if (any) comm_->end();
+  }
   std::vector<Req*> done;
   for (const AgentId& id : order_) {
     Req& r = reqs_.at(id);
@@ -460,6 +493,11 @@ GpuMetricQ& GpuEngine::ee_evaluator(int i, int hidden, std::uint64_t seed, doubl
     e = std::make_unique<GpuMetricQ>(hidden, seed, tau, diag, std::max(members, 8), std::max(max_tokens, 512), stream_);
   e->reset(seed, tau, diag);
   return *e;
+}
+
+void GpuEngine::attach_comm(std::unique_ptr<PeerComm> comm) {
+  if (!reqs_.empty()) throw RunError("engine: attach the communicator before adding agents");
+  comm_ = std::move(comm);
 }
 
 void GpuEngine::set_probing(bool on) {

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "common.hpp"
+#include "comm.hpp"
 #include "metricq.hpp"
 #include "model.hpp"
 
@@ -68,7 +69,16 @@ class GpuEngine {
   GpuEngine& operator=(const GpuEngine&) = delete;
 
   // ---- SimWorld protocol ----
-  void add_agent(const AgentId& id, int model);
+  // owner = rank that computes the agent (-1: this rank).  Every rank
+  // registers every agent in the same order (replicated control plane);
+  // only owned agents bind KV and contribute rows to the forwards.
+  void add_agent(const AgentId& id, int model, int owner = -1);
+  // Tree-partitioned serving: chunks of an agent's output are sent by its
+  // owner to every other rank (NCCL P2P) into the same output-cache slots.
+  void attach_comm(std::unique_ptr<PeerComm> comm);
+  int rank() const { return comm_ ? comm_->rank() : 0; }
+  int world() const { return comm_ ? comm_->world() : 1; }
+  bool is_local(const AgentId& id) const { return req(id).local; }
   void submit_prefill_only(const AgentId& id, int expected_start, const TokenSeq& tokens);
   void submit_generate(const AgentId& id, const TokenSeq& full_prompt, int max_new, int apc_chunk,
                        int prefill_chunk = 0);
@@ -137,7 +147,8 @@ class GpuEngine {
   };
   struct Req {
     AgentId id;
-    int model = 0, slot = 0, kv = 0;
+    int model = 0, slot = 0, kv = 0, owner = 0;
+    bool local = true;
     TokenSeq prompt;
     int prefilled = 0, max_computed = 0;
     std::uint64_t gen = 0;
@@ -155,6 +166,7 @@ class GpuEngine {
                           const std::vector<int>& lout);
 
   EngineOptions opt_;
+  std::unique_ptr<PeerComm> comm_;
   cudaStream_t stream_ = nullptr;
   std::vector<std::unique_ptr<DeviceModel>> models_;
   std::map<AgentId, Req> reqs_;

@@ -24,6 +24,16 @@ void RunConfig::validate() const {  // orchestrator.cpp:21-62
     }
 }
 
+std::map<AgentId, int> tree_placement(const Topology& topo, int world) {
+  std::map<AgentId, int> at;
+  const auto& leaves = topo.layers().front();
+  const int n = static_cast<int>(leaves.size());
+  for (int i = 0; i < n; ++i) at[leaves[static_cast<std::size_t>(i)]] = static_cast<int>((1LL * i * world) / n);
+  for (std::size_t l = 1; l < topo.layers().size(); ++l)
+    for (const AgentId& a : topo.layers()[l]) at[a] = at.at(topo.precursors(a).front());
+  return at;
+}
+
 namespace {
 
 bool incremental(ScheduleMode m) { return m == ScheduleMode::IncrementalOverlap; }
@@ -33,16 +43,16 @@ class Driver {
  public:
   Driver(GpuEngine& eng, ScheduleMode mode, int chunk) : eng_(eng), mode_(mode), chunk_(chunk) {}
 
-  void add_source(const AgentId& a, int model, TokenSeq prompt, int n) {
-    eng_.add_agent(a, model);
+  void add_source(const AgentId& a, int model, int owner, TokenSeq prompt, int n) {
+    eng_.add_agent(a, model, owner);
     order_.push_back(a);
     dependent_[a] = false;
     out_len_[a] = n;
     plans_.emplace(a, SlotPlan(a, PromptTemplate(std::move(prompt), {}, {}), false));
   }
 
-  void add_plan(const AgentId& a, int model, PromptTemplate tmpl, int n) {
-    eng_.add_agent(a, model);
+  void add_plan(const AgentId& a, int model, int owner, PromptTemplate tmpl, int n) {
+    eng_.add_agent(a, model, owner);
     order_.push_back(a);
     dependent_[a] = !tmpl.slots().empty();
     out_len_[a] = n;
@@ -137,6 +147,7 @@ QueryResult run_query(GpuEngine& eng, const RunConfig& cfg, int sample, bool res
   const std::uint64_t ss = rng::hash_combine(cfg.seed, static_cast<std::uint64_t>(sample));
   eng.reset();
   Driver drv(eng, cfg.mode, cfg.chunk_size);
+  const std::map<AgentId, int> owner = tree_placement(topo, eng.world());
 
   // prompt synthesis + registration (orchestrator.cpp:151-191)
   const TokenSeq query = rng::synth_tokens(ss, "query", cfg.query_tokens);
@@ -153,7 +164,7 @@ QueryResult run_query(GpuEngine& eng, const RunConfig& cfg, int sample, bool res
       if (topo.precursors(a).empty()) {
         TokenSeq prompt = rng::synth_tokens(ss, "leaf_prefix:" + a.str(), cfg.leaf_prefix_tokens);
         prompt.insert(prompt.end(), query.begin(), query.end());
-        drv.add_source(a, cfg.model_of.at(a), std::move(prompt), n);
+        drv.add_source(a, cfg.model_of.at(a), owner.at(a), std::move(prompt), n);
       } else {
         std::vector<Slot> slots;
         const auto& pre = topo.precursors(a);
@@ -162,7 +173,7 @@ QueryResult run_query(GpuEngine& eng, const RunConfig& cfg, int sample, bool res
                                                          cfg.separator_tokens)});
         PromptTemplate tmpl(rng::synth_tokens(ss, "agg_prefix:" + a.str(), cfg.agg_prefix_tokens), std::move(slots),
                             rng::synth_tokens(ss, "suffix:" + a.str(), cfg.suffix_tokens));
-        drv.add_plan(a, cfg.model_of.at(a), std::move(tmpl), n);
+        drv.add_plan(a, cfg.model_of.at(a), owner.at(a), std::move(tmpl), n);
       }
     }
 

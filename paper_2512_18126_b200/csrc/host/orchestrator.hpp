@@ -72,6 +72,13 @@ struct QueryResult {
   double host_ms = 0.0;  // host time inside engine ticks
 };
 
+// GPU placement along the tree: leaves are spread in
+// contiguous blocks over the ranks (so a cluster's leaves share a rank when
+// there are fewer ranks than leaves, and each gets its own when there are
+// enough); every dependent agent runs on the rank of its first precursor (the
+// cluster aggregator sits with its cluster's first leaf, the root on rank 0).
+std::map<AgentId, int> tree_placement(const Topology& topo, int world);
+
 // One orchestrated request on `eng` (which must hold every model the config
 // names).  `resolve` = copy literal prompts/outputs back to the host.
 QueryResult run_query(GpuEngine& eng, const RunConfig& cfg, int sample, bool resolve = true);
