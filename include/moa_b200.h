@@ -82,6 +82,14 @@ int moa_engine_probe_stats(moa_engine* eng, int kind, int* launches, double* ms,
  * owner to the other ranks with NCCL P2P. */
 int moa_nccl_unique_id(uint8_t* out /* 128 bytes */);
 int moa_engine_attach_comm(moa_engine* eng, const uint8_t* id /* 128 bytes */, int rank, int world);
+/* Same protocol for several engines inside ONE process (one thread per
+ * engine, any devices -- the same GPU included, which NCCL refuses): a hub
+ * joins `world` engines, chunk payloads move by device-to-device copy.  Used
+ * to run the partitioned engine on a single-GPU box. */
+typedef struct moa_loopback moa_loopback;
+int moa_loopback_create(int world, moa_loopback** out);
+int moa_loopback_destroy(moa_loopback* hub);
+int moa_engine_attach_loopback(moa_engine* eng, moa_loopback* hub, int rank);
 /* ranks[k] = owning rank of agent k (layer-major order) for `world` GPUs. */
 int moa_placement(int kind, int n_layers, const int* widths, const int* cluster_sizes, int world, int* ranks);
 

@@ -95,6 +95,9 @@ _SIGS = {
     "moa_engine_reset": ([C.c_void_p], C.c_int),
     "moa_nccl_unique_id": ([_P(C.c_uint8)], C.c_int),
     "moa_engine_attach_comm": ([C.c_void_p, _P(C.c_uint8), C.c_int, C.c_int], C.c_int),
+    "moa_loopback_create": ([C.c_int, _P(C.c_void_p)], C.c_int),
+    "moa_loopback_destroy": ([C.c_void_p], C.c_int),
+    "moa_engine_attach_loopback": ([C.c_void_p, C.c_void_p, C.c_int], C.c_int),
     "moa_placement": ([C.c_int, C.c_int, _P(C.c_int), _P(C.c_int), C.c_int, _P(C.c_int)], C.c_int),
     "moa_engine_probe": ([C.c_void_p, C.c_int], C.c_int),
     "moa_engine_probe_stats": ([C.c_void_p, C.c_int, _P(C.c_int), _P(C.c_double), _P(C.c_double)], C.c_int),
@@ -256,6 +259,11 @@ class Engine:
         buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
         check(lib().moa_engine_attach_comm(self.h, buf, rank, world))
 
+    def attach_loopback(self, hub: "LoopbackHub", rank: int):
+        """Join an in-process partitioned group (one thread per engine)."""
+        check(lib().moa_engine_attach_loopback(self.h, hub.h, rank))
+        self._hub = hub  # keep the hub alive as long as the engine
+
     PROBE_KINDS = ("embed", "qkv", "attention", "o_proj", "gate_up", "down", "lm_head")
 
     def probe(self, enable: bool):
@@ -396,6 +404,20 @@ def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     check(lib().moa_nccl_unique_id(buf))
     return bytes(buf)
+
+
+class LoopbackHub:
+    """In-process stand-in for the NCCL group (see include/moa_b200.h)."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        check(lib().moa_loopback_create(world, C.byref(h)))
+        self.h, self.world = h, world
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            lib().moa_loopback_destroy(self.h)
+            self.h = None
 
 
 def placement(topology: dict, world: int) -> dict:

@@ -193,7 +193,7 @@ int moa_engine_reset(moa_engine* eng) {
 int moa_nccl_unique_id(uint8_t* out) {
   return guard([&] {
     need(out, "out");
-    moa::PeerComm::unique_id(out);
+    moa::NcclComm::unique_id(out);
   });
 }
 
@@ -202,7 +202,32 @@ int moa_engine_attach_comm(moa_engine* eng, const uint8_t* id, int rank, int wor
     need(id, "id");
     moa::GpuEngine& g = E(eng);
     MOA_CUDA(cudaSetDevice(g.device()));
-    g.attach_comm(std::make_unique<moa::PeerComm>(id, rank, world));
+    g.attach_comm(std::make_unique<moa::NcclComm>(id, rank, world));
+  });
+}
+
+struct moa_loopback {
+  std::shared_ptr<moa::LoopbackHub> hub;
+};
+
+int moa_loopback_create(int world, moa_loopback** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = new moa_loopback{std::make_shared<moa::LoopbackHub>(world)};
+  });
+}
+
+int moa_loopback_destroy(moa_loopback* hub) {
+  delete hub;
+  return 0;
+}
+
+int moa_engine_attach_loopback(moa_engine* eng, moa_loopback* hub, int rank) {
+  return guard([&] {
+    need(hub, "hub");
+    moa::GpuEngine& g = E(eng);
+    MOA_CUDA(cudaSetDevice(g.device()));
+    g.attach_comm(std::make_unique<moa::LoopbackComm>(hub->hub, rank));
   });
 }
 

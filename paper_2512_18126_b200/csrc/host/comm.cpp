@@ -55,37 +55,113 @@ void check(ncclResult r, const char* what) {
 
 }  // namespace
 
-void PeerComm::unique_id(std::uint8_t* out) {
+PeerComm::PeerComm(int rank, int world) : rank_(rank), world_(world) {
+  if (world < 1 || rank < 0 || rank >= world) throw ValidationError("comm: rank must be in [0, world)");
+}
+
+// ---- NCCL ----
+
+void NcclComm::unique_id(std::uint8_t* out) {
   NcclId id;
   check(nccl().get_unique_id(&id), "ncclGetUniqueId");
   for (int i = 0; i < kNcclIdBytes; ++i) out[i] = static_cast<std::uint8_t>(id.internal[i]);
 }
 
-PeerComm::PeerComm(const std::uint8_t* id, int rank, int world) : rank_(rank), world_(world) {
-  if (world < 1 || rank < 0 || rank >= world) throw ValidationError("comm: rank must be in [0, world)");
+NcclComm::NcclComm(const std::uint8_t* id, int rank, int world) : PeerComm(rank, world) {
   NcclId nid;
   for (int i = 0; i < kNcclIdBytes; ++i) nid.internal[i] = static_cast<char>(id[i]);
   check(nccl().comm_init_rank(&comm_, world, nid, rank), "ncclCommInitRank");
 }
 
-PeerComm::~PeerComm() {
+NcclComm::~NcclComm() {
   if (comm_) nccl().comm_destroy(comm_);
 }
 
-void PeerComm::begin() { check(nccl().group_start(), "ncclGroupStart"); }
-void PeerComm::end() { check(nccl().group_end(), "ncclGroupEnd"); }
+void NcclComm::begin() { check(nccl().group_start(), "ncclGroupStart"); }
+void NcclComm::end() { check(nccl().group_end(), "ncclGroupEnd"); }
 
-void PeerComm::send_i32(const int* buf, long long n, int peer, cudaStream_t st) {
-  check(nccl().send(buf, static_cast<std::size_t>(n), kNcclInt32, peer, comm_, st), "ncclSend");
+namespace {
+int nccl_type(int elem) { return elem == PeerComm::kI32 ? kNcclInt32 : kNcclFloat32; }
+}  // namespace
+
+void NcclComm::send(const void* buf, long long bytes, int elem, int peer, cudaStream_t st) {
+  check(nccl().send(buf, static_cast<std::size_t>(bytes / 4), nccl_type(elem), peer, comm_, st), "ncclSend");
 }
-void PeerComm::recv_i32(int* buf, long long n, int peer, cudaStream_t st) {
-  check(nccl().recv(buf, static_cast<std::size_t>(n), kNcclInt32, peer, comm_, st), "ncclRecv");
+void NcclComm::recv(void* buf, long long bytes, int elem, int peer, cudaStream_t st) {
+  check(nccl().recv(buf, static_cast<std::size_t>(bytes / 4), nccl_type(elem), peer, comm_, st), "ncclRecv");
 }
-void PeerComm::send_f32(const float* buf, long long n, int peer, cudaStream_t st) {
-  check(nccl().send(buf, static_cast<std::size_t>(n), kNcclFloat32, peer, comm_, st), "ncclSend");
+
+// ---- in-process loopback ----
+
+LoopbackHub::LoopbackHub(int world)
+    : world_(world), q_(static_cast<std::size_t>(world) * world), head_(static_cast<std::size_t>(world) * world, 0) {
+  if (world < 1) throw ValidationError("loopback: world must be >= 1");
 }
-void PeerComm::recv_f32(float* buf, long long n, int peer, cudaStream_t st) {
-  check(nccl().recv(buf, static_cast<std::size_t>(n), kNcclFloat32, peer, comm_, st), "ncclRecv");
+
+void LoopbackHub::barrier() {
+  std::unique_lock<std::mutex> lk(mu_);
+  const long long gen = generation_;
+  if (++arrived_ == world_) {
+    arrived_ = 0;
+    ++generation_;
+    cv_.notify_all();
+  } else {
+    cv_.wait(lk, [&] { return generation_ != gen; });
+  }
+}
+
+void LoopbackHub::post(int from, int to, const Msg& m) {
+  std::lock_guard<std::mutex> lk(mu_);
+  q_[static_cast<std::size_t>(from) * world_ + to].push_back(m);
+}
+
+LoopbackHub::Msg LoopbackHub::take(int from, int to) {
+  std::lock_guard<std::mutex> lk(mu_);
+  const std::size_t k = static_cast<std::size_t>(from) * world_ + to;
+  if (head_[k] >= q_[k].size()) throw RunError("loopback: receive without a matching send");
+  Msg m = q_[k][head_[k]++];
+  if (head_[k] == q_[k].size()) {
+    q_[k].clear();
+    head_[k] = 0;
+  }
+  return m;
+}
+
+LoopbackComm::LoopbackComm(std::shared_ptr<LoopbackHub> hub, int rank)
+    : PeerComm(rank, hub->world()), hub_(std::move(hub)) {}
+
+void LoopbackComm::begin() {
+  if (open_) throw RunError("loopback: nested group");
+  open_ = true;
+  recvs_.clear();
+  streams_.clear();
+}
+
+void LoopbackComm::send(const void* buf, long long bytes, int elem, int peer, cudaStream_t st) {
+  streams_.push_back(st);
+  hub_->post(rank(), peer, {buf, bytes, elem});
+}
+
+void LoopbackComm::recv(void* buf, long long bytes, int elem, int peer, cudaStream_t st) {
+  streams_.push_back(st);
+  recvs_.push_back({buf, bytes, elem, peer});
+}
+
+// Every rank of the group calls end() (as with NCCL, where a rank with
+// nothing to exchange this tick simply issues no group -- here too: ranks
+// exchange only in ticks where some chunk completes, which the replicated
+// schedule makes identical on every rank).
+void LoopbackComm::end() {
+  if (!open_) throw RunError("loopback: end without begin");
+  open_ = false;
+  for (cudaStream_t st : streams_) MOA_CUDA(cudaStreamSynchronize(st));  // send buffers final
+  hub_->barrier();                                                      // all sends posted
+  for (const Recv& r : recvs_) {
+    const LoopbackHub::Msg m = hub_->take(r.peer, rank());
+    if (m.bytes != r.bytes || m.elem != r.elem) throw RunError("loopback: send / receive size or type mismatch");
+    MOA_CUDA(cudaMemcpy(r.dst, m.src, static_cast<std::size_t>(r.bytes), cudaMemcpyDefault));
+  }
+  hub_->barrier();  // senders may reuse their buffers
 }
 
 }  // namespace moa

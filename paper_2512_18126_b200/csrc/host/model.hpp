@@ -19,7 +19,9 @@
 namespace moa {
 
 void cuda_check(cudaError_t e, const char* what);
+#ifndef MOA_CUDA
 #define MOA_CUDA(x) ::moa::cuda_check((x), #x)
+#endif
 
 struct ModelSpec {
   std::string tag;

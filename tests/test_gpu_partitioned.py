@@ -1,0 +1,80 @@
+"""Tree-partitioned engine on ONE GPU: two or three engines in
+one process, one thread each, joined by the in-process loopback hub -- the
+same per-tick message sequence the engine issues to NCCL across GPUs.  With
+the batch-invariant GEMV path (gemv_only) every agent's tokens and logprobs do
+not depend on which rows share its forward, so each rank must reproduce the
+single-engine run bit for bit: outputs, schedule and MetricQ decisions."""
+import threading
+
+import pytest
+
+from paper_2512_18126_b200 import capi
+from paper_2512_18126_b200.configs import C0, C1U
+
+pytestmark = pytest.mark.gpu
+
+
+def _single(cfg, sample):
+    eng, qc = capi.engine_for(cfg, gemv_only=True)
+    try:
+        return eng.run_query(qc, sample=sample)
+    finally:
+        eng.close()
+
+
+def _partitioned(cfg, sample, world):
+    hub = capi.LoopbackHub(world)
+    engs = []
+    for r in range(world):
+        eng, qc = capi.engine_for(cfg, gemv_only=True)
+        eng.attach_loopback(hub, r)
+        engs.append(eng)
+    out, err = [None] * world, []
+
+    def run(r):
+        try:
+            out[r] = engs[r].run_query(qc, sample=sample)
+        except Exception as e:  # surfaced below
+            err.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in th), "partitioned run hung"
+    for e in engs:
+        e.close()
+    if err:
+        raise err[0]
+    return out
+
+
+TREE9 = dict(kind="tree", widths=[9, 3, 1], branching=[3, 3])
+
+
+@pytest.mark.parametrize("name,cfg,sample,world", [
+    ("C0", dict(C0), 0, 2),
+    ("C1U", dict(C1U), 3, 2),
+    ("C1U-w3", dict(C1U), 0, 3),
+    ("T931-ee", dict(C1U, topology=TREE9, out_len=[[16, 64], 32, 32]), 1, 2),
+])
+def test_partitioned_engine_matches_single(name, cfg, sample, world):
+    single = _single(cfg, sample)
+    owner = capi.placement(cfg["topology"], world)
+    assert len(set(owner.values())) == world
+    for rank, o in enumerate(_partitioned(cfg, sample, world)):
+        assert o["tokens"] == single["tokens"], (name, rank)
+        assert [(m["completed"], m["evaluated"], m["q"], m["exited"], m["pruned"]) for m in o["metricq"]] == \
+               [(m["completed"], m["evaluated"], m["q"], m["exited"], m["pruned"]) for m in single["metricq"]]
+        for k, a in single["agents"].items():
+            b = o["agents"][k]
+            for f in ("prompt", "complete", "decode_start", "pruned", "output_tokens", "prefill_only_calls",
+                      "recomputed_tokens"):
+                assert b[f] == a[f], (name, rank, k, f)
+            n = len(a["output"])
+            if a["pruned"] and owner[k] != rank:
+                # a remote agent cut mid-chunk is known up to its last hand-off
+                n = (n // cfg["chunk_size"]) * cfg["chunk_size"]
+            assert b["output"][:n] == a["output"][:n], (name, rank, k)
+            assert b["logprobs"][:n] == a["logprobs"][:n], (name, rank, k)
