@@ -170,6 +170,7 @@ def reference_simulator_time(cfg, reps=24):
 def run_reference_arm(args, cfg, rank, world):
     if rank != 0:
         return
+    tree = world > 1 and args.placement == "tree"
     steps = []
     from oracle.configs import models_of, run_config
     from oracle.orchestrator import run_query

@@ -70,9 +70,15 @@ int moa_engine_destroy(moa_engine* eng);
 int moa_engine_reset(moa_engine* eng);
 /* Kernel probes: CUDA events around every forward kernel (graphs bypassed)
  * with each launch's algorithmic bytes.  kind: 0 embed, 1 qkv, 2 attention,
- * 3 o-proj, 4 gate/up, 5 down, 6 lm-head. */
+ * 3 o-proj, 4 gate/up, 5 down, 6 lm-head, 7 persistent decode forward. */
 int moa_engine_probe(moa_engine* eng, int enable);
 int moa_engine_probe_stats(moa_engine* eng, int kind, int* launches, double* ms, double* bytes);
+/* Persistent decode forward of model `model`: enable (1) / disable (0) it, and
+ * optionally a %globaltimer trace of its phases (8 stamps per phase per CTA;
+ * *n receives phases * grid * 8; the last forward's stamps are copied to out
+ * when out != NULL and cap suffices). */
+int moa_engine_megakernel(moa_engine* eng, int model, int enable, int trace);
+int moa_engine_mk_trace(moa_engine* eng, int model, uint64_t* out, long long cap, long long* n);
 
 /* ---- tree-partitioned serving over several GPUs (one process per GPU) ----
  * Rank 0 creates the id, the caller broadcasts it (e.g. torch.distributed),
@@ -234,6 +240,7 @@ int moa_k_gemv(uintptr_t A, uintptr_t X, int R, uintptr_t W, int N, int K, uintp
 int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
 /* Decode GEMV on the tensor cores (swap-AB, split-K): out[R][N] fp32 =
  * A[R][K] . W[N][K]^T for R <= 16; A must have >= 16 allocated rows. */
+int moa_k_debug_trace(uintptr_t buf); /* debug: gemv_tc per-CTA %globaltimer stamps, 0 = off */
 int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
 /* Hash-uniform weight init of a logical [rows][cols] tensor into a device row
  * layout (0 identity, 1 RoPE-pair interleave per hd rows, 2 even rows, 3 odd rows). */

@@ -99,7 +99,10 @@ _SIGS = {
     "moa_loopback_destroy": ([C.c_void_p], C.c_int),
     "moa_engine_attach_loopback": ([C.c_void_p, C.c_void_p, C.c_int], C.c_int),
     "moa_placement": ([C.c_int, C.c_int, _P(C.c_int), _P(C.c_int), C.c_int, _P(C.c_int)], C.c_int),
+    "moa_k_debug_trace": ([C.c_size_t], C.c_int),
     "moa_engine_probe": ([C.c_void_p, C.c_int], C.c_int),
+    "moa_engine_megakernel": ([C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
+    "moa_engine_mk_trace": ([C.c_void_p, C.c_int, _P(C.c_uint64), C.c_longlong, _P(C.c_longlong)], C.c_int),
     "moa_engine_probe_stats": ([C.c_void_p, C.c_int, _P(C.c_int), _P(C.c_double), _P(C.c_double)], C.c_int),
     "moa_add_agent": ([C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
     "moa_prefill_only": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_int32), C.c_int], C.c_int),
@@ -264,10 +267,22 @@ class Engine:
         check(lib().moa_engine_attach_loopback(self.h, hub.h, rank))
         self._hub = hub  # keep the hub alive as long as the engine
 
-    PROBE_KINDS = ("embed", "qkv", "attention", "o_proj", "gate_up", "down", "lm_head")
+    PROBE_KINDS = ("embed", "qkv", "attention", "o_proj", "gate_up", "down", "lm_head", "decode_mk")
 
     def probe(self, enable: bool):
         check(lib().moa_engine_probe(self.h, int(enable)))
+
+    def megakernel(self, model: int, enable: bool = True, trace: bool = False):
+        check(lib().moa_engine_megakernel(self.h, model, int(enable), int(trace)))
+
+    def mk_trace(self, model: int):
+        """Last persistent-forward trace of `model`: uint64 [phases][grid][8] %globaltimer ns."""
+        import numpy as np
+        n = C.c_longlong()
+        check(lib().moa_engine_mk_trace(self.h, model, None, 0, C.byref(n)))
+        buf = np.zeros(n.value, dtype=np.uint64)
+        check(lib().moa_engine_mk_trace(self.h, model, buf.ctypes.data_as(_P(C.c_uint64)), n.value, C.byref(n)))
+        return buf
 
     def probe_stats(self):
         out = {}

@@ -247,6 +247,24 @@ int moa_engine_probe(moa_engine* eng, int enable) {
   return guard([&] { E(eng).set_probing(enable != 0); });
 }
 
+int moa_engine_megakernel(moa_engine* eng, int model, int enable, int trace) {
+  return guard([&] {
+    if (model < 0 || model >= E(eng).n_models()) throw moa::ValidationError("engine: model index out of range");
+    MOA_CUDA(cudaStreamSynchronize(E(eng).stream()));
+    E(eng).model(model).set_megakernel(enable != 0);
+    E(eng).model(model).set_mk_trace(trace != 0);
+  });
+}
+
+int moa_engine_mk_trace(moa_engine* eng, int model, uint64_t* out, long long cap, long long* n) {
+  return guard([&] {
+    need(n, "n");
+    if (model < 0 || model >= E(eng).n_models()) throw moa::ValidationError("engine: model index out of range");
+    MOA_CUDA(cudaStreamSynchronize(E(eng).stream()));
+    *n = E(eng).model(model).mk_trace_copy(reinterpret_cast<unsigned long long*>(out), cap);
+  });
+}
+
 int moa_engine_probe_stats(moa_engine* eng, int kind, int* launches, double* ms, double* bytes) {
   return guard([&] {
     need(launches, "launches");
@@ -642,6 +660,10 @@ int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, 
     moa::k::gemm_tc(ma, mw, a, reinterpret_cast<cudaStream_t>(stream));
     MOA_CUDA(cudaGetLastError());
   });
+}
+
+int moa_k_debug_trace(uintptr_t buf) {
+  return guard([&] { moa::k::gemv_tc_debug_trace(reinterpret_cast<unsigned long long*>(buf)); });
 }
 
 int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream) {

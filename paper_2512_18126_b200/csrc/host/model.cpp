@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 namespace moa {
 
@@ -56,6 +57,7 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
     : spec_(spec), max_agents_(max_agents), max_ctx_(max_ctx), max_rows_(max_rows), max_lrows_(max_logit_rows),
       use_graphs_(use_graphs) {
   spec_.validate();
+  if (max_ctx > 8192) throw ValidationError("model " + spec.tag + ": max_ctx above 8192 is not supported");
   const ModelSpec& s = spec_;
   const long long D = s.d, hd = s.head_dim, V = s.vocab;
   dev_alloc(&wbase_, s.weight_elems());
@@ -149,6 +151,57 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
     ws = std::max(ws, k::gemv_tc_ws_floats(n, kk));
   dev_alloc(&gv_ws_, ws);
   dev_alloc(&gv_cnt_, (std::max({s.qkv_cols(), 2 * s.ffn, s.d}) + 127) / 128);
+  // persistent decode forward: tensor maps in device memory + its scratch
+  mk_ok_ = tc_ok_ && k::decode_mk_supported(D, s.n_heads, s.n_kv_heads, hd, s.ffn) && max_rows >= k::kMkRows;
+  if (mk_ok_) {
+    int dev = 0;
+    MOA_CUDA(cudaGetDevice(&dev));
+    MOA_CUDA(cudaDeviceGetAttribute(&mk_grid_, cudaDevAttrMultiProcessorCount, dev));
+    std::vector<k::TmaMap> maps;
+    for (const LayerMaps& m : wmaps_) {
+      maps.push_back(m.wqkv);
+      maps.push_back(m.wo);
+      maps.push_back(m.wgu);
+      maps.push_back(m.wd);
+    }
+    maps.push_back(wmap_lm_);
+    MOA_CUDA(cudaMalloc(&mk_maps_, sizeof(k::TmaMap) * maps.size()));
+    MOA_CUDA(cudaMemcpyAsync(mk_maps_, maps.data(), sizeof(k::TmaMap) * maps.size(), cudaMemcpyHostToDevice, st));
+    const int R = k::kMkRows;
+    dev_alloc(&mk_ssq_, static_cast<long long>(R) * (D / 128));
+    dev_alloc(&mk_ws_, k::decode_mk_ws_floats(mk_grid_));
+    const int max_tiles = (std::max({s.vocab, 2 * s.ffn, s.qkv_cols(), s.d}) + 127) / 128;
+    dev_alloc(&mk_cnt_, max_tiles);
+    MOA_CUDA(cudaMemsetAsync(mk_cnt_, 0, sizeof(int) * max_tiles, st));
+    mk_attn_splits_ = k::decode_mk_attn_splits(hd, max_ctx);
+    dev_alloc(&mk_attn_ws_, static_cast<long long>(R) * s.n_heads * mk_attn_splits_ * (2 + hd));
+    dev_alloc(&mk_attn_cnt_, static_cast<long long>(R) * s.n_kv_heads);
+    MOA_CUDA(cudaMemsetAsync(mk_attn_cnt_, 0, sizeof(int) * R * s.n_kv_heads, st));
+    dev_alloc(&mk_lm_part_, static_cast<long long>(R) * ((s.vocab + 127) / 128));
+    dev_alloc(&mk_lm_cnt_, 1);
+    MOA_CUDA(cudaMemsetAsync(mk_lm_cnt_, 0, sizeof(int), st));
+    dev_alloc(&mk_gbar_, 2);
+    MOA_CUDA(cudaMemsetAsync(mk_gbar_, 0, sizeof(unsigned) * 2, st));
+    k::MkParams pp;
+    pp.L = s.n_layers;
+    pp.D = s.d;
+    pp.nh = s.n_heads;
+    pp.nkv = s.n_kv_heads;
+    pp.hd = s.head_dim;
+    pp.ffn = s.ffn;
+    pp.V = s.vocab;
+    std::vector<k::MkCtaPlan> plan;
+    mk_ok_ = k::decode_mk_plan(pp, mk_grid_, &plan, &mk_xs_kt_, &mk_stages_, &mk_smem_);
+    if (mk_ok_) {
+      MOA_CUDA(cudaMalloc(&mk_plan_, sizeof(k::MkCtaPlan) * plan.size()));
+      MOA_CUDA(cudaMemcpyAsync(mk_plan_, plan.data(), sizeof(k::MkCtaPlan) * plan.size(), cudaMemcpyHostToDevice, st));
+      MOA_CUDA(cudaStreamSynchronize(st));
+    }
+    if (const char* e = std::getenv("MOA_MK_STAGES")) mk_stages_ = std::min(mk_stages_, std::max(2, std::atoi(e)));
+  }
+  // persistent forward: opt-in (MOA_MK=1) until it beats the per-kernel chain
+  use_mk_ = false;
+  if (const char* e = std::getenv("MOA_MK")) use_mk_ = std::string(e) != "0";
   MOA_CUDA(cudaMemsetAsync(gv_cnt_, 0, sizeof(int) * ((std::max({s.qkv_cols(), 2 * s.ffn, s.d}) + 127) / 128), st));
   MOA_CUDA(cudaGetLastError());
 }
@@ -160,7 +213,10 @@ DeviceModel::~DeviceModel() {
                     static_cast<void*>(h_), static_cast<void*>(q_), static_cast<void*>(attn_ws_),
                     static_cast<void*>(attn_cnt_), static_cast<void*>(part_), static_cast<void*>(lm_cnt_),
                     static_cast<void*>(buf_.rows), static_cast<void*>(buf_.sel), static_cast<void*>(hn_),
-                    static_cast<void*>(gv_ws_), static_cast<void*>(gv_cnt_)})
+                    static_cast<void*>(gv_ws_), static_cast<void*>(gv_cnt_), mk_maps_, static_cast<void*>(mk_ssq_),
+                    static_cast<void*>(mk_ws_), static_cast<void*>(mk_cnt_), static_cast<void*>(mk_attn_ws_),
+                    static_cast<void*>(mk_attn_cnt_), static_cast<void*>(mk_lm_part_), static_cast<void*>(mk_lm_cnt_),
+                    static_cast<void*>(mk_gbar_), static_cast<void*>(mk_trace_), static_cast<void*>(mk_plan_)})
     if (ptr) cudaFree(ptr);
 }
 
@@ -216,7 +272,7 @@ void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int*
     launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st);
     return;
   }
-  const auto key = std::make_tuple(rcap, nsplit, (Rl > 0 ? 1 : 0) | (use_tc_ ? 2 : 0), logits ? 1 : 0);
+  const auto key = std::make_tuple(rcap, nsplit, (Rl > 0 ? 1 : 0) | (use_tc_ ? 2 : 0) | (use_mk_ ? 4 : 0), logits ? 1 : 0);
   auto it = graphs_.find(key);
   if (it == graphs_.end()) {
     cudaGraph_t g = nullptr;
@@ -237,6 +293,10 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   const int D = s.d, hd = s.head_dim, nh = s.n_heads, nkv = s.n_kv_heads;
   const float eps = static_cast<float>(s.norm_eps);
   const int* meta = buf_.sel + 2 * max_lrows_;
+  if (use_mk_ && use_tc_ && mk_ok_ && rcap <= k::kMkRows) {
+    launch_mk(out_tok_read, out_tok, out_lp, out_ent, logits, st);
+    return;
+  }
   // tensor-core path for row buckets >= kTcMinRows (prefill-heavy ticks)
   const bool tc = use_tc_ && tc_ok_ && rcap >= k::kTcMinRows;
   // decode ticks of large models: swap-AB tensor-core GEMV (pure weight stream)
@@ -370,6 +430,84 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     }
     probe_end();
   }
+  MOA_CUDA(cudaGetLastError());
+}
+
+void DeviceModel::graphs_clear() {
+  for (auto& [key, exec] : graphs_) cudaGraphExecDestroy(exec);
+  graphs_.clear();
+}
+
+void DeviceModel::set_mk_trace(bool on) {
+  if (on && !mk_trace_ && mk_ok_) {
+    const long long n = static_cast<long long>(3 + 5 * spec_.n_layers) * mk_grid_ * 8;
+    dev_alloc(&mk_trace_, n);
+    MOA_CUDA(cudaMemset(mk_trace_, 0, sizeof(unsigned long long) * n));
+  } else if (!on && mk_trace_) {
+    cudaFree(mk_trace_);
+    mk_trace_ = nullptr;
+  }
+  graphs_clear();
+}
+
+long long DeviceModel::mk_trace_copy(unsigned long long* out, long long cap) {
+  if (!mk_trace_) return 0;
+  const long long n = static_cast<long long>(3 + 5 * spec_.n_layers) * mk_grid_ * 8;
+  if (out && cap >= n) MOA_CUDA(cudaMemcpy(out, mk_trace_, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
+  return n;
+}
+
+void DeviceModel::launch_mk(const int* out_tok_read, int* out_tok, float* out_lp, float* out_ent, float* logits,
+                            cudaStream_t st) {
+  const ModelSpec& s = spec_;
+  k::MkParams p;
+  p.maps = mk_maps_;
+  p.L = s.n_layers;
+  p.D = s.d;
+  p.nh = s.n_heads;
+  p.nkv = s.n_kv_heads;
+  p.hd = s.head_dim;
+  p.ffn = s.ffn;
+  p.V = s.vocab;
+  p.eps = static_cast<float>(s.norm_eps);
+  p.rows = buf_.rows;
+  p.meta = buf_.sel + 2 * max_lrows_;
+  p.sel = buf_.sel;
+  p.out_idx = buf_.sel + max_lrows_;
+  p.out_tok_read = out_tok_read;
+  p.emb = emb_;
+  p.g = ones_;
+  p.rope = rope_;
+  p.kpool = kpool_;
+  p.vpool = vpool_;
+  p.kv_stride = kv_stride_;
+  p.layer_stride = layer_stride_;
+  p.max_ctx = max_ctx_;
+  p.x = x_;
+  p.ssq = mk_ssq_;
+  p.q = q_;
+  p.o = h_;
+  p.h = h_;
+  p.ws = mk_ws_;
+  p.cnt = mk_cnt_;
+  p.attn_ws = mk_attn_ws_;
+  p.attn_cnt = mk_attn_cnt_;
+  p.attn_nsplit_max = mk_attn_splits_;
+  p.lm_part = mk_lm_part_;
+  p.lm_cnt = mk_lm_cnt_;
+  p.out_tok = out_tok;
+  p.out_lp = out_lp;
+  p.out_ent = out_ent;
+  p.logits = logits;
+  p.gbar = mk_gbar_;
+  p.stages = mk_stages_;
+  p.xs_kt = mk_xs_kt_;
+  p.trace = mk_trace_;
+  p.plan = mk_plan_;
+  const double kv_bytes = 4.0 * static_cast<double>(live_keys_) * s.n_kv_heads * s.head_dim * s.n_layers;
+  if (probes_) probes_->begin(KernelProbes::DecodeMk, weight_bytes() + kv_bytes, st);
+  k::decode_mk(p, mk_grid_, mk_smem_, st);
+  if (probes_) probes_->end(st);
   MOA_CUDA(cudaGetLastError());
 }
 

@@ -46,7 +46,7 @@ struct ForwardBuffers {
 // without graphs and every launch is bracketed by an event pair together with
 // its algorithmic bytes.
 struct KernelProbes {
-  enum Kind { Embed = 0, Qkv, Attention, OProj, GateUp, Down, LmHead, kKinds };
+  enum Kind { Embed = 0, Qkv, Attention, OProj, GateUp, Down, LmHead, DecodeMk, kKinds };
   struct Rec {
     int kind;
     double bytes;
@@ -69,6 +69,13 @@ class DeviceModel {
  public:
   void attach_probes(KernelProbes* p) { probes_ = p; }
   void set_tensor_cores(bool on) { use_tc_ = on; }
+  void set_megakernel(bool on) {
+    use_mk_ = on;
+    graphs_clear();
+  }
+  void set_mk_trace(bool on);
+  long long mk_trace_copy(unsigned long long* out, long long cap);  // entries; copies when out && cap suffices
+  bool megakernel_ready() const { return mk_ok_; }
   bool tensor_cores_ready() const { return tc_ok_; }
   DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int max_rows, int max_logit_rows,
               cudaStream_t st, bool use_graphs = true);
@@ -103,6 +110,24 @@ class DeviceModel {
   bool use_graphs_ = true;
   bool use_tc_ = true;  // tensor-core path for ticks with >= kTcMinRows rows
   bool tc_ok_ = false;
+  // persistent decode forward (decode_mk.cu) for ticks of <= 16 rows
+  bool use_mk_ = true;
+  bool mk_ok_ = false;
+  int mk_grid_ = 0, mk_stages_ = 0, mk_xs_kt_ = 0, mk_smem_ = 0;
+  void* mk_maps_ = nullptr;  // CUtensorMap[4L + 1]
+  float* mk_ssq_ = nullptr;
+  float* mk_ws_ = nullptr;
+  int* mk_cnt_ = nullptr;
+  float* mk_attn_ws_ = nullptr;
+  int* mk_attn_cnt_ = nullptr;
+  int mk_attn_splits_ = 0;
+  k::LmStat* mk_lm_part_ = nullptr;
+  int* mk_lm_cnt_ = nullptr;
+  unsigned* mk_gbar_ = nullptr;
+  unsigned long long* mk_trace_ = nullptr;
+  k::MkCtaPlan* mk_plan_ = nullptr;
+  void graphs_clear();
+  void launch_mk(const int* out_tok_read, int* out_tok, float* out_lp, float* out_ent, float* logits, cudaStream_t st);
   struct LayerMaps {
     k::TmaMap wqkv, wo, wgu, wd;
   };

@@ -9,10 +9,29 @@
 #include <cfloat>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <set>
 
 #include "kernels.cuh"
 
 namespace moa::k {
+
+// Every forward kernel runs with the maximum shared-memory carveout: when
+// consecutive kernels ask for different L1/shared splits the SM must drain
+// and reconfigure between them, which serialises the chain and defeats
+// programmatic dependent launch.  MOA_CARVEOUT=0 disables (A/B runs).
+void uniform_carveout(const void* fn) {
+  static std::mutex mu;
+  static std::set<const void*> done;
+  static const bool on = [] {
+    const char* e = std::getenv("MOA_CARVEOUT");
+    return !(e && e[0] == '0');
+  }();
+  if (!on) return;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert(fn).second) cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
 
 namespace {
 
@@ -30,6 +49,7 @@ constexpr unsigned kFull = 0xffffffffu;
 
 template <class... KArgs, class... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args&&... args) {
+  uniform_carveout(reinterpret_cast<const void*>(kern));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -447,13 +467,30 @@ attention_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, c
   if (!last) return;
   __threadfence();
   const float* pr = ws + (static_cast<long long>(r) * nh + h) * nsplit_max * (2 + HD);
+  // split statistics loaded in parallel (thread t: split t), then the
+  // weighted sum with every split's partial in flight (fixed split order)
+  __shared__ float sw_s[64];
+  for (int t = threadIdx.x; t < nsplit; t += NW * 32) sw_s[t] = __ldcg(pr + t * (2 + HD));
+  __syncthreads();
   float Mg = -INFINITY;
-  for (int t = 0; t < nsplit; ++t) Mg = fmaxf(Mg, __ldcg(pr + t * (2 + HD)));
+  for (int t = 0; t < nsplit; ++t) Mg = fmaxf(Mg, sw_s[t]);
+  __syncthreads();
+  for (int t = threadIdx.x; t < nsplit; t += NW * 32) sw_s[t] = __expf(sw_s[t] - Mg);
+  __shared__ float sl_s[64];
+  for (int t = threadIdx.x; t < nsplit; t += NW * 32) sl_s[t] = __ldcg(pr + t * (2 + HD) + 1);
+  __syncthreads();
   float Lg = 0.f;
-  for (int t = 0; t < nsplit; ++t) Lg += __expf(__ldcg(pr + t * (2 + HD)) - Mg) * __ldcg(pr + t * (2 + HD) + 1);
+  for (int t = 0; t < nsplit; ++t) Lg += sw_s[t] * sl_s[t];
   for (int e = threadIdx.x; e < HD; e += NW * 32) {
     float val = 0.f;
-    for (int t = 0; t < nsplit; ++t) val += __expf(__ldcg(pr + t * (2 + HD)) - Mg) * __ldcg(pr + t * (2 + HD) + 2 + e);
+    for (int t0 = 0; t0 < nsplit; t0 += 8) {
+      float pv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) pv[u] = t0 + u < nsplit ? __ldcg(pr + (t0 + u) * (2 + HD) + 2 + e) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (t0 + u < nsplit) val += sw_s[t0 + u] * pv[u];
+    }
     orow[e] = __float2bfloat16_rn(val / Lg);
   }
   if (threadIdx.x == 0) cnt[r * nh + h] = 0;

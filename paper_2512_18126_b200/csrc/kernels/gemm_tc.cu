@@ -321,6 +321,7 @@ void gemm_tc(const TmaMap& map_a, const TmaMap& map_w, const GemvArgs& a, cudaSt
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    uniform_carveout(reinterpret_cast<const void*>(gemm_tc_kernel));
     attr = true;
   }
   dim3 grid(a.N / kBN, (a.R + kBM - 1) / kBM);
@@ -340,6 +341,7 @@ void rmsnorm_rows(const float* x, int R_cap, const int* meta, int K, const float
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  uniform_carveout(reinterpret_cast<const void*>(rmsnorm_rows_kernel));
   cudaLaunchKernelEx(&cfg, rmsnorm_rows_kernel, x, sel, meta, meta_idx, K, g, eps, h);
 }
 

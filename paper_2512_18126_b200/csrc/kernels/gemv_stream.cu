@@ -256,6 +256,7 @@ void gemv_stream(const GemvArgs& a, cudaStream_t st) {
   static int attr = 0;  // largest dynamic smem opted in so far
   if (smem > attr) {
     cudaFuncSetAttribute(gemv_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    uniform_carveout(reinterpret_cast<const void*>(gemv_stream_kernel));
     attr = smem;
   }
   const int groups = (a.N + kGroup - 1) / kGroup;

@@ -28,6 +28,20 @@ constexpr int kTileX = kN * kBK * 2;  // 2 KB
 constexpr int kSmem = kStages * (kTileW + kTileX) + 1024 + 256;
 constexpr std::uint32_t kIdesc = idesc_bf16(kM, kN);
 
+// debug: per-CTA %globaltimer stamps (tools/gvisolated.py), off when null
+__device__ unsigned long long* g_gv_trace = nullptr;
+__device__ __forceinline__ void gv_stamp(int ev) {
+  if (g_gv_trace) {
+    unsigned long long t;
+    unsigned smid;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    const long long cta = blockIdx.y * gridDim.x + blockIdx.x;
+    g_gv_trace[cta * 8 + ev] = t;
+    g_gv_trace[cta * 8 + 7] = smid;
+  }
+}
+
 __device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const float (&v)[16]) {
   const int lane = threadIdx.x & 31;
   (void)lane;
@@ -185,11 +199,13 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     mbar_init(done, 1);
     mbar_fence_init();
   }
+  if (threadIdx.x == 0) gv_stamp(0);
   if (warp == 0) tmem_alloc<32>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const std::uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) gv_stamp(1);
 
   if (warp == 0 && lane == 0) {
     // TMA producer.  Weight tiles do not depend on the previous kernel, so
@@ -212,6 +228,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     for (int kt = 0; kt < kt_n; ++kt) {
       const int s = kt % kStages;
       mbar_wait(&full[s], (kt / kStages) & 1);
+      if (kt == 0) gv_stamp(2);
       tc_fence_after();
       const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + s * kTileX);
 #pragma unroll
@@ -225,6 +242,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   mbar_wait(done, 0);
   tc_fence_after();
   pdl_launch_dependents();
+  if (threadIdx.x == 0) gv_stamp(3);
 
   const int R = a.meta ? __ldcg(a.meta) : a.R;
   const int row = warp * 32 + lane, n = m0 + row;
@@ -246,15 +264,27 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
       __threadfence();
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = 0.f;
-      for (int s = 0; s < S; ++s) {
-        const float4* q = reinterpret_cast<const float4*>(ws + ((static_cast<long long>(tile) * S + s) * kM + row) * kN);
+      // all splits' partials in flight per round trip (8 at a time), summed in
+      // split order
+      for (int s0 = 0; s0 < S; s0 += 8) {
+        float4 t[8][4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 t = __ldcg(q + i);
-          v[4 * i] += t.x;
-          v[4 * i + 1] += t.y;
-          v[4 * i + 2] += t.z;
-          v[4 * i + 3] += t.w;
+        for (int u = 0; u < 8; ++u) {
+          if (s0 + u >= S) break;
+          const float4* q = reinterpret_cast<const float4*>(ws + ((static_cast<long long>(tile) * S + s0 + u) * kM + row) * kN);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) t[u][i] = __ldcg(q + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (s0 + u >= S) break;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            v[4 * i] += t[u][i].x;
+            v[4 * i + 1] += t[u][i].y;
+            v[4 * i + 2] += t[u][i].z;
+            v[4 * i + 3] += t[u][i].w;
+          }
         }
       }
       epilogue(a, n, R, v);
@@ -263,10 +293,13 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) gv_stamp(4);
   if (warp == 0) tmem_dealloc<32>(tmem);
 }
 
 }  // namespace
+
+void gemv_tc_debug_trace(unsigned long long* buf) { cudaMemcpyToSymbol(g_gv_trace, &buf, sizeof(buf)); }
 
 int gemv_tc_splits(int N, int K, int epi) {
   const int tiles = (N + kM - 1) / kM, kts = K / kBK;
@@ -288,6 +321,7 @@ void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float*
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    uniform_carveout(reinterpret_cast<const void*>(gemv_tc_kernel));
     attr = true;
   }
   const int S = gemv_tc_splits(a.N, a.K, a.epi);

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -36,6 +37,9 @@ enum RowMap : int {
   kRowsEven = 2,            // r -> 2r     (gate rows)
   kRowsOdd = 3,             // r -> 2r + 1 (up rows)
 };
+
+// Request the maximum shared-memory carveout for a kernel (once per kernel).
+void uniform_carveout(const void* fn);
 
 void init_uniform_rows(bf16* dst, long long rows, long long cols, std::uint64_t base, float scale, int map,
                        int hd, cudaStream_t st);
@@ -113,6 +117,71 @@ bool gemv_tc_supported(const GemvArgs& a);
 int gemv_tc_splits(int N, int K, int epi);
 long long gemv_tc_ws_floats(int N, int K);
 void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float* ws, int* cnt, cudaStream_t st);
+void gemv_tc_debug_trace(unsigned long long* buf);  // per-CTA stamps [cta][8] (debug), nullptr = off
+
+// ---- persistent decode forward (decode_mk.cu): one launch per tick of <= 16
+// rows of a model, one CTA per SM (cooperative launch) ----
+constexpr int kMkRows = 16;
+constexpr int kMkMaxGroupDims = 512;  // (n_heads / n_kv_heads) * head_dim
+constexpr int kMkMaxSeg = 8;          // segments per CTA per GEMV shape
+constexpr int kMkMaxKt = 64;          // staged k-tiles per CTA per GEMV shape
+// One CTA's piece of a GEMV phase inside one 128-row weight tile: k-tiles
+// [k0, k1) of tile t; the CTAs c_first..c_last share the tile (split-K).
+struct MkSeg {
+  int t, k0, k1;
+  int slot_self;   // partial slot this CTA writes (0: first segment of its range, 1: last)
+  int c_first, c_last;
+  int first_slot;  // slot holding c_first's partial of this tile
+  int pad;
+};
+struct alignas(16) MkCtaPlan {
+  int nseg = 0, nkt = 0, pad0 = 0, pad1 = 0;
+  MkSeg seg[kMkMaxSeg];
+  short kt[kMkMaxKt];  // distinct k-tiles to stage, in first-use order
+};
+struct MkParams {
+  const void* maps;  // CUtensorMap[4L + 1] in device memory: per layer wqkv, wo, wgu, wd; then the LM head
+  int L = 0, D = 0, nh = 0, nkv = 0, hd = 0, ffn = 0, V = 0;
+  float eps = 1e-5f;
+  const RowDesc* rows = nullptr;
+  const int* meta = nullptr;     // [R, Rl, max_pos]
+  const int* sel = nullptr;      // logits rows [Rl]
+  const int* out_idx = nullptr;  // flat output index per logits row
+  const int* out_tok_read = nullptr;
+  const bf16* emb = nullptr;
+  const float* g = nullptr;  // norm gains
+  const float2* rope = nullptr;
+  bf16* kpool = nullptr;
+  bf16* vpool = nullptr;
+  long long kv_stride = 0, layer_stride = 0;
+  int max_ctx = 0;
+  float* x = nullptr;    // [16][D] fp32 residual stream
+  float* ssq = nullptr;  // [16][D/128] per-tile row sums of squares
+  bf16* q = nullptr;     // [16][nh*hd]
+  bf16* o = nullptr;     // [16][nh*hd] attention output
+  bf16* h = nullptr;     // [16][ffn] SwiGLU output
+  float* ws = nullptr;   // split-K partials [grid][2][128][16]
+  int* cnt = nullptr;    // [max tiles], zero-initialised once
+  float* attn_ws = nullptr;  // [16][nh][attn_nsplit_max][2 + hd]
+  int* attn_cnt = nullptr;   // [16][nkv], zero-initialised once
+  int attn_nsplit_max = 0;
+  LmStat* lm_part = nullptr;  // [16][ceil(V/128)]
+  int* lm_cnt = nullptr;
+  int* out_tok = nullptr;
+  float* out_lp = nullptr;
+  float* out_ent = nullptr;
+  float* logits = nullptr;
+  unsigned* gbar = nullptr;  // [2], zero-initialised once
+  const MkCtaPlan* plan = nullptr;  // [grid][5] (decode_mk_plan)
+  int stages = 0, xs_kt = 0;  // weight ring depth, activation staging slots (decode_mk_plan)
+  unsigned long long* trace = nullptr;  // optional [phases][grid][8] %globaltimer stamps (tools/mktrace.py)
+};
+long long decode_mk_ws_floats(int grid);
+int decode_mk_attn_splits(int hd, int max_ctx);
+bool decode_mk_supported(int d, int nh, int nkv, int hd, int ffn);
+bool decode_mk_plan(const MkParams& p, int grid, std::vector<MkCtaPlan>* plan, int* xs_kt, int* stages,
+                    int* smem_bytes);
+void decode_mk(const MkParams& p, int grid, int smem_bytes, cudaStream_t st);
 
 // o[r][h] = softmax(q k^T / sqrt(hd)) v over keys [0, pos] of the row's agent;
 // keys split across CTAs (kKvSplit keys each), partials combined in split
