@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(128) rmsnorm_rows_kernel(const float* __restri
                                                            bf16* __restrict__ h) {
   __shared__ float red[4];
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int i = blockIdx.x;
   if (i >= meta[meta_idx]) return;
   const int r = sel ? sel[i] : i;
@@ -263,7 +264,6 @@ __global__ void __launch_bounds__(128) rmsnorm_rows_kernel(const float* __restri
   __syncthreads();
   const float tot = red[0] + red[1] + red[2] + red[3];
   const float inv = 1.0f / sqrtf(tot / static_cast<float>(K) + eps);
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const float4* gr = reinterpret_cast<const float4*>(g);
   for (int v = threadIdx.x; v < K / 8; v += 128) {
     const float4 a = xr[2 * v], b = xr[2 * v + 1];

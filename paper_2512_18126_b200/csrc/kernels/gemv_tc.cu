@@ -12,6 +12,7 @@
 // Epilogues: the GEMV path's (RoPE + KV append, residual, SwiGLU, fp32);
 // RoPE / gate-up partners are adjacent weight rows = adjacent lanes.
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "tc_common.cuh"
@@ -22,7 +23,7 @@ namespace {
 
 using namespace tc;
 
-constexpr int kM = 128, kN = 16, kBK = 64, kStages = 6;
+constexpr int kM = 128, kN = 16, kBK = 64, kStages = 5;  // 92 KB: two kernels' CTAs co-reside (PDL overlap)
 constexpr int kTileW = kM * kBK * 2;  // 16 KB
 constexpr int kTileX = kN * kBK * 2;  // 2 KB
 constexpr int kSmem = kStages * (kTileW + kTileX) + 1024 + 256;
@@ -34,7 +35,7 @@ __device__ __forceinline__ void gv_stamp(int ev) {
   if (g_gv_trace) {
     unsigned long long t;
     unsigned smid;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    t = clock64();
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
     const long long cta = blockIdx.y * gridDim.x + blockIdx.x;
     g_gv_trace[cta * 8 + ev] = t;
@@ -84,6 +85,22 @@ __device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const 
       }
     }
   }
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ std::uint32_t dsmem_addr(std::uint32_t local, int rank) {
+  std::uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ float4 dsmem_ld4(std::uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ LmStat stat_merge(LmStat a, LmStat b) {
@@ -187,7 +204,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x, split = blockIdx.y;
   const int m0 = tile * kM;
-  const int kt_n = a.K / kBK / S, kt0 = split * kt_n;
+  const int KT = a.K / kBK, kt0 = split * KT / S, kt_n = (split + 1) * KT / S - kt0;
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&map_w);
@@ -200,6 +217,11 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     mbar_fence_init();
   }
   if (threadIdx.x == 0) gv_stamp(0);
+  // Dependents may launch now: they prefetch their own weights while this
+  // grid runs, then wait (griddepcontrol.wait) for its completion before
+  // reading its outputs.  Grids are sized to one CTA per SM, so this grid and
+  // the next fit side by side.
+  pdl_launch_dependents();
   if (warp == 0) tmem_alloc<32>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -241,7 +263,6 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   pdl_wait();  // every epilogue thread reads the previous kernel's outputs (rows, residual)
   mbar_wait(done, 0);
   tc_fence_after();
-  pdl_launch_dependents();
   if (threadIdx.x == 0) gv_stamp(3);
 
   const int R = a.meta ? __ldcg(a.meta) : a.R;
@@ -253,43 +274,50 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   } else if (S == 1) {
     epilogue(a, n, R, v);
   } else {
-    float4* p = reinterpret_cast<float4*>(ws + ((static_cast<long long>(tile) * S + split) * kM + row) * kN);
+    // Split-K inside a thread-block cluster (the S CTAs of this weight tile):
+    // every CTA parks its 128 x 16 partial in its own shared memory (the ring
+    // is idle once the MMAs are done), then CTA q reduces weight rows
+    // [q*128/S, (q+1)*128/S) by reading all S partials over DSMEM in rank
+    // order and runs their epilogue.  No global round trips, deterministic.
+    float4* park = reinterpret_cast<float4*>(smem) + row * 4;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) p[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(cnt + tile, 1) == S - 1;
-    __syncthreads();
-    if (last) {
-      __threadfence();
+    for (int i = 0; i < 4; ++i) park[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    cluster_sync();
+    if (threadIdx.x == 0) gv_stamp(5);
+    const int per = kM / S;  // weight rows reduced by this CTA
+    if (warp * 32 < per) {   // warps holding at least one of them (whole warps: the epilogue shuffles)
+      const bool mine = row < per;
+      const int wr = split * per + (mine ? row : 0);
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = 0.f;
-      // all splits' partials in flight per round trip (8 at a time), summed in
-      // split order
-      for (int s0 = 0; s0 < S; s0 += 8) {
-        float4 t[8][4];
+      if (mine) {
+        const std::uint32_t local = smem_u32(reinterpret_cast<float4*>(smem) + wr * 4);
+        for (int q0 = 0; q0 < S; q0 += 4) {
+          float4 t[4][4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (s0 + u >= S) break;
-          const float4* q = reinterpret_cast<const float4*>(ws + ((static_cast<long long>(tile) * S + s0 + u) * kM + row) * kN);
+          for (int u = 0; u < 4; ++u) {
+            if (q0 + u >= S) break;
+            const std::uint32_t ra = dsmem_addr(local, q0 + u);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) t[u][i] = __ldcg(q + i);
-        }
+            for (int i = 0; i < 4; ++i) t[u][i] = dsmem_ld4(ra + 16 * i);
+          }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (s0 + u >= S) break;
+          for (int u = 0; u < 4; ++u) {
+            if (q0 + u >= S) break;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            v[4 * i] += t[u][i].x;
-            v[4 * i + 1] += t[u][i].y;
-            v[4 * i + 2] += t[u][i].z;
-            v[4 * i + 3] += t[u][i].w;
+            for (int i = 0; i < 4; ++i) {
+              v[4 * i] += t[u][i].x;
+              v[4 * i + 1] += t[u][i].y;
+              v[4 * i + 2] += t[u][i].z;
+              v[4 * i + 3] += t[u][i].w;
+            }
           }
         }
       }
-      epilogue(a, n, R, v);
-      if (threadIdx.x == 0) cnt[tile] = 0;
+      if (threadIdx.x == 0) gv_stamp(6);
+      epilogue(a, mine ? m0 + wr : a.N, R, v);
     }
+    cluster_sync();  // partials stay readable until every CTA of the cluster has reduced
   }
   tc_fence_before();
   __syncthreads();
@@ -301,11 +329,14 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
 
 void gemv_tc_debug_trace(unsigned long long* buf) { cudaMemcpyToSymbol(g_gv_trace, &buf, sizeof(buf)); }
 
+// K splits per weight tile: as many as keep the grid within one CTA per SM
+// (148), at least 4 k-tiles per split (uneven splits allowed; the partials
+// are summed in split order, so the result depends only on (N, K)).
 int gemv_tc_splits(int N, int K, int epi) {
   const int tiles = (N + kM - 1) / kM, kts = K / kBK;
-  int S = 1;
   if (epi == kEpiLmStats) return 1;
-  while (tiles * S * 2 <= 2 * 148 && kts % (S * 2) == 0 && S < 16) S *= 2;
+  int S = 1;  // power of two <= 8 (one cluster per tile), >= 4 k-tiles per split, <= 2 CTAs per SM
+  while (S < 8 && tiles * S * 2 <= 2 * 148 && kts / (S * 2) >= 4) S *= 2;
   return S;
 }
 
@@ -330,11 +361,26 @@ void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float*
   cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr_pdl[1];
-  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr_pdl;
-  cfg.numAttrs = 1;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  static const bool no_pdl = [] {
+    const char* e = std::getenv("MOA_NO_PDL");
+    return e && e[0] == '1';
+  }();
+  if (!no_pdl) {
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (S > 1) {  // the S K-splits of a weight tile form one cluster (DSMEM reduction)
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = 1;
+    attrs[na].val.clusterDim.y = S;
+    attrs[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
   cudaLaunchKernelEx(&cfg, gemv_tc_kernel, *reinterpret_cast<const CUtensorMap*>(&map_w),
                      *reinterpret_cast<const CUtensorMap*>(&map_x), a, S, ws, cnt);
 }

@@ -24,14 +24,20 @@ for (N, K) in ((3072, 2048), (2048, 2048), (16384, 2048), (2048, 8192)):
         torch.cuda.synchronize()
     t = tr.cpu().numpy().reshape(-1, 8)
     t = t[t[:, 0] > 0]
-    base = t[:, 0].min()
-    rel = (t[:, :5] - base) / 1e3
+    # SM cycle counters (not comparable across SMs): intervals relative to each CTA's own start, in us @1.965 GHz
+    rel = np.where(t[:, :7] > 0, (t[:, :7] - t[:, :1]) / 1965.0, np.nan)
     sm = t[:, 7]
     per_sm = np.bincount(sm.astype(np.int64))
     print(f'N={N} K={K} ctas={len(t)} event_ms={e0.elapsed_time(e1):.4f} | start max {rel[:,0].max():.1f} | tmem max {rel[:,1].max():.1f} '
           f'| first tile med {np.median(rel[:,2]):.1f} max {rel[:,2].max():.1f} | mma done med {np.median(rel[:,3]):.1f} max {rel[:,3].max():.1f} '
           f'| end med {np.median(rel[:,4]):.1f} max {rel[:,4].max():.1f} | sms used {np.count_nonzero(per_sm)} max ctas/sm {per_sm.max()}')
-    slow = np.argsort(-rel[:, 4])[:3]
+    last = ~np.isnan(rel[:, 6])
+    print('   nonzero per slot', [(t[:, k] > 0).sum() for k in range(8)])
+    if not last.any():
+        continue
+    med = [np.nanmedian(rel[last][:, k]) for k in (3, 5, 6, 4)]
+    print('   last arrivers: n %d mma done med %.1f atomic-ret med %.1f loads-done med %.1f end med %.1f max %.1f' % (last.sum(), *med, np.nanmax(rel[last][:, 4])))
+    slow = np.argsort(-np.nan_to_num(rel[:, 4]))[:3]
     for i in slow:
         print('   slow cta', i, 'sm', sm[i], 'stamps', np.round(rel[i], 1))
 L.moa_k_debug_trace(0)
