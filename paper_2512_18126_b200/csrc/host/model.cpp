@@ -28,6 +28,7 @@ void ModelSpec::validate() const {
     throw ValidationError("model " + tag + ": dimensions must be positive");
   if (head_dim != 64 && head_dim != 128) throw ValidationError("model " + tag + ": head_dim must be 64 or 128");
   if (n_heads % n_kv_heads) throw ValidationError("model " + tag + ": n_heads % n_kv_heads != 0");
+  if (n_heads / n_kv_heads > 4) throw ValidationError("model " + tag + ": at most 4 query heads per kv head");
   for (int k : {d, n_heads * head_dim, ffn})
     if (k % 256) throw ValidationError("model " + tag + ": GEMM K dims must be multiples of 256");
 }
@@ -123,7 +124,13 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   dev_alloc(&attn_ws_, attn_ws_floats_);
   dev_alloc(&attn_cnt_, static_cast<long long>(max_rows) * s.n_heads);
   MOA_CUDA(cudaMemsetAsync(attn_cnt_, 0, sizeof(int) * max_rows * s.n_heads, st));
-  dev_alloc(&part_, static_cast<long long>(max_logit_rows) * k::lm_head_blocks(s.vocab));
+  {
+    int dev = 0;
+    MOA_CUDA(cudaGetDevice(&dev));
+    MOA_CUDA(cudaDeviceGetAttribute(&lm_grid_, cudaDevAttrMultiProcessorCount, dev));
+  }
+  dev_alloc(&part_, std::max<long long>(static_cast<long long>(max_logit_rows) * k::lm_head_blocks(s.vocab),
+                                        static_cast<long long>(k::kGemvTcRows) * lm_grid_));
   dev_alloc(&lm_cnt_, 1);
   MOA_CUDA(cudaMemsetAsync(lm_cnt_, 0, sizeof(int), st));
   dev_alloc(&buf_.rows, max_rows);
@@ -423,7 +430,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       lm.out_lp = out_lp;
       lm.out_ent = out_ent;
       lm.logits = logits;
-      k::gemv_tc(wmap_lm_, map_hn16_, lm, gv_ws_, gv_cnt_, st);
+      k::lm_head_tc(wmap_lm_, map_hn16_, lm, part_, lm_cnt_, lm_grid_, st);
     } else {
       k::lm_head(x_, buf_.sel, meta, ones_, eps, lm_, s.vocab, D, part_, lm_cnt_, buf_.sel + max_lrows_, out_tok,
                  out_lp, out_ent, logits, st);

@@ -113,6 +113,7 @@ class DeviceModel {
   // persistent decode forward (decode_mk.cu) for ticks of <= 16 rows
   bool use_mk_ = true;
   bool mk_ok_ = false;
+  int lm_grid_ = 148;
   int mk_grid_ = 0, mk_stages_ = 0, mk_xs_kt_ = 0, mk_smem_ = 0;
   void* mk_maps_ = nullptr;  // CUtensorMap[4L + 1]
   float* mk_ssq_ = nullptr;

@@ -128,9 +128,6 @@ __device__ __forceinline__ void mbar_wait_g(std::uint64_t* bar, std::uint32_t pa
   }
 }
 
-__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 

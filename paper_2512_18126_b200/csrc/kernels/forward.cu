@@ -9,6 +9,7 @@
 #include <cfloat>
 #include <climits>
 #include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 #include <mutex>
 #include <set>
@@ -496,6 +497,191 @@ attention_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, c
   if (threadIdx.x == 0) cnt[r * nh + h] = 0;
 }
 
+
+// GQA attention: CTA = (row, kv head, key split of kv_split(hd) keys); the
+// group's q heads (<= 4) share every K/V load.  Warp w takes 32-key chunks
+// w, w+8, ... with an online softmax per head (K: lane = key, full row in
+// registers; V: lane = HD/32 output dims of every key), warps combine in
+// smem in a fixed order; a row whose context spans several CTAs writes
+// per-head partials and the last-arriving CTA combines them in split order.
+template <int HD>
+__global__ void __launch_bounds__(256, 1)
+attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, const int* __restrict__ meta, int nh,
+                     int nkv, const bf16* __restrict__ kpool, const bf16* __restrict__ vpool, long long kv_stride,
+                     long long layer_off, int max_ctx, bf16* __restrict__ o, float* __restrict__ ws,
+                     int* __restrict__ cnt, int nsplit_max, int split_keys) {
+  MOA_PDL_ENTRY();
+  constexpr int NW = 8, HPG = 4, E = HD / 32;
+  __shared__ float qs[HPG][HD];
+  __shared__ float wm[NW][HPG], wl[NW][HPG];
+  __shared__ float wo[NW][HPG][HD];
+  __shared__ float cm_s[HPG], cl_s[HPG];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.x, g = blockIdx.y, s = blockIdx.z;
+  if (r >= __ldg(meta)) return;
+  const RowDesc rd = rows[r];
+  const int n = rd.pos + 1;
+  const int nsplit = (n + split_keys - 1) / split_keys;
+  if (s >= nsplit) return;
+  const int hpg = nh / nkv;
+  const int kb = s * split_keys, ke = min(n, kb + split_keys);
+  const bf16* K = kpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
+  const bf16* V = vpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
+  for (int i = threadIdx.x; i < hpg * HD; i += NW * 32)
+    qs[i / HD][i % HD] = __bfloat162float(q[(static_cast<long long>(r) * nh + g * hpg + i / HD) * HD + i % HD]);
+  __syncthreads();
+  const float scale = rsqrtf(static_cast<float>(HD));
+  float m[HPG], l[HPG], acc[HPG][E];
+#pragma unroll
+  for (int h = 0; h < HPG; ++h) {
+    m[h] = -INFINITY;
+    l[h] = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[h][e] = 0.f;
+  }
+  // TPK lanes per key (64 dims each): KC keys per warp chunk
+  constexpr int TPK = HD / 64, KC = 32 / TPK;
+  const int key = lane / TPK, part = lane % TPK;
+  using VT = typename std::conditional<E == 2, unsigned, uint2>::type;
+  for (int j0 = kb + warp * KC; j0 < ke; j0 += NW * KC) {
+    const int j = j0 + key;
+    uint4 kk[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+      kk[v] = j < ke ? __ldg(reinterpret_cast<const uint4*>(K + static_cast<long long>(j) * HD + part * 64) + v)
+                     : make_uint4(0, 0, 0, 0);
+    VT vv[KC];
+#pragma unroll
+    for (int jj = 0; jj < KC; ++jj)
+      vv[jj] = j0 + jj < ke ? __ldg(reinterpret_cast<const VT*>(V + static_cast<long long>(j0 + jj) * HD + lane * E)) : VT{};
+#pragma unroll
+    for (int h = 0; h < HPG; ++h) {
+      if (h >= hpg) break;
+      float d = 0.f;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        float f[8];
+        unpack8(kk[v], f);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) d = fmaf(qs[h][part * 64 + v * 8 + t], f[t], d);
+      }
+      if constexpr (TPK == 2) d += __shfl_xor_sync(kFull, d, 1);
+      const float sc = j < ke ? d * scale : -INFINITY;
+      float cmax = sc;
+#pragma unroll
+      for (int off = 16; off; off >>= 1) cmax = fmaxf(cmax, __shfl_xor_sync(kFull, cmax, off));
+      const float mn = fmaxf(m[h], cmax);
+      const float resc = m[h] == -INFINITY ? 0.f : __expf(m[h] - mn);
+      const float p = j < ke ? __expf(sc - mn) : 0.f;
+      l[h] = l[h] * resc + warp_sum(part == 0 ? p : 0.f);
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[h][e] *= resc;
+#pragma unroll
+      for (int jj = 0; jj < KC; ++jj) {
+        const float pj = __shfl_sync(kFull, p, jj * TPK);
+        if constexpr (E == 2) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv[jj]));
+          acc[h][0] = fmaf(pj, f.x, acc[h][0]);
+          acc[h][1] = fmaf(pj, f.y, acc[h][1]);
+        } else {
+          const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv[jj].x));
+          const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv[jj].y));
+          acc[h][0] = fmaf(pj, f0.x, acc[h][0]);
+          acc[h][1] = fmaf(pj, f0.y, acc[h][1]);
+          acc[h][2] = fmaf(pj, f1.x, acc[h][2]);
+          acc[h][3] = fmaf(pj, f1.y, acc[h][3]);
+        }
+      }
+      m[h] = mn;
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < HPG; ++h) {
+    if (h >= hpg) break;
+    if (lane == 0) {
+      wm[warp][h] = m[h];
+      wl[warp][h] = l[h];
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) wo[warp][h][lane * E + e] = acc[h][e];
+  }
+  __syncthreads();
+  // CTA combine of the warps, per head, fixed warp order
+  if (threadIdx.x < hpg) {
+    const int h = threadIdx.x;
+    float M = -INFINITY;
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, wm[w][h]);
+    float Lsum = 0.f;
+    for (int w = 0; w < NW; ++w) Lsum += wm[w][h] == -INFINITY ? 0.f : __expf(wm[w][h] - M) * wl[w][h];
+    cm_s[h] = M;
+    cl_s[h] = Lsum;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < hpg * HD; i += NW * 32) {
+    const int h = i / HD, e = i % HD;
+    const float M = cm_s[h];
+    float val = 0.f;
+    for (int w = 0; w < NW; ++w)
+      if (wm[w][h] != -INFINITY) val += __expf(wm[w][h] - M) * wo[w][h][e];
+    const int head = g * hpg + h;
+    if (nsplit == 1) {
+      o[(static_cast<long long>(r) * nh + head) * HD + e] = __float2bfloat16_rn(val / cl_s[h]);
+    } else {
+      float* part = ws + ((static_cast<long long>(r) * nh + head) * nsplit_max + s) * (2 + HD);
+      __stcg(part + 2 + e, val);
+      if (e == 0) {
+        __stcg(part, M);
+        __stcg(part + 1, cl_s[h]);
+      }
+    }
+  }
+  if (nsplit == 1) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned prev;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(cnt + r * nkv + g) : "memory");
+    last = prev == static_cast<unsigned>(nsplit - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  // combine the splits (split order); split stats read in parallel
+  __shared__ float sw_s[HPG][64];
+  for (int i = threadIdx.x; i < hpg * nsplit; i += NW * 32) {
+    const int h = i / nsplit, t = i % nsplit;
+    sw_s[h][t] = __ldcg(ws + ((static_cast<long long>(r) * nh + g * hpg + h) * nsplit_max + t) * (2 + HD));
+  }
+  __syncthreads();
+  if (threadIdx.x < hpg) {
+    const int h = threadIdx.x;
+    float M = -INFINITY;
+    for (int t = 0; t < nsplit; ++t) M = fmaxf(M, sw_s[h][t]);
+    float Lsum = 0.f;
+    for (int t = 0; t < nsplit; ++t) {
+      const float w = __expf(sw_s[h][t] - M);
+      Lsum += w * __ldcg(ws + ((static_cast<long long>(r) * nh + g * hpg + h) * nsplit_max + t) * (2 + HD) + 1);
+      sw_s[h][t] = w;
+    }
+    cl_s[h] = Lsum;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < hpg * HD; i += NW * 32) {
+    const int h = i / HD, e = i % HD;
+    const float* pr = ws + (static_cast<long long>(r) * nh + g * hpg + h) * nsplit_max * (2 + HD);
+    float val = 0.f;
+    for (int t0 = 0; t0 < nsplit; t0 += 8) {
+      float pv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) pv[u] = t0 + u < nsplit ? __ldcg(pr + (t0 + u) * (2 + HD) + 2 + e) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (t0 + u < nsplit) val += sw_s[h][t0 + u] * pv[u];
+    }
+    o[(static_cast<long long>(r) * nh + g * hpg + h) * HD + e] = __float2bfloat16_rn(val / cl_s[h]);
+  }
+  if (threadIdx.x == 0) cnt[r * nkv + g] = 0;
+}
+
 // LM head: block b owns a contiguous vocab slice; warps take 4 columns x 8
 // rows at a time; rows are normalised on the fly.  The last CTA merges all
 // slices per row in slice order and writes token / logprob / entropy.
@@ -663,13 +849,14 @@ void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, co
                float* ws, int* cnt, cudaStream_t st) {
   if (R_cap <= 0) return;
   const int nsplit_max = (max_ctx + kKvSplit - 1) / kKvSplit;
-  dim3 grid(R_cap, nh, nsplit_cap);
+  const int split_keys = kv_split(hd);
+  dim3 grid(R_cap, nkv, nsplit_cap);
   if (hd == 64)
-    launch_pdl(attention_kernel<64, 8>, grid, dim3(256), st, q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx,
-                                               o, ws, cnt, nsplit_max);
+    launch_pdl(attention_gqa_kernel<64>, grid, dim3(256), st, q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off,
+               max_ctx, o, ws, cnt, nsplit_max, split_keys);
   else if (hd == 128)
-    launch_pdl(attention_kernel<128, 4>, grid, dim3(128), st, q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx,
-                                                o, ws, cnt, nsplit_max);
+    launch_pdl(attention_gqa_kernel<128>, grid, dim3(256), st, q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off,
+               max_ctx, o, ws, cnt, nsplit_max, split_keys);
   else
     printf("attention: unsupported head_dim %d\n", hd);
 }

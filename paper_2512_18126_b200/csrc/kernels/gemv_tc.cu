@@ -48,9 +48,10 @@ __device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const 
   (void)lane;
 #pragma unroll
   for (int r = 0; r < kN; ++r) {
+    if (r >= R) break;  // R is CTA-uniform
     const float x = v[r];
     const float partner = __shfl_xor_sync(0xffffffffu, x, 1);  // weight row n ^ 1
-    if (r >= R || n >= a.N) continue;
+    if (n >= a.N) continue;
     switch (a.epi) {
       case kEpiF32:
         a.out[static_cast<long long>(r) * a.N + n] = x;
@@ -136,7 +137,8 @@ __device__ void lm_stats_epilogue(const GemvArgs& a, int n, int R, const float (
   const LmStat none{-INFINITY, 0.f, 0.f, 0x7fffffff};
 #pragma unroll
   for (int r = 0; r < kN; ++r) {
-    const bool ok = r < R && n < a.N;
+    if (r >= R) break;  // R is CTA-uniform: no work (and no shuffles) for absent rows
+    const bool ok = n < a.N;
     if (ok && a.logits) a.logits[static_cast<long long>(r) * a.N + n] = v[r];
     LmStat st = ok ? LmStat{v[r], 1.f, 0.f, n} : none;
 #pragma unroll
@@ -325,7 +327,218 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   if (warp == 0) tmem_dealloc<32>(tmem);
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent LM head (greedy statistics), one CTA per SM.  CTA c owns the
+// contiguous vocab tiles [c*T/G, (c+1)*T/G); the weight/activation ring runs
+// across its tiles without a break (the next tile's tiles stream while the
+// current one's epilogue runs: accumulators double-buffered in TMEM).  Per
+// logits row the CTA folds each tile's statistics into a running LmStat
+// (tile order), writes one partial, and the last CTA merges the G partials in
+// CTA order -> token / logprob / entropy.  Replaces one CTA per tile (two
+// waves, a T-way atomic and a T-way merge).
+constexpr int kLmStages = 8;
+constexpr int kLmSmem = kLmStages * (kTileW + kTileX) + 1024 + 512;
+
+__global__ void __launch_bounds__(192, 1)
+lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, const GemvArgs a,
+                  LmStat* __restrict__ part, int* __restrict__ cnt) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  unsigned char* sw = smem;
+  unsigned char* sx = smem + kLmStages * kTileW;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sx + kLmStages * kTileX);
+  std::uint64_t* empty = full + kLmStages;
+  std::uint64_t* accf = empty + kLmStages;  // [2]
+  std::uint64_t* acce = accf + 2;           // [2]
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(acce + 2);
+  __shared__ LmStat red[4][kN];
+  __shared__ LmStat run[kN];
+  __shared__ bool last;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = (a.N + kM - 1) / kM, G = gridDim.x, c = blockIdx.x;
+  const int t0 = static_cast<int>(static_cast<long long>(c) * T / G), t1 = static_cast<int>(static_cast<long long>(c + 1) * T / G);
+  const int KT = a.K / kBK;
+  const LmStat none{-INFINITY, 0.f, 0.f, 0x7fffffff};
+
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) gv_stamp(0);
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&map_w);
+    prefetch_tmap(&map_x);
+    for (int s = 0; s < kLmStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], 4);
+    }
+    mbar_fence_init();
+  }
+  if (threadIdx.x < kN) run[threadIdx.x] = none;
+  if (warp == 0) tmem_alloc<32>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer: weights before the PDL wait, activations after
+      const int total = (t1 - t0) * KT;
+      int q = 0;
+      for (; q < total && q < kLmStages; ++q) {
+        mbar_expect_tx(&full[q], kTileW + kTileX);
+        tma_load_2d(sw + q * kTileW, &map_w, &full[q], (q % KT) * kBK, (t0 + q / KT) * kM);
+      }
+      pdl_wait();
+      for (int j = 0; j < q; ++j) tma_load_2d(sx + j * kTileX, &map_x, &full[j], (j % KT) * kBK, 0);
+      for (; q < total; ++q) {
+        const int s = q % kLmStages;
+        mbar_wait(&empty[s], ((q / kLmStages) - 1) & 1);
+        mbar_expect_tx(&full[s], kTileW + kTileX);
+        tma_load_2d(sw + s * kTileW, &map_w, &full[s], (q % KT) * kBK, (t0 + q / KT) * kM);
+        tma_load_2d(sx + s * kTileX, &map_x, &full[s], (q % KT) * kBK, 0);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int q = 0;
+      for (int t = t0; t < t1; ++t) {
+        const int j = t - t0, b = j & 1;
+        if (j >= 2) mbar_wait(&acce[b], ((j >> 1) - 1) & 1);
+        tc_fence_after();
+        for (int kt = 0; kt < KT; ++kt, ++q) {
+          const int s = q % kLmStages;
+          mbar_wait(&full[s], (q / kLmStages) & 1);
+          if (q == 0) gv_stamp(1);
+          tc_fence_after();
+          const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + s * kTileX);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_bf16(tmem + b * kN, umma_desc(w0 + k * 32), umma_desc(x0 + k * 32), kIdesc, (kt | k) ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&accf[b]);
+      }
+      gv_stamp(2);
+    }
+    __syncwarp();
+  } else {
+    // epilogue warps 2-5: TMEM lane quarter = warp % 4
+    pdl_wait();
+    const int R = a.meta ? __ldcg(a.meta) : a.R;
+    const int ew = warp - 2, quarter = warp & 3;
+    const int et = threadIdx.x - 64;  // 0..127
+    for (int t = t0; t < t1; ++t) {
+      const int j = t - t0, b = j & 1;
+      mbar_wait(&accf[b], (j >> 1) & 1);
+      tc_fence_after();
+      float v[16];
+      tmem_ld16(tmem + b * kN + (static_cast<std::uint32_t>(quarter * 32) << 16), v);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[b]);
+      const int n = t * kM + quarter * 32 + lane;
+#pragma unroll
+      for (int r = 0; r < kN; ++r) {
+        if (r >= R) break;
+        const bool ok = n < a.N;
+        if (ok && a.logits) a.logits[static_cast<long long>(r) * a.N + n] = v[r];
+        LmStat st = ok ? LmStat{v[r], 1.f, 0.f, n} : none;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const LmStat o = shfl_stat(st, off);
+          st = (lane & off) ? stat_merge(o, st) : stat_merge(st, o);
+        }
+        if (lane == 0) red[quarter][r] = st;  // quarter order = vocab order within the tile
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (et < R) {
+        LmStat st = red[0][et];
+        for (int w = 1; w < 4; ++w) st = stat_merge(st, red[w][et]);
+        run[et] = stat_merge(run[et], st);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      (void)ew;
+    }
+    if (et == 0) gv_stamp(3);
+    if (et < R) {
+      const LmStat st = run[et];
+      __stcg(reinterpret_cast<float4*>(part + static_cast<long long>(et) * G + c),
+             make_float4(st.m, st.s, st.t, __int_as_float(st.idx)));
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (et == 0) {
+      unsigned prev;
+      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(cnt) : "memory");
+      last = prev == static_cast<unsigned>(G - 1);
+      gv_stamp(4);
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (last) {
+      for (int r = et >> 5; r < R; r += 4) {
+        LmStat st = none;
+        const float4* pr = reinterpret_cast<const float4*>(part + static_cast<long long>(r) * G);
+        for (int b0 = lane; b0 < G; b0 += 32 * 8) {
+          float4 raw[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int bb = b0 + 32 * u;
+            raw[u] = bb < G ? __ldcg(pr + bb) : make_float4(-INFINITY, 0.f, 0.f, __int_as_float(0x7fffffff));
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) st = stat_merge(st, LmStat{raw[u].x, raw[u].y, raw[u].z, __float_as_int(raw[u].w)});
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const LmStat o = shfl_stat(st, off);
+          st = (lane & off) ? stat_merge(o, st) : stat_merge(st, o);
+        }
+        if (lane == 0) {
+          const int oi = a.out_idx[r];
+          const float ls = logf(st.s);
+          a.out_tok[oi] = st.idx;
+          a.out_lp[oi] = -ls;
+          a.out_ent[oi] = ls - st.t / st.s;
+        }
+      }
+      if (et == 0) __stcg(cnt, 0);
+      if (et == 0) gv_stamp(5);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<32>(tmem);
+}
+
 }  // namespace
+
+void lm_head_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, LmStat* part, int* cnt, int grid,
+                cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(lm_head_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLmSmem);
+    uniform_carveout(reinterpret_cast<const void*>(lm_head_tc_kernel));
+    attr = true;
+  }
+  const int T = (a.N + kM - 1) / kM;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid < T ? grid : T);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = kLmSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, lm_head_tc_kernel, *reinterpret_cast<const CUtensorMap*>(&map_w),
+                     *reinterpret_cast<const CUtensorMap*>(&map_x), a, part, cnt);
+}
 
 void gemv_tc_debug_trace(unsigned long long* buf) { cudaMemcpyToSymbol(g_gv_trace, &buf, sizeof(buf)); }
 

@@ -117,7 +117,12 @@ bool gemv_tc_supported(const GemvArgs& a);
 int gemv_tc_splits(int N, int K, int epi);
 long long gemv_tc_ws_floats(int N, int K);
 void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float* ws, int* cnt, cudaStream_t st);
-void gemv_tc_debug_trace(unsigned long long* buf);  // per-CTA stamps [cta][8] (debug), nullptr = off
+void gemv_tc_debug_trace(unsigned long long* buf);
+// Persistent LM head with fused greedy statistics (epi kEpiLmStats args): one
+// CTA per SM over contiguous vocab tiles; part >= 16 * grid LmStat, cnt one
+// int zero-initialised once.
+void lm_head_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, LmStat* part, int* cnt, int grid,
+                cudaStream_t st);  // per-CTA stamps [cta][8] (debug), nullptr = off
 
 // ---- persistent decode forward (decode_mk.cu): one launch per tick of <= 16
 // rows of a model, one CTA per SM (cooperative launch) ----
@@ -189,7 +194,7 @@ void decode_mk(const MkParams& p, int grid, int smem_bytes, cudaStream_t st);
 // `cnt` >= R*nh ints, zero-initialised once (the kernel leaves them zero).
 constexpr int kKvSplit = 128;  // smallest split (sizes the partial workspace)
 // keys per attention CTA: 8 warps x 32 for hd 64, 4 warps x 32 for hd 128
-inline int kv_split(int hd) { return hd == 64 ? 256 : 128; }
+inline int kv_split(int hd) { return hd == 64 ? 1024 : 512; }  // keys per attention CTA (GQA kernel)
 long long attention_ws_floats(int R, int nh, int hd, int max_ctx);
 void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, const int* meta, int nh, int nkv,
                int hd, const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx,
