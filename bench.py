@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--placement", default="replicas", choices=["replicas", "tree"],
                     help="N>1: independent replicas (weak scaling) or one request tree-partitioned over the ranks")
     ap.add_argument("--profile-only", action="store_true", help="run steps without JSON (for ncu)")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the secondary 1B-agent (C2) decode measurement reported beside the headline")
+    ap.add_argument("--secondary-out", type=int, default=128, help="C2 output tokens per agent for the secondary run")
     return ap.parse_args()
 
 
@@ -121,6 +124,45 @@ def roofline(probes, hbm_gbs, src):
             "frac": achieved / hbm_gbs, "traffic": traffic, "peak_source": src,
             "bytes_per_launch": v["bytes"] / v["launches"], "avg_us": 1e3 * v["ms"] / v["launches"],
             "share_of_probed_time": v["ms"] / max(1e-12, sum(p["ms"] for p in probes.values()))}
+
+
+def secondary_c2(args, hbm, src, local):
+    """The headline C1 agents are tiny (34 MB of weights, latency-bound); the
+    HBM roofline of the decode path is only visible at the ~1B shape.  One
+    C2-shaped request (tree 8-2-1 of ~1B agents, `--secondary-out` tokens per
+    agent) is timed with device events like the headline, then replayed with
+    kernel probes: per-kernel achieved GB/s against the measured HBM peak."""
+    import torch
+    from paper_2512_18126_b200 import capi
+    from paper_2512_18126_b200.configs import C2
+    cfg = dict(C2, out_len=[args.secondary_out] * 3)
+    eng, qc = capi.engine_for(cfg, device=local)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    eng.run_query(qc, sample=0, resolve=False, detail=False)  # warm-up (graph capture)
+    flush.fill_(1.0)
+    torch.cuda.synchronize()
+    r = eng.run_query(qc, sample=1, resolve=False, detail=False)
+    fwd_gb = r["weight_bytes"] / 1e9
+    out = {"config": {"workload": cfg["workload"].replace("greedy 512", f"greedy {args.secondary_out}"),
+                      "name": "C2", "models": {t: m["shape"] for t, m in cfg["models"].items()}},
+           "value": r["tokens"] / (r["e2e_ms"] / 1e3), "unit": UNIT, "e2e_ms": r["e2e_ms"], "ticks": r["ticks"],
+           "forwards": r["forwards"], "ms_per_forward": r["e2e_ms"] / max(1, r["forwards"]),
+           "weight_gb_per_forward": fwd_gb / max(1, r["forwards"]),
+           "weight_stream_gbs": fwd_gb / (r["e2e_ms"] / 1e3),
+           "weight_stream_frac": fwd_gb / (r["e2e_ms"] / 1e3) / hbm}
+    eng.probe(True)
+    eng.run_query(qc, sample=1, resolve=False, detail=False)
+    probes = eng.probe_stats()
+    eng.probe(False)
+    out["kernels"] = {k: {"launches": v["launches"], "avg_us": 1e3 * v["ms"] / max(1, v["launches"]),
+                          "gbs": v["bytes"] / max(1e-12, v["ms"] / 1e3) / 1e9,
+                          "frac_hbm": v["bytes"] / max(1e-12, v["ms"] / 1e3) / 1e9 / hbm}
+                      for k, v in probes.items() if v["launches"]}
+    out["roofline"] = roofline(probes, hbm, src)
+    out["note"] = ("kernels: CUDA events around every launch (graphs bypassed, so launch gaps are inside "
+                   "each kernel's time); weight_stream_frac: whole-forward weight bytes / device time")
+    eng.close()
+    return out
 
 
 def cpu_baseline(cfg, budget_s):
@@ -316,10 +358,14 @@ def main():
                    "weight_gb_per_request": wbytes / args.steps / 1e9,
                    "weight_stream_gbs": wbytes / (dev_ms / 1e3) / 1e9},
     }
+    if not args.no_secondary and args.config != "C2":
+        eng.close()
+        line["secondary"] = secondary_c2(args, hbm, src, local)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_baseline_s)
     print(json.dumps(line), flush=True)
-    eng.close()
+    if args.no_secondary or args.config == "C2":
+        eng.close()
     if pg:
         pg.destroy_process_group()
 

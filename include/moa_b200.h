@@ -78,6 +78,10 @@ int moa_engine_probe_stats(moa_engine* eng, int kind, int* launches, double* ms,
  * *n receives phases * grid * 8; the last forward's stamps are copied to out
  * when out != NULL and cap suffices). */
 int moa_engine_megakernel(moa_engine* eng, int model, int enable, int trace);
+/* Cluster-resident small-agent forward (16-CTA cluster, ticks of <= 16 rows)
+ * for model `model`: enable (1) / disable (0); returns UNSUPPORTED when the
+ * model shape does not fit it. */
+int moa_engine_small_forward(moa_engine* eng, int model, int enable);
 int moa_engine_mk_trace(moa_engine* eng, int model, uint64_t* out, long long cap, long long* n);
 
 /* ---- tree-partitioned serving over several GPUs (one process per GPU) ----
@@ -240,7 +244,8 @@ int moa_k_gemv(uintptr_t A, uintptr_t X, int R, uintptr_t W, int N, int K, uintp
 int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
 /* Decode GEMV on the tensor cores (swap-AB, split-K): out[R][N] fp32 =
  * A[R][K] . W[N][K]^T for R <= 16; A must have >= 16 allocated rows. */
-int moa_k_debug_trace(uintptr_t buf); /* debug: gemv_tc per-CTA %globaltimer stamps, 0 = off */
+int moa_k_debug_trace(uintptr_t buf); /* debug: gemv_tc per-CTA clock stamps, 0 = off */
+int moa_k_debug_trace_small(uintptr_t buf); /* debug: small-agent forward per-CTA clock stamps, 0 = off */
 int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
 /* Hash-uniform weight init of a logical [rows][cols] tensor into a device row
  * layout (0 identity, 1 RoPE-pair interleave per hd rows, 2 even rows, 3 odd rows). */

@@ -28,6 +28,10 @@ class RunError(Exception):
     """MOA_ERR_RUNTIME -- the reference's RunError (errors.hpp:17-20)."""
 
 
+class UnsupportedError(Exception):
+    """MOA_ERR_UNSUPPORTED: a valid request this build / device cannot serve."""
+
+
 class DeviceError(RunError):
     """MOA_ERR_DEVICE -- CUDA failure."""
 
@@ -100,8 +104,10 @@ _SIGS = {
     "moa_engine_attach_loopback": ([C.c_void_p, C.c_void_p, C.c_int], C.c_int),
     "moa_placement": ([C.c_int, C.c_int, _P(C.c_int), _P(C.c_int), C.c_int, _P(C.c_int)], C.c_int),
     "moa_k_debug_trace": ([C.c_size_t], C.c_int),
+    "moa_k_debug_trace_small": ([C.c_size_t], C.c_int),
     "moa_engine_probe": ([C.c_void_p, C.c_int], C.c_int),
     "moa_engine_megakernel": ([C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
+    "moa_engine_small_forward": ([C.c_void_p, C.c_int, C.c_int], C.c_int),
     "moa_engine_mk_trace": ([C.c_void_p, C.c_int, _P(C.c_uint64), C.c_longlong, _P(C.c_longlong)], C.c_int),
     "moa_engine_probe_stats": ([C.c_void_p, C.c_int, _P(C.c_int), _P(C.c_double), _P(C.c_double)], C.c_int),
     "moa_add_agent": ([C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
@@ -163,6 +169,8 @@ def check(rc: int):
         raise ValidationError(msg)
     if rc == MOA_ERR_DEVICE:
         raise DeviceError(msg)
+    if rc == MOA_ERR_UNSUPPORTED:
+        raise UnsupportedError(msg)
     raise RunError(msg)
 
 
@@ -267,13 +275,16 @@ class Engine:
         check(lib().moa_engine_attach_loopback(self.h, hub.h, rank))
         self._hub = hub  # keep the hub alive as long as the engine
 
-    PROBE_KINDS = ("embed", "qkv", "attention", "o_proj", "gate_up", "down", "lm_head", "decode_mk")
+    PROBE_KINDS = ("embed", "qkv", "attention", "o_proj", "gate_up", "down", "lm_head", "decode_mk", "small_fwd")
 
     def probe(self, enable: bool):
         check(lib().moa_engine_probe(self.h, int(enable)))
 
     def megakernel(self, model: int, enable: bool = True, trace: bool = False):
         check(lib().moa_engine_megakernel(self.h, model, int(enable), int(trace)))
+
+    def small_forward(self, model: int, enable: bool = True):
+        check(lib().moa_engine_small_forward(self.h, model, int(enable)))
 
     def mk_trace(self, model: int):
         """Last persistent-forward trace of `model`: uint64 [phases][grid][8] %globaltimer ns."""

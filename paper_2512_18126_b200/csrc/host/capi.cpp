@@ -36,6 +36,9 @@ int guard(F&& f) {
   } catch (const moa::ValidationError& e) {
     g_err = e.what();
     return MOA_ERR_VALIDATION;
+  } catch (const moa::UnsupportedError& e) {
+    g_err = e.what();
+    return MOA_ERR_UNSUPPORTED;
   } catch (const moa::DeviceError& e) {
     g_err = e.what();
     return MOA_ERR_DEVICE;
@@ -253,6 +256,16 @@ int moa_engine_megakernel(moa_engine* eng, int model, int enable, int trace) {
     MOA_CUDA(cudaStreamSynchronize(E(eng).stream()));
     E(eng).model(model).set_megakernel(enable != 0);
     E(eng).model(model).set_mk_trace(trace != 0);
+  });
+}
+
+int moa_engine_small_forward(moa_engine* eng, int model, int enable) {
+  return guard([&] {
+    if (model < 0 || model >= E(eng).n_models()) throw moa::ValidationError("engine: model index out of range");
+    if (enable && !E(eng).model(model).small_forward_ready())
+      throw moa::UnsupportedError("engine: the small-agent forward does not fit this model shape");
+    MOA_CUDA(cudaStreamSynchronize(E(eng).stream()));
+    E(eng).model(model).set_small_forward(enable != 0);
   });
 }
 
@@ -664,6 +677,12 @@ int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, 
 
 int moa_k_debug_trace(uintptr_t buf) {
   return guard([&] { moa::k::gemv_tc_debug_trace(reinterpret_cast<unsigned long long*>(buf)); });
+}
+
+
+
+int moa_k_debug_trace_small(uintptr_t buf) {
+  return guard([&] { moa::k::small_forward_debug_trace(reinterpret_cast<unsigned long long*>(buf)); });
 }
 
 int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream) {

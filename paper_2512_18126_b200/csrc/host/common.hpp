@@ -25,6 +25,10 @@ struct RunError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 // Device / CUDA failure: a RunError with its own status code at the C-ABI.
+// a valid request this build/device cannot serve (C-ABI MOA_ERR_UNSUPPORTED)
+struct UnsupportedError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 struct DeviceError : RunError {
   using RunError::RunError;
 };

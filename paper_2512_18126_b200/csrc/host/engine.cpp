@@ -50,6 +50,18 @@ GpuEngine::GpuEngine(std::vector<ModelSpec> models, std::vector<int> agents_per_
     ring_.push_back(s);
   }
   MOA_CUDA(cudaEventCreate(&start_ev_));
+  MOA_CUDA(cudaEventCreateWithFlags(&tick_fork_, cudaEventDisableTiming));
+  for (std::size_t m = 0; m < models_.size(); ++m) {
+    cudaStream_t s2;
+    cudaEvent_t e2;
+    MOA_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    MOA_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+    mstreams_.push_back(s2);
+    mdone_.push_back(e2);
+  }
+  // two persistent (cooperative, one CTA per SM) forwards must never run side by side
+  if (const char* e = std::getenv("MOA_MK")) overlap_models_ = std::string(e) == "0";
+  if (const char* e = std::getenv("MOA_OVERLAP")) overlap_models_ = overlap_models_ && std::string(e) != "0";
   MOA_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -63,6 +75,12 @@ GpuEngine::~GpuEngine() {
     cudaEventDestroy(s.done);
   }
   for (auto e : tick_ev_) cudaEventDestroy(e);
+  for (auto s2 : mstreams_) {
+    cudaStreamSynchronize(s2);
+    cudaStreamDestroy(s2);
+  }
+  for (auto e2 : mdone_) cudaEventDestroy(e2);
+  if (tick_fork_) cudaEventDestroy(tick_fork_);
   if (start_ev_) cudaEventDestroy(start_ev_);
   for (void* p : {static_cast<void*>(out_tok_), static_cast<void*>(out_lp_), static_cast<void*>(out_ent_),
                   static_cast<void*>(logits_), static_cast<void*>(logits_scratch_)})
@@ -206,7 +224,7 @@ void GpuEngine::start_decode(Req& r, int n_out) {
 }
 
 void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, const std::vector<int>& lsel,
-                                   const std::vector<int>& lout) {
+                                   const std::vector<int>& lout, cudaStream_t st) {
   DeviceModel& dm = *models_[static_cast<std::size_t>(m)];
   Staging& s = ring_[ring_next_];
   ring_next_ = (ring_next_ + 1) % ring_.size();
@@ -231,18 +249,18 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   sel[2 * L] = static_cast<int>(rows.size());
   sel[2 * L + 1] = static_cast<int>(lsel.size());
   sel[2 * L + 2] = max_pos;
-  MOA_CUDA(cudaMemcpyAsync(dm.buffers().rows, s.host, rb, cudaMemcpyHostToDevice, stream_));
-  MOA_CUDA(cudaMemcpyAsync(dm.buffers().sel, sel, sizeof(int) * (2 * L + 3), cudaMemcpyHostToDevice, stream_));
-  MOA_CUDA(cudaEventRecord(s.done, stream_));
+  MOA_CUDA(cudaMemcpyAsync(dm.buffers().rows, s.host, rb, cudaMemcpyHostToDevice, st));
+  MOA_CUDA(cudaMemcpyAsync(dm.buffers().sel, sel, sizeof(int) * (2 * L + 3), cudaMemcpyHostToDevice, st));
+  MOA_CUDA(cudaEventRecord(s.done, st));
   float* logits = (opt_.keep_logits && !lsel.empty()) ? logits_scratch_ : nullptr;
   dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), max_pos, keys, out_tok_, out_tok_,
-             out_lp_, out_ent_, logits, stream_);
+             out_lp_, out_ent_, logits, st);
   if (logits) {  // debug path: scatter each logits row to its (slot, k) home
     const long long V = dm.spec().vocab;
     for (std::size_t i = 0; i < lsel.size(); ++i)
       MOA_CUDA(cudaMemcpyAsync(logits_ + static_cast<long long>(lout[i]) * logits_v_,
                                logits_scratch_ + static_cast<long long>(i) * V, sizeof(float) * V,
-                               cudaMemcpyDeviceToDevice, stream_));
+                               cudaMemcpyDeviceToDevice, st));
   }
   rows_total_ += static_cast<long long>(rows.size());
   weight_bytes_ += dm.weight_bytes();
@@ -314,12 +332,30 @@ void GpuEngine::step() {
       }
     }
   }
+  // Forwards of different models in one tick are independent (disjoint
+  // weights, KV pools, workspaces and output slots): each runs on its model's
+  // stream after the previous tick, and the engine stream joins them -- a
+  // successor's incremental prefill overlaps its predecessors' decode.
+  int active = 0;
+  for (std::size_t m = 0; m < nm; ++m) active += !rows[m].empty();
+  const bool fan_out = active > 1 && overlap_models_;
+  if (fan_out) MOA_CUDA(cudaEventRecord(tick_fork_, stream_));
   for (std::size_t m = 0; m < nm; ++m)
     if (!rows[m].empty()) {
       const auto t_api = std::chrono::steady_clock::now();
-      upload_and_forward(static_cast<int>(m), rows[m], lsel[m], lout[m]);
+      cudaStream_t st = stream_;
+      if (fan_out) {
+        st = mstreams_[m];
+        MOA_CUDA(cudaStreamWaitEvent(st, tick_fork_, 0));
+      }
+      upload_and_forward(static_cast<int>(m), rows[m], lsel[m], lout[m], st);
+      if (fan_out) {
+        MOA_CUDA(cudaEventRecord(mdone_[m], st));
+        MOA_CUDA(cudaStreamWaitEvent(stream_, mdone_[m], 0));
+      }
       host_api_ms_ += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_api).count();
     }
+  overlapped_ticks_ += fan_out;
   if (opt_.time_ticks) {
     if (static_cast<int>(tick_ev_.size()) <= tick_) {
       cudaEvent_t e;
@@ -481,6 +517,7 @@ void GpuEngine::reset() {
   rows_total_ = 0;
   weight_bytes_ = 0.0;
   forwards_ = 0;
+  overlapped_ticks_ = 0;
   host_ms_ = host_api_ms_ = host_wait_ms_ = 0.0;
   for (auto& m : models_) m->reset_bindings();
 }

@@ -137,6 +137,7 @@ class GpuEngine {
   double bytes_moved() const { return weight_bytes_; }
   long long rows_processed() const { return rows_total_; }
   int kernel_forwards() const { return forwards_; }
+  int overlapped_ticks() const { return overlapped_ticks_; }  // ticks whose model forwards ran on parallel streams
   double host_ms() const { return host_ms_; }  // host time spent inside step() (incl. EE syncs)
   double host_api_ms() const { return host_api_ms_; }    // of which: uploads + graph launches
   double host_wait_ms() const { return host_wait_ms_; }  // of which: blocked on the staging ring (GPU behind)
@@ -163,11 +164,17 @@ class GpuEngine {
   const Req& req(const AgentId& id) const;
   void start_decode(Req& r, int n_out);
   void upload_and_forward(int m, const std::vector<k::RowDesc>& rows, const std::vector<int>& lsel,
-                          const std::vector<int>& lout);
+                          const std::vector<int>& lout, cudaStream_t st);
 
   EngineOptions opt_;
   std::unique_ptr<PeerComm> comm_;
   cudaStream_t stream_ = nullptr;
+  // per-model streams: forwards of different models in one tick run side by side
+  std::vector<cudaStream_t> mstreams_;
+  std::vector<cudaEvent_t> mdone_;
+  cudaEvent_t tick_fork_ = nullptr;
+  bool overlap_models_ = true;
+  int overlapped_ticks_ = 0;
   std::vector<std::unique_ptr<DeviceModel>> models_;
   std::map<AgentId, Req> reqs_;
   std::vector<AgentId> order_;

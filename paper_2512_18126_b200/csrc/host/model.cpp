@@ -206,6 +206,38 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
     }
     if (const char* e = std::getenv("MOA_MK_STAGES")) mk_stages_ = std::min(mk_stages_, std::max(2, std::atoi(e)));
   }
+  // cluster-resident forward for small agents
+  {
+    k::SmallParams& sp = small_;
+    sp.L = s.n_layers;
+    sp.D = s.d;
+    sp.nh = s.n_heads;
+    sp.nkv = s.n_kv_heads;
+    sp.hd = s.head_dim;
+    sp.ffn = s.ffn;
+    sp.eps = static_cast<float>(s.norm_eps);
+    sp.rows = buf_.rows;
+    sp.meta = buf_.sel + 2 * max_lrows_;
+    sp.emb = emb_;
+    sp.g = ones_;
+    sp.rope = rope_;
+    sp.kpool = kpool_;
+    sp.vpool = vpool_;
+    sp.kv_stride = kv_stride_;
+    sp.layer_stride = layer_stride_;
+    sp.max_ctx = max_ctx_;
+    sp.w0 = layers_[0].wqkv;
+    sp.wstride = layers_.size() > 1 ? layers_[1].wqkv - layers_[0].wqkv : 0;
+    sp.off_o = layers_[0].wo - layers_[0].wqkv;
+    sp.off_gu = layers_[0].wgu - layers_[0].wqkv;
+    sp.off_d = layers_[0].wd - layers_[0].wqkv;
+    sp.x_out = x_;
+    small_ok_ = max_rows >= k::kMkRows && k::small_forward_supported(sp);
+    cudaGetLastError();
+    // opt-in (MOA_SMALL=1): faster than the kernel chain in isolation, not yet end to end
+    use_small_ = false;
+    if (const char* e = std::getenv("MOA_SMALL")) use_small_ = std::string(e) != "0";
+  }
   // persistent forward: opt-in (MOA_MK=1) until it beats the per-kernel chain
   use_mk_ = false;
   if (const char* e = std::getenv("MOA_MK")) use_mk_ = std::string(e) != "0";
@@ -304,6 +336,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     launch_mk(out_tok_read, out_tok, out_lp, out_ent, logits, st);
     return;
   }
+  const bool small = use_small_ && use_tc_ && small_ok_ && rcap <= k::kMkRows;
   // tensor-core path for row buckets >= kTcMinRows (prefill-heavy ticks)
   const bool tc = use_tc_ && tc_ok_ && rcap >= k::kTcMinRows;
   // decode ticks of large models: swap-AB tensor-core GEMV (pure weight stream)
@@ -332,10 +365,19 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   auto probe_end = [&]() {
     if (probes_) probes_->end(st);
   };
+  if (small) {
+    k::SmallParams sp = small_;
+    sp.out_tok_read = out_tok_read;
+    const double kv_bytes = 4.0 * static_cast<double>(live_keys_) * nkv * hd * s.n_layers;
+    probe_begin(KernelProbes::SmallFwd, weight_bytes() - 2.0 * s.vocab * D + kv_bytes);
+    k::small_forward(sp, st);
+    probe_end();
+  } else {
   probe_begin(KernelProbes::Embed, 6.0 * live_R_ * D);
   k::embed(buf_.rows, rcap, meta, out_tok_read, emb_, D, x_, st);
   probe_end();
-  for (int l = 0; l < s.n_layers; ++l) {
+  }
+  for (int l = 0; l < (small ? 0 : s.n_layers); ++l) {
     const Layer& L = layers_[static_cast<std::size_t>(l)];
     const long long loff = layer_stride_ * l;
     // rmsnorm -> QKV -> RoPE -> KV append

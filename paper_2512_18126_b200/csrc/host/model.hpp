@@ -46,7 +46,7 @@ struct ForwardBuffers {
 // without graphs and every launch is bracketed by an event pair together with
 // its algorithmic bytes.
 struct KernelProbes {
-  enum Kind { Embed = 0, Qkv, Attention, OProj, GateUp, Down, LmHead, DecodeMk, kKinds };
+  enum Kind { Embed = 0, Qkv, Attention, OProj, GateUp, Down, LmHead, DecodeMk, SmallFwd, kKinds };
   struct Rec {
     int kind;
     double bytes;
@@ -69,6 +69,11 @@ class DeviceModel {
  public:
   void attach_probes(KernelProbes* p) { probes_ = p; }
   void set_tensor_cores(bool on) { use_tc_ = on; }
+  void set_small_forward(bool on) {
+    use_small_ = on;
+    graphs_clear();
+  }
+  bool small_forward_ready() const { return small_ok_; }
   void set_megakernel(bool on) {
     use_mk_ = on;
     graphs_clear();
@@ -110,6 +115,10 @@ class DeviceModel {
   bool use_graphs_ = true;
   bool use_tc_ = true;  // tensor-core path for ticks with >= kTcMinRows rows
   bool tc_ok_ = false;
+  // cluster-resident small-agent forward (small_fwd.cu) for ticks of <= 16 rows
+  bool use_small_ = true;
+  bool small_ok_ = false;
+  k::SmallParams small_;
   // persistent decode forward (decode_mk.cu) for ticks of <= 16 rows
   bool use_mk_ = true;
   bool mk_ok_ = false;

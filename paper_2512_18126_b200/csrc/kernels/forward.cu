@@ -22,6 +22,14 @@ namespace moa::k {
 // consecutive kernels ask for different L1/shared splits the SM must drain
 // and reconfigure between them, which serialises the chain and defeats
 // programmatic dependent launch.  MOA_CARVEOUT=0 disables (A/B runs).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MOA_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 void uniform_carveout(const void* fn) {
   static std::mutex mu;
   static std::set<const void*> done;
@@ -60,7 +68,7 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, 
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 constexpr int kRB = 8;    // rows per CTA row-block

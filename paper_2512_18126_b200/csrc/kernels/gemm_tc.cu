@@ -340,7 +340,7 @@ void rmsnorm_rows(const float* x, int R_cap, const int* meta, int K, const float
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   uniform_carveout(reinterpret_cast<const void*>(rmsnorm_rows_kernel));
   cudaLaunchKernelEx(&cfg, rmsnorm_rows_kernel, x, sel, meta, meta_idx, K, g, eps, h);
 }

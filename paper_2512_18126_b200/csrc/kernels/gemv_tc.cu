@@ -535,7 +535,7 @@ void lm_head_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, LmS
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   cudaLaunchKernelEx(&cfg, lm_head_tc_kernel, *reinterpret_cast<const CUtensorMap*>(&map_w),
                      *reinterpret_cast<const CUtensorMap*>(&map_x), a, part, cnt);
 }
@@ -576,11 +576,7 @@ void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float*
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
   int na = 0;
-  static const bool no_pdl = [] {
-    const char* e = std::getenv("MOA_NO_PDL");
-    return e && e[0] == '1';
-  }();
-  if (!no_pdl) {
+  if (pdl_enabled()) {
     attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attrs[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;

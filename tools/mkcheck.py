@@ -3,7 +3,7 @@ on C1 (tiny) and a short C2 (1b): timing, token agreement, oracle check."""
 import json, os, subprocess, sys
 sys.path.insert(0, '/root/repo')
 
-def run(mk, name, out):
+def run(mk, name, out, var='MOA_MK'):
     code = f"""
 import json, sys
 sys.path.insert(0, '/root/repo')
@@ -19,7 +19,7 @@ for i in range(3):
                     agents={{k: dict(output=v['output'], logprobs=[float(x) for x in v['logprobs']], prompt=v['prompt']) for k, v in r['agents'].items()}}))
 print('JSON' + json.dumps(res))
 """
-    env = dict(os.environ, MOA_MK=str(mk))
+    env = dict(os.environ, **{var: str(mk)})
     p = subprocess.run([sys.executable, '-c', code], env=env, capture_output=True, text=True, timeout=600)
     if p.returncode != 0:
         print(name, 'mk', mk, 'FAILED', p.returncode, p.stderr[-3000:], p.stdout[-2000:])
@@ -27,12 +27,13 @@ print('JSON' + json.dumps(res))
     line = [l for l in p.stdout.splitlines() if l.startswith('JSON')][0]
     return json.loads(line[4:])
 
+VAR = sys.argv[1] if len(sys.argv) > 1 else 'MOA_MK'
 for name, out in (('C1', 0), ('C2', 48)):
-    a = run(0, name, out)
-    b = run(1, name, out)
+    a = run(0, name, out, VAR)
+    b = run(1, name, out, VAR)
     if not a or not b:
         continue
-    print(name, 'per-op e2e_ms', [round(x['e2e_ms'], 2) for x in a], 'megakernel e2e_ms', [round(x['e2e_ms'], 2) for x in b])
+    print(name, VAR, '=0 e2e_ms', [round(x['e2e_ms'], 2) for x in a], '=1 e2e_ms', [round(x['e2e_ms'], 2) for x in b])
     ra, rb = a[-1], b[-1]
     same = sum(ra['agents'][k]['output'] == rb['agents'][k]['output'] for k in ra['agents'])
     first_diff = {k: next((i for i, (x, y) in enumerate(zip(ra['agents'][k]['output'], rb['agents'][k]['output'])) if x != y), None) for k in ra['agents']}
