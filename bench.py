@@ -107,11 +107,11 @@ def peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def roofline(probes, hbm_gbs, src):
+def roofline(probes, hbm_gbs, src, cfg_name="C1"):
     """Dominant kernel (largest share of probed time): algorithmic bytes per
     launch / average launch duration, against the measured HBM copy peak.
-    `traffic` = DRAM bytes per launch from the committed ncu --set full
-    capture (profiles/ncu_traffic.json) when present."""
+    `traffic` = DRAM bytes per launch of that kernel from the committed ncu
+    --set full capture of this config (profiles/ncu_traffic.json)."""
     kind, v = max(probes.items(), key=lambda kv: kv[1]["ms"])
     if v["launches"] == 0:
         return None
@@ -119,7 +119,7 @@ def roofline(probes, hbm_gbs, src):
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
     if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get(kind)
+        traffic = json.loads(tfile.read_text()).get(cfg_name, {}).get(kind)
     return {"kernel": kind, "bound": "hbm", "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s",
             "frac": achieved / hbm_gbs, "traffic": traffic, "peak_source": src,
             "bytes_per_launch": v["bytes"] / v["launches"], "avg_us": 1e3 * v["ms"] / v["launches"],
@@ -158,7 +158,7 @@ def secondary_c2(args, hbm, src, local):
                           "gbs": v["bytes"] / max(1e-12, v["ms"] / 1e3) / 1e9,
                           "frac_hbm": v["bytes"] / max(1e-12, v["ms"] / 1e3) / 1e9 / hbm}
                       for k, v in probes.items() if v["launches"]}
-    out["roofline"] = roofline(probes, hbm, src)
+    out["roofline"] = roofline(probes, hbm, src, "C2")
     out["note"] = ("kernels: CUDA events around every launch (graphs bypassed, so launch gaps are inside "
                    "each kernel's time); weight_stream_frac: whole-forward weight bytes / device time")
     eng.close()
@@ -347,7 +347,7 @@ def main():
         "e2e": {"value": e2e_toks_all / (e2e_ms_max / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps},
         "gpu_launches": int(sum(v["launches"] for v in probes.values()) + n_ee_launches),
-        "roofline": roofline(probes, hbm, src),
+        "roofline": roofline(probes, hbm, src, cfg["name"]),
         "kernels": {k: {"launches": v["launches"], "ms_per_request": v["ms"] / args.steps,
                         "avg_us": 1e3 * v["ms"] / max(1, v["launches"]),
                         "gbs": v["bytes"] / max(1e-12, v["ms"] / 1e3) / 1e9} for k, v in probes.items()},
