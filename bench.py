@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the secondary 1B-agent (C2) decode measurement reported beside the headline")
     ap.add_argument("--secondary-out", type=int, default=128, help="C2 output tokens per agent for the secondary run")
+    ap.add_argument("--concurrency", default="4,8",
+                    help="continuous-batching sweep reported beside the headline (comma list; '' to skip)")
     return ap.parse_args()
 
 
@@ -162,6 +164,31 @@ def secondary_c2(args, hbm, src, local):
     out["note"] = ("kernels: CUDA events around every launch (graphs bypassed, so launch gaps are inside "
                    "each kernel's time); weight_stream_frac: whole-forward weight bytes / device time")
     eng.close()
+    return out
+
+
+def concurrency_sweep(cfg, levels, local):
+    """Continuous batching: B independent requests of the same config served
+    concurrently by one engine (moa_run_batch).  Throughput = all requests'
+    agent tokens / the batch's device time; latency = each request's own
+    first-tick -> last-completion time.  Reported beside the single-request
+    headline (which matches the reference's one-request-at-a-time
+    run_repetitions, orchestrator.cpp:297-302)."""
+    import torch
+    from paper_2512_18126_b200 import capi
+    out = []
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    for b in levels:
+        eng, qc = capi.engine_for(cfg, device=local, concurrency=b)
+        eng.run_batch(qc, list(range(b)), resolve=False, detail=False)  # warm-up (graph capture)
+        flush.fill_(2.0)
+        torch.cuda.synchronize()
+        rs = eng.run_batch(qc, [b + i for i in range(b)], resolve=False, detail=False)
+        eng.close()
+        batch_ms = max(r["e2e_ms"] for r in rs)
+        lat = sorted(r["e2e_ms"] for r in rs)
+        out.append({"concurrent_requests": b, "value": sum(r["tokens"] for r in rs) / (batch_ms / 1e3), "unit": UNIT,
+                    "batch_ms": batch_ms, "p50_ms_per_request": lat[len(lat) // 2], "ticks": rs[0]["ticks"]})
     return out
 
 
@@ -358,14 +385,15 @@ def main():
                    "weight_gb_per_request": wbytes / args.steps / 1e9,
                    "weight_stream_gbs": wbytes / (dev_ms / 1e3) / 1e9},
     }
+    eng.close()  # the headline engine; the extra measurements build their own
     if not args.no_secondary and args.config != "C2":
-        eng.close()
         line["secondary"] = secondary_c2(args, hbm, src, local)
+    levels = [int(x) for x in args.concurrency.split(",") if x.strip()]
+    if levels and not tree:
+        line["concurrency"] = concurrency_sweep(cfg, levels, local)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_baseline_s)
     print(json.dumps(line), flush=True)
-    if args.no_secondary or args.config == "C2":
-        eng.close()
     if pg:
         pg.destroy_process_group()
 

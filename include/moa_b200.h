@@ -201,6 +201,15 @@ typedef struct {
 /* resolve != 0 copies literal prompts/outputs back (needed by moa_query_*). */
 int moa_run_query(moa_engine* eng, const moa_run_config* cfg, int sample, int resolve,
                   moa_run_summary* summary, moa_query** out /* may be NULL */);
+/* Continuous batching: n independent requests (samples[i]) served
+ * concurrently by one engine -- each keeps its own prompts, slot plans, exit
+ * groups and RNG streams exactly as moa_run_query(samples[i]); their agents
+ * share the engine's ticks (one weight pass per model per tick for all of
+ * them).  summaries[i] / out[i] (out may be NULL) describe request i; e2e_ms
+ * is its own first-tick -> last-completion latency.  The engine needs agent
+ * capacity for n requests. */
+int moa_run_batch(moa_engine* eng, const moa_run_config* cfg, const int* samples, int n, int resolve,
+                  moa_run_summary* summaries, moa_query** out);
 int moa_query_agent(const moa_query* q, int i, moa_agent_record* rec);
 /* which: 0 = prompt, 1 = output. */
 int moa_query_tokens(const moa_query* q, int i, int which, int32_t* dst, int cap, int* n);
@@ -244,6 +253,7 @@ int moa_k_gemv(uintptr_t A, uintptr_t X, int R, uintptr_t W, int N, int K, uintp
 int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
 /* Decode GEMV on the tensor cores (swap-AB, split-K): out[R][N] fp32 =
  * A[R][K] . W[N][K]^T for R <= 16; A must have >= 16 allocated rows. */
+int moa_k_noop(uintptr_t p, int ctas, uintptr_t stream); /* trivial PDL kernel: launch-chain cost probe */
 int moa_k_debug_trace(uintptr_t buf); /* debug: gemv_tc per-CTA clock stamps, 0 = off */
 int moa_k_debug_trace_small(uintptr_t buf); /* debug: small-agent forward per-CTA clock stamps, 0 = off */
 int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);

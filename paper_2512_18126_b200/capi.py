@@ -104,6 +104,7 @@ _SIGS = {
     "moa_engine_attach_loopback": ([C.c_void_p, C.c_void_p, C.c_int], C.c_int),
     "moa_placement": ([C.c_int, C.c_int, _P(C.c_int), _P(C.c_int), C.c_int, _P(C.c_int)], C.c_int),
     "moa_k_debug_trace": ([C.c_size_t], C.c_int),
+    "moa_k_noop": ([C.c_size_t, C.c_int, C.c_size_t], C.c_int),
     "moa_k_debug_trace_small": ([C.c_size_t], C.c_int),
     "moa_engine_probe": ([C.c_void_p, C.c_int], C.c_int),
     "moa_engine_megakernel": ([C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
@@ -121,6 +122,7 @@ _SIGS = {
                         C.c_int),
     "moa_read_logits": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_float)], C.c_int),
     "moa_agent_state": ([C.c_void_p, C.c_int, C.c_int] + [_P(C.c_int)] * 4, C.c_int),
+    "moa_run_batch": ([C.c_void_p, C.c_void_p, _P(C.c_int), C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
     "moa_run_query": ([C.c_void_p, _P(RunConfigC), C.c_int, C.c_int, _P(RunSummary), _P(C.c_void_p)], C.c_int),
     "moa_query_agent": ([C.c_void_p, C.c_int, _P(AgentRecordC)], C.c_int),
     "moa_query_tokens": ([C.c_void_p, C.c_int, C.c_int, _P(C.c_int32), C.c_int, _P(C.c_int)], C.c_int),
@@ -304,6 +306,24 @@ class Engine:
         return out
 
     # --- run_query ---
+    def run_batch(self, cfg: "QueryConfig", samples, resolve=True, detail=True):
+        """Concurrent requests (continuous batching); one result dict per sample."""
+        n = len(samples)
+        arr = (C.c_int * n)(*samples)
+        sums = (RunSummary * n)()
+        qs = (C.c_void_p * n)()
+        check(lib().moa_run_batch(self.h, C.byref(cfg.c), arr, n, int(resolve), sums, qs if detail else None))
+        out = []
+        for i in range(n):
+            res = {k: getattr(sums[i], k) for k, _ in RunSummary._fields_}
+            if detail:
+                try:
+                    res.update(_query_detail(C.c_void_p(qs[i]), sums[i], resolve))
+                finally:
+                    lib().moa_query_free(C.c_void_p(qs[i]))
+            out.append(res)
+        return out
+
     def run_query(self, cfg: "QueryConfig", sample=0, resolve=True, detail=True):
         s = RunSummary()
         q = C.c_void_p()
@@ -394,8 +414,9 @@ class QueryConfig:
             provider_seed=cfg.get("provider_seed", 0))
 
 
-def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16384, gemv_only=False):
-    """Engine holding every model the config names, sized for its agents."""
+def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16384, gemv_only=False, concurrency=1):
+    """Engine holding every model the config names, sized for its agents
+    (times `concurrency` requests served at once by run_batch)."""
     from collections import Counter
     counts = Counter()
     t = cfg["topology"]
@@ -404,7 +425,7 @@ def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16
             counts[_configs.agent_tag(cfg, l + 1, p)] += 1
     tags = list(cfg["models"])
     specs = [model_spec(tag, cfg["models"][tag]["shape"], cfg["models"][tag].get("seed", 0),
-                        max_agents=max(1, counts[tag])) for tag in tags]
+                        max_agents=max(1, counts[tag] * concurrency)) for tag in tags]
     out_max = max(x if isinstance(x, int) else x[1] for x in cfg["out_len"])
     if max_ctx is None:
         prompt_max = max(cfg["query_tokens"] + cfg["leaf_prefix_tokens"],

@@ -390,6 +390,38 @@ int moa_run_query(moa_engine* eng, const moa_run_config* cfg, int sample, int re
   });
 }
 
+int moa_run_batch(moa_engine* eng, const moa_run_config* cfg, const int* samples, int n, int resolve,
+                  moa_run_summary* summaries, moa_query** out) {
+  return guard([&] {
+    need(samples, "samples");
+    if (n <= 0) throw moa::ValidationError("run_batch: n must be > 0");
+    std::vector<int> smp(samples, samples + n);
+    auto rs = moa::run_queries(E(eng), run_config_of(cfg), smp, resolve != 0);
+    for (int i = 0; i < n; ++i) {
+      const auto& r = rs[static_cast<std::size_t>(i)];
+      if (summaries) {
+        moa_run_summary& s = summaries[i];
+        s.ticks = r.ticks;
+        s.n_agents = static_cast<int>(r.agents.size());
+        s.n_evals = static_cast<int>(r.metricq.size());
+        s.forwards = r.forwards;
+        s.tokens = r.tokens;
+        s.decoded_tokens = r.decoded_tokens;
+        s.rows = r.rows;
+        s.e2e_ms = r.e2e_ms;
+        s.wall_ms = r.wall_ms;
+        s.weight_bytes = r.weight_bytes;
+        s.host_ms = r.host_ms;
+      }
+      if (out) {
+        auto q = std::make_unique<moa_query>();
+        q->r = std::move(rs[static_cast<std::size_t>(i)]);
+        out[i] = q.release();
+      }
+    }
+  });
+}
+
 int moa_query_agent(const moa_query* q, int i, moa_agent_record* rec) {
   return guard([&] {
     need(q, "query");
@@ -673,6 +705,10 @@ int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, 
     moa::k::gemm_tc(ma, mw, a, reinterpret_cast<cudaStream_t>(stream));
     MOA_CUDA(cudaGetLastError());
   });
+}
+
+int moa_k_noop(uintptr_t p, int ctas, uintptr_t stream) {
+  return guard([&] { moa::k::noop_chain_link(reinterpret_cast<int*>(p), ctas, reinterpret_cast<cudaStream_t>(stream)); });
 }
 
 int moa_k_debug_trace(uintptr_t buf) {

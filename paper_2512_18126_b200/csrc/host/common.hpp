@@ -36,8 +36,13 @@ struct DeviceError : RunError {
 struct AgentId {
   int layer = 1;
   int position = 0;
+  int req = 0;  // request of a concurrent batch (engine-internal; 0 for a single request)
   auto operator<=>(const AgentId&) const = default;
+  // the reference's "layer:position" (agent.hpp:16-38); labels of synthetic
+  // prompts and RNG streams always use this form, whatever the request
   std::string str() const { return std::to_string(layer) + ":" + std::to_string(position); }
+  AgentId in_request(int r) const { return AgentId{layer, position, r}; }
+  AgentId topo() const { return AgentId{layer, position, 0}; }
 };
 
 namespace rng {

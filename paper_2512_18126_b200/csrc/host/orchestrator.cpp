@@ -140,48 +140,58 @@ struct ExitGroup {
 
 }  // namespace
 
-QueryResult run_query(GpuEngine& eng, const RunConfig& cfg, int sample, bool resolve) {
-  const auto t0 = std::chrono::steady_clock::now();
-  cfg.validate();
-  const Topology& topo = cfg.topology;
-  const std::uint64_t ss = rng::hash_combine(cfg.seed, static_cast<std::uint64_t>(sample));
-  eng.reset();
-  Driver drv(eng, cfg.mode, cfg.chunk_size);
-  const std::map<AgentId, int> owner = tree_placement(topo, eng.world());
+namespace {
 
-  // prompt synthesis + registration (orchestrator.cpp:151-191)
-  const TokenSeq query = rng::synth_tokens(ss, "query", cfg.query_tokens);
-  int max_out = 0;
-  for (const auto& layer : topo.layers())
-    for (const AgentId& a : layer) {
-      const OutLen ol = cfg.out_len.at(a);
-      int n = ol.lo;
-      if (ol.hi != ol.lo) {
-        rng::Stream s = rng::Stream::derive(ss, "outlen:" + a.str());
-        n = static_cast<int>(s.next_int(ol.lo, ol.hi));
-      }
-      max_out = std::max(max_out, n);
-      if (topo.precursors(a).empty()) {
-        TokenSeq prompt = rng::synth_tokens(ss, "leaf_prefix:" + a.str(), cfg.leaf_prefix_tokens);
-        prompt.insert(prompt.end(), query.begin(), query.end());
-        drv.add_source(a, cfg.model_of.at(a), owner.at(a), std::move(prompt), n);
-      } else {
-        std::vector<Slot> slots;
-        const auto& pre = topo.precursors(a);
-        for (std::size_t k = 0; k < pre.size(); ++k)
-          slots.push_back(Slot{pre[k], rng::synth_tokens(ss, "sep:" + a.str() + ":" + std::to_string(k),
-                                                         cfg.separator_tokens)});
-        PromptTemplate tmpl(rng::synth_tokens(ss, "agg_prefix:" + a.str(), cfg.agg_prefix_tokens), std::move(slots),
-                            rng::synth_tokens(ss, "suffix:" + a.str(), cfg.suffix_tokens));
-        drv.add_plan(a, cfg.model_of.at(a), owner.at(a), std::move(tmpl), n);
-      }
-    }
+// One request of a (possibly concurrent) batch: its driver, exit groups and
+// result.  Engine agent ids carry the request index; prompt / RNG labels use
+// the topology ids (AgentId::str ignores the request).
+struct Request {
+  Request(GpuEngine& eng, const RunConfig& cfg, int req, int sample, int group_base)
+      : eng(eng), cfg(cfg), req(req), sample(sample), group_base(group_base), drv(eng, cfg.mode, cfg.chunk_size) {}
 
-  // exit groups (orchestrator.cpp:193-220)
+  GpuEngine& eng;
+  const RunConfig& cfg;
+  int req, sample, group_base;
+  Driver drv;
   QueryResult res;
   std::vector<std::unique_ptr<ExitGroup>> groups;
   std::map<AgentId, ExitGroup*> group_of;
-  if (cfg.early_exit && topo.depth() > 1) {
+
+  AgentId id(const AgentId& topo_id) const { return topo_id.in_request(req); }
+
+  void build(const std::map<AgentId, int>& owner) {
+    const Topology& topo = cfg.topology;
+    const std::uint64_t ss = rng::hash_combine(cfg.seed, static_cast<std::uint64_t>(sample));
+    // prompt synthesis + registration (orchestrator.cpp:151-191)
+    const TokenSeq query = rng::synth_tokens(ss, "query", cfg.query_tokens);
+    int max_out = 0;
+    for (const auto& layer : topo.layers())
+      for (const AgentId& a : layer) {
+        const OutLen ol = cfg.out_len.at(a);
+        int n = ol.lo;
+        if (ol.hi != ol.lo) {
+          rng::Stream s = rng::Stream::derive(ss, "outlen:" + a.str());
+          n = static_cast<int>(s.next_int(ol.lo, ol.hi));
+        }
+        max_out = std::max(max_out, n);
+        if (topo.precursors(a).empty()) {
+          TokenSeq prompt = rng::synth_tokens(ss, "leaf_prefix:" + a.str(), cfg.leaf_prefix_tokens);
+          prompt.insert(prompt.end(), query.begin(), query.end());
+          drv.add_source(id(a), cfg.model_of.at(a), owner.at(a), std::move(prompt), n);
+        } else {
+          std::vector<Slot> slots;
+          const auto& pre = topo.precursors(a);
+          for (std::size_t k = 0; k < pre.size(); ++k)
+            slots.push_back(Slot{id(pre[k]), rng::synth_tokens(ss, "sep:" + a.str() + ":" + std::to_string(k),
+                                                               cfg.separator_tokens)});
+          PromptTemplate tmpl(rng::synth_tokens(ss, "agg_prefix:" + a.str(), cfg.agg_prefix_tokens), std::move(slots),
+                              rng::synth_tokens(ss, "suffix:" + a.str(), cfg.suffix_tokens));
+          drv.add_plan(id(a), cfg.model_of.at(a), owner.at(a), std::move(tmpl), n);
+        }
+      }
+
+    // exit groups (orchestrator.cpp:193-220)
+    if (!(cfg.early_exit && topo.depth() > 1)) return;
     std::vector<std::vector<AgentId>> sets;
     if (cfg.exit_scope == ExitScope::Layer || topo.kind() == TopologyKind::AllToAll) {
       for (int l = 1; l < topo.depth(); ++l) sets.push_back(topo.layer(l));
@@ -192,27 +202,27 @@ QueryResult run_query(GpuEngine& eng, const RunConfig& cfg, int sample, bool res
     for (std::size_t g = 0; g < sets.size(); ++g) {
       auto grp = std::make_unique<ExitGroup>();
       grp->index = static_cast<int>(g);
-      grp->members = sets[g];
-      grp->eval = &eng.ee_evaluator(static_cast<int>(g), cfg.hidden, cfg.provider_seed, cfg.tau,
+      for (const AgentId& m : sets[g]) grp->members.push_back(id(m));
+      grp->eval = &eng.ee_evaluator(group_base + static_cast<int>(g), cfg.hidden, cfg.provider_seed, cfg.tau,
                                     cfg.include_diagonal, static_cast<int>(sets[g].size()), std::max(1, max_out));
       grp->stream = rng::Stream::derive(ss, "ee:" + std::to_string(g));
       for (const AgentId& m : grp->members) group_of[m] = grp.get();
       groups.push_back(std::move(grp));
     }
     // completion gate (orchestrator.cpp:222-276); evaluations run between ticks
-    drv.gate = [&](const AgentId& producer) {
+    drv.gate = [this](const AgentId& producer) {
       auto it = group_of.find(producer);
       if (it == group_of.end() || it->second->exited) {
         drv.release(producer);
         return;
       }
       ExitGroup* grp = it->second;
-      eng.defer([&, producer, grp]() {
+      eng.defer([this, producer, grp]() {
         MetricQRecord rec;
         rec.tick = eng.tick();
         rec.group = grp->index;
         rec.eval_index = grp->evals;
-        rec.completed = producer;
+        rec.completed = producer.topo();
         if (grp->exited) {
           res.metricq.push_back(rec);
           drv.release(producer);
@@ -224,54 +234,88 @@ QueryResult run_query(GpuEngine& eng, const RunConfig& cfg, int sample, bool res
         rec.score = grp->eval->add_completion(eng.d_out_tok(), eng.d_out_lp(), eng.out_offset(producer), n);
         const double q = cfg.force_q ? *cfg.force_q : rec.score.q;
         rec.decision = decide_exit(q, grp->stream);
+        std::vector<AgentId> pruned;
         if (rec.decision.exited) {
           grp->exited = true;
           for (const AgentId& m : grp->members) {
             if (m == producer || eng.finished(m) || eng.cancelled(m)) continue;
-            rec.pruned.push_back(m);
+            pruned.push_back(m);
           }
         }
-        for (const AgentId& m : rec.pruned) drv.prune(m);
+        for (const AgentId& m : pruned) {
+          drv.prune(m);
+          rec.pruned.push_back(m.topo());
+        }
         res.metricq.push_back(rec);
         drv.release(producer);
       });
     };
   }
 
-  eng.mark_start();
-  drv.start();
-  eng.run();
-
-  // roll-up
-  res.agents = drv.order();
-  int last = -1;
-  for (const AgentId& a : res.agents) {
-    const AgentRecord& r = eng.record(a);
-    res.records[a] = r;
-    last = std::max(last, r.complete);
-    if (r.invoked && !r.pruned) res.tokens += r.output_tokens;
-    res.decoded_tokens += eng.decoded(a);
-  }
-  res.ticks = last + 1;
-  res.e2e_ms = eng.ms_since_start(last);
-  res.weight_bytes = eng.bytes_moved();
-  res.rows = eng.rows_processed();
-  res.forwards = eng.kernel_forwards();
-  res.host_ms = eng.host_ms();
-  if (resolve) {
-    for (const AgentId& a : res.agents) {
-      res.prompts[a] = eng.resolve(eng.prompt(a));
-      const int n = eng.record(a).output_tokens;
+  void roll_up(bool resolve) {
+    int last = -1;
+    for (const AgentId& ea : drv.order()) {
+      const AgentId a = ea.topo();
+      res.agents.push_back(a);
+      AgentRecord r = eng.record(ea);
+      r.id = a;
+      res.records[a] = r;
+      last = std::max(last, r.complete);
+      if (r.invoked && !r.pruned) res.tokens += r.output_tokens;
+      res.decoded_tokens += eng.decoded(ea);
+    }
+    res.ticks = last + 1;
+    res.e2e_ms = eng.ms_since_start(last);
+    res.weight_bytes = eng.bytes_moved();
+    res.rows = eng.rows_processed();
+    res.forwards = eng.kernel_forwards();
+    res.host_ms = eng.host_ms();
+    if (!resolve) return;
+    for (const AgentId& ea : drv.order()) {
+      const AgentId a = ea.topo();
+      res.prompts[a] = eng.resolve(eng.prompt(ea));
+      const int n = eng.record(ea).output_tokens;
       TokenSeq out(static_cast<std::size_t>(n));
       std::vector<float> lp(static_cast<std::size_t>(n)), ent(static_cast<std::size_t>(n));
-      if (n > 0) eng.read_outputs(a, n, out.data(), lp.data(), ent.data());
+      if (n > 0) eng.read_outputs(ea, n, out.data(), lp.data(), ent.data());
       res.outputs[a] = std::move(out);
       res.logprobs[a] = std::move(lp);
       res.entropy[a] = std::move(ent);
     }
   }
-  res.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  return res;
+};
+
+}  // namespace
+
+std::vector<QueryResult> run_queries(GpuEngine& eng, const RunConfig& cfg, const std::vector<int>& samples,
+                                     bool resolve) {
+  const auto t0 = std::chrono::steady_clock::now();
+  cfg.validate();
+  if (samples.empty()) throw ValidationError("run: at least one request is required");
+  eng.reset();
+  const std::map<AgentId, int> owner = tree_placement(cfg.topology, eng.world());
+  const int groups_per_request = cfg.topology.agent_count();  // upper bound on exit groups per request
+  std::vector<std::unique_ptr<Request>> reqs;
+  for (std::size_t i = 0; i < samples.size(); ++i) {
+    reqs.push_back(std::make_unique<Request>(eng, cfg, static_cast<int>(i), samples[i],
+                                             static_cast<int>(i) * groups_per_request));
+    reqs.back()->build(owner);
+  }
+  eng.mark_start();
+  for (auto& r : reqs) r->drv.start();
+  eng.run();
+  std::vector<QueryResult> out;
+  const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  for (auto& r : reqs) {
+    r->roll_up(resolve);
+    r->res.wall_ms = wall;
+    out.push_back(std::move(r->res));
+  }
+  return out;
+}
+
+QueryResult run_query(GpuEngine& eng, const RunConfig& cfg, int sample, bool resolve) {
+  return std::move(run_queries(eng, cfg, {sample}, resolve).front());
 }
 
 }  // namespace moa

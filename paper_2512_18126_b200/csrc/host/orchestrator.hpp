@@ -83,4 +83,14 @@ std::map<AgentId, int> tree_placement(const Topology& topo, int world);
 // names).  `resolve` = copy literal prompts/outputs back to the host.
 QueryResult run_query(GpuEngine& eng, const RunConfig& cfg, int sample, bool resolve = true);
 
+// Several independent requests served concurrently by one engine (continuous
+// batching): every request keeps its own prompts, slot plans, exit groups
+// and RNG streams (sample s_i, exactly as run_query(s_i)); their agents share
+// the engine's ticks, so decode rows of all requests ride one weight pass per
+// model.  Results are per request, keyed by the topology's agent ids; e2e_ms
+// is each request's own first-tick -> last-completion latency.  The engine
+// needs capacity for every request's agents.
+std::vector<QueryResult> run_queries(GpuEngine& eng, const RunConfig& cfg, const std::vector<int>& samples,
+                                     bool resolve = true);
+
 }  // namespace moa

@@ -799,6 +799,13 @@ lm_head_kernel(const float* __restrict__ X, const int* __restrict__ sel, const i
   if (threadIdx.x == 0) *cnt = 0;
 }
 
+// chain-overhead probe: waits for its predecessor, releases its dependents,
+// touches one int
+__global__ void noop_kernel(int* p) {
+  MOA_PDL_ENTRY();
+  if (threadIdx.x == 0 && blockIdx.x == 0) p[0] += 1;
+}
+
 inline int grid_for(long long n, int block) {
   long long g = (n + block - 1) / block;
   return static_cast<int>(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
@@ -825,6 +832,8 @@ void init_uniform_rows(bf16* dst, long long rows, long long cols, std::uint64_t 
                        cudaStream_t st) {
   init_uniform_rows_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(dst, rows, cols, base, scale, map, hd);
 }
+
+void noop_chain_link(int* p, int ctas, cudaStream_t st) { launch_pdl(noop_kernel, dim3(ctas), dim3(128), st, p); }
 
 void fill_f32(float* dst, long long n, float v, cudaStream_t st) {
   fill_f32_kernel<<<grid_for(n, 256), 256, 0, st>>>(dst, n, v);

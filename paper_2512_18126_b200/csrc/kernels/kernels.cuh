@@ -46,6 +46,8 @@ void uniform_carveout(const void* fn);
 void init_uniform_rows(bf16* dst, long long rows, long long cols, std::uint64_t base, float scale, int map,
                        int hd, cudaStream_t st);
 void fill_f32(float* dst, long long n, float v, cudaStream_t st);
+// one trivial PDL kernel (measures the per-kernel cost of a launch chain)
+void noop_chain_link(int* p, int ctas, cudaStream_t st);
 
 // Tick metadata in device memory, read by every kernel of a forward so one
 // captured CUDA graph per (rows, context) bucket serves every tick:

@@ -418,3 +418,43 @@ def test_fused_decode_paths_match_oracle(path):
         mm = cfg["models"][tag]
         chk = check_agent(_cpu_model(tag, mm["shape"], mm["seed"]), ga["prompt"], ga["output"], ga["logprobs"])
         assert chk["mismatches"] == [] and chk["lp_ok"], (path, name, chk)
+
+
+@pytest.mark.parametrize("cfg", [C1, C1U], ids=lambda v: v["name"])
+def test_concurrent_requests(cfg):
+    """Continuous batching (moa_run_batch): three requests share the engine's
+    ticks.  Each must be its own request -- prompts, outputs, early-exit
+    evaluations and pruning exactly as the oracle orchestration replays them
+    on that request's completions -- and every agent's stream must pass the
+    teacher-forced oracle check."""
+    samples = [0, 5, 3]
+    eng, qc = capi.engine_for(cfg, concurrency=len(samples))
+    try:
+        gs = eng.run_batch(qc, samples)
+    finally:
+        eng.close()
+    for g, sample in zip(gs, samples):
+        o = _replay(cfg, g, sample)
+        for name, oa in o["agents"].items():
+            ga = g["agents"][name]
+            assert ga["prompt"] == oa["prompt"], (sample, name)
+            assert ga["output"] == oa["output"], (sample, name)
+            for k in ("invoked", "pruned", "empty_input", "prompt_tokens", "output_tokens"):
+                assert ga[k] == int(oa[k]), (sample, name, k)
+        assert g["tokens"] == o["tokens"]
+        assert len(g["metricq"]) == len(o["metricq"])
+        for ge, oe in zip(g["metricq"], o["metricq"]):
+            assert ge["completed"] == oe["completed"] and bool(ge["evaluated"]) == oe["evaluated"]
+            if oe["evaluated"]:
+                assert ge["q"] == pytest.approx(oe["q"], rel=1e-9, abs=1e-12)
+                assert ge["draw"] == oe["draw"]
+                assert bool(ge["exited"]) == oe["exited"]
+                assert ge["pruned"] == oe["pruned"]
+        for name, ga in g["agents"].items():
+            if not ga["output"]:
+                continue
+            tag = cfg["assign"][min(int(name[0]) - 1, len(cfg["assign"]) - 1)]
+            tag = tag[int(name.split(":")[1]) % len(tag)]
+            mm = cfg["models"][tag]
+            chk = check_agent(_cpu_model(tag, mm["shape"], mm["seed"]), ga["prompt"], ga["output"], ga["logprobs"])
+            assert chk["mismatches"] == [] and chk["lp_ok"], (sample, name, chk)
