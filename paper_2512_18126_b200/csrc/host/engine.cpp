@@ -42,7 +42,7 @@ GpuEngine::GpuEngine(std::vector<ModelSpec> models, std::vector<int> agents_per_
     MOA_CUDA(cudaMalloc(&logits_, sizeof(float) * nout * logits_v_));
     MOA_CUDA(cudaMalloc(&logits_scratch_, sizeof(float) * static_cast<long long>(max_slots_) * logits_v_));
   }
-  ring_bytes_ = sizeof(k::RowDesc) * (opt_.max_rows + max_slots_) + sizeof(int) * (2 * max_slots_ + 3);
+  ring_bytes_ = sizeof(k::RowDesc) * (opt_.max_rows + max_slots_) + sizeof(int) * (2 * max_slots_ + 3) + 16;
   for (int i = 0; i < kRing; ++i) {
     Staging s;
     MOA_CUDA(cudaMallocHost(&s.host, ring_bytes_));
@@ -233,8 +233,10 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
     MOA_CUDA(cudaEventSynchronize(s.done));  // the copy that last used this slot has consumed it
     host_wait_ms_ += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wait).count();
   }
+  // staging layout = the device blob: [sel | meta] (padded) then the rows
   const std::size_t rb = sizeof(k::RowDesc) * rows.size();
-  std::memcpy(s.host, rows.data(), rb);
+  const int sb = dm.buffers().sel_bytes;
+  std::memcpy(s.host + sb, rows.data(), rb);
   const int L = dm.max_logit_rows();
   int max_pos = 0;
   long long keys = 0;
@@ -243,14 +245,13 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
     keys += rd.pos + 1;
   }
   // [lsel (L)][lout (L)][meta: R, Rl, max_pos] -- the graph's kernels read meta
-  int* sel = reinterpret_cast<int*>(s.host + rb);
+  int* sel = reinterpret_cast<int*>(s.host);
   std::memcpy(sel, lsel.data(), sizeof(int) * lsel.size());
   std::memcpy(sel + L, lout.data(), sizeof(int) * lout.size());
   sel[2 * L] = static_cast<int>(rows.size());
   sel[2 * L + 1] = static_cast<int>(lsel.size());
   sel[2 * L + 2] = max_pos;
-  MOA_CUDA(cudaMemcpyAsync(dm.buffers().rows, s.host, rb, cudaMemcpyHostToDevice, st));
-  MOA_CUDA(cudaMemcpyAsync(dm.buffers().sel, sel, sizeof(int) * (2 * L + 3), cudaMemcpyHostToDevice, st));
+  MOA_CUDA(cudaMemcpyAsync(dm.buffers().sel, s.host, sb + rb, cudaMemcpyHostToDevice, st));
   MOA_CUDA(cudaEventRecord(s.done, st));
   float* logits = (opt_.keep_logits && !lsel.empty()) ? logits_scratch_ : nullptr;
   dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), max_pos, keys, out_tok_, out_tok_,

@@ -133,8 +133,12 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
                                         static_cast<long long>(k::kGemvTcRows) * lm_grid_));
   dev_alloc(&lm_cnt_, 1);
   MOA_CUDA(cudaMemsetAsync(lm_cnt_, 0, sizeof(int), st));
-  dev_alloc(&buf_.rows, max_rows);
-  dev_alloc(&buf_.sel, 2LL * max_logit_rows + 3);
+  // tick metadata in one allocation, uploaded with one copy per tick:
+  // [sel: lsel (L) | lout (L) | meta (3)] padded to 16 bytes, then the rows
+  buf_.sel_bytes = static_cast<int>(((2LL * max_logit_rows + 3) * sizeof(int) + 15) / 16 * 16);
+  MOA_CUDA(cudaMalloc(&meta_blob_, buf_.sel_bytes + sizeof(k::RowDesc) * static_cast<std::size_t>(max_rows)));
+  buf_.sel = reinterpret_cast<int*>(meta_blob_);
+  buf_.rows = reinterpret_cast<k::RowDesc*>(static_cast<char*>(meta_blob_) + buf_.sel_bytes);
   dev_alloc(&hn_, static_cast<long long>(max_rows) * D);
   // TMA descriptors for the tensor-core prefill path (weights: 128-row boxes)
   tc_ok_ = k::gemm_tc_supported(s.qkv_cols(), D) && k::gemm_tc_supported(D, s.n_heads * s.head_dim) &&
@@ -251,7 +255,7 @@ DeviceModel::~DeviceModel() {
                     static_cast<void*>(kpool_), static_cast<void*>(vpool_), static_cast<void*>(x_),
                     static_cast<void*>(h_), static_cast<void*>(q_), static_cast<void*>(attn_ws_),
                     static_cast<void*>(attn_cnt_), static_cast<void*>(part_), static_cast<void*>(lm_cnt_),
-                    static_cast<void*>(buf_.rows), static_cast<void*>(buf_.sel), static_cast<void*>(hn_),
+                    meta_blob_, static_cast<void*>(hn_),
                     static_cast<void*>(gv_ws_), static_cast<void*>(gv_cnt_), mk_maps_, static_cast<void*>(mk_ssq_),
                     static_cast<void*>(mk_ws_), static_cast<void*>(mk_cnt_), static_cast<void*>(mk_attn_ws_),
                     static_cast<void*>(mk_attn_cnt_), static_cast<void*>(mk_lm_part_), static_cast<void*>(mk_lm_cnt_),

@@ -38,8 +38,9 @@ struct ModelSpec {
 };
 
 struct ForwardBuffers {
-  k::RowDesc* rows = nullptr;  // [max_rows]
+  k::RowDesc* rows = nullptr;  // [max_rows], right after sel in one allocation
   int* sel = nullptr;  // [2 * max_logit_rows + 3]: logits row index, flat output index, meta {R, Rl, max_pos}
+  int sel_bytes = 0;   // sel region padded to 16 bytes (rows start there)
 };
 
 // Per-kernel CUDA-event probes (bench roofline): when attached, forwards run
@@ -176,6 +177,7 @@ class DeviceModel {
   k::LmStat* part_ = nullptr;
   int* lm_cnt_ = nullptr;
   ForwardBuffers buf_;
+  void* meta_blob_ = nullptr;
 };
 
 }  // namespace moa
