@@ -162,6 +162,24 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
     ws = std::max(ws, k::gemv_tc_ws_floats(n, kk));
   dev_alloc(&gv_ws_, ws);
   dev_alloc(&gv_cnt_, (std::max({s.qkv_cols(), 2 * s.ffn, s.d}) + 127) / 128);
+  // RMSNorm folded into the decode GEMVs: ssq partials [16 rows][d/16]
+  dev_alloc(&ssq_, static_cast<long long>(k::kGemvTcRows) * (D / 16));
+  {
+    k::GemvArgs q1, g1, o1, d1;
+    q1.R = g1.R = o1.R = d1.R = k::kGemvTcRows;
+    q1.N = s.qkv_cols(), q1.K = D, g1.N = 2 * s.ffn, g1.K = D;
+    o1.N = D, o1.K = s.n_heads * s.head_dim, d1.N = D, d1.K = s.ffn;
+    q1.ssq = g1.ssq = ssq_;
+    q1.epi = k::kEpiQkv, g1.epi = k::kEpiSwiGlu;
+    o1.epi = d1.epi = k::kEpiResidual;
+    nfold_ok_ = tc_ok_ && D % 16 == 0 && k::gemv_tc_norm_supported(q1) && k::gemv_tc_norm_supported(g1) &&
+                k::gemv_tc_supported(o1) && k::gemv_tc_supported(d1);
+    // opt-in (MOA_NORM_FOLD=1): one kernel fewer per normed GEMV, but the
+    // in-kernel staging puts two dependent round trips (ssq, x) on the
+    // critical path -- measured ~2% slower than the separate rmsnorm kernel
+    use_nfold_ = false;
+    if (const char* e = std::getenv("MOA_NORM_FOLD")) use_nfold_ = std::string(e) != "0";
+  }
   // persistent decode forward: tensor maps in device memory + its scratch
   mk_ok_ = tc_ok_ && k::decode_mk_supported(D, s.n_heads, s.n_kv_heads, hd, s.ffn) && max_rows >= k::kMkRows;
   if (mk_ok_) {
@@ -256,7 +274,7 @@ DeviceModel::~DeviceModel() {
                     static_cast<void*>(h_), static_cast<void*>(q_), static_cast<void*>(attn_ws_),
                     static_cast<void*>(attn_cnt_), static_cast<void*>(part_), static_cast<void*>(lm_cnt_),
                     meta_blob_, static_cast<void*>(hn_),
-                    static_cast<void*>(gv_ws_), static_cast<void*>(gv_cnt_), mk_maps_, static_cast<void*>(mk_ssq_),
+                    static_cast<void*>(gv_ws_), static_cast<void*>(gv_cnt_), static_cast<void*>(ssq_), mk_maps_, static_cast<void*>(mk_ssq_),
                     static_cast<void*>(mk_ws_), static_cast<void*>(mk_cnt_), static_cast<void*>(mk_attn_ws_),
                     static_cast<void*>(mk_attn_cnt_), static_cast<void*>(mk_lm_part_), static_cast<void*>(mk_lm_cnt_),
                     static_cast<void*>(mk_gbar_), static_cast<void*>(mk_trace_), static_cast<void*>(mk_plan_)})
@@ -345,10 +363,18 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   const bool tc = use_tc_ && tc_ok_ && rcap >= k::kTcMinRows;
   // decode ticks of large models: swap-AB tensor-core GEMV (pure weight stream)
   const bool swap_ab = use_tc_ && tc_ok_ && rcap <= k::kGemvTcRows;
+  // decode ticks: RMSNorm folded into the swap-AB GEMV when every normed
+  // GEMV of the model qualifies (the residual producers then write ssq)
+  const bool norm_fold = swap_ab && nfold_ok_ && use_nfold_;
   auto run_gemm = [&](k::GemvArgs& g, const k::TmaMap* map_a, const k::TmaMap* map_a16, const k::TmaMap& map_w) {
     const bool dec_tc = swap_ab && k::gemv_tc_supported(g);
     if (!tc && !dec_tc) {
       k::gemv(g, st);
+      return;
+    }
+    if (g.X && dec_tc && norm_fold) {  // the swap-AB GEMV normalises x itself (ssq from the producer)
+      g.ssq = ssq_;
+      k::gemv_tc(map_w, map_hn16_ /* unused: X is staged in-kernel */, g, gv_ws_, gv_cnt_, st);
       return;
     }
     if (g.X) {  // materialise bf16(rmsnorm(x)) once, then TMA-load it
@@ -378,7 +404,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     probe_end();
   } else {
   probe_begin(KernelProbes::Embed, 6.0 * live_R_ * D);
-  k::embed(buf_.rows, rcap, meta, out_tok_read, emb_, D, x_, st);
+  k::embed(buf_.rows, rcap, meta, out_tok_read, emb_, D, x_, st, norm_fold ? ssq_ : nullptr);
   probe_end();
   }
   for (int l = 0; l < (small ? 0 : s.n_layers); ++l) {
@@ -423,6 +449,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     o.W = L.wo;
     o.epi = k::kEpiResidual;
     o.out = x_;
+    if (norm_fold) o.ssq_out = ssq_;
     probe_begin(KernelProbes::OProj, 2.0 * o.N * o.K + 2.0 * live_R_ * o.K + 8.0 * live_R_ * D);
     run_gemm(o, &map_h_attn_, &map_h_attn16_, wmaps_[static_cast<std::size_t>(l)].wo);
     probe_end();
@@ -451,6 +478,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     dn.W = L.wd;
     dn.epi = k::kEpiResidual;
     dn.out = x_;
+    if (norm_fold) dn.ssq_out = ssq_;
     probe_begin(KernelProbes::Down, 2.0 * dn.N * dn.K + 2.0 * live_R_ * dn.K + 8.0 * live_R_ * D);
     run_gemm(dn, &map_h_ffn_, &map_h_ffn16_, wmaps_[static_cast<std::size_t>(l)].wd);
     probe_end();

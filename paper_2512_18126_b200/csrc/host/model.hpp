@@ -116,6 +116,9 @@ class DeviceModel {
   bool use_graphs_ = true;
   bool use_tc_ = true;  // tensor-core path for ticks with >= kTcMinRows rows
   bool tc_ok_ = false;
+  // RMSNorm folded into the swap-AB decode GEMVs (qkv, gate/up)
+  bool nfold_ok_ = false, use_nfold_ = true;
+  float* ssq_ = nullptr;
   // cluster-resident small-agent forward (small_fwd.cu) for ticks of <= 16 rows
   bool use_small_ = true;
   bool small_ok_ = false;

@@ -225,7 +225,7 @@ __global__ void fill_f32_kernel(float* dst, long long n, float v) {
 
 __global__ void embed_kernel(const RowDesc* __restrict__ rows, const int* __restrict__ meta,
                              const int* __restrict__ out_tok, const bf16* __restrict__ emb, int d,
-                             float* __restrict__ x) {
+                             float* __restrict__ x, float* __restrict__ ssq) {
   MOA_PDL_ENTRY();
   const int r = blockIdx.x;
   if (r >= meta[0]) return;
@@ -238,6 +238,13 @@ __global__ void embed_kernel(const RowDesc* __restrict__ rows, const int* __rest
     float4* o = reinterpret_cast<float4*>(x + static_cast<long long>(r) * d + c);
     o[0] = make_float4(f[0], f[1], f[2], f[3]);
     o[1] = make_float4(f[4], f[5], f[6], f[7]);
+    if (ssq) {  // per-16-column sums of squares (two threads per group) for the next norm
+      float sq = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sq = fmaf(f[i], f[i], sq);
+      sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+      if (!(threadIdx.x & 1)) ssq[static_cast<long long>(r) * (d / 16) + c / 16] = sq;
+    }
   }
 }
 
@@ -840,8 +847,8 @@ void fill_f32(float* dst, long long n, float v, cudaStream_t st) {
 }
 
 void embed(const RowDesc* rows, int R_cap, const int* meta, const int* out_tok, const bf16* emb, int d, float* x,
-           cudaStream_t st) {
-  if (R_cap > 0) launch_pdl(embed_kernel, dim3(R_cap), dim3(128), st, rows, meta, out_tok, emb, d, x);
+           cudaStream_t st, float* ssq) {
+  if (R_cap > 0) launch_pdl(embed_kernel, dim3(R_cap), dim3(128), st, rows, meta, out_tok, emb, d, x, ssq);
 }
 
 void gemv(const GemvArgs& a, cudaStream_t st) {

@@ -27,6 +27,10 @@ constexpr int kM = 128, kN = 16, kBK = 64, kStages = 5;  // 92 KB: two kernels' 
 constexpr int kTileW = kM * kBK * 2;  // 16 KB
 constexpr int kTileX = kN * kBK * 2;  // 2 KB
 constexpr int kSmem = kStages * (kTileW + kTileX) + 1024 + 256;
+// norm-from-x mode: the CTA stages its K range of bf16(rmsnorm(x)) itself
+// (no rmsnorm kernel, no TMA for X): a 4-stage weight ring + <= 16 k-tiles
+constexpr int kNxStages = 4, kNxMaxKt = 16;
+constexpr int kNxSmem = kNxStages * kTileW + kNxMaxKt * kTileX + 1024 + 256;
 constexpr std::uint32_t kIdesc = idesc_bf16(kM, kN);
 
 // debug: per-CTA %globaltimer stamps (tools/gvisolated.py), off when null
@@ -45,7 +49,27 @@ __device__ __forceinline__ void gv_stamp(int ev) {
 
 __device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const float (&v)[16]) {
   const int lane = threadIdx.x & 31;
-  (void)lane;
+  if (a.epi == kEpiResidual && a.ssq_out) {
+    // residual + per-16-column sums of squares of the new rows (the next
+    // RMSNorm's statistics; 16 consecutive lanes = 16 consecutive columns)
+#pragma unroll
+    for (int r = 0; r < kN; ++r) {
+      if (r >= R) break;
+      float nv = 0.f;
+      if (n < a.N) {
+        float* xp = a.out + static_cast<long long>(r) * a.N + n;
+        nv = *xp + v[r];
+        *xp = nv;
+      }
+      float sq = nv * nv;
+      sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+      sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+      sq += __shfl_xor_sync(0xffffffffu, sq, 4);
+      sq += __shfl_xor_sync(0xffffffffu, sq, 8);
+      if ((lane & 15) == 0 && n < a.N) a.ssq_out[static_cast<long long>(r) * (a.N / 16) + n / 16] = sq;
+    }
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < kN; ++r) {
     if (r >= R) break;  // R is CTA-uniform
@@ -195,23 +219,27 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  const bool nx = a.X != nullptr;  // norm-from-x: stage bf16(rmsnorm(x)) in smem, no X TMA
+  const int stages = nx ? kNxStages : kStages;
   unsigned char* sw = smem;
-  unsigned char* sx = smem + kStages * kTileW;
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sx + kStages * kTileX);
+  unsigned char* sx = smem + stages * kTileW;  // per-stage X tiles, or the norm-from-x staging
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sx + (nx ? kNxMaxKt : kStages) * kTileX);
   std::uint64_t* empty = full + kStages;
   std::uint64_t* done = empty + kStages;
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
   __shared__ bool last;
+  __shared__ float inv_s[kN];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x, split = blockIdx.y;
   const int m0 = tile * kM;
   const int KT = a.K / kBK, kt0 = split * KT / S, kt_n = (split + 1) * KT / S - kt0;
+  const std::uint32_t wtx = nx ? kTileW : kTileW + kTileX;
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&map_w);
-    prefetch_tmap(&map_x);
-    for (int s = 0; s < kStages; ++s) {
+    if (!nx) prefetch_tmap(&map_x);
+    for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -231,30 +259,92 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   const std::uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) gv_stamp(1);
 
+  // Weight tiles do not depend on the previous kernel: the first ring's worth
+  // is issued before waiting on it (PDL).
+  int kt_issued = 0;
   if (warp == 0 && lane == 0) {
-    // TMA producer.  Weight tiles do not depend on the previous kernel, so
-    // the first ring's worth is issued before waiting on it (PDL).
-    int kt = 0;
-    for (; kt < kt_n && kt < kStages; ++kt) {
-      mbar_expect_tx(&full[kt], kTileW + kTileX);
-      tma_load_2d(sw + kt * kTileW, &map_w, &full[kt], (kt0 + kt) * kBK, m0);
+    for (; kt_issued < kt_n && kt_issued < stages; ++kt_issued) {
+      mbar_expect_tx(&full[kt_issued], wtx);
+      tma_load_2d(sw + kt_issued * kTileW, &map_w, &full[kt_issued], (kt0 + kt_issued) * kBK, m0);
     }
+  }
+  if (nx) {
+    // Norm-from-x staging by all 128 threads (before the producer / MMA
+    // threads take their roles): inverse RMS of each row from the 16-column
+    // sums of squares its producer wrote, then this CTA's k-tiles of
+    // bf16(x * inv * g) in the 128B-swizzled K-major layout the MMA reads.
     pdl_wait();
-    for (int j = 0; j < kt; ++j) tma_load_2d(sx + j * kTileX, &map_x, &full[j], (kt0 + j) * kBK, 0);
+    const int R = a.meta ? __ldcg(a.meta) : a.R;
+    const int groups = a.K / 16;
+    {
+      const int r = threadIdx.x >> 3, j = threadIdx.x & 7;  // 8 threads per row
+      float ss = 0.f;
+      if (r < R)
+        for (int gidx = j; gidx < groups; gidx += 8) ss += __ldcg(a.ssq + static_cast<long long>(r) * groups + gidx);
+      ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+      ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+      ss += __shfl_xor_sync(0xffffffffu, ss, 4);
+      if (j == 0 && r < kN) inv_s[r] = r < R ? 1.0f / sqrtf(ss / static_cast<float>(a.K) + a.eps) : 0.f;
+    }
+    __syncthreads();
+    const int nchunk = kt_n * R * 8;  // (k-tile, row, 16-byte chunk); rows >= R feed ignored columns
+    for (int c0 = 0; c0 < nchunk; c0 += 128 * 8) {
+      float4 xa[8], xb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int ch = c0 + u * 128 + threadIdx.x;
+        if (ch >= nchunk) continue;
+        const int t = ch / (R * 8), r = (ch >> 3) % R, cc = ch & 7;
+        const float4* xp = reinterpret_cast<const float4*>(a.X + static_cast<long long>(r) * a.K + (kt0 + t) * kBK + cc * 8);
+        xa[u] = __ldcg(xp);
+        xb[u] = __ldcg(xp + 1);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int ch = c0 + u * 128 + threadIdx.x;
+        if (ch >= nchunk) continue;
+        const int t = ch / (R * 8), r = (ch >> 3) % R, cc = ch & 7;
+        const int col = (kt0 + t) * kBK + cc * 8;
+        const float4 g0 = __ldg(reinterpret_cast<const float4*>(a.g + col));
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(a.g + col + 4));
+        const float iv = inv_s[r];
+        __align__(16) bf16 o8[8];
+        o8[0] = __float2bfloat16_rn(xa[u].x * iv * g0.x);
+        o8[1] = __float2bfloat16_rn(xa[u].y * iv * g0.y);
+        o8[2] = __float2bfloat16_rn(xa[u].z * iv * g0.z);
+        o8[3] = __float2bfloat16_rn(xa[u].w * iv * g0.w);
+        o8[4] = __float2bfloat16_rn(xb[u].x * iv * g1.x);
+        o8[5] = __float2bfloat16_rn(xb[u].y * iv * g1.y);
+        o8[6] = __float2bfloat16_rn(xb[u].z * iv * g1.z);
+        o8[7] = __float2bfloat16_rn(xb[u].w * iv * g1.w);
+        *reinterpret_cast<uint4*>(sx + t * kTileX + r * 128 + ((cc ^ (r & 7)) * 16)) = *reinterpret_cast<const uint4*>(o8);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+  }
+
+  if (warp == 0 && lane == 0) {
+    // TMA producer (the rest of the weight stream; activations by TMA unless nx)
+    int kt = kt_issued;
+    if (!nx) {
+      pdl_wait();
+      for (int j = 0; j < kt; ++j) tma_load_2d(sx + j * kTileX, &map_x, &full[j], (kt0 + j) * kBK, 0);
+    }
     for (; kt < kt_n; ++kt) {
-      const int s = kt % kStages;
-      mbar_wait(&empty[s], ((kt / kStages) - 1) & 1);
-      mbar_expect_tx(&full[s], kTileW + kTileX);
+      const int s = kt % stages;
+      mbar_wait(&empty[s], ((kt / stages) - 1) & 1);
+      mbar_expect_tx(&full[s], wtx);
       tma_load_2d(sw + s * kTileW, &map_w, &full[s], (kt0 + kt) * kBK, m0);
-      tma_load_2d(sx + s * kTileX, &map_x, &full[s], (kt0 + kt) * kBK, 0);
+      if (!nx) tma_load_2d(sx + s * kTileX, &map_x, &full[s], (kt0 + kt) * kBK, 0);
     }
   } else if (warp == 1 && lane == 0) {
     for (int kt = 0; kt < kt_n; ++kt) {
-      const int s = kt % kStages;
-      mbar_wait(&full[s], (kt / kStages) & 1);
+      const int s = kt % stages;
+      mbar_wait(&full[s], (kt / stages) & 1);
       if (kt == 0) gv_stamp(2);
       tc_fence_after();
-      const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + s * kTileX);
+      const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + (nx ? kt : s) * kTileX);
 #pragma unroll
       for (int k = 0; k < kBK / 16; ++k) umma_bf16(tmem, umma_desc(w0 + k * 32), umma_desc(x0 + k * 32), kIdesc, (kt | k) ? 1u : 0u);
       umma_commit(&empty[s]);
@@ -557,6 +647,12 @@ long long gemv_tc_ws_floats(int N, int K) {
   return static_cast<long long>((N + kM - 1) / kM) * gemv_tc_splits(N, K, kEpiF32) * kM * kN;
 }
 
+bool gemv_tc_norm_supported(const GemvArgs& a) {
+  const int S = gemv_tc_splits(a.N, a.K, a.epi);
+  const int KT = a.K / kBK;
+  return gemv_tc_supported(a) && (KT + S - 1) / S <= kNxMaxKt && a.K % 16 == 0 && a.ssq != nullptr;
+}
+
 bool gemv_tc_supported(const GemvArgs& a) {
   return a.R <= kN && a.K % kBK == 0 && a.N % 2 == 0 && static_cast<long long>(a.N) * a.K >= (2LL << 20);
 }
@@ -564,7 +660,7 @@ bool gemv_tc_supported(const GemvArgs& a) {
 void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float* ws, int* cnt, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(gemv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem > kNxSmem ? kSmem : kNxSmem);
     uniform_carveout(reinterpret_cast<const void*>(gemv_tc_kernel));
     attr = true;
   }
@@ -572,7 +668,7 @@ void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float*
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((a.N + kM - 1) / kM, S);
   cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = kSmem;
+  cfg.dynamicSmemBytes = a.X ? kNxSmem : kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
   int na = 0;

@@ -53,8 +53,9 @@ void noop_chain_link(int* p, int ctas, cudaStream_t st);
 // captured CUDA graph per (rows, context) bucket serves every tick:
 // meta[0] = live rows R, meta[1] = logits rows Rl, meta[2] = max position.
 // Grids are sized for the bucket caps; CTAs past the live counts exit.
+// ssq (optional): per-16-column sums of squares of the rows [R][d/16]
 void embed(const RowDesc* rows, int R_cap, const int* meta, const int* out_tok, const bf16* emb, int d, float* x,
-           cudaStream_t st);
+           cudaStream_t st, float* ssq = nullptr);
 
 // Fused skinny GEMM  y[r][n] = sum_k A[r][k] W[n][k]  for decode/incremental
 // rows.  A is either bf16 activations or, with `norm`, the fp32 residual rows
@@ -88,6 +89,10 @@ struct GemvArgs {
   float* out_lp = nullptr;
   float* out_ent = nullptr;
   float* logits = nullptr;  // optional fp32 [rows][N]
+  // norm-from-x (gemv_tc): per-16-column sums of squares of the X rows [R][K/16]
+  const float* ssq = nullptr;
+  // kEpiResidual: also write the new rows' per-16-column sums of squares [R][N/16]
+  float* ssq_out = nullptr;
 };
 void gemv(const GemvArgs& a, cudaStream_t st);  // dispatches to gemv_stream for large matrices
 // HBM-streaming variant (gemv_stream.cu): persistent CTAs, cp.async.bulk ring.
@@ -118,6 +123,9 @@ constexpr int kTcMinRows = 17;  // ticks with more rows than the swap-AB GEMV ho
 // kernel has finished.
 constexpr int kGemvTcRows = 16;
 bool gemv_tc_supported(const GemvArgs& a);
+// gemv_tc with X = fp32 residual rows normalised in-kernel (a.X, a.g, a.eps,
+// a.ssq): no separate rmsnorm launch
+bool gemv_tc_norm_supported(const GemvArgs& a);
 int gemv_tc_splits(int N, int K, int epi);
 long long gemv_tc_ws_floats(int N, int K);
 void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float* ws, int* cnt, cudaStream_t st);

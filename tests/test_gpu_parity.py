@@ -15,6 +15,8 @@ Tolerances (stated here):
 import math
 
 import numpy as np
+import os
+
 import pytest
 
 from oracle import metricq as mq
@@ -395,18 +397,26 @@ def test_tensor_core_path_parity(mode):
         assert chk["mismatches"] == [] and chk["lp_ok"], (name, chk)
 
 
-@pytest.mark.parametrize("path", ["megakernel", "small_forward"])
+@pytest.mark.parametrize("path", ["megakernel", "small_forward", "norm_fold"])
 def test_fused_decode_paths_match_oracle(path):
     """The fused decode forwards (persistent grid megakernel; 16-CTA cluster
     forward for small agents) replace the per-kernel chain for ticks of <= 16
     rows: every agent of a C1 request must pass the teacher-forced oracle
     check and the replayed orchestration must match."""
     cfg = dict(C1)
-    eng, qc = capi.engine_for(cfg)
+    if path == "norm_fold":  # the folded norm needs tensor-core-sized matrices: 1B agents, short outputs
+        cfg = dict(CONFIGS["C2"], topology=dict(kind="tree", widths=[2, 1], branching=[2]), assign=[["leaf"], ["agg"]],
+                   out_len=[12, 12], early_exit=False, query_tokens=32, leaf_prefix_tokens=16, agg_prefix_tokens=16,
+                   suffix_tokens=8)
+        os.environ["MOA_NORM_FOLD"] = "1"
+    try:
+        eng, qc = capi.engine_for(cfg)
+    finally:
+        os.environ.pop("MOA_NORM_FOLD", None)
     for m in range(len(cfg["models"])):
         if path == "megakernel":
             eng.megakernel(m, True)
-        else:
+        elif path == "small_forward":
             eng.small_forward(m, True)
     r = eng.run_query(qc, sample=2, resolve=True, detail=True)
     eng.close()
