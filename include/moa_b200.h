@@ -210,6 +210,12 @@ int moa_run_query(moa_engine* eng, const moa_run_config* cfg, int sample, int re
  * capacity for n requests. */
 int moa_run_batch(moa_engine* eng, const moa_run_config* cfg, const int* samples, int n, int resolve,
                   moa_run_summary* summaries, moa_query** out);
+/* RunTrace JSONL of a request (reference format, trace.cpp:209-337; times in
+ * device seconds since the first tick).  Timestamps need engine tracing on
+ * before the request (moa_engine_trace); *len = bytes, written to buf when
+ * cap > *len. */
+int moa_engine_trace(moa_engine* eng, int enable);
+int moa_query_trace(const moa_query* q, char* buf, long long cap, long long* len);
 int moa_query_agent(const moa_query* q, int i, moa_agent_record* rec);
 /* which: 0 = prompt, 1 = output. */
 int moa_query_tokens(const moa_query* q, int i, int which, int32_t* dst, int cap, int* n);

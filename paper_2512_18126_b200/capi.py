@@ -122,6 +122,8 @@ _SIGS = {
                         C.c_int),
     "moa_read_logits": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_float)], C.c_int),
     "moa_agent_state": ([C.c_void_p, C.c_int, C.c_int] + [_P(C.c_int)] * 4, C.c_int),
+    "moa_engine_trace": ([C.c_void_p, C.c_int], C.c_int),
+    "moa_query_trace": ([C.c_void_p, C.c_char_p, C.c_longlong, _P(C.c_longlong)], C.c_int),
     "moa_run_batch": ([C.c_void_p, C.c_void_p, _P(C.c_int), C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
     "moa_run_query": ([C.c_void_p, _P(RunConfigC), C.c_int, C.c_int, _P(RunSummary), _P(C.c_void_p)], C.c_int),
     "moa_query_agent": ([C.c_void_p, C.c_int, _P(AgentRecordC)], C.c_int),
@@ -324,15 +326,26 @@ class Engine:
             out.append(res)
         return out
 
-    def run_query(self, cfg: "QueryConfig", sample=0, resolve=True, detail=True):
+    def trace(self, enable: bool = True):
+        """Record per-tick device times so run_query(..., trace=True) returns a RunTrace JSONL."""
+        check(lib().moa_engine_trace(self.h, int(enable)))
+
+    def run_query(self, cfg: "QueryConfig", sample=0, resolve=True, detail=True, trace=False):
         s = RunSummary()
         q = C.c_void_p()
         check(lib().moa_run_query(self.h, C.byref(cfg.c), sample, int(resolve), C.byref(s),
-                                  C.byref(q) if detail else None))
+                                  C.byref(q) if (detail or trace) else None))
         res = {k: getattr(s, k) for k, _ in RunSummary._fields_}
-        if detail:
+        if detail or trace:
             try:
-                res.update(_query_detail(q, s, resolve))
+                if detail:
+                    res.update(_query_detail(q, s, resolve))
+                if trace:
+                    n = C.c_longlong()
+                    check(lib().moa_query_trace(q, None, 0, C.byref(n)))
+                    buf = C.create_string_buffer(n.value + 1)
+                    check(lib().moa_query_trace(q, buf, n.value + 1, C.byref(n)))
+                    res["trace"] = buf.value.decode()
             finally:
                 lib().moa_query_free(q)
         return res

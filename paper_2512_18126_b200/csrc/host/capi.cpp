@@ -1,6 +1,7 @@
 // extern "C" boundary (include/moa_b200.h).  Exceptions never cross it: they
 // become status codes plus a thread-local message.
 #include "../../../include/moa_b200.h"
+#include "trace.hpp"
 
 #include <cstring>
 #include <memory>
@@ -419,6 +420,20 @@ int moa_run_batch(moa_engine* eng, const moa_run_config* cfg, const int* samples
         out[i] = q.release();
       }
     }
+  });
+}
+
+int moa_engine_trace(moa_engine* eng, int enable) {
+  return guard([&] { E(eng).set_tracing(enable != 0); });
+}
+
+int moa_query_trace(const moa_query* q, char* buf, long long cap, long long* len) {
+  return guard([&] {
+    need(q, "query");
+    need(len, "len");
+    const std::string s = moa::trace_jsonl(q->r);
+    *len = static_cast<long long>(s.size());
+    if (buf && cap > *len) std::memcpy(buf, s.c_str(), s.size() + 1);
   });
 }
 

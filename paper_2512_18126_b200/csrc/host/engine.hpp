@@ -137,7 +137,10 @@ class GpuEngine {
   double bytes_moved() const { return weight_bytes_; }
   long long rows_processed() const { return rows_total_; }
   int kernel_forwards() const { return forwards_; }
-  int overlapped_ticks() const { return overlapped_ticks_; }  // ticks whose model forwards ran on parallel streams
+  int overlapped_ticks() const { return overlapped_ticks_; }
+  // RunTrace timestamps: run_query reads every tick's device time (synchronises)
+  void set_tracing(bool on) { tracing_ = on; }
+  bool tracing() const { return tracing_; }  // ticks whose model forwards ran on parallel streams
   double host_ms() const { return host_ms_; }  // host time spent inside step() (incl. EE syncs)
   double host_api_ms() const { return host_api_ms_; }    // of which: uploads + graph launches
   double host_wait_ms() const { return host_wait_ms_; }  // of which: blocked on the staging ring (GPU behind)
@@ -174,6 +177,7 @@ class GpuEngine {
   std::vector<cudaEvent_t> mdone_;
   cudaEvent_t tick_fork_ = nullptr;
   bool overlap_models_ = true;
+  bool tracing_ = false;
   int overlapped_ticks_ = 0;
   std::vector<std::unique_ptr<DeviceModel>> models_;
   std::map<AgentId, Req> reqs_;

@@ -266,6 +266,18 @@ struct Request {
     }
     res.ticks = last + 1;
     res.e2e_ms = eng.ms_since_start(last);
+    if (eng.tracing())
+      for (int t = 0; t <= last; ++t) res.tick_ms.push_back(eng.ms_since_start(t));
+    for (int m = 0; m < eng.n_models(); ++m) res.model_tags.push_back(eng.model(m).spec().tag);
+    res.seed = cfg.seed;
+    res.sample = sample;
+    res.topology_kind = cfg.topology.kind();
+    res.mode = static_cast<int>(cfg.mode);
+    res.early_exit = cfg.early_exit;
+    res.hidden = cfg.hidden;
+    res.provider_seed = cfg.provider_seed;
+    res.tau = cfg.tau;
+    res.include_diagonal = cfg.include_diagonal;
     res.weight_bytes = eng.bytes_moved();
     res.rows = eng.rows_processed();
     res.forwards = eng.kernel_forwards();

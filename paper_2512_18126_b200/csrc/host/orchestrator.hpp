@@ -70,6 +70,18 @@ struct QueryResult {
   long long rows = 0;
   int forwards = 0;
   double host_ms = 0.0;  // host time inside engine ticks
+  // trace context (RunTrace JSONL, trace.hpp)
+  std::vector<double> tick_ms;  // device ms at the end of each tick (engine tracing on)
+  std::vector<std::string> model_tags;
+  std::uint64_t seed = 0;
+  int sample = 0;
+  TopologyKind topology_kind = TopologyKind::Tree;
+  int mode = 3;
+  bool early_exit = false;
+  int hidden = 64;
+  std::uint64_t provider_seed = 0;
+  double tau = kDefaultTau;
+  bool include_diagonal = true;
 };
 
 // GPU placement along the tree: leaves are spread in

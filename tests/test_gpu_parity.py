@@ -468,3 +468,30 @@ def test_concurrent_requests(cfg):
             mm = cfg["models"][tag]
             chk = check_agent(_cpu_model(tag, mm["shape"], mm["seed"]), ga["prompt"], ga["output"], ga["logprobs"])
             assert chk["mismatches"] == [] and chk["lp_ok"], (sample, name, chk)
+
+
+@pytest.mark.parametrize("sample", [0, 3])
+def test_trace_replay_verifier(sample):
+    """RunTrace JSONL of a GPU request (reference format) re-scored by the
+    reference's own MetricQEvaluator over the GPU's completion order
+    (tools/replay_verify.py): every evaluation's q, draw and exit decision."""
+    ref_lib = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "libmoaref.so")
+    if not os.path.exists(ref_lib):
+        pytest.skip("reference build (oracle/_ref) not present")
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "replay_verify", os.path.join(os.path.dirname(ref_lib), "..", "..", "tools", "replay_verify.py"))
+    rv = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(rv)
+    eng, qc = capi.engine_for(C1U)
+    eng.trace(True)
+    try:
+        r = eng.run_query(qc, sample=sample, resolve=True, detail=True, trace=True)
+    finally:
+        eng.close()
+    meta, agents, evals = rv.parse(r["trace"])
+    assert meta["mode"] == "tree|incremental-overlap|ee" and len(agents) == 7
+    assert meta["e2e_latency"] == pytest.approx(r["e2e_ms"] / 1e3)
+    res = rv.verify(r["trace"])
+    assert res["ok"], res["failures"]
+    assert res["evaluations_checked"] == sum(1 for e in r["metricq"] if e["evaluated"]) > 0
