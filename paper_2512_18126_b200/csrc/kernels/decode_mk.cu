@@ -587,6 +587,146 @@ __device__ __noinline__ void embed_phase(const MkParams& P, int R, int G) {
   }
 }
 
+// Stage one GEMV phase's activation k-tiles into smem (workers, warps 0-5):
+// rows < `rows` only (MMA columns are independent, stale rows only feed
+// ignored outputs); the norm statistics and the activations load in the same
+// round trip.  Out of line: its own register allocation (no spills).
+__device__ __noinline__ void stage_activations(const MkParams& P, const Gemv g, const MkCtaPlan& pl, int rows,
+                                               const Smem& sm) {
+  const int wt = threadIdx.x;
+        constexpr int U = 4;
+        const int nchunk = pl.nkt * rows * 8;  // (k-tile, row, 16-byte chunk)
+        float ssq_part = 0.f;
+        if (g.xsrc != XS_BF16 && wt < kN * 8) {  // 8 threads per row sum the row's tile partials
+          const int r = wt >> 3, j = wt & 7;
+          if (r < rows) {
+            const int src = g.xsrc == XS_NORM_SEL ? __ldg(P.sel + r) : r;
+            const int tiles = P.D / kM;
+            for (int t = j; t < tiles; t += 8) ssq_part += __ldcg(P.ssq + src * tiles + t);
+          }
+        }
+        uint4 out[U];
+        float4 ra[U], rb[U];
+        int dst[U], col[U], rr[U];
+        for (int base = 0; base < nchunk; base += kWorkers * U) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int ch = base + u * kWorkers + wt;
+            dst[u] = -1;
+            if (ch >= nchunk) continue;
+            const int si = ch / (rows * 8), r = (ch >> 3) % rows, cc = ch & 7;
+            const int kt = pl.kt[si];
+            rr[u] = r;
+            dst[u] = (kt % P.xs_kt) * kTileX + r * 128 + ((cc ^ (r & 7)) * 16);
+            col[u] = kt * kBK + cc * 8;
+            if (g.xsrc == XS_BF16) {
+              out[u] = __ldcg(reinterpret_cast<const uint4*>(g.xb + static_cast<long long>(r) * g.K + col[u]));
+            } else {
+              const int src = g.xsrc == XS_NORM_SEL ? __ldg(P.sel + r) : r;
+              const float4* xp = reinterpret_cast<const float4*>(P.x + static_cast<long long>(src) * P.D + col[u]);
+              ra[u] = __ldcg(xp);
+              rb[u] = __ldcg(xp + 1);
+            }
+          }
+          if (g.xsrc != XS_BF16) {
+            if (base == 0) {  // finish the norm statistics: 8 partials per row -> inv
+              float t = ssq_part;
+              t += __shfl_xor_sync(0xffffffffu, t, 1);
+              t += __shfl_xor_sync(0xffffffffu, t, 2);
+              t += __shfl_xor_sync(0xffffffffu, t, 4);
+              if (wt < kN * 8 && (wt & 7) == 0) sm.inv[wt >> 3] = 1.0f / sqrtf(t / static_cast<float>(P.D) + P.eps);
+              named_sync(1, kWorkers);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              if (dst[u] < 0) continue;
+              const float iv = sm.inv[rr[u]];
+              const float4 ga = __ldg(reinterpret_cast<const float4*>(P.g + col[u]));
+              const float4 gb = __ldg(reinterpret_cast<const float4*>(P.g + col[u] + 4));
+              __align__(16) bf16 o8[8];
+              o8[0] = __float2bfloat16_rn(ra[u].x * iv * ga.x);
+              o8[1] = __float2bfloat16_rn(ra[u].y * iv * ga.y);
+              o8[2] = __float2bfloat16_rn(ra[u].z * iv * ga.z);
+              o8[3] = __float2bfloat16_rn(ra[u].w * iv * ga.w);
+              o8[4] = __float2bfloat16_rn(rb[u].x * iv * gb.x);
+              o8[5] = __float2bfloat16_rn(rb[u].y * iv * gb.y);
+              o8[6] = __float2bfloat16_rn(rb[u].z * iv * gb.z);
+              o8[7] = __float2bfloat16_rn(rb[u].w * iv * gb.w);
+              out[u] = *reinterpret_cast<const uint4*>(o8);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (dst[u] >= 0) *reinterpret_cast<uint4*>(sm.xs + dst[u]) = out[u];
+        }
+}
+
+// The GEMV epilogues of one phase for this CTA's segments (warps 0-3):
+// tcgen05.ld, split-K partials + deterministic last-arriver reduction, fused
+// epilogue.  Returns the running segment counter.  Out of line (registers).
+__device__ __noinline__ int gemv_epilogues(const MkParams& P, const Gemv g, const MkCtaPlan& pl, int rows,
+                                           const Smem& sm, std::uint32_t tmem, int sc, int c, int p) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      for (int i = 0; i < pl.nseg; ++i) {
+        const MkSeg s = pl.seg[i];
+        const int b = sc & 1;
+        mbar_wait_g(&sm.acc_full[b], (sc >> 1) & 1);
+        tc_fence_after();
+        if (threadIdx.x == 0 && i == 0) stamp(P, p, 3);
+        float v[kN];
+        tmem_ld16(tmem + b * kN + (static_cast<std::uint32_t>(warp * 32) << 16), v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.acc_empty[b]);
+        ++sc;
+        const int n = s.t * kM + warp * 32 + lane;
+        const int nseg = s.c_last - s.c_first + 1;
+        if (nseg > 1) {
+          // split-K: partial of this CTA; the last arriver sums all in CTA order
+          float4* pw = reinterpret_cast<float4*>(P.ws + ((static_cast<long long>(c) * 2 + s.slot_self) * kM +
+                                                         warp * 32 + lane) * kN);
+#pragma unroll
+          for (int j = 0; j < kN / 4; ++j) __stcg(pw + j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+          named_sync(2, 128);
+          if (threadIdx.x == 0)
+            sm.flag[1] =
+                atom_add_acq_rel(reinterpret_cast<unsigned*>(P.cnt + s.t), 1u) == static_cast<unsigned>(nseg - 1);
+          named_sync(2, 128);
+          if (!sm.flag[1]) continue;
+#pragma unroll
+          for (int j = 0; j < kN; ++j) v[j] = 0.f;
+          // partials of 4 CTAs in flight per round trip, summed in CTA order
+          for (int c0 = s.c_first; c0 <= s.c_last; c0 += 2) {
+            float4 t4[2][kN / 4];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int cc = c0 + k;
+              if (cc > s.c_last) break;
+              const int slot = cc == s.c_first ? s.first_slot : 0;
+              const float4* pr = reinterpret_cast<const float4*>(
+                  P.ws + ((static_cast<long long>(cc) * 2 + slot) * kM + warp * 32 + lane) * kN);
+#pragma unroll
+              for (int j = 0; j < kN / 4; ++j) t4[k][j] = __ldcg(pr + j);
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              if (c0 + k > s.c_last) break;
+#pragma unroll
+              for (int j = 0; j < kN / 4; ++j) {
+                v[4 * j] += t4[k][j].x;
+                v[4 * j + 1] += t4[k][j].y;
+                v[4 * j + 2] += t4[k][j].z;
+                v[4 * j + 3] += t4[k][j].w;
+              }
+            }
+          }
+          if (threadIdx.x == 0) __stcg(P.cnt + s.t, 0);
+        }
+        epi_store(P, g, n, rows, v, sm, s.t);
+      }
+  return sc;
+}
+
 // ---------------- the kernel ----------------
 
 __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const MkParams P) {
@@ -718,74 +858,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const MkParams P
       const MkCtaPlan& pl = sm.plan[shape_of(kind)];
       const int rows = kind == PK_LM ? Rl : R;
       if (pl.nseg > 0) {
-        // ---- stage this phase's activation k-tiles (rows < `rows` only: MMA
-        // columns are independent, stale rows only feed ignored outputs).
-        // The norm statistics and the activations load in the same round trip.
-        constexpr int U = 8;
-        const int nchunk = pl.nkt * rows * 8;  // (k-tile, row, 16-byte chunk)
-        float ssq_part = 0.f;
-        if (g.xsrc != XS_BF16 && wt < kN * 8) {  // 8 threads per row sum the row's tile partials
-          const int r = wt >> 3, j = wt & 7;
-          if (r < rows) {
-            const int src = g.xsrc == XS_NORM_SEL ? __ldg(P.sel + r) : r;
-            const int tiles = P.D / kM;
-            for (int t = j; t < tiles; t += 8) ssq_part += __ldcg(P.ssq + src * tiles + t);
-          }
-        }
-        uint4 out[U];
-        float4 ra[U], rb[U];
-        int dst[U], col[U], rr[U];
-        for (int base = 0; base < nchunk; base += kWorkers * U) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int ch = base + u * kWorkers + wt;
-            dst[u] = -1;
-            if (ch >= nchunk) continue;
-            const int si = ch / (rows * 8), r = (ch >> 3) % rows, cc = ch & 7;
-            const int kt = pl.kt[si];
-            rr[u] = r;
-            dst[u] = (kt % P.xs_kt) * kTileX + r * 128 + ((cc ^ (r & 7)) * 16);
-            col[u] = kt * kBK + cc * 8;
-            if (g.xsrc == XS_BF16) {
-              out[u] = __ldcg(reinterpret_cast<const uint4*>(g.xb + static_cast<long long>(r) * g.K + col[u]));
-            } else {
-              const int src = g.xsrc == XS_NORM_SEL ? __ldg(P.sel + r) : r;
-              const float4* xp = reinterpret_cast<const float4*>(P.x + static_cast<long long>(src) * P.D + col[u]);
-              ra[u] = __ldcg(xp);
-              rb[u] = __ldcg(xp + 1);
-            }
-          }
-          if (g.xsrc != XS_BF16) {
-            if (base == 0) {  // finish the norm statistics: 8 partials per row -> inv
-              float t = ssq_part;
-              t += __shfl_xor_sync(0xffffffffu, t, 1);
-              t += __shfl_xor_sync(0xffffffffu, t, 2);
-              t += __shfl_xor_sync(0xffffffffu, t, 4);
-              if (wt < kN * 8 && (wt & 7) == 0) sm.inv[wt >> 3] = 1.0f / sqrtf(t / static_cast<float>(P.D) + P.eps);
-              named_sync(1, kWorkers);
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              if (dst[u] < 0) continue;
-              const float iv = sm.inv[rr[u]];
-              const float4 ga = __ldg(reinterpret_cast<const float4*>(P.g + col[u]));
-              const float4 gb = __ldg(reinterpret_cast<const float4*>(P.g + col[u] + 4));
-              __align__(16) bf16 o8[8];
-              o8[0] = __float2bfloat16_rn(ra[u].x * iv * ga.x);
-              o8[1] = __float2bfloat16_rn(ra[u].y * iv * ga.y);
-              o8[2] = __float2bfloat16_rn(ra[u].z * iv * ga.z);
-              o8[3] = __float2bfloat16_rn(ra[u].w * iv * ga.w);
-              o8[4] = __float2bfloat16_rn(rb[u].x * iv * gb.x);
-              o8[5] = __float2bfloat16_rn(rb[u].y * iv * gb.y);
-              o8[6] = __float2bfloat16_rn(rb[u].z * iv * gb.z);
-              o8[7] = __float2bfloat16_rn(rb[u].w * iv * gb.w);
-              out[u] = *reinterpret_cast<const uint4*>(o8);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (dst[u] >= 0) *reinterpret_cast<uint4*>(sm.xs + dst[u]) = out[u];
-        }
+        stage_activations(P, g, pl, rows, sm);
         fence_proxy_async_smem();
         named_sync(1, kWorkers);
         if (wt == 0) {
@@ -795,63 +868,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const MkParams P
       }
       if (!epi) continue;
       // ---------------- epilogue (warps 0-3) ----------------
-      for (int i = 0; i < pl.nseg; ++i) {
-        const MkSeg s = pl.seg[i];
-        const int b = sc & 1;
-        mbar_wait_g(&sm.acc_full[b], (sc >> 1) & 1);
-        tc_fence_after();
-        if (threadIdx.x == 0 && i == 0) stamp(P, p, 3);
-        float v[kN];
-        tmem_ld16(tmem + b * kN + (static_cast<std::uint32_t>(warp * 32) << 16), v);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.acc_empty[b]);
-        ++sc;
-        const int n = s.t * kM + warp * 32 + lane;
-        const int nseg = s.c_last - s.c_first + 1;
-        if (nseg > 1) {
-          // split-K: partial of this CTA; the last arriver sums all in CTA order
-          float4* pw = reinterpret_cast<float4*>(P.ws + ((static_cast<long long>(c) * 2 + s.slot_self) * kM +
-                                                         warp * 32 + lane) * kN);
-#pragma unroll
-          for (int j = 0; j < kN / 4; ++j) __stcg(pw + j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-          named_sync(2, 128);
-          if (threadIdx.x == 0)
-            sm.flag[1] =
-                atom_add_acq_rel(reinterpret_cast<unsigned*>(P.cnt + s.t), 1u) == static_cast<unsigned>(nseg - 1);
-          named_sync(2, 128);
-          if (!sm.flag[1]) continue;
-#pragma unroll
-          for (int j = 0; j < kN; ++j) v[j] = 0.f;
-          // partials of 4 CTAs in flight per round trip, summed in CTA order
-          for (int c0 = s.c_first; c0 <= s.c_last; c0 += 2) {
-            float4 t4[2][kN / 4];
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const int cc = c0 + k;
-              if (cc > s.c_last) break;
-              const int slot = cc == s.c_first ? s.first_slot : 0;
-              const float4* pr = reinterpret_cast<const float4*>(
-                  P.ws + ((static_cast<long long>(cc) * 2 + slot) * kM + warp * 32 + lane) * kN);
-#pragma unroll
-              for (int j = 0; j < kN / 4; ++j) t4[k][j] = __ldcg(pr + j);
-            }
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              if (c0 + k > s.c_last) break;
-#pragma unroll
-              for (int j = 0; j < kN / 4; ++j) {
-                v[4 * j] += t4[k][j].x;
-                v[4 * j + 1] += t4[k][j].y;
-                v[4 * j + 2] += t4[k][j].z;
-                v[4 * j + 3] += t4[k][j].w;
-              }
-            }
-          }
-          if (threadIdx.x == 0) __stcg(P.cnt + s.t, 0);
-        }
-        epi_store(P, g, n, rows, v, sm, s.t);
-      }
+      sc = gemv_epilogues(P, g, pl, rows, sm, tmem, sc, c, p);
       named_sync(2, 128);
       if (threadIdx.x == 0) {
         stamp(P, p, 4);

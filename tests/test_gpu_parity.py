@@ -495,3 +495,52 @@ def test_trace_replay_verifier(sample):
     res = rv.verify(r["trace"])
     assert res["ok"], res["failures"]
     assert res["evaluations_checked"] == sum(1 for e in r["metricq"] if e["evaluated"]) > 0
+
+
+# ---- the reference's early-exit known answers (test_orchestrator.cpp:140-256)
+# on the preset's 9-3-1 tree, with GPU agents (tiny shape, outputs ~U(24, 96)
+# so completions inside a cluster are spread over ticks) ----
+_PRESET_931 = dict(CONFIGS["C4-tree"], name="EE-931", out_len=[[24, 96], [24, 96], 64], early_exit=True,
+                   workload="9-3-1 tree, tiny agents, outputs ~U(24,96)")
+
+
+def _ee_run(cfg, sample=0):
+    g = _gpu_query(cfg, sample)
+    o = _replay(cfg, g, sample)
+    for name, oa in o["agents"].items():  # orchestration parity first
+        assert g["agents"][name]["prompt"] == oa["prompt"], name
+        assert bool(g["agents"][name]["pruned"]) == oa["pruned"], name
+    return g
+
+
+def test_never_exiting_evaluator_leaves_schedule_identical():
+    """force_q = 0 (test_orchestrator.cpp:140-170): every completion below the
+    root is evaluated (9 proposers + 3 mid aggregators = 12), none exits, and
+    the schedule equals early-exit off tick for tick."""
+    off = _gpu_query(dict(_PRESET_931, early_exit=False))
+    on = _ee_run(dict(_PRESET_931, force_q=0.0))
+    assert sum(1 for e in on["metricq"] if e["evaluated"]) == 12
+    assert all(not e["exited"] and not e["pruned"] for e in on["metricq"])
+    for name, a in off["agents"].items():
+        b = on["agents"][name]
+        assert (b["decode_start"], b["complete"], b["output"]) == (a["decode_start"], a["complete"], a["output"]), name
+        assert not b["pruned"]
+    assert on["ticks"] == off["ticks"]
+
+
+@pytest.mark.parametrize("scope,groups", [("cluster", 4), ("layer", 2)])
+def test_certain_exit_prunes_unfinished_members(scope, groups):
+    """force_q = 1 (test_orchestrator.cpp:193-256): each exit group exits at
+    its first completion -- one evaluation per group (4 with cluster scope: 3
+    leaf clusters + the mid cluster; 2 with layer scope), q = 1, every member
+    still running at that moment is pruned, the root is never gated."""
+    g = _ee_run(dict(_PRESET_931, force_q=1.0, exit_scope=scope))
+    evald = [e for e in g["metricq"] if e["evaluated"]]
+    assert len(evald) == groups
+    assert all(e["exited"] and e["q"] == 1.0 for e in evald)
+    assert not g["agents"]["3:0"]["pruned"] and g["agents"]["3:0"]["invoked"]
+    pruned = {n for n, a in g["agents"].items() if a["pruned"]}
+    named = {p for e in evald for p in e["pruned"]}
+    assert pruned == named and len(pruned) >= 1
+    for n in pruned:  # pruned agents stopped early
+        assert g["agents"][n]["output_tokens"] < 96
