@@ -269,8 +269,8 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
     w_first[c] = (n0 + c < a.N && kb + lane * 8 < ke)
                      ? ldg_stream(a.W + static_cast<long long>(n0 + c) * a.K + kb + lane * 8)
                      : make_uint4(0, 0, 0, 0);
+  const int live = a.meta ? __ldg(a.meta) : a.R;  // tick metadata: not produced by the previous kernel
   MOA_PDL_ENTRY();
-  const int live = a.meta ? __ldg(a.meta) : a.R;
   if (r0 >= live) return;  // uniform across the CTA
   const int rows = min(kRB, live - r0);
   if constexpr (NORM) {
@@ -525,7 +525,6 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
                      int nkv, const bf16* __restrict__ kpool, const bf16* __restrict__ vpool, long long kv_stride,
                      long long layer_off, int max_ctx, bf16* __restrict__ o, float* __restrict__ ws,
                      int* __restrict__ cnt, int nsplit_max, int split_keys) {
-  MOA_PDL_ENTRY();
   constexpr int NW = 8, HPG = 4, E = HD / 32;
   __shared__ float qs[HPG][HD];
   __shared__ float wm[NW][HPG], wl[NW][HPG];
@@ -534,6 +533,8 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.x, g = blockIdx.y, s = blockIdx.z;
+  // Tick metadata and the keys of earlier ticks are not produced by this
+  // forward's previous kernel: read / prefetch them before the PDL wait.
   if (r >= __ldg(meta)) return;
   const RowDesc rd = rows[r];
   const int n = rd.pos + 1;
@@ -543,6 +544,11 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
   const int kb = s * split_keys, ke = min(n, kb + split_keys);
   const bf16* K = kpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
   const bf16* V = vpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
+  for (int j = kb + threadIdx.x; j < ke - 1 && j < kb + 2 * NW * 32; j += NW * 32) {  // old keys only (pos is new)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(K + static_cast<long long>(j) * HD));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(V + static_cast<long long>(j) * HD));
+  }
+  MOA_PDL_ENTRY();
   for (int i = threadIdx.x; i < hpg * HD; i += NW * 32)
     qs[i / HD][i % HD] = __bfloat162float(q[(static_cast<long long>(r) * nh + g * hpg + i / HD) * HD + i % HD]);
   __syncthreads();

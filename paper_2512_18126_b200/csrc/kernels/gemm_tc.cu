@@ -244,11 +244,11 @@ __global__ void __launch_bounds__(128) rmsnorm_rows_kernel(const float* __restri
                                                            const float* __restrict__ g, float eps,
                                                            bf16* __restrict__ h) {
   __shared__ float red[4];
+  const int i = blockIdx.x;
+  if (i >= meta[meta_idx]) return;  // tick metadata: not produced by the previous kernel
+  const int r = sel ? sel[i] : i;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int i = blockIdx.x;
-  if (i >= meta[meta_idx]) return;
-  const int r = sel ? sel[i] : i;
   const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long long>(r) * K);
   float ss = 0.f;
   for (int v = threadIdx.x; v < K / 4; v += 128) {

@@ -247,6 +247,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     mbar_fence_init();
   }
   if (threadIdx.x == 0) gv_stamp(0);
+  const int R = a.meta ? __ldcg(a.meta) : a.R;  // tick metadata: not produced by the previous kernel
   // Dependents may launch now: they prefetch their own weights while this
   // grid runs, then wait (griddepcontrol.wait) for its completion before
   // reading its outputs.  Grids are sized to one CTA per SM, so this grid and
@@ -274,7 +275,6 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     // sums of squares its producer wrote, then this CTA's k-tiles of
     // bf16(x * inv * g) in the 128B-swizzled K-major layout the MMA reads.
     pdl_wait();
-    const int R = a.meta ? __ldcg(a.meta) : a.R;
     const int groups = a.K / 16;
     {
       const int r = threadIdx.x >> 3, j = threadIdx.x & 7;  // 8 threads per row
@@ -357,7 +357,6 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   tc_fence_after();
   if (threadIdx.x == 0) gv_stamp(3);
 
-  const int R = a.meta ? __ldcg(a.meta) : a.R;
   const int row = warp * 32 + lane, n = m0 + row;
   float v[16];
   tmem_ld16(tmem + (static_cast<std::uint32_t>(warp * 32) << 16), v);
@@ -519,8 +518,8 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
     __syncwarp();
   } else {
     // epilogue warps 2-5: TMEM lane quarter = warp % 4
+    const int R = a.meta ? __ldcg(a.meta) : a.R;  // tick metadata, before the PDL wait
     pdl_wait();
-    const int R = a.meta ? __ldcg(a.meta) : a.R;
     const int ew = warp - 2, quarter = warp & 3;
     const int et = threadIdx.x - 64;  // 0..127
     for (int t = t0; t < t1; ++t) {
