@@ -168,6 +168,8 @@ typedef struct {
   int query_tokens, leaf_prefix_tokens, agg_prefix_tokens, separator_tokens, suffix_tokens;
   int hidden; /* mock embedding width (ProviderSpec::hidden) */
   uint64_t provider_seed;
+  int embed_model; /* -1: MockProvider; >= 0: hidden states of this engine model (EmbeddingProvider,
+                      embedding.hpp:38-44; width = its d_model) */
 } moa_run_config;
 
 typedef struct {

@@ -32,6 +32,9 @@ def run_config(cfg: dict) -> RunConfig:
     kw = {k: cfg[k] for k in keys if k in cfg}
     if cfg.get("force_q") is not None:
         kw["force_q"] = cfg["force_q"]
+    if cfg.get("provider", "mock") == "hidden":  # hidden-state provider: the embedding model's final rows
+        em = models_of(cfg, 1024)[cfg["embed_model"]]
+        kw["embed_fn"] = em.hidden_embed
     return RunConfig(topology=topo, assign=assign, out_len=out_len, **kw)
 
 

@@ -174,6 +174,25 @@ class CpuModel:
         ascending position order.  Returns (logits[n_out, V]) for rows whose
         want_logits flag is set."""
         sp, w = self.spec, self.w
+        x = self.layers(rows)
+        sel = np.nonzero(np.asarray(want_logits, bool))[0]
+        if len(sel) == 0:
+            return np.zeros((0, sp.vocab), np.float32)
+        hf = bf16_round(rmsnorm(x[sel], sp.norm_eps))
+        return hf @ w.lm.T
+
+    def hidden_embed(self, tokens) -> np.ndarray:
+        """Hidden-state embedding provider (csrc ee_hidden_embed): the final
+        residual rows of `tokens` at positions 0..n-1 on a fresh KV,
+        RMS-normalised in fp64: e[r] = x[r] / sqrt(mean(x[r]^2) + eps)."""
+        kv = self.new_kv()
+        x = self.layers([(kv, i, int(t)) for i, t in enumerate(tokens)]).astype(np.float64)
+        inv = 1.0 / np.sqrt((x * x).sum(axis=1) / x.shape[1] + self.spec.norm_eps)
+        return x * inv[:, None]
+
+    def layers(self, rows):
+        """The transformer layers over a ragged batch of rows: final residual x [R, d] (fp32)."""
+        sp, w = self.spec, self.w
         R = len(rows)
         hd, nh, nkv = sp.head_dim, sp.n_heads, sp.n_kv_heads
         half = hd // 2
@@ -212,8 +231,4 @@ class CpuModel:
             u = h2 @ L["wu"].T
             a = bf16_round(g / (np.float32(1.0) + np.exp(-g)) * u)
             x = x + a @ L["wd"].T
-        sel = np.nonzero(np.asarray(want_logits, bool))[0]
-        if len(sel) == 0:
-            return np.zeros((0, sp.vocab), np.float32)
-        hf = bf16_round(rmsnorm(x[sel], sp.norm_eps))
-        return hf @ w.lm.T
+        return x

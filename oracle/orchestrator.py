@@ -12,7 +12,7 @@ streams, gate semantics, pruning rule -- is the reference's.
 from __future__ import annotations
 
 from dataclasses import dataclass, field
-from typing import Optional
+from typing import Callable, Optional
 
 from . import metricq as mq
 from .engine import TickEngine
@@ -45,6 +45,9 @@ class RunConfig:
     suffix_tokens: int = 32
     hidden: int = 64
     provider_seed: int = 0
+    # embedding provider: None = MockProvider(hidden, provider_seed); else a
+    # callable tokens -> fp64 [n, h] (the hidden-state provider, CpuModel.hidden_embed)
+    embed_fn: Optional[Callable] = None
 
     def validate(self):
         """orchestrator.cpp:21-62."""
@@ -172,8 +175,8 @@ def exit_groups(cfg: RunConfig, ss: int):
     groups = []
     for g, members in enumerate(sets):
         label = f"ee:{g}"
-        ev = mq.MetricQEvaluator(lambda t: mq.mock_embed(t, cfg.hidden, cfg.provider_seed),
-                                 cfg.tau, cfg.include_diagonal)
+        embed = cfg.embed_fn or (lambda t: mq.mock_embed(t, cfg.hidden, cfg.provider_seed))
+        ev = mq.MetricQEvaluator(embed, cfg.tau, cfg.include_diagonal)
         groups.append(ExitGroup(label, members, ev, RngStream.derive_from(ss, label)))
     return groups
 

@@ -64,7 +64,7 @@ class RunConfigC(C.Structure):
                 ("use_force_q", C.c_int), ("force_q", C.c_double), ("chunk_size", C.c_int),
                 ("seed", C.c_uint64), ("query_tokens", C.c_int), ("leaf_prefix_tokens", C.c_int),
                 ("agg_prefix_tokens", C.c_int), ("separator_tokens", C.c_int), ("suffix_tokens", C.c_int),
-                ("hidden", C.c_int), ("provider_seed", C.c_uint64)]
+                ("hidden", C.c_int), ("provider_seed", C.c_uint64), ("embed_model", C.c_int)]
 
 
 class RunSummary(C.Structure):
@@ -424,7 +424,8 @@ class QueryConfig:
             query_tokens=cfg["query_tokens"], leaf_prefix_tokens=cfg["leaf_prefix_tokens"],
             agg_prefix_tokens=cfg["agg_prefix_tokens"], separator_tokens=cfg["separator_tokens"],
             suffix_tokens=cfg["suffix_tokens"], hidden=cfg.get("hidden", 64),
-            provider_seed=cfg.get("provider_seed", 0))
+            provider_seed=cfg.get("provider_seed", 0),
+            embed_model=model_index[cfg["embed_model"]] if cfg.get("provider", "mock") == "hidden" else -1)
 
 
 def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16384, gemv_only=False, concurrency=1):
@@ -436,6 +437,8 @@ def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16
     for l, w in enumerate(t["widths"]):
         for p in range(w):
             counts[_configs.agent_tag(cfg, l + 1, p)] += 1
+    if cfg.get("provider", "mock") == "hidden":  # the hidden-state provider reserves one KV slot of its model
+        counts[cfg["embed_model"]] += 1
     tags = list(cfg["models"])
     specs = [model_spec(tag, cfg["models"][tag]["shape"], cfg["models"][tag].get("seed", 0),
                         max_agents=max(1, counts[tag] * concurrency)) for tag in tags]

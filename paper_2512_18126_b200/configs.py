@@ -61,7 +61,15 @@ C4_TREE = dict(copy.deepcopy(C0), name="C4-tree", workload="tree 9-3-1 (13 tiny 
 C4_DENSE = dict(copy.deepcopy(C0), name="C4-dense", workload="all-to-all 6-6-1 (13 tiny agents)",
                 topology=dict(kind="all_to_all", widths=[6, 6, 1]))
 
-CONFIGS = {c["name"]: c for c in (C0, C1, C1U, C2, C3, C4_TREE, C4_DENSE)}
+# C1 with the hidden-state embedding provider: the
+# semantic agreement is measured on the final hidden states of a separate
+# random-init embedding model (the Qwen3-Embedding analogue)
+# instead of the MockProvider hash embeddings.
+C1H = dict(copy.deepcopy(C1U), name="C1H", provider="hidden", embed_model="embed",
+           models=dict(leaf=dict(shape="tiny", seed=1), agg=dict(shape="tiny", seed=2), embed=dict(shape="tiny", seed=7)),
+           workload="C1U with the hidden-state embedding provider (tiny embedding model, h = 256)")
+
+CONFIGS = {c["name"]: c for c in (C0, C1, C1U, C1H, C2, C3, C4_TREE, C4_DENSE)}
 
 
 def agent_tag(cfg: dict, layer: int, position: int) -> str:

@@ -127,6 +127,7 @@ moa::RunConfig run_config_of(const moa_run_config* c) {
   cfg.suffix_tokens = c->suffix_tokens;
   cfg.hidden = c->hidden;
   cfg.provider_seed = c->provider_seed;
+  cfg.embed_model = c->embed_model;
   return cfg;
 }
 

@@ -521,6 +521,23 @@ void GpuEngine::reset() {
   overlapped_ticks_ = 0;
   host_ms_ = host_api_ms_ = host_wait_ms_ = 0.0;
   for (auto& m : models_) m->reset_bindings();
+  embed_kv_.clear();
+}
+
+void GpuEngine::hidden_embed(int m, const AgentId& src, int n, GpuMetricQ& ev) {
+  if (m < 0 || m >= n_models()) throw ValidationError("provider: embedding model index out of range");
+  DeviceModel& dm = *models_[static_cast<std::size_t>(m)];
+  if (ev.hidden() != dm.spec().d) throw ValidationError("provider: evaluator width differs from the embedding model");
+  if (n > opt_.max_ctx) throw ValidationError("provider: completion longer than the embedding model's context");
+  auto it = embed_kv_.find(m);
+  if (it == embed_kv_.end()) it = embed_kv_.emplace(m, dm.bind_agent()).first;
+  const Req& r = req(src);
+  std::vector<k::RowDesc> rows;
+  rows.reserve(static_cast<std::size_t>(n));
+  for (int i = 0; i < n; ++i) rows.push_back(k::RowDesc{it->second, i, ref(r.slot, i), -1});
+  upload_and_forward(m, rows, {}, {}, stream_);
+  k::ee_hidden_embed(dm.residual(), n, dm.spec().d, dm.spec().norm_eps, ev.emb_buffer(), stream_);
+  MOA_CUDA(cudaGetLastError());
 }
 
 GpuMetricQ& GpuEngine::ee_evaluator(int i, int hidden, std::uint64_t seed, double tau, bool diag, int members,

@@ -130,6 +130,11 @@ class GpuEngine {
   // Pooled early-exit evaluator #i (device buffers reused across requests).
   GpuMetricQ& ee_evaluator(int i, int hidden, std::uint64_t seed, double tau, bool diag, int members,
                            int max_tokens);
+  // Hidden-state embedding provider: the first n output tokens of `src` run
+  // through model `m` (positions 0..n-1 in a KV slot reserved for this duty),
+  // and the final residual rows, RMS-normalised in fp64, land in the
+  // evaluator's embedding buffer.  Runs on the engine stream between ticks.
+  void hidden_embed(int m, const AgentId& src, int n, GpuMetricQ& ev);
 
   // Timing: event recorded at run start / after a tick (time_ticks).
   void mark_start();
@@ -178,6 +183,7 @@ class GpuEngine {
   cudaEvent_t tick_fork_ = nullptr;
   bool overlap_models_ = true;
   bool tracing_ = false;
+  std::map<int, int> embed_kv_;  // model -> reserved KV slot of the hidden-state provider
   int overlapped_ticks_ = 0;
   std::vector<std::unique_ptr<DeviceModel>> models_;
   std::map<AgentId, Req> reqs_;

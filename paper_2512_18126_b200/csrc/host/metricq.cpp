@@ -82,12 +82,22 @@ GpuMetricQ::~GpuMetricQ() {
 QualityScore GpuMetricQ::add_completion(const int* d_tok, const float* d_lp, long long base, int n) {
   if (n <= 0) throw ValidationError("logprobs: need at least one token");
   if (n > max_tokens_) throw ValidationError("metricq: completion longer than the evaluator capacity");
+  k::ee_mock_embed(d_tok, base, n, hidden_, seed_, d_emb_, st_);
+  return finish(d_lp, base, n);
+}
+
+QualityScore GpuMetricQ::add_completion_embedded(const float* d_lp, long long base, int n) {
+  if (n <= 0) throw ValidationError("logprobs: need at least one token");
+  if (n > max_tokens_) throw ValidationError("metricq: completion longer than the evaluator capacity");
+  return finish(d_lp, base, n);
+}
+
+QualityScore GpuMetricQ::finish(const float* d_lp, long long base, int n) {
   const int m = completions();
   if (m >= max_members_) throw ValidationError("metricq: exit group capacity exceeded");
   const long long hh = static_cast<long long>(hidden_) * hidden_;
   double* corr_new = d_corrs_ + hh * m;
   k::ee_confidence(d_lp + base, n, d_out_, st_);
-  k::ee_mock_embed(d_tok, base, n, hidden_, seed_, d_emb_, st_);
   k::ee_corr(d_emb_, n, hidden_, 1e-12, d_gram_, corr_new, st_);
   k::ee_fcs(corr_new, d_corrs_, m, hidden_, d_out_ + 1, st_);
   MOA_CUDA(cudaMemcpyAsync(h_out_, d_out_, sizeof(double) * (1 + m), cudaMemcpyDeviceToHost, st_));

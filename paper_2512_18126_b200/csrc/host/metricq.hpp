@@ -48,6 +48,10 @@ class GpuMetricQ {
   // Completion = n device tokens at d_tok[base..] with fp32 logprobs at
   // d_lp[base..].  Synchronises the stream once (reads C and the sim row).
   QualityScore add_completion(const int* d_tok, const float* d_lp, long long base, int n);
+  // Same with the embedding rows already in emb_buffer() (hidden-state provider).
+  QualityScore add_completion_embedded(const float* d_lp, long long base, int n);
+  double* emb_buffer() { return d_emb_; }
+  int hidden() const { return hidden_; }
   int completions() const { return static_cast<int>(conf_.size()); }
   // Reuse the device buffers for a new group (no reallocation).
   bool fits(int hidden, int max_members, int max_tokens) const {
@@ -62,6 +66,7 @@ class GpuMetricQ {
   }
 
  private:
+  QualityScore finish(const float* d_lp, long long base, int n);
   QualityScore current() const;
   int hidden_;
   std::uint64_t seed_;

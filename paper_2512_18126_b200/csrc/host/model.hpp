@@ -95,6 +95,7 @@ class DeviceModel {
   int max_rows() const { return max_rows_; }
   int max_logit_rows() const { return max_lrows_; }
   const ForwardBuffers& buffers() const { return buf_; }
+  const float* residual() const { return x_; }  // final residual rows of the last forward
 
   // R rows / Rl logits rows already resident in buffers(); out_* are the
   // engine's flat per-agent output arrays; logits (optional) [Rl][V] fp32.

@@ -203,7 +203,8 @@ struct Request {
       auto grp = std::make_unique<ExitGroup>();
       grp->index = static_cast<int>(g);
       for (const AgentId& m : sets[g]) grp->members.push_back(id(m));
-      grp->eval = &eng.ee_evaluator(group_base + static_cast<int>(g), cfg.hidden, cfg.provider_seed, cfg.tau,
+      const int width = cfg.embed_model >= 0 ? eng.model(cfg.embed_model).spec().d : cfg.hidden;
+      grp->eval = &eng.ee_evaluator(group_base + static_cast<int>(g), width, cfg.provider_seed, cfg.tau,
                                     cfg.include_diagonal, static_cast<int>(sets[g].size()), std::max(1, max_out));
       grp->stream = rng::Stream::derive(ss, "ee:" + std::to_string(g));
       for (const AgentId& m : grp->members) group_of[m] = grp.get();
@@ -231,7 +232,12 @@ struct Request {
         grp->evals += 1;
         rec.evaluated = true;
         const int n = eng.record(producer).output_tokens;
-        rec.score = grp->eval->add_completion(eng.d_out_tok(), eng.d_out_lp(), eng.out_offset(producer), n);
+        if (cfg.embed_model >= 0) {
+          eng.hidden_embed(cfg.embed_model, producer, n, *grp->eval);
+          rec.score = grp->eval->add_completion_embedded(eng.d_out_lp(), eng.out_offset(producer), n);
+        } else {
+          rec.score = grp->eval->add_completion(eng.d_out_tok(), eng.d_out_lp(), eng.out_offset(producer), n);
+        }
         const double q = cfg.force_q ? *cfg.force_q : rec.score.q;
         rec.decision = decide_exit(q, grp->stream);
         std::vector<AgentId> pruned;

@@ -39,6 +39,9 @@ struct RunConfig {  // orchestrator.hpp:23-53 (+ model per agent, which replaces
       suffix_tokens = 32;
   int hidden = 64;
   std::uint64_t provider_seed = 0;
+  // embedding provider: -1 = the reference's MockProvider (hidden, provider_seed);
+  // >= 0 = hidden states of engine model `embed_model` (width = its d_model)
+  int embed_model = -1;
 
   void validate() const;
 };

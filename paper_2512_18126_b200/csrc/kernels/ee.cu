@@ -139,6 +139,34 @@ void ee_mock_embed(const int* out_tok, long long base, int n, int h, std::uint64
                                                                                           seed, emb);
 }
 
+// hidden-state embedding rows: e[r][c] = x[r][c] / sqrt(mean(x[r]^2) + eps) in
+// fp64 from the fp32 final residual rows (the oracle's hidden_embed)
+__global__ void hidden_embed_kernel(const float* __restrict__ x, int d, double eps, double* __restrict__ emb) {
+  __shared__ double red[32];
+  const int r = blockIdx.x;
+  double ss = 0.0;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    const double v = x[static_cast<long long>(r) * d + c];
+    ss = fma(v, v, ss);
+  }
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+    red[0] = 1.0 / sqrt(t / d + eps);
+  }
+  __syncthreads();
+  const double inv = red[0];
+  for (int c = threadIdx.x; c < d; c += blockDim.x)
+    emb[static_cast<long long>(r) * d + c] = static_cast<double>(x[static_cast<long long>(r) * d + c]) * inv;
+}
+
+void ee_hidden_embed(const float* x, int n, int d, double eps, double* emb, cudaStream_t st) {
+  if (n > 0) hidden_embed_kernel<<<n, 256, 0, st>>>(x, d, eps, emb);
+}
+
 void ee_corr(const double* emb, int n, int h, double eps, double* gram, double* corr, cudaStream_t st) {
   const long long total = static_cast<long long>(h) * h;
   const int blocks = static_cast<int>((total + 255) / 256 < 592 ? (total + 255) / 256 : 592);

@@ -255,6 +255,9 @@ void ee_confidence(const float* lp, int n, double* c, cudaStream_t st);
 // MockProvider rows for tokens out_tok[base .. base+n) (embedding.cpp:91-113).
 void ee_mock_embed(const int* out_tok, long long base, int n, int h, std::uint64_t seed, double* emb,
                    cudaStream_t st);
+// Hidden-state provider rows: emb[r][c] = x[r][c] / sqrt(mean(x[r]^2) + eps)
+// (fp64) from the embedding model's fp32 final residual rows.
+void ee_hidden_embed(const float* x, int n, int d, double eps, double* emb, cudaStream_t st);
 // corr = correlation_from_gram(emb^T emb) (metricq.cpp:32-53), h x h.
 void ee_corr(const double* emb, int n, int h, double eps, double* gram, double* corr, cudaStream_t st);
 // sim[j] = frob_cos_sim_corr(corr_new, corrs[j]) for j < m (metricq.cpp:55-64).

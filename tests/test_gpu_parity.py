@@ -544,3 +544,29 @@ def test_certain_exit_prunes_unfinished_members(scope, groups):
     assert pruned == named and len(pruned) >= 1
     for n in pruned:  # pruned agents stopped early
         assert g["agents"][n]["output_tokens"] < 96
+
+
+def test_hidden_state_provider():
+    """Hidden-state embedding provider: the early-exit
+    agreement is computed on the final hidden states of a separate embedding
+    model run over each completion on the GPU.  The oracle recomputes every
+    evaluation with its CPU model on the GPU's completions: q agrees to 2e-3
+    (fp32 hidden states through different accumulation orders), and every
+    exit decision whose margin |q - draw| exceeds that tolerance is identical."""
+    cfg = CONFIGS["C1H"]
+    g = _gpu_query(cfg, 3)
+    o = _replay(cfg, g, 3)
+    evald = [e for e in g["metricq"] if e["evaluated"]]
+    assert evald, "no early-exit evaluation ran"
+    oe_by = {(e["completed"], e["eval_index"]): e for e in o["metricq"] if e["evaluated"]}
+    decisive = 0
+    for e in evald:
+        oe = oe_by.get((e["completed"], e["eval_index"]))
+        if oe is None:  # the replay diverged after an earlier near-tie decision
+            continue
+        assert e["q"] == pytest.approx(oe["q"], abs=2e-3), e
+        assert e["draw"] == oe["draw"]
+        if abs(oe["q"] - oe["draw"]) > 2e-3:
+            assert bool(e["exited"]) == oe["exited"], e
+            decisive += 1
+    assert decisive >= 1

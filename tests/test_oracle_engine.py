@@ -97,3 +97,20 @@ def test_force_q_gate_rules():
     n0 = run_query(run_config(dict(base, early_exit=False)), tiny_models(base), 1)
     assert {k: v["output"] for k, v in n0["agents"].items()} == {k: v["output"] for k, v in o0["agents"].items()}
     assert n0["e2e_ticks"] == o0["e2e_ticks"]
+
+
+def test_oracle_hidden_state_provider():
+    """The oracle's hidden-state provider (CpuModel.hidden_embed) feeds the
+    MetricQ evaluator: rows are unit-RMS fp64, a C1H request evaluates."""
+    import numpy as np
+    from oracle.configs import models_of, run_config
+    from oracle.orchestrator import run_query
+    from paper_2512_18126_b200.configs import CONFIGS
+    cfg = dict(CONFIGS["C1H"], out_len=[[8, 16], 8, 8], query_tokens=16, leaf_prefix_tokens=8,
+               agg_prefix_tokens=8, suffix_tokens=4)
+    rc = run_config(cfg)
+    e = rc.embed_fn([5, 17, 99])
+    assert e.shape == (3, 256) and e.dtype == np.float64
+    assert np.allclose((e * e).mean(axis=1), 1.0, rtol=1e-4)
+    r = run_query(rc, models_of(cfg, 256), 0)
+    assert any(m["evaluated"] for m in r["metricq"])
