@@ -240,9 +240,12 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   const int L = dm.max_logit_rows();
   int max_pos = 0;
   long long keys = 0;
-  for (const auto& rd : rows) {
+  bool distinct = rows.size() <= 64;  // every row a different agent (pure decode)?
+  for (std::size_t i = 0; i < rows.size(); ++i) {
+    const auto& rd = rows[i];
     max_pos = std::max(max_pos, rd.pos);
     keys += rd.pos + 1;
+    for (std::size_t j = 0; j < i && distinct; ++j) distinct = rows[j].kv != rd.kv;
   }
   // [lsel (L)][lout (L)][meta: R, Rl, max_pos] -- the graph's kernels read meta
   int* sel = reinterpret_cast<int*>(s.host);
@@ -255,7 +258,7 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   MOA_CUDA(cudaEventRecord(s.done, st));
   float* logits = (opt_.keep_logits && !lsel.empty()) ? logits_scratch_ : nullptr;
   dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), max_pos, keys, out_tok_, out_tok_,
-             out_lp_, out_ent_, logits, st);
+             out_lp_, out_ent_, logits, st, distinct);
   if (logits) {  // debug path: scatter each logits row to its (slot, k) home
     const long long V = dm.spec().vocab;
     for (std::size_t i = 0; i < lsel.size(); ++i)

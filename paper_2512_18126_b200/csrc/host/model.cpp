@@ -162,6 +162,8 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
     ws = std::max(ws, k::gemv_tc_ws_floats(n, kk));
   dev_alloc(&gv_ws_, ws);
   dev_alloc(&gv_cnt_, (std::max({s.qkv_cols(), 2 * s.ffn, s.d}) + 127) / 128);
+  qkv_attn_ok_ = k::qkv_attention_supported(D, s.n_heads, s.n_kv_heads, static_cast<int>(hd));
+  if (const char* e = std::getenv("MOA_QKV_ATTN")) use_qkv_attn_ = std::string(e) != "0";
   // RMSNorm folded into the decode GEMVs: ssq partials [16 rows][d/16]
   dev_alloc(&ssq_, static_cast<long long>(k::kGemvTcRows) * (D / 16));
   {
@@ -317,7 +319,7 @@ int pow2_at_least(int v, int lo) {
 }  // namespace
 
 void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int* out_tok_read, int* out_tok,
-                          float* out_lp, float* out_ent, float* logits, cudaStream_t st) {
+                          float* out_lp, float* out_ent, float* logits, cudaStream_t st, bool distinct) {
   if (R <= 0) return;
   if (R > max_rows_) throw RunError("model " + spec_.tag + ": tick rows exceed workspace");
   if (Rl > max_lrows_ || Rl > k::kLmMaxRows) throw RunError("model " + spec_.tag + ": logits rows exceed workspace");
@@ -330,15 +332,16 @@ void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int*
     live_R_ = R;
     live_Rl_ = Rl;
     live_keys_ = keys;
-    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st);
+    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st, distinct);
     return;
   }
-  const auto key = std::make_tuple(rcap, nsplit, (Rl > 0 ? 1 : 0) | (use_tc_ ? 2 : 0) | (use_mk_ ? 4 : 0), logits ? 1 : 0);
+  const auto key = std::make_tuple(rcap, nsplit, (Rl > 0 ? 1 : 0) | (use_tc_ ? 2 : 0) | (use_mk_ ? 4 : 0) |
+                                                     (distinct ? 8 : 0), logits ? 1 : 0);
   auto it = graphs_.find(key);
   if (it == graphs_.end()) {
     cudaGraph_t g = nullptr;
     MOA_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st);
+    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st, distinct);
     MOA_CUDA(cudaStreamEndCapture(st, &g));
     cudaGraphExec_t exec = nullptr;
     MOA_CUDA(cudaGraphInstantiate(&exec, g, 0));
@@ -349,7 +352,7 @@ void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int*
 }
 
 void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_tok_read, int* out_tok,
-                         float* out_lp, float* out_ent, float* logits, cudaStream_t st) {
+                         float* out_lp, float* out_ent, float* logits, cudaStream_t st, bool distinct) {
   const ModelSpec& s = spec_;
   const int D = s.d, hd = s.head_dim, nh = s.n_heads, nkv = s.n_kv_heads;
   const float eps = static_cast<float>(s.norm_eps);
@@ -407,9 +410,17 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   k::embed(buf_.rows, rcap, meta, out_tok_read, emb_, D, x_, st, norm_fold ? ssq_ : nullptr);
   probe_end();
   }
+  // decode ticks of small agents: RMSNorm + QKV + RoPE + KV append + attention in one launch
+  const bool qkv_attn = !small && use_tc_ && use_qkv_attn_ && qkv_attn_ok_ && distinct && rcap <= k::kGemvTcRows;
   for (int l = 0; l < (small ? 0 : s.n_layers); ++l) {
     const Layer& L = layers_[static_cast<std::size_t>(l)];
     const long long loff = layer_stride_ * l;
+    if (qkv_attn) {
+      probe_begin(KernelProbes::Attention, 2.0 * s.qkv_cols() * D + 4.0 * live_keys_ * nkv * hd + 4.0 * live_R_ * D);
+      k::qkv_attention(x_, ones_, eps, D, L.wqkv, buf_.rows, rcap, meta, rope_, nh, nkv, hd, kpool_, vpool_, kv_stride_,
+                       loff, max_ctx_, h_, st);
+      probe_end();
+    } else {
     // rmsnorm -> QKV -> RoPE -> KV append
     k::GemvArgs qkv;
     qkv.X = x_;
@@ -439,6 +450,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     k::attention(q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_,
                  attn_ws_, attn_cnt_, st);
     probe_end();
+    }
     // x += o . Wo^T
     k::GemvArgs o;
     o.A = h_;

@@ -99,9 +99,9 @@ class DeviceModel {
 
   // R rows / Rl logits rows already resident in buffers(); out_* are the
   // engine's flat per-agent output arrays; logits (optional) [Rl][V] fp32.
+  // distinct: every row belongs to a different agent (a pure decode tick)
   void forward(int R, int Rl, int max_pos, long long keys, const int* out_tok_read, int* out_tok, float* out_lp,
-               float* out_ent,
-               float* logits, cudaStream_t st);
+               float* out_ent, float* logits, cudaStream_t st, bool distinct = false);
 
   // Algorithmic bytes one forward must move for weights (every tick reads the
   // full weight set once) -- the roofline basis.
@@ -110,7 +110,8 @@ class DeviceModel {
 
  private:
   void launch(int rcap, int nsplit, bool with_logits, const int* out_tok_read, int* out_tok, float* out_lp,
-              float* out_ent, float* logits, cudaStream_t st);
+              float* out_ent, float* logits, cudaStream_t st, bool distinct);
+  bool qkv_attn_ok_ = false, use_qkv_attn_ = true;  // fused QKV + attention for small-agent decode ticks
   std::map<std::tuple<int, int, int, int>, cudaGraphExec_t> graphs_;
   ModelSpec spec_;
   int max_agents_, max_ctx_, max_rows_, max_lrows_;

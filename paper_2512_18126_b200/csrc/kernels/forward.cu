@@ -703,6 +703,224 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
   if (threadIdx.x == 0) cnt[r * nkv + g] = 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// Decode-tick QKV + attention in one kernel for small agents (every row is
+// the only row of its agent: pure decode).  CTA = (row, kv head): its
+// (hpg + 2) * hd rows of Wqkv (the group's q heads, k, v -- three contiguous
+// slabs) stream into smem by bulk copy *before* the PDL wait (weights never
+// depend on the previous kernel), then the row is RMS-normalised from the
+// residual, the CTA computes its q/k/v columns (warp = 32 columns, lanes split
+// K, one transpose-reduce), applies RoPE, appends k/v at the row's position
+// and runs the group's attention (warps split the keys, online softmax,
+// smem combine).  Replaces two launches and the q round trip through HBM.
+template <int HD>
+__global__ void __launch_bounds__(256, 1)
+qkv_attention_kernel(const float* __restrict__ X, const float* __restrict__ g_norm, float eps, int D,
+                     const bf16* __restrict__ wqkv, const RowDesc* __restrict__ rows, const int* __restrict__ meta,
+                     const float2* __restrict__ rope, int nh, int nkv, bf16* __restrict__ kpool,
+                     bf16* __restrict__ vpool, long long kv_stride, long long layer_off, int max_ctx,
+                     bf16* __restrict__ o) {
+  constexpr int NW = 8, HPG = 4, E = HD / 32, half = HD / 2;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ float qs[HPG][HD];
+  __shared__ float wm[NW][HPG], wl[NW][HPG];
+  __shared__ float wo[NW][HPG][HD];
+  __shared__ float cm_s[HPG], cl_s[HPG];
+  __shared__ float red[NW];
+  __shared__ __align__(8) unsigned long long wbar;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.x, g = blockIdx.y;
+  const int hpg = nh / nkv, ncol = (hpg + 2) * HD;
+  bf16* W = reinterpret_cast<bf16*>(dsm);                          // [ncol][D]
+  bf16* xn = reinterpret_cast<bf16*>(dsm + static_cast<long long>(ncol) * D * 2);  // [D]
+  if (r >= __ldg(meta)) return;  // tick metadata: not produced by the previous kernel
+  const RowDesc rd = rows[r];
+  const int n = rd.pos + 1;
+  const bf16* K = kpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
+  const bf16* V = vpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
+  const std::uint32_t bar = static_cast<std::uint32_t>(__cvta_generic_to_shared(&wbar));
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned qb = hpg * HD * D * 2, kb = HD * D * 2;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(qb + 2 * kb));
+    const bf16* srcs[3] = {wqkv + static_cast<long long>(g * hpg * HD) * D,
+                           wqkv + static_cast<long long>((nh + g) * HD) * D,
+                           wqkv + static_cast<long long>((nh + nkv + g) * HD) * D};
+    const unsigned bytes[3] = {qb, kb, kb};
+    unsigned off = 0;
+    for (int i = 0; i < 3; ++i) {
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              static_cast<std::uint32_t>(__cvta_generic_to_shared(dsm + off))),
+          "l"(srcs[i]), "r"(bytes[i]), "r"(bar)
+          : "memory");
+      off += bytes[i];
+    }
+  }
+  for (int j = threadIdx.x; j < n - 1 && j < 2 * NW * 32; j += NW * 32) {  // keys of earlier ticks
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(K + static_cast<long long>(j) * HD));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(V + static_cast<long long>(j) * HD));
+  }
+  MOA_PDL_ENTRY();
+  // RMS norm of the residual row -> bf16 (the oracle's rounding point)
+  const float* x = X + static_cast<long long>(r) * D;
+  float ss = 0.f;
+  for (int c = threadIdx.x * 4; c < D; c += 256 * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(x + c);
+    ss = fmaf(v.x, v.x, ss);
+    ss = fmaf(v.y, v.y, ss);
+    ss = fmaf(v.z, v.z, ss);
+    ss = fmaf(v.w, v.w, ss);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) red[warp] = ss;
+  __syncthreads();
+  float tot = 0.f;
+  for (int w = 0; w < NW; ++w) tot += red[w];
+  const float inv = 1.0f / sqrtf(tot / static_cast<float>(D) + eps);
+  for (int c = threadIdx.x; c < D; c += 256) xn[c] = __float2bfloat16_rn(x[c] * inv * g_norm[c]);
+  // weights landed
+  {
+    std::uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}\n"
+                   : "=r"(ok)
+                   : "r"(bar)
+                   : "memory");
+  }
+  __syncthreads();
+  // q/k/v columns: warp w takes column groups of 32 (lanes split K)
+  for (int grp = warp; grp < ncol / 32; grp += NW) {
+    float acc[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+    for (int k = lane * 8; k < D; k += 256) {
+      float xf[8];
+      unpack8(*reinterpret_cast<const uint4*>(xn + k), xf);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = dot8(xf, *reinterpret_cast<const uint4*>(W + static_cast<long long>(grp * 32 + j) * D + k), acc[j]);
+    }
+    const float v = transpose_reduce32(acc, lane);
+    const float partner = __shfl_xor_sync(kFull, v, 1);
+    const int c = grp * 32 + lane;  // column within the CTA's slab
+    if (c < (hpg + 1) * HD) {       // q or k: rotate the (even, odd) pair
+      const int e = (c % HD) / 2;
+      const float2 cs = rope[static_cast<long long>(rd.pos) * half + e];
+      const float y = (lane & 1) ? __fadd_rn(__fmul_rn(v, cs.x), __fmul_rn(partner, cs.y))
+                                 : __fsub_rn(__fmul_rn(v, cs.x), __fmul_rn(partner, cs.y));
+      const int d = e + ((lane & 1) ? half : 0);  // natural dim
+      const bf16 yb = __float2bfloat16_rn(y);
+      if (c < hpg * HD)
+        qs[c / HD][d] = __bfloat162float(yb);
+      else
+        const_cast<bf16*>(K)[static_cast<long long>(rd.pos) * HD + d] = yb;
+    } else {
+      const_cast<bf16*>(V)[static_cast<long long>(rd.pos) * HD + (c - (hpg + 1) * HD)] = __float2bfloat16_rn(v);
+    }
+  }
+  __threadfence_block();
+  __syncthreads();
+  // attention over keys 0..pos (this row's own key included, just appended)
+  constexpr int TPK = HD / 64, KC = 32 / TPK;
+  const int key = lane / TPK, part = lane % TPK;
+  using VT = typename std::conditional<E == 2, unsigned, uint2>::type;
+  const float scale = rsqrtf(static_cast<float>(HD));
+  float m[HPG], l[HPG], acc[HPG][E];
+#pragma unroll
+  for (int h = 0; h < HPG; ++h) {
+    m[h] = -INFINITY;
+    l[h] = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[h][e] = 0.f;
+  }
+  for (int j0 = warp * KC; j0 < n; j0 += NW * KC) {
+    const int j = j0 + key;
+    uint4 kk[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+      kk[v] = j < n ? __ldcg(reinterpret_cast<const uint4*>(K + static_cast<long long>(j) * HD + part * 64) + v)
+                    : make_uint4(0, 0, 0, 0);
+    VT vv[KC];
+#pragma unroll
+    for (int jj = 0; jj < KC; ++jj)
+      vv[jj] = j0 + jj < n ? __ldcg(reinterpret_cast<const VT*>(V + static_cast<long long>(j0 + jj) * HD + lane * E)) : VT{};
+#pragma unroll
+    for (int h = 0; h < HPG; ++h) {
+      if (h >= hpg) break;
+      float d = 0.f;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        float f[8];
+        unpack8(kk[v], f);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) d = fmaf(qs[h][part * 64 + v * 8 + t], f[t], d);
+      }
+      if constexpr (TPK == 2) d += __shfl_xor_sync(kFull, d, 1);
+      const float sc = j < n ? d * scale : -INFINITY;
+      float cmax = sc;
+#pragma unroll
+      for (int off = 16; off; off >>= 1) cmax = fmaxf(cmax, __shfl_xor_sync(kFull, cmax, off));
+      const float mn = fmaxf(m[h], cmax);
+      const float resc = m[h] == -INFINITY ? 0.f : __expf(m[h] - mn);
+      const float p = j < n ? __expf(sc - mn) : 0.f;
+      l[h] = l[h] * resc + warp_sum(part == 0 ? p : 0.f);
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[h][e] *= resc;
+#pragma unroll
+      for (int jj = 0; jj < KC; ++jj) {
+        const float pj = __shfl_sync(kFull, p, jj * TPK);
+        if constexpr (E == 2) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv[jj]));
+          acc[h][0] = fmaf(pj, f.x, acc[h][0]);
+          acc[h][1] = fmaf(pj, f.y, acc[h][1]);
+        } else {
+          const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv[jj].x));
+          const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv[jj].y));
+          acc[h][0] = fmaf(pj, f0.x, acc[h][0]);
+          acc[h][1] = fmaf(pj, f0.y, acc[h][1]);
+          acc[h][2] = fmaf(pj, f1.x, acc[h][2]);
+          acc[h][3] = fmaf(pj, f1.y, acc[h][3]);
+        }
+      }
+      m[h] = mn;
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < HPG; ++h) {
+    if (h >= hpg) break;
+    if (lane == 0) {
+      wm[warp][h] = m[h];
+      wl[warp][h] = l[h];
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) wo[warp][h][lane * E + e] = acc[h][e];
+  }
+  __syncthreads();
+  if (threadIdx.x < hpg) {
+    const int h = threadIdx.x;
+    float M = -INFINITY;
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, wm[w][h]);
+    float Ls = 0.f;
+    for (int w = 0; w < NW; ++w) Ls += wm[w][h] == -INFINITY ? 0.f : __expf(wm[w][h] - M) * wl[w][h];
+    cm_s[h] = M;
+    cl_s[h] = Ls;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < hpg * HD; i += NW * 32) {
+    const int h = i / HD, e = i % HD;
+    const float M = cm_s[h];
+    float val = 0.f;
+    for (int w = 0; w < NW; ++w)
+      if (wm[w][h] != -INFINITY) val += __expf(wm[w][h] - M) * wo[w][h][e];
+    o[(static_cast<long long>(r) * nh + g * hpg + h) * HD + e] = __float2bfloat16_rn(val / cl_s[h]);
+  }
+}
+
 // LM head: block b owns a contiguous vocab slice; warps take 4 columns x 8
 // rows at a time; rows are normalised on the fly.  The last CTA merges all
 // slices per row in slice order and writes token / logprob / entropy.
@@ -889,6 +1107,48 @@ void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, co
                max_ctx, o, ws, cnt, nsplit_max, split_keys);
   else
     printf("attention: unsupported head_dim %d\n", hd);
+}
+
+int qkv_attention_smem(int D, int nh, int nkv, int hd) { return ((nh / nkv) + 2) * hd * D * 2 + D * 2 + 128; }
+
+bool qkv_attention_supported(int D, int nh, int nkv, int hd) {
+  return (hd == 64 || hd == 128) && nh % nkv == 0 && nh / nkv <= 4 && D % 256 == 0 &&
+         (((nh / nkv) + 2) * hd) % 32 == 0 && qkv_attention_smem(D, nh, nkv, hd) <= 160 * 1024;
+}
+
+void qkv_attention(const float* X, const float* g, float eps, int D, const bf16* wqkv, const RowDesc* rows, int R_cap,
+                   const int* meta, const float2* rope, int nh, int nkv, int hd, bf16* kpool, bf16* vpool,
+                   long long kv_stride, long long layer_off, int max_ctx, bf16* o, cudaStream_t st) {
+  const int smem = qkv_attention_smem(D, nh, nkv, hd);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(R_cap, nkv);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  if (hd == 64) {
+    static bool a64 = false;
+    if (!a64) {
+      cudaFuncSetAttribute(qkv_attention_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      uniform_carveout(reinterpret_cast<const void*>(qkv_attention_kernel<64>));
+      a64 = true;
+    }
+    cudaLaunchKernelEx(&cfg, qkv_attention_kernel<64>, X, g, eps, D, wqkv, rows, meta, rope, nh, nkv, kpool, vpool,
+                       kv_stride, layer_off, max_ctx, o);
+  } else {
+    static bool a128 = false;
+    if (!a128) {
+      cudaFuncSetAttribute(qkv_attention_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      uniform_carveout(reinterpret_cast<const void*>(qkv_attention_kernel<128>));
+      a128 = true;
+    }
+    cudaLaunchKernelEx(&cfg, qkv_attention_kernel<128>, X, g, eps, D, wqkv, rows, meta, rope, nh, nkv, kpool, vpool,
+                       kv_stride, layer_off, max_ctx, o);
+  }
 }
 
 int lm_head_blocks(int V) {

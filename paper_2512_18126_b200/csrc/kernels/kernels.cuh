@@ -239,6 +239,14 @@ void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, co
                int hd, const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx,
                bf16* o, float* ws, int* cnt, cudaStream_t st);
 
+// Decode ticks of small agents (every row the only row of its agent):
+// RMSNorm + QKV + RoPE + KV append + attention in one launch, CTA = (row, kv
+// head) with its Wqkv slabs in smem.  o as attention().
+bool qkv_attention_supported(int D, int nh, int nkv, int hd);
+void qkv_attention(const float* X, const float* g, float eps, int D, const bf16* wqkv, const RowDesc* rows, int R_cap,
+                   const int* meta, const float2* rope, int nh, int nkv, int hd, bf16* kpool, bf16* vpool,
+                   long long kv_stride, long long layer_off, int max_ctx, bf16* o, cudaStream_t st);
+
 // LM head over selected rows: logits = bf16(rmsnorm(x[sel[i]]) * g) . W^T,
 // fused greedy statistics; the last CTA merges the per-slice partials and
 // writes token / logprob / entropy to out_*[out_idx[i]].  `logits`
