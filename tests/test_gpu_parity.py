@@ -292,7 +292,13 @@ def _replay(cfg, g, sample):
     return oracle_run_query(run_config(cfg), {}, sample, forced=forced)
 
 
-@pytest.mark.parametrize("cfg,sample", [(C0, 0), (C1, 0), (C1, 5), (C1U, 0), (C1U, 3)],
+_DENSE_EE = dict(CONFIGS["C4-dense"], name="C4-dense-ee", early_exit=True, out_len=[[24, 96], [24, 96], 64])
+_CHUNKED = dict(C1U, name="C1U-chunked", mode="dp-chunked-prefill")
+_SEQ = dict(C1U, name="C1U-seq", mode="sequential-pd")
+
+
+@pytest.mark.parametrize("cfg,sample", [(C0, 0), (C1, 0), (C1, 5), (C1U, 0), (C1U, 3), (_DENSE_EE, 1), (_CHUNKED, 2),
+                                        (_SEQ, 4)],
                          ids=lambda v: v["name"] if isinstance(v, dict) else str(v))
 def test_run_query_replay_and_numerics(cfg, sample):
     g = _gpu_query(cfg, sample)
