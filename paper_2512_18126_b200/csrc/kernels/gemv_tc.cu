@@ -229,6 +229,9 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
   __shared__ bool last;
   __shared__ float inv_s[kN];
+  // split-K landing buffer: [src rank][row of this CTA's 128/S slice][16] fp32
+  __shared__ __align__(16) float land[kM * kN];
+  __shared__ __align__(8) std::uint64_t land_bar;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x, split = blockIdx.y;
@@ -244,6 +247,10 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
+    if (S > 1) {
+      mbar_init(&land_bar, 1);
+      mbar_expect_tx(&land_bar, kM * kN * 4);  // every rank's slice of this CTA's rows (128/S x 16 x S)
+    }
     mbar_fence_init();
   }
   if (threadIdx.x == 0) gv_stamp(0);
@@ -259,6 +266,9 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   tc_fence_after();
   const std::uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) gv_stamp(1);
+  // split-K: announce this CTA's landing barrier as initialised (waited on
+  // just before the partials are pushed, long after)
+  if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 
   // Weight tiles do not depend on the previous kernel: the first ring's worth
   // is issued before waiting on it (PDL).
@@ -366,49 +376,47 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     epilogue(a, n, R, v);
   } else {
     // Split-K inside a thread-block cluster (the S CTAs of this weight tile):
-    // every CTA parks its 128 x 16 partial in its own shared memory (the ring
-    // is idle once the MMAs are done), then CTA q reduces weight rows
-    // [q*128/S, (q+1)*128/S) by reading all S partials over DSMEM in rank
-    // order and runs their epilogue.  No global round trips, deterministic.
-    float4* park = reinterpret_cast<float4*>(smem) + row * 4;
+    // CTA q reduces weight rows [q*128/S, (q+1)*128/S).  Every CTA pushes the
+    // partial rows owned by q straight into q's landing buffer with st.async
+    // (DSMEM stores that complete transactions on q's mbarrier), so a reducer
+    // waits only for its own data -- no cluster-wide barrier, no remote loads
+    // -- then sums the S partials in rank order (deterministic) and runs the
+    // epilogue of its rows.
+    const int per = kM / S;
+    const int q = row / per, rq = row % per;
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every landing barrier is initialised
+    {
+      const std::uint32_t dst = dsmem_addr(smem_u32(land + (split * per + rq) * kN), q);
+      const std::uint32_t bar = dsmem_addr(smem_u32(&land_bar), q);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) park[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-    cluster_sync();
+      for (int i = 0; i < 4; ++i)
+        asm volatile(
+            "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst + 16 * i),
+            "f"(v[4 * i]), "f"(v[4 * i + 1]), "f"(v[4 * i + 2]), "f"(v[4 * i + 3]), "r"(bar)
+            : "memory");
+    }
     if (threadIdx.x == 0) gv_stamp(5);
-    const int per = kM / S;  // weight rows reduced by this CTA
-    if (warp * 32 < per) {   // warps holding at least one of them (whole warps: the epilogue shuffles)
+    if (warp * 32 < per) {  // warps holding at least one reduced row (whole warps: the epilogue shuffles)
+      mbar_wait(&land_bar, 0);
       const bool mine = row < per;
       const int wr = split * per + (mine ? row : 0);
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = 0.f;
-      if (mine) {
-        const std::uint32_t local = smem_u32(reinterpret_cast<float4*>(smem) + wr * 4);
-        for (int q0 = 0; q0 < S; q0 += 4) {
-          float4 t[4][4];
+      if (mine)
+        for (int src = 0; src < S; ++src) {
+          const float4* p = reinterpret_cast<const float4*>(land + (src * per + row) * kN);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (q0 + u >= S) break;
-            const std::uint32_t ra = dsmem_addr(local, q0 + u);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) t[u][i] = dsmem_ld4(ra + 16 * i);
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (q0 + u >= S) break;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              v[4 * i] += t[u][i].x;
-              v[4 * i + 1] += t[u][i].y;
-              v[4 * i + 2] += t[u][i].z;
-              v[4 * i + 3] += t[u][i].w;
-            }
+          for (int i = 0; i < 4; ++i) {
+            const float4 t = p[i];
+            v[4 * i] += t.x;
+            v[4 * i + 1] += t.y;
+            v[4 * i + 2] += t.z;
+            v[4 * i + 3] += t.w;
           }
         }
-      }
       if (threadIdx.x == 0) gv_stamp(6);
       epilogue(a, mine ? m0 + wr : a.N, R, v);
     }
-    cluster_sync();  // partials stay readable until every CTA of the cluster has reduced
   }
   tc_fence_before();
   __syncthreads();
