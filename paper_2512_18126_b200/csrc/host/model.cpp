@@ -398,6 +398,9 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   auto probe_end = [&]() {
     if (probes_) probes_->end(st);
   };
+  // decode ticks of small agents: (embedding gather +) RMSNorm + QKV + RoPE + KV
+  // append + attention in one launch per layer
+  const bool qkv_attn = !small && use_tc_ && use_qkv_attn_ && qkv_attn_ok_ && distinct && rcap <= k::kGemvTcRows;
   if (small) {
     k::SmallParams sp = small_;
     sp.out_tok_read = out_tok_read;
@@ -405,20 +408,18 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     probe_begin(KernelProbes::SmallFwd, weight_bytes() - 2.0 * s.vocab * D + kv_bytes);
     k::small_forward(sp, st);
     probe_end();
-  } else {
+  } else if (!qkv_attn) {  // (the fused QKV + attention kernel gathers layer 0's embeddings itself)
   probe_begin(KernelProbes::Embed, 6.0 * live_R_ * D);
   k::embed(buf_.rows, rcap, meta, out_tok_read, emb_, D, x_, st, norm_fold ? ssq_ : nullptr);
   probe_end();
   }
-  // decode ticks of small agents: RMSNorm + QKV + RoPE + KV append + attention in one launch
-  const bool qkv_attn = !small && use_tc_ && use_qkv_attn_ && qkv_attn_ok_ && distinct && rcap <= k::kGemvTcRows;
   for (int l = 0; l < (small ? 0 : s.n_layers); ++l) {
     const Layer& L = layers_[static_cast<std::size_t>(l)];
     const long long loff = layer_stride_ * l;
     if (qkv_attn) {
       probe_begin(KernelProbes::Attention, 2.0 * s.qkv_cols() * D + 4.0 * live_keys_ * nkv * hd + 4.0 * live_R_ * D);
       k::qkv_attention(x_, ones_, eps, D, L.wqkv, buf_.rows, rcap, meta, rope_, nh, nkv, hd, kpool_, vpool_, kv_stride_,
-                       loff, max_ctx_, h_, st);
+                       loff, max_ctx_, h_, st, l == 0 ? emb_ : nullptr, out_tok_read);
       probe_end();
     } else {
     // rmsnorm -> QKV -> RoPE -> KV append
@@ -500,9 +501,21 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     if (use_tc_ && tc_ok_ && max_lrows_ <= k::kGemvTcRows) {
       // normalise the selected rows, then the swap-AB tensor-core GEMV with
       // the fused greedy-statistics epilogue (LM head = one weight stream)
-      k::rmsnorm_rows(x_, max_lrows_, meta, D, ones_, eps, hn_, st, buf_.sel, 1);
       k::GemvArgs lm;
       lm.A = hn_;
+      static const bool lm_fold = [] {
+        const char* e = std::getenv("MOA_LM_FOLD");
+        return !(e && e[0] == '0');
+      }();
+      if (lm_fold) {
+        // the LM head normalises its selected rows itself (no rmsnorm launch)
+        lm.X = x_;
+        lm.g = ones_;
+        lm.eps = eps;
+        lm.sel = buf_.sel;
+      } else {
+        k::rmsnorm_rows(x_, max_lrows_, meta, D, ones_, eps, hn_, st, buf_.sel, 1);
+      }
       lm.R = k::kGemvTcRows;
       lm.meta = meta + 1;  // live logits rows
       lm.N = s.vocab;

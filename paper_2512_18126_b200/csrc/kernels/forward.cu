@@ -716,11 +716,11 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
 // smem combine).  Replaces two launches and the q round trip through HBM.
 template <int HD>
 __global__ void __launch_bounds__(256, 1)
-qkv_attention_kernel(const float* __restrict__ X, const float* __restrict__ g_norm, float eps, int D,
+qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, float eps, int D,
                      const bf16* __restrict__ wqkv, const RowDesc* __restrict__ rows, const int* __restrict__ meta,
                      const float2* __restrict__ rope, int nh, int nkv, bf16* __restrict__ kpool,
                      bf16* __restrict__ vpool, long long kv_stride, long long layer_off, int max_ctx,
-                     bf16* __restrict__ o) {
+                     bf16* __restrict__ o, const bf16* __restrict__ emb, const int* __restrict__ out_tok) {
   constexpr int NW = 8, HPG = 4, E = HD / 32, half = HD / 2;
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ float qs[HPG][HD];
@@ -767,8 +767,23 @@ qkv_attention_kernel(const float* __restrict__ X, const float* __restrict__ g_no
     asm volatile("prefetch.global.L2 [%0];" ::"l"(V + static_cast<long long>(j) * HD));
   }
   MOA_PDL_ENTRY();
-  // RMS norm of the residual row -> bf16 (the oracle's rounding point)
-  const float* x = X + static_cast<long long>(r) * D;
+  // layer 0 (emb != nullptr): the residual row is the token's embedding --
+  // gathered here (the embed kernel is folded in) and written once for the
+  // later kernels by the kv-head-0 CTA
+  float* x = X + static_cast<long long>(r) * D;
+  if (emb) {
+    int tok = rd.tok;
+    if (tok < 0) tok = out_tok[-1 - tok];
+    const bf16* e = emb + static_cast<long long>(tok) * D;
+    float* xs = reinterpret_cast<float*>(dsm + static_cast<long long>(ncol) * D * 2 + D * 2);  // [D] fp32 row
+    for (int c = threadIdx.x; c < D; c += 256) {
+      const float v = __bfloat162float(e[c]);
+      xs[c] = v;
+      if (g == 0) x[c] = v;
+    }
+    __syncthreads();
+    x = xs;
+  }
   float ss = 0.f;
   for (int c = threadIdx.x * 4; c < D; c += 256 * 4) {
     const float4 v = *reinterpret_cast<const float4*>(x + c);
@@ -1109,16 +1124,17 @@ void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, co
     printf("attention: unsupported head_dim %d\n", hd);
 }
 
-int qkv_attention_smem(int D, int nh, int nkv, int hd) { return ((nh / nkv) + 2) * hd * D * 2 + D * 2 + 128; }
+int qkv_attention_smem(int D, int nh, int nkv, int hd) { return ((nh / nkv) + 2) * hd * D * 2 + D * 2 + D * 4 + 128; }
 
 bool qkv_attention_supported(int D, int nh, int nkv, int hd) {
   return (hd == 64 || hd == 128) && nh % nkv == 0 && nh / nkv <= 4 && D % 256 == 0 &&
          (((nh / nkv) + 2) * hd) % 32 == 0 && qkv_attention_smem(D, nh, nkv, hd) <= 160 * 1024;
 }
 
-void qkv_attention(const float* X, const float* g, float eps, int D, const bf16* wqkv, const RowDesc* rows, int R_cap,
+void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv, const RowDesc* rows, int R_cap,
                    const int* meta, const float2* rope, int nh, int nkv, int hd, bf16* kpool, bf16* vpool,
-                   long long kv_stride, long long layer_off, int max_ctx, bf16* o, cudaStream_t st) {
+                   long long kv_stride, long long layer_off, int max_ctx, bf16* o, cudaStream_t st, const bf16* emb,
+                   const int* out_tok) {
   const int smem = qkv_attention_smem(D, nh, nkv, hd);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(R_cap, nkv);
@@ -1138,7 +1154,7 @@ void qkv_attention(const float* X, const float* g, float eps, int D, const bf16*
       a64 = true;
     }
     cudaLaunchKernelEx(&cfg, qkv_attention_kernel<64>, X, g, eps, D, wqkv, rows, meta, rope, nh, nkv, kpool, vpool,
-                       kv_stride, layer_off, max_ctx, o);
+                       kv_stride, layer_off, max_ctx, o, emb, out_tok);
   } else {
     static bool a128 = false;
     if (!a128) {
@@ -1147,7 +1163,7 @@ void qkv_attention(const float* X, const float* g, float eps, int D, const bf16*
       a128 = true;
     }
     cudaLaunchKernelEx(&cfg, qkv_attention_kernel<128>, X, g, eps, D, wqkv, rows, meta, rope, nh, nkv, kpool, vpool,
-                       kv_stride, layer_off, max_ctx, o);
+                       kv_stride, layer_off, max_ctx, o, emb, out_tok);
   }
 }
 

@@ -436,6 +436,12 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
 // waves, a T-way atomic and a T-way merge).
 constexpr int kLmStages = 8;
 constexpr int kLmSmem = kLmStages * (kTileW + kTileX) + 1024 + 512;
+// norm-folded LM head: all K tiles of the normalised rows staged once + a weight ring
+__host__ __device__ inline int lm_fold_stages(int K) {
+  const int st = (220 * 1024 - (K / kBK) * kTileX) / kTileW;
+  return st > kLmStages ? kLmStages : st;
+}
+inline int lm_fold_smem(int K) { return lm_fold_stages(K) * kTileW + (K / kBK) * kTileX + 1024 + 512; }
 
 __global__ void __launch_bounds__(192, 1)
 lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, const GemvArgs a,
@@ -443,29 +449,34 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  const bool fold = a.X != nullptr;  // normalise the selected residual rows in-kernel
+  const int KT = a.K / kBK;
+  const int stages = fold ? lm_fold_stages(a.K) : kLmStages;
   unsigned char* sw = smem;
-  unsigned char* sx = smem + kLmStages * kTileW;
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sx + kLmStages * kTileX);
+  unsigned char* sx = smem + stages * kTileW;  // per-stage X tiles, or (fold) all KT normalised tiles
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sx + (fold ? KT : kLmStages) * kTileX);
   std::uint64_t* empty = full + kLmStages;
   std::uint64_t* accf = empty + kLmStages;  // [2]
   std::uint64_t* acce = accf + 2;           // [2]
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(acce + 2);
+  std::uint64_t* xrdy = acce + 2;           // fold: staging written
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(xrdy + 1);
   __shared__ LmStat red[4][kN];
   __shared__ LmStat run[kN];
   __shared__ bool last;
+  __shared__ float inv_s[kN];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = (a.N + kM - 1) / kM, G = gridDim.x, c = blockIdx.x;
   const int t0 = static_cast<int>(static_cast<long long>(c) * T / G), t1 = static_cast<int>(static_cast<long long>(c + 1) * T / G);
-  const int KT = a.K / kBK;
+  const std::uint32_t wtx = fold ? kTileW : kTileW + kTileX;
   const LmStat none{-INFINITY, 0.f, 0.f, 0x7fffffff};
 
   pdl_launch_dependents();
   if (threadIdx.x == 0) gv_stamp(0);
   if (threadIdx.x == 0) {
     prefetch_tmap(&map_w);
-    prefetch_tmap(&map_x);
-    for (int s = 0; s < kLmStages; ++s) {
+    if (!fold) prefetch_tmap(&map_x);
+    for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -473,6 +484,7 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
       mbar_init(&accf[b], 1);
       mbar_init(&acce[b], 4);
     }
+    mbar_init(xrdy, 1);
     mbar_fence_init();
   }
   if (threadIdx.x < kN) run[threadIdx.x] = none;
@@ -486,34 +498,37 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
     if (lane == 0) {  // TMA producer: weights before the PDL wait, activations after
       const int total = (t1 - t0) * KT;
       int q = 0;
-      for (; q < total && q < kLmStages; ++q) {
-        mbar_expect_tx(&full[q], kTileW + kTileX);
+      for (; q < total && q < stages; ++q) {
+        mbar_expect_tx(&full[q], wtx);
         tma_load_2d(sw + q * kTileW, &map_w, &full[q], (q % KT) * kBK, (t0 + q / KT) * kM);
       }
-      pdl_wait();
-      for (int j = 0; j < q; ++j) tma_load_2d(sx + j * kTileX, &map_x, &full[j], (j % KT) * kBK, 0);
+      if (!fold) {
+        pdl_wait();
+        for (int j = 0; j < q; ++j) tma_load_2d(sx + j * kTileX, &map_x, &full[j], (j % KT) * kBK, 0);
+      }
       for (; q < total; ++q) {
-        const int s = q % kLmStages;
-        mbar_wait(&empty[s], ((q / kLmStages) - 1) & 1);
-        mbar_expect_tx(&full[s], kTileW + kTileX);
+        const int s = q % stages;
+        mbar_wait(&empty[s], ((q / stages) - 1) & 1);
+        mbar_expect_tx(&full[s], wtx);
         tma_load_2d(sw + s * kTileW, &map_w, &full[s], (q % KT) * kBK, (t0 + q / KT) * kM);
-        tma_load_2d(sx + s * kTileX, &map_x, &full[s], (q % KT) * kBK, 0);
+        if (!fold) tma_load_2d(sx + s * kTileX, &map_x, &full[s], (q % KT) * kBK, 0);
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       int q = 0;
+      if (fold && t1 > t0) mbar_wait(xrdy, 0);  // the normalised rows are staged
       for (int t = t0; t < t1; ++t) {
         const int j = t - t0, b = j & 1;
         if (j >= 2) mbar_wait(&acce[b], ((j >> 1) - 1) & 1);
         tc_fence_after();
         for (int kt = 0; kt < KT; ++kt, ++q) {
-          const int s = q % kLmStages;
-          mbar_wait(&full[s], (q / kLmStages) & 1);
+          const int s = q % stages;
+          mbar_wait(&full[s], (q / stages) & 1);
           if (q == 0) gv_stamp(1);
           tc_fence_after();
-          const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + s * kTileX);
+          const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + (fold ? kt : s) * kTileX);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
             umma_bf16(tmem + b * kN, umma_desc(w0 + k * 32), umma_desc(x0 + k * 32), kIdesc, (kt | k) ? 1u : 0u);
@@ -528,6 +543,52 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
     // epilogue warps 2-5: TMEM lane quarter = warp % 4
     const int R = a.meta ? __ldcg(a.meta) : a.R;  // tick metadata, before the PDL wait
     pdl_wait();
+    if (fold) {
+      // stage bf16(rmsnorm(x[sel[r]]) * g) for every k-tile (128B-swizzled K-major)
+      const int et0 = threadIdx.x - 64;
+      {
+        const int r = et0 >> 3, j = et0 & 7;  // 8 threads per row
+        float ss = 0.f;
+        if (r < R) {
+          const float* xr = a.X + static_cast<long long>(__ldg(a.sel + r)) * a.K;
+          for (int k = j * 4; k < a.K; k += 32) {
+            const float4 v = __ldcg(reinterpret_cast<const float4*>(xr + k));
+            ss = fmaf(v.x, v.x, ss);
+            ss = fmaf(v.y, v.y, ss);
+            ss = fmaf(v.z, v.z, ss);
+            ss = fmaf(v.w, v.w, ss);
+          }
+        }
+        ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+        ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+        ss += __shfl_xor_sync(0xffffffffu, ss, 4);
+        if (j == 0 && r < kN) inv_s[r] = r < R ? 1.0f / sqrtf(ss / static_cast<float>(a.K) + a.eps) : 0.f;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const int nchunk = KT * R * 8;
+      for (int ch = et0; ch < nchunk; ch += 128) {
+        const int t = ch / (R * 8), r = (ch >> 3) % R, cc = ch & 7;
+        const int col = t * kBK + cc * 8;
+        const float* xr = a.X + static_cast<long long>(__ldg(a.sel + r)) * a.K + col;
+        const float4 x0 = __ldcg(reinterpret_cast<const float4*>(xr)), x1 = __ldcg(reinterpret_cast<const float4*>(xr + 4));
+        const float4 g0 = __ldg(reinterpret_cast<const float4*>(a.g + col));
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(a.g + col + 4));
+        const float iv = inv_s[r];
+        __align__(16) bf16 o8[8];
+        o8[0] = __float2bfloat16_rn(x0.x * iv * g0.x);
+        o8[1] = __float2bfloat16_rn(x0.y * iv * g0.y);
+        o8[2] = __float2bfloat16_rn(x0.z * iv * g0.z);
+        o8[3] = __float2bfloat16_rn(x0.w * iv * g0.w);
+        o8[4] = __float2bfloat16_rn(x1.x * iv * g1.x);
+        o8[5] = __float2bfloat16_rn(x1.y * iv * g1.y);
+        o8[6] = __float2bfloat16_rn(x1.z * iv * g1.z);
+        o8[7] = __float2bfloat16_rn(x1.w * iv * g1.w);
+        *reinterpret_cast<uint4*>(sx + t * kTileX + r * 128 + ((cc ^ (r & 7)) * 16)) = *reinterpret_cast<const uint4*>(o8);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (et0 == 0) mbar_arrive(xrdy);
+    }
     const int ew = warp - 2, quarter = warp & 3;
     const int et = threadIdx.x - 64;  // 0..127
     for (int t = t0; t < t1; ++t) {
@@ -618,7 +679,7 @@ void lm_head_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, LmS
                 cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(lm_head_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLmSmem);
+    cudaFuncSetAttribute(lm_head_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024);
     uniform_carveout(reinterpret_cast<const void*>(lm_head_tc_kernel));
     attr = true;
   }
@@ -626,7 +687,7 @@ void lm_head_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, LmS
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid < T ? grid : T);
   cfg.blockDim = dim3(192);
-  cfg.dynamicSmemBytes = kLmSmem;
+  cfg.dynamicSmemBytes = a.X ? lm_fold_smem(a.K) : kLmSmem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -93,6 +93,8 @@ struct GemvArgs {
   const float* ssq = nullptr;
   // kEpiResidual: also write the new rows' per-16-column sums of squares [R][N/16]
   float* ssq_out = nullptr;
+  // lm_head_tc with X (norm folded in): the residual rows to normalise, selected by sel[i]
+  const int* sel = nullptr;
 };
 void gemv(const GemvArgs& a, cudaStream_t st);  // dispatches to gemv_stream for large matrices
 // HBM-streaming variant (gemv_stream.cu): persistent CTAs, cp.async.bulk ring.
@@ -132,7 +134,8 @@ void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float*
 void gemv_tc_debug_trace(unsigned long long* buf);
 // Persistent LM head with fused greedy statistics (epi kEpiLmStats args): one
 // CTA per SM over contiguous vocab tiles; part >= 16 * grid LmStat, cnt one
-// int zero-initialised once.
+// int zero-initialised once.  With a.X set (and a.sel, a.g, a.eps) the CTA
+// normalises the selected residual rows itself (no rmsnorm launch, no X TMA).
 void lm_head_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, LmStat* part, int* cnt, int grid,
                 cudaStream_t st);  // per-CTA stamps [cta][8] (debug), nullptr = off
 
@@ -243,9 +246,12 @@ void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, co
 // RMSNorm + QKV + RoPE + KV append + attention in one launch, CTA = (row, kv
 // head) with its Wqkv slabs in smem.  o as attention().
 bool qkv_attention_supported(int D, int nh, int nkv, int hd);
-void qkv_attention(const float* X, const float* g, float eps, int D, const bf16* wqkv, const RowDesc* rows, int R_cap,
+// emb / out_tok (layer 0): gather the rows' embeddings in-kernel and write X
+// (the embed kernel folded in); nullptr: X holds the residual rows.
+void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv, const RowDesc* rows, int R_cap,
                    const int* meta, const float2* rope, int nh, int nkv, int hd, bf16* kpool, bf16* vpool,
-                   long long kv_stride, long long layer_off, int max_ctx, bf16* o, cudaStream_t st);
+                   long long kv_stride, long long layer_off, int max_ctx, bf16* o, cudaStream_t st,
+                   const bf16* emb = nullptr, const int* out_tok = nullptr);
 
 // LM head over selected rows: logits = bf16(rmsnorm(x[sel[i]]) * g) . W^T,
 // fused greedy statistics; the last CTA merges the per-slice partials and
