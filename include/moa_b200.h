@@ -218,6 +218,9 @@ int moa_run_batch(moa_engine* eng, const moa_run_config* cfg, const int* samples
  * cap > *len. */
 int moa_engine_trace(moa_engine* eng, int enable);
 int moa_query_trace(const moa_query* q, char* buf, long long cap, long long* len);
+/* Device time (ms since the request's first tick) at the end of every tick;
+ * needs engine tracing (moa_engine_trace).  *n = ticks, min(cap, *n) written. */
+int moa_query_ticks(const moa_query* q, double* ms, int cap, int* n);
 int moa_query_agent(const moa_query* q, int i, moa_agent_record* rec);
 /* which: 0 = prompt, 1 = output. */
 int moa_query_tokens(const moa_query* q, int i, int which, int32_t* dst, int cap, int* n);
@@ -263,6 +266,7 @@ int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, 
  * A[R][K] . W[N][K]^T for R <= 16; A must have >= 16 allocated rows. */
 int moa_k_noop(uintptr_t p, int ctas, uintptr_t stream); /* trivial PDL kernel: launch-chain cost probe */
 int moa_k_debug_trace(uintptr_t buf); /* debug: gemv_tc per-CTA clock stamps, 0 = off */
+int moa_k_chain_stamp(uintptr_t buf); /* debug: decode-chain per-CTA globaltimer stamps (stamp.cuh), 0 = off */
 int moa_k_debug_trace_small(uintptr_t buf); /* debug: small-agent forward per-CTA clock stamps, 0 = off */
 int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
 /* Hash-uniform weight init of a logical [rows][cols] tensor into a device row

@@ -106,6 +106,7 @@ _SIGS = {
     "moa_k_debug_trace": ([C.c_size_t], C.c_int),
     "moa_k_noop": ([C.c_size_t, C.c_int, C.c_size_t], C.c_int),
     "moa_k_debug_trace_small": ([C.c_size_t], C.c_int),
+    "moa_k_chain_stamp": ([C.c_size_t], C.c_int),
     "moa_engine_probe": ([C.c_void_p, C.c_int], C.c_int),
     "moa_engine_megakernel": ([C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
     "moa_engine_small_forward": ([C.c_void_p, C.c_int, C.c_int], C.c_int),
@@ -124,6 +125,7 @@ _SIGS = {
     "moa_agent_state": ([C.c_void_p, C.c_int, C.c_int] + [_P(C.c_int)] * 4, C.c_int),
     "moa_engine_trace": ([C.c_void_p, C.c_int], C.c_int),
     "moa_query_trace": ([C.c_void_p, C.c_char_p, C.c_longlong, _P(C.c_longlong)], C.c_int),
+    "moa_query_ticks": ([C.c_void_p, _P(C.c_double), C.c_int, _P(C.c_int)], C.c_int),
     "moa_run_batch": ([C.c_void_p, C.c_void_p, _P(C.c_int), C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
     "moa_run_query": ([C.c_void_p, _P(RunConfigC), C.c_int, C.c_int, _P(RunSummary), _P(C.c_void_p)], C.c_int),
     "moa_query_agent": ([C.c_void_p, C.c_int, _P(AgentRecordC)], C.c_int),
@@ -346,6 +348,11 @@ class Engine:
                     buf = C.create_string_buffer(n.value + 1)
                     check(lib().moa_query_trace(q, buf, n.value + 1, C.byref(n)))
                     res["trace"] = buf.value.decode()
+                    nt = C.c_int()
+                    check(lib().moa_query_ticks(q, None, 0, C.byref(nt)))
+                    tb = (C.c_double * max(1, nt.value))()
+                    check(lib().moa_query_ticks(q, tb, nt.value, C.byref(nt)))
+                    res["tick_ms"] = list(tb[: nt.value])
             finally:
                 lib().moa_query_free(q)
         return res

@@ -438,6 +438,16 @@ int moa_query_trace(const moa_query* q, char* buf, long long cap, long long* len
   });
 }
 
+int moa_query_ticks(const moa_query* q, double* ms, int cap, int* n) {
+  return guard([&] {
+    need(q, "query");
+    need(n, "n");
+    *n = static_cast<int>(q->r.tick_ms.size());
+    if (ms)
+      for (int i = 0; i < std::min(cap, *n); ++i) ms[i] = q->r.tick_ms[static_cast<std::size_t>(i)];
+  });
+}
+
 int moa_query_agent(const moa_query* q, int i, moa_agent_record* rec) {
   return guard([&] {
     need(q, "query");
@@ -732,6 +742,13 @@ int moa_k_debug_trace(uintptr_t buf) {
 }
 
 
+
+int moa_k_chain_stamp(uintptr_t buf) {
+  return guard([&] {
+    moa::k::forward_chain_stamp(reinterpret_cast<unsigned long long*>(buf));
+    moa::k::gemv_tc_chain_stamp(reinterpret_cast<unsigned long long*>(buf));
+  });
+}
 
 int moa_k_debug_trace_small(uintptr_t buf) {
   return guard([&] { moa::k::small_forward_debug_trace(reinterpret_cast<unsigned long long*>(buf)); });

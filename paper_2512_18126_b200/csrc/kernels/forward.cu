@@ -10,11 +10,13 @@
 #include <climits>
 #include <cstdio>
 #include <type_traits>
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include <set>
 
 #include "kernels.cuh"
+#include "stamp.cuh"
 
 namespace moa::k {
 
@@ -270,7 +272,14 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
                      ? ldg_stream(a.W + static_cast<long long>(n0 + c) * a.K + kb + lane * 8)
                      : make_uint4(0, 0, 0, 0);
   const int live = a.meta ? __ldg(a.meta) : a.R;  // tick metadata: not produced by the previous kernel
+  const unsigned stag = (1u << 16) | (static_cast<unsigned>(a.epi) << 12) | ((a.K >> 4) & 0xfff);
+  __shared__ unsigned long long cst[kChainPhases];
+  if (threadIdx.x == 0) {
+    chain_reset(cst);
+    chain_mark(cst, 0);
+  }
   MOA_PDL_ENTRY();
+  if (threadIdx.x == 0) chain_mark(cst, 1);
   if (r0 >= live) return;  // uniform across the CTA
   const int rows = min(kRB, live - r0);
   if constexpr (NORM) {
@@ -356,6 +365,10 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
       }
       break;
     }
+  }
+  if (threadIdx.x == 0) {
+    chain_mark(cst, 2);
+    chain_flush(cst, stag);
   }
 }
 
@@ -714,14 +727,15 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
 // K, one transpose-reduce), applies RoPE, appends k/v at the row's position
 // and runs the group's attention (warps split the keys, online softmax,
 // smem combine).  Replaces two launches and the q round trip through HBM.
-template <int HD>
+template <int HD, int HPG>
 __global__ void __launch_bounds__(256, 1)
 qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, float eps, int D,
                      const bf16* __restrict__ wqkv, const RowDesc* __restrict__ rows, const int* __restrict__ meta,
                      const float2* __restrict__ rope, int nh, int nkv, bf16* __restrict__ kpool,
                      bf16* __restrict__ vpool, long long kv_stride, long long layer_off, int max_ctx,
-                     bf16* __restrict__ o, const bf16* __restrict__ emb, const int* __restrict__ out_tok) {
-  constexpr int NW = 8, HPG = 4, E = HD / 32, half = HD / 2;
+                     bf16* __restrict__ o, const bf16* __restrict__ emb, const int* __restrict__ out_tok,
+                     int kv_cap) {
+  constexpr int NW = 8, E = HD / 32, half = HD / 2;  // HPG >= q heads per kv head
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ float qs[HPG][HD];
   __shared__ float wm[NW][HPG], wl[NW][HPG];
@@ -734,20 +748,31 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
   const int hpg = nh / nkv, ncol = (hpg + 2) * HD;
   bf16* W = reinterpret_cast<bf16*>(dsm);                          // [ncol][D]
   bf16* xn = reinterpret_cast<bf16*>(dsm + static_cast<long long>(ncol) * D * 2);  // [D]
+  // keys of earlier ticks staged in smem (never produced by the previous kernel)
+  bf16* Ks = reinterpret_cast<bf16*>(dsm + static_cast<long long>(ncol) * D * 2 + D * 6);  // [kv_cap][HD]
+  bf16* Vs = Ks + static_cast<long long>(kv_cap) * HD;
   if (r >= __ldg(meta)) return;  // tick metadata: not produced by the previous kernel
   const RowDesc rd = rows[r];
   const int n = rd.pos + 1;
+  const int ks = min(n - 1, kv_cap);  // staged earlier keys
+  const int nsm = min(n, kv_cap);     // keys read from smem (the own key lands there too when it fits)
   const bf16* K = kpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
   const bf16* V = vpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
   const std::uint32_t bar = static_cast<std::uint32_t>(__cvta_generic_to_shared(&wbar));
+  const unsigned stag = (2u << 16) | (emb ? 1u : 0u);
+  __shared__ unsigned long long cst[kChainPhases];
+  if (threadIdx.x == 0) {
+    chain_reset(cst);
+    chain_mark(cst, 0);
+  }
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned qb = hpg * HD * D * 2, kb = HD * D * 2;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(qb + 2 * kb));
+    const unsigned qb = hpg * HD * D * 2, kb = HD * D * 2, kvb = static_cast<unsigned>(ks) * HD * 2;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(qb + 2 * kb + 2 * kvb));
     const bf16* srcs[3] = {wqkv + static_cast<long long>(g * hpg * HD) * D,
                            wqkv + static_cast<long long>((nh + g) * HD) * D,
                            wqkv + static_cast<long long>((nh + nkv + g) * HD) * D};
@@ -761,12 +786,27 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
           : "memory");
       off += bytes[i];
     }
+    if (kvb) {
+      const bf16* kv_src[2] = {K, V};
+      bf16* kv_dst[2] = {Ks, Vs};
+      for (int i = 0; i < 2; ++i)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                static_cast<std::uint32_t>(__cvta_generic_to_shared(kv_dst[i]))),
+            "l"(kv_src[i]), "r"(kvb), "r"(bar)
+            : "memory");
+    }
   }
-  for (int j = threadIdx.x; j < n - 1 && j < 2 * NW * 32; j += NW * 32) {  // keys of earlier ticks
+  for (int j = ks + threadIdx.x; j < n - 1 && j < ks + 2 * NW * 32; j += NW * 32) {  // unstaged earlier keys
     asm volatile("prefetch.global.L2 [%0];" ::"l"(K + static_cast<long long>(j) * HD));
     asm volatile("prefetch.global.L2 [%0];" ::"l"(V + static_cast<long long>(j) * HD));
   }
+  // RoPE factors of this warp's first column group (the position is tick metadata)
+  float2 cs0 = make_float2(0.f, 0.f);
+  if (warp < ncol / 32 && warp * 32 + lane < (hpg + 1) * HD)
+    cs0 = __ldg(rope + static_cast<long long>(rd.pos) * half + ((warp * 32 + lane) % HD) / 2);
   MOA_PDL_ENTRY();
+  if (threadIdx.x == 0) chain_mark(cst, 1);
   // layer 0 (emb != nullptr): the residual row is the token's embedding --
   // gathered here (the embed kernel is folded in) and written once for the
   // later kernels by the kv-head-0 CTA
@@ -809,6 +849,7 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
                    : "memory");
   }
   __syncthreads();
+  if (threadIdx.x == 0) chain_mark(cst, 3);
   // q/k/v columns: warp w takes column groups of 32 (lanes split K)
   for (int grp = warp; grp < ncol / 32; grp += NW) {
     float acc[32];
@@ -825,21 +866,26 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
     const int c = grp * 32 + lane;  // column within the CTA's slab
     if (c < (hpg + 1) * HD) {       // q or k: rotate the (even, odd) pair
       const int e = (c % HD) / 2;
-      const float2 cs = rope[static_cast<long long>(rd.pos) * half + e];
+      const float2 cs = grp == warp ? cs0 : rope[static_cast<long long>(rd.pos) * half + e];
       const float y = (lane & 1) ? __fadd_rn(__fmul_rn(v, cs.x), __fmul_rn(partner, cs.y))
                                  : __fsub_rn(__fmul_rn(v, cs.x), __fmul_rn(partner, cs.y));
       const int d = e + ((lane & 1) ? half : 0);  // natural dim
       const bf16 yb = __float2bfloat16_rn(y);
-      if (c < hpg * HD)
+      if (c < hpg * HD) {
         qs[c / HD][d] = __bfloat162float(yb);
-      else
+      } else {
         const_cast<bf16*>(K)[static_cast<long long>(rd.pos) * HD + d] = yb;
+        if (rd.pos < kv_cap) Ks[static_cast<long long>(rd.pos) * HD + d] = yb;
+      }
     } else {
-      const_cast<bf16*>(V)[static_cast<long long>(rd.pos) * HD + (c - (hpg + 1) * HD)] = __float2bfloat16_rn(v);
+      const bf16 vb = __float2bfloat16_rn(v);
+      const_cast<bf16*>(V)[static_cast<long long>(rd.pos) * HD + (c - (hpg + 1) * HD)] = vb;
+      if (rd.pos < kv_cap) Vs[static_cast<long long>(rd.pos) * HD + (c - (hpg + 1) * HD)] = vb;
     }
   }
   __threadfence_block();
   __syncthreads();
+  if (threadIdx.x == 0) chain_mark(cst, 4);
   // attention over keys 0..pos (this row's own key included, just appended)
   constexpr int TPK = HD / 64, KC = 32 / TPK;
   const int key = lane / TPK, part = lane % TPK;
@@ -855,15 +901,21 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
   }
   for (int j0 = warp * KC; j0 < n; j0 += NW * KC) {
     const int j = j0 + key;
+    // 16-byte chunk v of a key row is read as chunk (v + lane) & 7: the lanes of
+    // a quarter warp hit distinct banks when the row is in smem
+    // (generic loads: staged keys from smem, the rest from L2/HBM -- written by
+    // earlier kernels or, for the own key, by this CTA before the barrier)
     uint4 kk[8];
+    const uint4* krow = reinterpret_cast<const uint4*>((j < nsm ? Ks : K) + static_cast<long long>(j) * HD + part * 64);
 #pragma unroll
-    for (int v = 0; v < 8; ++v)
-      kk[v] = j < n ? __ldcg(reinterpret_cast<const uint4*>(K + static_cast<long long>(j) * HD + part * 64) + v)
-                    : make_uint4(0, 0, 0, 0);
+    for (int v = 0; v < 8; ++v) kk[v] = j < n ? krow[(v + lane) & 7] : make_uint4(0, 0, 0, 0);
     VT vv[KC];
 #pragma unroll
-    for (int jj = 0; jj < KC; ++jj)
-      vv[jj] = j0 + jj < n ? __ldcg(reinterpret_cast<const VT*>(V + static_cast<long long>(j0 + jj) * HD + lane * E)) : VT{};
+    for (int jj = 0; jj < KC; ++jj) {
+      const int jv = j0 + jj;
+      const VT* vrow = reinterpret_cast<const VT*>((jv < nsm ? Vs : V) + static_cast<long long>(jv) * HD + lane * E);
+      vv[jj] = jv < n ? *vrow : VT{};
+    }
 #pragma unroll
     for (int h = 0; h < HPG; ++h) {
       if (h >= hpg) break;
@@ -872,8 +924,9 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
       for (int v = 0; v < 8; ++v) {
         float f[8];
         unpack8(kk[v], f);
+        const float* qv = &qs[h][part * 64 + ((v + lane) & 7) * 8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) d = fmaf(qs[h][part * 64 + v * 8 + t], f[t], d);
+        for (int t = 0; t < 8; ++t) d = fmaf(qv[t], f[t], d);
       }
       if constexpr (TPK == 2) d += __shfl_xor_sync(kFull, d, 1);
       const float sc = j < n ? d * scale : -INFINITY;
@@ -916,6 +969,7 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
     for (int e = 0; e < E; ++e) wo[warp][h][lane * E + e] = acc[h][e];
   }
   __syncthreads();
+  if (threadIdx.x == 0) chain_mark(cst, 5);
   if (threadIdx.x < hpg) {
     const int h = threadIdx.x;
     float M = -INFINITY;
@@ -933,6 +987,10 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
     for (int w = 0; w < NW; ++w)
       if (wm[w][h] != -INFINITY) val += __expf(wm[w][h] - M) * wo[w][h][e];
     o[(static_cast<long long>(r) * nh + g * hpg + h) * HD + e] = __float2bfloat16_rn(val / cl_s[h]);
+  }
+  if (threadIdx.x == 0) {
+    chain_mark(cst, 2);
+    chain_flush(cst, stag);
   }
 }
 
@@ -1124,7 +1182,20 @@ void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, co
     printf("attention: unsupported head_dim %d\n", hd);
 }
 
+MOA_CHAIN_STAMP_SETTER(forward_chain_stamp)
+
 int qkv_attention_smem(int D, int nh, int nkv, int hd) { return ((nh / nkv) + 2) * hd * D * 2 + D * 2 + D * 4 + 128; }
+// earlier keys one CTA stages in smem next to its weight slab (<= 200 KB of
+// dynamic smem: the kernel's static arrays take up to ~19 KB of the 227)
+static int qkv_attention_kv_cap(int D, int nh, int nkv, int hd, int max_ctx) {
+  static const int limit = [] {  // MOA_QKV_KV_STAGE=n caps the staged keys (0: none; tests)
+    const char* e = std::getenv("MOA_QKV_KV_STAGE");
+    return e ? std::atoi(e) : 1 << 30;
+  }();
+  int c = (200 * 1024 - qkv_attention_smem(D, nh, nkv, hd)) / (hd * 4);
+  c = std::min({c, max_ctx, limit});
+  return c < 0 ? 0 : c;
+}
 
 bool qkv_attention_supported(int D, int nh, int nkv, int hd) {
   return (hd == 64 || hd == 128) && nh % nkv == 0 && nh / nkv <= 4 && D % 256 == 0 &&
@@ -1135,7 +1206,8 @@ void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv,
                    const int* meta, const float2* rope, int nh, int nkv, int hd, bf16* kpool, bf16* vpool,
                    long long kv_stride, long long layer_off, int max_ctx, bf16* o, cudaStream_t st, const bf16* emb,
                    const int* out_tok) {
-  const int smem = qkv_attention_smem(D, nh, nkv, hd);
+  const int kv_cap = qkv_attention_kv_cap(D, nh, nkv, hd, max_ctx);
+  const int smem = qkv_attention_smem(D, nh, nkv, hd) + kv_cap * hd * 4;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(R_cap, nkv);
   cfg.blockDim = dim3(256);
@@ -1146,24 +1218,24 @@ void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv,
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const int hpg = nh / nkv;
+  auto go = [&](auto kern) {
+    static std::set<const void*> attr;
+    if (attr.insert(reinterpret_cast<const void*>(kern)).second) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      uniform_carveout(reinterpret_cast<const void*>(kern));
+    }
+    cudaLaunchKernelEx(&cfg, kern, X, g, eps, D, wqkv, rows, meta, rope, nh, nkv, kpool, vpool, kv_stride, layer_off,
+                       max_ctx, o, emb, out_tok, kv_cap);
+  };
   if (hd == 64) {
-    static bool a64 = false;
-    if (!a64) {
-      cudaFuncSetAttribute(qkv_attention_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      uniform_carveout(reinterpret_cast<const void*>(qkv_attention_kernel<64>));
-      a64 = true;
-    }
-    cudaLaunchKernelEx(&cfg, qkv_attention_kernel<64>, X, g, eps, D, wqkv, rows, meta, rope, nh, nkv, kpool, vpool,
-                       kv_stride, layer_off, max_ctx, o, emb, out_tok);
+    if (hpg == 1) go(qkv_attention_kernel<64, 1>);
+    else if (hpg == 2) go(qkv_attention_kernel<64, 2>);
+    else go(qkv_attention_kernel<64, 4>);
   } else {
-    static bool a128 = false;
-    if (!a128) {
-      cudaFuncSetAttribute(qkv_attention_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      uniform_carveout(reinterpret_cast<const void*>(qkv_attention_kernel<128>));
-      a128 = true;
-    }
-    cudaLaunchKernelEx(&cfg, qkv_attention_kernel<128>, X, g, eps, D, wqkv, rows, meta, rope, nh, nkv, kpool, vpool,
-                       kv_stride, layer_off, max_ctx, o, emb, out_tok);
+    if (hpg == 1) go(qkv_attention_kernel<128, 1>);
+    else if (hpg == 2) go(qkv_attention_kernel<128, 2>);
+    else go(qkv_attention_kernel<128, 4>);
   }
 }
 

@@ -16,6 +16,7 @@
 
 #include "kernels.cuh"
 #include "tc_common.cuh"
+#include "stamp.cuh"
 
 namespace moa::k {
 
@@ -449,6 +450,11 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  __shared__ unsigned long long cst[kChainPhases];
+  if (threadIdx.x == 0) {
+    chain_reset(cst);
+    chain_mark(cst, 0);
+  }
   const bool fold = a.X != nullptr;  // normalise the selected residual rows in-kernel
   const int KT = a.K / kBK;
   const int stages = fold ? lm_fold_stages(a.K) : kLmStages;
@@ -543,6 +549,7 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
     // epilogue warps 2-5: TMEM lane quarter = warp % 4
     const int R = a.meta ? __ldcg(a.meta) : a.R;  // tick metadata, before the PDL wait
     pdl_wait();
+    if (threadIdx.x == 64) chain_mark(cst, 1);
     if (fold) {
       // stage bf16(rmsnorm(x[sel[r]]) * g) for every k-tile (128B-swizzled K-major)
       const int et0 = threadIdx.x - 64;
@@ -588,6 +595,7 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (et0 == 0) mbar_arrive(xrdy);
+      if (et0 == 0) chain_mark(cst, 3);
     }
     const int ew = warp - 2, quarter = warp & 3;
     const int et = threadIdx.x - 64;  // 0..127
@@ -624,6 +632,7 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
       (void)ew;
     }
     if (et == 0) gv_stamp(3);
+    if (et == 0) chain_mark(cst, 4);
     if (et < R) {
       const LmStat st = run[et];
       __stcg(reinterpret_cast<float4*>(part + static_cast<long long>(et) * G + c),
@@ -666,6 +675,11 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
       }
       if (et == 0) __stcg(cnt, 0);
       if (et == 0) gv_stamp(5);
+      if (et == 0) chain_mark(cst, 6);
+    }
+    if (et == 0) {
+      chain_mark(cst, 2);
+      chain_flush(cst, 3u << 16);
     }
   }
   tc_fence_before();
@@ -698,6 +712,7 @@ void lm_head_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, LmS
                      *reinterpret_cast<const CUtensorMap*>(&map_x), a, part, cnt);
 }
 
+MOA_CHAIN_STAMP_SETTER(gemv_tc_chain_stamp)
 void gemv_tc_debug_trace(unsigned long long* buf) { cudaMemcpyToSymbol(g_gv_trace, &buf, sizeof(buf)); }
 
 // K splits per weight tile: as many as keep the grid within one CTA per SM

@@ -200,6 +200,30 @@ def test_single_agent_decode_matches_oracle():
     eng.close()
 
 
+def test_long_context_decode_matches_oracle():
+    """Decode past the fused QKV+attention kernel's smem key stage (~400 keys
+    for tiny agents): the staged keys come from smem, the rest from HBM, and
+    two agents decode side by side (distinct-row ticks)."""
+    model = _cpu_model("leaf", "tiny", 1)
+    eng = capi.Engine([capi.model_spec("leaf", "tiny", 1, max_agents=2)], max_ctx=1024, max_out=64, keep_logits=True)
+    prompts = [orng.synth_tokens(5, "p", 380), orng.synth_tokens(6, "p", 700)]
+    agents = [(1, 0), (1, 1)]
+    for a, p in zip(agents, prompts):
+        eng.add_agent(a, 0)
+        eng.generate(a, p, 40, 8)
+    busy = True
+    while busy:
+        _, busy = eng.step()
+    for a, p in zip(agents, prompts):
+        tok, lp, _ = eng.read_output(a, 40)
+        logits = np.stack([eng.read_logits(a, k) for k in range(40)])
+        err = float(np.abs(logits - teacher_forced(model, p, tok)).max())
+        assert err < LOGIT_ATOL, (a, err)
+        chk = check_agent(model, p, tok, lp)
+        assert chk["mismatches"] == [] and chk["lp_ok"], chk
+    eng.close()
+
+
 def test_incremental_prefill_equals_one_shot():
     """Appending the prompt in contiguous pieces (prefill_only) gives the same
     KV and tokens as one generate (zero recompute, pdsim.cpp:155-174)."""
