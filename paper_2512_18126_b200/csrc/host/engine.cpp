@@ -58,7 +58,16 @@ GpuEngine::GpuEngine(std::vector<ModelSpec> models, std::vector<int> agents_per_
     MOA_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
     mstreams_.push_back(s2);
     mdone_.push_back(e2);
+    MOA_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    cstreams_.push_back(s2);
+    for (int b = 0; b < 2; ++b) {
+      MOA_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+      blob_free_.push_back(e2);
+      MOA_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+      blob_ready_.push_back(e2);
+    }
   }
+  if (const char* e = std::getenv("MOA_ASYNC_UPLOAD")) async_upload_ = std::string(e) != "0";
   // two persistent (cooperative, one CTA per SM) forwards must never run side by side
   if (const char* e = std::getenv("MOA_MK")) overlap_models_ = std::string(e) == "0";
   if (const char* e = std::getenv("MOA_OVERLAP")) overlap_models_ = overlap_models_ && std::string(e) != "0";
@@ -80,6 +89,12 @@ GpuEngine::~GpuEngine() {
     cudaStreamDestroy(s2);
   }
   for (auto e2 : mdone_) cudaEventDestroy(e2);
+  for (auto s2 : cstreams_) {
+    cudaStreamSynchronize(s2);
+    cudaStreamDestroy(s2);
+  }
+  for (auto e2 : blob_free_) cudaEventDestroy(e2);
+  for (auto e2 : blob_ready_) cudaEventDestroy(e2);
   if (tick_fork_) cudaEventDestroy(tick_fork_);
   if (start_ev_) cudaEventDestroy(start_ev_);
   for (void* p : {static_cast<void*>(out_tok_), static_cast<void*>(out_lp_), static_cast<void*>(out_ent_),
@@ -254,8 +269,23 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   sel[2 * L] = static_cast<int>(rows.size());
   sel[2 * L + 1] = static_cast<int>(lsel.size());
   sel[2 * L + 2] = max_pos;
-  MOA_CUDA(cudaMemcpyAsync(dm.buffers().sel, s.host, sb + rb, cudaMemcpyHostToDevice, st));
-  MOA_CUDA(cudaEventRecord(s.done, st));
+  int b = 0;
+  if (async_upload_) {
+    // into the blob the previous forward of this model is not reading, on the
+    // model's copy stream: the copy runs while that forward executes
+    b = dm.blob() ^ 1;
+    dm.use_blob(b);
+    const std::size_t ev = 2 * static_cast<std::size_t>(m) + static_cast<std::size_t>(b);
+    cudaStream_t cs = cstreams_[static_cast<std::size_t>(m)];
+    MOA_CUDA(cudaStreamWaitEvent(cs, blob_free_[ev], 0));  // the forward that last read blob b is done
+    MOA_CUDA(cudaMemcpyAsync(dm.buffers().sel, s.host, sb + rb, cudaMemcpyHostToDevice, cs));
+    MOA_CUDA(cudaEventRecord(s.done, cs));
+    MOA_CUDA(cudaEventRecord(blob_ready_[ev], cs));
+    MOA_CUDA(cudaStreamWaitEvent(st, blob_ready_[ev], 0));
+  } else {
+    MOA_CUDA(cudaMemcpyAsync(dm.buffers().sel, s.host, sb + rb, cudaMemcpyHostToDevice, st));
+    MOA_CUDA(cudaEventRecord(s.done, st));
+  }
   float* logits = (opt_.keep_logits && !lsel.empty()) ? logits_scratch_ : nullptr;
   dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), max_pos, keys, out_tok_, out_tok_,
              out_lp_, out_ent_, logits, st, distinct);
@@ -266,6 +296,7 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
                                logits_scratch_ + static_cast<long long>(i) * V, sizeof(float) * V,
                                cudaMemcpyDeviceToDevice, st));
   }
+  if (async_upload_) MOA_CUDA(cudaEventRecord(blob_free_[2 * static_cast<std::size_t>(m) + static_cast<std::size_t>(b)], st));
   rows_total_ += static_cast<long long>(rows.size());
   weight_bytes_ += dm.weight_bytes();
   forwards_ += 1;
@@ -360,14 +391,6 @@ void GpuEngine::step() {
       host_api_ms_ += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_api).count();
     }
   overlapped_ticks_ += fan_out;
-  if (opt_.time_ticks) {
-    if (static_cast<int>(tick_ev_.size()) <= tick_) {
-      cudaEvent_t e;
-      MOA_CUDA(cudaEventCreate(&e));
-      tick_ev_.push_back(e);
-    }
-    MOA_CUDA(cudaEventRecord(tick_ev_[static_cast<std::size_t>(tick_)], stream_));
-  }
   // state update
   for (Plan& p : plan) {
     Req& r = *p.r;
@@ -395,6 +418,23 @@ void GpuEngine::step() {
         start_decode(r, 0);
         break;
     }
+  }
+  // Tick-end timing event: a timed event record costs ~4 us of device time
+  // between two ticks' graphs, so it is recorded only where a time is read --
+  // ticks on which a decode completes (request e2e, orchestrator.cpp:290-292)
+  // and every tick while tracing.
+  if (opt_.time_ticks) {
+    bool completes = tracing_;
+    for (const Plan& p : plan)
+      completes = completes || (p.r->dec_started && !p.r->finished && !p.r->cancelled && p.r->n_out == p.r->max_new);
+    if (static_cast<int>(tick_ev_.size()) <= tick_) {
+      cudaEvent_t e;
+      MOA_CUDA(cudaEventCreate(&e));
+      tick_ev_.push_back(e);
+      tick_timed_.push_back(0);
+    }
+    tick_timed_[static_cast<std::size_t>(tick_)] = completes;
+    if (completes) MOA_CUDA(cudaEventRecord(tick_ev_[static_cast<std::size_t>(tick_)], stream_));
   }
   const int t = tick_;
   tick_ += 1;
@@ -586,6 +626,8 @@ void GpuEngine::mark_start() { MOA_CUDA(cudaEventRecord(start_ev_, stream_)); }
 
 double GpuEngine::ms_since_start(int t) {
   if (t < 0 || t >= static_cast<int>(tick_ev_.size())) return 0.0;
+  if (!tick_timed_[static_cast<std::size_t>(t)])
+    throw RunError("engine: tick " + std::to_string(t) + " has no timing event (enable tracing)");
   MOA_CUDA(cudaEventSynchronize(tick_ev_[static_cast<std::size_t>(t)]));
   float ms = 0.f;
   MOA_CUDA(cudaEventElapsedTime(&ms, start_ev_, tick_ev_[static_cast<std::size_t>(t)]));

@@ -138,7 +138,7 @@ class GpuEngine {
 
   // Timing: event recorded at run start / after a tick (time_ticks).
   void mark_start();
-  double ms_since_start(int tick);  // synchronises on that tick's event
+  double ms_since_start(int tick);  // synchronises on that tick's event (completion ticks / tracing)
   double bytes_moved() const { return weight_bytes_; }
   long long rows_processed() const { return rows_total_; }
   int kernel_forwards() const { return forwards_; }
@@ -181,6 +181,11 @@ class GpuEngine {
   std::vector<cudaStream_t> mstreams_;
   std::vector<cudaEvent_t> mdone_;
   cudaEvent_t tick_fork_ = nullptr;
+  // tick metadata uploads run on a copy stream per model into the blob the
+  // previous tick is not reading, so the copy overlaps that tick's forward
+  std::vector<cudaStream_t> cstreams_;
+  std::vector<cudaEvent_t> blob_free_, blob_ready_;  // [model][2]
+  bool async_upload_ = true;
   bool overlap_models_ = true;
   bool tracing_ = false;
   std::map<int, int> embed_kv_;  // model -> reserved KV slot of the hidden-state provider
@@ -212,6 +217,7 @@ class GpuEngine {
   // timing
   cudaEvent_t start_ev_ = nullptr;
   std::vector<cudaEvent_t> tick_ev_;
+  std::vector<char> tick_timed_;  // tick_ev_[t] recorded (completion ticks, or every tick while tracing)
   double weight_bytes_ = 0.0;
   long long rows_total_ = 0;
   int forwards_ = 0;

@@ -136,9 +136,9 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   // tick metadata in one allocation, uploaded with one copy per tick:
   // [sel: lsel (L) | lout (L) | meta (3)] padded to 16 bytes, then the rows
   buf_.sel_bytes = static_cast<int>(((2LL * max_logit_rows + 3) * sizeof(int) + 15) / 16 * 16);
-  MOA_CUDA(cudaMalloc(&meta_blob_, buf_.sel_bytes + sizeof(k::RowDesc) * static_cast<std::size_t>(max_rows)));
-  buf_.sel = reinterpret_cast<int*>(meta_blob_);
-  buf_.rows = reinterpret_cast<k::RowDesc*>(static_cast<char*>(meta_blob_) + buf_.sel_bytes);
+  blob_bytes_ = (buf_.sel_bytes + sizeof(k::RowDesc) * static_cast<std::size_t>(max_rows) + 255) / 256 * 256;
+  MOA_CUDA(cudaMalloc(&meta_blob_, 2 * blob_bytes_));
+  use_blob(0);
   dev_alloc(&hn_, static_cast<long long>(max_rows) * D);
   // TMA descriptors for the tensor-core prefill path (weights: 128-row boxes)
   tc_ok_ = k::gemm_tc_supported(s.qkv_cols(), D) && k::gemm_tc_supported(D, s.n_heads * s.head_dim) &&
@@ -269,6 +269,13 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   MOA_CUDA(cudaGetLastError());
 }
 
+void DeviceModel::use_blob(int b) {
+  blob_ = b & 1;
+  char* base = static_cast<char*>(meta_blob_) + blob_ * blob_bytes_;
+  buf_.sel = reinterpret_cast<int*>(base);
+  buf_.rows = reinterpret_cast<k::RowDesc*>(base + buf_.sel_bytes);
+}
+
 DeviceModel::~DeviceModel() {
   for (auto& [key, exec] : graphs_) cudaGraphExecDestroy(exec);
   for (void* ptr : {static_cast<void*>(wbase_), static_cast<void*>(ones_), static_cast<void*>(rope_),
@@ -336,7 +343,7 @@ void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int*
     return;
   }
   const auto key = std::make_tuple(rcap, nsplit, (Rl > 0 ? 1 : 0) | (use_tc_ ? 2 : 0) | (use_mk_ ? 4 : 0) |
-                                                     (distinct ? 8 : 0), logits ? 1 : 0);
+                                                     (distinct ? 8 : 0) | (blob_ << 4), logits ? 1 : 0);
   auto it = graphs_.find(key);
   if (it == graphs_.end()) {
     cudaGraph_t g = nullptr;
@@ -404,6 +411,8 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   if (small) {
     k::SmallParams sp = small_;
     sp.out_tok_read = out_tok_read;
+    sp.rows = buf_.rows;
+    sp.meta = buf_.sel + 2 * max_lrows_;
     const double kv_bytes = 4.0 * static_cast<double>(live_keys_) * nkv * hd * s.n_layers;
     probe_begin(KernelProbes::SmallFwd, weight_bytes() - 2.0 * s.vocab * D + kv_bytes);
     k::small_forward(sp, st);
@@ -462,6 +471,8 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     o.W = L.wo;
     o.epi = k::kEpiResidual;
     o.out = x_;
+    // x was last written two kernels back, except when layer 0's fused kernel gathered it
+    o.res_early = !(qkv_attn && l == 0);
     if (norm_fold) o.ssq_out = ssq_;
     probe_begin(KernelProbes::OProj, 2.0 * o.N * o.K + 2.0 * live_R_ * o.K + 8.0 * live_R_ * D);
     run_gemm(o, &map_h_attn_, &map_h_attn16_, wmaps_[static_cast<std::size_t>(l)].wo);
@@ -491,6 +502,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     dn.W = L.wd;
     dn.epi = k::kEpiResidual;
     dn.out = x_;
+    dn.res_early = true;  // x was written by the o-projection, two kernels back
     if (norm_fold) dn.ssq_out = ssq_;
     probe_begin(KernelProbes::Down, 2.0 * dn.N * dn.K + 2.0 * live_R_ * dn.K + 8.0 * live_R_ * D);
     run_gemm(dn, &map_h_ffn_, &map_h_ffn16_, wmaps_[static_cast<std::size_t>(l)].wd);
@@ -510,7 +522,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       if (lm_fold) {
         // the LM head normalises its selected rows itself (no rmsnorm launch)
         lm.X = x_;
-        lm.g = ones_;
+        lm.g = nullptr;  // unit gains (the final norm's gains are ones)
         lm.eps = eps;
         lm.sel = buf_.sel;
       } else {

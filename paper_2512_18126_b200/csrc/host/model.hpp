@@ -95,6 +95,10 @@ class DeviceModel {
   int max_rows() const { return max_rows_; }
   int max_logit_rows() const { return max_lrows_; }
   const ForwardBuffers& buffers() const { return buf_; }
+  // Two tick-metadata blobs: the next tick's upload lands in one while the
+  // current tick's graph reads the other (graphs are keyed by the blob).
+  void use_blob(int b);
+  int blob() const { return blob_; }
   const float* residual() const { return x_; }  // final residual rows of the last forward
 
   // R rows / Rl logits rows already resident in buffers(); out_* are the
@@ -182,7 +186,9 @@ class DeviceModel {
   k::LmStat* part_ = nullptr;
   int* lm_cnt_ = nullptr;
   ForwardBuffers buf_;
-  void* meta_blob_ = nullptr;
+  void* meta_blob_ = nullptr;  // [2][sel_bytes + rows]
+  std::size_t blob_bytes_ = 0;
+  int blob_ = 0;
 };
 
 }  // namespace moa

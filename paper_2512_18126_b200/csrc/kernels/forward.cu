@@ -153,13 +153,12 @@ __device__ __forceinline__ float row_inv_rms(const float* __restrict__ x, int K,
 
 // A fragment: 8 consecutive K elements of one row, as fp32 values of bf16.
 template <bool NORM>
-__device__ __forceinline__ void load_a(const GemvArgs& a, int row, int k, float inv, float (&f)[8]) {
+__device__ __forceinline__ void load_a(const GemvArgs& a, int row, int k, float inv, float (&f)[8], float4 g0,
+                                       float4 g1) {
   if constexpr (NORM) {
     const float* x = a.X + static_cast<long long>(row) * a.K + k;
     const float4 x0 = __ldg(reinterpret_cast<const float4*>(x));
     const float4 x1 = __ldg(reinterpret_cast<const float4*>(x + 4));
-    const float4 g0 = __ldg(reinterpret_cast<const float4*>(a.g + k));
-    const float4 g1 = __ldg(reinterpret_cast<const float4*>(a.g + k + 4));
     f[0] = bf16r(x0.x * inv * g0.x);
     f[1] = bf16r(x0.y * inv * g0.y);
     f[2] = bf16r(x0.z * inv * g0.z);
@@ -271,7 +270,19 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
     w_first[c] = (n0 + c < a.N && kb + lane * 8 < ke)
                      ? ldg_stream(a.W + static_cast<long long>(n0 + c) * a.K + kb + lane * 8)
                      : make_uint4(0, 0, 0, 0);
+  // norm gains of the first k-step: weights too
+  float4 g_first0 = make_float4(0.f, 0.f, 0.f, 0.f), g_first1 = g_first0;
+  if (NORM && kb + lane * 8 < ke) {
+    g_first0 = __ldg(reinterpret_cast<const float4*>(a.g + kb + lane * 8));
+    g_first1 = __ldg(reinterpret_cast<const float4*>(a.g + kb + lane * 8 + 4));
+  }
   const int live = a.meta ? __ldg(a.meta) : a.R;  // tick metadata: not produced by the previous kernel
+  // residual of this lane's epilogue element (lane L: column n0 + L/8, row r0 + L%8)
+  float res = 0.f;
+  if (a.res_early && a.epi == kEpiResidual && kb == 0) {
+    const int rr = r0 + lane % kRB, nn = n0 + lane / kRB;
+    if (rr < live && nn < a.N) res = a.out[static_cast<long long>(rr) * a.N + nn];
+  }
   const unsigned stag = (1u << 16) | (static_cast<unsigned>(a.epi) << 12) | ((a.K >> 4) & 0xfff);
   __shared__ unsigned long long cst[kChainPhases];
   if (threadIdx.x == 0) {
@@ -289,6 +300,7 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
     }
     __syncthreads();
   }
+  if (threadIdx.x == 0) chain_mark(cst, 3);
   float acc[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) acc[i] = 0.f;
@@ -304,13 +316,19 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
       for (int r = 0; r < kRB; ++r) {
         if (r < rows) {
           float f[8];
-          load_a<NORM>(a, r0 + r, k, NORM ? inv_s[r] : 0.f, f);
+          float4 g0 = g_first0, g1 = g_first1;
+          if (NORM && k != kb + lane * 8) {
+            g0 = __ldg(reinterpret_cast<const float4*>(a.g + k));
+            g1 = __ldg(reinterpret_cast<const float4*>(a.g + k + 4));
+          }
+          load_a<NORM>(a, r0 + r, k, NORM ? inv_s[r] : 0.f, f, g0, g1);
 #pragma unroll
           for (int c = 0; c < kCPW; ++c) acc[c * kRB + r] = dot8(f, w[c], acc[c * kRB + r]);
         }
       }
     }
   }
+  if (threadIdx.x == 0) chain_mark(cst, 4);
   float v = transpose_reduce32(acc, lane);
   if constexpr (KP > 1) {
     red[kp][cg][lane] = v;
@@ -320,6 +338,7 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
 #pragma unroll
     for (int p = 1; p < KP; ++p) v += red[p][cg][lane];
   }
+  if (threadIdx.x == 0) chain_mark(cst, 5);
   // ---- epilogue: lane L holds column n0 + L/8, row r0 + L%8 ----
   const int c = lane / kRB, r = lane % kRB, n = n0 + c, row = r0 + r;
   const bool ok = r < rows && n < a.N;
@@ -329,7 +348,10 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
       if (ok) a.out[static_cast<long long>(row) * a.N + n] = v;
       break;
     case kEpiResidual:
-      if (ok) a.out[static_cast<long long>(row) * a.N + n] += v;
+      if (ok) {
+        float* dst = a.out + static_cast<long long>(row) * a.N + n;
+        *dst = (a.res_early ? res : *dst) + v;
+      }
       break;
     case kEpiSwiGlu:  // device rows interleave gate (even) / up (odd)
       if (ok && !(n & 1)) {
@@ -801,6 +823,7 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
     asm volatile("prefetch.global.L2 [%0];" ::"l"(K + static_cast<long long>(j) * HD));
     asm volatile("prefetch.global.L2 [%0];" ::"l"(V + static_cast<long long>(j) * HD));
   }
+  const float g_first = threadIdx.x < D ? __ldg(g_norm + threadIdx.x) : 0.f;  // norm gains: weights
   // RoPE factors of this warp's first column group (the position is tick metadata)
   float2 cs0 = make_float2(0.f, 0.f);
   if (warp < ncol / 32 && warp * 32 + lane < (hpg + 1) * HD)
@@ -838,7 +861,8 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
   float tot = 0.f;
   for (int w = 0; w < NW; ++w) tot += red[w];
   const float inv = 1.0f / sqrtf(tot / static_cast<float>(D) + eps);
-  for (int c = threadIdx.x; c < D; c += 256) xn[c] = __float2bfloat16_rn(x[c] * inv * g_norm[c]);
+  for (int c = threadIdx.x; c < D; c += 256)
+    xn[c] = __float2bfloat16_rn(x[c] * inv * (c == threadIdx.x ? g_first : g_norm[c]));
   // weights landed
   {
     std::uint32_t ok = 0;
@@ -1040,7 +1064,8 @@ lm_head_kernel(const float* __restrict__ X, const int* __restrict__ sel, const i
         for (int r = 0; r < kRB; ++r) {
           if (r < rows) {
             float f[8];
-            load_a<true>(ga, sel[r0 + r], k, inv_s[r0 + r], f);
+            load_a<true>(ga, sel[r0 + r], k, inv_s[r0 + r], f, __ldg(reinterpret_cast<const float4*>(ga.g + k)),
+                         __ldg(reinterpret_cast<const float4*>(ga.g + k + 4)));
 #pragma unroll
             for (int c = 0; c < kCPW; ++c) acc[c * kRB + r] = dot8(f, w[c], acc[c * kRB + r]);
           }

@@ -428,21 +428,33 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
 
 // ---------------------------------------------------------------------------
 // Persistent LM head (greedy statistics), one CTA per SM.  CTA c owns the
-// contiguous vocab tiles [c*T/G, (c+1)*T/G); the weight/activation ring runs
-// across its tiles without a break (the next tile's tiles stream while the
-// current one's epilogue runs: accumulators double-buffered in TMEM).  Per
-// logits row the CTA folds each tile's statistics into a running LmStat
-// (tile order), writes one partial, and the last CTA merges the G partials in
-// CTA order -> token / logprob / entropy.  Replaces one CTA per tile (two
-// waves, a T-way atomic and a T-way merge).
-constexpr int kLmStages = 8;
-constexpr int kLmSmem = kLmStages * (kTileW + kTileX) + 1024 + 512;
+// contiguous vocab tiles [c*T/G, (c+1)*T/G); the weight ring runs across its
+// tiles without a break and every tile accumulates into its own 16 TMEM
+// columns (<= 32 tiles per CTA), so the MMAs never wait for an epilogue.  The
+// epilogue warps fold each finished tile into a per-lane running statistic
+// with single-column TMEM loads (tile order), reduce once per row across the
+// warp and the four lane quarters, write one partial per row, and the last
+// CTA merges the G partials in CTA order -> token / logprob / entropy.
+constexpr int kLmStages = 8;       // weight+activation ring (activations by TMA)
+constexpr int kLmMaxStages = 16;   // weight ring with the norm folded in
+constexpr int kLmMaxTiles = 32;    // TMEM: 32 tiles x 16 columns
+constexpr int kLmSmem = kLmStages * (kTileW + kTileX) + 1024 + 1024;
 // norm-folded LM head: all K tiles of the normalised rows staged once + a weight ring
 __host__ __device__ inline int lm_fold_stages(int K) {
   const int st = (220 * 1024 - (K / kBK) * kTileX) / kTileW;
-  return st > kLmStages ? kLmStages : st;
+  return st > kLmMaxStages ? kLmMaxStages : st;
 }
-inline int lm_fold_smem(int K) { return lm_fold_stages(K) * kTileW + (K / kBK) * kTileX + 1024 + 512; }
+inline int lm_fold_smem(int K) { return lm_fold_stages(K) * kTileW + (K / kBK) * kTileX + 1024 + 1024; }
+
+__device__ __forceinline__ float tmem_ld1(std::uint32_t taddr) {
+  std::uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+template <int COLS>
+__device__ __forceinline__ void lm_tmem_alloc(std::uint32_t* slot) { tmem_alloc<COLS>(slot); }
 
 __global__ void __launch_bounds__(192, 1)
 lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, const GemvArgs a,
@@ -461,19 +473,18 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
   unsigned char* sw = smem;
   unsigned char* sx = smem + stages * kTileW;  // per-stage X tiles, or (fold) all KT normalised tiles
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sx + (fold ? KT : kLmStages) * kTileX);
-  std::uint64_t* empty = full + kLmStages;
-  std::uint64_t* accf = empty + kLmStages;  // [2]
-  std::uint64_t* acce = accf + 2;           // [2]
-  std::uint64_t* xrdy = acce + 2;           // fold: staging written
+  std::uint64_t* empty = full + kLmMaxStages;
+  std::uint64_t* accf = empty + kLmMaxStages;  // [kLmMaxTiles]: tile j accumulated
+  std::uint64_t* xrdy = accf + kLmMaxTiles;    // fold: staging written
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(xrdy + 1);
   __shared__ LmStat red[4][kN];
-  __shared__ LmStat run[kN];
   __shared__ bool last;
   __shared__ float inv_s[kN];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = (a.N + kM - 1) / kM, G = gridDim.x, c = blockIdx.x;
   const int t0 = static_cast<int>(static_cast<long long>(c) * T / G), t1 = static_cast<int>(static_cast<long long>(c + 1) * T / G);
+  const int tmax = (T + G - 1) / G;  // tiles of the largest CTA (uniform TMEM allocation)
   const std::uint32_t wtx = fold ? kTileW : kTileW + kTileX;
   const LmStat none{-INFINITY, 0.f, 0.f, 0x7fffffff};
 
@@ -486,15 +497,17 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&accf[b], 1);
-      mbar_init(&acce[b], 4);
-    }
+    for (int j = 0; j < t1 - t0; ++j) mbar_init(&accf[j], 1);
     mbar_init(xrdy, 1);
     mbar_fence_init();
   }
-  if (threadIdx.x < kN) run[threadIdx.x] = none;
-  if (warp == 0) tmem_alloc<32>(tmem_slot);
+  if (warp == 0) {
+    if (tmax <= 2) lm_tmem_alloc<32>(tmem_slot);
+    else if (tmax <= 4) lm_tmem_alloc<64>(tmem_slot);
+    else if (tmax <= 8) lm_tmem_alloc<128>(tmem_slot);
+    else if (tmax <= 16) lm_tmem_alloc<256>(tmem_slot);
+    else lm_tmem_alloc<512>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -522,12 +535,11 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer
+    if (lane == 0) {  // MMA issuer: tile j -> TMEM columns [16j, 16j + 16)
       int q = 0;
       if (fold && t1 > t0) mbar_wait(xrdy, 0);  // the normalised rows are staged
       for (int t = t0; t < t1; ++t) {
-        const int j = t - t0, b = j & 1;
-        if (j >= 2) mbar_wait(&acce[b], ((j >> 1) - 1) & 1);
+        const int j = t - t0;
         tc_fence_after();
         for (int kt = 0; kt < KT; ++kt, ++q) {
           const int s = q % stages;
@@ -537,10 +549,10 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
           const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + (fold ? kt : s) * kTileX);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
-            umma_bf16(tmem + b * kN, umma_desc(w0 + k * 32), umma_desc(x0 + k * 32), kIdesc, (kt | k) ? 1u : 0u);
+            umma_bf16(tmem + j * kN, umma_desc(w0 + k * 32), umma_desc(x0 + k * 32), kIdesc, (kt | k) ? 1u : 0u);
           umma_commit(&empty[s]);
         }
-        umma_commit(&accf[b]);
+        umma_commit(&accf[j]);
       }
       gv_stamp(2);
     }
@@ -559,7 +571,7 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
         if (r < R) {
           const float* xr = a.X + static_cast<long long>(__ldg(a.sel + r)) * a.K;
           for (int k = j * 4; k < a.K; k += 32) {
-            const float4 v = __ldcg(reinterpret_cast<const float4*>(xr + k));
+            const float4 v = __ldg(reinterpret_cast<const float4*>(xr + k));
             ss = fmaf(v.x, v.x, ss);
             ss = fmaf(v.y, v.y, ss);
             ss = fmaf(v.z, v.z, ss);
@@ -577,9 +589,10 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
         const int t = ch / (R * 8), r = (ch >> 3) % R, cc = ch & 7;
         const int col = t * kBK + cc * 8;
         const float* xr = a.X + static_cast<long long>(__ldg(a.sel + r)) * a.K + col;
-        const float4 x0 = __ldcg(reinterpret_cast<const float4*>(xr)), x1 = __ldcg(reinterpret_cast<const float4*>(xr + 4));
-        const float4 g0 = __ldg(reinterpret_cast<const float4*>(a.g + col));
-        const float4 g1 = __ldg(reinterpret_cast<const float4*>(a.g + col + 4));
+        const float4 x0 = __ldg(reinterpret_cast<const float4*>(xr)), x1 = __ldg(reinterpret_cast<const float4*>(xr + 4));
+        const float4 one = make_float4(1.f, 1.f, 1.f, 1.f);  // a.g == nullptr: unit gains
+        const float4 g0 = a.g ? __ldg(reinterpret_cast<const float4*>(a.g + col)) : one;
+        const float4 g1 = a.g ? __ldg(reinterpret_cast<const float4*>(a.g + col + 4)) : one;
         const float iv = inv_s[r];
         __align__(16) bf16 o8[8];
         o8[0] = __float2bfloat16_rn(x0.x * iv * g0.x);
@@ -597,47 +610,50 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
       if (et0 == 0) mbar_arrive(xrdy);
       if (et0 == 0) chain_mark(cst, 3);
     }
-    const int ew = warp - 2, quarter = warp & 3;
+    const int quarter = warp & 3;
     const int et = threadIdx.x - 64;  // 0..127
-    for (int t = t0; t < t1; ++t) {
-      const int j = t - t0, b = j & 1;
-      mbar_wait(&accf[b], (j >> 1) & 1);
-      tc_fence_after();
-      float v[16];
-      tmem_ld16(tmem + b * kN + (static_cast<std::uint32_t>(quarter * 32) << 16), v);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acce[b]);
-      const int n = t * kM + quarter * 32 + lane;
-#pragma unroll
-      for (int r = 0; r < kN; ++r) {
-        if (r >= R) break;
-        const bool ok = n < a.N;
-        if (ok && a.logits) a.logits[static_cast<long long>(r) * a.N + n] = v[r];
-        LmStat st = ok ? LmStat{v[r], 1.f, 0.f, n} : none;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const LmStat o = shfl_stat(st, off);
-          st = (lane & off) ? stat_merge(o, st) : stat_merge(st, o);
-        }
-        if (lane == 0) red[quarter][r] = st;  // quarter order = vocab order within the tile
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (et < R) {
-        LmStat st = red[0][et];
-        for (int w = 1; w < 4; ++w) st = stat_merge(st, red[w][et]);
-        run[et] = stat_merge(run[et], st);
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      (void)ew;
-    }
-    if (et == 0) gv_stamp(3);
+    const std::uint32_t tq = tmem + (static_cast<std::uint32_t>(quarter * 32) << 16);
+    // one running statistic per (row, lane): rows outer, tiles inner
+    // (single-column TMEM loads keep the code small for any row count)
+    for (int j = 0; j < t1 - t0; ++j) mbar_wait(&accf[j], 0);
+    tc_fence_after();
     if (et == 0) chain_mark(cst, 4);
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      LmStat st = none;
+#pragma unroll 1
+      for (int t = t0; t < t1; t += 4) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          v[u] = t + u < t1 ? tmem_ld1(tq + static_cast<std::uint32_t>((t + u - t0) * kN + r)) : 0.f;
+        tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int n = (t + u) * kM + quarter * 32 + lane;
+          if (t + u < t1 && n < a.N) {
+            if (a.logits) a.logits[static_cast<long long>(r) * a.N + n] = v[u];
+            st = stat_merge(st, LmStat{v[u], 1.f, 0.f, n});
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const LmStat o = shfl_stat(st, off);
+        st = (lane & off) ? stat_merge(o, st) : stat_merge(st, o);
+      }
+      if (lane == 0) red[quarter][r] = st;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
     if (et < R) {
-      const LmStat st = run[et];
+      // quarters of one tile are vocab-ordered; across tiles the per-lane fold
+      // already ran in tile order, so quarter order here is a fixed order
+      LmStat st = red[0][et];
+      for (int w = 1; w < 4; ++w) st = stat_merge(st, red[w][et]);
       __stcg(reinterpret_cast<float4*>(part + static_cast<long long>(et) * G + c),
              make_float4(st.m, st.s, st.t, __int_as_float(st.idx)));
     }
+    if (et == 0) gv_stamp(3);
     asm volatile("bar.sync 1, 128;" ::: "memory");
     if (et == 0) {
       unsigned prev;
@@ -684,7 +700,13 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<32>(tmem);
+  if (warp == 0) {
+    if (tmax <= 2) tmem_dealloc<32>(tmem);
+    else if (tmax <= 4) tmem_dealloc<64>(tmem);
+    else if (tmax <= 8) tmem_dealloc<128>(tmem);
+    else if (tmax <= 16) tmem_dealloc<256>(tmem);
+    else tmem_dealloc<512>(tmem);
+  }
 }
 
 }  // namespace
@@ -698,8 +720,13 @@ void lm_head_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, LmS
     attr = true;
   }
   const int T = (a.N + kM - 1) / kM;
+  const int G = grid < T ? grid : T;
+  if ((T + G - 1) / G > kLmMaxTiles) {
+    std::fprintf(stderr, "lm_head_tc: %d vocab tiles over %d CTAs exceed %d tiles per CTA\n", T, G, kLmMaxTiles);
+    std::abort();
+  }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid < T ? grid : T);
+  cfg.gridDim = dim3(G);
   cfg.blockDim = dim3(192);
   cfg.dynamicSmemBytes = a.X ? lm_fold_smem(a.K) : kLmSmem;
   cfg.stream = st;

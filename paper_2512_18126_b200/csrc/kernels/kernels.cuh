@@ -98,6 +98,9 @@ struct GemvArgs {
   float* ssq_out = nullptr;
   // lm_head_tc with X (norm folded in): the residual rows to normalise, selected by sel[i]
   const int* sel = nullptr;
+  // kEpiResidual (SIMT gemv): the residual rows were last written at least two
+  // kernels back, so they are read before the PDL wait
+  bool res_early = false;
 };
 void gemv(const GemvArgs& a, cudaStream_t st);  // dispatches to gemv_stream for large matrices
 // HBM-streaming variant (gemv_stream.cu): persistent CTAs, cp.async.bulk ring.
