@@ -538,6 +538,7 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
     if (lane == 0) {  // MMA issuer: tile j -> TMEM columns [16j, 16j + 16)
       int q = 0;
       if (fold && t1 > t0) mbar_wait(xrdy, 0);  // the normalised rows are staged
+      chain_mark(cst, 5);
       for (int t = t0; t < t1; ++t) {
         const int j = t - t0;
         tc_fence_after();
@@ -554,6 +555,7 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
         }
         umma_commit(&accf[j]);
       }
+      chain_mark(cst, 7);
       gv_stamp(2);
     }
     __syncwarp();

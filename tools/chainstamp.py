@@ -13,7 +13,7 @@ sys.path.insert(0, '/root/repo')
 from paper_2512_18126_b200 import capi
 from paper_2512_18126_b200.configs import CONFIGS
 
-NAMES = {0x10010: 'o_proj', 0x12010: 'gate_up', 0x11040: 'down', 0x10040: 'down', 0x20000: 'qkv_attn', 0x20001: 'qkv_attn0',
+NAMES = {0x40000: 'o_gate_up', 0x10010: 'o_proj', 0x12010: 'gate_up', 0x11040: 'down', 0x10040: 'down', 0x20000: 'qkv_attn', 0x20001: 'qkv_attn0',
          0x30000: 'lm_head'}
 name = sys.argv[1] if len(sys.argv) > 1 else 'C1'
 eng, qc = capi.engine_for(dict(CONFIGS[name]))
@@ -82,10 +82,13 @@ for pos in range(L):
 tick_len = np.median([max(tk[-1]['ph'][2]) - tk[0]['t0'] for tk in sel])
 gap = np.median([sel[i + 1][0]['t0'] - max(sel[i][-1]['ph'][2]) for i in range(len(sel) - 1)])
 print('median tick: first entry -> lm_head end %.2f us; lm end -> next tick first entry %.2f us' % (tick_len / 1e3, gap / 1e3))
-print('%-10s %8s %8s %8s %8s %8s %8s %8s %8s' % ('kernel', 'start', 'wait_rel', 'p3', 'p4', 'p5', 'end_max', 'dur', 'rel-prev'))
+print('%-10s %8s %8s %8s %8s %8s %8s %8s %8s %8s %8s' % ('kernel', 'start', 'wait_rel', 'p3', 'p4', 'p5', 'p6', 'p7', 'end_max', 'dur', 'rel-prev'))
 for nm, v in rows:
     def g(k):
         return '%8.2f' % (v[k] / 1e3) if k in v else '%8s' % '-'
     dur = (v.get('p2_max', 0) - v.get('p1_max', 0)) / 1e3
-    print('%-10s %s %s %s %s %s %s %8.2f %s' % (nm, g('start'), g('p1_max'), g('p3_max'), g('p4_max'), g('p5_max'),
-                                             g('p2_max'), dur, g('release_after_prev_end')))
+    print('%-10s %s %s %s %s %s %s %s %s %8.2f %s' % (nm, g('start'), g('p1_max'), g('p3_max'), g('p4_max'), g('p5_max'),
+                                                   g('p6_max'), g('p7_max'), g('p2_max'), dur, g('release_after_prev_end')))
+    if nm == 'lm_head':
+        print('  lm_head min-over-CTAs: wait %s staged %s mma_start %s mma_issued %s tiles %s end %s' % (
+            g('p1_min'), g('p3_min'), g('p5_min'), g('p7_min'), g('p4_min'), g('p2_min')))
