@@ -217,6 +217,15 @@ int moa_run_batch(moa_engine* eng, const moa_run_config* cfg, const int* samples
  * before the request (moa_engine_trace); *len = bytes, written to buf when
  * cap > *len. */
 int moa_engine_trace(moa_engine* eng, int enable);
+/* Engine clock for protocol-level callers (the HTTP engine service,
+ * engine_service.cpp:49-171): mark time zero on the engine stream, then read
+ * the device time at the end of a tick (seconds; needs moa_engine_trace on
+ * while that tick ran).  moa_agent_record: the engine's record of one agent
+ * (ticks of decode start / end, prompt / output sizes). */
+int moa_engine_mark_start(moa_engine* eng);
+int moa_engine_tick(moa_engine* eng, int* tick); /* ticks run so far (the next tick's index) */
+int moa_tick_seconds(moa_engine* eng, int tick, double* seconds);
+int moa_agent_record_get(moa_engine* eng, int layer, int position, moa_agent_record* rec);
 int moa_query_trace(const moa_query* q, char* buf, long long cap, long long* len);
 /* Device time (ms since the request's first tick) at the end of every tick;
  * needs engine tracing (moa_engine_trace).  *n = ticks, min(cap, *n) written. */

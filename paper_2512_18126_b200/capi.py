@@ -124,6 +124,10 @@ _SIGS = {
     "moa_read_logits": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_float)], C.c_int),
     "moa_agent_state": ([C.c_void_p, C.c_int, C.c_int] + [_P(C.c_int)] * 4, C.c_int),
     "moa_engine_trace": ([C.c_void_p, C.c_int], C.c_int),
+    "moa_engine_mark_start": ([C.c_void_p], C.c_int),
+    "moa_engine_tick": ([C.c_void_p, _P(C.c_int)], C.c_int),
+    "moa_tick_seconds": ([C.c_void_p, C.c_int, _P(C.c_double)], C.c_int),
+    "moa_agent_record_get": ([C.c_void_p, C.c_int, C.c_int, _P(AgentRecordC)], C.c_int),
     "moa_query_trace": ([C.c_void_p, C.c_char_p, C.c_longlong, _P(C.c_longlong)], C.c_int),
     "moa_query_ticks": ([C.c_void_p, _P(C.c_double), C.c_int, _P(C.c_int)], C.c_int),
     "moa_run_batch": ([C.c_void_p, C.c_void_p, _P(C.c_int), C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
@@ -270,6 +274,27 @@ class Engine:
 
     def reset(self):
         check(lib().moa_engine_reset(self.h))
+
+    def mark_start(self):
+        """Time zero of tick_seconds (engine stream)."""
+        check(lib().moa_engine_mark_start(self.h))
+
+    def tick(self) -> int:
+        """Ticks run so far (the index of the next tick)."""
+        v = C.c_int()
+        check(lib().moa_engine_tick(self.h, C.byref(v)))
+        return v.value
+
+    def tick_seconds(self, tick: int) -> float:
+        """Device seconds from mark_start to the end of `tick` (needs trace(True) while it ran)."""
+        v = C.c_double()
+        check(lib().moa_tick_seconds(self.h, tick, C.byref(v)))
+        return v.value
+
+    def record(self, a) -> dict:
+        r = AgentRecordC()
+        check(lib().moa_agent_record_get(self.h, a[0], a[1], C.byref(r)))
+        return {k: getattr(r, k) for k, _ in AgentRecordC._fields_}
 
     def attach_comm(self, nccl_id: bytes, rank: int, world: int):
         """Join a tree-partitioned serving group (call before the first request)."""
@@ -506,3 +531,64 @@ def placement(topology: dict, world: int) -> dict:
     check(lib().moa_placement(kind, len(widths), w, cs, world, out))
     names = [f"{l + 1}:{p}" for l, n in enumerate(widths) for p in range(n)]
     return dict(zip(names, list(out)))
+
+
+class SlotPlan:
+    """Incremental slot filling of one consumer (router.cpp:38-184) over the
+    C-ABI moa_slotplan_*: each event returns the engine actions it triggers,
+    as dicts {"kind": "prefill_only"|"generate"|"reclaim", "start", "tokens"}."""
+
+    _OPS = {"start": 0, "chunk": 1, "done": 2, "cancelled": 3}
+    _KINDS = {0: "prefill_only", 1: "generate", 2: "reclaim"}
+
+    def __init__(self, self_id, prefix, slots, suffix, incremental=True):
+        """slots: [(producer (layer, position), separator tokens), ...] in slot order."""
+        sl = (C.c_int * max(1, len(slots)))(*[int(p[0]) for p, _ in slots])
+        sp = (C.c_int * max(1, len(slots)))(*[int(p[1]) for p, _ in slots])
+        seps = [int(t) for _, sep in slots for t in sep]
+        st = (C.c_int32 * max(1, len(seps)))(*seps)
+        sn = (C.c_int * max(1, len(slots)))(*[len(sep) for _, sep in slots])
+        pre, npre = _ints(prefix)
+        suf, nsuf = _ints(suffix)
+        h = C.c_void_p()
+        check(lib().moa_slotplan_create(int(self_id[0]), int(self_id[1]), pre, npre, sl, sp, st, sn, len(slots), suf,
+                                        nsuf, int(bool(incremental)), C.byref(h)))
+        self.h = h
+        self.self_id = (int(self_id[0]), int(self_id[1]))
+
+    def _event(self, op, producer=(0, 0), tokens=()):
+        tb, n = _ints(tokens)
+        cap = 1 << 16
+        buf = (C.c_int32 * cap)()
+        nw = C.c_int()
+        check(lib().moa_slotplan_event(self.h, self._OPS[op], int(producer[0]), int(producer[1]), tb, n, buf, cap,
+                                       C.byref(nw)))
+        out, i = [], 0
+        while i < nw.value:
+            k, s, m = buf[i], buf[i + 1], buf[i + 2]
+            out.append({"kind": self._KINDS[k], "start": s, "tokens": list(buf[i + 3:i + 3 + m])})
+            i += 3 + m
+        return out
+
+    def start(self):
+        return self._event("start")
+
+    def on_chunk(self, producer, tokens):
+        return self._event("chunk", producer, tokens)
+
+    def on_precursor_done(self, producer):
+        return self._event("done", producer)
+
+    def on_precursor_cancelled(self, producer):
+        return self._event("cancelled", producer)
+
+    def close(self):
+        if self.h:
+            lib().moa_slotplan_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

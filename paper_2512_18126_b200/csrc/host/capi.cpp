@@ -428,6 +428,47 @@ int moa_engine_trace(moa_engine* eng, int enable) {
   return guard([&] { E(eng).set_tracing(enable != 0); });
 }
 
+int moa_engine_mark_start(moa_engine* eng) {
+  return guard([&] { E(eng).mark_start(); });
+}
+
+int moa_engine_tick(moa_engine* eng, int* tick) {
+  return guard([&] {
+    need(tick, "tick");
+    *tick = E(eng).tick();
+  });
+}
+
+int moa_tick_seconds(moa_engine* eng, int tick, double* seconds) {
+  return guard([&] {
+    need(seconds, "seconds");
+    *seconds = E(eng).ms_since_start(tick) / 1e3;
+  });
+}
+
+int moa_agent_record_get(moa_engine* eng, int layer, int position, moa_agent_record* rec) {
+  return guard([&] {
+    need(rec, "rec");
+    const moa::AgentId id{layer, position};
+    const moa::AgentRecord& r = E(eng).record(id);
+    *rec = moa_agent_record{layer,
+                            position,
+                            r.model,
+                            r.invoked,
+                            r.pruned,
+                            r.empty_input,
+                            r.prompt_tokens,
+                            r.output_tokens,
+                            r.prefill_only_calls,
+                            r.recomputed_tokens,
+                            r.reclaimed_tokens,
+                            r.decode_start,
+                            r.decode_end,
+                            r.complete,
+                            r.precursor_ready_tick};
+  });
+}
+
 int moa_query_trace(const moa_query* q, char* buf, long long cap, long long* len) {
   return guard([&] {
     need(q, "query");
