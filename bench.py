@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the secondary 1B-agent (C2) decode measurement reported beside the headline")
     ap.add_argument("--secondary-out", type=int, default=128, help="C2 output tokens per agent for the secondary run")
+    ap.add_argument("--no-timeline", action="store_true", help="skip the in-graph tick timeline (chain stamps)")
     ap.add_argument("--concurrency", default="4,8",
                     help="continuous-batching sweep reported beside the headline (comma list; '' to skip)")
     return ap.parse_args()
@@ -347,6 +348,15 @@ def main():
         n_ee_launches += sum(4 + (e["outputs"] > 1) for e in r["metricq"] if e["evaluated"])
     probes = eng.probe_stats()
     eng.probe(False)
+    # in-graph tick timeline of one more (untimed) request: per-CTA %globaltimer
+    # stamps of the decode chain (chain.py) -- the probes above bypass the graphs
+    timeline = None
+    if rank == 0 and not args.no_timeline:
+        from paper_2512_18126_b200 import chain
+        try:
+            timeline = chain.request_timeline(eng, qc, sample_of(0))
+        except Exception as e:  # diagnostics only
+            timeline = {"error": str(e)}
     if pg:
         t = torch.tensor([dev_ms, e2e_wall * 1e3, toks, e2e_toks], dtype=torch.float64, device="cuda")
         mx = t.clone()
@@ -378,6 +388,7 @@ def main():
         "kernels": {k: {"launches": v["launches"], "ms_per_request": v["ms"] / args.steps,
                         "avg_us": 1e3 * v["ms"] / max(1, v["launches"]),
                         "gbs": v["bytes"] / max(1e-12, v["ms"] / 1e3) / 1e9} for k, v in probes.items()},
+        "tick_timeline": timeline,
         "clocks": clk.summary(),
         "peaks": {"hbm_gbs": hbm, "bf16_tflops": tf, "source": src},
         "engine": {"rows_per_request": rows / args.steps, "forwards_per_request": fwd / args.steps,
