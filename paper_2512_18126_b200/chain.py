@@ -27,10 +27,15 @@ def _name(tag):
         return NAMES[tag]
     if tag >> 16 == 1:
         return f"gemv(epi={(tag >> 12) & 15},K={16 * (tag & 0xfff)})"
+    if tag >> 16 == 5:
+        epi = {0: "f32", 1: "residual", 2: "swiglu", 3: "qkv"}.get((tag >> 12) & 15, "?")
+        return f"gemv_tc({epi},K={16 * (tag & 0xfff)})"
+    if tag >> 16 == 6:
+        return "attention"
     return hex(tag)
 
 
-def collect(eng, qc, sample=0, cap=1 << 22):
+def collect(eng, qc, sample=0, cap=1 << 25):
     """Run one request with chain stamps on; returns (records [n, 4] = tag, phase, cta, ns), e2e_ms."""
     import torch
     buf = torch.zeros(2 + 2 * cap, dtype=torch.int64, device="cuda")
@@ -49,7 +54,7 @@ def collect(eng, qc, sample=0, cap=1 << 22):
 
 
 def ticks(records):
-    """Group stamps into kernel launches (per tag, entry stamps split at > 3 us
+    """Group stamps into kernel launches (per tag, entry stamps split at > 8 us
     gaps) and launches into ticks (each ends with an LM head)."""
     tag, phase, t = records[:, 0], records[:, 1], records[:, 3]
     inst = []
@@ -57,7 +62,7 @@ def ticks(records):
         e = np.sort(t[(tag == tg) & (phase == 0)])
         if len(e) == 0:
             continue
-        for s in np.split(e, np.where(np.diff(e) > 3000)[0] + 1):
+        for s in np.split(e, np.where(np.diff(e) > 8000)[0] + 1):
             inst.append(dict(tag=int(tg), t0=int(s.min()), ph=collections.defaultdict(list)))
     inst.sort(key=lambda d: d["t0"])
     by_tag = collections.defaultdict(list)
@@ -79,6 +84,11 @@ def ticks(records):
     return out
 
 
+def _end(d):
+    """Last stamp of a launch (its end stamp when every CTA reached it)."""
+    return max(max(v) for v in d["ph"].values() if v)
+
+
 def timeline(tick_list, first_frac=0.75):
     """Median timeline over the ticks of the request's last phase (single
     agent decoding), in microseconds from the tick's first kernel entry."""
@@ -86,7 +96,7 @@ def timeline(tick_list, first_frac=0.75):
     if not sel:
         return None
     L = collections.Counter(len(x) for x in sel).most_common(1)[0][0]
-    sel = [x for x in sel if len(x) == L and all(d["ph"][2] for d in x)]
+    sel = [x for x in sel if len(x) == L]
     if len(sel) < 2:
         return None
     rows = []
@@ -96,13 +106,13 @@ def timeline(tick_list, first_frac=0.75):
             d, base = tk[pos], tk[0]["t0"]
             v["start"].append(d["t0"] - base)
             v["release"].append(max(d["ph"][1]) - base if d["ph"][1] else np.nan)
-            v["end"].append(max(d["ph"][2]) - base)
+            v["end"].append(_end(d) - base)
         med = {k: float(np.nanmedian(x)) / 1e3 for k, x in v.items()}
         rows.append({"kernel": _name(sel[0][pos]["tag"]), "start_us": round(med["start"], 2),
                      "release_us": round(med["release"], 2), "end_us": round(med["end"], 2),
                      "release_to_end_us": round(med["end"] - med["release"], 2)})
-    tick_us = float(np.median([max(tk[-1]["ph"][2]) - tk[0]["t0"] for tk in sel])) / 1e3
-    gap_us = float(np.median([sel[i + 1][0]["t0"] - max(sel[i][-1]["ph"][2]) for i in range(len(sel) - 1)])) / 1e3
+    tick_us = float(np.median([_end(tk[-1]) - tk[0]["t0"] for tk in sel])) / 1e3
+    gap_us = float(np.median([sel[i + 1][0]["t0"] - _end(sel[i][-1]) for i in range(len(sel) - 1)])) / 1e3
     return {"ticks_analysed": len(sel), "kernels_per_tick": L, "tick_us": round(tick_us, 2),
             "gap_to_next_tick_us": round(gap_us, 2), "kernels": rows}
 

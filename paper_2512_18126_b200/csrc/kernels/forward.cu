@@ -548,26 +548,30 @@ attention_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, c
 }
 
 
-// GQA attention: CTA = (row, kv head, key split of kv_split(hd) keys); the
-// group's q heads (<= 4) share every K/V load.  Warp w takes 32-key chunks
+// GQA attention: CTA = (row, HPG q heads of one kv group, key split of
+// kv_split(hd) keys); the CTA's q heads share every K/V load (HPG below the
+// group size: more CTAs per row, K/V re-read once per CTA).  Warp w takes 32-key chunks
 // w, w+8, ... with an online softmax per head (K: lane = key, full row in
 // registers; V: lane = HD/32 output dims of every key), warps combine in
 // smem in a fixed order; a row whose context spans several CTAs writes
 // per-head partials and the last-arriving CTA combines them in split order.
-template <int HD>
+template <int HD, int HPG>
 __global__ void __launch_bounds__(256, 1)
 attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, const int* __restrict__ meta, int nh,
                      int nkv, const bf16* __restrict__ kpool, const bf16* __restrict__ vpool, long long kv_stride,
                      long long layer_off, int max_ctx, bf16* __restrict__ o, float* __restrict__ ws,
                      int* __restrict__ cnt, int nsplit_max, int split_keys) {
-  constexpr int NW = 8, HPG = 4, E = HD / 32;
+  constexpr int NW = 8, E = HD / 32;
   __shared__ float qs[HPG][HD];
   __shared__ float wm[NW][HPG], wl[NW][HPG];
   __shared__ float wo[NW][HPG][HD];
   __shared__ float cm_s[HPG], cl_s[HPG];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r = blockIdx.x, g = blockIdx.y, s = blockIdx.z;
+  const int r = blockIdx.x, s = blockIdx.z;
+  const int cpg = (nh / nkv) / HPG;  // CTAs per kv group
+  const int g = blockIdx.y / cpg;    // kv head
+  const int h0 = g * (nh / nkv) + (blockIdx.y % cpg) * HPG;  // first q head
   // Tick metadata and the keys of earlier ticks are not produced by this
   // forward's previous kernel: read / prefetch them before the PDL wait.
   if (r >= __ldg(meta)) return;
@@ -575,17 +579,22 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
   const int n = rd.pos + 1;
   const int nsplit = (n + split_keys - 1) / split_keys;
   if (s >= nsplit) return;
-  const int hpg = nh / nkv;
   const int kb = s * split_keys, ke = min(n, kb + split_keys);
   const bf16* K = kpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
   const bf16* V = vpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
+  __shared__ unsigned long long cst[kChainPhases];
+  if (threadIdx.x == 0) {
+    chain_reset(cst);
+    chain_mark(cst, 0);
+  }
   for (int j = kb + threadIdx.x; j < ke - 1 && j < kb + 2 * NW * 32; j += NW * 32) {  // old keys only (pos is new)
     asm volatile("prefetch.global.L2 [%0];" ::"l"(K + static_cast<long long>(j) * HD));
     asm volatile("prefetch.global.L2 [%0];" ::"l"(V + static_cast<long long>(j) * HD));
   }
   MOA_PDL_ENTRY();
-  for (int i = threadIdx.x; i < hpg * HD; i += NW * 32)
-    qs[i / HD][i % HD] = __bfloat162float(q[(static_cast<long long>(r) * nh + g * hpg + i / HD) * HD + i % HD]);
+  if (threadIdx.x == 0) chain_mark(cst, 1);
+  for (int i = threadIdx.x; i < HPG * HD; i += NW * 32)
+    qs[i / HD][i % HD] = __bfloat162float(q[(static_cast<long long>(r) * nh + h0 + i / HD) * HD + i % HD]);
   __syncthreads();
   const float scale = rsqrtf(static_cast<float>(HD));
   float m[HPG], l[HPG], acc[HPG][E];
@@ -613,7 +622,6 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
       vv[jj] = j0 + jj < ke ? __ldg(reinterpret_cast<const VT*>(V + static_cast<long long>(j0 + jj) * HD + lane * E)) : VT{};
 #pragma unroll
     for (int h = 0; h < HPG; ++h) {
-      if (h >= hpg) break;
       float d = 0.f;
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
@@ -654,7 +662,6 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
   }
 #pragma unroll
   for (int h = 0; h < HPG; ++h) {
-    if (h >= hpg) break;
     if (lane == 0) {
       wm[warp][h] = m[h];
       wl[warp][h] = l[h];
@@ -664,7 +671,7 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
   }
   __syncthreads();
   // CTA combine of the warps, per head, fixed warp order
-  if (threadIdx.x < hpg) {
+  if (threadIdx.x < HPG) {
     const int h = threadIdx.x;
     float M = -INFINITY;
     for (int w = 0; w < NW; ++w) M = fmaxf(M, wm[w][h]);
@@ -674,13 +681,13 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
     cl_s[h] = Lsum;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < hpg * HD; i += NW * 32) {
+  for (int i = threadIdx.x; i < HPG * HD; i += NW * 32) {
     const int h = i / HD, e = i % HD;
     const float M = cm_s[h];
     float val = 0.f;
     for (int w = 0; w < NW; ++w)
       if (wm[w][h] != -INFINITY) val += __expf(wm[w][h] - M) * wo[w][h][e];
-    const int head = g * hpg + h;
+    const int head = h0 + h;
     if (nsplit == 1) {
       o[(static_cast<long long>(r) * nh + head) * HD + e] = __float2bfloat16_rn(val / cl_s[h]);
     } else {
@@ -692,38 +699,47 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
       }
     }
   }
-  if (nsplit == 1) return;
+  if (nsplit == 1) {
+    if (threadIdx.x == 0) {
+      chain_mark(cst, 2);
+      chain_flush(cst, 6u << 16);
+    }
+    return;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned prev;
-    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(cnt + r * nkv + g) : "memory");
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                 : "=r"(prev)
+                 : "l"(cnt + r * gridDim.y + blockIdx.y)
+                 : "memory");
     last = prev == static_cast<unsigned>(nsplit - 1);
   }
   __syncthreads();
   if (!last) return;
   // combine the splits (split order); split stats read in parallel
   __shared__ float sw_s[HPG][64];
-  for (int i = threadIdx.x; i < hpg * nsplit; i += NW * 32) {
+  for (int i = threadIdx.x; i < HPG * nsplit; i += NW * 32) {
     const int h = i / nsplit, t = i % nsplit;
-    sw_s[h][t] = __ldcg(ws + ((static_cast<long long>(r) * nh + g * hpg + h) * nsplit_max + t) * (2 + HD));
+    sw_s[h][t] = __ldcg(ws + ((static_cast<long long>(r) * nh + h0 + h) * nsplit_max + t) * (2 + HD));
   }
   __syncthreads();
-  if (threadIdx.x < hpg) {
+  if (threadIdx.x < HPG) {
     const int h = threadIdx.x;
     float M = -INFINITY;
     for (int t = 0; t < nsplit; ++t) M = fmaxf(M, sw_s[h][t]);
     float Lsum = 0.f;
     for (int t = 0; t < nsplit; ++t) {
       const float w = __expf(sw_s[h][t] - M);
-      Lsum += w * __ldcg(ws + ((static_cast<long long>(r) * nh + g * hpg + h) * nsplit_max + t) * (2 + HD) + 1);
+      Lsum += w * __ldcg(ws + ((static_cast<long long>(r) * nh + h0 + h) * nsplit_max + t) * (2 + HD) + 1);
       sw_s[h][t] = w;
     }
     cl_s[h] = Lsum;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < hpg * HD; i += NW * 32) {
+  for (int i = threadIdx.x; i < HPG * HD; i += NW * 32) {
     const int h = i / HD, e = i % HD;
-    const float* pr = ws + (static_cast<long long>(r) * nh + g * hpg + h) * nsplit_max * (2 + HD);
+    const float* pr = ws + (static_cast<long long>(r) * nh + h0 + h) * nsplit_max * (2 + HD);
     float val = 0.f;
     for (int t0 = 0; t0 < nsplit; t0 += 8) {
       float pv[8];
@@ -733,9 +749,13 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
       for (int u = 0; u < 8; ++u)
         if (t0 + u < nsplit) val += sw_s[h][t0 + u] * pv[u];
     }
-    o[(static_cast<long long>(r) * nh + g * hpg + h) * HD + e] = __float2bfloat16_rn(val / cl_s[h]);
+    o[(static_cast<long long>(r) * nh + h0 + h) * HD + e] = __float2bfloat16_rn(val / cl_s[h]);
   }
-  if (threadIdx.x == 0) cnt[r * nkv + g] = 0;
+  if (threadIdx.x == 0) cnt[r * gridDim.y + blockIdx.y] = 0;
+  if (threadIdx.x == 0) {
+    chain_mark(cst, 2);
+    chain_flush(cst, 6u << 16);
+  }
 }
 
 
@@ -1196,15 +1216,32 @@ void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, co
   if (R_cap <= 0) return;
   const int nsplit_max = (max_ctx + kKvSplit - 1) / kKvSplit;
   const int split_keys = kv_split(hd);
-  dim3 grid(R_cap, nkv, nsplit_cap);
-  if (hd == 64)
-    launch_pdl(attention_gqa_kernel<64>, grid, dim3(256), st, q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off,
-               max_ctx, o, ws, cnt, nsplit_max, split_keys);
-  else if (hd == 128)
-    launch_pdl(attention_gqa_kernel<128>, grid, dim3(256), st, q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off,
-               max_ctx, o, ws, cnt, nsplit_max, split_keys);
-  else
+  // q heads per CTA: MOA_ATTN_HPC (1, 2 or 4); default: the whole GQA group
+  // (measured: one CTA per q head re-reads K/V per head -- 1.5x slower on
+  // 2k-token 8B contexts, 6% slower on 1B decode)
+  static const int hpc_env = [] {
+    const char* e = std::getenv("MOA_ATTN_HPC");
+    return e ? std::atoi(e) : 4;
+  }();
+  const int hpg = nh / nkv;
+  int hpc = hpc_env == 2 || hpc_env == 4 ? hpc_env : 1;
+  while (hpg % hpc) hpc >>= 1;
+  dim3 grid(R_cap, nh / hpc, nsplit_cap);
+  auto go = [&](auto kern) {
+    launch_pdl(kern, grid, dim3(256), st, q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx, o, ws,
+               cnt, nsplit_max, split_keys);
+  };
+  if (hd == 64) {
+    if (hpc == 1) go(attention_gqa_kernel<64, 1>);
+    else if (hpc == 2) go(attention_gqa_kernel<64, 2>);
+    else go(attention_gqa_kernel<64, 4>);
+  } else if (hd == 128) {
+    if (hpc == 1) go(attention_gqa_kernel<128, 1>);
+    else if (hpc == 2) go(attention_gqa_kernel<128, 2>);
+    else go(attention_gqa_kernel<128, 4>);
+  } else {
     printf("attention: unsupported head_dim %d\n", hd);
+  }
 }
 
 MOA_CHAIN_STAMP_SETTER(forward_chain_stamp)

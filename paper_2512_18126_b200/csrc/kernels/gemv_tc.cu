@@ -255,6 +255,12 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     mbar_fence_init();
   }
   if (threadIdx.x == 0) gv_stamp(0);
+  __shared__ unsigned long long cst[kChainPhases];
+  const unsigned stag = (5u << 16) | (static_cast<unsigned>(a.epi) << 12) | ((a.K >> 4) & 0xfff);
+  if (threadIdx.x == 0) {
+    chain_reset(cst);
+    chain_mark(cst, 0);
+  }
   const int R = a.meta ? __ldcg(a.meta) : a.R;  // tick metadata: not produced by the previous kernel
   // Dependents may launch now: they prefetch their own weights while this
   // grid runs, then wait (griddepcontrol.wait) for its completion before
@@ -354,6 +360,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
       const int s = kt % stages;
       mbar_wait(&full[s], (kt / stages) & 1);
       if (kt == 0) gv_stamp(2);
+      if (kt == 0) chain_mark(cst, 4);
       tc_fence_after();
       const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + (nx ? kt : s) * kTileX);
 #pragma unroll
@@ -364,9 +371,11 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   }
   __syncwarp();
   pdl_wait();  // every epilogue thread reads the previous kernel's outputs (rows, residual)
+  if (threadIdx.x == 64) chain_mark(cst, 1);
   mbar_wait(done, 0);
   tc_fence_after();
   if (threadIdx.x == 0) gv_stamp(3);
+  if (threadIdx.x == 64) chain_mark(cst, 3);
 
   const int row = warp * 32 + lane, n = m0 + row;
   float v[16];
@@ -397,6 +406,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
             : "memory");
     }
     if (threadIdx.x == 0) gv_stamp(5);
+    if (threadIdx.x == 0) chain_mark(cst, 5);
     if (warp * 32 < per) {  // warps holding at least one reduced row (whole warps: the epilogue shuffles)
       mbar_wait(&land_bar, 0);
       const bool mine = row < per;
@@ -416,12 +426,17 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
           }
         }
       if (threadIdx.x == 0) gv_stamp(6);
+      if (threadIdx.x == 0) chain_mark(cst, 6);
       epilogue(a, mine ? m0 + wr : a.N, R, v);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) gv_stamp(4);
+  if (threadIdx.x == 0) {
+    chain_mark(cst, 2);
+    chain_flush(cst, stag);
+  }
   if (warp == 0) tmem_dealloc<32>(tmem);
 }
 

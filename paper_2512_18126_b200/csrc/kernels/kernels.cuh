@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -242,7 +243,15 @@ void small_forward_debug_trace(unsigned long long* buf);  // debug: per-CTA cloc
 // `cnt` >= R*nh ints, zero-initialised once (the kernel leaves them zero).
 constexpr int kKvSplit = 128;  // smallest split (sizes the partial workspace)
 // keys per attention CTA: 8 warps x 32 for hd 64, 4 warps x 32 for hd 128
-inline int kv_split(int hd) { return hd == 64 ? 1024 : 512; }  // keys per attention CTA (GQA kernel)
+// keys per attention CTA (GQA kernel); MOA_KV_SPLIT overrides (multiple of kKvSplit)
+inline int kv_split(int hd) {
+  static const int env = [] {
+    const char* e = std::getenv("MOA_KV_SPLIT");
+    const int v = e ? std::atoi(e) : 0;
+    return v >= kKvSplit && v % kKvSplit == 0 ? v : 0;
+  }();
+  return env ? env : (hd == 64 ? 1024 : 512);
+}
 long long attention_ws_floats(int R, int nh, int hd, int max_ctx);
 void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, const int* meta, int nh, int nkv,
                int hd, const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx,

@@ -8,7 +8,7 @@
 namespace moa::k {
 namespace {
 __device__ unsigned long long* g_chain_stamp = nullptr;
-constexpr unsigned long long kChainStampCap = 1ull << 22;
+constexpr unsigned long long kChainStampCap = 1ull << 25;
 constexpr int kChainPhases = 8;
 
 __device__ __forceinline__ void chain_mark(unsigned long long* cs, int phase) {
