@@ -28,8 +28,12 @@ GpuEngine::GpuEngine(std::vector<ModelSpec> models, std::vector<int> agents_per_
     throw ValidationError("engine: agents x max_out exceeds the symbolic token range");
   for (std::size_t m = 0; m < models.size(); ++m) {
     const int cap = std::max(1, agents_per_model[m]);
+    static const bool graphs = [] {
+      const char* e = std::getenv("MOA_GRAPHS");
+      return !(e && e[0] == '0');
+    }();
     models_.push_back(std::make_unique<DeviceModel>(models[m], cap, opt_.max_ctx, opt_.max_rows + max_slots_,
-                                                    max_slots_, stream_));
+                                                    max_slots_, stream_, graphs));
     logits_v_ = std::max(logits_v_, models[m].vocab);
     models_.back()->set_tensor_cores(opt_.tensor_cores);
   }
@@ -43,6 +47,7 @@ GpuEngine::GpuEngine(std::vector<ModelSpec> models, std::vector<int> agents_per_
     MOA_CUDA(cudaMalloc(&logits_scratch_, sizeof(float) * static_cast<long long>(max_slots_) * logits_v_));
   }
   ring_bytes_ = sizeof(k::RowDesc) * (opt_.max_rows + max_slots_) + sizeof(int) * (2 * max_slots_ + 3) + 16;
+  for (const auto& dm : models_) ring_bytes_ = std::max(ring_bytes_, DeviceModel::kMaxRun * dm->run_stride());
   for (int i = 0; i < kRing; ++i) {
     Staging s;
     MOA_CUDA(cudaMallocHost(&s.host, ring_bytes_));
@@ -68,6 +73,16 @@ GpuEngine::GpuEngine(std::vector<ModelSpec> models, std::vector<int> agents_per_
     }
   }
   if (const char* e = std::getenv("MOA_ASYNC_UPLOAD")) async_upload_ = std::string(e) != "0";
+  for (std::size_t m = 0; m < models_.size(); ++m)
+    for (int b = 0; b < 2; ++b) {
+      cudaEvent_t e2;
+      MOA_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+      run_free_.push_back(e2);
+      MOA_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+      run_ready_.push_back(e2);
+    }
+  run_par_.assign(models_.size(), 0);
+  if (const char* e = std::getenv("MOA_DECODE_RUN")) max_run_ = std::max(1, std::min(DeviceModel::kMaxRun, std::atoi(e)));
   // two persistent (cooperative, one CTA per SM) forwards must never run side by side
   if (const char* e = std::getenv("MOA_MK")) overlap_models_ = std::string(e) == "0";
   if (const char* e = std::getenv("MOA_OVERLAP")) overlap_models_ = overlap_models_ && std::string(e) != "0";
@@ -95,6 +110,8 @@ GpuEngine::~GpuEngine() {
   }
   for (auto e2 : blob_free_) cudaEventDestroy(e2);
   for (auto e2 : blob_ready_) cudaEventDestroy(e2);
+  for (auto e2 : run_free_) cudaEventDestroy(e2);
+  for (auto e2 : run_ready_) cudaEventDestroy(e2);
   if (tick_fork_) cudaEventDestroy(tick_fork_);
   if (start_ev_) cudaEventDestroy(start_ev_);
   for (void* p : {static_cast<void*>(out_tok_), static_cast<void*>(out_lp_), static_cast<void*>(out_ent_),
@@ -302,6 +319,54 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   forwards_ += 1;
 }
 
+void GpuEngine::upload_and_forward_run(int m, int K, const std::vector<k::RowDesc>& rows, const std::vector<int>& lout,
+                                       cudaStream_t st) {
+  DeviceModel& dm = *models_[static_cast<std::size_t>(m)];
+  Staging& s = ring_[ring_next_];
+  ring_next_ = (ring_next_ + 1) % ring_.size();
+  {
+    const auto t_wait = std::chrono::steady_clock::now();
+    MOA_CUDA(cudaEventSynchronize(s.done));
+    host_wait_ms_ += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wait).count();
+  }
+  // K compact tick blobs [lsel | lout | meta] (padded) + rows: tick j's rows
+  // advance one position and read the token decoded by tick j - 1
+  const std::size_t stride = dm.run_stride();
+  const int L = dm.max_logit_rows(), sb = dm.buffers().sel_bytes, R = static_cast<int>(rows.size());
+  int max_pos = 0;
+  for (int j = 0; j < K; ++j) {
+    char* base = s.host + j * stride;
+    int* sel = reinterpret_cast<int*>(base);
+    auto* rd = reinterpret_cast<k::RowDesc*>(base + sb);
+    for (int i = 0; i < R; ++i) {
+      k::RowDesc d = rows[static_cast<std::size_t>(i)];
+      d.pos += j;
+      d.tok = j == 0 ? d.tok : d.tok - j;  // ref(slot, k) = -1 - (slot * max_out + k): k advances with the tick
+      d.out = d.out + j;
+      rd[i] = d;
+      sel[i] = i;
+      sel[L + i] = lout[static_cast<std::size_t>(i)] + j;
+      max_pos = std::max(max_pos, d.pos);
+    }
+    sel[2 * L] = R;
+    sel[2 * L + 1] = R;
+    sel[2 * L + 2] = max_pos;
+  }
+  const int p = run_par_[static_cast<std::size_t>(m)] ^= 1;
+  const std::size_t ev = 2 * static_cast<std::size_t>(m) + static_cast<std::size_t>(p);
+  cudaStream_t cs = cstreams_[static_cast<std::size_t>(m)];
+  MOA_CUDA(cudaStreamWaitEvent(cs, run_free_[ev], 0));
+  MOA_CUDA(cudaMemcpyAsync(dm.run_blob(p), s.host, K * stride, cudaMemcpyHostToDevice, cs));
+  MOA_CUDA(cudaEventRecord(s.done, cs));
+  MOA_CUDA(cudaEventRecord(run_ready_[ev], cs));
+  MOA_CUDA(cudaStreamWaitEvent(st, run_ready_[ev], 0));
+  dm.forward_run(K, R, max_pos, out_tok_, out_tok_, out_lp_, out_ent_, st, p);
+  MOA_CUDA(cudaEventRecord(run_free_[ev], st));
+  rows_total_ += static_cast<long long>(K) * R;
+  weight_bytes_ += K * dm.weight_bytes();
+  forwards_ += K;
+}
+
 void GpuEngine::step() {
   const auto host_t0 = std::chrono::steady_clock::now();
   struct HostTimer {
@@ -373,6 +438,33 @@ void GpuEngine::step() {
   // successor's incremental prefill overlaps its predecessors' decode.
   int active = 0;
   for (std::size_t m = 0; m < nm; ++m) active += !rows[m].empty();
+  // Decode run: when every row of this tick is a decode row and no request
+  // reaches a chunk boundary or its end before tick t + K - 1, the K ticks
+  // differ only by one position and one token each -- they run as one graph
+  // launch (no host decision can change them: callbacks fire only on chunk /
+  // completion events, which the run ends on).
+  int K = 1;
+  if (in_run_ && max_run_ > 1 && world() == 1 && !tracing_ && !probing_ && !opt_.keep_logits && !plan.empty()) {
+    K = max_run_;
+    for (const Plan& p : plan) {
+      const Req& r = *p.r;
+      if (p.kind != Decode || !r.local) {
+        K = 1;
+        break;
+      }
+      for (int j = 0; j < K; ++j) {  // first tick of the run that emits an event
+        const int n = r.n_out + j + 1;
+        if (n - r.chunk_begin >= r.apc || n == r.max_new) {
+          K = j + 1;
+          break;
+        }
+      }
+    }
+    for (std::size_t m = 0; m < nm && K > 1; ++m)
+      if (!rows[m].empty() && (!models_[m]->runs_supported() || static_cast<int>(rows[m].size()) >
+                                                                     models_[m]->max_logit_rows()))
+        K = 1;
+  }
   const bool fan_out = active > 1 && overlap_models_;
   if (fan_out) MOA_CUDA(cudaEventRecord(tick_fork_, stream_));
   for (std::size_t m = 0; m < nm; ++m)
@@ -383,7 +475,10 @@ void GpuEngine::step() {
         st = mstreams_[m];
         MOA_CUDA(cudaStreamWaitEvent(st, tick_fork_, 0));
       }
-      upload_and_forward(static_cast<int>(m), rows[m], lsel[m], lout[m], st);
+      if (K > 1)
+        upload_and_forward_run(static_cast<int>(m), K, rows[m], lout[m], st);
+      else
+        upload_and_forward(static_cast<int>(m), rows[m], lsel[m], lout[m], st);
       if (fan_out) {
         MOA_CUDA(cudaEventRecord(mdone_[m], st));
         MOA_CUDA(cudaStreamWaitEvent(stream_, mdone_[m], 0));
@@ -391,6 +486,20 @@ void GpuEngine::step() {
       host_api_ms_ += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_api).count();
     }
   overlapped_ticks_ += fan_out;
+  // the first K - 1 ticks of a decode run: no event, no timing
+  for (int j = 0; j + 1 < K; ++j) {
+    for (Plan& p : plan) p.r->n_out += 1;
+    if (opt_.time_ticks) {
+      if (static_cast<int>(tick_ev_.size()) <= tick_) {
+        cudaEvent_t e;
+        MOA_CUDA(cudaEventCreate(&e));
+        tick_ev_.push_back(e);
+        tick_timed_.push_back(0);
+      }
+      tick_timed_[static_cast<std::size_t>(tick_)] = 0;
+    }
+    tick_ += 1;
+  }
   // state update
   for (Plan& p : plan) {
     Req& r = *p.r;
@@ -509,6 +618,14 @@ void GpuEngine::step() {
 }
 
 void GpuEngine::run(int max_ticks) {
+  // decode runs only here: the caller regains control only through event
+  // callbacks, which end a run.  step() alone keeps one tick per call (the
+  // protocol lets a caller cancel / reclaim between any two ticks).
+  struct RunsOn {
+    bool& f;
+    explicit RunsOn(bool& x) : f(x) { f = true; }
+    ~RunsOn() { f = false; }
+  } runs_on(in_run_);
   while (busy()) {
     step();
     if (tick_ > max_ticks) throw RunError("engine: tick limit exceeded");

@@ -173,6 +173,8 @@ class GpuEngine {
   void start_decode(Req& r, int n_out);
   void upload_and_forward(int m, const std::vector<k::RowDesc>& rows, const std::vector<int>& lsel,
                           const std::vector<int>& lout, cudaStream_t st);
+  void upload_and_forward_run(int m, int K, const std::vector<k::RowDesc>& rows, const std::vector<int>& lout,
+                              cudaStream_t st);
 
   EngineOptions opt_;
   std::unique_ptr<PeerComm> comm_;
@@ -186,6 +188,10 @@ class GpuEngine {
   std::vector<cudaStream_t> cstreams_;
   std::vector<cudaEvent_t> blob_free_, blob_ready_;  // [model][2]
   bool async_upload_ = true;
+  std::vector<cudaEvent_t> run_free_, run_ready_;  // [model][2] decode-run blobs
+  std::vector<int> run_par_;
+  int max_run_ = DeviceModel::kMaxRun;  // MOA_DECODE_RUN=K (1: off)
+  bool in_run_ = false;                 // inside run(): decode runs allowed
   bool overlap_models_ = true;
   bool tracing_ = false;
   std::map<int, int> embed_kv_;  // model -> reserved KV slot of the hidden-state provider

@@ -139,6 +139,8 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   blob_bytes_ = (buf_.sel_bytes + sizeof(k::RowDesc) * static_cast<std::size_t>(max_rows) + 255) / 256 * 256;
   MOA_CUDA(cudaMalloc(&meta_blob_, 2 * blob_bytes_));
   use_blob(0);
+  run_stride_ = (buf_.sel_bytes + sizeof(k::RowDesc) * static_cast<std::size_t>(max_logit_rows) + 255) / 256 * 256;
+  MOA_CUDA(cudaMalloc(&run_area_, 2 * kMaxRun * run_stride_));
   dev_alloc(&hn_, static_cast<long long>(max_rows) * D);
   // TMA descriptors for the tensor-core prefill path (weights: 128-row boxes)
   tc_ok_ = k::gemm_tc_supported(s.qkv_cols(), D) && k::gemm_tc_supported(D, s.n_heads * s.head_dim) &&
@@ -282,7 +284,7 @@ DeviceModel::~DeviceModel() {
                     static_cast<void*>(kpool_), static_cast<void*>(vpool_), static_cast<void*>(x_),
                     static_cast<void*>(h_), static_cast<void*>(q_), static_cast<void*>(attn_ws_),
                     static_cast<void*>(attn_cnt_), static_cast<void*>(part_), static_cast<void*>(lm_cnt_),
-                    meta_blob_, static_cast<void*>(hn_),
+                    meta_blob_, run_area_, static_cast<void*>(hn_),
                     static_cast<void*>(gv_ws_), static_cast<void*>(gv_cnt_), static_cast<void*>(ssq_), mk_maps_, static_cast<void*>(mk_ssq_),
                     static_cast<void*>(mk_ws_), static_cast<void*>(mk_cnt_), static_cast<void*>(mk_attn_ws_),
                     static_cast<void*>(mk_attn_cnt_), static_cast<void*>(mk_lm_part_), static_cast<void*>(mk_lm_cnt_),
@@ -350,6 +352,37 @@ void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int*
     MOA_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st, distinct);
     MOA_CUDA(cudaStreamEndCapture(st, &g));
+    cudaGraphExec_t exec = nullptr;
+    MOA_CUDA(cudaGraphInstantiate(&exec, g, 0));
+    MOA_CUDA(cudaGraphDestroy(g));
+    it = graphs_.emplace(key, exec).first;
+  }
+  MOA_CUDA(cudaGraphLaunch(it->second, st));
+}
+
+void DeviceModel::forward_run(int K, int R, int max_pos, const int* out_tok_read, int* out_tok, float* out_lp,
+                              float* out_ent, cudaStream_t st, int parity) {
+  if (K < 2 || K > kMaxRun || !runs_supported()) throw RunError("model " + spec_.tag + ": invalid decode run");
+  if (R <= 0 || R > max_lrows_ || R > k::kLmMaxRows) throw RunError("model " + spec_.tag + ": run rows exceed workspace");
+  if (max_pos >= max_ctx_) throw RunError("model " + spec_.tag + ": position exceeds max_ctx");
+  const int rcap = std::min(pow2_at_least(R, 8), max_rows_);
+  const int ks = k::kv_split(spec_.head_dim);
+  const int nsplit = pow2_at_least((max_pos + ks) / ks, 1);  // the last tick's: a cap for the earlier ones
+  const auto key = std::make_tuple(rcap, nsplit, 1 | (use_tc_ ? 2 : 0) | (use_mk_ ? 4 : 0) | 8 | (parity << 4),
+                                   2 * K);
+  auto it = graphs_.find(key);
+  if (it == graphs_.end()) {
+    const int keep = blob_;
+    cudaGraph_t g = nullptr;
+    MOA_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    for (int j = 0; j < K; ++j) {
+      char* base = static_cast<char*>(run_blob(parity)) + j * run_stride_;
+      buf_.sel = reinterpret_cast<int*>(base);
+      buf_.rows = reinterpret_cast<k::RowDesc*>(base + buf_.sel_bytes);
+      launch(rcap, nsplit, true, out_tok_read, out_tok, out_lp, out_ent, nullptr, st, true);
+    }
+    MOA_CUDA(cudaStreamEndCapture(st, &g));
+    use_blob(keep);
     cudaGraphExec_t exec = nullptr;
     MOA_CUDA(cudaGraphInstantiate(&exec, g, 0));
     MOA_CUDA(cudaGraphDestroy(g));

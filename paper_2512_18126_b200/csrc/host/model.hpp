@@ -99,6 +99,13 @@ class DeviceModel {
   // current tick's graph reads the other (graphs are keyed by the blob).
   void use_blob(int b);
   int blob() const { return blob_; }
+  // Decode runs: K consecutive pure-decode ticks launched as one graph, each
+  // tick reading its own compact metadata blob (run area [2][kMaxRun][stride],
+  // rows <= max_logit_rows).  run_blob(p) = device base of parity p.
+  static constexpr int kMaxRun = 8;
+  std::size_t run_stride() const { return run_stride_; }
+  void* run_blob(int parity) const { return static_cast<char*>(run_area_) + parity * kMaxRun * run_stride_; }
+  bool runs_supported() const { return use_graphs_ && !probes_; }
   const float* residual() const { return x_; }  // final residual rows of the last forward
 
   // R rows / Rl logits rows already resident in buffers(); out_* are the
@@ -106,6 +113,10 @@ class DeviceModel {
   // distinct: every row belongs to a different agent (a pure decode tick)
   void forward(int R, int Rl, int max_pos, long long keys, const int* out_tok_read, int* out_tok, float* out_lp,
                float* out_ent, float* logits, cudaStream_t st, bool distinct = false);
+  // K ticks of R decode rows each (every row its own agent, one logits row per
+  // row), metadata already in run_blob(parity); max_pos of the last tick.
+  void forward_run(int K, int R, int max_pos, const int* out_tok_read, int* out_tok, float* out_lp, float* out_ent,
+                   cudaStream_t st, int parity);
 
   // Algorithmic bytes one forward must move for weights (every tick reads the
   // full weight set once) -- the roofline basis.
@@ -187,6 +198,8 @@ class DeviceModel {
   int* lm_cnt_ = nullptr;
   ForwardBuffers buf_;
   void* meta_blob_ = nullptr;  // [2][sel_bytes + rows]
+  void* run_area_ = nullptr;   // [2][kMaxRun][run_stride_]
+  std::size_t run_stride_ = 0;
   std::size_t blob_bytes_ = 0;
   int blob_ = 0;
 };
