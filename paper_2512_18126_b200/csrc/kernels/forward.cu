@@ -622,14 +622,16 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
       vv[jj] = j0 + jj < ke ? __ldg(reinterpret_cast<const VT*>(V + static_cast<long long>(j0 + jj) * HD + lane * E)) : VT{};
 #pragma unroll
     for (int h = 0; h < HPG; ++h) {
-      float d = 0.f;
+      float dv[8];  // one partial per 16-byte chunk: 8 short FMA chains instead of one of 64
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         float f[8];
         unpack8(kk[v], f);
+        dv[v] = 0.f;
 #pragma unroll
-        for (int t = 0; t < 8; ++t) d = fmaf(qs[h][part * 64 + v * 8 + t], f[t], d);
+        for (int t = 0; t < 8; ++t) dv[v] = fmaf(qs[h][part * 64 + v * 8 + t], f[t], dv[v]);
       }
+      float d = ((dv[0] + dv[1]) + (dv[2] + dv[3])) + ((dv[4] + dv[5]) + (dv[6] + dv[7]));
       if constexpr (TPK == 2) d += __shfl_xor_sync(kFull, d, 1);
       const float sc = j < ke ? d * scale : -INFINITY;
       float cmax = sc;
@@ -963,15 +965,17 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
 #pragma unroll
     for (int h = 0; h < HPG; ++h) {
       if (h >= hpg) break;
-      float d = 0.f;
+      float dv[8];  // one partial per 16-byte chunk: 8 short FMA chains instead of one of 64
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         float f[8];
         unpack8(kk[v], f);
         const float* qv = &qs[h][part * 64 + ((v + lane) & 7) * 8];
+        dv[v] = 0.f;
 #pragma unroll
-        for (int t = 0; t < 8; ++t) d = fmaf(qv[t], f[t], d);
+        for (int t = 0; t < 8; ++t) dv[v] = fmaf(qv[t], f[t], dv[v]);
       }
+      float d = ((dv[0] + dv[1]) + (dv[2] + dv[3])) + ((dv[4] + dv[5]) + (dv[6] + dv[7]));
       if constexpr (TPK == 2) d += __shfl_xor_sync(kFull, d, 1);
       const float sc = j < n ? d * scale : -INFINITY;
       float cmax = sc;

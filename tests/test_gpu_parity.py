@@ -224,6 +224,29 @@ def test_long_context_decode_matches_oracle():
     eng.close()
 
 
+@pytest.mark.parametrize("cfg", [C1, C1U])
+def test_decode_runs_match_tick_by_tick(cfg):
+    """Decode runs (up to 8 pure-decode ticks launched as one graph) replay the
+    same per-tick forwards: tokens, logprobs, the schedule and every early-exit
+    decision are bit-identical to tick-by-tick launches."""
+    outs = []
+    for run in ("8", "1"):
+        os.environ["MOA_DECODE_RUN"] = run
+        try:
+            eng, qc = capi.engine_for(cfg)
+        finally:
+            del os.environ["MOA_DECODE_RUN"]
+        outs.append(eng.run_query(qc, sample=3))
+        eng.close()
+    a, b = outs
+    assert a["ticks"] == b["ticks"] and a["tokens"] == b["tokens"]
+    for name, ga in a["agents"].items():
+        gb = b["agents"][name]
+        assert ga["output"] == gb["output"] and ga["logprobs"] == gb["logprobs"], name
+        assert (ga["decode_start"], ga["decode_end"], ga["pruned"]) == (gb["decode_start"], gb["decode_end"], gb["pruned"])
+    assert [(e["tick"], e["q"], e["exited"]) for e in a["metricq"]] == [(e["tick"], e["q"], e["exited"]) for e in b["metricq"]]
+
+
 def test_incremental_prefill_equals_one_shot():
     """Appending the prompt in contiguous pieces (prefill_only) gives the same
     KV and tokens as one generate (zero recompute, pdsim.cpp:155-174)."""
