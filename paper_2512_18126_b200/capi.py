@@ -147,6 +147,8 @@ _SIGS = {
     "moa_slotplan_event": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_int32), C.c_int, _P(C.c_int32), C.c_int,
                             _P(C.c_int)], C.c_int),
     "moa_slotplan_free": ([C.c_void_p], C.c_int),
+    "moa_k_attention": ([C.c_size_t, C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_size_t,
+                         C.c_size_t, C.c_longlong, C.c_int, C.c_size_t, C.c_int, C.c_size_t], C.c_int),
     "moa_k_gemv": ([C.c_size_t, C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_size_t], C.c_int),
     "moa_k_gemm_tc": ([C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_size_t], C.c_int),
     "moa_k_gemv_tc": ([C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_size_t], C.c_int),

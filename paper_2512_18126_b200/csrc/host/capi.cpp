@@ -727,6 +727,36 @@ int moa_slotplan_free(moa_slotplan* p) {
   return guard([&] { delete p; });
 }
 
+int moa_k_attention(uintptr_t q, uintptr_t rows, int R, uintptr_t meta, int nh, int nkv, int hd, uintptr_t kpool,
+                    uintptr_t vpool, long long kv_stride, int max_ctx, uintptr_t out, int prefill, uintptr_t stream) {
+  return guard([&] {
+    if ((hd != 64 && hd != 128) || nh % nkv || R <= 0) throw moa::ValidationError("attention: unsupported shape");
+    const auto st = reinterpret_cast<cudaStream_t>(stream);
+    const auto* qp = reinterpret_cast<const moa::k::bf16*>(q);
+    const auto* rp = reinterpret_cast<const moa::k::RowDesc*>(rows);
+    const auto* mp = reinterpret_cast<const int*>(meta);
+    const auto* kp = reinterpret_cast<const moa::k::bf16*>(kpool);
+    const auto* vp = reinterpret_cast<const moa::k::bf16*>(vpool);
+    auto* op = reinterpret_cast<moa::k::bf16*>(out);
+    if (prefill) moa::k::attention_prefill(qp, rp, R, mp, nh, nkv, hd, kp, vp, kv_stride, 0, max_ctx, op, st);
+    {  // prefill: the per-row kernel takes the rows alone in their run
+      float* ws = nullptr;
+      int* cnt = nullptr;
+      MOA_CUDA(cudaMalloc(&ws, sizeof(float) * moa::k::attention_ws_floats(R, nh, hd, max_ctx)));
+      MOA_CUDA(cudaMalloc(&cnt, sizeof(int) * R * nh));
+      MOA_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * R * nh, st));
+      const int ks = moa::k::kv_split(hd);
+      int ns = 1;
+      while (ns * ks < max_ctx) ns <<= 1;
+      moa::k::attention(qp, rp, R, ns, mp, nh, nkv, hd, kp, vp, kv_stride, 0, max_ctx, op, ws, cnt, st, prefill != 0);
+      MOA_CUDA(cudaStreamSynchronize(st));
+      cudaFree(ws);
+      cudaFree(cnt);
+    }
+    MOA_CUDA(cudaGetLastError());
+  });
+}
+
 int moa_k_gemv(uintptr_t A, uintptr_t X, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream) {
   return guard([&] {
     if (K % 256) throw moa::ValidationError("gemv: K must be a multiple of 256");

@@ -273,12 +273,18 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   int max_pos = 0;
   long long keys = 0;
   bool distinct = rows.size() <= 64;  // every row a different agent (pure decode)?
+  int runs = 0;                        // maximal same-agent runs of consecutive positions
   for (std::size_t i = 0; i < rows.size(); ++i) {
     const auto& rd = rows[i];
     max_pos = std::max(max_pos, rd.pos);
     keys += rd.pos + 1;
     for (std::size_t j = 0; j < i && distinct; ++j) distinct = rows[j].kv != rd.kv;
+    runs += i == 0 || rows[i - 1].kv != rd.kv || rows[i - 1].pos + 1 != rd.pos;
   }
+  // prompt-prefill tick: long same-agent runs -> tiled prefill attention (below
+  // ~512 rows the per-row kernel's CTA count wins: measured on C1's
+  // aggregator chunk ticks)
+  const bool prefill = rows.size() >= 512 && static_cast<std::size_t>(runs) * 64 <= rows.size();
   // [lsel (L)][lout (L)][meta: R, Rl, max_pos] -- the graph's kernels read meta
   int* sel = reinterpret_cast<int*>(s.host);
   std::memcpy(sel, lsel.data(), sizeof(int) * lsel.size());
@@ -305,7 +311,7 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   }
   float* logits = (opt_.keep_logits && !lsel.empty()) ? logits_scratch_ : nullptr;
   dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), max_pos, keys, out_tok_, out_tok_,
-             out_lp_, out_ent_, logits, st, distinct);
+             out_lp_, out_ent_, logits, st, distinct, prefill);
   if (logits) {  // debug path: scatter each logits row to its (slot, k) home
     const long long V = dm.spec().vocab;
     for (std::size_t i = 0; i < lsel.size(); ++i)

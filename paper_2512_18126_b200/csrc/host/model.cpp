@@ -166,6 +166,7 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   dev_alloc(&gv_cnt_, (std::max({s.qkv_cols(), 2 * s.ffn, s.d}) + 127) / 128);
   qkv_attn_ok_ = k::qkv_attention_supported(D, s.n_heads, s.n_kv_heads, static_cast<int>(hd));
   if (const char* e = std::getenv("MOA_QKV_ATTN")) use_qkv_attn_ = std::string(e) != "0";
+  if (const char* e = std::getenv("MOA_PREFILL_ATTN")) use_prefill_attn_ = std::string(e) != "0";
   // RMSNorm folded into the decode GEMVs: ssq partials [16 rows][d/16]
   dev_alloc(&ssq_, static_cast<long long>(k::kGemvTcRows) * (D / 16));
   {
@@ -328,7 +329,10 @@ int pow2_at_least(int v, int lo) {
 }  // namespace
 
 void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int* out_tok_read, int* out_tok,
-                          float* out_lp, float* out_ent, float* logits, cudaStream_t st, bool distinct) {
+                          float* out_lp, float* out_ent, float* logits, cudaStream_t st, bool distinct, bool prefill) {
+  // (tensor-core ticks only: the GEMV-only path keeps every row's attention in
+  // one kernel, so its tokens stay bit-identical across schedule modes)
+  prefill = prefill && use_prefill_attn_ && use_tc_;
   if (R <= 0) return;
   if (R > max_rows_) throw RunError("model " + spec_.tag + ": tick rows exceed workspace");
   if (Rl > max_lrows_ || Rl > k::kLmMaxRows) throw RunError("model " + spec_.tag + ": logits rows exceed workspace");
@@ -341,16 +345,17 @@ void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int*
     live_R_ = R;
     live_Rl_ = Rl;
     live_keys_ = keys;
-    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st, distinct);
+    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st, distinct, prefill);
     return;
   }
   const auto key = std::make_tuple(rcap, nsplit, (Rl > 0 ? 1 : 0) | (use_tc_ ? 2 : 0) | (use_mk_ ? 4 : 0) |
-                                                     (distinct ? 8 : 0) | (blob_ << 4), logits ? 1 : 0);
+                                                     (distinct ? 8 : 0) | (blob_ << 4) | (prefill ? 32 : 0),
+                                   logits ? 1 : 0);
   auto it = graphs_.find(key);
   if (it == graphs_.end()) {
     cudaGraph_t g = nullptr;
     MOA_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st, distinct);
+    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st, distinct, prefill);
     MOA_CUDA(cudaStreamEndCapture(st, &g));
     cudaGraphExec_t exec = nullptr;
     MOA_CUDA(cudaGraphInstantiate(&exec, g, 0));
@@ -392,7 +397,7 @@ void DeviceModel::forward_run(int K, int R, int max_pos, const int* out_tok_read
 }
 
 void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_tok_read, int* out_tok,
-                         float* out_lp, float* out_ent, float* logits, cudaStream_t st, bool distinct) {
+                         float* out_lp, float* out_ent, float* logits, cudaStream_t st, bool distinct, bool prefill) {
   const ModelSpec& s = spec_;
   const int D = s.d, hd = s.head_dim, nh = s.n_heads, nkv = s.n_kv_heads;
   const float eps = static_cast<float>(s.norm_eps);
@@ -490,8 +495,12 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     run_gemm(qkv, nullptr, nullptr, wmaps_[static_cast<std::size_t>(l)].wqkv);
     probe_end();
     probe_begin(KernelProbes::Attention, 4.0 * live_keys_ * nkv * hd + 4.0 * live_R_ * nh * hd);
+    // prompt-prefill ticks: runs of a prompt by the tiled kernel, the tick's
+    // decode rows (alone in their run) by the per-row kernel
+    if (prefill)
+      k::attention_prefill(q_, buf_.rows, rcap, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_, st);
     k::attention(q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_,
-                 attn_ws_, attn_cnt_, st);
+                 attn_ws_, attn_cnt_, st, prefill);
     probe_end();
     }
     // x += o . Wo^T

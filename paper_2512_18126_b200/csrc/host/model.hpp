@@ -111,8 +111,9 @@ class DeviceModel {
   // R rows / Rl logits rows already resident in buffers(); out_* are the
   // engine's flat per-agent output arrays; logits (optional) [Rl][V] fp32.
   // distinct: every row belongs to a different agent (a pure decode tick)
+  // prefill: the rows are long same-agent runs (prompt prefill): tiled attention
   void forward(int R, int Rl, int max_pos, long long keys, const int* out_tok_read, int* out_tok, float* out_lp,
-               float* out_ent, float* logits, cudaStream_t st, bool distinct = false);
+               float* out_ent, float* logits, cudaStream_t st, bool distinct = false, bool prefill = false);
   // K ticks of R decode rows each (every row its own agent, one logits row per
   // row), metadata already in run_blob(parity); max_pos of the last tick.
   void forward_run(int K, int R, int max_pos, const int* out_tok_read, int* out_tok, float* out_lp, float* out_ent,
@@ -125,8 +126,9 @@ class DeviceModel {
 
  private:
   void launch(int rcap, int nsplit, bool with_logits, const int* out_tok_read, int* out_tok, float* out_lp,
-              float* out_ent, float* logits, cudaStream_t st, bool distinct);
+              float* out_ent, float* logits, cudaStream_t st, bool distinct, bool prefill = false);
   bool qkv_attn_ok_ = false, use_qkv_attn_ = true;  // fused QKV + attention for small-agent decode ticks
+  bool use_prefill_attn_ = true;  // tiled prefill attention for prompt-prefill ticks (MOA_PREFILL_ATTN)
   std::map<std::tuple<int, int, int, int>, cudaGraphExec_t> graphs_;
   ModelSpec spec_;
   int max_agents_, max_ctx_, max_rows_, max_lrows_;

@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(256, 1)
 attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, const int* __restrict__ meta, int nh,
                      int nkv, const bf16* __restrict__ kpool, const bf16* __restrict__ vpool, long long kv_stride,
                      long long layer_off, int max_ctx, bf16* __restrict__ o, float* __restrict__ ws,
-                     int* __restrict__ cnt, int nsplit_max, int split_keys) {
+                     int* __restrict__ cnt, int nsplit_max, int split_keys, int skip_runs) {
   constexpr int NW = 8, E = HD / 32;
   __shared__ float qs[HPG][HD];
   __shared__ float wm[NW][HPG], wl[NW][HPG];
@@ -574,8 +574,14 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
   const int h0 = g * (nh / nkv) + (blockIdx.y % cpg) * HPG;  // first q head
   // Tick metadata and the keys of earlier ticks are not produced by this
   // forward's previous kernel: read / prefetch them before the PDL wait.
-  if (r >= __ldg(meta)) return;
+  const int live = __ldg(meta);
+  if (r >= live) return;
   const RowDesc rd = rows[r];
+  if (skip_runs) {  // rows inside same-agent runs belong to attention_prefill
+    if ((r > 0 && rows[r - 1].kv == rd.kv && rows[r - 1].pos + 1 == rd.pos) ||
+        (r + 1 < live && rows[r + 1].kv == rd.kv && rows[r + 1].pos == rd.pos + 1))
+      return;
+  }
   const int n = rd.pos + 1;
   const int nsplit = (n + split_keys - 1) / split_keys;
   if (s >= nsplit) return;
@@ -760,6 +766,172 @@ attention_gqa_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ row
   }
 }
 
+
+// Prefill attention: CTA = (64 consecutive rows of the tick, q head), 8 warps
+// x 8 rows.  The rows of one agent's prefill job are consecutive with
+// increasing positions, so the block's rows split into a few same-agent
+// segments; for each, the segment's keys stream through smem in blocks of
+// 64 (K transposed, fp32) shared by every row of the segment, each warp runs
+// an online softmax for its rows (lane = 2 keys for the scores, lane = HD/32
+// output dims for P.V) with the causal mask pos(key) <= pos(row).  Replaces
+// one CTA per (row, kv head) re-reading the whole context from L2 for every
+// row of a long prompt.
+constexpr int kPfRows = 64, kPfKeys = 64;
+template <int HD>
+__global__ void __launch_bounds__(256, 1)
+attention_prefill_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, const int* __restrict__ meta,
+                         int nh, int nkv, const bf16* __restrict__ kpool, const bf16* __restrict__ vpool,
+                         long long kv_stride, long long layer_off, int max_ctx, bf16* __restrict__ o) {
+  constexpr int E = HD / 32, KS = kPfKeys + 1;  // Kt row stride (fp32): conflict-free transposed stores
+  extern __shared__ __align__(16) float pf_sm[];
+  float* Kt = pf_sm;                       // [HD][KS]
+  float* Vs = Kt + HD * KS;                // [64][HD]
+  float* Qs = Vs + kPfKeys * HD;           // [8 warps][8 rows][HD]
+  float* Ps = Qs + 8 * 8 * HD;             // [8 warps][64 keys][8 rows]
+  __shared__ int seg_s[kPfRows + 1], seg_end_s[kPfRows];
+  __shared__ int nseg_s;
+  __shared__ RowDesc rd_s[kPfRows];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b0 = blockIdx.x * kPfRows, h = blockIdx.y;
+  const int live = __ldg(meta);
+  if (b0 >= live) return;
+  const int nb = min(kPfRows, live - b0);
+  const int g = h / (nh / nkv);
+  if (threadIdx.x < nb) rd_s[threadIdx.x] = rows[b0 + threadIdx.x];  // tick metadata (not the previous kernel's)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // same-agent runs of consecutive positions; a row alone in its run (a
+    // decode row) is left to the per-row kernel (attention(..., skip_runs))
+    int n = 0;
+    for (int i = 0; i < nb; ++i)
+      if (i == 0 || rd_s[i].kv != rd_s[i - 1].kv || rd_s[i].pos != rd_s[i - 1].pos + 1) seg_s[n++] = i;
+    seg_s[n] = nb;
+    int m = 0;
+    for (int k = 0; k < n; ++k) {
+      const int a = seg_s[k], b = seg_s[k + 1];
+      const bool single = b - a == 1 && !(a == 0 && b0 > 0 && rows[b0 - 1].kv == rd_s[0].kv &&
+                                            rows[b0 - 1].pos + 1 == rd_s[0].pos) &&
+                          !(b == nb && b0 + nb < live && rows[b0 + nb].kv == rd_s[nb - 1].kv &&
+                            rows[b0 + nb].pos == rd_s[nb - 1].pos + 1);
+      if (!single) {
+        seg_s[m] = a;
+        seg_end_s[m] = b;
+        ++m;
+      }
+    }
+    nseg_s = m;
+  }
+  MOA_PDL_ENTRY();
+  __syncthreads();
+  const float scale = rsqrtf(static_cast<float>(HD));
+  float* qs = Qs + warp * 8 * HD;
+  float* ps = Ps + warp * kPfKeys * 8;
+  for (int sg = 0; sg < nseg_s; ++sg) {
+    const int a = seg_s[sg], b = seg_end_s[sg];
+    const RowDesc first = rd_s[a];
+    const int maxpos = rd_s[b - 1].pos;
+    const bf16* K = kpool + first.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
+    const bf16* V = vpool + first.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
+    // this warp's rows of the segment: block rows [warp*8, warp*8+8) within [a, b)
+    const int r_lo = max(a, warp * 8), r_hi = min(b, warp * 8 + 8);
+    const bool active = r_lo < r_hi;
+    int pos[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) pos[r] = (warp * 8 + r >= r_lo && warp * 8 + r < r_hi) ? rd_s[warp * 8 + r].pos : -1;
+    if (active)
+      for (int i = lane; i < 8 * HD; i += 32) {
+        const int r = i / HD, d = i % HD;
+        qs[i] = pos[r] >= 0 ? __bfloat162float(q[(static_cast<long long>(b0 + warp * 8 + r) * nh + h) * HD + d]) : 0.f;
+      }
+    float m[8], l[8], acc[8][E];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      m[r] = -INFINITY;
+      l[r] = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[r][e] = 0.f;
+    }
+    for (int kb = 0; kb <= maxpos; kb += kPfKeys) {
+      __syncthreads();  // the previous key block is consumed
+      for (int c = threadIdx.x; c < kPfKeys * (HD / 8); c += 256) {
+        const int key = c / (HD / 8), d0 = (c % (HD / 8)) * 8;
+        float kf[8], vf[8];
+        if (kb + key <= maxpos) {
+          unpack8(__ldcg(reinterpret_cast<const uint4*>(K + static_cast<long long>(kb + key) * HD + d0)), kf);
+          unpack8(__ldcg(reinterpret_cast<const uint4*>(V + static_cast<long long>(kb + key) * HD + d0)), vf);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) kf[i] = vf[i] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) Kt[(d0 + i) * KS + key] = kf[i];
+        *reinterpret_cast<float4*>(Vs + key * HD + d0) = make_float4(vf[0], vf[1], vf[2], vf[3]);
+        *reinterpret_cast<float4*>(Vs + key * HD + d0 + 4) = make_float4(vf[4], vf[5], vf[6], vf[7]);
+      }
+      __syncthreads();
+      if (!active) continue;
+      float s0[8], s1[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) s0[r] = s1[r] = 0.f;
+      for (int d = 0; d < HD; d += 4) {
+        float k0[4], k1[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          k0[i] = Kt[(d + i) * KS + lane];
+          k1[i] = Kt[(d + i) * KS + lane + 32];
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const float4 qv = *reinterpret_cast<const float4*>(qs + r * HD + d);
+          s0[r] = fmaf(qv.x, k0[0], fmaf(qv.y, k0[1], fmaf(qv.z, k0[2], fmaf(qv.w, k0[3], s0[r]))));
+          s1[r] = fmaf(qv.x, k1[0], fmaf(qv.y, k1[1], fmaf(qv.z, k1[2], fmaf(qv.w, k1[3], s1[r]))));
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const bool ok0 = kb + lane <= pos[r], ok1 = kb + lane + 32 <= pos[r];
+        const float a0 = ok0 ? s0[r] * scale : -INFINITY, a1 = ok1 ? s1[r] * scale : -INFINITY;
+        float bm = fmaxf(a0, a1);
+#pragma unroll
+        for (int off = 16; off; off >>= 1) bm = fmaxf(bm, __shfl_xor_sync(kFull, bm, off));
+        const float mn = fmaxf(m[r], bm);
+        const float corr = (m[r] == -INFINITY) ? 0.f : __expf(m[r] - mn);
+        const float p0 = ok0 ? __expf(a0 - mn) : 0.f, p1 = ok1 ? __expf(a1 - mn) : 0.f;
+        if (mn != -INFINITY) {  // rows with no key in this block keep their state
+          l[r] = l[r] * corr + warp_sum(p0 + p1);
+#pragma unroll
+          for (int e = 0; e < E; ++e) acc[r][e] *= corr;
+          m[r] = mn;
+        }
+        ps[lane * 8 + r] = p0;
+        ps[(lane + 32) * 8 + r] = p1;
+      }
+      __syncwarp();
+      for (int k = 0; k < kPfKeys && kb + k <= maxpos; ++k) {
+        const float4 pa = *reinterpret_cast<const float4*>(ps + k * 8);
+        const float4 pb = *reinterpret_cast<const float4*>(ps + k * 8 + 4);
+        const float pk[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const float v = Vs[k * HD + lane + 32 * e];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) acc[r][e] = fmaf(pk[r], v, acc[r][e]);
+        }
+      }
+      __syncwarp();
+    }
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        if (pos[r] < 0) continue;
+        const float inv = 1.0f / l[r];
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          o[(static_cast<long long>(b0 + warp * 8 + r) * nh + h) * HD + lane + 32 * e] = __float2bfloat16_rn(acc[r][e] * inv);
+      }
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Decode-tick QKV + attention in one kernel for small agents (every row is
@@ -1216,7 +1388,7 @@ long long attention_ws_floats(int R, int nh, int hd, int max_ctx) {
 
 void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, const int* meta, int nh, int nkv, int hd,
                const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx, bf16* o,
-               float* ws, int* cnt, cudaStream_t st) {
+               float* ws, int* cnt, cudaStream_t st, bool skip_runs) {
   if (R_cap <= 0) return;
   const int nsplit_max = (max_ctx + kKvSplit - 1) / kKvSplit;
   const int split_keys = kv_split(hd);
@@ -1233,7 +1405,7 @@ void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, co
   dim3 grid(R_cap, nh / hpc, nsplit_cap);
   auto go = [&](auto kern) {
     launch_pdl(kern, grid, dim3(256), st, q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx, o, ws,
-               cnt, nsplit_max, split_keys);
+               cnt, nsplit_max, split_keys, skip_runs ? 1 : 0);
   };
   if (hd == 64) {
     if (hpc == 1) go(attention_gqa_kernel<64, 1>);
@@ -1249,6 +1421,34 @@ void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, co
 }
 
 MOA_CHAIN_STAMP_SETTER(forward_chain_stamp)
+
+void attention_prefill(const bf16* q, const RowDesc* rows, int R_cap, const int* meta, int nh, int nkv, int hd,
+                       const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx,
+                       bf16* o, cudaStream_t st) {
+  const int smem = (hd * (kPfKeys + 1) + kPfKeys * hd + 8 * 8 * hd + 8 * kPfKeys * 8) * 4;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((R_cap + kPfRows - 1) / kPfRows, nh);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  auto go = [&](auto kern) {
+    static std::set<const void*> attr;
+    if (attr.insert(reinterpret_cast<const void*>(kern)).second) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      uniform_carveout(reinterpret_cast<const void*>(kern));
+    }
+    cudaLaunchKernelEx(&cfg, kern, q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx, o);
+  };
+  if (hd == 64)
+    go(attention_prefill_kernel<64>);
+  else
+    go(attention_prefill_kernel<128>);
+}
 
 int qkv_attention_smem(int D, int nh, int nkv, int hd) { return ((nh / nkv) + 2) * hd * D * 2 + D * 2 + D * 4 + 128; }
 // earlier keys one CTA stages in smem next to its weight slab (<= 200 KB of

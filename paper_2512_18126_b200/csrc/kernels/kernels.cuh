@@ -253,9 +253,18 @@ inline int kv_split(int hd) {
   return env ? env : (hd == 64 ? 1024 : 512);
 }
 long long attention_ws_floats(int R, int nh, int hd, int max_ctx);
+// skip_runs: leave rows inside same-agent runs of consecutive positions to
+// attention_prefill (which skips the rows alone in their run).
 void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, const int* meta, int nh, int nkv,
                int hd, const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx,
-               bf16* o, float* ws, int* cnt, cudaStream_t st);
+               bf16* o, float* ws, int* cnt, cudaStream_t st, bool skip_runs = false);
+
+// Prefill ticks (rows of long same-agent runs): CTA = 64 consecutive rows x q
+// head, keys streamed through smem once per same-agent segment; rows alone in
+// their run are skipped (pair with attention(..., skip_runs = true)).  hd 64 / 128.
+void attention_prefill(const bf16* q, const RowDesc* rows, int R_cap, const int* meta, int nh, int nkv, int hd,
+                       const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx,
+                       bf16* o, cudaStream_t st);
 
 // Decode ticks of small agents (every row the only row of its agent):
 // RMSNorm + QKV + RoPE + KV append + attention in one launch, CTA = (row, kv

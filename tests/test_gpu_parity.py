@@ -173,6 +173,41 @@ def _cpu_model(tag, shape, seed):
     return _MODELS[key]
 
 
+@pytest.mark.parametrize("nh,nkv,hd", [(4, 4, 64), (32, 8, 64), (8, 2, 128)])
+def test_attention_kernels_match_torch(torch_cuda, nh, nkv, hd):
+    """Both attention kernels (tiled prefill, per-row GQA) against fp32 torch on
+    a tick mixing two prompt runs (one starting mid-context), a one-row
+    segment and a position break inside one agent's rows."""
+    torch = torch_cuda
+    g = torch.Generator(device="cpu").manual_seed(7 + nh + hd)
+    max_ctx, slots = 512, 4
+    kv_stride = nkv * max_ctx * hd
+    kpool = (torch.randn(slots * kv_stride, generator=g) * 0.5).to(torch.bfloat16).cuda()
+    vpool = torch.randn(slots * kv_stride, generator=g).to(torch.bfloat16).cuda()
+    rows = [(0, p) for p in range(100, 230)] + [(1, p) for p in range(0, 70)] + [(2, 300)] + \
+           [(3, p) for p in range(10, 20)] + [(3, p) for p in range(40, 45)]
+    R = len(rows)
+    q = torch.randn(R, nh, hd, generator=g).to(torch.bfloat16).cuda()
+    rd = torch.tensor([[kv, pos, 0, 0] for kv, pos in rows], dtype=torch.int32).cuda()
+    meta = torch.tensor([R, 0, max(p for _, p in rows)], dtype=torch.int32).cuda()
+    K = kpool.float().view(slots, nkv, max_ctx, hd)
+    V = vpool.float().view(slots, nkv, max_ctx, hd)
+    ref = torch.empty(R, nh, hd, device="cuda")
+    for i, (kv, pos) in enumerate(rows):
+        for h in range(nh):
+            kh = h // (nh // nkv)
+            sc = (q[i, h].float() @ K[kv, kh, :pos + 1].T) / math.sqrt(hd)
+            ref[i, h] = torch.softmax(sc, -1) @ V[kv, kh, :pos + 1]
+    for prefill in (1, 0):
+        out = torch.zeros(R, nh, hd, dtype=torch.bfloat16, device="cuda")
+        capi.check(capi.lib().moa_k_attention(q.data_ptr(), rd.data_ptr(), R, meta.data_ptr(), nh, nkv, hd,
+                                              kpool.data_ptr(), vpool.data_ptr(), kv_stride, max_ctx, out.data_ptr(),
+                                              prefill, 0))
+        torch.cuda.synchronize()
+        err = float((out.float() - ref).abs().max())
+        assert err < 2e-2, (prefill, err)
+
+
 def test_single_agent_decode_matches_oracle():
     model = _cpu_model("leaf", "tiny", 1)
     eng = capi.Engine([capi.model_spec("leaf", "tiny", 1, max_agents=2)], max_ctx=1024, max_out=64, keep_logits=True)
