@@ -284,7 +284,11 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   // prompt-prefill tick: long same-agent runs -> tiled prefill attention (below
   // ~512 rows the per-row kernel's CTA count wins: measured on C1's
   // aggregator chunk ticks)
-  const bool prefill = rows.size() >= 512 && static_cast<std::size_t>(runs) * 64 <= rows.size();
+  static const std::size_t min_rows = [] {
+    const char* e = std::getenv("MOA_PREFILL_MIN_ROWS");
+    return static_cast<std::size_t>(e ? std::atoi(e) : 512);
+  }();
+  const bool prefill = rows.size() >= min_rows && static_cast<std::size_t>(runs) * 16 <= rows.size();
   // [lsel (L)][lout (L)][meta: R, Rl, max_pos] -- the graph's kernels read meta
   int* sel = reinterpret_cast<int*>(s.host);
   std::memcpy(sel, lsel.data(), sizeof(int) * lsel.size());

@@ -933,6 +933,225 @@ attention_prefill_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__
   }
 }
 
+// Prefill attention on the tensor cores (mma.sync m16n8k16 bf16 -> fp32,
+// FlashAttention-2 dataflow): CTA = (64 consecutive rows of the tick, q head),
+// 4 warps x 16 rows.  Same segment logic as attention_prefill_kernel (rows
+// alone in their run are left to the per-row kernel).  Per segment the Q rows
+// stay in registers as A fragments; each 64-key block of K and V is staged in
+// smem (16-byte chunks XOR-swizzled by row so ldmatrix is conflict-free);
+// S = Q.K^T per warp (8 n-tiles), causal mask by position, online softmax on
+// the accumulator fragments, P reused in registers as the A operand of P.V.
+__device__ __forceinline__ void ldsm_x4(std::uint32_t addr, std::uint32_t& r0, std::uint32_t& r1, std::uint32_t& r2,
+                                        std::uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(std::uint32_t addr, std::uint32_t& r0, std::uint32_t& r1, std::uint32_t& r2,
+                                          std::uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], std::uint32_t a0, std::uint32_t a1, std::uint32_t a2,
+                                         std::uint32_t a3, std::uint32_t b0, std::uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ std::uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const std::uint32_t*>(&v);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(128, 1)
+attention_prefill_mma_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, const int* __restrict__ meta,
+                             int nh, int nkv, const bf16* __restrict__ kpool, const bf16* __restrict__ vpool,
+                             long long kv_stride, long long layer_off, int max_ctx, bf16* __restrict__ o) {
+  constexpr int RB = HD * 2;       // smem row bytes
+  constexpr int KSTEPS = HD / 16;  // k-steps of Q.K^T
+  constexpr int NT = HD / 8;       // n-tiles of P.V
+  extern __shared__ __align__(128) unsigned char pm_sm[];
+  unsigned char* Qs = pm_sm;                 // [64][HD] bf16, swizzled
+  unsigned char* Ks = Qs + kPfRows * RB;     // [64][HD]
+  unsigned char* Vs = Ks + kPfKeys * RB;     // [64][HD]
+  __shared__ int seg_s[kPfRows + 1], seg_end_s[kPfRows];
+  __shared__ int nseg_s;
+  __shared__ RowDesc rd_s[kPfRows];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int b0 = blockIdx.x * kPfRows, h = blockIdx.y;
+  const int live = __ldg(meta);
+  if (b0 >= live) return;
+  const int nb = min(kPfRows, live - b0);
+  const int kvh = h / (nh / nkv);
+  if (threadIdx.x < nb) rd_s[threadIdx.x] = rows[b0 + threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int i = 0; i < nb; ++i)
+      if (i == 0 || rd_s[i].kv != rd_s[i - 1].kv || rd_s[i].pos != rd_s[i - 1].pos + 1) seg_s[n++] = i;
+    seg_s[n] = nb;
+    int m = 0;
+    for (int k = 0; k < n; ++k) {
+      const int a = seg_s[k], b = seg_s[k + 1];
+      const bool single = b - a == 1 && !(a == 0 && b0 > 0 && rows[b0 - 1].kv == rd_s[0].kv &&
+                                            rows[b0 - 1].pos + 1 == rd_s[0].pos) &&
+                          !(b == nb && b0 + nb < live && rows[b0 + nb].kv == rd_s[nb - 1].kv &&
+                            rows[b0 + nb].pos == rd_s[nb - 1].pos + 1);
+      if (!single) {
+        seg_s[m] = a;
+        seg_end_s[m] = b;
+        ++m;
+      }
+    }
+    nseg_s = m;
+  }
+  MOA_PDL_ENTRY();
+  // Q rows of the block -> smem (rows past the live ones: zeros)
+  for (int c = threadIdx.x; c < kPfRows * (HD / 8); c += 128) {
+    const int r = c / (HD / 8), ch = c % (HD / 8);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < nb) v = __ldcg(reinterpret_cast<const uint4*>(q + (static_cast<long long>(b0 + r) * nh + h) * HD) + ch);
+    *reinterpret_cast<uint4*>(Qs + r * RB + ((ch ^ (r & 7)) << 4)) = v;
+  }
+  __syncthreads();
+  const std::uint32_t qs_u = static_cast<std::uint32_t>(__cvta_generic_to_shared(Qs));
+  const std::uint32_t ks_u = static_cast<std::uint32_t>(__cvta_generic_to_shared(Ks));
+  const std::uint32_t vs_u = static_cast<std::uint32_t>(__cvta_generic_to_shared(Vs));
+  // A fragments of this warp's 16 rows
+  std::uint32_t qa[KSTEPS][4];
+  {
+    const int r = warp * 16 + (lane & 15);
+#pragma unroll
+    for (int kk = 0; kk < KSTEPS; ++kk) {
+      const int ch = kk * 2 + (lane >> 4);
+      ldsm_x4(qs_u + r * RB + ((ch ^ (r & 7)) << 4), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+    }
+  }
+  const float sl2 = rsqrtf(static_cast<float>(HD)) * 1.4426950408889634f;  // scale * log2(e)
+  const int ra = warp * 16 + g8, rb = ra + 8;  // block rows of this thread's two accumulator rows
+  for (int sg = 0; sg < nseg_s; ++sg) {
+    const int a = seg_s[sg], b = seg_end_s[sg];
+    const int maxpos = rd_s[b - 1].pos;
+    const int kvslot = rd_s[a].kv;
+    const bf16* K = kpool + kvslot * kv_stride + layer_off + static_cast<long long>(kvh) * max_ctx * HD;
+    const bf16* V = vpool + kvslot * kv_stride + layer_off + static_cast<long long>(kvh) * max_ctx * HD;
+    const int pa = (ra >= a && ra < b) ? rd_s[ra].pos : -1, pb = (rb >= a && rb < b) ? rd_s[rb].pos : -1;
+    const bool warp_active = warp * 16 < b && warp * 16 + 16 > a;
+    float m_a = -1e30f, m_b = -1e30f, l_a = 0.f, l_b = 0.f;
+    float oacc[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) oacc[nt][0] = oacc[nt][1] = oacc[nt][2] = oacc[nt][3] = 0.f;
+    for (int kb = 0; kb <= maxpos; kb += kPfKeys) {
+      __syncthreads();  // the previous block's K / V are consumed
+      for (int c = threadIdx.x; c < kPfKeys * (HD / 8); c += 128) {
+        const int r = c / (HD / 8), ch = c % (HD / 8);
+        uint4 kv4 = make_uint4(0, 0, 0, 0), vv4 = make_uint4(0, 0, 0, 0);
+        if (kb + r <= maxpos) {
+          kv4 = __ldcg(reinterpret_cast<const uint4*>(K + static_cast<long long>(kb + r) * HD) + ch);
+          vv4 = __ldcg(reinterpret_cast<const uint4*>(V + static_cast<long long>(kb + r) * HD) + ch);
+        }
+        *reinterpret_cast<uint4*>(Ks + r * RB + ((ch ^ (r & 7)) << 4)) = kv4;
+        *reinterpret_cast<uint4*>(Vs + r * RB + ((ch ^ (r & 7)) << 4)) = vv4;
+      }
+      __syncthreads();
+      if (!warp_active) continue;
+      // S = Q K^T: 16 rows x 64 keys (8 n-tiles of 8 keys)
+      float sacc[8][4];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < KSTEPS; ++kk) {
+#pragma unroll
+        for (int jp = 0; jp < 4; ++jp) {  // two n-tiles per ldmatrix.x4
+          const int kr = jp * 16 + (lane & 7) + ((lane >> 4) << 3);
+          const int ch = kk * 2 + ((lane >> 3) & 1);
+          std::uint32_t b00, b01, b10, b11;
+          ldsm_x4(ks_u + kr * RB + ((ch ^ (kr & 7)) << 4), b00, b01, b10, b11);
+          mma_bf16(sacc[2 * jp], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b00, b01);
+          mma_bf16(sacc[2 * jp + 1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b10, b11);
+        }
+      }
+      // causal mask + online softmax (rows ra: c0,c1; rb: c2,c3), in log2 units
+      float mx_a = -1e30f, mx_b = -1e30f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int key = kb + 8 * j + 2 * t4;
+        sacc[j][0] = key <= pa ? sacc[j][0] * sl2 : -1e30f;
+        sacc[j][1] = key + 1 <= pa ? sacc[j][1] * sl2 : -1e30f;
+        sacc[j][2] = key <= pb ? sacc[j][2] * sl2 : -1e30f;
+        sacc[j][3] = key + 1 <= pb ? sacc[j][3] * sl2 : -1e30f;
+        mx_a = fmaxf(mx_a, fmaxf(sacc[j][0], sacc[j][1]));
+        mx_b = fmaxf(mx_b, fmaxf(sacc[j][2], sacc[j][3]));
+      }
+      mx_a = fmaxf(mx_a, __shfl_xor_sync(kFull, mx_a, 1));
+      mx_a = fmaxf(mx_a, __shfl_xor_sync(kFull, mx_a, 2));
+      mx_b = fmaxf(mx_b, __shfl_xor_sync(kFull, mx_b, 1));
+      mx_b = fmaxf(mx_b, __shfl_xor_sync(kFull, mx_b, 2));
+      const float mn_a = fmaxf(m_a, mx_a), mn_b = fmaxf(m_b, mx_b);
+      const float ca = exp2f(m_a - mn_a), cb = exp2f(m_b - mn_b);
+      m_a = mn_a;
+      m_b = mn_b;
+      float ps_a = 0.f, ps_b = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        sacc[j][0] = sacc[j][0] <= -1e29f ? 0.f : exp2f(sacc[j][0] - mn_a);
+        sacc[j][1] = sacc[j][1] <= -1e29f ? 0.f : exp2f(sacc[j][1] - mn_a);
+        sacc[j][2] = sacc[j][2] <= -1e29f ? 0.f : exp2f(sacc[j][2] - mn_b);
+        sacc[j][3] = sacc[j][3] <= -1e29f ? 0.f : exp2f(sacc[j][3] - mn_b);
+        ps_a += sacc[j][0] + sacc[j][1];
+        ps_b += sacc[j][2] + sacc[j][3];
+      }
+      l_a = l_a * ca + ps_a;
+      l_b = l_b * cb + ps_b;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        oacc[nt][0] *= ca;
+        oacc[nt][1] *= ca;
+        oacc[nt][2] *= cb;
+        oacc[nt][3] *= cb;
+      }
+      // O += P V: P (16 x 64) from the S fragments, V^T fragments by ldmatrix.trans
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const std::uint32_t pa0 = pack_bf16(sacc[2 * kk][0], sacc[2 * kk][1]);
+        const std::uint32_t pa1 = pack_bf16(sacc[2 * kk][2], sacc[2 * kk][3]);
+        const std::uint32_t pa2 = pack_bf16(sacc[2 * kk + 1][0], sacc[2 * kk + 1][1]);
+        const std::uint32_t pa3 = pack_bf16(sacc[2 * kk + 1][2], sacc[2 * kk + 1][3]);
+#pragma unroll
+        for (int np = 0; np < NT / 2; ++np) {  // two dim n-tiles per ldmatrix.x4.trans
+          const int vr = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+          const int ch = np * 2 + (lane >> 4);
+          std::uint32_t v00, v01, v10, v11;
+          ldsm_x4_t(vs_u + vr * RB + ((ch ^ (vr & 7)) << 4), v00, v01, v10, v11);
+          mma_bf16(oacc[2 * np], pa0, pa1, pa2, pa3, v00, v01);
+          mma_bf16(oacc[2 * np + 1], pa0, pa1, pa2, pa3, v10, v11);
+        }
+      }
+    }
+    if (warp_active) {
+      l_a += __shfl_xor_sync(kFull, l_a, 1);
+      l_a += __shfl_xor_sync(kFull, l_a, 2);
+      l_b += __shfl_xor_sync(kFull, l_b, 1);
+      l_b += __shfl_xor_sync(kFull, l_b, 2);
+      const float ia = pa >= 0 ? 1.0f / l_a : 0.f, ib = pb >= 0 ? 1.0f / l_b : 0.f;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int d = nt * 8 + 2 * t4;
+        if (pa >= 0)
+          *reinterpret_cast<__nv_bfloat162*>(o + (static_cast<long long>(b0 + ra) * nh + h) * HD + d) =
+              __floats2bfloat162_rn(oacc[nt][0] * ia, oacc[nt][1] * ia);
+        if (pb >= 0)
+          *reinterpret_cast<__nv_bfloat162*>(o + (static_cast<long long>(b0 + rb) * nh + h) * HD + d) =
+              __floats2bfloat162_rn(oacc[nt][2] * ib, oacc[nt][3] * ib);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Decode-tick QKV + attention in one kernel for small agents (every row is
 // the only row of its agent: pure decode).  CTA = (row, kv head): its
@@ -1425,10 +1644,15 @@ MOA_CHAIN_STAMP_SETTER(forward_chain_stamp)
 void attention_prefill(const bf16* q, const RowDesc* rows, int R_cap, const int* meta, int nh, int nkv, int hd,
                        const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx,
                        bf16* o, cudaStream_t st) {
-  const int smem = (hd * (kPfKeys + 1) + kPfKeys * hd + 8 * 8 * hd + 8 * kPfKeys * 8) * 4;
+  static const bool mma = [] {  // MOA_PREFILL_MMA=0: the SIMT kernel
+    const char* e = std::getenv("MOA_PREFILL_MMA");
+    return !(e && e[0] == '0');
+  }();
+  const int smem = mma ? (kPfRows + 2 * kPfKeys) * hd * 2
+                       : (hd * (kPfKeys + 1) + kPfKeys * hd + 8 * 8 * hd + 8 * kPfKeys * 8) * 4;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((R_cap + kPfRows - 1) / kPfRows, nh);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(mma ? 128 : 256);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -1444,10 +1668,16 @@ void attention_prefill(const bf16* q, const RowDesc* rows, int R_cap, const int*
     }
     cudaLaunchKernelEx(&cfg, kern, q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx, o);
   };
-  if (hd == 64)
+  if (mma) {
+    if (hd == 64)
+      go(attention_prefill_mma_kernel<64>);
+    else
+      go(attention_prefill_mma_kernel<128>);
+  } else if (hd == 64) {
     go(attention_prefill_kernel<64>);
-  else
+  } else {
     go(attention_prefill_kernel<128>);
+  }
 }
 
 int qkv_attention_smem(int D, int nh, int nkv, int hd) { return ((nh / nkv) + 2) * hd * D * 2 + D * 2 + D * 4 + 128; }
