@@ -1152,6 +1152,257 @@ attention_prefill_mma_kernel(const bf16* __restrict__ q, const RowDesc* __restri
   }
 }
 
+// GQA decode attention on the tensor cores: CTA = (row, kv head, key split),
+// 4 warps.  The group's q heads (<= 16) are the M rows of an m16n8k16 tile
+// (rows past the group are zero), so one K/V read serves every head of the
+// group at MMA speed.  Warp w takes the split's 64-key blocks w, w+4, ...: it
+// stages K and V of a block in its own swizzled smem slice, S = Q.K^T,
+// online softmax on the fragments, O += P.V; the warps then combine in smem
+// in a fixed order and a row spanning several splits is combined by the
+// last-arriving CTA (as attention_gqa_kernel).
+template <int HD>
+__global__ void __launch_bounds__(128, 1)
+attention_decode_mma_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, const int* __restrict__ meta,
+                            int nh, int nkv, const bf16* __restrict__ kpool, const bf16* __restrict__ vpool,
+                            long long kv_stride, long long layer_off, int max_ctx, bf16* __restrict__ o,
+                            float* __restrict__ ws, int* __restrict__ cnt, int nsplit_max, int split_keys,
+                            int skip_runs) {
+  constexpr int RB = HD * 2, KSTEPS = HD / 16, NT = HD / 8, NWARP = 4;
+  extern __shared__ __align__(128) unsigned char dm_sm[];
+  unsigned char* Qs = dm_sm;                           // [16][HD] bf16, swizzled
+  unsigned char* KV = dm_sm + 16 * RB;                 // per warp: K [64][HD], V [64][HD]
+  float* wo = reinterpret_cast<float*>(KV);            // after the key loop: [4 warps][16][HD] fp32
+  __shared__ float wm[NWARP][16], wl[NWARP][16], cm_s[16], cl_s[16];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int r = blockIdx.x, g = blockIdx.y, s = blockIdx.z;
+  const int live = __ldg(meta);
+  if (r >= live) return;
+  const RowDesc rd = rows[r];
+  if (skip_runs) {
+    if ((r > 0 && rows[r - 1].kv == rd.kv && rows[r - 1].pos + 1 == rd.pos) ||
+        (r + 1 < live && rows[r + 1].kv == rd.kv && rows[r + 1].pos == rd.pos + 1))
+      return;
+  }
+  const int n = rd.pos + 1;
+  const int nsplit = (n + split_keys - 1) / split_keys;
+  if (s >= nsplit) return;
+  const int hpg = nh / nkv;
+  const int kb = s * split_keys, ke = min(n, kb + split_keys);
+  const bf16* K = kpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
+  const bf16* V = vpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
+  for (int j = kb + threadIdx.x; j < ke - 1 && j < kb + 4 * 128; j += 128) {  // old keys only (pos is new)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(K + static_cast<long long>(j) * HD));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(V + static_cast<long long>(j) * HD));
+  }
+  MOA_PDL_ENTRY();
+  for (int c = threadIdx.x; c < 16 * (HD / 8); c += 128) {
+    const int hr = c / (HD / 8), ch = c % (HD / 8);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (hr < hpg) v = __ldcg(reinterpret_cast<const uint4*>(q + (static_cast<long long>(r) * nh + g * hpg + hr) * HD) + ch);
+    *reinterpret_cast<uint4*>(Qs + hr * RB + ((ch ^ (hr & 7)) << 4)) = v;
+  }
+  __syncthreads();
+  const std::uint32_t qs_u = static_cast<std::uint32_t>(__cvta_generic_to_shared(Qs));
+  unsigned char* Ks = KV + warp * 2 * kPfKeys * RB;
+  unsigned char* Vs = Ks + kPfKeys * RB;
+  const std::uint32_t ks_u = static_cast<std::uint32_t>(__cvta_generic_to_shared(Ks));
+  const std::uint32_t vs_u = static_cast<std::uint32_t>(__cvta_generic_to_shared(Vs));
+  std::uint32_t qa[KSTEPS][4];
+#pragma unroll
+  for (int kk = 0; kk < KSTEPS; ++kk) {
+    const int hr = lane & 15, ch = kk * 2 + (lane >> 4);
+    ldsm_x4(qs_u + hr * RB + ((ch ^ (hr & 7)) << 4), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+  }
+  const float sl2 = rsqrtf(static_cast<float>(HD)) * 1.4426950408889634f;
+  float m_a = -1e30f, m_b = -1e30f, l_a = 0.f, l_b = 0.f;
+  float oacc[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) oacc[nt][0] = oacc[nt][1] = oacc[nt][2] = oacc[nt][3] = 0.f;
+  for (int b0k = kb + warp * kPfKeys; b0k < ke; b0k += NWARP * kPfKeys) {
+    // stage this warp's block (all loads in flight, then the stores)
+    constexpr int CH = kPfKeys * (HD / 8) / 32;  // 16-byte chunks per lane per matrix
+#pragma unroll
+    for (int i0 = 0; i0 < CH; i0 += 8) {  // 8 K + 8 V chunks in flight per lane
+      uint4 kr[8], vr[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c = (i0 + i) * 32 + lane, key = c / (HD / 8), ch = c % (HD / 8);
+        const bool ok = b0k + key < ke;
+        kr[i] = ok ? __ldcg(reinterpret_cast<const uint4*>(K + static_cast<long long>(b0k + key) * HD) + ch)
+                   : make_uint4(0, 0, 0, 0);
+        vr[i] = ok ? __ldcg(reinterpret_cast<const uint4*>(V + static_cast<long long>(b0k + key) * HD) + ch)
+                   : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c = (i0 + i) * 32 + lane, key = c / (HD / 8), ch = c % (HD / 8);
+        *reinterpret_cast<uint4*>(Ks + key * RB + ((ch ^ (key & 7)) << 4)) = kr[i];
+        *reinterpret_cast<uint4*>(Vs + key * RB + ((ch ^ (key & 7)) << 4)) = vr[i];
+      }
+    }
+    __syncwarp();
+    float sacc[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < KSTEPS; ++kk) {
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) {
+        const int krow = jp * 16 + (lane & 7) + ((lane >> 4) << 3);
+        const int ch = kk * 2 + ((lane >> 3) & 1);
+        std::uint32_t b00, b01, b10, b11;
+        ldsm_x4(ks_u + krow * RB + ((ch ^ (krow & 7)) << 4), b00, b01, b10, b11);
+        mma_bf16(sacc[2 * jp], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b00, b01);
+        mma_bf16(sacc[2 * jp + 1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b10, b11);
+      }
+    }
+    float mx_a = -1e30f, mx_b = -1e30f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int key = b0k + 8 * j + 2 * t4;
+      sacc[j][0] = key < ke ? sacc[j][0] * sl2 : -1e30f;
+      sacc[j][1] = key + 1 < ke ? sacc[j][1] * sl2 : -1e30f;
+      sacc[j][2] = key < ke ? sacc[j][2] * sl2 : -1e30f;
+      sacc[j][3] = key + 1 < ke ? sacc[j][3] * sl2 : -1e30f;
+      mx_a = fmaxf(mx_a, fmaxf(sacc[j][0], sacc[j][1]));
+      mx_b = fmaxf(mx_b, fmaxf(sacc[j][2], sacc[j][3]));
+    }
+    mx_a = fmaxf(mx_a, __shfl_xor_sync(kFull, mx_a, 1));
+    mx_a = fmaxf(mx_a, __shfl_xor_sync(kFull, mx_a, 2));
+    mx_b = fmaxf(mx_b, __shfl_xor_sync(kFull, mx_b, 1));
+    mx_b = fmaxf(mx_b, __shfl_xor_sync(kFull, mx_b, 2));
+    const float mn_a = fmaxf(m_a, mx_a), mn_b = fmaxf(m_b, mx_b);
+    const float ca = exp2f(m_a - mn_a), cb = exp2f(m_b - mn_b);
+    m_a = mn_a;
+    m_b = mn_b;
+    float ps_a = 0.f, ps_b = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sacc[j][0] = sacc[j][0] <= -1e29f ? 0.f : exp2f(sacc[j][0] - mn_a);
+      sacc[j][1] = sacc[j][1] <= -1e29f ? 0.f : exp2f(sacc[j][1] - mn_a);
+      sacc[j][2] = sacc[j][2] <= -1e29f ? 0.f : exp2f(sacc[j][2] - mn_b);
+      sacc[j][3] = sacc[j][3] <= -1e29f ? 0.f : exp2f(sacc[j][3] - mn_b);
+      ps_a += sacc[j][0] + sacc[j][1];
+      ps_b += sacc[j][2] + sacc[j][3];
+    }
+    l_a = l_a * ca + ps_a;
+    l_b = l_b * cb + ps_b;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      oacc[nt][0] *= ca;
+      oacc[nt][1] *= ca;
+      oacc[nt][2] *= cb;
+      oacc[nt][3] *= cb;
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const std::uint32_t pa0 = pack_bf16(sacc[2 * kk][0], sacc[2 * kk][1]);
+      const std::uint32_t pa1 = pack_bf16(sacc[2 * kk][2], sacc[2 * kk][3]);
+      const std::uint32_t pa2 = pack_bf16(sacc[2 * kk + 1][0], sacc[2 * kk + 1][1]);
+      const std::uint32_t pa3 = pack_bf16(sacc[2 * kk + 1][2], sacc[2 * kk + 1][3]);
+#pragma unroll
+      for (int np = 0; np < NT / 2; ++np) {
+        const int vrow = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+        const int ch = np * 2 + (lane >> 4);
+        std::uint32_t v00, v01, v10, v11;
+        ldsm_x4_t(vs_u + vrow * RB + ((ch ^ (vrow & 7)) << 4), v00, v01, v10, v11);
+        mma_bf16(oacc[2 * np], pa0, pa1, pa2, pa3, v00, v01);
+        mma_bf16(oacc[2 * np + 1], pa0, pa1, pa2, pa3, v10, v11);
+      }
+    }
+    __syncwarp();  // this warp's staging is consumed before the next block overwrites it
+  }
+  // per-warp row stats (quad sums) and unnormalised outputs -> smem
+  l_a += __shfl_xor_sync(kFull, l_a, 1);
+  l_a += __shfl_xor_sync(kFull, l_a, 2);
+  l_b += __shfl_xor_sync(kFull, l_b, 1);
+  l_b += __shfl_xor_sync(kFull, l_b, 2);
+  __syncthreads();  // every warp is done with its K/V staging (wo reuses it)
+  if (t4 == 0) {
+    wm[warp][g8] = m_a;
+    wl[warp][g8] = l_a;
+    wm[warp][g8 + 8] = m_b;
+    wl[warp][g8 + 8] = l_b;
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int d = nt * 8 + 2 * t4;
+    wo[(warp * 16 + g8) * HD + d] = oacc[nt][0];
+    wo[(warp * 16 + g8) * HD + d + 1] = oacc[nt][1];
+    wo[(warp * 16 + g8 + 8) * HD + d] = oacc[nt][2];
+    wo[(warp * 16 + g8 + 8) * HD + d + 1] = oacc[nt][3];
+  }
+  __syncthreads();
+  if (threadIdx.x < hpg) {
+    const int h = threadIdx.x;
+    float M = -1e30f;
+    for (int w = 0; w < NWARP; ++w) M = fmaxf(M, wm[w][h]);
+    float Lsum = 0.f;
+    for (int w = 0; w < NWARP; ++w) Lsum += wl[w][h] == 0.f ? 0.f : exp2f(wm[w][h] - M) * wl[w][h];
+    cm_s[h] = M;
+    cl_s[h] = Lsum;
+  }
+  __syncthreads();
+  // natural-log stats for the split workspace (the combine below is shared with attention_gqa's layout)
+  for (int i = threadIdx.x; i < hpg * HD; i += 128) {
+    const int h = i / HD, e = i % HD;
+    const float M = cm_s[h];
+    float val = 0.f;
+    for (int w = 0; w < NWARP; ++w)
+      if (wl[w][h] != 0.f) val += exp2f(wm[w][h] - M) * wo[(w * 16 + h) * HD + e];
+    const int head = g * hpg + h;
+    if (nsplit == 1) {
+      o[(static_cast<long long>(r) * nh + head) * HD + e] = __float2bfloat16_rn(val / cl_s[h]);
+    } else {
+      float* part = ws + ((static_cast<long long>(r) * nh + head) * nsplit_max + s) * (2 + HD);
+      __stcg(part + 2 + e, val);
+      if (e == 0) {
+        __stcg(part, M * 0.6931471805599453f);  // log2 -> natural units
+        __stcg(part + 1, cl_s[h]);
+      }
+    }
+  }
+  if (nsplit == 1) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned prev;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(cnt + r * nkv + g) : "memory");
+    last = prev == static_cast<unsigned>(nsplit - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  // combine the splits (split order)
+  float* sw_s = reinterpret_cast<float*>(KV);  // [16][64] weights
+  for (int i = threadIdx.x; i < hpg * nsplit; i += 128) {
+    const int h = i / nsplit, t = i % nsplit;
+    sw_s[h * 64 + t] = __ldcg(ws + ((static_cast<long long>(r) * nh + g * hpg + h) * nsplit_max + t) * (2 + HD));
+  }
+  __syncthreads();
+  if (threadIdx.x < hpg) {
+    const int h = threadIdx.x;
+    float M = -INFINITY;
+    for (int t = 0; t < nsplit; ++t) M = fmaxf(M, sw_s[h * 64 + t]);
+    float Lsum = 0.f;
+    for (int t = 0; t < nsplit; ++t) {
+      const float w = __expf(sw_s[h * 64 + t] - M);
+      Lsum += w * __ldcg(ws + ((static_cast<long long>(r) * nh + g * hpg + h) * nsplit_max + t) * (2 + HD) + 1);
+      sw_s[h * 64 + t] = w;
+    }
+    cl_s[h] = Lsum;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < hpg * HD; i += 128) {
+    const int h = i / HD, e = i % HD;
+    const float* pr = ws + (static_cast<long long>(r) * nh + g * hpg + h) * nsplit_max * (2 + HD);
+    float val = 0.f;
+    for (int t = 0; t < nsplit; ++t) val += sw_s[h * 64 + t] * __ldcg(pr + t * (2 + HD) + 2 + e);
+    o[(static_cast<long long>(r) * nh + g * hpg + h) * HD + e] = __float2bfloat16_rn(val / cl_s[h]);
+  }
+  if (threadIdx.x == 0) cnt[r * nkv + g] = 0;
+}
+
 // ---------------------------------------------------------------------------
 // Decode-tick QKV + attention in one kernel for small agents (every row is
 // the only row of its agent: pure decode).  CTA = (row, kv head): its
@@ -1619,6 +1870,37 @@ void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, co
     return e ? std::atoi(e) : 4;
   }();
   const int hpg = nh / nkv;
+  static const bool mma = [] {  // MOA_DECODE_MMA=0: the SIMT kernel
+    const char* e = std::getenv("MOA_DECODE_MMA");
+    return !(e && e[0] == '0');
+  }();
+  if (mma && hpg <= 16 && nsplit_max <= 64) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(R_cap, nkv, nsplit_cap);
+    cfg.blockDim = dim3(128);
+    const int smem = 16 * hd * 2 + 4 * 2 * kPfKeys * hd * 2;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    auto gm = [&](auto kern) {
+      static std::set<const void*> attr;
+      if (attr.insert(reinterpret_cast<const void*>(kern)).second) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        uniform_carveout(reinterpret_cast<const void*>(kern));
+      }
+      cudaLaunchKernelEx(&cfg, kern, q, rows, meta, nh, nkv, kpool, vpool, kv_stride, layer_off, max_ctx, o, ws, cnt,
+                         nsplit_max, split_keys, skip_runs ? 1 : 0);
+    };
+    if (hd == 64)
+      gm(attention_decode_mma_kernel<64>);
+    else
+      gm(attention_decode_mma_kernel<128>);
+    return;
+  }
   int hpc = hpc_env == 2 || hpc_env == 4 ? hpc_env : 1;
   while (hpg % hpc) hpc >>= 1;
   dim3 grid(R_cap, nh / hpc, nsplit_cap);

@@ -173,19 +173,23 @@ def _cpu_model(tag, shape, seed):
     return _MODELS[key]
 
 
-@pytest.mark.parametrize("nh,nkv,hd", [(4, 4, 64), (32, 8, 64), (8, 2, 128)])
-def test_attention_kernels_match_torch(torch_cuda, nh, nkv, hd):
-    """Both attention kernels (tiled prefill, per-row GQA) against fp32 torch on
-    a tick mixing two prompt runs (one starting mid-context), a one-row
-    segment and a position break inside one agent's rows."""
+@pytest.mark.parametrize("nh,nkv,hd,max_ctx", [(4, 4, 64, 512), (32, 8, 64, 512), (8, 2, 128, 512),
+                                                (32, 8, 128, 2048)])
+def test_attention_kernels_match_torch(torch_cuda, nh, nkv, hd, max_ctx):
+    """Both attention paths (tiled prefill + per-row kernel for the rows alone
+    in their run; per-row kernel alone) against fp32 torch on a tick mixing
+    two prompt runs (one starting mid-context), one-row segments (decode rows,
+    several key splits when the context is long) and a position break inside
+    one agent's rows."""
     torch = torch_cuda
     g = torch.Generator(device="cpu").manual_seed(7 + nh + hd)
-    max_ctx, slots = 512, 4
+    slots = 4
     kv_stride = nkv * max_ctx * hd
     kpool = (torch.randn(slots * kv_stride, generator=g) * 0.5).to(torch.bfloat16).cuda()
     vpool = torch.randn(slots * kv_stride, generator=g).to(torch.bfloat16).cuda()
-    rows = [(0, p) for p in range(100, 230)] + [(1, p) for p in range(0, 70)] + [(2, 300)] + \
-           [(3, p) for p in range(10, 20)] + [(3, p) for p in range(40, 45)]
+    late = max_ctx - 200
+    rows = [(0, p) for p in range(100, 230)] + [(1, p) for p in range(0, 70)] + [(2, late)] + \
+           [(3, p) for p in range(10, 20)] + [(3, p) for p in range(40, 45)] + [(1, late + 150)]
     R = len(rows)
     q = torch.randn(R, nh, hd, generator=g).to(torch.bfloat16).cuda()
     rd = torch.tensor([[kv, pos, 0, 0] for kv, pos in rows], dtype=torch.int32).cuda()
