@@ -165,6 +165,9 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   dev_alloc(&gv_ws_, ws);
   dev_alloc(&gv_cnt_, (std::max({s.qkv_cols(), 2 * s.ffn, s.d}) + 127) / 128);
   qkv_attn_ok_ = k::qkv_attention_supported(D, s.n_heads, s.n_kv_heads, static_cast<int>(hd));
+  // K / V pools as [rows][hd] TMA maps (64-key boxes) for the fused kernel's swizzled key stage
+  kv_maps_ok_ = hd == 64 && k::make_tmap_bf16(&kmap_, kpool_, kv_stride_ * max_agents / hd, hd, 64) &&
+                k::make_tmap_bf16(&vmap_, vpool_, kv_stride_ * max_agents / hd, hd, 64);
   if (const char* e = std::getenv("MOA_QKV_ATTN")) use_qkv_attn_ = std::string(e) != "0";
   if (const char* e = std::getenv("MOA_PREFILL_ATTN")) use_prefill_attn_ = std::string(e) != "0";
   // RMSNorm folded into the decode GEMVs: ssq partials [16 rows][d/16]
@@ -466,7 +469,8 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     if (qkv_attn) {
       probe_begin(KernelProbes::Attention, 2.0 * s.qkv_cols() * D + 4.0 * live_keys_ * nkv * hd + 4.0 * live_R_ * D);
       k::qkv_attention(x_, ones_, eps, D, L.wqkv, buf_.rows, rcap, meta, rope_, nh, nkv, hd, kpool_, vpool_, kv_stride_,
-                       loff, max_ctx_, h_, st, l == 0 ? emb_ : nullptr, out_tok_read);
+                       loff, max_ctx_, h_, st, l == 0 ? emb_ : nullptr, out_tok_read, kv_maps_ok_ ? &kmap_ : nullptr,
+                       kv_maps_ok_ ? &vmap_ : nullptr);
       probe_end();
     } else {
     // rmsnorm -> QKV -> RoPE -> KV append

@@ -166,6 +166,8 @@ class DeviceModel {
   };
   std::vector<LayerMaps> wmaps_;
   k::TmaMap wmap_lm_;  // LM head [V][d], 128-row boxes
+  k::TmaMap kmap_, vmap_;  // K / V pools as [rows][hd], 64-row boxes (fused QKV + attention, hd 64)
+  bool kv_maps_ok_ = false;
   k::TmaMap map_hn_, map_h_attn_, map_h_ffn_;        // A operands, 128-row boxes (prefill)
   k::TmaMap map_hn16_, map_h_attn16_, map_h_ffn16_;  // 16-row boxes (decode, swap-AB)
   float* gv_ws_ = nullptr;                           // gemv_tc split-K partials

@@ -15,7 +15,10 @@
 #include <mutex>
 #include <set>
 
+#include <cuda.h>
+
 #include "kernels.cuh"
+#include "tc_common.cuh"
 #include "stamp.cuh"
 
 namespace moa::k {
@@ -1403,6 +1406,20 @@ attention_decode_mma_kernel(const bf16* __restrict__ q, const RowDesc* __restric
   if (threadIdx.x == 0) cnt[r * nkv + g] = 0;
 }
 
+// Element index of (key, dim) in a staged key block: plain [key][HD], or (HD
+// 64, TMA SWIZZLE_128B) the 16-byte chunk XOR-ed with key % 8.
+__device__ __forceinline__ std::uint32_t tcpack(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const std::uint32_t*>(&v);
+}
+
+template <int HD>
+__device__ __forceinline__ long long kv_smem_index_t(int key, int d, int swz) {
+  return swz ? static_cast<long long>(key) * HD + ((((d >> 3) ^ (key & 7)) << 3) | (d & 7))
+             : static_cast<long long>(key) * HD + d;
+}
+#define kv_smem_index(key, d, swz) kv_smem_index_t<HD>((key), (d), (swz))
+
 // ---------------------------------------------------------------------------
 // Decode-tick QKV + attention in one kernel for small agents (every row is
 // the only row of its agent: pure decode).  CTA = (row, kv head): its
@@ -1420,7 +1437,8 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
                      const float2* __restrict__ rope, int nh, int nkv, bf16* __restrict__ kpool,
                      bf16* __restrict__ vpool, long long kv_stride, long long layer_off, int max_ctx,
                      bf16* __restrict__ o, const bf16* __restrict__ emb, const int* __restrict__ out_tok,
-                     int kv_cap) {
+                     int kv_cap, const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                     int tma_kv) {
   constexpr int NW = 8, E = HD / 32, half = HD / 2;  // HPG >= q heads per kv head
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ float qs[HPG][HD];
@@ -1434,14 +1452,20 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
   const int hpg = nh / nkv, ncol = (hpg + 2) * HD;
   bf16* W = reinterpret_cast<bf16*>(dsm);                          // [ncol][D]
   bf16* xn = reinterpret_cast<bf16*>(dsm + static_cast<long long>(ncol) * D * 2);  // [D]
-  // keys of earlier ticks staged in smem (never produced by the previous kernel)
-  bf16* Ks = reinterpret_cast<bf16*>(dsm + static_cast<long long>(ncol) * D * 2 + D * 6);  // [kv_cap][HD]
+  // keys of earlier ticks staged in smem (never produced by the previous kernel);
+  // tma_kv (HD 64): 64-key TMA boxes, 128B-swizzled, 1024-aligned, for ldmatrix
+  const std::uintptr_t kv_raw = reinterpret_cast<std::uintptr_t>(dsm) + static_cast<std::uintptr_t>(ncol) * D * 2 + D * 6;
+  bf16* Ks = reinterpret_cast<bf16*>(tma_kv ? (kv_raw + 1023) & ~std::uintptr_t(1023) : kv_raw);  // [kv_cap][HD]
   bf16* Vs = Ks + static_cast<long long>(kv_cap) * HD;
   if (r >= __ldg(meta)) return;  // tick metadata: not produced by the previous kernel
   const RowDesc rd = rows[r];
   const int n = rd.pos + 1;
   const int ks = min(n - 1, kv_cap);  // staged earlier keys
-  const int nsm = min(n, kv_cap);     // keys read from smem (the own key lands there too when it fits)
+  // keys read from smem (the own key lands there too when it fits); with the
+  // swizzled TMA stage the whole context must fit (else every key from HBM)
+  const bool mma_att = tma_kv && n <= kv_cap;
+  const int nsm = tma_kv ? (mma_att ? n : 0) : min(n, kv_cap);
+  const int kboxes = mma_att ? (ks + 63) / 64 : 0;
   const bf16* K = kpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
   const bf16* V = vpool + rd.kv * kv_stride + layer_off + static_cast<long long>(g) * max_ctx * HD;
   const std::uint32_t bar = static_cast<std::uint32_t>(__cvta_generic_to_shared(&wbar));
@@ -1457,7 +1481,8 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned qb = hpg * HD * D * 2, kb = HD * D * 2, kvb = static_cast<unsigned>(ks) * HD * 2;
+    const unsigned qb = hpg * HD * D * 2, kb = HD * D * 2;
+    const unsigned kvb = tma_kv ? static_cast<unsigned>(kboxes) * 64 * HD * 2 : static_cast<unsigned>(ks) * HD * 2;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(qb + 2 * kb + 2 * kvb));
     const bf16* srcs[3] = {wqkv + static_cast<long long>(g * hpg * HD) * D,
                            wqkv + static_cast<long long>((nh + g) * HD) * D,
@@ -1472,7 +1497,13 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
           : "memory");
       off += bytes[i];
     }
-    if (kvb) {
+    if (tma_kv && kvb) {
+      const int row0 = static_cast<int>((K - kpool) / HD);  // the pool as [rows][HD]
+      for (int b = 0; b < kboxes; ++b) {
+        tc::tma_load_2d(Ks + b * 64 * HD, &kmap, reinterpret_cast<std::uint64_t*>(&wbar), 0, row0 + b * 64);
+        tc::tma_load_2d(Vs + b * 64 * HD, &vmap, reinterpret_cast<std::uint64_t*>(&wbar), 0, row0 + b * 64);
+      }
+    } else if (kvb) {
       const bf16* kv_src[2] = {K, V};
       bf16* kv_dst[2] = {Ks, Vs};
       for (int i = 0; i < 2; ++i)
@@ -1563,18 +1594,130 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
         qs[c / HD][d] = __bfloat162float(yb);
       } else {
         const_cast<bf16*>(K)[static_cast<long long>(rd.pos) * HD + d] = yb;
-        if (rd.pos < kv_cap) Ks[static_cast<long long>(rd.pos) * HD + d] = yb;
+        if (rd.pos < kv_cap) Ks[kv_smem_index(rd.pos, d, tma_kv)] = yb;
       }
     } else {
       const bf16 vb = __float2bfloat16_rn(v);
       const_cast<bf16*>(V)[static_cast<long long>(rd.pos) * HD + (c - (hpg + 1) * HD)] = vb;
-      if (rd.pos < kv_cap) Vs[static_cast<long long>(rd.pos) * HD + (c - (hpg + 1) * HD)] = vb;
+      if (rd.pos < kv_cap) Vs[kv_smem_index(rd.pos, c - (hpg + 1) * HD, tma_kv)] = vb;
     }
   }
   __threadfence_block();
   __syncthreads();
   if (threadIdx.x == 0) chain_mark(cst, 4);
   // attention over keys 0..pos (this row's own key included, just appended)
+  if constexpr (HD == 64) {
+    if (mma_att) {
+      // tensor-core attention: the group's q heads are the M rows of
+      // m16n8k16 tiles (Q tile in the now-free weight slab), warp w takes the
+      // staged 64-key blocks w, w + 8, ... (TMA-swizzled K / V, ldmatrix)
+      unsigned char* Qt = dsm;
+      // keys past the own one in the last 64-key box hold whatever the pool
+      // held (possibly NaN bit patterns): zero them so 0 * V stays 0
+      for (int i = threadIdx.x; i < (((n + 63) & ~63) - n) * (HD / 8); i += NW * 32) {
+        const int key = n + i / (HD / 8), ch = i % (HD / 8);
+        *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(Ks) + key * 128 + (ch << 4)) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(Vs) + key * 128 + (ch << 4)) = make_uint4(0, 0, 0, 0);
+      }
+      for (int i = threadIdx.x; i < 16 * (HD / 8); i += NW * 32) {
+        const int hr = i / (HD / 8), ch = i % (HD / 8);
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (hr < hpg) {
+          const float* qf = &qs[hr < HPG ? hr : 0][ch * 8];
+          v = make_uint4(tcpack(qf[0], qf[1]), tcpack(qf[2], qf[3]), tcpack(qf[4], qf[5]), tcpack(qf[6], qf[7]));
+        }
+        *reinterpret_cast<uint4*>(Qt + hr * 128 + ((ch ^ (hr & 7)) << 4)) = v;
+      }
+      __syncthreads();
+      const std::uint32_t qt_u = static_cast<std::uint32_t>(__cvta_generic_to_shared(Qt));
+      const std::uint32_t ks_u = static_cast<std::uint32_t>(__cvta_generic_to_shared(Ks));
+      const std::uint32_t vs_u = static_cast<std::uint32_t>(__cvta_generic_to_shared(Vs));
+      const int g8 = lane >> 2, t4 = lane & 3;
+      std::uint32_t qa[4][4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int hr = lane & 15, ch = kk * 2 + (lane >> 4);
+        ldsm_x4(qt_u + hr * 128 + ((ch ^ (hr & 7)) << 4), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+      }
+      const float sl2 = rsqrtf(64.f) * 1.4426950408889634f;
+      float m_a = -1e30f, l_a = 0.f;
+      float oacc[8][4];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) oacc[nt][0] = oacc[nt][1] = oacc[nt][2] = oacc[nt][3] = 0.f;
+      for (int b0k = warp * 64; b0k < n; b0k += NW * 64) {
+        float sacc[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+#pragma unroll
+          for (int jp = 0; jp < 4; ++jp) {
+            const int krow = b0k + jp * 16 + (lane & 7) + ((lane >> 4) << 3);
+            const int ch = kk * 2 + ((lane >> 3) & 1);
+            std::uint32_t b00, b01, b10, b11;
+            ldsm_x4(ks_u + krow * 128 + ((ch ^ (krow & 7)) << 4), b00, b01, b10, b11);
+            mma_bf16(sacc[2 * jp], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b00, b01);
+            mma_bf16(sacc[2 * jp + 1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b10, b11);
+          }
+        }
+        float mx = -1e30f;  // rows g8 (< 8) carry the heads; rows g8 + 8 are padding
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int kq = b0k + 8 * j + 2 * t4;
+          sacc[j][0] = kq < n ? sacc[j][0] * sl2 : -1e30f;
+          sacc[j][1] = kq + 1 < n ? sacc[j][1] * sl2 : -1e30f;
+          sacc[j][2] = sacc[j][3] = -1e30f;
+          mx = fmaxf(mx, fmaxf(sacc[j][0], sacc[j][1]));
+        }
+        mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 2));
+        const float mn = fmaxf(m_a, mx), ca = exp2f(m_a - mn);
+        m_a = mn;
+        float ps = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          sacc[j][0] = sacc[j][0] <= -1e29f ? 0.f : exp2f(sacc[j][0] - mn);
+          sacc[j][1] = sacc[j][1] <= -1e29f ? 0.f : exp2f(sacc[j][1] - mn);
+          sacc[j][2] = sacc[j][3] = 0.f;
+          ps += sacc[j][0] + sacc[j][1];
+        }
+        l_a = l_a * ca + ps;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+          oacc[nt][0] *= ca;
+          oacc[nt][1] *= ca;
+        }
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const std::uint32_t pa0 = tcpack(sacc[2 * kk][0], sacc[2 * kk][1]);
+          const std::uint32_t pa2 = tcpack(sacc[2 * kk + 1][0], sacc[2 * kk + 1][1]);
+#pragma unroll
+          for (int np = 0; np < 4; ++np) {
+            const int vrow = b0k + kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+            const int ch = np * 2 + (lane >> 4);
+            std::uint32_t v00, v01, v10, v11;
+            ldsm_x4_t(vs_u + vrow * 128 + ((ch ^ (vrow & 7)) << 4), v00, v01, v10, v11);
+            mma_bf16(oacc[2 * np], pa0, 0u, pa2, 0u, v00, v01);
+            mma_bf16(oacc[2 * np + 1], pa0, 0u, pa2, 0u, v10, v11);
+          }
+        }
+      }
+      l_a += __shfl_xor_sync(kFull, l_a, 1);
+      l_a += __shfl_xor_sync(kFull, l_a, 2);
+      if (g8 < hpg && g8 < HPG) {
+        if (t4 == 0) {
+          wm[warp][g8] = l_a == 0.f ? -INFINITY : m_a * 0.6931471805599453f;  // log2 -> natural units
+          wl[warp][g8] = l_a;
+        }
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+          wo[warp][g8][nt * 8 + 2 * t4] = oacc[nt][0];
+          wo[warp][g8][nt * 8 + 2 * t4 + 1] = oacc[nt][1];
+        }
+      }
+    }
+  }
+  if (!mma_att) {
   constexpr int TPK = HD / 64, KC = 32 / TPK;
   const int key = lane / TPK, part = lane % TPK;
   using VT = typename std::conditional<E == 2, unsigned, uint2>::type;
@@ -1658,6 +1801,7 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
 #pragma unroll
     for (int e = 0; e < E; ++e) wo[warp][h][lane * E + e] = acc[h][e];
   }
+  }  // !mma_att
   __syncthreads();
   if (threadIdx.x == 0) chain_mark(cst, 5);
   if (threadIdx.x < hpg) {
@@ -1983,9 +2127,18 @@ bool qkv_attention_supported(int D, int nh, int nkv, int hd) {
 void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv, const RowDesc* rows, int R_cap,
                    const int* meta, const float2* rope, int nh, int nkv, int hd, bf16* kpool, bf16* vpool,
                    long long kv_stride, long long layer_off, int max_ctx, bf16* o, cudaStream_t st, const bf16* emb,
-                   const int* out_tok) {
-  const int kv_cap = qkv_attention_kv_cap(D, nh, nkv, hd, max_ctx);
-  const int smem = qkv_attention_smem(D, nh, nkv, hd) + kv_cap * hd * 4;
+                   const int* out_tok, const TmaMap* kmap, const TmaMap* vmap) {
+  static const bool mma_env = [] {  // MOA_QKV_MMA=0: SIMT attention phase
+    const char* e = std::getenv("MOA_QKV_MMA");
+    return !(e && e[0] == '0');
+  }();
+  const int tma_kv = (mma_env && hd == 64 && kmap && vmap) ? 1 : 0;
+  int kv_cap = qkv_attention_kv_cap(D, nh, nkv, hd, max_ctx);
+  if (tma_kv) kv_cap = (kv_cap - 1024 / (hd * 4)) / 64 * 64;  // whole 64-key boxes after the 1 KB alignment pad
+  const int smem = qkv_attention_smem(D, nh, nkv, hd) + kv_cap * hd * 4 + (tma_kv ? 1024 : 0);
+  static const CUtensorMap no_map{};
+  const CUtensorMap& km = tma_kv ? *reinterpret_cast<const CUtensorMap*>(kmap) : no_map;
+  const CUtensorMap& vm = tma_kv ? *reinterpret_cast<const CUtensorMap*>(vmap) : no_map;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(R_cap, nkv);
   cfg.blockDim = dim3(256);
@@ -2004,7 +2157,7 @@ void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv,
       uniform_carveout(reinterpret_cast<const void*>(kern));
     }
     cudaLaunchKernelEx(&cfg, kern, X, g, eps, D, wqkv, rows, meta, rope, nh, nkv, kpool, vpool, kv_stride, layer_off,
-                       max_ctx, o, emb, out_tok, kv_cap);
+                       max_ctx, o, emb, out_tok, kv_cap, km, vm, tma_kv);
   };
   if (hd == 64) {
     if (hpg == 1) go(qkv_attention_kernel<64, 1>);
