@@ -313,8 +313,8 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
         if (ch >= nchunk) continue;
         const int t = ch / (R * 8), r = (ch >> 3) % R, cc = ch & 7;
         const float4* xp = reinterpret_cast<const float4*>(a.X + static_cast<long long>(r) * a.K + (kt0 + t) * kBK + cc * 8);
-        xa[u] = __ldcg(xp);
-        xb[u] = __ldcg(xp + 1);
+        xa[u] = __ldg(xp);
+        xb[u] = __ldg(xp + 1);
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
