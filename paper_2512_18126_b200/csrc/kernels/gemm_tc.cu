@@ -163,15 +163,69 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     umma_commit(done);
   }
   __syncwarp();
-  mbar_wait(done, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-
   // ---- epilogue: thread = row m0 + 32*warp + lane; 16 columns per tcgen05.ld ----
   const int row = m0 + warp * 32 + lane;
   const bool row_ok = row < live;
   const std::uint32_t lane_base = static_cast<std::uint32_t>(warp * 32) << 16;
   RowDesc rd{};
-  if (row_ok && a.epi == kEpiQkv) rd = a.rows[row];
+  if (row_ok && a.epi == kEpiQkv) {
+    // while the main loop runs: this row's descriptor and its RoPE table row
+    // into L1 (the epilogue reads one cos/sin pair per column pair)
+    rd = a.rows[row];
+    const char* rp = reinterpret_cast<const char*>(a.rope + static_cast<long long>(rd.pos) * (a.hd / 2));
+    for (int off = 0; off < a.hd * 4; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + off));
+  }
+  mbar_wait(done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (a.epi == kEpiQkv && kBN % a.hd == 0) {
+    // RoPE + q / K / V rows staged as a bf16 tile in the (now idle) pipeline
+    // smem in natural head order, then written out in 16-byte chunks: one
+    // head row (hd x 2 bytes) per destination, instead of one 2-byte store per
+    // element scattered over q and the KV pool
+    bf16* st = reinterpret_cast<bf16*>(smem);  // [kBM][kBN]
+    __shared__ RowDesc rds[kBM];
+    rds[warp * 32 + lane] = rd;
+    const int hd = a.hd, half = hd / 2, qk_cols = (a.nh + a.nkv) * hd;
+    for (int c0 = 0; c0 < kBN; c0 += 16) {
+      float v[16];
+      tmem_ld16(tmem + lane_base + static_cast<std::uint32_t>(c0), v);
+      if (!row_ok) continue;
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) {
+        const int n = n0 + c0 + i, cl = c0 + i;
+        if (n < qk_cols) {
+          const int e = (n % hd) / 2, hb = cl - (n % hd);  // tile-local head start
+          const float2 cs = a.rope[static_cast<long long>(rd.pos) * half + e];
+          const float x0 = v[i], x1 = v[i + 1];
+          st[(warp * 32 + lane) * kBN + hb + e] = __float2bfloat16_rn(__fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y)));
+          st[(warp * 32 + lane) * kBN + hb + e + half] =
+              __float2bfloat16_rn(__fadd_rn(__fmul_rn(x1, cs.x), __fmul_rn(x0, cs.y)));
+        } else {
+          st[(warp * 32 + lane) * kBN + cl] = __float2bfloat16_rn(v[i]);
+          st[(warp * 32 + lane) * kBN + cl + 1] = __float2bfloat16_rn(v[i + 1]);
+        }
+      }
+    }
+    __syncthreads();
+    const int cpr = kBN / 8;  // 16-byte chunks per tile row
+    for (int c = threadIdx.x; c < kBM * cpr; c += 128) {
+      const int rl = c / cpr, ch = c % cpr, r = m0 + rl;
+      const int n = n0 + ch * 8;
+      if (r >= live || n >= a.N) continue;
+      const RowDesc d = rds[rl];
+      const uint4 val = *reinterpret_cast<const uint4*>(st + rl * kBN + ch * 8);
+      const int head = n / hd, e = n % hd;
+      bf16* dst;
+      if (head < a.nh)
+        dst = a.out_bf16 + (static_cast<long long>(r) * a.nh + head) * hd + e;
+      else if (head < a.nh + a.nkv)
+        dst = a.kpool + d.kv * a.kv_stride + a.layer_off + (static_cast<long long>(head - a.nh) * a.max_ctx + d.pos) * hd + e;
+      else
+        dst = a.vpool + d.kv * a.kv_stride + a.layer_off +
+              (static_cast<long long>(head - a.nh - a.nkv) * a.max_ctx + d.pos) * hd + e;
+      *reinterpret_cast<uint4*>(dst) = val;
+    }
+  } else
   for (int c0 = 0; c0 < kBN; c0 += 16) {
     float v[16];
     tmem_ld16(tmem + lane_base + static_cast<std::uint32_t>(c0), v);
