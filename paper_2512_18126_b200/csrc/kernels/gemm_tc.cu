@@ -252,13 +252,15 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         }
         break;
       }
-      case kEpiSwiGlu: {
-        bf16* o = a.out_bf16 + static_cast<long long>(row) * (a.N / 2) + nb / 2;
+      case kEpiSwiGlu: {  // 8 outputs = one 16-byte store
+        __align__(16) bf16 o8[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const float g = v[2 * i], u = v[2 * i + 1];
-          o[i] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
+          o8[i] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
         }
+        *reinterpret_cast<uint4*>(a.out_bf16 + static_cast<long long>(row) * (a.N / 2) + nb / 2) =
+            *reinterpret_cast<const uint4*>(o8);
         break;
       }
       case kEpiQkv: {
