@@ -175,6 +175,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const char* rp = reinterpret_cast<const char*>(a.rope + static_cast<long long>(rd.pos) * (a.hd / 2));
     for (int off = 0; off < a.hd * 4; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + off));
   }
+  if (row_ok && a.epi == kEpiResidual) {  // the tile's residual row segment into L1 while the main loop runs
+    const char* xp = reinterpret_cast<const char*>(a.out + static_cast<long long>(row) * a.N + n0);
+    for (int off = 0; off < kBN * 4 && n0 + off / 4 < a.N; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(xp + off));
+  }
   mbar_wait(done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (a.epi == kEpiQkv && kBN % a.hd == 0) {
@@ -182,7 +186,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // smem in natural head order, then written out in 16-byte chunks: one
     // head row (hd x 2 bytes) per destination, instead of one 2-byte store per
     // element scattered over q and the KV pool
-    bf16* st = reinterpret_cast<bf16*>(smem);  // [kBM][kBN]
+    bf16* st = reinterpret_cast<bf16*>(smem);  // [kBM][kBN], 16-byte chunks XOR-ed with row % 16
+    // (a warp's threads are 32 rows writing the same column: without the
+    // swizzle every store of a warp hits one bank)
+    auto sti = [](int rr, int cc) { return rr * kBN + ((((cc >> 3) ^ (rr & 15))) << 3) + (cc & 7); };
     __shared__ RowDesc rds[kBM];
     rds[warp * 32 + lane] = rd;
     const int hd = a.hd, half = hd / 2, qk_cols = (a.nh + a.nkv) * hd;
@@ -197,12 +204,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
           const int e = (n % hd) / 2, hb = cl - (n % hd);  // tile-local head start
           const float2 cs = a.rope[static_cast<long long>(rd.pos) * half + e];
           const float x0 = v[i], x1 = v[i + 1];
-          st[(warp * 32 + lane) * kBN + hb + e] = __float2bfloat16_rn(__fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y)));
-          st[(warp * 32 + lane) * kBN + hb + e + half] =
+          st[sti(warp * 32 + lane, hb + e)] = __float2bfloat16_rn(__fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y)));
+          st[sti(warp * 32 + lane, hb + e + half)] =
               __float2bfloat16_rn(__fadd_rn(__fmul_rn(x1, cs.x), __fmul_rn(x0, cs.y)));
         } else {
-          st[(warp * 32 + lane) * kBN + cl] = __float2bfloat16_rn(v[i]);
-          st[(warp * 32 + lane) * kBN + cl + 1] = __float2bfloat16_rn(v[i + 1]);
+          st[sti(warp * 32 + lane, cl)] = __float2bfloat16_rn(v[i]);
+          st[sti(warp * 32 + lane, cl + 1)] = __float2bfloat16_rn(v[i + 1]);
         }
       }
     }
@@ -213,7 +220,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       const int n = n0 + ch * 8;
       if (r >= live || n >= a.N) continue;
       const RowDesc d = rds[rl];
-      const uint4 val = *reinterpret_cast<const uint4*>(st + rl * kBN + ch * 8);
+      const uint4 val = *reinterpret_cast<const uint4*>(st + sti(rl, ch * 8));
       const int head = n / hd, e = n % hd;
       bf16* dst;
       if (head < a.nh)
