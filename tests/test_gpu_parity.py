@@ -31,6 +31,11 @@ from paper_2512_18126_b200.configs import C0, C1, C1U, CONFIGS
 
 pytestmark = pytest.mark.gpu
 
+# two different leaf models decoding side by side (per-model streams, decode runs on both)
+_HETERO = dict(C1, name="C1-hetero", models=dict(a=dict(shape="tiny", seed=1), b=dict(shape="tiny", seed=3),
+                                                agg=dict(shape="tiny", seed=2)),
+               assign=[["a", "b"], ["agg"], ["b"]])
+
 
 
 @pytest.fixture(scope="module")
@@ -263,7 +268,7 @@ def test_long_context_decode_matches_oracle():
     eng.close()
 
 
-@pytest.mark.parametrize("cfg", [C1, C1U])
+@pytest.mark.parametrize("cfg", [C1, C1U, _HETERO])
 def test_decode_runs_match_tick_by_tick(cfg):
     """Decode runs (up to 8 pure-decode ticks launched as one graph) replay the
     same per-tick forwards: tokens, logprobs, the schedule and every early-exit
@@ -384,7 +389,7 @@ _SEQ = dict(C1U, name="C1U-seq", mode="sequential-pd")
 
 
 @pytest.mark.parametrize("cfg,sample", [(C0, 0), (C1, 0), (C1, 5), (C1U, 0), (C1U, 3), (_DENSE_EE, 1), (_CHUNKED, 2),
-                                        (_SEQ, 4)],
+                                        (_SEQ, 4), (_HETERO, 1)],
                          ids=lambda v: v["name"] if isinstance(v, dict) else str(v))
 def test_run_query_replay_and_numerics(cfg, sample):
     g = _gpu_query(cfg, sample)
