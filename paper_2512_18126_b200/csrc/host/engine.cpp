@@ -273,13 +273,17 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   int max_pos = 0;
   long long keys = 0;
   bool distinct = rows.size() <= 64;  // every row a different agent (pure decode)?
-  int runs = 0;                        // maximal same-agent runs of consecutive positions
+  int runs = 0, singles = 0;           // maximal same-agent runs of consecutive positions; runs of one row
+  auto joined = [&](std::size_t i) {    // rows i - 1 and i are one run
+    return i > 0 && i < rows.size() && rows[i - 1].kv == rows[i].kv && rows[i - 1].pos + 1 == rows[i].pos;
+  };
   for (std::size_t i = 0; i < rows.size(); ++i) {
     const auto& rd = rows[i];
     max_pos = std::max(max_pos, rd.pos);
     keys += rd.pos + 1;
     for (std::size_t j = 0; j < i && distinct; ++j) distinct = rows[j].kv != rd.kv;
-    runs += i == 0 || rows[i - 1].kv != rd.kv || rows[i - 1].pos + 1 != rd.pos;
+    runs += !joined(i);
+    singles += !joined(i) && !joined(i + 1);
   }
   // prompt-prefill tick: long same-agent runs -> tiled prefill attention (below
   // ~512 rows the per-row kernel's CTA count wins: measured on C1's
@@ -315,7 +319,7 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   }
   float* logits = (opt_.keep_logits && !lsel.empty()) ? logits_scratch_ : nullptr;
   dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), max_pos, keys, out_tok_, out_tok_,
-             out_lp_, out_ent_, logits, st, distinct, prefill);
+             out_lp_, out_ent_, logits, st, distinct, prefill, singles > 0);
   if (logits) {  // debug path: scatter each logits row to its (slot, k) home
     const long long V = dm.spec().vocab;
     for (std::size_t i = 0; i < lsel.size(); ++i)

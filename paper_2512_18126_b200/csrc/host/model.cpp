@@ -332,7 +332,8 @@ int pow2_at_least(int v, int lo) {
 }  // namespace
 
 void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int* out_tok_read, int* out_tok,
-                          float* out_lp, float* out_ent, float* logits, cudaStream_t st, bool distinct, bool prefill) {
+                          float* out_lp, float* out_ent, float* logits, cudaStream_t st, bool distinct, bool prefill,
+                          bool singles) {
   // (tensor-core ticks only: the GEMV-only path keeps every row's attention in
   // one kernel, so its tokens stay bit-identical across schedule modes)
   prefill = prefill && use_prefill_attn_ && use_tc_;
@@ -348,17 +349,18 @@ void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int*
     live_R_ = R;
     live_Rl_ = Rl;
     live_keys_ = keys;
-    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st, distinct, prefill);
+    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st, distinct, prefill, singles);
     return;
   }
   const auto key = std::make_tuple(rcap, nsplit, (Rl > 0 ? 1 : 0) | (use_tc_ ? 2 : 0) | (use_mk_ ? 4 : 0) |
-                                                     (distinct ? 8 : 0) | (blob_ << 4) | (prefill ? 32 : 0),
+                                                     (distinct ? 8 : 0) | (blob_ << 4) | (prefill ? 32 : 0) |
+                                                     (prefill && !singles ? 64 : 0),
                                    logits ? 1 : 0);
   auto it = graphs_.find(key);
   if (it == graphs_.end()) {
     cudaGraph_t g = nullptr;
     MOA_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st, distinct, prefill);
+    launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st, distinct, prefill, singles);
     MOA_CUDA(cudaStreamEndCapture(st, &g));
     cudaGraphExec_t exec = nullptr;
     MOA_CUDA(cudaGraphInstantiate(&exec, g, 0));
@@ -400,7 +402,8 @@ void DeviceModel::forward_run(int K, int R, int max_pos, const int* out_tok_read
 }
 
 void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_tok_read, int* out_tok,
-                         float* out_lp, float* out_ent, float* logits, cudaStream_t st, bool distinct, bool prefill) {
+                         float* out_lp, float* out_ent, float* logits, cudaStream_t st, bool distinct, bool prefill,
+                         bool singles) {
   const ModelSpec& s = spec_;
   const int D = s.d, hd = s.head_dim, nh = s.n_heads, nkv = s.n_kv_heads;
   const float eps = static_cast<float>(s.norm_eps);
@@ -503,8 +506,9 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     // decode rows (alone in their run) by the per-row kernel
     if (prefill)
       k::attention_prefill(q_, buf_.rows, rcap, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_, st);
-    k::attention(q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_,
-                 attn_ws_, attn_cnt_, st, prefill);
+    if (!prefill || singles)
+      k::attention(q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_,
+                   attn_ws_, attn_cnt_, st, prefill);
     probe_end();
     }
     // x += o . Wo^T

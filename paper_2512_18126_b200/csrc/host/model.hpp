@@ -112,8 +112,10 @@ class DeviceModel {
   // engine's flat per-agent output arrays; logits (optional) [Rl][V] fp32.
   // distinct: every row belongs to a different agent (a pure decode tick)
   // prefill: the rows are long same-agent runs (prompt prefill): tiled attention
+  // (singles: some rows are alone in their run -- the per-row kernel serves them)
   void forward(int R, int Rl, int max_pos, long long keys, const int* out_tok_read, int* out_tok, float* out_lp,
-               float* out_ent, float* logits, cudaStream_t st, bool distinct = false, bool prefill = false);
+               float* out_ent, float* logits, cudaStream_t st, bool distinct = false, bool prefill = false,
+               bool singles = true);
   // K ticks of R decode rows each (every row its own agent, one logits row per
   // row), metadata already in run_blob(parity); max_pos of the last tick.
   void forward_run(int K, int R, int max_pos, const int* out_tok_read, int* out_tok, float* out_lp, float* out_ent,
@@ -126,7 +128,8 @@ class DeviceModel {
 
  private:
   void launch(int rcap, int nsplit, bool with_logits, const int* out_tok_read, int* out_tok, float* out_lp,
-              float* out_ent, float* logits, cudaStream_t st, bool distinct, bool prefill = false);
+              float* out_ent, float* logits, cudaStream_t st, bool distinct, bool prefill = false,
+              bool singles = true);
   bool qkv_attn_ok_ = false, use_qkv_attn_ = true;  // fused QKV + attention for small-agent decode ticks
   bool use_prefill_attn_ = true;  // tiled prefill attention for prompt-prefill ticks (MOA_PREFILL_ATTN)
   std::map<std::tuple<int, int, int, int>, cudaGraphExec_t> graphs_;
