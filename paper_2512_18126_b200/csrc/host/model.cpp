@@ -165,6 +165,23 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   dev_alloc(&gv_ws_, ws);
   dev_alloc(&gv_cnt_, (std::max({s.qkv_cols(), 2 * s.ffn, s.d}) + 127) / 128);
   qkv_attn_ok_ = k::qkv_attention_supported(D, s.n_heads, s.n_kv_heads, static_cast<int>(hd));
+  {
+    // the o-projection regrouped by kv group, [L][nkv][D][hpg*hd], for the fused
+    // QKV + attention + o-projection decode kernel (small agents; MOA_FUSE_O=0: off)
+    const char* e = std::getenv("MOA_FUSE_O");
+    const int hpg = s.n_heads / s.n_kv_heads;
+    const long long blk = static_cast<long long>(D) * hpg * hd;
+    if (qkv_attn_ok_ && !(e && e[0] == '0') && D % s.n_kv_heads == 0 && s.n_kv_heads <= 8 &&
+        4096 + blk * 2 + D * 4 <= static_cast<long long>(hpg + 2) * hd * D * 2) {
+      dev_alloc(&wo_blk_, blk * s.n_kv_heads * s.n_layers);
+      for (int l = 0; l < s.n_layers; ++l)
+        for (int gq = 0; gq < s.n_kv_heads; ++gq)
+          MOA_CUDA(cudaMemcpy2DAsync(wo_blk_ + (static_cast<long long>(l) * s.n_kv_heads + gq) * blk, hpg * hd * 2,
+                                     layers_[static_cast<std::size_t>(l)].wo + static_cast<long long>(gq) * hpg * hd,
+                                     static_cast<long long>(s.n_heads) * hd * 2, hpg * hd * 2, D,
+                                     cudaMemcpyDeviceToDevice, st));
+    }
+  }
   // K / V pools as [rows][hd] TMA maps (64-key boxes) for the fused kernel's swizzled key stage
   kv_maps_ok_ = hd == 64 && k::make_tmap_bf16(&kmap_, kpool_, kv_stride_ * max_agents / hd, hd, 64) &&
                 k::make_tmap_bf16(&vmap_, vpool_, kv_stride_ * max_agents / hd, hd, 64);
@@ -288,7 +305,7 @@ DeviceModel::~DeviceModel() {
                     static_cast<void*>(kpool_), static_cast<void*>(vpool_), static_cast<void*>(x_),
                     static_cast<void*>(h_), static_cast<void*>(q_), static_cast<void*>(attn_ws_),
                     static_cast<void*>(attn_cnt_), static_cast<void*>(part_), static_cast<void*>(lm_cnt_),
-                    meta_blob_, run_area_, static_cast<void*>(hn_),
+                    meta_blob_, run_area_, static_cast<void*>(hn_), static_cast<void*>(wo_blk_),
                     static_cast<void*>(gv_ws_), static_cast<void*>(gv_cnt_), static_cast<void*>(ssq_), mk_maps_, static_cast<void*>(mk_ssq_),
                     static_cast<void*>(mk_ws_), static_cast<void*>(mk_cnt_), static_cast<void*>(mk_attn_ws_),
                     static_cast<void*>(mk_attn_cnt_), static_cast<void*>(mk_lm_part_), static_cast<void*>(mk_lm_cnt_),
@@ -452,6 +469,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   // decode ticks of small agents: (embedding gather +) RMSNorm + QKV + RoPE + KV
   // append + attention in one launch per layer
   const bool qkv_attn = !small && use_tc_ && use_qkv_attn_ && qkv_attn_ok_ && distinct && rcap <= k::kGemvTcRows;
+  const bool fuse_o = qkv_attn && wo_blk_ != nullptr;
   if (small) {
     k::SmallParams sp = small_;
     sp.out_tok_read = out_tok_read;
@@ -473,7 +491,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       probe_begin(KernelProbes::Attention, 2.0 * s.qkv_cols() * D + 4.0 * live_keys_ * nkv * hd + 4.0 * live_R_ * D);
       k::qkv_attention(x_, ones_, eps, D, L.wqkv, buf_.rows, rcap, meta, rope_, nh, nkv, hd, kpool_, vpool_, kv_stride_,
                        loff, max_ctx_, h_, st, l == 0 ? emb_ : nullptr, out_tok_read, kv_maps_ok_ ? &kmap_ : nullptr,
-                       kv_maps_ok_ ? &vmap_ : nullptr);
+                       kv_maps_ok_ ? &vmap_ : nullptr, fuse_o ? wo_blk_ + static_cast<long long>(l) * D * nh * hd : nullptr);
       probe_end();
     } else {
     // rmsnorm -> QKV -> RoPE -> KV append
@@ -511,7 +529,8 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
                    attn_ws_, attn_cnt_, st, prefill);
     probe_end();
     }
-    // x += o . Wo^T
+    // x += o . Wo^T (folded into the fused QKV + attention kernel when fuse_o)
+    if (!fuse_o) {
     k::GemvArgs o;
     o.A = h_;
     o.R = rcap;
@@ -527,6 +546,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     probe_begin(KernelProbes::OProj, 2.0 * o.N * o.K + 2.0 * live_R_ * o.K + 8.0 * live_R_ * D);
     run_gemm(o, &map_h_attn_, &map_h_attn16_, wmaps_[static_cast<std::size_t>(l)].wo);
     probe_end();
+    }
     // a = silu(gate) * up over rmsnorm(x)
     k::GemvArgs gu;
     gu.X = x_;

@@ -170,6 +170,7 @@ class DeviceModel {
   std::vector<LayerMaps> wmaps_;
   k::TmaMap wmap_lm_;  // LM head [V][d], 128-row boxes
   k::TmaMap kmap_, vmap_;  // K / V pools as [rows][hd], 64-row boxes (fused QKV + attention, hd 64)
+  k::bf16* wo_blk_ = nullptr;  // [L][nkv][D][hpg*hd]: Wo regrouped for the fused o-projection
   bool kv_maps_ok_ = false;
   k::TmaMap map_hn_, map_h_attn_, map_h_ffn_;        // A operands, 128-row boxes (prefill)
   k::TmaMap map_hn16_, map_h_attn16_, map_h_ffn16_;  // 16-row boxes (decode, swap-AB)

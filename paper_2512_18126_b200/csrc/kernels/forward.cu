@@ -1438,7 +1438,7 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
                      bf16* __restrict__ vpool, long long kv_stride, long long layer_off, int max_ctx,
                      bf16* __restrict__ o, const bf16* __restrict__ emb, const int* __restrict__ out_tok,
                      int kv_cap, const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
-                     int tma_kv) {
+                     int tma_kv, const bf16* __restrict__ wo_blk) {
   constexpr int NW = 8, E = HD / 32, half = HD / 2;  // HPG >= q heads per kv head
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ float qs[HPG][HD];
@@ -1446,7 +1446,7 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
   __shared__ float wo[NW][HPG][HD];
   __shared__ float cm_s[HPG], cl_s[HPG];
   __shared__ float red[NW];
-  __shared__ __align__(8) unsigned long long wbar;
+  __shared__ __align__(8) unsigned long long wbar, obar;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.x, g = blockIdx.y;
   const int hpg = nh / nkv, ncol = (hpg + 2) * HD;
@@ -1475,8 +1475,10 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
     chain_reset(cst);
     chain_mark(cst, 0);
   }
+  const std::uint32_t obar_u = static_cast<std::uint32_t>(__cvta_generic_to_shared(&obar));
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(obar_u));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -1537,7 +1539,7 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
     for (int c = threadIdx.x; c < D; c += 256) {
       const float v = __bfloat162float(e[c]);
       xs[c] = v;
-      if (g == 0) x[c] = v;
+      if (g == 0 && !wo_blk) x[c] = v;  // fused o-projection: the owners write the final rows
     }
     __syncthreads();
     x = xs;
@@ -1605,6 +1607,21 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
   __threadfence_block();
   __syncthreads();
   if (threadIdx.x == 0) chain_mark(cst, 4);
+  // fused o-projection: this group's Wo block [D][hpg*HD] into the (now free)
+  // weight slab, past the 4 KB the tensor-core attention uses for its Q tile
+  const int obytes = D * hpg * HD * 2;
+  if (wo_blk && threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(obar_u), "r"(obytes));
+    for (int off = 0; off < obytes; off += 32768) {
+      const int nbytes = obytes - off < 32768 ? obytes - off : 32768;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              static_cast<std::uint32_t>(__cvta_generic_to_shared(dsm + 4096 + off))),
+          "l"(reinterpret_cast<const char*>(wo_blk + static_cast<long long>(g) * D * hpg * HD) + off), "r"(nbytes),
+          "r"(obar_u)
+          : "memory");
+    }
+  }
   // attention over keys 0..pos (this row's own key included, just appended)
   if constexpr (HD == 64) {
     if (mma_att) {
@@ -1820,7 +1837,55 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
     float val = 0.f;
     for (int w = 0; w < NW; ++w)
       if (wm[w][h] != -INFINITY) val += __expf(wm[w][h] - M) * wo[w][h][e];
-    o[(static_cast<long long>(r) * nh + g * hpg + h) * HD + e] = __float2bfloat16_rn(val / cl_s[h]);
+    const bf16 ob = __float2bfloat16_rn(val / cl_s[h]);
+    if (wo_blk)
+      qs[h][e] = __bfloat162float(ob);  // the group's attention rows stay on chip
+    else
+      o[(static_cast<long long>(r) * nh + g * hpg + h) * HD + e] = ob;
+  }
+  if (wo_blk) {
+    // x[row] += o . Wo^T over the cluster of this row's kv-head CTAs: CTA g
+    // forms its heads' contribution to every output column, pushes slice q of
+    // it into CTA q's smem (DSMEM), and CTA q adds the slices in rank order
+    // to the residual and writes its D / nkv columns
+    const int S = D / nkv;
+    float* recv = reinterpret_cast<float*>(dsm + 4096 + obytes);  // [nkv][S]
+    __syncthreads();
+    {
+      std::uint32_t ok = 0;
+      while (!ok)
+        asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok)
+                     : "r"(obar_u)
+                     : "memory");
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    const int K8 = hpg * HD / 8;  // 16-byte chunks per Wo row
+    const bf16* wob = reinterpret_cast<const bf16*>(dsm + 4096);
+    for (int n = threadIdx.x; n < D; n += NW * 32) {
+      const uint4* wr = reinterpret_cast<const uint4*>(wob + static_cast<long long>(n) * hpg * HD);
+      float acc = 0.f;
+      for (int c = 0; c < K8; ++c) {
+        const int cr = (c + n) % K8;  // rotated: the rows of a quarter warp hit distinct banks
+        float w8[8];
+        unpack8(wr[cr], w8);
+        const int h = (cr * 8) / HD, d0 = (cr * 8) % HD;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc = fmaf(qs[h][d0 + t], w8[t], acc);
+      }
+      const int q = n / S, i = n % S;
+      std::uint32_t dst;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                   : "=r"(dst)
+                   : "r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(recv + g * S + i))), "r"(q));
+      asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(dst), "f"(acc) : "memory");
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    for (int i = threadIdx.x; i < S; i += NW * 32) {
+      float v = x[g * S + i];
+      for (int src = 0; src < nkv; ++src) v += recv[src * S + i];
+      X[static_cast<long long>(r) * D + g * S + i] = v;
+    }
   }
   if (threadIdx.x == 0) {
     chain_mark(cst, 2);
@@ -2127,7 +2192,7 @@ bool qkv_attention_supported(int D, int nh, int nkv, int hd) {
 void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv, const RowDesc* rows, int R_cap,
                    const int* meta, const float2* rope, int nh, int nkv, int hd, bf16* kpool, bf16* vpool,
                    long long kv_stride, long long layer_off, int max_ctx, bf16* o, cudaStream_t st, const bf16* emb,
-                   const int* out_tok, const TmaMap* kmap, const TmaMap* vmap) {
+                   const int* out_tok, const TmaMap* kmap, const TmaMap* vmap, const bf16* wo_blk) {
   static const bool mma_env = [] {  // MOA_QKV_MMA=0: SIMT attention phase
     const char* e = std::getenv("MOA_QKV_MMA");
     return !(e && e[0] == '0');
@@ -2136,6 +2201,8 @@ void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv,
   int kv_cap = qkv_attention_kv_cap(D, nh, nkv, hd, max_ctx);
   if (tma_kv) kv_cap = (kv_cap - 1024 / (hd * 4)) / 64 * 64;  // whole 64-key boxes after the 1 KB alignment pad
   const int smem = qkv_attention_smem(D, nh, nkv, hd) + kv_cap * hd * 4 + (tma_kv ? 1024 : 0);
+  if (wo_blk && 4096 + D * (nh / nkv) * hd * 2 + D * 4 > ((nh / nkv) + 2) * hd * D * 2)
+    wo_blk = nullptr;  // the Wo block and the receive slices must fit the weight slab
   static const CUtensorMap no_map{};
   const CUtensorMap& km = tma_kv ? *reinterpret_cast<const CUtensorMap*>(kmap) : no_map;
   const CUtensorMap& vm = tma_kv ? *reinterpret_cast<const CUtensorMap*>(vmap) : no_map;
@@ -2144,11 +2211,22 @@ void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv,
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (wo_blk) {  // a row's kv-head CTAs form one cluster (the fused o-projection exchanges over DSMEM)
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 1;
+    at[na].val.clusterDim.y = nkv;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = na;
   const int hpg = nh / nkv;
   auto go = [&](auto kern) {
     static std::set<const void*> attr;
@@ -2157,7 +2235,7 @@ void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv,
       uniform_carveout(reinterpret_cast<const void*>(kern));
     }
     cudaLaunchKernelEx(&cfg, kern, X, g, eps, D, wqkv, rows, meta, rope, nh, nkv, kpool, vpool, kv_stride, layer_off,
-                       max_ctx, o, emb, out_tok, kv_cap, km, vm, tma_kv);
+                       max_ctx, o, emb, out_tok, kv_cap, km, vm, tma_kv, wo_blk);
   };
   if (hd == 64) {
     if (hpg == 1) go(qkv_attention_kernel<64, 1>);

@@ -275,11 +275,14 @@ bool qkv_attention_supported(int D, int nh, int nkv, int hd);
 // vmap (hd 64): the K / V pools as [rows][64] TMA maps with 64-row boxes --
 // the earlier keys arrive 128B-swizzled and the attention phase runs on the
 // tensor cores (mma.sync) when the whole context fits the smem stage.
+// wo_blk ([nkv][D][hpg*hd], the o-projection regrouped by kv group): the
+// kernel also applies x += o . Wo^T across a cluster of the row's nkv CTAs
+// (DSMEM) -- the o-projection launch folded in; o is then not written.
 void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv, const RowDesc* rows, int R_cap,
                    const int* meta, const float2* rope, int nh, int nkv, int hd, bf16* kpool, bf16* vpool,
                    long long kv_stride, long long layer_off, int max_ctx, bf16* o, cudaStream_t st,
                    const bf16* emb = nullptr, const int* out_tok = nullptr, const TmaMap* kmap = nullptr,
-                   const TmaMap* vmap = nullptr);
+                   const TmaMap* vmap = nullptr, const bf16* wo_blk = nullptr);
 
 // LM head over selected rows: logits = bf16(rmsnorm(x[sel[i]]) * g) . W^T,
 // fused greedy statistics; the last CTA merges the per-slice partials and
