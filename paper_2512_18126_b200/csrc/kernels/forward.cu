@@ -1430,6 +1430,7 @@ __device__ __forceinline__ long long kv_smem_index_t(int key, int d, int swz) {
 // K, one transpose-reduce), applies RoPE, appends k/v at the row's position
 // and runs the group's attention (warps split the keys, online softmax,
 // smem combine).  Replaces two launches and the q round trip through HBM.
+constexpr int kQkvOprojMaxD = 1024;
 template <int HD, int HPG>
 __global__ void __launch_bounds__(256, 1)
 qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, float eps, int D,
@@ -1447,6 +1448,7 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
   __shared__ float cm_s[HPG], cl_s[HPG];
   __shared__ float red[NW];
   __shared__ __align__(8) unsigned long long wbar, obar;
+  __shared__ float recv_s[kQkvOprojMaxD];  // fused o-projection: slices pushed by the cluster
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = blockIdx.x, g = blockIdx.y;
   const int hpg = nh / nkv, ncol = (hpg + 2) * HD;
@@ -1476,6 +1478,9 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
     chain_mark(cst, 0);
   }
   const std::uint32_t obar_u = static_cast<std::uint32_t>(__cvta_generic_to_shared(&obar));
+  // fused o-projection: announce this CTA as started (DSMEM pushes into a
+  // cluster peer wait for this before the first remote store)
+  if (wo_blk) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(obar_u));
@@ -1848,8 +1853,10 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
     // forms its heads' contribution to every output column, pushes slice q of
     // it into CTA q's smem (DSMEM), and CTA q adds the slices in rank order
     // to the residual and writes its D / nkv columns
+    // (the receive slices are a dedicated static buffer: pushes need no
+    // barrier before them, only the one that publishes them)
     const int S = D / nkv;
-    float* recv = reinterpret_cast<float*>(dsm + 4096 + obytes);  // [nkv][S]
+    float* recv = recv_s;  // [nkv][S]
     __syncthreads();
     {
       std::uint32_t ok = 0;
@@ -1859,7 +1866,7 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
                      : "r"(obar_u)
                      : "memory");
     }
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every peer has started
     const int K8 = hpg * HD / 8;  // 16-byte chunks per Wo row
     const bf16* wob = reinterpret_cast<const bf16*>(dsm + 4096);
     for (int n = threadIdx.x; n < D; n += NW * 32) {
@@ -2201,8 +2208,8 @@ void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv,
   int kv_cap = qkv_attention_kv_cap(D, nh, nkv, hd, max_ctx);
   if (tma_kv) kv_cap = (kv_cap - 1024 / (hd * 4)) / 64 * 64;  // whole 64-key boxes after the 1 KB alignment pad
   const int smem = qkv_attention_smem(D, nh, nkv, hd) + kv_cap * hd * 4 + (tma_kv ? 1024 : 0);
-  if (wo_blk && 4096 + D * (nh / nkv) * hd * 2 + D * 4 > ((nh / nkv) + 2) * hd * D * 2)
-    wo_blk = nullptr;  // the Wo block and the receive slices must fit the weight slab
+  if (wo_blk && (4096 + D * (nh / nkv) * hd * 2 > ((nh / nkv) + 2) * hd * D * 2 || D > kQkvOprojMaxD))
+    wo_blk = nullptr;  // the Wo block must fit the weight slab, the slices the receive buffer
   static const CUtensorMap no_map{};
   const CUtensorMap& km = tma_kv ? *reinterpret_cast<const CUtensorMap*>(kmap) : no_map;
   const CUtensorMap& vm = tma_kv ? *reinterpret_cast<const CUtensorMap*>(vmap) : no_map;
