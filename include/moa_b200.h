@@ -69,20 +69,13 @@ int moa_engine_destroy(moa_engine* eng);
 /* Drops every request; weights and buffers stay resident. */
 int moa_engine_reset(moa_engine* eng);
 /* Kernel probes: CUDA events around every forward kernel (graphs bypassed)
- * with each launch's algorithmic bytes.  kind: 0 embed, 1 qkv, 2 attention,
- * 3 o-proj, 4 gate/up, 5 down, 6 lm-head, 7 persistent decode forward. */
+ * with each launch's algorithmic (unique) bytes and dense flops.  kind:
+ * decode regime (rows <= 16): 0 embed, 1 qkv GEMV, 2 per-row attention,
+ * 3 o-proj GEMV, 4 gate/up GEMV, 5 down GEMV, 6 LM head, 7 fused small-agent
+ * QKV + attention (+ o-proj); prefill regime: 8 tiled prompt attention,
+ * 9 qkv GEMM, 10 o-proj GEMM, 11 gate/up GEMM, 12 down GEMM.  flops may be NULL. */
 int moa_engine_probe(moa_engine* eng, int enable);
-int moa_engine_probe_stats(moa_engine* eng, int kind, int* launches, double* ms, double* bytes);
-/* Persistent decode forward of model `model`: enable (1) / disable (0) it, and
- * optionally a %globaltimer trace of its phases (8 stamps per phase per CTA;
- * *n receives phases * grid * 8; the last forward's stamps are copied to out
- * when out != NULL and cap suffices). */
-int moa_engine_megakernel(moa_engine* eng, int model, int enable, int trace);
-/* Cluster-resident small-agent forward (16-CTA cluster, ticks of <= 16 rows)
- * for model `model`: enable (1) / disable (0); returns UNSUPPORTED when the
- * model shape does not fit it. */
-int moa_engine_small_forward(moa_engine* eng, int model, int enable);
-int moa_engine_mk_trace(moa_engine* eng, int model, uint64_t* out, long long cap, long long* n);
+int moa_engine_probe_stats(moa_engine* eng, int kind, int* launches, double* ms, double* bytes, double* flops);
 
 /* ---- tree-partitioned serving over several GPUs (one process per GPU) ----
  * Rank 0 creates the id, the caller broadcasts it (e.g. torch.distributed),
@@ -135,7 +128,9 @@ int moa_busy(moa_engine* eng, int* busy);
  * fp32 softmax entropy).  Any pointer may be NULL. */
 int moa_read_output(moa_engine* eng, int layer, int position, int n, int32_t* tokens, float* logprobs,
                     float* entropy);
-int moa_read_logits(moa_engine* eng, int layer, int position, int k, float* logits /* [vocab] */);
+/* fp32 logits of output token k (keep_logits engines); cap = floats in
+ * `logits`, at least the agent model's vocab (else VALIDATION). */
+int moa_read_logits(moa_engine* eng, int layer, int position, int k, float* logits, int cap);
 int moa_agent_state(moa_engine* eng, int layer, int position, int* scheduled, int* decoded,
                     int* finished, int* cancelled);
 
@@ -184,6 +179,7 @@ typedef struct {
   double wall_ms;      /* host wall clock of the whole call            */
   double weight_bytes; /* weight bytes the forwards had to read        */
   double host_ms;      /* host time spent inside engine ticks          */
+  double host_wait_ms; /* of which: blocked on the GPU (staging ring)  */
 } moa_run_summary;
 
 typedef struct {
@@ -281,7 +277,6 @@ int moa_k_attention(uintptr_t q, uintptr_t rows, int R, uintptr_t meta, int nh, 
 int moa_k_noop(uintptr_t p, int ctas, uintptr_t stream); /* trivial PDL kernel: launch-chain cost probe */
 int moa_k_debug_trace(uintptr_t buf); /* debug: gemv_tc per-CTA clock stamps, 0 = off */
 int moa_k_chain_stamp(uintptr_t buf); /* debug: decode-chain per-CTA globaltimer stamps (stamp.cuh), 0 = off */
-int moa_k_debug_trace_small(uintptr_t buf); /* debug: small-agent forward per-CTA clock stamps, 0 = off */
 int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
 /* Hash-uniform weight init of a logical [rows][cols] tensor into a device row
  * layout (0 identity, 1 RoPE-pair interleave per hd rows, 2 even rows, 3 odd rows). */

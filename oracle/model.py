@@ -81,20 +81,41 @@ def tensor_scale(spec: ModelSpec, name: str) -> np.float32:
     return np.float32(s)
 
 
+def _init_chunk(out, s0, s1, base, scale):
+    with np.errstate(over="ignore"):
+        idx = np.arange(s0, s1, dtype=np.uint64)
+        bits = mix64_np(idx + np.uint64(base))
+        u = (bits >> np.uint64(40)).astype(np.float32) * np.float32(2.0 ** -23) - np.float32(1.0)
+        out[s0:s1] = bf16_round(u * scale)
+
+
 def init_tensor(spec: ModelSpec, name: str, rows: int, cols: int) -> np.ndarray:
-    """Hash-uniform bf16 weights (as fp32 values), logical [rows, cols]."""
+    """Hash-uniform bf16 weights (as fp32 values), logical [rows, cols].
+    Chunks are independent (element i depends only on base + i), so they are
+    generated on all host threads (numpy releases the GIL)."""
     base = hash_combine(hash_combine(spec.seed, fnv1a(spec.tag)), fnv1a(name))
     n = rows * cols
     out = np.empty(n, dtype=np.float32)
     scale = tensor_scale(spec, name)
-    step = 1 << 24
-    with np.errstate(over="ignore"):
-        for s0 in range(0, n, step):
-            idx = np.arange(s0, min(n, s0 + step), dtype=np.uint64)
-            bits = mix64_np(idx + np.uint64(base))
-            u = (bits >> np.uint64(40)).astype(np.float32) * np.float32(2.0 ** -23) - np.float32(1.0)
-            out[s0:s0 + len(idx)] = u * scale
-    return bf16_round(out).reshape(rows, cols)
+    step = 1 << 22
+    spans = [(s0, min(n, s0 + step)) for s0 in range(0, n, step)]
+    if len(spans) == 1:
+        _init_chunk(out, 0, n, base, scale)
+    else:
+        list(_pool().map(lambda sp: _init_chunk(out, sp[0], sp[1], base, scale), spans))
+    return out.reshape(rows, cols)
+
+
+_POOL = None
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=os.cpu_count() or 4)
+    return _POOL
 
 
 class Weights:
@@ -149,6 +170,16 @@ def logit_stats(logits: np.ndarray):
     lp = -np.log(S)
     ent = np.log(S) - T / S
     return tok.astype(np.int32), lp.astype(np.float32), ent.astype(np.float32)
+
+
+def _runs(rows):
+    """Maximal runs of rows of one agent at consecutive positions [i0, i1)."""
+    out, i0 = [], 0
+    for i in range(1, len(rows) + 1):
+        if i == len(rows) or rows[i][0] is not rows[i - 1][0] or rows[i][1] != rows[i - 1][1] + 1:
+            out.append((i0, i))
+            i0 = i
+    return out
 
 
 class AgentKV:
@@ -216,14 +247,23 @@ class CpuModel:
                 kv.k[l, :, p] = k[i]
                 kv.v[l, :, p] = v[i]
             o = np.empty((R, nh, hd), np.float32)
-            for i, (kv, p, _) in enumerate(rows):
-                K = kv.k[l, :, : p + 1]  # [nkv, p+1, hd]
-                V = kv.v[l, :, : p + 1]
-                qi = q[i].reshape(nkv, grp, hd)
-                s = np.einsum("kgd,ktd->kgt", qi, K) * scale
-                s = s - s.max(axis=-1, keepdims=True)
-                e = np.exp(s)
-                o[i] = (np.einsum("kgt,ktd->kgd", e, V) / e.sum(axis=-1, keepdims=True)).reshape(nh, hd)
+            for i0, i1 in _runs(rows):
+                kv, p1 = rows[i0][0], rows[i1 - 1][1] + 1
+                K = kv.k[l, :, :p1]  # [nkv, p1, hd]
+                V = kv.v[l, :, :p1]
+                for c0 in range(i0, i1, 256):  # causal attention of a run of consecutive positions
+                    c1 = min(i1, c0 + 256)
+                    n = c1 - c0
+                    qi = q[c0:c1].reshape(n, nkv, grp, hd).transpose(1, 0, 2, 3).reshape(nkv, n * grp, hd)
+                    s = np.matmul(qi, K.transpose(0, 2, 1)) * scale  # [nkv, n*grp, p1]
+                    s = s.reshape(nkv, n, grp, p1)
+                    mask = np.arange(p1)[None, :] > pos[c0:c1][:, None]  # [n, p1]
+                    s = np.where(mask[None, :, None, :], np.float32(-np.inf), s)
+                    s = s - s.max(axis=-1, keepdims=True)
+                    e = np.exp(s)
+                    e = e / e.sum(axis=-1, keepdims=True)
+                    oi = np.matmul(e.reshape(nkv, n * grp, p1), V)  # [nkv, n*grp, hd]
+                    o[c0:c1] = oi.reshape(nkv, n, grp, hd).transpose(1, 0, 2, 3).reshape(n, nh, hd)
             o = bf16_round(o.reshape(R, nh * hd))
             x = x + o @ L["wo"].T
             h2 = bf16_round(rmsnorm(x, sp.norm_eps))

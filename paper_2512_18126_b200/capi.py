@@ -71,7 +71,7 @@ class RunSummary(C.Structure):
     _fields_ = [("ticks", C.c_int), ("n_agents", C.c_int), ("n_evals", C.c_int), ("forwards", C.c_int),
                 ("tokens", C.c_longlong), ("decoded_tokens", C.c_longlong), ("rows", C.c_longlong),
                 ("e2e_ms", C.c_double), ("wall_ms", C.c_double), ("weight_bytes", C.c_double),
-                ("host_ms", C.c_double)]
+                ("host_ms", C.c_double), ("host_wait_ms", C.c_double)]
 
 
 class AgentRecordC(C.Structure):
@@ -105,13 +105,10 @@ _SIGS = {
     "moa_placement": ([C.c_int, C.c_int, _P(C.c_int), _P(C.c_int), C.c_int, _P(C.c_int)], C.c_int),
     "moa_k_debug_trace": ([C.c_size_t], C.c_int),
     "moa_k_noop": ([C.c_size_t, C.c_int, C.c_size_t], C.c_int),
-    "moa_k_debug_trace_small": ([C.c_size_t], C.c_int),
     "moa_k_chain_stamp": ([C.c_size_t], C.c_int),
     "moa_engine_probe": ([C.c_void_p, C.c_int], C.c_int),
-    "moa_engine_megakernel": ([C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
-    "moa_engine_small_forward": ([C.c_void_p, C.c_int, C.c_int], C.c_int),
-    "moa_engine_mk_trace": ([C.c_void_p, C.c_int, _P(C.c_uint64), C.c_longlong, _P(C.c_longlong)], C.c_int),
-    "moa_engine_probe_stats": ([C.c_void_p, C.c_int, _P(C.c_int), _P(C.c_double), _P(C.c_double)], C.c_int),
+    "moa_engine_probe_stats": ([C.c_void_p, C.c_int, _P(C.c_int), _P(C.c_double), _P(C.c_double), _P(C.c_double)],
+                               C.c_int),
     "moa_add_agent": ([C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_int),
     "moa_prefill_only": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_int32), C.c_int], C.c_int),
     "moa_generate": ([C.c_void_p, C.c_int, C.c_int, _P(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
@@ -121,7 +118,7 @@ _SIGS = {
     "moa_busy": ([C.c_void_p, _P(C.c_int)], C.c_int),
     "moa_read_output": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_int32), _P(C.c_float), _P(C.c_float)],
                         C.c_int),
-    "moa_read_logits": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_float)], C.c_int),
+    "moa_read_logits": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_float), C.c_int], C.c_int),
     "moa_agent_state": ([C.c_void_p, C.c_int, C.c_int] + [_P(C.c_int)] * 4, C.c_int),
     "moa_engine_trace": ([C.c_void_p, C.c_int], C.c_int),
     "moa_engine_mark_start": ([C.c_void_p], C.c_int),
@@ -263,9 +260,10 @@ class Engine:
         check(lib().moa_read_output(self.h, a[0], a[1], n, tok, lp, ent))
         return list(tok[:n]), list(lp[:n]), list(ent[:n])
 
-    def read_logits(self, a, k, vocab=50000):
+    def read_logits(self, a, k):
+        vocab = self.models[self.record(a)["model"]].vocab
         buf = (C.c_float * vocab)()
-        check(lib().moa_read_logits(self.h, a[0], a[1], k, buf))
+        check(lib().moa_read_logits(self.h, a[0], a[1], k, buf, vocab))
         import numpy as np
         return np.ctypeslib.as_array(buf).copy()
 
@@ -308,32 +306,20 @@ class Engine:
         check(lib().moa_engine_attach_loopback(self.h, hub.h, rank))
         self._hub = hub  # keep the hub alive as long as the engine
 
-    PROBE_KINDS = ("embed", "qkv", "attention", "o_proj", "gate_up", "down", "lm_head", "decode_mk", "small_fwd")
+    # include/moa_b200.h moa_engine_probe_stats: decode-regime kinds, then prefill-regime kinds
+    PROBE_KINDS = ("embed", "qkv", "attn_decode", "o_proj", "gate_up", "down", "lm_head", "qkv_attn",
+                   "attn_prefill", "pf_qkv", "pf_o_proj", "pf_gate_up", "pf_down")
+    PREFILL_KINDS = ("attn_prefill", "pf_qkv", "pf_o_proj", "pf_gate_up", "pf_down")
 
     def probe(self, enable: bool):
         check(lib().moa_engine_probe(self.h, int(enable)))
 
-    def megakernel(self, model: int, enable: bool = True, trace: bool = False):
-        check(lib().moa_engine_megakernel(self.h, model, int(enable), int(trace)))
-
-    def small_forward(self, model: int, enable: bool = True):
-        check(lib().moa_engine_small_forward(self.h, model, int(enable)))
-
-    def mk_trace(self, model: int):
-        """Last persistent-forward trace of `model`: uint64 [phases][grid][8] %globaltimer ns."""
-        import numpy as np
-        n = C.c_longlong()
-        check(lib().moa_engine_mk_trace(self.h, model, None, 0, C.byref(n)))
-        buf = np.zeros(n.value, dtype=np.uint64)
-        check(lib().moa_engine_mk_trace(self.h, model, buf.ctypes.data_as(_P(C.c_uint64)), n.value, C.byref(n)))
-        return buf
-
     def probe_stats(self):
         out = {}
         for k, name in enumerate(self.PROBE_KINDS):
-            n, ms, b = C.c_int(), C.c_double(), C.c_double()
-            check(lib().moa_engine_probe_stats(self.h, k, C.byref(n), C.byref(ms), C.byref(b)))
-            out[name] = {"launches": n.value, "ms": ms.value, "bytes": b.value}
+            n, ms, b, f = C.c_int(), C.c_double(), C.c_double(), C.c_double()
+            check(lib().moa_engine_probe_stats(self.h, k, C.byref(n), C.byref(ms), C.byref(b), C.byref(f)))
+            out[name] = {"launches": n.value, "ms": ms.value, "bytes": b.value, "flops": f.value}
         return out
 
     # --- run_query ---

@@ -252,40 +252,15 @@ int moa_engine_probe(moa_engine* eng, int enable) {
   return guard([&] { E(eng).set_probing(enable != 0); });
 }
 
-int moa_engine_megakernel(moa_engine* eng, int model, int enable, int trace) {
-  return guard([&] {
-    if (model < 0 || model >= E(eng).n_models()) throw moa::ValidationError("engine: model index out of range");
-    MOA_CUDA(cudaStreamSynchronize(E(eng).stream()));
-    E(eng).model(model).set_megakernel(enable != 0);
-    E(eng).model(model).set_mk_trace(trace != 0);
-  });
-}
-
-int moa_engine_small_forward(moa_engine* eng, int model, int enable) {
-  return guard([&] {
-    if (model < 0 || model >= E(eng).n_models()) throw moa::ValidationError("engine: model index out of range");
-    if (enable && !E(eng).model(model).small_forward_ready())
-      throw moa::UnsupportedError("engine: the small-agent forward does not fit this model shape");
-    MOA_CUDA(cudaStreamSynchronize(E(eng).stream()));
-    E(eng).model(model).set_small_forward(enable != 0);
-  });
-}
-
-int moa_engine_mk_trace(moa_engine* eng, int model, uint64_t* out, long long cap, long long* n) {
-  return guard([&] {
-    need(n, "n");
-    if (model < 0 || model >= E(eng).n_models()) throw moa::ValidationError("engine: model index out of range");
-    MOA_CUDA(cudaStreamSynchronize(E(eng).stream()));
-    *n = E(eng).model(model).mk_trace_copy(reinterpret_cast<unsigned long long*>(out), cap);
-  });
-}
-
-int moa_engine_probe_stats(moa_engine* eng, int kind, int* launches, double* ms, double* bytes) {
+int moa_engine_probe_stats(moa_engine* eng, int kind, int* launches, double* ms, double* bytes, double* flops) {
   return guard([&] {
     need(launches, "launches");
     need(ms, "ms");
     need(bytes, "bytes");
-    E(eng).probe_stats(kind, launches, ms, bytes);
+    if (kind < 0 || kind >= moa::KernelProbes::kKinds) throw moa::ValidationError("probe kind out of range");
+    double f = 0.0;
+    E(eng).probe_stats(kind, launches, ms, bytes, &f);
+    if (flops) *flops = f;
   });
 }
 
@@ -346,12 +321,16 @@ int moa_read_output(moa_engine* eng, int layer, int position, int n, int32_t* to
   });
 }
 
-int moa_read_logits(moa_engine* eng, int layer, int position, int k, float* logits) {
+int moa_read_logits(moa_engine* eng, int layer, int position, int k, float* logits, int cap) {
   return guard([&] {
     need(logits, "logits");
     moa::GpuEngine& g = E(eng);
     const moa::AgentId id{layer, position};
     if (k < 0 || k >= g.decoded(id)) throw moa::ValidationError("read_logits: token index out of range");
+    const int vocab = g.model(g.record(id).model).spec().vocab;
+    if (cap < vocab)
+      throw moa::ValidationError("read_logits: buffer of " + std::to_string(cap) + " floats < vocab " +
+                                 std::to_string(vocab));
     g.read_logits(id, k, logits);
   });
 }
@@ -387,6 +366,7 @@ int moa_run_query(moa_engine* eng, const moa_run_config* cfg, int sample, int re
       summary->wall_ms = r.wall_ms;
       summary->weight_bytes = r.weight_bytes;
       summary->host_ms = r.host_ms;
+      summary->host_wait_ms = r.host_wait_ms;
     }
     if (out) *out = q.release();
   });
@@ -414,6 +394,7 @@ int moa_run_batch(moa_engine* eng, const moa_run_config* cfg, const int* samples
         s.wall_ms = r.wall_ms;
         s.weight_bytes = r.weight_bytes;
         s.host_ms = r.host_ms;
+        s.host_wait_ms = r.host_wait_ms;
       }
       if (out) {
         auto q = std::make_unique<moa_query>();
@@ -819,10 +800,6 @@ int moa_k_chain_stamp(uintptr_t buf) {
     moa::k::forward_chain_stamp(reinterpret_cast<unsigned long long*>(buf));
     moa::k::gemv_tc_chain_stamp(reinterpret_cast<unsigned long long*>(buf));
   });
-}
-
-int moa_k_debug_trace_small(uintptr_t buf) {
-  return guard([&] { moa::k::small_forward_debug_trace(reinterpret_cast<unsigned long long*>(buf)); });
 }
 
 int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream) {

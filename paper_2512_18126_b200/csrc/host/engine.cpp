@@ -83,8 +83,6 @@ GpuEngine::GpuEngine(std::vector<ModelSpec> models, std::vector<int> agents_per_
     }
   run_par_.assign(models_.size(), 0);
   if (const char* e = std::getenv("MOA_DECODE_RUN")) max_run_ = std::max(1, std::min(DeviceModel::kMaxRun, std::atoi(e)));
-  // two persistent (cooperative, one CTA per SM) forwards must never run side by side
-  if (const char* e = std::getenv("MOA_MK")) overlap_models_ = std::string(e) == "0";
   if (const char* e = std::getenv("MOA_OVERLAP")) overlap_models_ = overlap_models_ && std::string(e) != "0";
   MOA_CUDA(cudaStreamSynchronize(stream_));
 }
@@ -151,6 +149,17 @@ void GpuEngine::add_agent(const AgentId& id, int model, int owner) {
   order_.push_back(id);
 }
 
+// Literal token ids index the model's embedding table on the device: reject
+// anything outside [0, vocab) (negative ids are the engine's own symbolic
+// references to decoded tokens, created only by the host orchestrator).
+void GpuEngine::check_tokens(const Req& r, const TokenSeq& tokens, std::size_t from) const {
+  const int vocab = models_[static_cast<std::size_t>(r.model)]->spec().vocab;
+  for (std::size_t i = from; i < tokens.size(); ++i)
+    if (tokens[i] >= vocab)
+      throw ValidationError("engine: token " + std::to_string(tokens[i]) + " of agent " + r.id.str() +
+                            " outside the model's vocabulary [0, " + std::to_string(vocab) + ")");
+}
+
 // pdsim.cpp:155-174
 void GpuEngine::submit_prefill_only(const AgentId& id, int expected_start, const TokenSeq& tokens) {
   Req& r = req(id);
@@ -164,6 +173,7 @@ void GpuEngine::submit_prefill_only(const AgentId& id, int expected_start, const
   if (tokens.empty()) return;
   if (sched + static_cast<int>(tokens.size()) > opt_.max_ctx)
     throw ValidationError("engine: prompt of " + id.str() + " exceeds max_ctx");
+  check_tokens(r, tokens, 0);
   r.prompt.insert(r.prompt.end(), tokens.begin(), tokens.end());
   r.rec.prefill_only_calls += 1;
   r.queue.push_back(Job{sched, sched + static_cast<int>(tokens.size())});
@@ -183,6 +193,7 @@ void GpuEngine::submit_generate(const AgentId& id, const TokenSeq& full, int max
   if (max_new > opt_.max_out) throw ValidationError("engine: max_new exceeds max_out");
   if (static_cast<int>(full.size()) + max_new > opt_.max_ctx)
     throw ValidationError("engine: prompt + output of " + id.str() + " exceeds max_ctx");
+  check_tokens(r, full, static_cast<std::size_t>(sched));
   r.prompt = full;
   r.max_new = max_new;
   r.apc = apc_chunk;
@@ -271,7 +282,7 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   std::memcpy(s.host + sb, rows.data(), rb);
   const int L = dm.max_logit_rows();
   int max_pos = 0;
-  long long keys = 0;
+  TickStats ts;
   bool distinct = rows.size() <= 64;  // every row a different agent (pure decode)?
   int runs = 0, singles = 0;           // maximal same-agent runs of consecutive positions; runs of one row
   auto joined = [&](std::size_t i) {    // rows i - 1 and i are one run
@@ -280,11 +291,19 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
   for (std::size_t i = 0; i < rows.size(); ++i) {
     const auto& rd = rows[i];
     max_pos = std::max(max_pos, rd.pos);
-    keys += rd.pos + 1;
+    ts.keys += rd.pos + 1;
     for (std::size_t j = 0; j < i && distinct; ++j) distinct = rows[j].kv != rd.kv;
     runs += !joined(i);
-    singles += !joined(i) && !joined(i + 1);
+    const bool single = !joined(i) && !joined(i + 1);
+    singles += single;
+    if (single) {
+      ts.single_keys += rd.pos + 1;
+    } else {
+      ts.run_pairs += rd.pos + 1;
+      if (!joined(i + 1)) ts.run_keys += rd.pos + 1;  // last row of its run: the run's key prefix
+    }
   }
+  ts.singles = singles;
   // prompt-prefill tick: long same-agent runs -> tiled prefill attention (below
   // ~512 rows the per-row kernel's CTA count wins: measured on C1's
   // aggregator chunk ticks)
@@ -318,7 +337,7 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
     MOA_CUDA(cudaEventRecord(s.done, st));
   }
   float* logits = (opt_.keep_logits && !lsel.empty()) ? logits_scratch_ : nullptr;
-  dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), max_pos, keys, out_tok_, out_tok_,
+  dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), max_pos, ts, out_tok_, out_tok_,
              out_lp_, out_ent_, logits, st, distinct, prefill, singles > 0);
   if (logits) {  // debug path: scatter each logits row to its (slot, k) home
     const long long V = dm.spec().vocab;
@@ -736,10 +755,10 @@ void GpuEngine::set_probing(bool on) {
   for (auto& m : models_) m->attach_probes(on ? &probes_ : nullptr);
 }
 
-void GpuEngine::probe_stats(int kind, int* count, double* ms, double* bytes) {
+void GpuEngine::probe_stats(int kind, int* count, double* ms, double* bytes, double* flops) {
   MOA_CUDA(cudaStreamSynchronize(stream_));
   int n = 0;
-  double t = 0.0, b = 0.0;
+  double t = 0.0, b = 0.0, f = 0.0;
   for (const auto& r : probes_.recs) {
     if (r.kind != kind) continue;
     float e = 0.f;
@@ -747,10 +766,12 @@ void GpuEngine::probe_stats(int kind, int* count, double* ms, double* bytes) {
     ++n;
     t += e;
     b += r.bytes;
+    f += r.flops;
   }
   *count = n;
   *ms = t;
   *bytes = b;
+  *flops = f;
 }
 
 void GpuEngine::mark_start() { MOA_CUDA(cudaEventRecord(start_ev_, stream_)); }

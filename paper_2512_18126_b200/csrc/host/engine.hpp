@@ -126,7 +126,7 @@ class GpuEngine {
   int n_models() const { return static_cast<int>(models_.size()); }
   // Kernel probes (bench roofline): attach to every model; stats after a run.
   void set_probing(bool on);
-  void probe_stats(int kind, int* count, double* ms, double* bytes);
+  void probe_stats(int kind, int* count, double* ms, double* bytes, double* flops);
   // Pooled early-exit evaluator #i (device buffers reused across requests).
   GpuMetricQ& ee_evaluator(int i, int hidden, std::uint64_t seed, double tau, bool diag, int members,
                            int max_tokens);
@@ -171,6 +171,7 @@ class GpuEngine {
   Req& req(const AgentId& id);
   const Req& req(const AgentId& id) const;
   void start_decode(Req& r, int n_out);
+  void check_tokens(const Req& r, const TokenSeq& tokens, std::size_t from) const;
   void upload_and_forward(int m, const std::vector<k::RowDesc>& rows, const std::vector<int>& lsel,
                           const std::vector<int>& lout, cudaStream_t st);
   void upload_and_forward_run(int m, int K, const std::vector<k::RowDesc>& rows, const std::vector<int>& lout,

@@ -171,8 +171,7 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
     const char* e = std::getenv("MOA_FUSE_O");
     const int hpg = s.n_heads / s.n_kv_heads;
     const long long blk = static_cast<long long>(D) * hpg * hd;
-    if (qkv_attn_ok_ && !(e && e[0] == '0') && D % s.n_kv_heads == 0 && s.n_kv_heads <= 8 &&
-        4096 + blk * 2 + D * 4 <= static_cast<long long>(hpg + 2) * hd * D * 2) {
+    if (qkv_attn_ok_ && !(e && e[0] == '0') && k::qkv_oproj_supported(D, s.n_heads, s.n_kv_heads, static_cast<int>(hd))) {
       dev_alloc(&wo_blk_, blk * s.n_kv_heads * s.n_layers);
       for (int l = 0; l < s.n_layers; ++l)
         for (int gq = 0; gq < s.n_kv_heads; ++gq)
@@ -205,89 +204,6 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
     use_nfold_ = D <= 2048;
     if (const char* e = std::getenv("MOA_NORM_FOLD")) use_nfold_ = std::string(e) != "0";
   }
-  // persistent decode forward: tensor maps in device memory + its scratch
-  mk_ok_ = tc_ok_ && k::decode_mk_supported(D, s.n_heads, s.n_kv_heads, hd, s.ffn) && max_rows >= k::kMkRows;
-  if (mk_ok_) {
-    int dev = 0;
-    MOA_CUDA(cudaGetDevice(&dev));
-    MOA_CUDA(cudaDeviceGetAttribute(&mk_grid_, cudaDevAttrMultiProcessorCount, dev));
-    std::vector<k::TmaMap> maps;
-    for (const LayerMaps& m : wmaps_) {
-      maps.push_back(m.wqkv);
-      maps.push_back(m.wo);
-      maps.push_back(m.wgu);
-      maps.push_back(m.wd);
-    }
-    maps.push_back(wmap_lm_);
-    MOA_CUDA(cudaMalloc(&mk_maps_, sizeof(k::TmaMap) * maps.size()));
-    MOA_CUDA(cudaMemcpyAsync(mk_maps_, maps.data(), sizeof(k::TmaMap) * maps.size(), cudaMemcpyHostToDevice, st));
-    const int R = k::kMkRows;
-    dev_alloc(&mk_ssq_, static_cast<long long>(R) * (D / 128));
-    dev_alloc(&mk_ws_, k::decode_mk_ws_floats(mk_grid_));
-    const int max_tiles = (std::max({s.vocab, 2 * s.ffn, s.qkv_cols(), s.d}) + 127) / 128;
-    dev_alloc(&mk_cnt_, max_tiles);
-    MOA_CUDA(cudaMemsetAsync(mk_cnt_, 0, sizeof(int) * max_tiles, st));
-    mk_attn_splits_ = k::decode_mk_attn_splits(hd, max_ctx);
-    dev_alloc(&mk_attn_ws_, static_cast<long long>(R) * s.n_heads * mk_attn_splits_ * (2 + hd));
-    dev_alloc(&mk_attn_cnt_, static_cast<long long>(R) * s.n_kv_heads);
-    MOA_CUDA(cudaMemsetAsync(mk_attn_cnt_, 0, sizeof(int) * R * s.n_kv_heads, st));
-    dev_alloc(&mk_lm_part_, static_cast<long long>(R) * ((s.vocab + 127) / 128));
-    dev_alloc(&mk_lm_cnt_, 1);
-    MOA_CUDA(cudaMemsetAsync(mk_lm_cnt_, 0, sizeof(int), st));
-    dev_alloc(&mk_gbar_, 2);
-    MOA_CUDA(cudaMemsetAsync(mk_gbar_, 0, sizeof(unsigned) * 2, st));
-    k::MkParams pp;
-    pp.L = s.n_layers;
-    pp.D = s.d;
-    pp.nh = s.n_heads;
-    pp.nkv = s.n_kv_heads;
-    pp.hd = s.head_dim;
-    pp.ffn = s.ffn;
-    pp.V = s.vocab;
-    std::vector<k::MkCtaPlan> plan;
-    mk_ok_ = k::decode_mk_plan(pp, mk_grid_, &plan, &mk_xs_kt_, &mk_stages_, &mk_smem_);
-    if (mk_ok_) {
-      MOA_CUDA(cudaMalloc(&mk_plan_, sizeof(k::MkCtaPlan) * plan.size()));
-      MOA_CUDA(cudaMemcpyAsync(mk_plan_, plan.data(), sizeof(k::MkCtaPlan) * plan.size(), cudaMemcpyHostToDevice, st));
-      MOA_CUDA(cudaStreamSynchronize(st));
-    }
-    if (const char* e = std::getenv("MOA_MK_STAGES")) mk_stages_ = std::min(mk_stages_, std::max(2, std::atoi(e)));
-  }
-  // cluster-resident forward for small agents
-  {
-    k::SmallParams& sp = small_;
-    sp.L = s.n_layers;
-    sp.D = s.d;
-    sp.nh = s.n_heads;
-    sp.nkv = s.n_kv_heads;
-    sp.hd = s.head_dim;
-    sp.ffn = s.ffn;
-    sp.eps = static_cast<float>(s.norm_eps);
-    sp.rows = buf_.rows;
-    sp.meta = buf_.sel + 2 * max_lrows_;
-    sp.emb = emb_;
-    sp.g = ones_;
-    sp.rope = rope_;
-    sp.kpool = kpool_;
-    sp.vpool = vpool_;
-    sp.kv_stride = kv_stride_;
-    sp.layer_stride = layer_stride_;
-    sp.max_ctx = max_ctx_;
-    sp.w0 = layers_[0].wqkv;
-    sp.wstride = layers_.size() > 1 ? layers_[1].wqkv - layers_[0].wqkv : 0;
-    sp.off_o = layers_[0].wo - layers_[0].wqkv;
-    sp.off_gu = layers_[0].wgu - layers_[0].wqkv;
-    sp.off_d = layers_[0].wd - layers_[0].wqkv;
-    sp.x_out = x_;
-    small_ok_ = max_rows >= k::kMkRows && k::small_forward_supported(sp);
-    cudaGetLastError();
-    // opt-in (MOA_SMALL=1): faster than the kernel chain in isolation, not yet end to end
-    use_small_ = false;
-    if (const char* e = std::getenv("MOA_SMALL")) use_small_ = std::string(e) != "0";
-  }
-  // persistent forward: opt-in (MOA_MK=1) until it beats the per-kernel chain
-  use_mk_ = false;
-  if (const char* e = std::getenv("MOA_MK")) use_mk_ = std::string(e) != "0";
   MOA_CUDA(cudaMemsetAsync(gv_cnt_, 0, sizeof(int) * ((std::max({s.qkv_cols(), 2 * s.ffn, s.d}) + 127) / 128), st));
   MOA_CUDA(cudaGetLastError());
 }
@@ -306,10 +222,7 @@ DeviceModel::~DeviceModel() {
                     static_cast<void*>(h_), static_cast<void*>(q_), static_cast<void*>(attn_ws_),
                     static_cast<void*>(attn_cnt_), static_cast<void*>(part_), static_cast<void*>(lm_cnt_),
                     meta_blob_, run_area_, static_cast<void*>(hn_), static_cast<void*>(wo_blk_),
-                    static_cast<void*>(gv_ws_), static_cast<void*>(gv_cnt_), static_cast<void*>(ssq_), mk_maps_, static_cast<void*>(mk_ssq_),
-                    static_cast<void*>(mk_ws_), static_cast<void*>(mk_cnt_), static_cast<void*>(mk_attn_ws_),
-                    static_cast<void*>(mk_attn_cnt_), static_cast<void*>(mk_lm_part_), static_cast<void*>(mk_lm_cnt_),
-                    static_cast<void*>(mk_gbar_), static_cast<void*>(mk_trace_), static_cast<void*>(mk_plan_)})
+                    static_cast<void*>(gv_ws_), static_cast<void*>(gv_cnt_), static_cast<void*>(ssq_)})
     if (ptr) cudaFree(ptr);
 }
 
@@ -328,8 +241,8 @@ cudaEvent_t KernelProbes::event() {
   return pool[next++];
 }
 
-void KernelProbes::begin(int kind, double bytes, cudaStream_t st) {
-  Rec r{kind, bytes, event(), event()};
+void KernelProbes::begin(int kind, double bytes, cudaStream_t st, double flops) {
+  Rec r{kind, bytes, flops, event(), event()};
   MOA_CUDA(cudaEventRecord(r.a, st));
   recs.push_back(r);
 }
@@ -348,7 +261,7 @@ int pow2_at_least(int v, int lo) {
 }
 }  // namespace
 
-void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int* out_tok_read, int* out_tok,
+void DeviceModel::forward(int R, int Rl, int max_pos, const TickStats& ts, const int* out_tok_read, int* out_tok,
                           float* out_lp, float* out_ent, float* logits, cudaStream_t st, bool distinct, bool prefill,
                           bool singles) {
   // (tensor-core ticks only: the GEMV-only path keeps every row's attention in
@@ -365,11 +278,11 @@ void DeviceModel::forward(int R, int Rl, int max_pos, long long keys, const int*
   if (!use_graphs_ || probes_) {
     live_R_ = R;
     live_Rl_ = Rl;
-    live_keys_ = keys;
+    live_ = ts;
     launch(rcap, nsplit, Rl > 0, out_tok_read, out_tok, out_lp, out_ent, logits, st, distinct, prefill, singles);
     return;
   }
-  const auto key = std::make_tuple(rcap, nsplit, (Rl > 0 ? 1 : 0) | (use_tc_ ? 2 : 0) | (use_mk_ ? 4 : 0) |
+  const auto key = std::make_tuple(rcap, nsplit, (Rl > 0 ? 1 : 0) | (use_tc_ ? 2 : 0) |
                                                      (distinct ? 8 : 0) | (blob_ << 4) | (prefill ? 32 : 0) |
                                                      (prefill && !singles ? 64 : 0),
                                    logits ? 1 : 0);
@@ -395,7 +308,7 @@ void DeviceModel::forward_run(int K, int R, int max_pos, const int* out_tok_read
   const int rcap = std::min(pow2_at_least(R, 8), max_rows_);
   const int ks = k::kv_split(spec_.head_dim);
   const int nsplit = pow2_at_least((max_pos + ks) / ks, 1);  // the last tick's: a cap for the earlier ones
-  const auto key = std::make_tuple(rcap, nsplit, 1 | (use_tc_ ? 2 : 0) | (use_mk_ ? 4 : 0) | 8 | (parity << 4),
+  const auto key = std::make_tuple(rcap, nsplit, 1 | (use_tc_ ? 2 : 0) | 8 | (parity << 4),
                                    2 * K);
   auto it = graphs_.find(key);
   if (it == graphs_.end()) {
@@ -425,11 +338,6 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   const int D = s.d, hd = s.head_dim, nh = s.n_heads, nkv = s.n_kv_heads;
   const float eps = static_cast<float>(s.norm_eps);
   const int* meta = buf_.sel + 2 * max_lrows_;
-  if (use_mk_ && use_tc_ && mk_ok_ && rcap <= k::kMkRows) {
-    launch_mk(out_tok_read, out_tok, out_lp, out_ent, logits, st);
-    return;
-  }
-  const bool small = use_small_ && use_tc_ && small_ok_ && rcap <= k::kMkRows;
   // tensor-core path for row buckets >= kTcMinRows (prefill-heavy ticks)
   const bool tc = use_tc_ && tc_ok_ && rcap >= k::kTcMinRows;
   // decode ticks of large models: swap-AB tensor-core GEMV (pure weight stream)
@@ -460,35 +368,33 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     else
       k::gemm_tc(*map_a, map_w, g, st);
   };
-  auto probe_begin = [&](int kind, double bytes) {
-    if (probes_) probes_->begin(kind, bytes, st);
+  // probes: decode-regime launches (rows <= 16) and prefill-regime ones
+  // (tcgen05 GEMM / tiled attention) are separate kinds; bytes are the
+  // launch's algorithmic (unique) bytes, flops its dense flops
+  auto probe_begin = [&](int kind, double bytes, double flops = 0.0) {
+    if (probes_) probes_->begin(kind, bytes, st, flops);
   };
+  auto gkind = [&](int dec, int pf) { return tc ? pf : dec; };
+  const double Rv = live_R_;
   auto probe_end = [&]() {
     if (probes_) probes_->end(st);
   };
   // decode ticks of small agents: (embedding gather +) RMSNorm + QKV + RoPE + KV
   // append + attention in one launch per layer
-  const bool qkv_attn = !small && use_tc_ && use_qkv_attn_ && qkv_attn_ok_ && distinct && rcap <= k::kGemvTcRows;
+  const bool qkv_attn = use_tc_ && use_qkv_attn_ && qkv_attn_ok_ && distinct && rcap <= k::kGemvTcRows;
   const bool fuse_o = qkv_attn && wo_blk_ != nullptr;
-  if (small) {
-    k::SmallParams sp = small_;
-    sp.out_tok_read = out_tok_read;
-    sp.rows = buf_.rows;
-    sp.meta = buf_.sel + 2 * max_lrows_;
-    const double kv_bytes = 4.0 * static_cast<double>(live_keys_) * nkv * hd * s.n_layers;
-    probe_begin(KernelProbes::SmallFwd, weight_bytes() - 2.0 * s.vocab * D + kv_bytes);
-    k::small_forward(sp, st);
-    probe_end();
-  } else if (!qkv_attn) {  // (the fused QKV + attention kernel gathers layer 0's embeddings itself)
+  if (!qkv_attn) {  // (the fused QKV + attention kernel gathers layer 0's embeddings itself)
   probe_begin(KernelProbes::Embed, 6.0 * live_R_ * D);
   k::embed(buf_.rows, rcap, meta, out_tok_read, emb_, D, x_, st, norm_fold ? ssq_ : nullptr);
   probe_end();
   }
-  for (int l = 0; l < (small ? 0 : s.n_layers); ++l) {
+  for (int l = 0; l < s.n_layers; ++l) {
     const Layer& L = layers_[static_cast<std::size_t>(l)];
     const long long loff = layer_stride_ * l;
     if (qkv_attn) {
-      probe_begin(KernelProbes::Attention, 2.0 * s.qkv_cols() * D + 4.0 * live_keys_ * nkv * hd + 4.0 * live_R_ * D);
+      // Wqkv (+ Wo when the o-projection is fused), every row's K/V prefix once, x in and out
+      probe_begin(KernelProbes::QkvAttn, 2.0 * s.qkv_cols() * D + (fuse_o ? 2.0 * D * nh * hd : 0.0) +
+                                             4.0 * live_.keys * nkv * hd + 8.0 * Rv * D);
       k::qkv_attention(x_, ones_, eps, D, L.wqkv, buf_.rows, rcap, meta, rope_, nh, nkv, hd, kpool_, vpool_, kv_stride_,
                        loff, max_ctx_, h_, st, l == 0 ? emb_ : nullptr, out_tok_read, kv_maps_ok_ ? &kmap_ : nullptr,
                        kv_maps_ok_ ? &vmap_ : nullptr, fuse_o ? wo_blk_ + static_cast<long long>(l) * D * nh * hd : nullptr);
@@ -516,18 +422,28 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     qkv.nh = nh;
     qkv.nkv = nkv;
     qkv.hd = hd;
-    probe_begin(KernelProbes::Qkv, 2.0 * qkv.N * qkv.K + 4.0 * live_R_ * D + 2.0 * live_R_ * qkv.N);
+    probe_begin(gkind(KernelProbes::Qkv, KernelProbes::PfQkv), 2.0 * qkv.N * qkv.K + 4.0 * Rv * D + 2.0 * Rv * qkv.N,
+                2.0 * Rv * qkv.N * qkv.K);
     run_gemm(qkv, nullptr, nullptr, wmaps_[static_cast<std::size_t>(l)].wqkv);
     probe_end();
-    probe_begin(KernelProbes::Attention, 4.0 * live_keys_ * nkv * hd + 4.0 * live_R_ * nh * hd);
-    // prompt-prefill ticks: runs of a prompt by the tiled kernel, the tick's
-    // decode rows (alone in their run) by the per-row kernel
-    if (prefill)
+    // prompt-prefill ticks: runs of a prompt by the tiled kernel (unique bytes:
+    // each run's key prefix once; flops: causal QK^T and PV), the tick's decode
+    // rows (alone in their run) by the per-row kernel (bytes: each row's prefix)
+    if (prefill) {
+      const double run_rows = Rv - static_cast<double>(live_.singles);
+      probe_begin(KernelProbes::AttnPrefill, 4.0 * live_.run_keys * nkv * hd + 4.0 * run_rows * nh * hd,
+                  4.0 * static_cast<double>(live_.run_pairs) * nh * hd);
       k::attention_prefill(q_, buf_.rows, rcap, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_, st);
-    if (!prefill || singles)
+      probe_end();
+    }
+    if (!prefill || singles) {
+      const double keys = prefill ? live_.single_keys : live_.keys, rows_n = prefill ? live_.singles : Rv;
+      probe_begin(KernelProbes::AttnDecode, 4.0 * keys * nkv * hd + 4.0 * rows_n * nh * hd,
+                  4.0 * keys * nh * hd);
       k::attention(q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_,
                    attn_ws_, attn_cnt_, st, prefill);
-    probe_end();
+      probe_end();
+    }
     }
     // x += o . Wo^T (folded into the fused QKV + attention kernel when fuse_o)
     if (!fuse_o) {
@@ -543,7 +459,8 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     // x was last written two kernels back, except when layer 0's fused kernel gathered it
     o.res_early = !(qkv_attn && l == 0);
     if (norm_fold) o.ssq_out = ssq_;
-    probe_begin(KernelProbes::OProj, 2.0 * o.N * o.K + 2.0 * live_R_ * o.K + 8.0 * live_R_ * D);
+    probe_begin(gkind(KernelProbes::OProj, KernelProbes::PfOProj), 2.0 * o.N * o.K + 2.0 * Rv * o.K + 8.0 * Rv * D,
+                2.0 * Rv * o.N * o.K);
     run_gemm(o, &map_h_attn_, &map_h_attn16_, wmaps_[static_cast<std::size_t>(l)].wo);
     probe_end();
     }
@@ -559,7 +476,8 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     gu.W = L.wgu;
     gu.epi = k::kEpiSwiGlu;
     gu.out_bf16 = h_;
-    probe_begin(KernelProbes::GateUp, 2.0 * gu.N * gu.K + 4.0 * live_R_ * D + 2.0 * live_R_ * s.ffn);
+    probe_begin(gkind(KernelProbes::GateUp, KernelProbes::PfGateUp), 2.0 * gu.N * gu.K + 4.0 * Rv * D + 2.0 * Rv * s.ffn,
+                2.0 * Rv * gu.N * gu.K);
     run_gemm(gu, nullptr, nullptr, wmaps_[static_cast<std::size_t>(l)].wgu);
     probe_end();
     // x += a . Wd^T
@@ -574,7 +492,8 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     dn.out = x_;
     dn.res_early = true;  // x was written by the o-projection, two kernels back
     if (norm_fold) dn.ssq_out = ssq_;
-    probe_begin(KernelProbes::Down, 2.0 * dn.N * dn.K + 2.0 * live_R_ * dn.K + 8.0 * live_R_ * D);
+    probe_begin(gkind(KernelProbes::Down, KernelProbes::PfDown), 2.0 * dn.N * dn.K + 2.0 * Rv * dn.K + 8.0 * Rv * D,
+                2.0 * Rv * dn.N * dn.K);
     run_gemm(dn, &map_h_ffn_, &map_h_ffn16_, wmaps_[static_cast<std::size_t>(l)].wd);
     probe_end();
   }
@@ -624,79 +543,6 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
 void DeviceModel::graphs_clear() {
   for (auto& [key, exec] : graphs_) cudaGraphExecDestroy(exec);
   graphs_.clear();
-}
-
-void DeviceModel::set_mk_trace(bool on) {
-  if (on && !mk_trace_ && mk_ok_) {
-    const long long n = static_cast<long long>(3 + 5 * spec_.n_layers) * mk_grid_ * 8;
-    dev_alloc(&mk_trace_, n);
-    MOA_CUDA(cudaMemset(mk_trace_, 0, sizeof(unsigned long long) * n));
-  } else if (!on && mk_trace_) {
-    cudaFree(mk_trace_);
-    mk_trace_ = nullptr;
-  }
-  graphs_clear();
-}
-
-long long DeviceModel::mk_trace_copy(unsigned long long* out, long long cap) {
-  if (!mk_trace_) return 0;
-  const long long n = static_cast<long long>(3 + 5 * spec_.n_layers) * mk_grid_ * 8;
-  if (out && cap >= n) MOA_CUDA(cudaMemcpy(out, mk_trace_, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
-  return n;
-}
-
-void DeviceModel::launch_mk(const int* out_tok_read, int* out_tok, float* out_lp, float* out_ent, float* logits,
-                            cudaStream_t st) {
-  const ModelSpec& s = spec_;
-  k::MkParams p;
-  p.maps = mk_maps_;
-  p.L = s.n_layers;
-  p.D = s.d;
-  p.nh = s.n_heads;
-  p.nkv = s.n_kv_heads;
-  p.hd = s.head_dim;
-  p.ffn = s.ffn;
-  p.V = s.vocab;
-  p.eps = static_cast<float>(s.norm_eps);
-  p.rows = buf_.rows;
-  p.meta = buf_.sel + 2 * max_lrows_;
-  p.sel = buf_.sel;
-  p.out_idx = buf_.sel + max_lrows_;
-  p.out_tok_read = out_tok_read;
-  p.emb = emb_;
-  p.g = ones_;
-  p.rope = rope_;
-  p.kpool = kpool_;
-  p.vpool = vpool_;
-  p.kv_stride = kv_stride_;
-  p.layer_stride = layer_stride_;
-  p.max_ctx = max_ctx_;
-  p.x = x_;
-  p.ssq = mk_ssq_;
-  p.q = q_;
-  p.o = h_;
-  p.h = h_;
-  p.ws = mk_ws_;
-  p.cnt = mk_cnt_;
-  p.attn_ws = mk_attn_ws_;
-  p.attn_cnt = mk_attn_cnt_;
-  p.attn_nsplit_max = mk_attn_splits_;
-  p.lm_part = mk_lm_part_;
-  p.lm_cnt = mk_lm_cnt_;
-  p.out_tok = out_tok;
-  p.out_lp = out_lp;
-  p.out_ent = out_ent;
-  p.logits = logits;
-  p.gbar = mk_gbar_;
-  p.stages = mk_stages_;
-  p.xs_kt = mk_xs_kt_;
-  p.trace = mk_trace_;
-  p.plan = mk_plan_;
-  const double kv_bytes = 4.0 * static_cast<double>(live_keys_) * s.n_kv_heads * s.head_dim * s.n_layers;
-  if (probes_) probes_->begin(KernelProbes::DecodeMk, weight_bytes() + kv_bytes, st);
-  k::decode_mk(p, mk_grid_, mk_smem_, st);
-  if (probes_) probes_->end(st);
-  MOA_CUDA(cudaGetLastError());
 }
 
 }  // namespace moa

@@ -37,6 +37,14 @@ struct ModelSpec {
   void validate() const;
 };
 
+// Per-tick row statistics (host-computed; the probes' algorithmic bytes):
+// keys = sum over rows of (pos + 1); rows alone in their same-agent run
+// (decode rows) and their keys; multi-row runs' unique key prefixes
+// (sum of last pos + 1) and causal (row, key) pairs.
+struct TickStats {
+  long long keys = 0, singles = 0, single_keys = 0, run_keys = 0, run_pairs = 0;
+};
+
 struct ForwardBuffers {
   k::RowDesc* rows = nullptr;  // [max_rows], right after sel in one allocation
   int* sel = nullptr;  // [2 * max_logit_rows + 3]: logits row index, flat output index, meta {R, Rl, max_pos}
@@ -47,17 +55,23 @@ struct ForwardBuffers {
 // without graphs and every launch is bracketed by an event pair together with
 // its algorithmic bytes.
 struct KernelProbes {
-  enum Kind { Embed = 0, Qkv, Attention, OProj, GateUp, Down, LmHead, DecodeMk, SmallFwd, kKinds };
+  // decode-regime kinds (rows <= 16: swap-AB GEMVs, per-row attention, the
+  // fused small-agent kernel) and prefill-regime kinds (tcgen05 GEMM, tiled
+  // prompt attention) are kept apart: they have different rooflines
+  enum Kind {
+    Embed = 0, Qkv, AttnDecode, OProj, GateUp, Down, LmHead, QkvAttn, AttnPrefill, PfQkv, PfOProj, PfGateUp, PfDown,
+    kKinds
+  };
   struct Rec {
     int kind;
-    double bytes;
+    double bytes, flops;
     cudaEvent_t a, b;
   };
   std::vector<cudaEvent_t> pool;
   std::size_t next = 0;
   std::vector<Rec> recs;
   cudaEvent_t event();
-  void begin(int kind, double bytes, cudaStream_t st);
+  void begin(int kind, double bytes, cudaStream_t st, double flops = 0.0);
   void end(cudaStream_t st);
   void reset() {
     next = 0;
@@ -70,18 +84,6 @@ class DeviceModel {
  public:
   void attach_probes(KernelProbes* p) { probes_ = p; }
   void set_tensor_cores(bool on) { use_tc_ = on; }
-  void set_small_forward(bool on) {
-    use_small_ = on;
-    graphs_clear();
-  }
-  bool small_forward_ready() const { return small_ok_; }
-  void set_megakernel(bool on) {
-    use_mk_ = on;
-    graphs_clear();
-  }
-  void set_mk_trace(bool on);
-  long long mk_trace_copy(unsigned long long* out, long long cap);  // entries; copies when out && cap suffices
-  bool megakernel_ready() const { return mk_ok_; }
   bool tensor_cores_ready() const { return tc_ok_; }
   DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int max_rows, int max_logit_rows,
               cudaStream_t st, bool use_graphs = true);
@@ -113,7 +115,7 @@ class DeviceModel {
   // distinct: every row belongs to a different agent (a pure decode tick)
   // prefill: the rows are long same-agent runs (prompt prefill): tiled attention
   // (singles: some rows are alone in their run -- the per-row kernel serves them)
-  void forward(int R, int Rl, int max_pos, long long keys, const int* out_tok_read, int* out_tok, float* out_lp,
+  void forward(int R, int Rl, int max_pos, const TickStats& ts, const int* out_tok_read, int* out_tok, float* out_lp,
                float* out_ent, float* logits, cudaStream_t st, bool distinct = false, bool prefill = false,
                bool singles = true);
   // K ticks of R decode rows each (every row its own agent, one logits row per
@@ -141,29 +143,8 @@ class DeviceModel {
   // RMSNorm folded into the swap-AB decode GEMVs (qkv, gate/up)
   bool nfold_ok_ = false, use_nfold_ = true;
   float* ssq_ = nullptr;
-  // cluster-resident small-agent forward (small_fwd.cu) for ticks of <= 16 rows
-  bool use_small_ = true;
-  bool small_ok_ = false;
-  k::SmallParams small_;
-  // persistent decode forward (decode_mk.cu) for ticks of <= 16 rows
-  bool use_mk_ = true;
-  bool mk_ok_ = false;
-  int lm_grid_ = 148;
-  int mk_grid_ = 0, mk_stages_ = 0, mk_xs_kt_ = 0, mk_smem_ = 0;
-  void* mk_maps_ = nullptr;  // CUtensorMap[4L + 1]
-  float* mk_ssq_ = nullptr;
-  float* mk_ws_ = nullptr;
-  int* mk_cnt_ = nullptr;
-  float* mk_attn_ws_ = nullptr;
-  int* mk_attn_cnt_ = nullptr;
-  int mk_attn_splits_ = 0;
-  k::LmStat* mk_lm_part_ = nullptr;
-  int* mk_lm_cnt_ = nullptr;
-  unsigned* mk_gbar_ = nullptr;
-  unsigned long long* mk_trace_ = nullptr;
-  k::MkCtaPlan* mk_plan_ = nullptr;
+  int lm_grid_ = 148;  // persistent LM head: one CTA per SM
   void graphs_clear();
-  void launch_mk(const int* out_tok_read, int* out_tok, float* out_lp, float* out_ent, float* logits, cudaStream_t st);
   struct LayerMaps {
     k::TmaMap wqkv, wo, wgu, wd;
   };
@@ -179,7 +160,7 @@ class DeviceModel {
   k::bf16* hn_ = nullptr;                      // normalised rows for the tensor-core path
   KernelProbes* probes_ = nullptr;
   int live_R_ = 0, live_Rl_ = 0;
-  long long live_keys_ = 0;  // sum over rows of (pos + 1): attention K/V reads
+  TickStats live_;
   int bound_ = 0;
   // weights
   k::bf16* wbase_ = nullptr;

@@ -288,6 +288,7 @@ struct Request {
     res.rows = eng.rows_processed();
     res.forwards = eng.kernel_forwards();
     res.host_ms = eng.host_ms();
+    res.host_wait_ms = eng.host_wait_ms();
     if (!resolve) return;
     for (const AgentId& ea : drv.order()) {
       const AgentId a = ea.topo();

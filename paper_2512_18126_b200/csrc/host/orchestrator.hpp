@@ -72,7 +72,8 @@ struct QueryResult {
   double weight_bytes = 0.0;     // sum of per-forward weight reads
   long long rows = 0;
   int forwards = 0;
-  double host_ms = 0.0;  // host time inside engine ticks
+  double host_ms = 0.0;       // host time inside engine ticks
+  double host_wait_ms = 0.0;  // of which: blocked on the GPU (the host is ahead)
   // trace context (RunTrace JSONL, trace.hpp)
   std::vector<double> tick_ms;  // device ms at the end of each tick (engine tracing on)
   std::vector<std::string> model_tags;

@@ -2196,6 +2196,12 @@ bool qkv_attention_supported(int D, int nh, int nkv, int hd) {
          (((nh / nkv) + 2) * hd) % 32 == 0 && qkv_attention_smem(D, nh, nkv, hd) <= 160 * 1024;
 }
 
+bool qkv_oproj_supported(int D, int nh, int nkv, int hd) {
+  // the Wo block must fit the freed weight slab, the pushed slices the receive buffer
+  return qkv_attention_supported(D, nh, nkv, hd) && D % nkv == 0 && nkv <= 8 && D <= kQkvOprojMaxD &&
+         4096 + D * (nh / nkv) * hd * 2 <= ((nh / nkv) + 2) * hd * D * 2;
+}
+
 void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv, const RowDesc* rows, int R_cap,
                    const int* meta, const float2* rope, int nh, int nkv, int hd, bf16* kpool, bf16* vpool,
                    long long kv_stride, long long layer_off, int max_ctx, bf16* o, cudaStream_t st, const bf16* emb,
@@ -2208,8 +2214,11 @@ void qkv_attention(float* X, const float* g, float eps, int D, const bf16* wqkv,
   int kv_cap = qkv_attention_kv_cap(D, nh, nkv, hd, max_ctx);
   if (tma_kv) kv_cap = (kv_cap - 1024 / (hd * 4)) / 64 * 64;  // whole 64-key boxes after the 1 KB alignment pad
   const int smem = qkv_attention_smem(D, nh, nkv, hd) + kv_cap * hd * 4 + (tma_kv ? 1024 : 0);
-  if (wo_blk && (4096 + D * (nh / nkv) * hd * 2 > ((nh / nkv) + 2) * hd * D * 2 || D > kQkvOprojMaxD))
-    wo_blk = nullptr;  // the Wo block must fit the weight slab, the slices the receive buffer
+  if (wo_blk && !qkv_oproj_supported(D, nh, nkv, hd)) {
+    // the caller dropped its o-projection launch: silently skipping it here would lose the projection
+    std::fprintf(stderr, "qkv_attention: fused o-projection requested for an unsupported shape\n");
+    std::abort();
+  }
   static const CUtensorMap no_map{};
   const CUtensorMap& km = tma_kv ? *reinterpret_cast<const CUtensorMap*>(kmap) : no_map;
   const CUtensorMap& vm = tma_kv ? *reinterpret_cast<const CUtensorMap*>(vmap) : no_map;

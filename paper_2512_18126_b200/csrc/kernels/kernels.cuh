@@ -146,97 +146,6 @@ void gemv_tc_debug_trace(unsigned long long* buf);
 void lm_head_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, LmStat* part, int* cnt, int grid,
                 cudaStream_t st);  // per-CTA stamps [cta][8] (debug), nullptr = off
 
-// ---- persistent decode forward (decode_mk.cu): one launch per tick of <= 16
-// rows of a model, one CTA per SM (cooperative launch) ----
-constexpr int kMkRows = 16;
-constexpr int kMkMaxGroupDims = 512;  // (n_heads / n_kv_heads) * head_dim
-constexpr int kMkMaxSeg = 8;          // segments per CTA per GEMV shape
-constexpr int kMkMaxKt = 64;          // staged k-tiles per CTA per GEMV shape
-// One CTA's piece of a GEMV phase inside one 128-row weight tile: k-tiles
-// [k0, k1) of tile t; the CTAs c_first..c_last share the tile (split-K).
-struct MkSeg {
-  int t, k0, k1;
-  int slot_self;   // partial slot this CTA writes (0: first segment of its range, 1: last)
-  int c_first, c_last;
-  int first_slot;  // slot holding c_first's partial of this tile
-  int pad;
-};
-struct alignas(16) MkCtaPlan {
-  int nseg = 0, nkt = 0, pad0 = 0, pad1 = 0;
-  MkSeg seg[kMkMaxSeg];
-  short kt[kMkMaxKt];  // distinct k-tiles to stage, in first-use order
-};
-struct MkParams {
-  const void* maps;  // CUtensorMap[4L + 1] in device memory: per layer wqkv, wo, wgu, wd; then the LM head
-  int L = 0, D = 0, nh = 0, nkv = 0, hd = 0, ffn = 0, V = 0;
-  float eps = 1e-5f;
-  const RowDesc* rows = nullptr;
-  const int* meta = nullptr;     // [R, Rl, max_pos]
-  const int* sel = nullptr;      // logits rows [Rl]
-  const int* out_idx = nullptr;  // flat output index per logits row
-  const int* out_tok_read = nullptr;
-  const bf16* emb = nullptr;
-  const float* g = nullptr;  // norm gains
-  const float2* rope = nullptr;
-  bf16* kpool = nullptr;
-  bf16* vpool = nullptr;
-  long long kv_stride = 0, layer_stride = 0;
-  int max_ctx = 0;
-  float* x = nullptr;    // [16][D] fp32 residual stream
-  float* ssq = nullptr;  // [16][D/128] per-tile row sums of squares
-  bf16* q = nullptr;     // [16][nh*hd]
-  bf16* o = nullptr;     // [16][nh*hd] attention output
-  bf16* h = nullptr;     // [16][ffn] SwiGLU output
-  float* ws = nullptr;   // split-K partials [grid][2][128][16]
-  int* cnt = nullptr;    // [max tiles], zero-initialised once
-  float* attn_ws = nullptr;  // [16][nh][attn_nsplit_max][2 + hd]
-  int* attn_cnt = nullptr;   // [16][nkv], zero-initialised once
-  int attn_nsplit_max = 0;
-  LmStat* lm_part = nullptr;  // [16][ceil(V/128)]
-  int* lm_cnt = nullptr;
-  int* out_tok = nullptr;
-  float* out_lp = nullptr;
-  float* out_ent = nullptr;
-  float* logits = nullptr;
-  unsigned* gbar = nullptr;  // [2], zero-initialised once
-  const MkCtaPlan* plan = nullptr;  // [grid][5] (decode_mk_plan)
-  int stages = 0, xs_kt = 0;  // weight ring depth, activation staging slots (decode_mk_plan)
-  unsigned long long* trace = nullptr;  // optional [phases][grid][8] %globaltimer stamps (tools/mktrace.py)
-};
-long long decode_mk_ws_floats(int grid);
-int decode_mk_attn_splits(int hd, int max_ctx);
-bool decode_mk_supported(int d, int nh, int nkv, int hd, int ffn);
-bool decode_mk_plan(const MkParams& p, int grid, std::vector<MkCtaPlan>* plan, int* xs_kt, int* stages,
-                    int* smem_bytes);
-void decode_mk(const MkParams& p, int grid, int smem_bytes, cudaStream_t st);
-
-// ---- cluster-resident decode forward for small agents (small_fwd.cu): all
-// layers of a tick of <= 16 rows in one 16-CTA cluster; writes the final
-// residual rows to x_out (the LM head runs as its own kernel) ----
-constexpr int kSmallCluster = 16;
-constexpr int kSmallSlotBytes = 64 * 1024;  // per-CTA weight slab slot (2 slots)
-struct SmallParams {
-  int L = 0, D = 0, nh = 0, nkv = 0, hd = 0, ffn = 0;
-  float eps = 1e-5f;
-  const RowDesc* rows = nullptr;
-  const int* meta = nullptr;
-  const int* out_tok_read = nullptr;
-  const bf16* emb = nullptr;
-  const float* g = nullptr;
-  const float2* rope = nullptr;
-  bf16* kpool = nullptr;
-  bf16* vpool = nullptr;
-  long long kv_stride = 0, layer_stride = 0;
-  int max_ctx = 0;
-  const bf16* w0 = nullptr;  // layer 0 wqkv; a layer is [wqkv][wo][wgu][wd] contiguous
-  long long wstride = 0, off_o = 0, off_gu = 0, off_d = 0;  // elements
-  float* x_out = nullptr;  // [R][D]
-};
-int small_forward_smem(const SmallParams& p);
-bool small_forward_supported(const SmallParams& p);
-void small_forward(const SmallParams& p, cudaStream_t st);
-void small_forward_debug_trace(unsigned long long* buf);  // debug: per-CTA clock64 stamps [16][64], nullptr = off
-
 // o[r][h] = softmax(q k^T / sqrt(hd)) v over keys [0, pos] of the row's agent;
 // keys split across CTAs (kKvSplit keys each), partials combined in split
 // order by the last-arriving CTA.  `ws` >= attention_ws_floats(...) floats,
@@ -270,6 +179,9 @@ void attention_prefill(const bf16* q, const RowDesc* rows, int R_cap, const int*
 // RMSNorm + QKV + RoPE + KV append + attention in one launch, CTA = (row, kv
 // head) with its Wqkv slabs in smem.  o as attention().
 bool qkv_attention_supported(int D, int nh, int nkv, int hd);
+// the fused o-projection (wo_blk != nullptr) of qkv_attention: the one check
+// shared by the host (which then drops its o-projection launch) and the launcher
+bool qkv_oproj_supported(int D, int nh, int nkv, int hd);
 // emb / out_tok (layer 0): gather the rows' embeddings in-kernel and write X
 // (the embed kernel folded in); nullptr: X holds the residual rows.  kmap /
 // vmap (hd 64): the K / V pools as [rows][64] TMA maps with 64-row boxes --

@@ -494,27 +494,33 @@ def test_tensor_core_path_parity(mode):
         assert chk["mismatches"] == [] and chk["lp_ok"], (name, chk)
 
 
-@pytest.mark.parametrize("path", ["megakernel", "small_forward", "norm_fold"])
-def test_fused_decode_paths_match_oracle(path):
-    """The fused decode forwards (persistent grid megakernel; 16-CTA cluster
-    forward for small agents) replace the per-kernel chain for ticks of <= 16
-    rows: every agent of a C1 request must pass the teacher-forced oracle
-    check and the replayed orchestration must match."""
+DECODE_VARIANTS = {
+    # RMSNorm folded into the swap-AB GEMVs (needs tensor-core-sized matrices: 1B agents, short outputs)
+    "norm_fold": {"MOA_NORM_FOLD": "1"},
+    # the small-agent fused kernel without its folded o-projection (the separate o-projection launch)
+    "unfused_oproj": {"MOA_FUSE_O": "0"},
+    # the per-kernel chain for small agents (no fused QKV + attention kernel)
+    "chain": {"MOA_QKV_ATTN": "0"},
+}
+
+
+@pytest.mark.parametrize("path", list(DECODE_VARIANTS))
+def test_decode_path_variants_match_oracle(path):
+    """Every decode-path variant the engine can select (switches read when the
+    engine is built) must pass the teacher-forced oracle check on every agent
+    of a request, with the replayed orchestration matching."""
     cfg = dict(C1)
-    if path == "norm_fold":  # the folded norm needs tensor-core-sized matrices: 1B agents, short outputs
+    if path == "norm_fold":
         cfg = dict(CONFIGS["C2"], topology=dict(kind="tree", widths=[2, 1], branching=[2]), assign=[["leaf"], ["agg"]],
                    out_len=[12, 12], early_exit=False, query_tokens=32, leaf_prefix_tokens=16, agg_prefix_tokens=16,
                    suffix_tokens=8)
-        os.environ["MOA_NORM_FOLD"] = "1"
+    env = DECODE_VARIANTS[path]
+    os.environ.update(env)
     try:
         eng, qc = capi.engine_for(cfg)
     finally:
-        os.environ.pop("MOA_NORM_FOLD", None)
-    for m in range(len(cfg["models"])):
-        if path == "megakernel":
-            eng.megakernel(m, True)
-        elif path == "small_forward":
-            eng.small_forward(m, True)
+        for k in env:
+            os.environ.pop(k, None)
     r = eng.run_query(qc, sample=2, resolve=True, detail=True)
     eng.close()
     o = _replay(cfg, r, 2)
