@@ -213,6 +213,9 @@ int moa_run_batch(moa_engine* eng, const moa_run_config* cfg, const int* samples
  * before the request (moa_engine_trace); *len = bytes, written to buf when
  * cap > *len. */
 int moa_engine_trace(moa_engine* eng, int enable);
+/* Test hook: the fp32 residual rows [rows][d] of model `model`'s last forward
+ * (tick row order, before the final RMSNorm) -- per-layer parity checks. */
+int moa_read_residual(moa_engine* eng, int model, int rows, float* out, long long cap);
 /* Engine clock for protocol-level callers (the HTTP engine service,
  * engine_service.cpp:49-171): mark time zero on the engine stream, then read
  * the device time at the end of a tick (seconds; needs moa_engine_trace on
@@ -269,11 +272,13 @@ int moa_k_gemv(uintptr_t A, uintptr_t X, int R, uintptr_t W, int N, int K, uintp
 int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
 /* Decode GEMV on the tensor cores (swap-AB, split-K): out[R][N] fp32 =
  * A[R][K] . W[N][K]^T for R <= 16; A must have >= 16 allocated rows. */
-/* Causal attention over a KV pool (layer 0 of kv_stride-sized slots): out[R][nh][hd] bf16 from q[R][nh][hd]
- * bf16, rows = moa row descriptors {kv, pos, tok, out}, meta[0] = live rows.  prefill = 1: the tiled prefill
- * kernel (rows in same-agent runs), 0: the per-row GQA kernel. */
+/* Causal attention over a KV pool (layer 0 of `slots` kv_stride-sized slots): out[R][nh][hd] bf16 from
+ * q[R][nh][hd] bf16, rows = moa row descriptors {kv, pos, tok, out}, meta[0] = live rows.  prefill bit 0:
+ * the tiled prefill kernel (rows in same-agent runs) + the per-row kernel for rows alone in their run; bit 1:
+ * the per-row kernel is the TMA-staged one (attn_decode.cu) instead of the register-staged one. */
 int moa_k_attention(uintptr_t q, uintptr_t rows, int R, uintptr_t meta, int nh, int nkv, int hd, uintptr_t kpool,
-                    uintptr_t vpool, long long kv_stride, int max_ctx, uintptr_t out, int prefill, uintptr_t stream);
+                    uintptr_t vpool, long long kv_stride, int max_ctx, uintptr_t out, int prefill, uintptr_t stream,
+                    int slots);
 int moa_k_noop(uintptr_t p, int ctas, uintptr_t stream); /* trivial PDL kernel: launch-chain cost probe */
 int moa_k_debug_trace(uintptr_t buf); /* debug: gemv_tc per-CTA clock stamps, 0 = off */
 int moa_k_chain_stamp(uintptr_t buf); /* debug: decode-chain per-CTA globaltimer stamps (stamp.cuh), 0 = off */

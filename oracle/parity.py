@@ -15,7 +15,9 @@ import numpy as np
 from .model import CpuModel, logit_stats
 
 LOGIT_ATOL = 0.2
-LOGPROB_ATOL = 0.1  # a logprob moves with the logit and the log-sum-exp: <= 2 x a logit error / 4
+# logprob = x_tok - logsumexp(x): its error is at most |d x_tok| + max |d x| <= 2 x LOGIT_ATOL; 0.1 (half a
+# logit bound) is the bar, observed max 0.052 on tiny agents and 0.023 on 8B-width ones
+LOGPROB_ATOL = 0.1
 
 
 def teacher_forced(model: CpuModel, prompt, outputs):
@@ -33,14 +35,27 @@ def teacher_forced(model: CpuModel, prompt, outputs):
     return model.forward([(kv, i, t) for i, t in enumerate(seq)], want)
 
 
-def check_agent(model: CpuModel, prompt, out_tokens, out_logprobs, logits_atol=LOGIT_ATOL, lp_atol=LOGPROB_ATOL):
+def check_agent(model: CpuModel, prompt, out_tokens, out_logprobs, logits_atol=LOGIT_ATOL, lp_atol=LOGPROB_ATOL,
+                gpu_logits=None):
     """Returns dict(checked, skipped_near_tie, mismatches, max_lp_err).  A
-    mismatch is a GPU greedy id that disagrees with a decisive oracle argmax."""
+    mismatch is a GPU greedy id that disagrees with a decisive oracle argmax.
+
+    With the GPU's own fp32 logits (keep_logits engines) the bound is the
+    measured one: every logit must be within logits_atol of the oracle's
+    (max_logit_err), and a token is decisive when the oracle's top-1 margin
+    exceeds 2 * max_logit_err -- then the GPU argmax provably equals the
+    oracle's.  Without them the margin must exceed 2 * logits_atol."""
     L = teacher_forced(model, prompt, out_tokens)
     tok, lp, _ = logit_stats(L)
     srt = np.sort(L, axis=-1)
     margin = srt[:, -1] - srt[:, -2]
-    decisive = margin > 2 * logits_atol
+    bound = logits_atol
+    logit_err = None
+    if gpu_logits is not None:
+        G = np.asarray(gpu_logits, dtype=np.float32).reshape(L.shape)
+        logit_err = float(np.abs(G - L).max()) if len(out_tokens) else 0.0
+        bound = min(logits_atol, logit_err)
+    decisive = margin > 2 * bound
     mism = [k for k in range(len(out_tokens)) if decisive[k] and int(tok[k]) != int(out_tokens[k])]
     # logprob of the GPU's token under the oracle
     z = L - L.max(axis=-1, keepdims=True)
@@ -48,4 +63,5 @@ def check_agent(model: CpuModel, prompt, out_tokens, out_logprobs, logits_atol=L
     lp_gpu_tok = np.array([z[k, out_tokens[k]] - lse[k] for k in range(len(out_tokens))])
     lp_err = float(np.abs(lp_gpu_tok - np.asarray(out_logprobs)).max()) if len(out_tokens) else 0.0
     return dict(checked=int(decisive.sum()), skipped_near_tie=int((~decisive).sum()), mismatches=mism,
-                max_lp_err=lp_err, lp_ok=lp_err <= lp_atol)
+                max_lp_err=lp_err, lp_ok=lp_err <= lp_atol and (logit_err is None or logit_err <= logits_atol),
+                max_logit_err=logit_err)

@@ -121,6 +121,7 @@ _SIGS = {
     "moa_read_logits": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _P(C.c_float), C.c_int], C.c_int),
     "moa_agent_state": ([C.c_void_p, C.c_int, C.c_int] + [_P(C.c_int)] * 4, C.c_int),
     "moa_engine_trace": ([C.c_void_p, C.c_int], C.c_int),
+    "moa_read_residual": ([C.c_void_p, C.c_int, C.c_int, _P(C.c_float), C.c_longlong], C.c_int),
     "moa_engine_mark_start": ([C.c_void_p], C.c_int),
     "moa_engine_tick": ([C.c_void_p, _P(C.c_int)], C.c_int),
     "moa_tick_seconds": ([C.c_void_p, C.c_int, _P(C.c_double)], C.c_int),
@@ -145,7 +146,7 @@ _SIGS = {
                             _P(C.c_int)], C.c_int),
     "moa_slotplan_free": ([C.c_void_p], C.c_int),
     "moa_k_attention": ([C.c_size_t, C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_size_t,
-                         C.c_size_t, C.c_longlong, C.c_int, C.c_size_t, C.c_int, C.c_size_t], C.c_int),
+                         C.c_size_t, C.c_longlong, C.c_int, C.c_size_t, C.c_int, C.c_size_t, C.c_int], C.c_int),
     "moa_k_gemv": ([C.c_size_t, C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_size_t], C.c_int),
     "moa_k_gemm_tc": ([C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_size_t], C.c_int),
     "moa_k_gemv_tc": ([C.c_size_t, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_size_t], C.c_int),
@@ -196,8 +197,9 @@ SHAPES = {
 
 
 def model_spec(tag: str, shape: str, seed: int = 0, max_agents: int = 16, vocab: int = 50000,
-               lm_gain: float = 4.0) -> ModelSpec:
-    s = SHAPES[shape]
+               lm_gain: float = 4.0, **over) -> ModelSpec:
+    """`over` overrides shape fields (e.g. n_layers=2: the shape's first layers, same weights)."""
+    s = {**SHAPES[shape], **over}
     return ModelSpec(tag=tag.encode()[:31], vocab=vocab, rope_theta=10000.0, norm_eps=1e-5, lm_gain=lm_gain,
                      seed=seed, max_agents=max_agents, **s)
 
@@ -266,6 +268,14 @@ class Engine:
         check(lib().moa_read_logits(self.h, a[0], a[1], k, buf, vocab))
         import numpy as np
         return np.ctypeslib.as_array(buf).copy()
+
+    def read_residual(self, model: int, rows: int):
+        """fp32 residual rows [rows][d] of the model's last forward (test hook)."""
+        import numpy as np
+        d = self.models[model].d
+        buf = np.zeros(rows * d, dtype=np.float32)
+        check(lib().moa_read_residual(self.h, model, rows, buf.ctypes.data_as(_P(C.c_float)), buf.size))
+        return buf.reshape(rows, d)
 
     def state(self, a):
         v = [C.c_int() for _ in range(4)]

@@ -405,6 +405,18 @@ int moa_run_batch(moa_engine* eng, const moa_run_config* cfg, const int* samples
   });
 }
 
+int moa_read_residual(moa_engine* eng, int model, int rows, float* out, long long cap) {
+  return guard([&] {
+    need(out, "out");
+    if (model < 0 || model >= E(eng).n_models()) throw moa::ValidationError("engine: model index out of range");
+    moa::DeviceModel& dm = E(eng).model(model);
+    const long long n = static_cast<long long>(rows) * dm.spec().d;
+    if (rows < 0 || rows > dm.max_rows() || n > cap) throw moa::ValidationError("read_residual: rows out of range");
+    MOA_CUDA(cudaStreamSynchronize(E(eng).stream()));
+    MOA_CUDA(cudaMemcpy(out, dm.residual(), sizeof(float) * n, cudaMemcpyDeviceToHost));
+  });
+}
+
 int moa_engine_trace(moa_engine* eng, int enable) {
   return guard([&] { E(eng).set_tracing(enable != 0); });
 }
@@ -709,7 +721,8 @@ int moa_slotplan_free(moa_slotplan* p) {
 }
 
 int moa_k_attention(uintptr_t q, uintptr_t rows, int R, uintptr_t meta, int nh, int nkv, int hd, uintptr_t kpool,
-                    uintptr_t vpool, long long kv_stride, int max_ctx, uintptr_t out, int prefill, uintptr_t stream) {
+                    uintptr_t vpool, long long kv_stride, int max_ctx, uintptr_t out, int prefill, uintptr_t stream,
+                    int slots) {
   return guard([&] {
     if ((hd != 64 && hd != 128) || nh % nkv || R <= 0) throw moa::ValidationError("attention: unsupported shape");
     const auto st = reinterpret_cast<cudaStream_t>(stream);
@@ -719,6 +732,8 @@ int moa_k_attention(uintptr_t q, uintptr_t rows, int R, uintptr_t meta, int nh, 
     const auto* kp = reinterpret_cast<const moa::k::bf16*>(kpool);
     const auto* vp = reinterpret_cast<const moa::k::bf16*>(vpool);
     auto* op = reinterpret_cast<moa::k::bf16*>(out);
+    const bool tma = (prefill & 2) != 0;  // bit 1: the TMA-staged per-row kernel
+    prefill &= 1;
     if (prefill) moa::k::attention_prefill(qp, rp, R, mp, nh, nkv, hd, kp, vp, kv_stride, 0, max_ctx, op, st);
     {  // prefill: the per-row kernel takes the rows alone in their run
       float* ws = nullptr;
@@ -726,10 +741,21 @@ int moa_k_attention(uintptr_t q, uintptr_t rows, int R, uintptr_t meta, int nh, 
       MOA_CUDA(cudaMalloc(&ws, sizeof(float) * moa::k::attention_ws_floats(R, nh, hd, max_ctx)));
       MOA_CUDA(cudaMalloc(&cnt, sizeof(int) * R * nh));
       MOA_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * R * nh, st));
-      const int ks = moa::k::kv_split(hd);
+      const int ks = tma ? moa::k::attention_decode_tma_keys(hd) : moa::k::kv_split(hd);
       int ns = 1;
       while (ns * ks < max_ctx) ns <<= 1;
-      moa::k::attention(qp, rp, R, ns, mp, nh, nkv, hd, kp, vp, kv_stride, 0, max_ctx, op, ws, cnt, st, prefill != 0);
+      if (tma) {
+        // the pools hold `slots` agents of one layer
+        const long long pool_rows = static_cast<long long>(slots) * kv_stride / hd;
+        moa::k::TmaMap km, vm;
+        if (!moa::k::make_tmap_bf16(&km, kp, pool_rows, hd, 64) || !moa::k::make_tmap_bf16(&vm, vp, pool_rows, hd, 64))
+          throw moa::DeviceError("attention: TMA map creation failed");
+        moa::k::attention_decode_tma(km, vm, qp, rp, R, ns, mp, nh, nkv, hd, kv_stride, 0, max_ctx, op, ws, cnt, st,
+                                     prefill != 0);
+      } else {
+        moa::k::attention(qp, rp, R, ns, mp, nh, nkv, hd, kp, vp, kv_stride, 0, max_ctx, op, ws, cnt, st,
+                          prefill != 0);
+      }
       MOA_CUDA(cudaStreamSynchronize(st));
       cudaFree(ws);
       cudaFree(cnt);

@@ -94,6 +94,7 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   }
   lm_ = take(V * D);
   init(lm_, "lm", V, D, k::kRowsIdentity);
+  if (const char* f = std::getenv("MOA_EVICT_FIRST")) evict_first_ = f[0] != '0';
 
   const int maxd = std::max({s.d, s.ffn, s.n_heads * s.head_dim});
   dev_alloc(&ones_, maxd);
@@ -116,6 +117,10 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   kv_stride_ = layer_stride_ * s.n_layers;
   dev_alloc(&kpool_, kv_stride_ * max_agents);
   dev_alloc(&vpool_, kv_stride_ * max_agents);
+  // finite everywhere: the TMA decode attention stages whole 64-key boxes
+  // (keys past a row's position are masked, but 0 * NaN would not be)
+  MOA_CUDA(cudaMemsetAsync(kpool_, 0, sizeof(k::bf16) * kv_stride_ * max_agents, st));
+  MOA_CUDA(cudaMemsetAsync(vpool_, 0, sizeof(k::bf16) * kv_stride_ * max_agents, st));
 
   dev_alloc(&x_, static_cast<long long>(max_rows) * D);
   dev_alloc(&h_, static_cast<long long>(max_rows) * maxd);
@@ -182,8 +187,12 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
     }
   }
   // K / V pools as [rows][hd] TMA maps (64-key boxes) for the fused kernel's swizzled key stage
-  kv_maps_ok_ = hd == 64 && k::make_tmap_bf16(&kmap_, kpool_, kv_stride_ * max_agents / hd, hd, 64) &&
+  kv_maps_ok_ = k::make_tmap_bf16(&kmap_, kpool_, kv_stride_ * max_agents / hd, hd, 64) &&
                 k::make_tmap_bf16(&vmap_, vpool_, kv_stride_ * max_agents / hd, hd, 64);
+  // decode rows of GQA agents: TMA-staged attention (MOA_DECODE_TMA=0: the register-staged kernel)
+  attn_tma_ = kv_maps_ok_ && k::attention_decode_tma_supported(s.n_heads, s.n_kv_heads, static_cast<int>(hd), max_ctx);
+  if (const char* e = std::getenv("MOA_DECODE_TMA")) attn_tma_ = attn_tma_ && e[0] != '0';
+  split_keys_ = attn_tma_ ? k::attention_decode_tma_keys(static_cast<int>(hd)) : k::kv_split(static_cast<int>(hd));
   if (const char* e = std::getenv("MOA_QKV_ATTN")) use_qkv_attn_ = std::string(e) != "0";
   if (const char* e = std::getenv("MOA_PREFILL_ATTN")) use_prefill_attn_ = std::string(e) != "0";
   // RMSNorm folded into the decode GEMVs: ssq partials [16 rows][d/16]
@@ -198,10 +207,9 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
     o1.epi = d1.epi = k::kEpiResidual;
     nfold_ok_ = tc_ok_ && D % 16 == 0 && k::gemv_tc_norm_supported(q1) && k::gemv_tc_norm_supported(g1) &&
                 k::gemv_tc_supported(o1) && k::gemv_tc_supported(d1);
-    // one kernel fewer per normed GEMV; the in-kernel staging puts the ssq
-    // and x reads on the critical path.  Default on up to d = 2048 (measured:
-    // 1B agents -3.5% per request, 8B agents +1%); MOA_NORM_FOLD=0/1 forces it
-    use_nfold_ = D <= 2048;
+    // one kernel fewer per normed GEMV: converter warps stage each k-tile of
+    // bf16(rmsnorm(x)) just in time beside the weight stream; MOA_NORM_FOLD=0 off
+    use_nfold_ = true;
     if (const char* e = std::getenv("MOA_NORM_FOLD")) use_nfold_ = std::string(e) != "0";
   }
   MOA_CUDA(cudaMemsetAsync(gv_cnt_, 0, sizeof(int) * ((std::max({s.qkv_cols(), 2 * s.ffn, s.d}) + 127) / 128), st));
@@ -273,7 +281,7 @@ void DeviceModel::forward(int R, int Rl, int max_pos, const TickStats& ts, const
   if (max_pos >= max_ctx_) throw RunError("model " + spec_.tag + ": position exceeds max_ctx");
   // bucket caps: one graph serves every tick whose live counts fit them
   const int rcap = std::min(pow2_at_least(R, 8), max_rows_);
-  const int ks = k::kv_split(spec_.head_dim);
+  const int ks = split_keys_;
   const int nsplit = pow2_at_least((max_pos + ks) / ks, 1);
   if (!use_graphs_ || probes_) {
     live_R_ = R;
@@ -306,7 +314,7 @@ void DeviceModel::forward_run(int K, int R, int max_pos, const int* out_tok_read
   if (R <= 0 || R > max_lrows_ || R > k::kLmMaxRows) throw RunError("model " + spec_.tag + ": run rows exceed workspace");
   if (max_pos >= max_ctx_) throw RunError("model " + spec_.tag + ": position exceeds max_ctx");
   const int rcap = std::min(pow2_at_least(R, 8), max_rows_);
-  const int ks = k::kv_split(spec_.head_dim);
+  const int ks = split_keys_;
   const int nsplit = pow2_at_least((max_pos + ks) / ks, 1);  // the last tick's: a cap for the earlier ones
   const auto key = std::make_tuple(rcap, nsplit, 1 | (use_tc_ ? 2 : 0) | 8 | (parity << 4),
                                    2 * K);
@@ -351,6 +359,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       k::gemv(g, st);
       return;
     }
+    g.evict_first = evict_first_;
     if (g.X && dec_tc && norm_fold) {  // the swap-AB GEMV normalises x itself (ssq from the producer)
       g.ssq = ssq_;
       k::gemv_tc(map_w, map_hn16_ /* unused: X is staged in-kernel */, g, gv_ws_, gv_cnt_, st);
@@ -440,8 +449,12 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       const double keys = prefill ? live_.single_keys : live_.keys, rows_n = prefill ? live_.singles : Rv;
       probe_begin(KernelProbes::AttnDecode, 4.0 * keys * nkv * hd + 4.0 * rows_n * nh * hd,
                   4.0 * keys * nh * hd);
-      k::attention(q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_,
-                   attn_ws_, attn_cnt_, st, prefill);
+      if (attn_tma_)
+        k::attention_decode_tma(kmap_, vmap_, q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kv_stride_, loff,
+                                max_ctx_, h_, attn_ws_, attn_cnt_, st, prefill);
+      else
+        k::attention(q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_,
+                     attn_ws_, attn_cnt_, st, prefill);
       probe_end();
     }
     }
@@ -530,6 +543,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       lm.out_lp = out_lp;
       lm.out_ent = out_ent;
       lm.logits = logits;
+      lm.evict_first = evict_first_;
       k::lm_head_tc(wmap_lm_, map_hn16_, lm, part_, lm_cnt_, lm_grid_, st);
     } else {
       k::lm_head(x_, buf_.sel, meta, ones_, eps, lm_, s.vocab, D, part_, lm_cnt_, buf_.sel + max_lrows_, out_tok,

@@ -144,6 +144,9 @@ class DeviceModel {
   bool nfold_ok_ = false, use_nfold_ = true;
   float* ssq_ = nullptr;
   int lm_grid_ = 148;  // persistent LM head: one CTA per SM
+  // decode GEMVs stream their weights with an L2 evict-first hint
+  // (MOA_EVICT_FIRST=0: off; measured -3.5..-6% per 1B / 8B decode tick)
+  bool evict_first_ = true;
   void graphs_clear();
   struct LayerMaps {
     k::TmaMap wqkv, wo, wgu, wd;
@@ -153,6 +156,8 @@ class DeviceModel {
   k::TmaMap kmap_, vmap_;  // K / V pools as [rows][hd], 64-row boxes (fused QKV + attention, hd 64)
   k::bf16* wo_blk_ = nullptr;  // [L][nkv][D][hpg*hd]: Wo regrouped for the fused o-projection
   bool kv_maps_ok_ = false;
+  bool attn_tma_ = false;  // decode rows: TMA-staged attention (attn_decode.cu)
+  int split_keys_ = 512;   // keys per attention CTA (sizes the graphs' split buckets)
   k::TmaMap map_hn_, map_h_attn_, map_h_ffn_;        // A operands, 128-row boxes (prefill)
   k::TmaMap map_hn16_, map_h_attn16_, map_h_ffn16_;  // 16-row boxes (decode, swap-AB)
   float* gv_ws_ = nullptr;                           // gemv_tc split-K partials

@@ -20,6 +20,7 @@
 #include "kernels.cuh"
 #include "tc_common.cuh"
 #include "stamp.cuh"
+#include "mma_common.cuh"
 
 namespace moa::k {
 
@@ -944,30 +945,6 @@ attention_prefill_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__
 // smem (16-byte chunks XOR-swizzled by row so ldmatrix is conflict-free);
 // S = Q.K^T per warp (8 n-tiles), causal mask by position, online softmax on
 // the accumulator fragments, P reused in registers as the A operand of P.V.
-__device__ __forceinline__ void ldsm_x4(std::uint32_t addr, std::uint32_t& r0, std::uint32_t& r1, std::uint32_t& r2,
-                                        std::uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(std::uint32_t addr, std::uint32_t& r0, std::uint32_t& r1, std::uint32_t& r2,
-                                          std::uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void mma_bf16(float (&d)[4], std::uint32_t a0, std::uint32_t a1, std::uint32_t a2,
-                                         std::uint32_t a3, std::uint32_t b0, std::uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ std::uint32_t pack_bf16(float lo, float hi) {
-  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<const std::uint32_t*>(&v);
-}
-
 template <int HD>
 __global__ void __launch_bounds__(128, 1)
 attention_prefill_mma_kernel(const bf16* __restrict__ q, const RowDesc* __restrict__ rows, const int* __restrict__ meta,

@@ -102,6 +102,10 @@ struct GemvArgs {
   // kEpiResidual (SIMT gemv): the residual rows were last written at least two
   // kernels back, so they are read before the PDL wait
   bool res_early = false;
+  // gemv_tc / lm_head_tc: stream the weights with an L2 evict-first hint
+  // (each weight byte is read once per forward; the activations, KV and
+  // partials the chain re-reads keep the L2)
+  bool evict_first = false;
 };
 void gemv(const GemvArgs& a, cudaStream_t st);  // dispatches to gemv_stream for large matrices
 // HBM-streaming variant (gemv_stream.cu): persistent CTAs, cp.async.bulk ring.
@@ -167,6 +171,17 @@ long long attention_ws_floats(int R, int nh, int hd, int max_ctx);
 void attention(const bf16* q, const RowDesc* rows, int R_cap, int nsplit_cap, const int* meta, int nh, int nkv,
                int hd, const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx,
                bf16* o, float* ws, int* cnt, cudaStream_t st, bool skip_runs = false);
+
+// The same contract on TMA-staged keys (attn_decode.cu): fixed splits of
+// attention_decode_tma_keys(hd) keys per CTA; kmap / vmap = the K / V pools as
+// [rows][hd] TMA maps (64-row boxes, 128B swizzle).  The pools must hold
+// finite values everywhere (zero-initialised): whole 64-key boxes are loaded.
+int attention_decode_tma_keys(int hd);
+bool attention_decode_tma_supported(int nh, int nkv, int hd, int max_ctx);
+void attention_decode_tma(const TmaMap& kmap, const TmaMap& vmap, const bf16* q, const RowDesc* rows, int R_cap,
+                          int nsplit_cap, const int* meta, int nh, int nkv, int hd, long long kv_stride,
+                          long long layer_off, int max_ctx, bf16* o, float* ws, int* cnt, cudaStream_t st,
+                          bool skip_runs = false);
 
 // Prefill ticks (rows of long same-agent runs): CTA = 64 consecutive rows x q
 // head, keys streamed through smem once per same-agent segment; rows alone in

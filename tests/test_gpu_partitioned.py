@@ -14,19 +14,19 @@ from paper_2512_18126_b200.configs import C0, C1U
 pytestmark = pytest.mark.gpu
 
 
-def _single(cfg, sample):
-    eng, qc = capi.engine_for(cfg, gemv_only=True)
+def _single(cfg, sample, gemv_only=True):
+    eng, qc = capi.engine_for(cfg, gemv_only=gemv_only)
     try:
         return eng.run_query(qc, sample=sample)
     finally:
         eng.close()
 
 
-def _partitioned(cfg, sample, world):
+def _partitioned(cfg, sample, world, gemv_only=True):
     hub = capi.LoopbackHub(world)
     engs = []
     for r in range(world):
-        eng, qc = capi.engine_for(cfg, gemv_only=True)
+        eng, qc = capi.engine_for(cfg, gemv_only=gemv_only)
         eng.attach_loopback(hub, r)
         engs.append(eng)
     out, err = [None] * world, []
@@ -78,3 +78,49 @@ def test_partitioned_engine_matches_single(name, cfg, sample, world):
                 n = (n // cfg["chunk_size"]) * cfg["chunk_size"]
             assert b["output"][:n] == a["output"][:n], (name, rank, k)
             assert b["logprobs"][:n] == a["logprobs"][:n], (name, rank, k)
+
+
+@pytest.mark.parametrize("name,cfg,sample,world", [
+    ("C0", dict(C0), 0, 2),
+    ("C1U", dict(C1U), 3, 2),
+    ("C1U-w3", dict(C1U), 1, 3),
+])
+def test_partitioned_engine_tensor_core_path(name, cfg, sample, world):
+    """The default (tensor-core) decode and prefill path under partitioning.
+    Which rows share a forward differs between the ranks and the single
+    engine, so bit-equality with the single run is not the contract; instead
+    every rank must hold exactly the owners' tokens (the hand-off is lossless:
+    the ranks agree bit for bit), every agent must pass the teacher-forced
+    oracle check, and without early exit the schedule equals the single run's."""
+    from oracle.model import CpuModel, make_spec
+    from oracle.parity import check_agent
+    outs = _partitioned(cfg, sample, world, gemv_only=False)
+    single = _single(cfg, sample, gemv_only=False)
+    owner = capi.placement(cfg["topology"], world)
+    ref = outs[owner["3:0"]]  # the root's rank: every chunk of every agent reached it
+    for rank, o in enumerate(outs):
+        assert [(m["completed"], m["evaluated"], m["q"], m["exited"], m["pruned"]) for m in o["metricq"]] == \
+               [(m["completed"], m["evaluated"], m["q"], m["exited"], m["pruned"]) for m in ref["metricq"]]
+        for k, a in ref["agents"].items():
+            b = o["agents"][k]
+            assert b["prompt"] == a["prompt"], (name, rank, k)
+            n = len(a["output"])
+            if a["pruned"] and owner[k] != rank:
+                n = (n // cfg["chunk_size"]) * cfg["chunk_size"]
+            assert b["output"][:n] == a["output"][:n], (name, rank, k)
+    if not cfg["early_exit"]:
+        for k, a in single["agents"].items():
+            for f in ("complete", "decode_start", "output_tokens", "prefill_only_calls", "recomputed_tokens"):
+                assert ref["agents"][k][f] == a[f], (name, k, f)
+    models = {}
+    for k, a in ref["agents"].items():
+        if not a["output"] or a["pruned"]:
+            continue
+        layer, pos = (int(x) for x in k.split(":"))
+        cyc = cfg["assign"][min(layer - 1, len(cfg["assign"]) - 1)]
+        tag = cyc[pos % len(cyc)]
+        mm = cfg["models"][tag]
+        if tag not in models:
+            models[tag] = CpuModel(make_spec(tag, mm["shape"], seed=mm["seed"]), 1024)
+        chk = check_agent(models[tag], a["prompt"], a["output"], a["logprobs"])
+        assert chk["mismatches"] == [] and chk["lp_ok"], (name, k, chk)
