@@ -247,6 +247,37 @@ int moa_metricq_run(const int32_t* tokens, const float* logprobs, const int* len
                     uint64_t seed, double tau, int include_diagonal, uint64_t master, const char* label,
                     double* out6, double* draw, int* exited, double* sim_out, int device);
 
+/* Incremental evaluator handle, one per exit group: MetricQEvaluator
+ * (metricq.hpp:102-122, metricq.cpp:148-194) with its state on the GPU.
+ * add_completion = MockProvider embeddings (embedding.cpp:86-120) computed on
+ * the device from the tokens; add_embedded = rows supplied by any
+ * EmbeddingProvider (embedding.hpp:38-44; emb row-major [n][hidden] fp64).
+ * logprobs are the reference's TokenLogProbs values (validated: non-empty,
+ * finite, <= 0 -> VALIDATION); the confidence is their sequential fp64 mean,
+ * exp'd on the host (bit-exact).  After the call `out` holds the group score
+ * (QualityScore) and, when sim != NULL and sim_cap >= outputs^2, the grown
+ * similarity matrix (row-major).  Groups wider than max_tokens use the n x n
+ * cross-Gram route. */
+typedef struct moa_mq_group moa_mq_group;
+typedef struct {
+  int outputs;
+  double c; /* this completion's confidence */
+  double c_bar, weight_sum, weighted, calibrated, q, tau;
+} moa_quality;
+int moa_mq_group_create(int hidden, uint64_t provider_seed, double tau, int include_diagonal, int max_members,
+                        int max_tokens, int device, moa_mq_group** out);
+int moa_mq_group_add_completion(moa_mq_group* g, const int32_t* tokens, const double* logprobs, int n,
+                                moa_quality* out, double* sim, int sim_cap);
+int moa_mq_group_add_embedded(moa_mq_group* g, const double* emb, const double* logprobs, int n, moa_quality* out,
+                              double* sim, int sim_cap);
+int moa_mq_group_completions(const moa_mq_group* g, int* n);
+int moa_mq_group_free(moa_mq_group* g);
+/* RngStream (rng.hpp:46-83): state of derive(master, label); decide_exit
+ * (metricq.cpp:125-131) draws next_uniform from *state (advanced) and exits
+ * iff draw < q -- add_and_decide = add + decide on the group's stream. */
+int moa_rng_derive(uint64_t master, const char* label, uint64_t* state);
+int moa_decide_exit(double q, uint64_t* state, double* draw, int* exited);
+
 /* ---- routing (topology.cpp:43-196, router.cpp:9-184) ------------------- */
 /* precursor lists: for agent k (layer-major order) pre_off[k]..pre_off[k+1]
  * index into pre (as layer-major agent indices). */

@@ -139,6 +139,16 @@ _SIGS = {
     "moa_metricq_run": ([_P(C.c_int32), _P(C.c_float), _P(C.c_int), C.c_int, C.c_int, C.c_uint64, C.c_double,
                          C.c_int, C.c_uint64, C.c_char_p, _P(C.c_double), _P(C.c_double), _P(C.c_int),
                          _P(C.c_double), C.c_int], C.c_int),
+    "moa_mq_group_create": ([C.c_int, C.c_uint64, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, _P(C.c_void_p)],
+                            C.c_int),
+    "moa_mq_group_add_completion": ([C.c_void_p, _P(C.c_int32), _P(C.c_double), C.c_int, C.c_void_p,
+                                     _P(C.c_double), C.c_int], C.c_int),
+    "moa_mq_group_add_embedded": ([C.c_void_p, _P(C.c_double), _P(C.c_double), C.c_int, C.c_void_p,
+                                   _P(C.c_double), C.c_int], C.c_int),
+    "moa_mq_group_completions": ([C.c_void_p, _P(C.c_int)], C.c_int),
+    "moa_mq_group_free": ([C.c_void_p], C.c_int),
+    "moa_rng_derive": ([C.c_uint64, C.c_char_p, _P(C.c_uint64)], C.c_int),
+    "moa_decide_exit": ([C.c_double, _P(C.c_uint64), _P(C.c_double), _P(C.c_int)], C.c_int),
     "moa_topology": ([C.c_int, C.c_int, _P(C.c_int), _P(C.c_int), _P(C.c_int), _P(C.c_int), C.c_int], C.c_int),
     "moa_slotplan_create": ([C.c_int, C.c_int, _P(C.c_int32), C.c_int, _P(C.c_int), _P(C.c_int), _P(C.c_int32),
                              _P(C.c_int), C.c_int, _P(C.c_int32), C.c_int, C.c_int, _P(C.c_void_p)], C.c_int),
@@ -481,6 +491,73 @@ def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16
     eng = Engine(specs, max_ctx=max_ctx, max_out=out_max, max_rows=max_rows, device=device, keep_logits=keep_logits,
                  gemv_only=gemv_only)
     return eng, QueryConfig(cfg, {t: i for i, t in enumerate(tags)})
+
+
+class Quality(C.Structure):
+    _fields_ = [("outputs", C.c_int)] + [(n, C.c_double) for n in ("c", "c_bar", "weight_sum", "weighted",
+                                                                    "calibrated", "q", "tau")]
+
+
+class MetricQGroup:
+    """One exit group's incremental evaluator on the GPU (moa_mq_group_*,
+    the reference's MetricQEvaluator, metricq.hpp:102-122)."""
+
+    def __init__(self, hidden: int, provider_seed: int = 0, tau: float = 0.7, include_diagonal: bool = True,
+                 max_members: int = 16, max_tokens: int = 4096, device: int = 0):
+        h = C.c_void_p()
+        check(lib().moa_mq_group_create(hidden, provider_seed, tau, int(include_diagonal), max_members, max_tokens,
+                                        device, C.byref(h)))
+        self.h, self.hidden, self.max_members = h, hidden, max_members
+
+    def _result(self, q, sim):
+        n = q.outputs
+        import numpy as np
+        d = {k: getattr(q, k) for k, _ in Quality._fields_}
+        d["sim"] = np.array(sim[: n * n]).reshape(n, n)
+        return d
+
+    def add_completion(self, tokens, logprobs):
+        """MockProvider embeddings of `tokens` (device)."""
+        n = len(tokens)
+        q, sim = Quality(), (C.c_double * (self.max_members ** 2))()
+        check(lib().moa_mq_group_add_completion(self.h, (C.c_int32 * n)(*tokens), (C.c_double * n)(*logprobs), n,
+                                                C.byref(q), sim, self.max_members ** 2))
+        return self._result(q, sim)
+
+    def add_embedded(self, emb, logprobs):
+        """Rows from any EmbeddingProvider: emb [n][hidden] fp64."""
+        import numpy as np
+        e = np.ascontiguousarray(emb, dtype=np.float64)
+        n = e.shape[0]
+        q, sim = Quality(), (C.c_double * (self.max_members ** 2))()
+        check(lib().moa_mq_group_add_embedded(self.h, e.ctypes.data_as(_P(C.c_double)), (C.c_double * n)(*logprobs),
+                                              n, C.byref(q), sim, self.max_members ** 2))
+        return self._result(q, sim)
+
+    def completions(self) -> int:
+        n = C.c_int()
+        check(lib().moa_mq_group_completions(self.h, C.byref(n)))
+        return n.value
+
+    def close(self):
+        if getattr(self, "h", None) and _lib is not None:
+            lib().moa_mq_group_free(self.h)
+            self.h = None
+
+    __del__ = close
+
+
+def rng_derive(master: int, label: str) -> int:
+    s = C.c_uint64()
+    check(lib().moa_rng_derive(master, label.encode(), C.byref(s)))
+    return s.value
+
+
+def decide_exit(q: float, state: int):
+    """(draw, exited, next state) -- decide_exit (metricq.cpp:125-131) on an RngStream state."""
+    s, d, e = C.c_uint64(state), C.c_double(), C.c_int()
+    check(lib().moa_decide_exit(q, C.byref(s), C.byref(d), C.byref(e)))
+    return d.value, bool(e.value), s.value
 
 
 def device_count() -> int:

@@ -594,6 +594,125 @@ int moa_mock_embed(const int32_t* tokens, int n, int hidden, uint64_t seed, doub
   });
 }
 
+}  // extern "C"
+
+struct moa_mq_group {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  int hidden = 0, max_tokens = 0;
+  std::uint64_t seed = 0;
+  int* d_tok = nullptr;
+  std::unique_ptr<moa::GpuMetricQ> ev;
+  ~moa_mq_group() {
+    ev.reset();
+    if (d_tok) cudaFree(d_tok);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+namespace {
+void fill_quality(const moa::QualityScore& qs, moa_quality* out, double* sim, int sim_cap) {
+  if (out) {
+    out->outputs = qs.outputs;
+    out->c = qs.confidences.back();
+    out->c_bar = qs.c_bar;
+    out->weight_sum = qs.weight_sum;
+    out->weighted = qs.weighted;
+    out->calibrated = qs.calibrated;
+    out->q = qs.q;
+    out->tau = qs.tau;
+  }
+  if (sim && sim_cap >= static_cast<int>(qs.sim.size()))
+    std::memcpy(sim, qs.sim.data(), sizeof(double) * qs.sim.size());
+}
+
+void check_group_input(const moa_mq_group* g, const double* logprobs, int n) {
+  if (!g) throw moa::ValidationError("metricq: null group");
+  need(logprobs, "logprobs");
+  if (n <= 0) throw moa::ValidationError("logprobs: need at least one token");
+  if (n > g->max_tokens) throw moa::ValidationError("metricq: completion longer than the evaluator capacity");
+}
+}  // namespace
+
+extern "C" {
+
+int moa_mq_group_create(int hidden, uint64_t provider_seed, double tau, int include_diagonal, int max_members,
+                        int max_tokens, int device, moa_mq_group** out) {
+  return guard([&] {
+    need(out, "out");
+    if (max_members <= 0 || max_tokens <= 0)
+      throw moa::ValidationError("metricq: max_members and max_tokens must be > 0");
+    MOA_CUDA(cudaSetDevice(device));
+    auto g = std::make_unique<moa_mq_group>();
+    g->device = device;
+    g->hidden = hidden;
+    g->max_tokens = max_tokens;
+    g->seed = provider_seed;
+    MOA_CUDA(cudaStreamCreateWithFlags(&g->st, cudaStreamNonBlocking));
+    MOA_CUDA(cudaMalloc(&g->d_tok, sizeof(int) * max_tokens));
+    g->ev = std::make_unique<moa::GpuMetricQ>(hidden, provider_seed, tau, include_diagonal != 0, max_members,
+                                              max_tokens, g->st);
+    *out = g.release();
+  });
+}
+
+int moa_mq_group_add_completion(moa_mq_group* g, const int32_t* tokens, const double* logprobs, int n,
+                                moa_quality* out, double* sim, int sim_cap) {
+  return guard([&] {
+    check_group_input(g, logprobs, n);
+    need(tokens, "tokens");
+    const double c = moa::geometric_mean_confidence(std::vector<double>(logprobs, logprobs + n));
+    MOA_CUDA(cudaSetDevice(g->device));
+    MOA_CUDA(cudaMemcpyAsync(g->d_tok, tokens, sizeof(int) * n, cudaMemcpyHostToDevice, g->st));
+    moa::k::ee_mock_embed(g->d_tok, 0, n, g->hidden, g->seed, g->ev->emb_buffer(), g->st);
+    fill_quality(g->ev->add_completion_conf(c, n), out, sim, sim_cap);
+  });
+}
+
+int moa_mq_group_add_embedded(moa_mq_group* g, const double* emb, const double* logprobs, int n, moa_quality* out,
+                              double* sim, int sim_cap) {
+  return guard([&] {
+    check_group_input(g, logprobs, n);
+    need(emb, "emb");
+    const double c = moa::geometric_mean_confidence(std::vector<double>(logprobs, logprobs + n));
+    MOA_CUDA(cudaSetDevice(g->device));
+    MOA_CUDA(cudaMemcpyAsync(g->ev->emb_buffer(), emb, sizeof(double) * n * g->hidden, cudaMemcpyHostToDevice,
+                             g->st));
+    fill_quality(g->ev->add_completion_conf(c, n), out, sim, sim_cap);
+  });
+}
+
+int moa_mq_group_completions(const moa_mq_group* g, int* n) {
+  return guard([&] {
+    need(n, "n");
+    if (!g) throw moa::ValidationError("metricq: null group");
+    *n = g->ev->completions();
+  });
+}
+
+int moa_mq_group_free(moa_mq_group* g) {
+  return guard([&] { delete g; });
+}
+
+int moa_rng_derive(uint64_t master, const char* label, uint64_t* state) {
+  return guard([&] {
+    need(label, "label");
+    need(state, "state");
+    *state = moa::rng::Stream::derive(master, label).state();
+  });
+}
+
+int moa_decide_exit(double q, uint64_t* state, double* draw, int* exited) {
+  return guard([&] {
+    need(state, "state");
+    moa::rng::Stream s(*state);
+    const moa::ExitDecision d = moa::decide_exit(q, s);
+    *state = s.state();
+    if (draw) *draw = d.draw;
+    if (exited) *exited = d.exited ? 1 : 0;
+  });
+}
+
 int moa_metricq_run(const int32_t* tokens, const float* logprobs, const int* lens, int m, int hidden, uint64_t seed,
                     double tau, int include_diagonal, uint64_t master, const char* label, double* out6,
                     double* draw, int* exited, double* sim_out, int device) {

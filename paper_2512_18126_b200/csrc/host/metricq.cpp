@@ -2,6 +2,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "../kernels/kernels.cuh"
 #include "model.hpp"
@@ -66,15 +68,24 @@ GpuMetricQ::GpuMetricQ(int hidden, std::uint64_t seed, double tau, bool include_
   if (hidden <= 0) throw ValidationError("provider.hidden: must be > 0");
   const long long hh = static_cast<long long>(hidden) * hidden;
   MOA_CUDA(cudaMalloc(&d_emb_, sizeof(double) * static_cast<long long>(max_tokens) * hidden));
-  MOA_CUDA(cudaMalloc(&d_gram_, sizeof(double) * hh));
-  MOA_CUDA(cudaMalloc(&d_corrs_, sizeof(double) * hh * max_members));
+  cross_ = hidden > max_tokens;
+  if (const char* e = std::getenv("MOA_FCS_ROUTE")) cross_ = std::string(e) == "nn";  // force one route (tests)
+  if (cross_) {
+    MOA_CUDA(cudaMalloc(&d_hat_, sizeof(double) * static_cast<long long>(max_members) * max_tokens * hidden));
+    MOA_CUDA(cudaMalloc(&d_nv_, sizeof(int) * max_members));
+    MOA_CUDA(cudaMalloc(&d_part_, sizeof(double) * k::ee_cross_parts(max_tokens, max_members)));
+  } else {
+    MOA_CUDA(cudaMalloc(&d_gram_, sizeof(double) * hh));
+    MOA_CUDA(cudaMalloc(&d_corrs_, sizeof(double) * hh * max_members));
+  }
   MOA_CUDA(cudaMalloc(&d_out_, sizeof(double) * (1 + max_members)));
   MOA_CUDA(cudaMallocHost(&h_out_, sizeof(double) * (1 + max_members)));
 }
 
 GpuMetricQ::~GpuMetricQ() {
   for (void* p : {static_cast<void*>(d_emb_), static_cast<void*>(d_gram_), static_cast<void*>(d_corrs_),
-                  static_cast<void*>(d_out_)})
+                  static_cast<void*>(d_out_), static_cast<void*>(d_hat_), static_cast<void*>(d_nv_),
+                  static_cast<void*>(d_part_)})
     if (p) cudaFree(p);
   if (h_out_) cudaFreeHost(h_out_);
 }
@@ -92,18 +103,43 @@ QualityScore GpuMetricQ::add_completion_embedded(const float* d_lp, long long ba
   return finish(d_lp, base, n);
 }
 
-QualityScore GpuMetricQ::finish(const float* d_lp, long long base, int n) {
+QualityScore GpuMetricQ::add_completion_conf(double c, int n) {
+  if (n <= 0) throw ValidationError("logprobs: need at least one token");
+  if (n > max_tokens_) throw ValidationError("metricq: completion longer than the evaluator capacity");
+  return finish(nullptr, 0, n, &c);
+}
+
+QualityScore GpuMetricQ::finish(const float* d_lp, long long base, int n, const double* conf) {
   const int m = completions();
   if (m >= max_members_) throw ValidationError("metricq: exit group capacity exceeded");
   const long long hh = static_cast<long long>(hidden_) * hidden_;
-  double* corr_new = d_corrs_ + hh * m;
-  k::ee_confidence(d_lp + base, n, d_out_, st_);
-  k::ee_corr(d_emb_, n, hidden_, 1e-12, d_gram_, corr_new, st_);
-  k::ee_fcs(corr_new, d_corrs_, m, hidden_, d_out_ + 1, st_);
-  MOA_CUDA(cudaMemcpyAsync(h_out_, d_out_, sizeof(double) * (1 + m), cudaMemcpyDeviceToHost, st_));
+  if (!conf) k::ee_confidence(d_lp + base, n, d_out_, st_);
+  const int nout = cross_ ? 2 + m : 1 + m;  // C, FCS numerators (+ the self term on the n x n route)
+  if (cross_) {
+    const long long stride = static_cast<long long>(max_tokens_) * hidden_;
+    double* hat = d_hat_ + stride * m;
+    k::ee_colnorm(d_emb_, n, hidden_, 1e-12, hat, st_);
+    MOA_CUDA(cudaMemcpyAsync(d_nv_ + m, &n, sizeof(int), cudaMemcpyHostToDevice, st_));
+    const int nmax = nv_.empty() ? n : std::max(n, *std::max_element(nv_.begin(), nv_.end()));
+    k::ee_cross_sumsq(hat, n, d_hat_, d_nv_, nmax, stride, m, hidden_, d_part_, d_out_ + 1, st_);
+  } else {
+    double* corr_new = d_corrs_ + hh * m;
+    k::ee_corr(d_emb_, n, hidden_, 1e-12, d_gram_, corr_new, st_);
+    k::ee_fcs(corr_new, d_corrs_, m, hidden_, d_out_ + 1, st_);
+  }
+  MOA_CUDA(cudaMemcpyAsync(h_out_, d_out_, sizeof(double) * nout, cudaMemcpyDeviceToHost, st_));
   MOA_CUDA(cudaStreamSynchronize(st_));
   MOA_CUDA(cudaGetLastError());
-  const double c = h_out_[0];
+  const double c = conf ? *conf : h_out_[0];
+  if (cross_) {  // frob_cos_sim_corr from the cross / self sums of squares (metricq.cpp:55-64)
+    const double self = std::sqrt(h_out_[1 + m]);
+    for (int j = 0; j < m; ++j)
+      h_out_[1 + j] = (self == 0.0 || self_[static_cast<std::size_t>(j)] == 0.0)
+                          ? 0.0
+                          : h_out_[1 + j] / (self * self_[static_cast<std::size_t>(j)]);
+    self_.push_back(self);
+    nv_.push_back(n);
+  }
   if (!std::isfinite(c) || c > 1.0) throw ValidationError("logprobs: values must be finite and <= 0");
   // grow the sim matrix by one row/column (metricq.cpp:159-168)
   const int nn = m + 1;

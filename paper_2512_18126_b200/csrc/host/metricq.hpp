@@ -36,7 +36,11 @@ ExitDecision decide_exit(double q, rng::Stream& s);  // metricq.cpp:125-131
 
 // Incremental evaluator for one exit group over device-resident completions
 // (metricq.cpp:148-194).  The mock provider (hidden, seed) is the embedding
-// source (embedding.cpp:86-120).
+// source (embedding.cpp:86-120), or the caller writes the rows into
+// emb_buffer() (hidden-state / external providers).  Groups whose width
+// exceeds their longest completion (h > n) use the n x n cross-Gram route
+// (kernels/ee.cu): per completion the column-normalised rows and the norm of
+// its correlation are kept instead of an h x h correlation matrix.
 class GpuMetricQ {
  public:
   GpuMetricQ(int hidden, std::uint64_t seed, double tau, bool include_diagonal, int max_members,
@@ -50,6 +54,10 @@ class GpuMetricQ {
   QualityScore add_completion(const int* d_tok, const float* d_lp, long long base, int n);
   // Same with the embedding rows already in emb_buffer() (hidden-state provider).
   QualityScore add_completion_embedded(const float* d_lp, long long base, int n);
+  // Embedding rows already in emb_buffer(), confidence computed by the caller
+  // (host fp64 logprobs: geometric_mean_confidence, bit-exact).
+  QualityScore add_completion_conf(double c, int n);
+  bool cross_route() const { return cross_; }
   double* emb_buffer() { return d_emb_; }
   int hidden() const { return hidden_; }
   int completions() const { return static_cast<int>(conf_.size()); }
@@ -63,10 +71,12 @@ class GpuMetricQ {
     diag_ = include_diagonal;
     conf_.clear();
     sim_.clear();
+    nv_.clear();
+    self_.clear();
   }
 
  private:
-  QualityScore finish(const float* d_lp, long long base, int n);
+  QualityScore finish(const float* d_lp, long long base, int n, const double* conf = nullptr);
   QualityScore current() const;
   int hidden_;
   std::uint64_t seed_;
@@ -81,6 +91,13 @@ class GpuMetricQ {
   double* h_out_ = nullptr;    // pinned mirror
   std::vector<double> conf_;
   std::vector<double> sim_;  // n x n
+  // n x n route (hidden_ > max_tokens_)
+  bool cross_ = false;
+  double* d_hat_ = nullptr;   // [max_members][max_tokens][h] column-normalised rows
+  int* d_nv_ = nullptr;       // [max_members] rows per stored completion
+  double* d_part_ = nullptr;  // per-tile partial sums of squares
+  std::vector<int> nv_;
+  std::vector<double> self_;  // ||Corr||_F per stored completion
 };
 
 }  // namespace moa

@@ -207,9 +207,13 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
     o1.epi = d1.epi = k::kEpiResidual;
     nfold_ok_ = tc_ok_ && D % 16 == 0 && k::gemv_tc_norm_supported(q1) && k::gemv_tc_norm_supported(g1) &&
                 k::gemv_tc_supported(o1) && k::gemv_tc_supported(d1);
-    // one kernel fewer per normed GEMV: converter warps stage each k-tile of
-    // bf16(rmsnorm(x)) just in time beside the weight stream; MOA_NORM_FOLD=0 off
-    use_nfold_ = true;
+    // one kernel fewer per normed GEMV; the in-kernel staging puts the ssq
+    // and x reads on the critical path.  Default on up to d = 2048 (measured:
+    // 1B agents -3.5% per request); above, the wide GEMVs' K ranges exceed the
+    // staging (gemv_tc_norm_supported).  A just-in-time variant (converter warps
+    // filling each ring stage) was slower at every width: one dependent L2 round
+    // trip per k-tile on the converter's critical path.  MOA_NORM_FOLD=0/1 forces it
+    use_nfold_ = D <= 2048;
     if (const char* e = std::getenv("MOA_NORM_FOLD")) use_nfold_ = std::string(e) != "0";
   }
   MOA_CUDA(cudaMemsetAsync(gv_cnt_, 0, sizeof(int) * ((std::max({s.qkv_cols(), 2 * s.ffn, s.d}) + 127) / 128), st));

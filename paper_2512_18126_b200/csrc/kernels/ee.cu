@@ -3,8 +3,13 @@
 //   mock embed  hash rows, row-centred           embedding.cpp:91-113 (bit-exact)
 //   corr        cosine-normalised Gram t^T t     metricq.cpp:32-53, :157
 //   FCS         Frobenius cosine of two corrs    metricq.cpp:55-64
-// The h x h formulation is used (h = 64 for the preset provider, h <= n);
-// DESIGN.md §6 gives the n x n cross-Gram route for hidden-state widths.
+// Two formulations of the FCS (SURVEY.md §7 "FCS at model width"):
+//   h x h (h <= n, e.g. the preset mock h = 64): the reference's own route,
+//     Gram t^T t -> correlation -> Frobenius cosine of two h x h matrices;
+//   n x n (h > n, hidden-state widths): A_hat = A D^-1/2 (dead columns zero),
+//     <Corr U, Corr V>_F = ||A_hat B_hat^T||_F^2 and ||Corr U||_F =
+//     ||A_hat A_hat^T||_F -- n_u x n_v dot products of length h instead of
+//     two h x h matrices per completion.
 #include "kernels.cuh"
 
 namespace moa::k {
@@ -126,7 +131,96 @@ __global__ void fcs_kernel(const double* __restrict__ cu, const double* __restri
   }
 }
 
+// A_hat[r][c] = A[r][c] / sqrt(sum_r A[r][c]^2), 0 for columns <= eps (the
+// reference's dead-column rule, metricq.cpp:32-53); column sums sequential in r.
+__global__ void colnorm_kernel(const double* __restrict__ a, int n, int h, double eps, double* __restrict__ ahat) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= h) return;
+  double g = 0.0;
+  for (int r = 0; r < n; ++r) {
+    const double v = a[static_cast<long long>(r) * h + c];
+    g = __dadd_rn(g, __dmul_rn(v, v));
+  }
+  const double inv = g > eps ? 1.0 / sqrt(g) : 0.0;
+  for (int r = 0; r < n; ++r) ahat[static_cast<long long>(r) * h + c] = a[static_cast<long long>(r) * h + c] * inv;
+}
+
+// Sum of squares of X = U V_j^T (U: nu x h, V_j: the j-th stored completion,
+// nv[j] x h) per 32 x 32 output tile -> part[j][tile] (fixed order in-CTA);
+// blockIdx.z = j (j == m: V = U itself, the self term).
+constexpr int kXT = 32;
+__global__ void __launch_bounds__(256) cross_sumsq_kernel(const double* __restrict__ u, int nu,
+                                                          const double* __restrict__ vs, const int* __restrict__ nv,
+                                                          long long vstride, int m, int h, double* __restrict__ part,
+                                                          int tiles) {
+  __shared__ double As[kXT][kXT + 1], Bs[kXT][kXT + 1];
+  __shared__ double red[8];
+  const int j = blockIdx.z;
+  const double* v = j == m ? u : vs + vstride * j;
+  const int n2 = j == m ? nu : nv[j];
+  const int a0 = blockIdx.x * kXT, b0 = blockIdx.y * kXT;
+  const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // output (a0 + ty + 8i, b0 + tx)
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (a0 < nu && b0 < n2) {
+    for (int k0 = 0; k0 < h; k0 += kXT) {
+      for (int e = threadIdx.x; e < kXT * kXT; e += 256) {
+        const int rr = e / kXT, kk = e % kXT;
+        As[rr][kk] = (a0 + rr < nu && k0 + kk < h) ? u[static_cast<long long>(a0 + rr) * h + k0 + kk] : 0.0;
+        Bs[rr][kk] = (b0 + rr < n2 && k0 + kk < h) ? v[static_cast<long long>(b0 + rr) * h + k0 + kk] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int kk = 0; kk < kXT; ++kk) {
+        const double b = Bs[tx][kk];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = fma(As[ty + 8 * i][kk], b, acc[i]);
+      }
+      __syncthreads();
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s = fma(acc[i], acc[i], s);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (tx == 0) red[ty] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[static_cast<long long>(j) * tiles + tile] = t;
+  }
+}
+
+__global__ void sum_parts_kernel(const double* __restrict__ part, int tiles, double* __restrict__ out) {
+  const int j = blockIdx.x;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < tiles; ++i) t += part[static_cast<long long>(j) * tiles + i];
+    out[j] = t;
+  }
+}
+
 }  // namespace
+
+void ee_colnorm(const double* emb, int n, int h, double eps, double* ahat, cudaStream_t st) {
+  if (n > 0) colnorm_kernel<<<(h + 127) / 128, 128, 0, st>>>(emb, n, h, eps, ahat);
+}
+
+long long ee_cross_parts(int max_n, int max_members) {
+  const long long t = (max_n + kXT - 1) / kXT;
+  return t * t * (max_members + 1);
+}
+
+void ee_cross_sumsq(const double* ahat, int n, const double* stored, const int* d_nv, int n_max_stored,
+                    long long stride, int m, int h, double* part, double* out, cudaStream_t st) {
+  const int tx = (n + kXT - 1) / kXT;
+  const int n2 = n_max_stored > n ? n_max_stored : n;
+  const int ty = (n2 + kXT - 1) / kXT;
+  cross_sumsq_kernel<<<dim3(tx, ty, m + 1), 256, 0, st>>>(ahat, n, stored, d_nv, stride, m, h, part, tx * ty);
+  sum_parts_kernel<<<m + 1, 32, 0, st>>>(part, tx * ty, out);
+}
 
 void ee_confidence(const float* lp, int n, double* c, cudaStream_t st) {
   confidence_kernel<<<1, 32, 0, st>>>(lp, n, c);

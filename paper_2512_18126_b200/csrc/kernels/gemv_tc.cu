@@ -28,10 +28,10 @@ constexpr int kM = 128, kN = 16, kBK = 64, kStages = 5;  // 92 KB: two kernels' 
 constexpr int kTileW = kM * kBK * 2;  // 16 KB
 constexpr int kTileX = kN * kBK * 2;  // 2 KB
 constexpr int kSmem = kStages * (kTileW + kTileX) + 1024 + 256;
-// norm-from-x mode: two converter warps write each ring stage's X tile
-// bf16(x * inv_rms * g) just in time (no rmsnorm kernel, no TMA for X); the
-// stage's full barrier then takes the producer's arrival + 64 converter ones
-constexpr int kNxConv = 64;
+// norm-from-x mode: the CTA stages its K range of bf16(rmsnorm(x)) itself
+// (no rmsnorm kernel, no TMA for X): a 4-stage weight ring + <= 16 k-tiles
+constexpr int kNxStages = 4, kNxMaxKt = 16;
+constexpr int kNxSmem = kNxStages * kTileW + kNxMaxKt * kTileX + 1024 + 256;
 constexpr std::uint32_t kIdesc = idesc_bf16(kM, kN);
 
 // debug: per-CTA %globaltimer stamps (tools/gvisolated.py), off when null
@@ -220,11 +220,11 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
-  const bool nx = a.X != nullptr;  // norm-from-x: converter warps stage bf16(rmsnorm(x)), no X TMA
-  const int stages = kStages;
+  const bool nx = a.X != nullptr;  // norm-from-x: stage bf16(rmsnorm(x)) in smem, no X TMA
+  const int stages = nx ? kNxStages : kStages;
   unsigned char* sw = smem;
-  unsigned char* sx = smem + stages * kTileW;  // per-stage X tiles
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sx + kStages * kTileX);
+  unsigned char* sx = smem + stages * kTileW;  // per-stage X tiles, or the norm-from-x staging
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sx + (nx ? kNxMaxKt : kStages) * kTileX);
   std::uint64_t* empty = full + kStages;
   std::uint64_t* done = empty + kStages;
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
@@ -244,7 +244,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     prefetch_tmap(&map_w);
     if (!nx) prefetch_tmap(&map_x);
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], nx ? 1 + kNxConv : 1);
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
@@ -293,6 +293,60 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
       load_w(kt_issued, kt_issued);
     }
   }
+  if (nx) {
+    // Norm-from-x staging by all 128 threads (before the producer / MMA
+    // threads take their roles): inverse RMS of each row from the 16-column
+    // sums of squares its producer wrote, then this CTA's k-tiles of
+    // bf16(x * inv * g) in the 128B-swizzled K-major layout the MMA reads.
+    pdl_wait();
+    const int groups = a.K / 16;
+    {
+      const int r = threadIdx.x >> 3, j = threadIdx.x & 7;  // 8 threads per row
+      float ss = 0.f;
+      if (r < R)
+        for (int gidx = j; gidx < groups; gidx += 8) ss += __ldcg(a.ssq + static_cast<long long>(r) * groups + gidx);
+      ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+      ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+      ss += __shfl_xor_sync(0xffffffffu, ss, 4);
+      if (j == 0 && r < kN) inv_s[r] = r < R ? 1.0f / sqrtf(ss / static_cast<float>(a.K) + a.eps) : 0.f;
+    }
+    __syncthreads();
+    const int nchunk = kt_n * R * 8;  // (k-tile, row, 16-byte chunk); rows >= R feed ignored columns
+    for (int c0 = 0; c0 < nchunk; c0 += 128 * 8) {
+      float4 xa[8], xb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int ch = c0 + u * 128 + threadIdx.x;
+        if (ch >= nchunk) continue;
+        const int t = ch / (R * 8), r = (ch >> 3) % R, cc = ch & 7;
+        const float4* xp = reinterpret_cast<const float4*>(a.X + static_cast<long long>(r) * a.K + (kt0 + t) * kBK + cc * 8);
+        xa[u] = __ldg(xp);
+        xb[u] = __ldg(xp + 1);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int ch = c0 + u * 128 + threadIdx.x;
+        if (ch >= nchunk) continue;
+        const int t = ch / (R * 8), r = (ch >> 3) % R, cc = ch & 7;
+        const int col = (kt0 + t) * kBK + cc * 8;
+        const float4 g0 = __ldg(reinterpret_cast<const float4*>(a.g + col));
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(a.g + col + 4));
+        const float iv = inv_s[r];
+        __align__(16) bf16 o8[8];
+        o8[0] = __float2bfloat16_rn(xa[u].x * iv * g0.x);
+        o8[1] = __float2bfloat16_rn(xa[u].y * iv * g0.y);
+        o8[2] = __float2bfloat16_rn(xa[u].z * iv * g0.z);
+        o8[3] = __float2bfloat16_rn(xa[u].w * iv * g0.w);
+        o8[4] = __float2bfloat16_rn(xb[u].x * iv * g1.x);
+        o8[5] = __float2bfloat16_rn(xb[u].y * iv * g1.y);
+        o8[6] = __float2bfloat16_rn(xb[u].z * iv * g1.z);
+        o8[7] = __float2bfloat16_rn(xb[u].w * iv * g1.w);
+        *reinterpret_cast<uint4*>(sx + t * kTileX + r * 128 + ((cc ^ (r & 7)) * 16)) = *reinterpret_cast<const uint4*>(o8);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+  }
 
   if (warp == 0 && lane == 0) {
     // TMA producer (the rest of the weight stream; activations by TMA unless nx)
@@ -308,60 +362,6 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
       load_w(s, kt);
       if (!nx) tma_load_2d(sx + s * kTileX, &map_x, &full[s], (kt0 + kt) * kBK, 0);
     }
-  } else if (nx && warp >= 2) {
-    // Converters: inverse RMS of each row from the 16-column sums of squares
-    // its producer wrote, then per ring stage this CTA's k-tile of
-    // bf16(x * inv * g) in the 128B-swizzled K-major layout the MMA reads
-    // (4 threads per row, 16 columns each; x for the next k-tile is loaded
-    // while the current one waits for its stage).
-    const int ct = threadIdx.x - 64, r = ct >> 2, q4 = ct & 3;
-    pdl_wait();
-    const int groups = a.K / 16;
-    float ss = 0.f;
-    if (r < R)
-      for (int gi = q4; gi < groups; gi += 4) ss += __ldcg(a.ssq + static_cast<long long>(r) * groups + gi);
-    ss += __shfl_xor_sync(0xffffffffu, ss, 1);
-    ss += __shfl_xor_sync(0xffffffffu, ss, 2);
-    const float iv = r < R ? 1.0f / sqrtf(ss / static_cast<float>(a.K) + a.eps) : 0.f;
-    const float4* xr = reinterpret_cast<const float4*>(a.X + static_cast<long long>(r < R ? r : 0) * a.K);
-    float4 xv[4];
-    auto load_x = [&](int kt) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) xv[u] = r < R ? __ldcg(xr + ((kt0 + kt) * kBK + q4 * 16) / 4 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
-    };
-    load_x(0);
-    for (int kt = 0; kt < kt_n; ++kt) {
-      const int s = kt % stages;
-      float4 cur[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) cur[u] = xv[u];
-      if (kt + 1 < kt_n) load_x(kt + 1);
-      if (kt >= stages) mbar_wait(&empty[s], ((kt / stages) - 1) & 1);
-      if (r < R) {
-        const int col = (kt0 + kt) * kBK + q4 * 16;
-#pragma unroll
-        for (int hlf = 0; hlf < 2; ++hlf) {
-          const float4 a0 = cur[2 * hlf], a1 = cur[2 * hlf + 1];
-          const float4 one = make_float4(1.f, 1.f, 1.f, 1.f);
-          const float4 g0 = a.g ? __ldg(reinterpret_cast<const float4*>(a.g + col + hlf * 8)) : one;
-          const float4 g1 = a.g ? __ldg(reinterpret_cast<const float4*>(a.g + col + hlf * 8 + 4)) : one;
-          __align__(16) bf16 o8[8];
-          o8[0] = __float2bfloat16_rn(a0.x * iv * g0.x);
-          o8[1] = __float2bfloat16_rn(a0.y * iv * g0.y);
-          o8[2] = __float2bfloat16_rn(a0.z * iv * g0.z);
-          o8[3] = __float2bfloat16_rn(a0.w * iv * g0.w);
-          o8[4] = __float2bfloat16_rn(a1.x * iv * g1.x);
-          o8[5] = __float2bfloat16_rn(a1.y * iv * g1.y);
-          o8[6] = __float2bfloat16_rn(a1.z * iv * g1.z);
-          o8[7] = __float2bfloat16_rn(a1.w * iv * g1.w);
-          const int cc = q4 * 2 + hlf;  // 16-byte chunk of the 128-byte row
-          *reinterpret_cast<uint4*>(sx + s * kTileX + r * 128 + ((cc ^ (r & 7)) * 16)) =
-              *reinterpret_cast<const uint4*>(o8);
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&full[s]);
-    }
   } else if (warp == 1 && lane == 0) {
     for (int kt = 0; kt < kt_n; ++kt) {
       const int s = kt % stages;
@@ -369,7 +369,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
       if (kt == 0) gv_stamp(2);
       if (kt == 0) chain_mark(cst, 4);
       tc_fence_after();
-      const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + s * kTileX);
+      const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + (nx ? kt : s) * kTileX);
 #pragma unroll
       for (int k = 0; k < kBK / 16; ++k) umma_bf16(tmem, umma_desc(w0 + k * 32), umma_desc(x0 + k * 32), kIdesc, (kt | k) ? 1u : 0u);
       umma_commit(&empty[s]);
@@ -550,7 +550,6 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
         mbar_expect_tx(&full[q], wtx);
         load_w(q, q);
       }
-
       if (!fold) {
         pdl_wait();
         for (int j = 0; j < q; ++j) tma_load_2d(sx + j * kTileX, &map_x, &full[j], (j % KT) * kBK, 0);
@@ -790,7 +789,9 @@ long long gemv_tc_ws_floats(int N, int K) {
 }
 
 bool gemv_tc_norm_supported(const GemvArgs& a) {
-  return gemv_tc_supported(a) && a.K % 16 == 0 && a.ssq != nullptr;
+  const int S = gemv_tc_splits(a.N, a.K, a.epi);
+  const int KT = a.K / kBK;
+  return gemv_tc_supported(a) && (KT + S - 1) / S <= kNxMaxKt && a.K % 16 == 0 && a.ssq != nullptr;
 }
 
 bool gemv_tc_supported(const GemvArgs& a) {
@@ -800,7 +801,7 @@ bool gemv_tc_supported(const GemvArgs& a) {
 void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float* ws, int* cnt, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(gemv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem > kNxSmem ? kSmem : kNxSmem);
     uniform_carveout(reinterpret_cast<const void*>(gemv_tc_kernel));
     attr = true;
   }
@@ -808,7 +809,7 @@ void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float*
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((a.N + kM - 1) / kM, S);
   cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = kSmem;
+  cfg.dynamicSmemBytes = a.X ? kNxSmem : kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
   int na = 0;

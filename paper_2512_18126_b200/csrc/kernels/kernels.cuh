@@ -232,6 +232,14 @@ void ee_mock_embed(const int* out_tok, long long base, int n, int h, std::uint64
 void ee_hidden_embed(const float* x, int n, int d, double eps, double* emb, cudaStream_t st);
 // corr = correlation_from_gram(emb^T emb) (metricq.cpp:32-53), h x h.
 void ee_corr(const double* emb, int n, int h, double eps, double* gram, double* corr, cudaStream_t st);
+// n x n route (h > n): ahat = emb with each column scaled to unit norm (0 if
+// its sum of squares <= eps); out[j] = ||ahat . stored_j^T||_F^2 for j < m
+// (stored_j = stored + j * stride, d_nv[j] rows) and out[m] = ||ahat ahat^T||_F^2.
+// part >= ee_cross_parts(max rows, m) doubles.
+void ee_colnorm(const double* emb, int n, int h, double eps, double* ahat, cudaStream_t st);
+long long ee_cross_parts(int max_n, int max_members);
+void ee_cross_sumsq(const double* ahat, int n, const double* stored, const int* d_nv, int n_max_stored,
+                    long long stride, int m, int h, double* part, double* out, cudaStream_t st);
 // sim[j] = frob_cos_sim_corr(corr_new, corrs[j]) for j < m (metricq.cpp:55-64).
 void ee_fcs(const double* corr_new, const double* corrs, int m, int h, double* sim, cudaStream_t st);
 

@@ -678,3 +678,42 @@ def test_hidden_state_provider():
             assert bool(e["exited"]) == oe["exited"], e
             decisive += 1
     assert decisive >= 1
+
+
+# ---------------------------------------------------------------- MetricQ group handle
+@pytest.mark.parametrize("route", ["hxh", "nxn"])
+def test_mq_group_handle_vs_oracle(route):
+    """moa_mq_group_* (the reference's incremental MetricQEvaluator behind the
+    C-ABI) against the oracle evaluator: the mock provider on the device at
+    the preset width (h x h route), and caller-supplied embeddings at a
+    hidden-state width (h = 2048 > n: the n x n cross-Gram route), with exit
+    draws from the same RngStream.  q / sim to 1e-12 relative (fp64 on both
+    sides; summation order differs on the n x n route); draws bit-exact."""
+    rs = np.random.default_rng(3 if route == "hxh" else 4)
+    state = capi.rng_derive(12345, "ee:0")
+    st = orng.RngStream.derive_from(12345, "ee:0")
+    if route == "hxh":
+        hidden, lens = 64, [64, 40, 96, 64]
+        g = capi.MetricQGroup(hidden, provider_seed=7, max_members=4, max_tokens=128)
+        ev = mq.MetricQEvaluator(lambda t: mq.mock_embed(t, hidden, 7))
+    else:
+        hidden, lens = 2048, [200, 64, 300]
+        g = capi.MetricQGroup(hidden, max_members=3, max_tokens=320)
+        embs = [rs.standard_normal((n, hidden)) for n in lens]
+        embs[1][:, 5] = 0.0  # a dead column (<= eps) is zeroed on both routes
+        table = {i: e for i, e in enumerate(embs)}
+        ev = mq.MetricQEvaluator(lambda t: table[t[0]])
+    for i, n in enumerate(lens):
+        toks = [int(x) for x in rs.integers(0, 50000, n)]
+        lps = [float(-abs(x)) for x in rs.standard_normal(n) * 0.3]
+        got = g.add_completion(toks, lps) if route == "hxh" else g.add_embedded(embs[i], lps)
+        want = ev.add_completion(toks if route == "hxh" else [i] * n, lps)
+        for k in ("c_bar", "weight_sum", "weighted", "calibrated", "q"):
+            assert got[k] == pytest.approx(want[k], rel=1e-12, abs=1e-14), (route, i, k)
+        assert got["c"] == want["confidences"][-1]  # host fp64 sequential mean: bit-exact
+        assert np.allclose(got["sim"], want["sim"], rtol=1e-12, atol=1e-14), route
+        draw, exited, state = capi.decide_exit(got["q"], state)
+        d = mq.decide_exit(want["q"], st)
+        assert draw == d["draw"] and exited == d["exited"]
+    assert g.completions() == len(lens)
+    g.close()
