@@ -236,6 +236,58 @@ int moa_query_logprobs(const moa_query* q, int i, float* logprobs, float* entrop
 int moa_query_eval(const moa_query* q, int i, moa_eval_record* rec, double* sim_row, int cap);
 int moa_query_free(moa_query* q);
 
+/* ---- RunSummary (orchestrator.hpp:59-86, orchestrator.cpp:297-382) ------ */
+/* A request trace as summarize reads it (RunTrace after roll_up,
+ * trace.hpp:31-124): times in any one unit (the GPU engine reports device
+ * seconds).  Activation is keyed by model index (the reference keys it by
+ * model_tag; a caller maps tags to indices). */
+typedef struct {
+  double start, end;
+  int wasted;
+} moa_prefill_span;
+typedef struct {
+  int layer, position, model;
+  int invoked, pruned;
+  int prefill_only_calls, recomputed_tokens;
+  double complete_t;
+  int n_prefill;
+  const moa_prefill_span* prefill;
+} moa_trace_agent;
+typedef struct {
+  double e2e_latency;
+  double ee_latency_total;
+  int n_agents;
+  const moa_trace_agent* agents;
+} moa_trace_view;
+#define MOA_SUMMARY_MAX_MODELS 16
+typedef struct {
+  int samples;
+  double mean_e2e, p50_e2e, p95_e2e; /* percentile: linear interpolation, orchestrator.cpp:306-314 */
+  double mean_ee_share, mean_prefill_only_calls, mean_recomputed_tokens;
+  double prefill_share; /* critical_path_prefill_share averaged (orchestrator.cpp:325-350) */
+  int n_models;         /* activation rows 0..n_models-1 */
+  int instances[MOA_SUMMARY_MAX_MODELS], invoked[MOA_SUMMARY_MAX_MODELS], pruned[MOA_SUMMARY_MAX_MODELS];
+  double activation[MOA_SUMMARY_MAX_MODELS]; /* invoked (and not pruned) / instances */
+} moa_summary;
+/* summarize(cfg, traces) over caller-supplied traces; the topology is given
+ * as for moa_topology (kind 0 tree / 1 all-to-all). */
+int moa_summarize(int kind, int n_layers, const int* widths, const int* cluster_sizes, const moa_trace_view* traces,
+                  int n, moa_summary* out);
+/* percentile (orchestrator.cpp:306-314) of v[0..n) at p in [0, 1]. */
+int moa_percentile(const double* v, int n, double p, double* out);
+/* run_repetitions + summarize on the GPU engine: samples 0..repetitions-1,
+ * one request at a time, engine tracing on (per-tick device times), times in
+ * device seconds; e2e_latency = first tick -> last completion, ee latency =
+ * the time early-exit evaluations held the engine between ticks.
+ * per_sample (may be NULL) receives each request's moa_run_summary. */
+int moa_run_repetitions(moa_engine* eng, const moa_run_config* cfg, int repetitions, moa_summary* out,
+                        moa_run_summary* per_sample);
+/* The trace view of a finished request (needs engine tracing while it ran):
+ * *n_agents agents written to agents (cap), their prefill spans to spans
+ * (span_cap; agents[i].prefill points into spans). */
+int moa_query_trace_view(const moa_query* q, moa_trace_view* view, moa_trace_agent* agents, int cap,
+                         moa_prefill_span* spans, int span_cap, int* n_agents, int* n_spans);
+
 /* ---- early-exit signals (metricq.hpp:25-122, embedding.cpp:86-120) ------ */
 /* MockProvider::embed on the GPU: out[n][hidden] fp64, bit-exact. */
 int moa_mock_embed(const int32_t* tokens, int n, int hidden, uint64_t seed, double* out, int device);

@@ -308,6 +308,41 @@ json cmd_time_run_query(const json& req) {
               {"sink", sink}};
 }
 
+// run_repetitions + summarize as shipped (orchestrator.cpp:297-382), plus the
+// per-trace fields summarize reads, so the C-ABI's moa_summarize can be fed
+// the same traces (tests/test_summary.py).
+json cmd_summarize(const json& req) {
+  RunConfig cfg = config_from(req);
+  cfg.repetitions = req.value("reps", 24);
+  if (req.contains("ee_eval_latency")) cfg.ee_eval_latency = req.at("ee_eval_latency").get<double>();
+  std::vector<RunTrace> traces = run_repetitions(cfg);
+  json tj = json::array();
+  for (const auto& t : traces) {
+    json agents = json::array();
+    for (const auto& [id, a] : t.agents) {
+      json pf = json::array();
+      for (const auto& p : a.prefill) pf.push_back({p.start, p.end, p.wasted});
+      agents.push_back({{"layer", id.layer},
+                        {"position", id.position},
+                        {"model_tag", a.model_tag},
+                        {"invoked", a.invoked},
+                        {"pruned", a.pruned},
+                        {"prefill_only_calls", a.prefill_only_calls},
+                        {"recomputed_tokens", a.recomputed_tokens},
+                        {"complete_t", a.complete_t},
+                        {"prefill", pf}});
+    }
+    tj.push_back({{"e2e_latency", t.e2e_latency},
+                  {"ee_latency_total", t.ee_latency_total},
+                  {"prefill_share", critical_path_prefill_share(cfg.topology, t)},
+                  {"agents", agents}});
+  }
+  json out;
+  out["summary"] = summarize(cfg, traces).to_json();
+  out["traces"] = tj;
+  return out;
+}
+
 json cmd_rng(const json& req) {
   std::uint64_t seed = req.value("seed", std::uint64_t{0});
   std::string label = req.value("label", std::string(""));
@@ -346,6 +381,7 @@ extern "C" const char* moaref_call(const char* request) {
     else if (cmd == "run_query") out = cmd_run_query(req);
     else if (cmd == "time_run_query") out = cmd_time_run_query(req);
     else if (cmd == "rng") out = cmd_rng(req);
+    else if (cmd == "summarize") out = cmd_summarize(req);
     else out = json{{"error", "unknown"}, {"what", cmd}};
   } catch (const ValidationError& e) {
     out = json{{"error", "ValidationError"}, {"what", e.what()}};

@@ -88,6 +88,46 @@ class EvalRecordC(C.Structure):
                 + [("pruned_layer", C.c_int * 16), ("pruned_position", C.c_int * 16)])
 
 
+class PrefillSpan(C.Structure):
+    _fields_ = [("start", C.c_double), ("end", C.c_double), ("wasted", C.c_int)]
+
+
+class TraceAgent(C.Structure):
+    _fields_ = [("layer", C.c_int), ("position", C.c_int), ("model", C.c_int), ("invoked", C.c_int),
+                ("pruned", C.c_int), ("prefill_only_calls", C.c_int), ("recomputed_tokens", C.c_int),
+                ("complete_t", C.c_double), ("n_prefill", C.c_int), ("prefill", C.POINTER(PrefillSpan))]
+
+
+class TraceView(C.Structure):
+    _fields_ = [("e2e_latency", C.c_double), ("ee_latency_total", C.c_double), ("n_agents", C.c_int),
+                ("agents", C.POINTER(TraceAgent))]
+
+
+SUMMARY_MAX_MODELS = 16
+
+
+class Summary(C.Structure):
+    _fields_ = [("samples", C.c_int), ("mean_e2e", C.c_double), ("p50_e2e", C.c_double), ("p95_e2e", C.c_double),
+                ("mean_ee_share", C.c_double), ("mean_prefill_only_calls", C.c_double),
+                ("mean_recomputed_tokens", C.c_double), ("prefill_share", C.c_double), ("n_models", C.c_int),
+                ("instances", C.c_int * SUMMARY_MAX_MODELS), ("invoked", C.c_int * SUMMARY_MAX_MODELS),
+                ("pruned", C.c_int * SUMMARY_MAX_MODELS), ("activation", C.c_double * SUMMARY_MAX_MODELS)]
+
+    def to_dict(self, model_tags=None):
+        """RunSummary::to_json field names (orchestrator.cpp:383-402); activation keyed by tag."""
+        act = {}
+        for m in range(self.n_models):
+            if self.instances[m] == 0:
+                continue
+            tag = model_tags[m] if model_tags else str(m)
+            act[tag] = dict(instances=self.instances[m], invoked=self.invoked[m], pruned=self.pruned[m],
+                            activation=self.activation[m])
+        return dict(samples=self.samples, mean_e2e=self.mean_e2e, p50_e2e=self.p50_e2e, p95_e2e=self.p95_e2e,
+                    mean_ee_latency_share=self.mean_ee_share, mean_prefill_only_calls=self.mean_prefill_only_calls,
+                    mean_recomputed_tokens=self.mean_recomputed_tokens,
+                    critical_path_prefill_share=self.prefill_share, activation=act)
+
+
 _lib = None
 
 _SIGS = {
@@ -135,6 +175,11 @@ _SIGS = {
     "moa_query_logprobs": ([C.c_void_p, C.c_int, _P(C.c_float), _P(C.c_float), C.c_int, _P(C.c_int)], C.c_int),
     "moa_query_eval": ([C.c_void_p, C.c_int, _P(EvalRecordC), _P(C.c_double), C.c_int], C.c_int),
     "moa_query_free": ([C.c_void_p], C.c_int),
+    "moa_summarize": ([C.c_int, C.c_int, _P(C.c_int), _P(C.c_int), _P(TraceView), C.c_int, _P(Summary)], C.c_int),
+    "moa_percentile": ([_P(C.c_double), C.c_int, C.c_double, _P(C.c_double)], C.c_int),
+    "moa_run_repetitions": ([C.c_void_p, _P(RunConfigC), C.c_int, _P(Summary), C.c_void_p], C.c_int),
+    "moa_query_trace_view": ([C.c_void_p, _P(TraceView), _P(TraceAgent), C.c_int, _P(PrefillSpan), C.c_int,
+                              _P(C.c_int), _P(C.c_int)], C.c_int),
     "moa_mock_embed": ([_P(C.c_int32), C.c_int, C.c_int, C.c_uint64, _P(C.c_double), C.c_int], C.c_int),
     "moa_metricq_run": ([_P(C.c_int32), _P(C.c_float), _P(C.c_int), C.c_int, C.c_int, C.c_uint64, C.c_double,
                          C.c_int, C.c_uint64, C.c_char_p, _P(C.c_double), _P(C.c_double), _P(C.c_int),
@@ -361,6 +406,15 @@ class Engine:
             out.append(res)
         return out
 
+    def run_repetitions(self, cfg: "QueryConfig", repetitions: int):
+        """run_repetitions + summarize (orchestrator.cpp:297-382) on the GPU: samples
+        0..repetitions-1, device seconds.  Returns (summary dict, per-sample summaries)."""
+        out = Summary()
+        per = (RunSummary * repetitions)()
+        check(lib().moa_run_repetitions(self.h, C.byref(cfg.c), int(repetitions), C.byref(out), per))
+        rows = [{k: getattr(per[i], k) for k, _ in RunSummary._fields_} for i in range(repetitions)]
+        return out.to_dict(cfg.model_tags), rows
+
     def trace(self, enable: bool = True):
         """Record per-tick device times so run_query(..., trace=True) returns a RunTrace JSONL."""
         check(lib().moa_engine_trace(self.h, int(enable)))
@@ -386,9 +440,27 @@ class Engine:
                     tb = (C.c_double * max(1, nt.value))()
                     check(lib().moa_query_ticks(q, tb, nt.value, C.byref(nt)))
                     res["tick_ms"] = list(tb[: nt.value])
+                    res["trace_view"] = _trace_view(q, cfg.model_tags)
             finally:
                 lib().moa_query_free(q)
         return res
+
+
+def _trace_view(q, model_tags):
+    """moa_query_trace_view as the dict capi.summarize takes (device seconds)."""
+    na, ns = C.c_int(), C.c_int()
+    check(lib().moa_query_trace_view(q, None, None, 0, None, 0, C.byref(na), C.byref(ns)))
+    ags, sps, view = (TraceAgent * max(1, na.value))(), (PrefillSpan * max(1, ns.value))(), TraceView()
+    check(lib().moa_query_trace_view(q, C.byref(view), ags, na.value, sps, ns.value, C.byref(na), C.byref(ns)))
+    agents = []
+    for i in range(na.value):
+        a = ags[i]
+        agents.append(dict(layer=a.layer, position=a.position, model_tag=model_tags[a.model], invoked=bool(a.invoked),
+                           pruned=bool(a.pruned), prefill_only_calls=a.prefill_only_calls,
+                           recomputed_tokens=a.recomputed_tokens, complete_t=a.complete_t,
+                           prefill=[(a.prefill[j].start, a.prefill[j].end, bool(a.prefill[j].wasted))
+                                    for j in range(a.n_prefill)]))
+    return dict(e2e_latency=view.e2e_latency, ee_latency_total=view.ee_latency_total, agents=agents)
 
 
 def _query_detail(q, s, resolve):
@@ -430,6 +502,7 @@ class QueryConfig:
         widths = list(t["widths"])
         L = len(widths)
         self._keep = []
+        self.model_tags = [k for k, _ in sorted(model_index.items(), key=lambda kv: kv[1])]
 
         def arr(v, ty=C.c_int):
             a = (ty * max(1, len(v)))(*v)
@@ -667,3 +740,39 @@ class SlotPlan:
             self.close()
         except Exception:
             pass
+
+
+def summarize(topology: dict, traces, model_index: dict):
+    """moa_summarize over traces given as dicts {e2e_latency, ee_latency_total,
+    agents: [{layer, position, model_tag, invoked, pruned, prefill_only_calls,
+    recomputed_tokens, complete_t, prefill: [(start, end, wasted)]}]}."""
+    kind = 1 if topology["kind"] == "all_to_all" else 0
+    widths = topology["widths"]
+    w = (C.c_int * len(widths))(*widths)
+    cs = None
+    if kind == 0:
+        br = topology.get("branching", [])
+        sizes = [br[l] for l in range(len(widths) - 1) for _ in range(widths[l + 1])]
+        cs = (C.c_int * max(1, len(sizes)))(*sizes)
+    keep, views = [], (TraceView * max(1, len(traces)))()
+    for i, t in enumerate(traces):
+        ags = (TraceAgent * max(1, len(t["agents"])))()
+        for k, a in enumerate(t["agents"]):
+            sp = (PrefillSpan * max(1, len(a["prefill"])))(*[PrefillSpan(p[0], p[1], int(p[2])) for p in a["prefill"]])
+            keep.append(sp)
+            ags[k] = TraceAgent(a["layer"], a["position"], model_index[a["model_tag"]], int(a["invoked"]),
+                                int(a["pruned"]), a["prefill_only_calls"], a["recomputed_tokens"], a["complete_t"],
+                                len(a["prefill"]), sp)
+        keep.append(ags)
+        views[i] = TraceView(t["e2e_latency"], t["ee_latency_total"], len(t["agents"]), ags)
+    out = Summary()
+    check(lib().moa_summarize(kind, len(widths), w, cs, views, len(traces), C.byref(out)))
+    tags = {v: k for k, v in model_index.items()}
+    return out.to_dict([tags.get(m, str(m)) for m in range(out.n_models)])
+
+
+def percentile(v, p: float) -> float:
+    arr = (C.c_double * max(1, len(v)))(*v)
+    out = C.c_double()
+    check(lib().moa_percentile(arr, len(v), float(p), C.byref(out)))
+    return out.value

@@ -12,6 +12,7 @@
 #include "graph.hpp"
 #include "metricq.hpp"
 #include "orchestrator.hpp"
+#include "summary.hpp"
 
 struct moa_engine {
   std::unique_ptr<moa::GpuEngine> eng;
@@ -572,6 +573,130 @@ int moa_query_eval(const moa_query* q, int i, moa_eval_record* rec, double* sim_
 
 int moa_query_free(moa_query* q) {
   return guard([&] { delete q; });
+}
+
+namespace {
+
+void fill_summary(const moa::RunSummary& s, moa_summary* out) {
+  *out = moa_summary{};
+  out->samples = s.samples;
+  out->mean_e2e = s.mean_e2e;
+  out->p50_e2e = s.p50_e2e;
+  out->p95_e2e = s.p95_e2e;
+  out->mean_ee_share = s.mean_ee_share;
+  out->mean_prefill_only_calls = s.mean_prefill_only_calls;
+  out->mean_recomputed_tokens = s.mean_recomputed_tokens;
+  out->prefill_share = s.prefill_share;
+  for (const auto& [m, a] : s.activation_counts) {
+    if (m < 0 || m >= MOA_SUMMARY_MAX_MODELS) throw moa::ValidationError("summarize: model index out of range");
+    out->n_models = std::max(out->n_models, m + 1);
+    out->instances[m] = a.instances;
+    out->invoked[m] = a.invoked;
+    out->pruned[m] = a.pruned;
+    out->activation[m] = s.activation.at(m);
+  }
+}
+
+void fill_run_summary(const moa::QueryResult& r, moa_run_summary& s) {
+  s.ticks = r.ticks;
+  s.n_agents = static_cast<int>(r.agents.size());
+  s.n_evals = static_cast<int>(r.metricq.size());
+  s.forwards = r.forwards;
+  s.tokens = r.tokens;
+  s.decoded_tokens = r.decoded_tokens;
+  s.rows = r.rows;
+  s.e2e_ms = r.e2e_ms;
+  s.wall_ms = r.wall_ms;
+  s.weight_bytes = r.weight_bytes;
+  s.host_ms = r.host_ms;
+  s.host_wait_ms = r.host_wait_ms;
+}
+
+}  // namespace
+
+int moa_summarize(int kind, int n_layers, const int* widths, const int* cluster_sizes, const moa_trace_view* traces,
+                  int n, moa_summary* out) {
+  return guard([&] {
+    need(out, "out");
+    if (n < 0) throw moa::ValidationError("summarize: n must be >= 0");
+    if (n > 0) need(traces, "traces");
+    const moa::Topology topo = topology_of(kind, n_layers, widths, cluster_sizes);
+    std::vector<moa::TraceView> views;
+    for (int i = 0; i < n; ++i) {
+      const moa_trace_view& t = traces[i];
+      if (t.n_agents < 0 || (t.n_agents > 0 && !t.agents)) throw moa::ValidationError("summarize: bad trace agents");
+      moa::TraceView v;
+      v.e2e_latency = t.e2e_latency;
+      v.ee_latency_total = t.ee_latency_total;
+      for (int k = 0; k < t.n_agents; ++k) {
+        const moa_trace_agent& a = t.agents[k];
+        if (a.n_prefill < 0 || (a.n_prefill > 0 && !a.prefill))
+          throw moa::ValidationError("summarize: bad prefill spans");
+        moa::TraceAgent ta;
+        ta.model = a.model;
+        ta.invoked = a.invoked != 0;
+        ta.pruned = a.pruned != 0;
+        ta.prefill_only_calls = a.prefill_only_calls;
+        ta.recomputed_tokens = a.recomputed_tokens;
+        ta.complete_t = a.complete_t;
+        for (int j = 0; j < a.n_prefill; ++j)
+          ta.prefill.push_back(moa::TracePrefill{a.prefill[j].start, a.prefill[j].end, a.prefill[j].wasted != 0});
+        v.agents[moa::AgentId{a.layer, a.position}] = std::move(ta);
+      }
+      views.push_back(std::move(v));
+    }
+    fill_summary(moa::summarize(topo, views), out);
+  });
+}
+
+int moa_percentile(const double* v, int n, double p, double* out) {
+  return guard([&] {
+    need(out, "out");
+    if (n < 0) throw moa::ValidationError("percentile: n must be >= 0");
+    if (n > 0) need(v, "v");
+    *out = moa::percentile(std::vector<double>(v, v + n), p);
+  });
+}
+
+int moa_run_repetitions(moa_engine* eng, const moa_run_config* cfg, int repetitions, moa_summary* out,
+                        moa_run_summary* per_sample) {
+  return guard([&] {
+    need(out, "out");
+    const moa::RunConfig rc = run_config_of(cfg);
+    const auto rs = moa::run_repetitions(E(eng), rc, repetitions, false);
+    std::vector<moa::TraceView> views;
+    for (std::size_t i = 0; i < rs.size(); ++i) {
+      views.push_back(moa::trace_view(rs[i]));
+      if (per_sample) fill_run_summary(rs[i], per_sample[i]);
+    }
+    fill_summary(moa::summarize(rc.topology, views), out);
+  });
+}
+
+int moa_query_trace_view(const moa_query* q, moa_trace_view* view, moa_trace_agent* agents, int cap,
+                         moa_prefill_span* spans, int span_cap, int* n_agents, int* n_spans) {
+  return guard([&] {
+    need(q, "query");
+    const moa::TraceView v = moa::trace_view(q->r);
+    int na = 0, ns = 0;
+    for (const auto& [id, a] : v.agents) {
+      const int first = ns;
+      for (const auto& p : a.prefill) {
+        if (spans && ns < span_cap) spans[ns] = moa_prefill_span{p.start, p.end, p.wasted ? 1 : 0};
+        ++ns;
+      }
+      if (agents && na < cap) {
+        agents[na] = moa_trace_agent{id.layer, id.position, a.model, a.invoked ? 1 : 0, a.pruned ? 1 : 0,
+                                     a.prefill_only_calls, a.recomputed_tokens, a.complete_t,
+                                     static_cast<int>(a.prefill.size()),
+                                     spans && ns <= span_cap ? spans + first : nullptr};
+      }
+      ++na;
+    }
+    if (view) *view = moa_trace_view{v.e2e_latency, v.ee_latency_total, std::min(na, cap), agents};
+    if (n_agents) *n_agents = na;
+    if (n_spans) *n_spans = ns;
+  });
 }
 
 int moa_mock_embed(const int32_t* tokens, int n, int hidden, uint64_t seed, double* out, int device) {

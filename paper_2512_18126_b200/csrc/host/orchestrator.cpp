@@ -219,6 +219,12 @@ struct Request {
       }
       ExitGroup* grp = it->second;
       eng.defer([this, producer, grp]() {
+        const auto t0 = std::chrono::steady_clock::now();
+        struct Clock {  // ee_latency_total analogue (orchestrator.cpp:236-240)
+          std::chrono::steady_clock::time_point t0;
+          double& acc;
+          ~Clock() { acc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
+        } clock{t0, res.ee_ms};
         MetricQRecord rec;
         rec.tick = eng.tick();
         rec.group = grp->index;

@@ -74,6 +74,7 @@ struct QueryResult {
   int forwards = 0;
   double host_ms = 0.0;       // host time inside engine ticks
   double host_wait_ms = 0.0;  // of which: blocked on the GPU (the host is ahead)
+  double ee_ms = 0.0;         // host time the early-exit evaluations held the engine between ticks
   // trace context (RunTrace JSONL, trace.hpp)
   std::vector<double> tick_ms;  // device ms at the end of each tick (engine tracing on)
   std::vector<std::string> model_tags;

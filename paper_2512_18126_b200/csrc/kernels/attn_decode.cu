@@ -2,9 +2,10 @@
 // §2.2): the row's KV prefix is cut into fixed splits of KEYS keys, one CTA
 // per (row, kv head, split).  A CTA stages its whole split of K and V with
 // TMA (64-key boxes, 128B-swizzled, 64-column subtiles) behind one mbarrier:
-// boxes that do not hold the tick's new key are issued before the
+// boxes below the first key written in this tick are issued before the
 // programmatic-dependent-launch wait (the previous kernel of the chain writes
-// only the key at `pos`), so the KV stream overlaps the QKV GEMV's tail.  The
+// the keys of this tick's rows: `pos`, and the earlier rows of an agent's
+// incremental-prefill run), so the KV stream overlaps the QKV GEMV's tail.  The
 // group's q heads are the M rows of mma.sync m16n8k16 tiles; each of the 4
 // warps takes KEYS/4 keys: S = Q.K^T, masked online softmax on the fragments,
 // O += P.V with V^T fragments from ldmatrix.trans; the warps combine in smem in
@@ -72,7 +73,28 @@ attention_decode_tma_kernel(const __grid_constant__ CUtensorMap kmap, const __gr
   const int hpg = nh / nkv;
   const int kb = s * C::KEYS, ke = min(n, kb + C::KEYS);
   const int nbox = (ke - kb + 63) / 64;
-  const int newbox = rd.pos >= kb && rd.pos < ke ? (rd.pos - kb) / 64 : -1;  // box holding this tick's new key
+  // First key written in this tick: the row's own key, or the first key of the
+  // run of consecutive rows of the same agent it ends (incremental-prefill
+  // rows of one agent share a tick and see each other's keys).  Warp 0 walks
+  // back 32 rows per step (tick metadata: readable before the PDL wait).
+  int first_new = rd.pos;
+  if (warp == 0) {
+    int base = r - 1, p = rd.pos - 1;
+    for (;;) {
+      const int rr = base - lane;
+      const bool c = rr >= 0 && rows[rr].kv == rd.kv && rows[rr].pos == p - lane;
+      const unsigned b = __ballot_sync(kAll, c);
+      if (b == kAll) {
+        base -= 32;
+        p -= 32;
+        continue;
+      }
+      first_new = p - (__ffs(~b) - 1) + 1;
+      break;
+    }
+  }
+  // boxes from this one on hold keys the previous kernel writes: issued after the wait
+  const int newbox = first_new < ke ? max(0, first_new - kb) / 64 : nbox;
   const int row0 = static_cast<int>((rd.kv * kv_stride + layer_off) / HD + static_cast<long long>(g) * max_ctx + kb);
   auto load_box = [&](int b) {
 #pragma unroll
@@ -87,12 +109,12 @@ attention_decode_tma_kernel(const __grid_constant__ CUtensorMap kmap, const __gr
     mbar_init(full, 1);
     mbar_fence_init();
     mbar_expect_tx(full, static_cast<std::uint32_t>(nbox * C::SUB * 2 * 64 * 128));
-    for (int b = 0; b < nbox; ++b)
-      if (b != newbox) load_box(b);  // keys of earlier ticks: not written by the previous kernel
+    for (int b = 0; b < newbox; ++b) load_box(b);  // keys of earlier ticks: not written by the previous kernel
   }
   pdl_wait();
   pdl_launch_dependents();
-  if (threadIdx.x == 0 && newbox >= 0) load_box(newbox);
+  if (threadIdx.x == 0)
+    for (int b = newbox; b < nbox; ++b) load_box(b);
   for (int c = threadIdx.x; c < 16 * (HD / 8); c += 128) {
     const int hr = c / (HD / 8), ch = c % (HD / 8);
     uint4 v = make_uint4(0, 0, 0, 0);

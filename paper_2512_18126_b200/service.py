@@ -113,12 +113,19 @@ class EngineService:
 
     # -- bookkeeping ------------------------------------------------------
     def _state(self, agent: str):
+        """Request state keyed by the parsed AgentId (so "01:0" and "1:0" are one
+        agent, as AgentId::parse makes them); the engine slot is bound only
+        once a request has passed validation (_bind)."""
         a = parse_agent(agent)  # rejects malformed ids
-        r = self._req.get(agent)
+        r = self._req.get(a)
         if r is None:
-            self.eng.add_agent(a, self.model_for(a))
-            r = self._req[agent] = {"id": a, "prompt": [], "generated": False}
+            r = self._req[a] = {"id": a, "prompt": [], "generated": False, "bound": False}
         return r
+
+    def _bind(self, r):
+        if not r["bound"]:
+            self.eng.add_agent(r["id"], self.model_for(r["id"]))
+            r["bound"] = True
 
     def _drive(self):
         """Tick the engine until it is idle; returns its events."""
@@ -158,6 +165,7 @@ class EngineService:
                                       f"{scheduled} tokens are scheduled")
             t_start = t_end = self._now
             if tokens:
+                self._bind(r)
                 self.eng.prefill_only(r["id"], start, tokens)
                 r["prompt"] += tokens
                 self._drive()
@@ -187,6 +195,7 @@ class EngineService:
             if chunk <= 0:
                 raise ValidationError("body.chunk_size: must be > 0")
             remainder = len(prompt) - len(have)
+            self._bind(r)
             self.eng.generate(r["id"], prompt, n, chunk)
             r["prompt"] = list(prompt)
             r["generated"] = True
@@ -212,7 +221,8 @@ class EngineService:
             scheduled = len(r["prompt"])
             if keep < 0 or keep > scheduled:
                 raise ValidationError(f"reclaim point {keep} outside scheduled prompt of {scheduled} tokens")
-            self.eng.reclaim(r["id"], keep)
+            if r["bound"]:
+                self.eng.reclaim(r["id"], keep)
             del r["prompt"][keep:]
             return {"agent": agent, "scheduled": keep}
 

@@ -171,9 +171,42 @@ def gen_metricq():
     dump("metricq.json", cases)
 
 
+SUMMARY_CASES = [
+    dict(topology=dict(kind="tree", widths=[4, 2, 1], branching=[2, 2]), assign=[["leaf"], ["agg"], ["agg"]],
+         profiles={"leaf": {"output_len": 64}, "agg": {"output_len": 64}}, early_exit=False, reps=6),
+    dict(topology=dict(kind="tree", widths=[4, 2, 1], branching=[2, 2]), assign=[["leaf"], ["agg"], ["agg"]],
+         profiles={"leaf": {"output_min": 24, "output_max": 96}, "agg": {"output_len": 64}}, early_exit=True,
+         reps=8),
+    dict(topology=dict(kind="tree", widths=[9, 3, 1], branching=[3, 3]), assign=[["4b", "8b", "32b"], ["agg"], ["root"]],
+         profiles={"4b": {"output_min": 100, "output_max": 400}, "8b": {"output_len": 200},
+                   "32b": {"output_len": 300, "prefill_rate": 2000.0}, "agg": {"output_len": 150},
+                   "root": {"output_len": 120}},
+         early_exit=True, ee_eval_latency=0.25, reps=6),
+    dict(topology=dict(kind="tree", widths=[9, 3, 1], branching=[3, 3]), assign=[["leaf"], ["agg"], ["agg"]],
+         profiles={"leaf": {"output_len": 64}, "agg": {"output_len": 64}}, early_exit=True, force_q=1.0, reps=3),
+    dict(topology=dict(kind="all_to_all", widths=[6, 6, 1]), assign=[["leaf"], ["agg"], ["agg"]],
+         profiles={"leaf": {"output_min": 30, "output_max": 90}, "agg": {"output_len": 64}}, early_exit=True,
+         mode="sequential-pd", reps=5),
+    dict(topology=dict(kind="tree", widths=[8, 2, 1], branching=[4, 2]), assign=[["leaf"], ["agg"], ["agg"]],
+         profiles={"leaf": {"output_len": 512}, "agg": {"output_len": 512}}, early_exit=False, mode="dp-chunked-prefill",
+         reps=4),
+]
+
+
+def gen_summary():
+    """RunSummary of the reference's own run_repetitions (orchestrator.cpp:297-382)
+    with the per-trace fields summarize reads."""
+    cases = []
+    for c in SUMMARY_CASES:
+        req = {"cmd": "summarize", "chunk_size": 32, "seed": 7, **c}
+        cases.append(dict(spec=c, out=ref(req)))
+    dump("summary.json", cases)
+
+
 if __name__ == "__main__":
     gen_rng()
     gen_topology()
     gen_slotplan()
     gen_mock_embed()
     gen_metricq()
+    gen_summary()

@@ -717,3 +717,44 @@ def test_mq_group_handle_vs_oracle(route):
         assert draw == d["draw"] and exited == d["exited"]
     assert g.completions() == len(lens)
     g.close()
+
+
+def test_run_repetitions_summary():
+    """moa_run_repetitions (run_repetitions + summarize, orchestrator.cpp:297-382)
+    on the GPU: the summary is the reference's summarize applied to the GPU
+    requests' own trace views (device seconds), and its activation counts are
+    those of the per-request agent records."""
+    eng, qc = capi.engine_for(C1U)
+    try:
+        summ, per = eng.run_repetitions(qc, 4)
+        # the same requests one by one, traced, re-summarised through moa_summarize
+        eng.trace(True)
+        traces, act = [], {}
+        for s in range(4):
+            r = eng.run_query(qc, sample=s, resolve=False, detail=True, trace=True)
+            assert r["tokens"] == per[s]["tokens"] and r["ticks"] == per[s]["ticks"]
+            traces.append(r["trace_view"])
+            for a in r["agents"].values():
+                v = act.setdefault(qc.model_tags[a["model"]], [0, 0, 0])
+                v[0] += 1
+                v[1] += a["invoked"] and not a["pruned"]
+                v[2] += a["pruned"]
+        eng.trace(False)
+    finally:
+        eng.close()
+    assert summ["samples"] == 4
+    e2e = sorted(p["e2e_ms"] / 1e3 for p in per)
+    assert summ["p50_e2e"] == pytest.approx(capi.percentile(e2e, 0.5), rel=1e-12)
+    assert summ["p95_e2e"] == pytest.approx(capi.percentile(e2e, 0.95), rel=1e-12)
+    assert summ["mean_e2e"] == pytest.approx(sum(e2e) / 4, rel=1e-12)
+    assert 0.0 < summ["critical_path_prefill_share"] < 1.0
+    assert 0.0 <= summ["mean_ee_latency_share"] < 1.0
+    assert summ["mean_recomputed_tokens"] == 0.0
+    for tag, (inst, inv, pr) in act.items():
+        a = summ["activation"][tag]
+        assert (a["instances"], a["invoked"], a["pruned"]) == (inst, inv, pr)
+    assert any(a["pruned"] for a in summ["activation"].values())  # C1U prunes
+    # device-time traces of the re-run requests summarise to the same shape
+    s2 = capi.summarize(C1U["topology"], traces, {t: i for i, t in enumerate(qc.model_tags)})
+    assert s2["samples"] == 4 and 0.0 < s2["critical_path_prefill_share"] < 1.0
+    assert s2["activation"] == summ["activation"]
