@@ -33,6 +33,10 @@ extern "C" {
 #define MOA_ERR_RUNTIME 3    /* RunError        (errors.hpp:17-20)            */
 #define MOA_ERR_DEVICE 4     /* CUDA failure (a RunError on the reference side) */
 #define MOA_ERR_UNSUPPORTED 5
+/* ProviderError kinds (errors.hpp:24-33), raised by an EmbeddingProvider */
+#define MOA_ERR_PROVIDER_TRANSPORT 6
+#define MOA_ERR_PROVIDER_CREDENTIALS 7
+#define MOA_ERR_PROVIDER_BAD_RESPONSE 8
 
 typedef struct moa_engine moa_engine;
 typedef struct moa_query moa_query;
@@ -165,6 +169,14 @@ typedef struct {
   uint64_t provider_seed;
   int embed_model; /* -1: MockProvider; >= 0: hidden states of this engine model (EmbeddingProvider,
                       embedding.hpp:38-44; width = its d_model) */
+  /* Caller-supplied EmbeddingProvider (embedding.hpp:38-44), used when
+   * non-NULL (embed_model must be -1): embed_fn(user, tokens, n, hidden, out)
+   * fills out[n][hidden] (row-major fp64) with the completion's embedding and
+   * returns MOA_OK, or MOA_ERR_PROVIDER_* (the request then fails with that
+   * code; moa_last_error reports the provider).  Called on the thread running
+   * the request, between engine ticks, once per early-exit evaluation. */
+  int (*embed_fn)(void* user, const int32_t* tokens, int n, int hidden, double* out);
+  void* embed_user;
 } moa_run_config;
 
 typedef struct {

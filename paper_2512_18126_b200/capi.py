@@ -16,6 +16,7 @@ from . import configs as _configs
 LIB_PATH = Path(__file__).resolve().parent / "libmoa_b200.so"
 
 MOA_OK, MOA_ERR_VALIDATION, MOA_ERR_RUNTIME, MOA_ERR_DEVICE, MOA_ERR_UNSUPPORTED = 0, 2, 3, 4, 5
+MOA_ERR_PROVIDER_TRANSPORT, MOA_ERR_PROVIDER_CREDENTIALS, MOA_ERR_PROVIDER_BAD_RESPONSE = 6, 7, 8
 MODES = {"sequential-pd": 0, "dp-only": 1, "dp-chunked-prefill": 2, "incremental-overlap": 3}
 EVENT_KINDS = {1: "chunk", 2: "decode_end", 3: "cancel", 4: "reclaim"}
 
@@ -34,6 +35,19 @@ class UnsupportedError(Exception):
 
 class DeviceError(RunError):
     """MOA_ERR_DEVICE -- CUDA failure."""
+
+
+class ProviderError(Exception):
+    """MOA_ERR_PROVIDER_* -- the reference's ProviderError (errors.hpp:24-33); kind is
+    "transport", "missing_credentials" or "bad_response"."""
+
+    def __init__(self, msg, kind):
+        super().__init__(msg)
+        self.kind = kind
+
+
+_PROVIDER_KINDS = {6: "transport", 7: "missing_credentials", 8: "bad_response"}
+EMBED_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int32), C.c_int, C.c_int, C.POINTER(C.c_double))
 
 
 class ModelSpec(C.Structure):
@@ -64,7 +78,8 @@ class RunConfigC(C.Structure):
                 ("use_force_q", C.c_int), ("force_q", C.c_double), ("chunk_size", C.c_int),
                 ("seed", C.c_uint64), ("query_tokens", C.c_int), ("leaf_prefix_tokens", C.c_int),
                 ("agg_prefix_tokens", C.c_int), ("separator_tokens", C.c_int), ("suffix_tokens", C.c_int),
-                ("hidden", C.c_int), ("provider_seed", C.c_uint64), ("embed_model", C.c_int)]
+                ("hidden", C.c_int), ("provider_seed", C.c_uint64), ("embed_model", C.c_int),
+                ("embed_fn", EMBED_FN), ("embed_user", C.c_void_p)]
 
 
 class RunSummary(C.Structure):
@@ -234,6 +249,8 @@ def check(rc: int):
         raise ValidationError(msg)
     if rc == MOA_ERR_DEVICE:
         raise DeviceError(msg)
+    if rc in _PROVIDER_KINDS:
+        raise ProviderError(msg, _PROVIDER_KINDS[rc])
     if rc == MOA_ERR_UNSUPPORTED:
         raise UnsupportedError(msg)
     raise RunError(msg)
@@ -497,7 +514,10 @@ def _query_detail(q, s, resolve):
 class QueryConfig:
     """moa_run_config built from a plain config dict (configs.py)."""
 
-    def __init__(self, cfg: dict, model_index: dict):
+    def __init__(self, cfg: dict, model_index: dict, embed=None):
+        """embed: optional EmbeddingProvider (embedding.hpp:38-44), a callable
+        tokens -> array [n][cfg["hidden"]] (fp64) used by the early-exit gate
+        instead of the mock; it may raise ProviderError."""
         t = cfg["topology"]
         widths = list(t["widths"])
         L = len(widths)
@@ -539,9 +559,28 @@ class QueryConfig:
             suffix_tokens=cfg["suffix_tokens"], hidden=cfg.get("hidden", 64),
             provider_seed=cfg.get("provider_seed", 0),
             embed_model=model_index[cfg["embed_model"]] if cfg.get("provider", "mock") == "hidden" else -1)
+        if embed is not None:
+            import numpy as np
+            codes = {v: k for k, v in _PROVIDER_KINDS.items()}
+
+            def _cb(user, toks, n, hidden, out):
+                try:
+                    e = np.ascontiguousarray(np.asarray(embed([toks[i] for i in range(n)]), dtype=np.float64))
+                    if e.shape != (n, hidden):
+                        return MOA_ERR_PROVIDER_BAD_RESPONSE
+                    C.memmove(out, e.ctypes.data, e.nbytes)
+                    return MOA_OK
+                except ProviderError as ex:
+                    return codes.get(ex.kind, MOA_ERR_PROVIDER_BAD_RESPONSE)
+                except Exception:
+                    return MOA_ERR_PROVIDER_BAD_RESPONSE
+
+            self._embed_cb = EMBED_FN(_cb)  # kept alive with the config
+            self.c.embed_fn = self._embed_cb
 
 
-def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16384, gemv_only=False, concurrency=1):
+def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16384, gemv_only=False, concurrency=1,
+               embed=None):
     """Engine holding every model the config names, sized for its agents
     (times `concurrency` requests served at once by run_batch)."""
     from collections import Counter
@@ -563,7 +602,7 @@ def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16
         max_ctx = ((prompt_max + out_max + 255) // 256) * 256
     eng = Engine(specs, max_ctx=max_ctx, max_out=out_max, max_rows=max_rows, device=device, keep_logits=keep_logits,
                  gemv_only=gemv_only)
-    return eng, QueryConfig(cfg, {t: i for i, t in enumerate(tags)})
+    return eng, QueryConfig(cfg, {t: i for i, t in enumerate(tags)}, embed=embed)
 
 
 class Quality(C.Structure):

@@ -30,8 +30,12 @@ def _name(tag):
     if tag >> 16 == 5:
         epi = {0: "f32", 1: "residual", 2: "swiglu", 3: "qkv"}.get((tag >> 12) & 15, "?")
         return f"gemv_tc({epi},K={16 * (tag & 0xfff)})"
+    if tag == 0x60001:
+        return "attn_decode_tma"
     if tag >> 16 == 6:
         return "attention"
+    if tag >> 16 == 7:
+        return "rmsnorm"
     return hex(tag)
 
 

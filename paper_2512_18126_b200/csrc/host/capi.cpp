@@ -47,6 +47,11 @@ int guard(F&& f) {
   } catch (const moa::RunError& e) {
     g_err = e.what();
     return MOA_ERR_RUNTIME;
+  } catch (const moa::ProviderError& e) {
+    g_err = e.what();
+    return e.kind == moa::ProviderError::Transport            ? MOA_ERR_PROVIDER_TRANSPORT
+           : e.kind == moa::ProviderError::MissingCredentials ? MOA_ERR_PROVIDER_CREDENTIALS
+                                                              : MOA_ERR_PROVIDER_BAD_RESPONSE;
   } catch (const std::exception& e) {
     g_err = e.what();
     return MOA_ERR_RUNTIME;
@@ -129,6 +134,19 @@ moa::RunConfig run_config_of(const moa_run_config* c) {
   cfg.hidden = c->hidden;
   cfg.provider_seed = c->provider_seed;
   cfg.embed_model = c->embed_model;
+  if (c->embed_fn) {
+    if (c->embed_model >= 0) throw moa::ValidationError("config: embed_fn and embed_model are exclusive");
+    auto fn = c->embed_fn;
+    void* user = c->embed_user;
+    cfg.embed_fn = [fn, user](const moa::TokenSeq& t, int hidden, double* out) {
+      const int rc = fn(user, t.data(), static_cast<int>(t.size()), hidden, out);
+      if (rc == MOA_OK) return;
+      const std::string what = "embedding provider failed (status " + std::to_string(rc) + ")";
+      if (rc == MOA_ERR_PROVIDER_TRANSPORT) throw moa::ProviderError(moa::ProviderError::Transport, what);
+      if (rc == MOA_ERR_PROVIDER_CREDENTIALS) throw moa::ProviderError(moa::ProviderError::MissingCredentials, what);
+      throw moa::ProviderError(moa::ProviderError::BadResponse, what);
+    };
+  }
   return cfg;
 }
 
@@ -1069,6 +1087,8 @@ int moa_k_chain_stamp(uintptr_t buf) {
   return guard([&] {
     moa::k::forward_chain_stamp(reinterpret_cast<unsigned long long*>(buf));
     moa::k::gemv_tc_chain_stamp(reinterpret_cast<unsigned long long*>(buf));
+    moa::k::gemm_tc_chain_stamp(reinterpret_cast<unsigned long long*>(buf));
+    moa::k::attn_decode_chain_stamp(reinterpret_cast<unsigned long long*>(buf));
   });
 }
 

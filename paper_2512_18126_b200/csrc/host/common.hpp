@@ -32,6 +32,12 @@ struct UnsupportedError : std::runtime_error {
 struct DeviceError : RunError {
   using RunError::RunError;
 };
+// Embedding provider failure (errors.hpp:24-33): Transport, MissingCredentials, BadResponse.
+struct ProviderError : std::runtime_error {
+  enum Kind { Transport, MissingCredentials, BadResponse };
+  ProviderError(Kind k, const std::string& what) : std::runtime_error(what), kind(k) {}
+  Kind kind;
+};
 
 struct AgentId {
   int layer = 1;

@@ -103,6 +103,13 @@ QualityScore GpuMetricQ::add_completion_embedded(const float* d_lp, long long ba
   return finish(d_lp, base, n);
 }
 
+QualityScore GpuMetricQ::add_completion_host(const double* emb, const float* d_lp, long long base, int n) {
+  if (n <= 0) throw ValidationError("logprobs: need at least one token");
+  if (n > max_tokens_) throw ValidationError("metricq: completion longer than the evaluator capacity");
+  MOA_CUDA(cudaMemcpyAsync(d_emb_, emb, sizeof(double) * n * hidden_, cudaMemcpyHostToDevice, st_));
+  return finish(d_lp, base, n);
+}
+
 QualityScore GpuMetricQ::add_completion_conf(double c, int n) {
   if (n <= 0) throw ValidationError("logprobs: need at least one token");
   if (n > max_tokens_) throw ValidationError("metricq: completion longer than the evaluator capacity");

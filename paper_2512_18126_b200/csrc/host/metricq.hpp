@@ -54,6 +54,8 @@ class GpuMetricQ {
   QualityScore add_completion(const int* d_tok, const float* d_lp, long long base, int n);
   // Same with the embedding rows already in emb_buffer() (hidden-state provider).
   QualityScore add_completion_embedded(const float* d_lp, long long base, int n);
+  // Same with host embedding rows emb[n][hidden] (a caller EmbeddingProvider).
+  QualityScore add_completion_host(const double* emb, const float* d_lp, long long base, int n);
   // Embedding rows already in emb_buffer(), confidence computed by the caller
   // (host fp64 logprobs: geometric_mean_confidence, bit-exact).
   QualityScore add_completion_conf(double c, int n);

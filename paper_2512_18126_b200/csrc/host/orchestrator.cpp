@@ -238,7 +238,13 @@ struct Request {
         grp->evals += 1;
         rec.evaluated = true;
         const int n = eng.record(producer).output_tokens;
-        if (cfg.embed_model >= 0) {
+        if (cfg.embed_fn) {
+          TokenSeq toks(static_cast<std::size_t>(n));
+          eng.read_outputs(producer, n, toks.data(), nullptr, nullptr);
+          std::vector<double> emb(static_cast<std::size_t>(n) * static_cast<std::size_t>(cfg.hidden));
+          cfg.embed_fn(toks, cfg.hidden, emb.data());
+          rec.score = grp->eval->add_completion_host(emb.data(), eng.d_out_lp(), eng.out_offset(producer), n);
+        } else if (cfg.embed_model >= 0) {
           eng.hidden_embed(cfg.embed_model, producer, n, *grp->eval);
           rec.score = grp->eval->add_completion_embedded(eng.d_out_lp(), eng.out_offset(producer), n);
         } else {

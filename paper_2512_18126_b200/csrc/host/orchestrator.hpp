@@ -4,6 +4,7 @@
 // agent outputs produced by greedy decode on the device.
 #pragma once
 
+#include <functional>
 #include <map>
 #include <memory>
 #include <optional>
@@ -42,6 +43,8 @@ struct RunConfig {  // orchestrator.hpp:23-53 (+ model per agent, which replaces
   // embedding provider: -1 = the reference's MockProvider (hidden, provider_seed);
   // >= 0 = hidden states of engine model `embed_model` (width = its d_model)
   int embed_model = -1;
+  // caller EmbeddingProvider (embedding.hpp:38-44): tokens -> out[n][hidden], width = hidden
+  std::function<void(const TokenSeq&, int hidden, double* out)> embed_fn;
 
   void validate() const;
 };

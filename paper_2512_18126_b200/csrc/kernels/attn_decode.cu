@@ -19,6 +19,7 @@
 #include "kernels.cuh"
 #include "mma_common.cuh"
 #include "tc_common.cuh"
+#include "stamp.cuh"
 
 namespace moa::k {
 namespace {
@@ -56,6 +57,7 @@ attention_decode_tma_kernel(const __grid_constant__ CUtensorMap kmap, const __gr
   float* wo = reinterpret_cast<float*>(Ks);  // after the key loop: [4 warps][16][HD] fp32
   __shared__ float wm[4][16], wl[4][16], cm_s[16], cl_s[16];
   __shared__ bool last;
+  __shared__ unsigned long long cst[kChainPhases];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g8 = lane >> 2, t4 = lane & 3;
   const int r = blockIdx.x, g = blockIdx.y, s = blockIdx.z;
@@ -70,6 +72,10 @@ attention_decode_tma_kernel(const __grid_constant__ CUtensorMap kmap, const __gr
   const int n = rd.pos + 1;
   const int nsplit = (n + C::KEYS - 1) / C::KEYS;
   if (s >= nsplit) return;
+  if (threadIdx.x == 0) {
+    chain_reset(cst);
+    chain_mark(cst, 0);
+  }
   const int hpg = nh / nkv;
   const int kb = s * C::KEYS, ke = min(n, kb + C::KEYS);
   const int nbox = (ke - kb + 63) / 64;
@@ -113,8 +119,10 @@ attention_decode_tma_kernel(const __grid_constant__ CUtensorMap kmap, const __gr
   }
   pdl_wait();
   pdl_launch_dependents();
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
+    chain_mark(cst, 1);
     for (int b = newbox; b < nbox; ++b) load_box(b);
+  }
   for (int c = threadIdx.x; c < 16 * (HD / 8); c += 128) {
     const int hr = c / (HD / 8), ch = c % (HD / 8);
     uint4 v = make_uint4(0, 0, 0, 0);
@@ -140,6 +148,7 @@ attention_decode_tma_kernel(const __grid_constant__ CUtensorMap kmap, const __gr
   for (int nt = 0; nt < NT; ++nt) oacc[nt][0] = oacc[nt][1] = oacc[nt][2] = oacc[nt][3] = 0.f;
   const int wk0 = warp * KW;  // this warp's first key (relative to kb)
   mbar_wait(full, 0);
+  if (threadIdx.x == 0) chain_mark(cst, 3);
   if (kb + wk0 < ke) {
     float sacc[NJ][4];
 #pragma unroll
@@ -248,7 +257,13 @@ attention_decode_tma_kernel(const __grid_constant__ CUtensorMap kmap, const __gr
       }
     }
   }
-  if (nsplit == 1) return;
+  if (nsplit == 1) {
+    if (g_chain_stamp != nullptr && threadIdx.x == 0) {
+      chain_mark(cst, 2);
+      chain_flush(cst, (6u << 16) | 1u);
+    }
+    return;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned prev;
@@ -256,7 +271,13 @@ attention_decode_tma_kernel(const __grid_constant__ CUtensorMap kmap, const __gr
     last = prev == static_cast<unsigned>(nsplit - 1);
   }
   __syncthreads();
-  if (!last) return;
+  if (!last) {
+    if (g_chain_stamp != nullptr && threadIdx.x == 0) {
+      chain_mark(cst, 2);
+      chain_flush(cst, (6u << 16) | 1u);
+    }
+    return;
+  }
   // combine the splits in split order
   float* sw_s = reinterpret_cast<float*>(Vs);  // [16][64] split weights
   for (int i = threadIdx.x; i < hpg * nsplit; i += 128) {
@@ -284,10 +305,16 @@ attention_decode_tma_kernel(const __grid_constant__ CUtensorMap kmap, const __gr
     for (int t = 0; t < nsplit; ++t) val += sw_s[h * 64 + t] * __ldcg(pr + t * (2 + HD) + 2 + e);
     o[(static_cast<long long>(r) * nh + g * hpg + h) * HD + e] = __float2bfloat16_rn(val / cl_s[h]);
   }
-  if (threadIdx.x == 0) cnt[r * nkv + g] = 0;
+  if (threadIdx.x == 0) {
+    cnt[r * nkv + g] = 0;
+    chain_mark(cst, 2);
+    chain_flush(cst, (6u << 16) | 1u);
+  }
 }
 
 }  // namespace
+
+MOA_CHAIN_STAMP_SETTER(attn_decode_chain_stamp)
 
 int attention_decode_tma_keys(int hd) { return hd == 128 ? DecTma<128>::KEYS : DecTma<64>::KEYS; }
 

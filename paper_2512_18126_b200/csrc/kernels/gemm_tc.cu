@@ -17,6 +17,7 @@
 #include <cstdio>
 
 #include "kernels.cuh"
+#include "stamp.cuh"
 
 namespace moa::k {
 
@@ -310,11 +311,17 @@ __global__ void __launch_bounds__(128) rmsnorm_rows_kernel(const float* __restri
                                                            const float* __restrict__ g, float eps,
                                                            bf16* __restrict__ h) {
   __shared__ float red[4];
+  __shared__ unsigned long long cst[kChainPhases];
   const int i = blockIdx.x;
   if (i >= meta[meta_idx]) return;  // tick metadata: not produced by the previous kernel
   const int r = sel ? sel[i] : i;
+  if (threadIdx.x == 0) {
+    chain_reset(cst);
+    chain_mark(cst, 0);
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (threadIdx.x == 0) chain_mark(cst, 1);
   const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long long>(r) * K);
   float ss = 0.f;
   for (int v = threadIdx.x; v < K / 4; v += 128) {
@@ -345,7 +352,15 @@ __global__ void __launch_bounds__(128) rmsnorm_rows_kernel(const float* __restri
     o[7] = __float2bfloat16_rn(b.w * inv * gb.w);
     reinterpret_cast<uint4*>(h + static_cast<long long>(i) * K)[v] = *reinterpret_cast<const uint4*>(o);
   }
+  if (g_chain_stamp != nullptr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      chain_mark(cst, 2);
+      chain_flush(cst, 7u << 16);
+    }
+  }
 }
+
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                               const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -410,5 +425,7 @@ void rmsnorm_rows(const float* x, int R_cap, const int* meta, int K, const float
   uniform_carveout(reinterpret_cast<const void*>(rmsnorm_rows_kernel));
   cudaLaunchKernelEx(&cfg, rmsnorm_rows_kernel, x, sel, meta, meta_idx, K, g, eps, h);
 }
+
+MOA_CHAIN_STAMP_SETTER(gemm_tc_chain_stamp)
 
 }  // namespace moa::k

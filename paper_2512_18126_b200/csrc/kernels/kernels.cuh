@@ -46,6 +46,8 @@ void uniform_carveout(const void* fn);
 // debug: per-CTA globaltimer stamps of the decode chain (stamp.cuh), nullptr = off
 void forward_chain_stamp(unsigned long long* buf);
 void gemv_tc_chain_stamp(unsigned long long* buf);
+void gemm_tc_chain_stamp(unsigned long long* buf);
+void attn_decode_chain_stamp(unsigned long long* buf);
 
 void init_uniform_rows(bf16* dst, long long rows, long long cols, std::uint64_t base, float scale, int map,
                        int hd, cudaStream_t st);

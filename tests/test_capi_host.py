@@ -128,3 +128,13 @@ def test_query_config_marshalling(name):
     q = capi.QueryConfig(cfg, {t: i for i, t in enumerate(cfg["models"])})
     assert q.c.n_layers == len(cfg["topology"]["widths"])
     assert q.c.mode == capi.MODES[cfg["mode"]]
+
+
+def test_library_has_no_unresolved_internal_symbols():
+    """Every moa:: symbol the library references is defined in it (dlopen with
+    RTLD_NOW fails on the GPU box otherwise)."""
+    import os
+    import subprocess
+    C.CDLL(str(capi.LIB_PATH), mode=os.RTLD_NOW)
+    out = subprocess.run(["nm", "-D", "--undefined-only", str(capi.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "_ZN3moa" not in out, [l for l in out.splitlines() if "_ZN3moa" in l]

@@ -126,6 +126,7 @@ def test_c2_full_tree_matches_oracle():
         assert g["agents"][name]["prompt"] == oa["prompt"], name
     assert g["ticks"] == o["e2e_ticks"]
     checked = total = 0
+    per = {}
     for tag in ("leaf", "agg"):
         mm = cfg["models"][tag]
         model = _cpu(tag, mm["shape"], mm["seed"])
@@ -136,5 +137,6 @@ def test_c2_full_tree_matches_oracle():
             assert chk["mismatches"] == [] and chk["lp_ok"], (name, chk)
             checked += chk["checked"]
             total += len(ga["output"])
+            per[name] = (chk["checked"], round(chk["max_logit_err"], 4))
     assert total == 11 * 64
-    assert checked >= DECISIVE_FRAC * total, (checked, total)
+    assert checked >= DECISIVE_FRAC * total, (checked, total, per)
