@@ -41,11 +41,11 @@ def check_agent(model: CpuModel, prompt, out_tokens, out_logprobs, logits_atol=L
     mismatch is a GPU greedy id that disagrees with a decisive oracle argmax.
 
     With the GPU's own fp32 logits (keep_logits engines) the bound is the
-    measured one, per token: every logit of token k must be within logits_atol
-    of the oracle's, e_k = max_v |gpu_k,v - oracle_k,v|, and token k is
-    decisive when the oracle's top-1 margin exceeds 2 * e_k -- then the GPU
-    argmax provably equals the oracle's (any other id gains at most 2 e_k on
-    the oracle's argmax).  Without them the margin must exceed 2 * logits_atol."""
+    measured one, per logit: every logit of token k must be within logits_atol
+    of the oracle's, and token k is decisive when the oracle's argmax a beats
+    every other id v by more than the two measured errors, L_a - L_v >
+    |dL_a| + |dL_v| -- then the GPU argmax provably equals the oracle's.
+    Without them the margin must exceed 2 * logits_atol."""
     L = teacher_forced(model, prompt, out_tokens)
     tok, lp, _ = logit_stats(L)
     srt = np.sort(L, axis=-1)
@@ -53,12 +53,22 @@ def check_agent(model: CpuModel, prompt, out_tokens, out_logprobs, logits_atol=L
     n = len(out_tokens)
     bound = np.full(n, logits_atol)
     logit_err = None
+    decisive = margin > 2 * bound
     if gpu_logits is not None:
         G = np.asarray(gpu_logits, dtype=np.float32).reshape(L.shape)
-        err_k = np.abs(G - L).max(axis=-1) if n else np.zeros(0)
+        E = np.abs(G - L)
+        err_k = E.max(axis=-1) if n else np.zeros(0)
         logit_err = float(err_k.max()) if n else 0.0
-        bound = np.minimum(logits_atol, err_k)
-    decisive = margin > 2 * bound
+        # pairwise bound: with measured per-logit errors e_v, the GPU ranks the
+        # oracle's argmax a above every v whenever L_a - L_v > e_a + e_v, so
+        # token k is decisive when min_v (L_a - e_a - L_v - e_v) > 0 (and every
+        # error is within logits_atol)
+        a = L.argmax(axis=-1)
+        ea = E[np.arange(n), a]
+        la = L[np.arange(n), a]
+        slack = (la - ea)[:, None] - (L + E)
+        slack[np.arange(n), a] = np.inf
+        decisive = (slack.min(axis=-1) > 0) & (err_k <= logits_atol) if n else np.zeros(0, bool)
     mism = [k for k in range(n) if decisive[k] and int(tok[k]) != int(out_tokens[k])]
     # logprob of the GPU's token under the oracle
     z = L - L.max(axis=-1, keepdims=True)

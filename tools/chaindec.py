@@ -42,9 +42,11 @@ recs = np.stack([(meta >> np.uint64(32)).astype(np.int64), ((meta >> np.uint64(2
 cnt = collections.Counter((chain._name(int(a)), int(b)) for a, b in zip(recs[:, 0], recs[:, 1]))
 print(shape, R, P, "records", n, dict(sorted(cnt.items())))
 L = {"tiny": 4, "1b": 16, "8b": 32}[shape]
-tag, ph, tt = recs[:, 0], recs[:, 1], recs[:, 3]
+recs = recs[np.argsort(recs[:, 3], kind="stable")]  # time order: each tick is one contiguous slice
+tag_all, ph_all, tt_all = recs[:, 0], recs[:, 1], recs[:, 3]
+tag, ph, tt = tag_all, ph_all, tt_all
 LM = 0x30000
-lm_end = np.sort(np.array([tt[(tag == LM) & (ph == 2)]]).ravel())
+lm_end = np.sort(tt_all[(tag_all == LM) & (ph_all == 2)])
 # LM head instances: cluster CTA end stamps (one instance per tick)
 ends = [s_.max() for s_ in np.split(lm_end, np.where(np.diff(lm_end) > 5000)[0] + 1)]
 per_tag_launch = {}
@@ -53,7 +55,9 @@ phases = collections.defaultdict(lambda: collections.defaultdict(list))
 ticks = 0
 for k in range(len(ends) // 3, len(ends) - 1):  # steady-state decode ticks
     lo, hi = ends[k], ends[k + 1]
-    m = (tt > lo) & (tt <= hi)
+    i0, i1 = np.searchsorted(tt_all, lo, side="right"), np.searchsorted(tt_all, hi, side="right")
+    tag, ph, tt = tag_all[i0:i1], ph_all[i0:i1], tt_all[i0:i1]
+    m = np.ones(len(tt), bool)
     insts = []
     for tg in np.unique(tag[m]):
         e = np.sort(tt[m & (tag == tg) & (ph == 0)])
@@ -95,6 +99,7 @@ for k in range(len(ends) // 3, len(ends) - 1):  # steady-state decode ticks
                 phases[key][p_].append(((np.median(v) - prev) / 1e3, (v.max() - prev) / 1e3))
         prev = max(prev, e_)
     ticks += 1
+tag, ph, tt = tag_all, ph_all, tt_all
 print(f"{ticks} steady ticks; tick median {np.median(np.diff(ends[len(ends)//3:])) / 1e3:.1f} us")
 tot = 0.0
 for key in sorted(rows):
