@@ -995,9 +995,21 @@ int moa_k_attention(uintptr_t q, uintptr_t rows, int R, uintptr_t meta, int nh, 
     const auto* vp = reinterpret_cast<const moa::k::bf16*>(vpool);
     auto* op = reinterpret_cast<moa::k::bf16*>(out);
     const bool tma = (prefill & 2) != 0;  // bit 1: the TMA-staged per-row kernel
+    const bool cluster = (prefill & 4) != 0;  // bit 2: the cluster-split kernel, splits = bits 8-15 (0: heuristic)
+    const int ns_req = (prefill >> 8) & 0xff;
     prefill &= 1;
     if (prefill) moa::k::attention_prefill(qp, rp, R, mp, nh, nkv, hd, kp, vp, kv_stride, 0, max_ctx, op, st);
-    {  // prefill: the per-row kernel takes the rows alone in their run
+    if (cluster) {
+      const long long pool_rows = static_cast<long long>(slots) * kv_stride / hd;
+      moa::k::TmaMap km, vm;
+      if (!moa::k::make_tmap_bf16(&km, kp, pool_rows, hd, 64) || !moa::k::make_tmap_bf16(&vm, vp, pool_rows, hd, 64))
+        throw moa::DeviceError("attention: TMA map creation failed");
+      if (ns_req > 8 || (ns_req & (ns_req - 1))) throw moa::ValidationError("attention: splits must be 1, 2, 4 or 8");
+      const int ns = ns_req ? ns_req : moa::k::attention_decode_cluster_splits(R, nkv, (max_ctx + 63) / 64);
+      moa::k::attention_decode_cluster(km, vm, qp, rp, R, ns, mp, nh, nkv, hd, kv_stride, 0, max_ctx, op, st,
+                                       prefill != 0);
+      MOA_CUDA(cudaStreamSynchronize(st));
+    } else {  // prefill: the per-row kernel takes the rows alone in their run
       float* ws = nullptr;
       int* cnt = nullptr;
       MOA_CUDA(cudaMalloc(&ws, sizeof(float) * moa::k::attention_ws_floats(R, nh, hd, max_ctx)));

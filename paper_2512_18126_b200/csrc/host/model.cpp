@@ -192,7 +192,12 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   // decode rows of GQA agents: TMA-staged attention (MOA_DECODE_TMA=0: the register-staged kernel)
   attn_tma_ = kv_maps_ok_ && k::attention_decode_tma_supported(s.n_heads, s.n_kv_heads, static_cast<int>(hd), max_ctx);
   if (const char* e = std::getenv("MOA_DECODE_TMA")) attn_tma_ = attn_tma_ && e[0] != '0';
-  split_keys_ = attn_tma_ ? k::attention_decode_tma_keys(static_cast<int>(hd)) : k::kv_split(static_cast<int>(hd));
+  // default: the cluster-split kernel (MOA_DECODE_CLUSTER=0: the fixed-split TMA kernel)
+  attn_cluster_ = kv_maps_ok_ && k::attention_decode_cluster_supported(s.n_heads, s.n_kv_heads, static_cast<int>(hd));
+  if (const char* e = std::getenv("MOA_DECODE_CLUSTER")) attn_cluster_ = attn_cluster_ && e[0] != '0';
+  split_keys_ = attn_cluster_ ? 64
+                : attn_tma_   ? k::attention_decode_tma_keys(static_cast<int>(hd))
+                              : k::kv_split(static_cast<int>(hd));
   if (const char* e = std::getenv("MOA_QKV_ATTN")) use_qkv_attn_ = std::string(e) != "0";
   if (const char* e = std::getenv("MOA_PREFILL_ATTN")) use_prefill_attn_ = std::string(e) != "0";
   // RMSNorm folded into the decode GEMVs: ssq partials [16 rows][d/16]
@@ -453,7 +458,11 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       const double keys = prefill ? live_.single_keys : live_.keys, rows_n = prefill ? live_.singles : Rv;
       probe_begin(KernelProbes::AttnDecode, 4.0 * keys * nkv * hd + 4.0 * rows_n * nh * hd,
                   4.0 * keys * nh * hd);
-      if (attn_tma_)
+      if (attn_cluster_)
+        k::attention_decode_cluster(kmap_, vmap_, q_, buf_.rows, rcap,
+                                    k::attention_decode_cluster_splits(rcap, nkv, nsplit), meta, nh, nkv, hd,
+                                    kv_stride_, loff, max_ctx_, h_, st, prefill);
+      else if (attn_tma_)
         k::attention_decode_tma(kmap_, vmap_, q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kv_stride_, loff,
                                 max_ctx_, h_, attn_ws_, attn_cnt_, st, prefill);
       else

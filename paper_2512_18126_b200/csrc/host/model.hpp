@@ -157,6 +157,7 @@ class DeviceModel {
   k::bf16* wo_blk_ = nullptr;  // [L][nkv][D][hpg*hd]: Wo regrouped for the fused o-projection
   bool kv_maps_ok_ = false;
   bool attn_tma_ = false;  // decode rows: TMA-staged attention (attn_decode.cu)
+  bool attn_cluster_ = false;  // decode rows: cluster-split TMA-ring attention (attn_decode.cu, default)
   int split_keys_ = 512;   // keys per attention CTA (sizes the graphs' split buckets)
   k::TmaMap map_hn_, map_h_attn_, map_h_ffn_;        // A operands, 128-row boxes (prefill)
   k::TmaMap map_hn16_, map_h_attn16_, map_h_ffn16_;  // 16-row boxes (decode, swap-AB)

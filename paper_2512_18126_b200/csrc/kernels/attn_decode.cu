@@ -13,6 +13,7 @@
 // last-arriving CTA in split order (deterministic for given shapes).
 //
 // Algorithmic bytes per (row, kv head): (pos + 1) * hd * 2 (K) * 2 (V).
+#include <algorithm>
 #include <cstdio>
 #include <set>
 
@@ -312,6 +313,308 @@ attention_decode_tma_kernel(const __grid_constant__ CUtensorMap kmap, const __gr
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Cluster-split decode attention.  The row's keys are cut into NS splits of
+// whole 64-key boxes; the NS CTAs of one (row, kv head) form a thread-block
+// cluster (grid x = split).  A producer warp streams the split's boxes (K and
+// V, 128B-swizzled TMA) through an STG-stage mbarrier ring; the four consumer
+// warps take 16 keys of every box each (q heads of the GQA group = the M rows
+// of mma.sync m16n8k16 tiles) with an online softmax across boxes, so loads
+// overlap compute and a CTA holds only STG boxes.  Partials are combined
+// without global memory: each CTA folds its warps (fixed order) into
+// (max, sum, o) in shared memory, and after one cluster barrier CTA s reads
+// every rank's partial over DSMEM for its slice of the outputs and combines
+// them in rank order (deterministic for given shapes).  NS = 8 for every row
+// (a row's splits depend only on its context length: batch invariant); two
+// ring stages per CTA suffice with 8 kv heads x 8 splits per row in flight
+// and leave room on the SM for the next GEMV's CTAs (PDL prologue).
+template <int HD>
+struct DecCl {
+  static constexpr int STG = HD == 128 ? 2 : 3;    // ring stages (64-key boxes of K and V)
+  static constexpr int SUB = HD / 64;              // 128-byte column subtiles per key row
+  static constexpr int BOX = 64 * HD * 2;          // bytes of one K (or V) box
+  static constexpr int STAGE = 2 * BOX;
+  static constexpr int QB = 16 * HD * 2;
+  static constexpr int WO = 4 * 16 * HD * 4;       // warp partials (reuse the ring)
+  static constexpr int PART = 16 * (HD + 2) * 4;   // CTA partial: [16][HD] o, then m[16], l[16]
+  static_assert(WO + PART <= STG * STAGE, "partials fit in the ring");
+  static constexpr int SMEM = 1024 + STG * STAGE + QB + 2 * STG * 8;
+};
+
+__device__ __forceinline__ void cluster_arrive_wait() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float dsmem_ldf(const float* local, int rank) {
+  std::uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(local)), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+
+template <int HD>
+__global__ void __launch_bounds__(160)
+attention_decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                                const bf16* __restrict__ q, const RowDesc* __restrict__ rows,
+                                const int* __restrict__ meta, int nh, int nkv, long long kv_stride,
+                                long long layer_off, int max_ctx, bf16* __restrict__ o, int skip_runs) {
+  using C = DecCl<HD>;
+  constexpr int KSTEPS = HD / 16, NT = HD / 8, RB = HD * 2, STG = C::STG;
+  extern __shared__ unsigned char dc_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(dc_raw) + 1023) &
+                                                       ~static_cast<std::uintptr_t>(1023));
+  unsigned char* ring = sm;                    // [STG][K box | V box], each [SUB][64][128 B] swizzled
+  unsigned char* Qs = sm + STG * C::STAGE;     // [16][HD] bf16, 16-byte chunks XOR-swizzled by row
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(Qs + C::QB);
+  std::uint64_t* empty = full + STG;
+  float* wo = reinterpret_cast<float*>(ring);  // after the box loop: [4 warps][16][HD]
+  float* po = reinterpret_cast<float*>(ring + C::WO);  // CTA partial o [16][HD], m [16], l [16]
+  float* pm = po + 16 * HD;
+  float* pl = pm + 16;
+  __shared__ float wm[4][16], wl[4][16];
+  __shared__ int first_new_s;
+  __shared__ unsigned long long cst[kChainPhases];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int s = blockIdx.x, NS = gridDim.x, g = blockIdx.y, r = blockIdx.z;
+  // cluster-uniform early exits (every CTA of a cluster has the same row)
+  const int live = __ldg(meta);
+  if (r >= live) return;
+  const RowDesc rd = rows[r];
+  if (skip_runs) {
+    if ((r > 0 && rows[r - 1].kv == rd.kv && rows[r - 1].pos + 1 == rd.pos) ||
+        (r + 1 < live && rows[r + 1].kv == rd.kv && rows[r + 1].pos == rd.pos + 1))
+      return;
+  }
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) {
+    chain_reset(cst);
+    chain_mark(cst, 0);
+  }
+  const int hpg = nh / nkv;
+  const int n = rd.pos + 1, nbox = (n + 63) / 64, bps = (nbox + NS - 1) / NS;
+  const int b0 = min(nbox, s * bps), nb = min(nbox, b0 + bps) - b0;
+  if (warp == 4) {
+    // First key written in this tick: the row's own, or the first of the run
+    // of consecutive rows of its agent it ends (incremental-prefill rows of one
+    // agent share a tick); boxes from there on are issued after the PDL wait.
+    int base = r - 1, p = rd.pos - 1, fn = rd.pos;
+    for (;;) {
+      const int rr = base - lane;
+      const bool c = rr >= 0 && rows[rr].kv == rd.kv && rows[rr].pos == p - lane;
+      const unsigned b = __ballot_sync(kAll, c);
+      if (b == kAll) {
+        base -= 32;
+        p -= 32;
+        continue;
+      }
+      fn = p - (__ffs(~b) - 1) + 1;
+      break;
+    }
+    if (lane == 0) {
+      first_new_s = fn;
+      for (int i = 0; i < STG; ++i) {
+        mbar_init(&full[i], 1);
+        mbar_init(&empty[i], 4);
+      }
+      mbar_fence_init();
+    }
+  }
+  __syncthreads();
+  if (warp == 4) {
+    if (lane == 0) {
+      prefetch_tmap(&kmap);
+      prefetch_tmap(&vmap);
+      const int newbox = first_new_s / 64;  // absolute index of the first box holding a new key
+      const int row0 = static_cast<int>((rd.kv * kv_stride + layer_off) / HD + static_cast<long long>(g) * max_ctx);
+      bool waited = false;
+      for (int i = 0; i < nb; ++i) {
+        const int st = i % STG, b = b0 + i;
+        if (i >= STG) mbar_wait(&empty[st], ((i / STG) - 1) & 1);
+        if (!waited && b >= newbox) {
+          pdl_wait();
+          waited = true;
+        }
+        mbar_expect_tx(&full[st], C::STAGE);
+        unsigned char* kd = ring + st * C::STAGE;
+#pragma unroll
+        for (int sub = 0; sub < C::SUB; ++sub) {
+          tma_load_2d(kd + sub * 8192, &kmap, &full[st], sub * 64, row0 + b * 64);
+          tma_load_2d(kd + C::BOX + sub * 8192, &vmap, &full[st], sub * 64, row0 + b * 64);
+        }
+      }
+    }
+  } else {
+    pdl_wait();  // q is written by the previous kernel
+    if (threadIdx.x == 0) chain_mark(cst, 1);
+    for (int c = threadIdx.x; c < 16 * (HD / 8); c += 128) {
+      const int hr = c / (HD / 8), ch = c % (HD / 8);
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (hr < hpg) v = __ldcg(reinterpret_cast<const uint4*>(q + (static_cast<long long>(r) * nh + g * hpg + hr) * HD) + ch);
+      *reinterpret_cast<uint4*>(Qs + hr * RB + ((ch ^ (hr & 7)) << 4)) = v;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // consumer warps only
+  }
+  float m_a = -1e30f, m_b = -1e30f, l_a = 0.f, l_b = 0.f;
+  float oacc[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) oacc[nt][0] = oacc[nt][1] = oacc[nt][2] = oacc[nt][3] = 0.f;
+  if (warp < 4) {
+    const std::uint32_t qs_u = smem_u32(Qs);
+    std::uint32_t qa[KSTEPS][4];
+#pragma unroll
+    for (int kk = 0; kk < KSTEPS; ++kk) {
+      const int hr = lane & 15, ch = kk * 2 + (lane >> 4);
+      ldsm_x4(qs_u + hr * RB + ((ch ^ (hr & 7)) << 4), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+    }
+    // element (key row kr, 16-byte chunk ch of the HD row) of a swizzled box
+    auto kv_addr = [](std::uint32_t base, int kr, int ch) {
+      return base + (ch >> 3) * 8192 + kr * 128 + (((ch & 7) ^ (kr & 7)) << 4);
+    };
+    const float sl2 = rsqrtf(static_cast<float>(HD)) * 1.4426950408889634f;
+    const int wk = warp * 16;  // this warp's 16 keys of every box
+    for (int i = 0; i < nb; ++i) {
+      const int st = i % STG;
+      const int kb = (b0 + i) * 64 + wk;  // absolute key of this warp's first key
+      const std::uint32_t ks_u = smem_u32(ring + st * C::STAGE), vs_u = ks_u + C::BOX;
+      mbar_wait(&full[st], (i / STG) & 1);
+      if (i == 0 && threadIdx.x == 0) chain_mark(cst, 3);
+      float sacc[2][4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < KSTEPS; ++kk) {
+        const int kr = wk + (lane & 7) + ((lane >> 4) << 3);
+        const int ch = kk * 2 + ((lane >> 3) & 1);
+        std::uint32_t b00, b01, b10, b11;
+        ldsm_x4(kv_addr(ks_u, kr, ch), b00, b01, b10, b11);
+        mma_bf16(sacc[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b00, b01);
+        mma_bf16(sacc[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b10, b11);
+      }
+      float mx_a = -1e30f, mx_b = -1e30f;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int key = kb + 8 * j + 2 * t4;
+        sacc[j][0] = key < n ? sacc[j][0] * sl2 : -1e30f;
+        sacc[j][1] = key + 1 < n ? sacc[j][1] * sl2 : -1e30f;
+        sacc[j][2] = key < n ? sacc[j][2] * sl2 : -1e30f;
+        sacc[j][3] = key + 1 < n ? sacc[j][3] * sl2 : -1e30f;
+        mx_a = fmaxf(mx_a, fmaxf(sacc[j][0], sacc[j][1]));
+        mx_b = fmaxf(mx_b, fmaxf(sacc[j][2], sacc[j][3]));
+      }
+      mx_a = fmaxf(mx_a, __shfl_xor_sync(kAll, mx_a, 1));
+      mx_a = fmaxf(mx_a, __shfl_xor_sync(kAll, mx_a, 2));
+      mx_b = fmaxf(mx_b, __shfl_xor_sync(kAll, mx_b, 1));
+      mx_b = fmaxf(mx_b, __shfl_xor_sync(kAll, mx_b, 2));
+      const float mn_a = fmaxf(m_a, mx_a), mn_b = fmaxf(m_b, mx_b);
+      const float al_a = exp2f(m_a - mn_a), al_b = exp2f(m_b - mn_b);
+      m_a = mn_a;
+      m_b = mn_b;
+      l_a *= al_a;
+      l_b *= al_b;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        oacc[nt][0] *= al_a;
+        oacc[nt][1] *= al_a;
+        oacc[nt][2] *= al_b;
+        oacc[nt][3] *= al_b;
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        sacc[j][0] = sacc[j][0] <= -1e29f ? 0.f : exp2f(sacc[j][0] - m_a);
+        sacc[j][1] = sacc[j][1] <= -1e29f ? 0.f : exp2f(sacc[j][1] - m_a);
+        sacc[j][2] = sacc[j][2] <= -1e29f ? 0.f : exp2f(sacc[j][2] - m_b);
+        sacc[j][3] = sacc[j][3] <= -1e29f ? 0.f : exp2f(sacc[j][3] - m_b);
+        l_a += sacc[j][0] + sacc[j][1];
+        l_b += sacc[j][2] + sacc[j][3];
+      }
+      const std::uint32_t pa0 = pack_bf16(sacc[0][0], sacc[0][1]);
+      const std::uint32_t pa1 = pack_bf16(sacc[0][2], sacc[0][3]);
+      const std::uint32_t pa2 = pack_bf16(sacc[1][0], sacc[1][1]);
+      const std::uint32_t pa3 = pack_bf16(sacc[1][2], sacc[1][3]);
+#pragma unroll
+      for (int np = 0; np < NT / 2; ++np) {
+        const int vr = wk + (lane & 7) + (((lane >> 3) & 1) << 3);
+        const int ch = np * 2 + (lane >> 4);
+        std::uint32_t v00, v01, v10, v11;
+        ldsm_x4_t(kv_addr(vs_u, vr, ch), v00, v01, v10, v11);
+        mma_bf16(oacc[2 * np], pa0, pa1, pa2, pa3, v00, v01);
+        mma_bf16(oacc[2 * np + 1], pa0, pa1, pa2, pa3, v10, v11);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    l_a += __shfl_xor_sync(kAll, l_a, 1);
+    l_a += __shfl_xor_sync(kAll, l_a, 2);
+    l_b += __shfl_xor_sync(kAll, l_b, 1);
+    l_b += __shfl_xor_sync(kAll, l_b, 2);
+  }
+  __syncthreads();  // every box consumed: the ring is free for the partials
+  if (warp < 4) {
+    if (t4 == 0) {
+      wm[warp][g8] = m_a;
+      wl[warp][g8] = l_a;
+      wm[warp][g8 + 8] = m_b;
+      wl[warp][g8 + 8] = l_b;
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int d = nt * 8 + 2 * t4;
+      *reinterpret_cast<float2*>(wo + (warp * 16 + g8) * HD + d) = make_float2(oacc[nt][0], oacc[nt][1]);
+      *reinterpret_cast<float2*>(wo + (warp * 16 + g8 + 8) * HD + d) = make_float2(oacc[nt][2], oacc[nt][3]);
+    }
+  }
+  __syncthreads();
+  // this CTA's partial over its boxes: warps folded in a fixed order
+  if (threadIdx.x < 16) {
+    const int h = threadIdx.x;
+    float M = -1e30f;
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, wm[w][h]);
+    float L = 0.f;
+    for (int w = 0; w < 4; ++w) L += wl[w][h] == 0.f ? 0.f : exp2f(wm[w][h] - M) * wl[w][h];
+    pm[h] = M;
+    pl[h] = L;
+  }
+  for (int i = threadIdx.x; i < hpg * HD; i += blockDim.x) {
+    const int h = i / HD, e = i % HD;
+    float M = -1e30f;
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, wm[w][h]);
+    float val = 0.f;
+    for (int w = 0; w < 4; ++w)
+      if (wl[w][h] != 0.f) val += exp2f(wm[w][h] - M) * wo[(w * 16 + h) * HD + e];
+    po[h * HD + e] = val;
+  }
+  cluster_arrive_wait();  // every rank's partial is visible
+  // rank s combines its slice of the (q head, column) outputs over all ranks, in rank order
+  for (int i = s * blockDim.x + threadIdx.x; i < hpg * HD; i += NS * blockDim.x) {
+    const int h = i / HD, e = i % HD;
+    float mt[8], lt[8], ot[8];
+    float M = -1e30f;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      mt[t] = t < NS ? dsmem_ldf(pm + h, t) : -1e30f;
+      lt[t] = t < NS ? dsmem_ldf(pl + h, t) : 0.f;
+      ot[t] = t < NS ? dsmem_ldf(po + h * HD + e, t) : 0.f;
+      M = fmaxf(M, mt[t]);
+    }
+    float L = 0.f, val = 0.f;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const float w = lt[t] == 0.f ? 0.f : exp2f(mt[t] - M);
+      L += w * lt[t];
+      val += w * ot[t];
+    }
+    o[(static_cast<long long>(r) * nh + g * hpg + h) * HD + e] = __float2bfloat16_rn(val / L);
+  }
+  cluster_arrive_wait();  // no CTA leaves while a peer may still read its partial
+  if (threadIdx.x == 0) {
+    chain_mark(cst, 2);
+    chain_flush(cst, (6u << 16) | 1u);
+  }
+}
+
 }  // namespace
 
 MOA_CHAIN_STAMP_SETTER(attn_decode_chain_stamp)
@@ -353,6 +656,53 @@ void attention_decode_tma(const TmaMap& kmap, const TmaMap& vmap, const bf16* q,
     go(attention_decode_tma_kernel<128>, DecTma<128>::SMEM);
   else
     go(attention_decode_tma_kernel<64>, DecTma<64>::SMEM);
+}
+
+
+int attention_decode_cluster_splits(int rcap, int nkv, int nbox_cap) {
+  // Fixed: a row's split structure (and so its accumulation order) depends
+  // only on its own context length, never on the tick's row count -- schedule
+  // modes that batch rows differently decode identical tokens.
+  (void)rcap, (void)nkv, (void)nbox_cap;
+  return 8;
+}
+
+bool attention_decode_cluster_supported(int nh, int nkv, int hd) {
+  return (hd == 64 || hd == 128) && nh % nkv == 0 && nh / nkv <= 16;
+}
+
+void attention_decode_cluster(const TmaMap& kmap, const TmaMap& vmap, const bf16* q, const RowDesc* rows, int R_cap,
+                              int ns, const int* meta, int nh, int nkv, int hd, long long kv_stride,
+                              long long layer_off, int max_ctx, bf16* o, cudaStream_t st, bool skip_runs) {
+  if (R_cap <= 0) return;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ns, nkv, R_cap);
+  cfg.blockDim = dim3(160);
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = ns;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  auto go = [&](auto kern, int smem) {
+    static std::set<const void*> attr;
+    if (attr.insert(reinterpret_cast<const void*>(kern)).second) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      uniform_carveout(reinterpret_cast<const void*>(kern));
+    }
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(&kmap),
+                       *reinterpret_cast<const CUtensorMap*>(&vmap), q, rows, meta, nh, nkv, kv_stride, layer_off,
+                       max_ctx, o, skip_runs ? 1 : 0);
+  };
+  if (hd == 128)
+    go(attention_decode_cluster_kernel<128>, DecCl<128>::SMEM);
+  else
+    go(attention_decode_cluster_kernel<64>, DecCl<64>::SMEM);
 }
 
 }  // namespace moa::k

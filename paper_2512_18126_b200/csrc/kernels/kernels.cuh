@@ -185,6 +185,16 @@ void attention_decode_tma(const TmaMap& kmap, const TmaMap& vmap, const bf16* q,
                           long long layer_off, int max_ctx, bf16* o, float* ws, int* cnt, cudaStream_t st,
                           bool skip_runs = false);
 
+// Cluster-split decode attention (attn_decode.cu): CTA = (split, kv head,
+// row), the ns <= 8 splits of a row's whole 64-key boxes form a thread-block
+// cluster and combine over DSMEM (no workspace); a producer warp streams each
+// split's boxes through a TMA ring.  Same maps and pool contract as above.
+int attention_decode_cluster_splits(int rcap, int nkv, int nbox_cap);
+bool attention_decode_cluster_supported(int nh, int nkv, int hd);
+void attention_decode_cluster(const TmaMap& kmap, const TmaMap& vmap, const bf16* q, const RowDesc* rows, int R_cap,
+                              int ns, const int* meta, int nh, int nkv, int hd, long long kv_stride,
+                              long long layer_off, int max_ctx, bf16* o, cudaStream_t st, bool skip_runs = false);
+
 // Prefill ticks (rows of long same-agent runs): CTA = 64 consecutive rows x q
 // head, keys streamed through smem once per same-agent segment; rows alone in
 // their run are skipped (pair with attention(..., skip_runs = true)).  hd 64 / 128.

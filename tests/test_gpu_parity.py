@@ -210,8 +210,8 @@ def test_attention_kernels_match_torch(torch_cuda, nh, nkv, hd, max_ctx):
             sc = (q[i, h].float() @ K[kv, kh, :pos + 1].T) / math.sqrt(hd)
             ref[i, h] = torch.softmax(sc, -1) @ V[kv, kh, :pos + 1]
     # mode bit 0: tiled prefill kernel + per-row kernel for the rows alone in their run
-    # bit 1: the per-row kernel is the TMA-staged one
-    for mode in (1, 0, 3, 2):
+    # bit 1: the per-row kernel is the TMA-staged one; bit 2: the cluster-split kernel, bits 8-15 its splits
+    for mode in (1, 0, 3, 2, 5, 4, 4 | (1 << 8), 4 | (2 << 8), 4 | (8 << 8), 5 | (8 << 8)):
         out = torch.zeros(R, nh, hd, dtype=torch.bfloat16, device="cuda")
         capi.check(capi.lib().moa_k_attention(q.data_ptr(), rd.data_ptr(), R, meta.data_ptr(), nh, nkv, hd,
                                               kpool.data_ptr(), vpool.data_ptr(), kv_stride, max_ctx, out.data_ptr(),
