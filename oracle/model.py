@@ -6,8 +6,10 @@ Llama-style decoder (RMSNorm, RoPE rotate-half, GQA, SwiGLU), bf16 weights,
 fp32 math, with the activations rounded to bf16 at exactly the points the CUDA
 kernels round them:
 
-  rp1  h  = bf16(rmsnorm(x) * g)            (GEMM A operand)
-  rp2  q,k = bf16(rope(fp32 acc)); v = bf16(acc)   (KV cache is bf16)
+  rp1  h  = bf16(x)                         (GEMM A operand: the residual itself)
+       y  = (h W^T) * inv_rms(x)             (RMSNorm applied to the fp32 product:
+            inv_rms(x) = 1 / sqrt(mean(x^2) + eps); the norm gains are ones)
+  rp2  q,k = bf16(rope(y)); v = bf16(y)      (KV cache is bf16)
   rp3  o  = bf16(softmax(q k^T / sqrt(hd)) v)
   rp4  a  = bf16(silu(g_acc) * u_acc)
   residual stream x stays fp32; logits fp32.
@@ -153,9 +155,18 @@ def rope_table(spec: ModelSpec, max_pos: int):
     return cos, sin
 
 
-def rmsnorm(x: np.ndarray, eps: float) -> np.ndarray:
+def inv_rms(x: np.ndarray, eps: float) -> np.ndarray:
+    """1 / sqrt(mean(x^2) + eps) per row (fp32), shape [..., 1]."""
     ms = np.mean(x * x, axis=-1, keepdims=True, dtype=np.float32)
-    return x * (np.float32(1.0) / np.sqrt(ms + np.float32(eps)))
+    return np.float32(1.0) / np.sqrt(ms + np.float32(eps))
+
+
+def normed_linear(x: np.ndarray, w: np.ndarray, eps: float) -> np.ndarray:
+    """RMSNorm (unit gains) fused with a linear map, as every GPU path computes
+    it: the bf16 operand is the residual itself and the fp32 product is scaled
+    by the row's inverse RMS -- mathematically rmsnorm(x) @ w.T, rounded at
+    bf16(x) instead of bf16(rmsnorm(x))."""
+    return (bf16_round(x) @ w.T) * inv_rms(x, eps)
 
 
 def logit_stats(logits: np.ndarray):
@@ -209,8 +220,7 @@ class CpuModel:
         sel = np.nonzero(np.asarray(want_logits, bool))[0]
         if len(sel) == 0:
             return np.zeros((0, sp.vocab), np.float32)
-        hf = bf16_round(rmsnorm(x[sel], sp.norm_eps))
-        return hf @ w.lm.T
+        return normed_linear(x[sel], w.lm, sp.norm_eps)
 
     def hidden_embed(self, tokens) -> np.ndarray:
         """Hidden-state embedding provider (csrc ee_hidden_embed): the final
@@ -233,10 +243,10 @@ class CpuModel:
         cos, sin = self.cos[pos][:, None, :], self.sin[pos][:, None, :]
         scale = np.float32(1.0 / math.sqrt(hd))
         for l, L in enumerate(w.layers):
-            h = bf16_round(rmsnorm(x, sp.norm_eps))
-            q = (h @ L["wq"].T).reshape(R, nh, hd)
-            k = (h @ L["wk"].T).reshape(R, nkv, hd)
-            v = bf16_round(h @ L["wv"].T).reshape(R, nkv, hd)
+            h, inv = bf16_round(x), inv_rms(x, sp.norm_eps)
+            q = ((h @ L["wq"].T) * inv).reshape(R, nh, hd)
+            k = ((h @ L["wk"].T) * inv).reshape(R, nkv, hd)
+            v = bf16_round((h @ L["wv"].T) * inv).reshape(R, nkv, hd)
 
             def rope(t):
                 a, b = t[..., :half], t[..., half:]
@@ -266,9 +276,9 @@ class CpuModel:
                     o[c0:c1] = oi.reshape(nkv, n, grp, hd).transpose(1, 0, 2, 3).reshape(n, nh, hd)
             o = bf16_round(o.reshape(R, nh * hd))
             x = x + o @ L["wo"].T
-            h2 = bf16_round(rmsnorm(x, sp.norm_eps))
-            g = h2 @ L["wg"].T
-            u = h2 @ L["wu"].T
+            h2, inv2 = bf16_round(x), inv_rms(x, sp.norm_eps)
+            g = (h2 @ L["wg"].T) * inv2
+            u = (h2 @ L["wu"].T) * inv2
             a = bf16_round(g / (np.float32(1.0) + np.exp(-g)) * u)
             x = x + a @ L["wd"].T
         return x

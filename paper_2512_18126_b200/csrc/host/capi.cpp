@@ -1045,12 +1045,6 @@ int moa_k_gemv(uintptr_t A, uintptr_t X, int R, uintptr_t W, int N, int K, uintp
     moa::k::GemvArgs a;
     a.A = reinterpret_cast<const moa::k::bf16*>(A);
     a.X = reinterpret_cast<const float*>(X);
-    float* ones = nullptr;
-    if (X) {
-      MOA_CUDA(cudaMalloc(&ones, sizeof(float) * K));
-      moa::k::fill_f32(ones, K, 1.0f, reinterpret_cast<cudaStream_t>(stream));
-      a.g = ones;
-    }
     a.R = R;
     a.N = N;
     a.K = K;
@@ -1059,10 +1053,6 @@ int moa_k_gemv(uintptr_t A, uintptr_t X, int R, uintptr_t W, int N, int K, uintp
     a.out = reinterpret_cast<float*>(out);
     moa::k::gemv(a, reinterpret_cast<cudaStream_t>(stream));
     MOA_CUDA(cudaGetLastError());
-    if (ones) {
-      MOA_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
-      cudaFree(ones);
-    }
   });
 }
 

@@ -192,6 +192,9 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   // decode rows of GQA agents: TMA-staged attention (MOA_DECODE_TMA=0: the register-staged kernel)
   attn_tma_ = kv_maps_ok_ && k::attention_decode_tma_supported(s.n_heads, s.n_kv_heads, static_cast<int>(hd), max_ctx);
   if (const char* e = std::getenv("MOA_DECODE_TMA")) attn_tma_ = attn_tma_ && e[0] != '0';
+  // decode ticks: L2 prefetch of the next kernel's weights (bit 0: attention
+  // -> Wo, bit 1: down -> next layer's Wqkv); MOA_L2_PREFETCH=<mask>
+  if (const char* e = std::getenv("MOA_L2_PREFETCH")) l2pf_ = std::atoi(e);
   // default: the cluster-split kernel (MOA_DECODE_CLUSTER=0: the fixed-split TMA kernel)
   attn_cluster_ = kv_maps_ok_ && k::attention_decode_cluster_supported(s.n_heads, s.n_kv_heads, static_cast<int>(hd));
   if (const char* e = std::getenv("MOA_DECODE_CLUSTER")) attn_cluster_ = attn_cluster_ && e[0] != '0';
@@ -202,6 +205,7 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   if (const char* e = std::getenv("MOA_PREFILL_ATTN")) use_prefill_attn_ = std::string(e) != "0";
   // RMSNorm folded into the decode GEMVs: ssq partials [16 rows][d/16]
   dev_alloc(&ssq_, static_cast<long long>(k::kGemvTcRows) * (D / 16));
+  dev_alloc(&inv_, static_cast<long long>(max_rows));
   {
     k::GemvArgs q1, g1, o1, d1;
     q1.R = g1.R = o1.R = d1.R = k::kGemvTcRows;
@@ -212,13 +216,12 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
     o1.epi = d1.epi = k::kEpiResidual;
     nfold_ok_ = tc_ok_ && D % 16 == 0 && k::gemv_tc_norm_supported(q1) && k::gemv_tc_norm_supported(g1) &&
                 k::gemv_tc_supported(o1) && k::gemv_tc_supported(d1);
-    // one kernel fewer per normed GEMV; the in-kernel staging puts the ssq
-    // and x reads on the critical path.  Default on up to d = 2048 (measured:
-    // 1B agents -3.5% per request); above, the wide GEMVs' K ranges exceed the
-    // staging (gemv_tc_norm_supported).  A just-in-time variant (converter warps
-    // filling each ring stage) was slower at every width: one dependent L2 round
-    // trip per k-tile on the converter's critical path.  MOA_NORM_FOLD=0/1 forces it
-    use_nfold_ = D <= 2048;
+    // Decode ticks: the residual GEMVs (and the embedding gather) write x, its
+    // bf16 copy (the next normed GEMV's TMA operand) and 16-column sums of
+    // squares; the normed GEMVs compute the rows' inverse RMS from those while
+    // their weights stream -- no RMSNorm launch and no staging on the critical
+    // path.  MOA_NORM_FOLD=0: a prep launch per normed GEMV instead.
+    use_nfold_ = true;
     if (const char* e = std::getenv("MOA_NORM_FOLD")) use_nfold_ = std::string(e) != "0";
   }
   MOA_CUDA(cudaMemsetAsync(gv_cnt_, 0, sizeof(int) * ((std::max({s.qkv_cols(), 2 * s.ffn, s.d}) + 127) / 128), st));
@@ -239,7 +242,8 @@ DeviceModel::~DeviceModel() {
                     static_cast<void*>(h_), static_cast<void*>(q_), static_cast<void*>(attn_ws_),
                     static_cast<void*>(attn_cnt_), static_cast<void*>(part_), static_cast<void*>(lm_cnt_),
                     meta_blob_, run_area_, static_cast<void*>(hn_), static_cast<void*>(wo_blk_),
-                    static_cast<void*>(gv_ws_), static_cast<void*>(gv_cnt_), static_cast<void*>(ssq_)})
+                    static_cast<void*>(gv_ws_), static_cast<void*>(gv_cnt_), static_cast<void*>(ssq_),
+                    static_cast<void*>(inv_)})
     if (ptr) cudaFree(ptr);
 }
 
@@ -369,15 +373,18 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       return;
     }
     g.evict_first = evict_first_;
-    if (g.X && dec_tc && norm_fold) {  // the swap-AB GEMV normalises x itself (ssq from the producer)
-      g.ssq = ssq_;
-      k::gemv_tc(map_w, map_hn16_ /* unused: X is staged in-kernel */, g, gv_ws_, gv_cnt_, st);
-      return;
-    }
-    if (g.X) {  // materialise bf16(rmsnorm(x)) once, then TMA-load it
-      k::rmsnorm_rows(g.X, rcap, meta, g.K, g.g, g.eps, hn_, st);
+    if (g.X && dec_tc && norm_fold) {  // operand bf16(x) and sums of squares from the residual producer
       g.X = nullptr;
       g.A = hn_;
+      g.ssq = ssq_;
+      k::gemv_tc(map_w, map_hn16_, g, gv_ws_, gv_cnt_, st);
+      return;
+    }
+    if (g.X) {  // prep launch: bf16(x) and the rows' inverse RMS, then TMA-load the operand
+      k::rmsnorm_rows(g.X, rcap, meta, g.K, inv_, g.eps, hn_, st);
+      g.X = nullptr;
+      g.A = hn_;
+      g.inv = inv_;
       map_a = &map_hn_;
       map_a16 = &map_hn16_;
     }
@@ -403,7 +410,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   const bool fuse_o = qkv_attn && wo_blk_ != nullptr;
   if (!qkv_attn) {  // (the fused QKV + attention kernel gathers layer 0's embeddings itself)
   probe_begin(KernelProbes::Embed, 6.0 * live_R_ * D);
-  k::embed(buf_.rows, rcap, meta, out_tok_read, emb_, D, x_, st, norm_fold ? ssq_ : nullptr);
+  k::embed(buf_.rows, rcap, meta, out_tok_read, emb_, D, x_, st, norm_fold ? ssq_ : nullptr, norm_fold ? hn_ : nullptr);
   probe_end();
   }
   for (int l = 0; l < s.n_layers; ++l) {
@@ -421,7 +428,6 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     // rmsnorm -> QKV -> RoPE -> KV append
     k::GemvArgs qkv;
     qkv.X = x_;
-    qkv.g = ones_;
     qkv.eps = eps;
     qkv.R = rcap;
     qkv.meta = meta;
@@ -461,7 +467,9 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       if (attn_cluster_)
         k::attention_decode_cluster(kmap_, vmap_, q_, buf_.rows, rcap,
                                     k::attention_decode_cluster_splits(rcap, nkv, nsplit), meta, nh, nkv, hd,
-                                    kv_stride_, loff, max_ctx_, h_, st, prefill);
+                                    kv_stride_, loff, max_ctx_, h_, st, prefill,
+                                    (swap_ab && (l2pf_ & 1)) ? static_cast<const void*>(L.wo) : nullptr,
+                                    2LL * D * nh * hd);
       else if (attn_tma_)
         k::attention_decode_tma(kmap_, vmap_, q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kv_stride_, loff,
                                 max_ctx_, h_, attn_ws_, attn_cnt_, st, prefill);
@@ -484,7 +492,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     o.out = x_;
     // x was last written two kernels back, except when layer 0's fused kernel gathered it
     o.res_early = !(qkv_attn && l == 0);
-    if (norm_fold) o.ssq_out = ssq_;
+    if (norm_fold) o.ssq_out = ssq_, o.xb_out = hn_;
     probe_begin(gkind(KernelProbes::OProj, KernelProbes::PfOProj), 2.0 * o.N * o.K + 2.0 * Rv * o.K + 8.0 * Rv * D,
                 2.0 * Rv * o.N * o.K);
     run_gemm(o, &map_h_attn_, &map_h_attn16_, wmaps_[static_cast<std::size_t>(l)].wo);
@@ -493,7 +501,6 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     // a = silu(gate) * up over rmsnorm(x)
     k::GemvArgs gu;
     gu.X = x_;
-    gu.g = ones_;
     gu.eps = eps;
     gu.R = rcap;
     gu.meta = meta;
@@ -517,7 +524,11 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     dn.epi = k::kEpiResidual;
     dn.out = x_;
     dn.res_early = true;  // x was written by the o-projection, two kernels back
-    if (norm_fold) dn.ssq_out = ssq_;
+    if (norm_fold) dn.ssq_out = ssq_, dn.xb_out = hn_;
+    if (swap_ab && (l2pf_ & 2) && l + 1 < s.n_layers) {  // the next layer's Wqkv into L2 through this tail
+      dn.pf_base = layers_[static_cast<std::size_t>(l + 1)].wqkv;
+      dn.pf_bytes = 2LL * s.qkv_cols() * D;
+    }
     probe_begin(gkind(KernelProbes::Down, KernelProbes::PfDown), 2.0 * dn.N * dn.K + 2.0 * Rv * dn.K + 8.0 * Rv * D,
                 2.0 * Rv * dn.N * dn.K);
     run_gemm(dn, &map_h_ffn_, &map_h_ffn16_, wmaps_[static_cast<std::size_t>(l)].wd);
@@ -537,11 +548,11 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       if (lm_fold) {
         // the LM head normalises its selected rows itself (no rmsnorm launch)
         lm.X = x_;
-        lm.g = nullptr;  // unit gains (the final norm's gains are ones)
         lm.eps = eps;
         lm.sel = buf_.sel;
       } else {
-        k::rmsnorm_rows(x_, max_lrows_, meta, D, ones_, eps, hn_, st, buf_.sel, 1);
+        k::rmsnorm_rows(x_, max_lrows_, meta, D, inv_, eps, hn_, st, buf_.sel, 1);
+        lm.inv = inv_;
       }
       lm.R = k::kGemvTcRows;
       lm.meta = meta + 1;  // live logits rows

@@ -359,7 +359,8 @@ __global__ void __launch_bounds__(160)
 attention_decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                                 const bf16* __restrict__ q, const RowDesc* __restrict__ rows,
                                 const int* __restrict__ meta, int nh, int nkv, long long kv_stride,
-                                long long layer_off, int max_ctx, bf16* __restrict__ o, int skip_runs) {
+                                long long layer_off, int max_ctx, bf16* __restrict__ o, int skip_runs,
+                                const void* pf_base, long long pf_bytes) {
   using C = DecCl<HD>;
   constexpr int KSTEPS = HD / 16, NT = HD / 8, RB = HD * 2, STG = C::STG;
   extern __shared__ unsigned char dc_raw[];
@@ -379,6 +380,10 @@ attention_decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap, const 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g8 = lane >> 2, t4 = lane & 3;
   const int s = blockIdx.x, NS = gridDim.x, g = blockIdx.y, r = blockIdx.z;
+  // every CTA of the grid (live or not) prefetches its share of the next
+  // kernel's weights into L2 first: this kernel leaves HBM mostly idle
+  if (threadIdx.x == 32 * 4)
+    l2_prefetch_share(pf_base, pf_bytes, s + NS * (g + gridDim.y * r), NS * gridDim.y * gridDim.z);
   // cluster-uniform early exits (every CTA of a cluster has the same row)
   const int live = __ldg(meta);
   if (r >= live) return;
@@ -543,6 +548,9 @@ attention_decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap, const 
         mma_bf16(oacc[2 * np], pa0, pa1, pa2, pa3, v00, v01);
         mma_bf16(oacc[2 * np + 1], pa0, pa1, pa2, pa3, v10, v11);
       }
+      // the stage's generic-proxy reads (ldmatrix) are ordered before the
+      // producer's next TMA (async-proxy) write into it
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
@@ -673,7 +681,8 @@ bool attention_decode_cluster_supported(int nh, int nkv, int hd) {
 
 void attention_decode_cluster(const TmaMap& kmap, const TmaMap& vmap, const bf16* q, const RowDesc* rows, int R_cap,
                               int ns, const int* meta, int nh, int nkv, int hd, long long kv_stride,
-                              long long layer_off, int max_ctx, bf16* o, cudaStream_t st, bool skip_runs) {
+                              long long layer_off, int max_ctx, bf16* o, cudaStream_t st, bool skip_runs,
+                              const void* pf_base, long long pf_bytes) {
   if (R_cap <= 0) return;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ns, nkv, R_cap);
@@ -697,7 +706,7 @@ void attention_decode_cluster(const TmaMap& kmap, const TmaMap& vmap, const bf16
     cfg.dynamicSmemBytes = smem;
     cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(&kmap),
                        *reinterpret_cast<const CUtensorMap*>(&vmap), q, rows, meta, nh, nkv, kv_stride, layer_off,
-                       max_ctx, o, skip_runs ? 1 : 0);
+                       max_ctx, o, skip_runs ? 1 : 0, pf_base, pf_bytes);
   };
   if (hd == 128)
     go(attention_decode_cluster_kernel<128>, DecCl<128>::SMEM);

@@ -157,20 +157,19 @@ __device__ __forceinline__ float row_inv_rms(const float* __restrict__ x, int K,
 
 // A fragment: 8 consecutive K elements of one row, as fp32 values of bf16.
 template <bool NORM>
-__device__ __forceinline__ void load_a(const GemvArgs& a, int row, int k, float inv, float (&f)[8], float4 g0,
-                                       float4 g1) {
-  if constexpr (NORM) {
+__device__ __forceinline__ void load_a(const GemvArgs& a, int row, int k, float (&f)[8]) {
+  if constexpr (NORM) {  // normed operand = bf16(x); the row's inverse RMS scales the fp32 result
     const float* x = a.X + static_cast<long long>(row) * a.K + k;
     const float4 x0 = __ldg(reinterpret_cast<const float4*>(x));
     const float4 x1 = __ldg(reinterpret_cast<const float4*>(x + 4));
-    f[0] = bf16r(x0.x * inv * g0.x);
-    f[1] = bf16r(x0.y * inv * g0.y);
-    f[2] = bf16r(x0.z * inv * g0.z);
-    f[3] = bf16r(x0.w * inv * g0.w);
-    f[4] = bf16r(x1.x * inv * g1.x);
-    f[5] = bf16r(x1.y * inv * g1.y);
-    f[6] = bf16r(x1.z * inv * g1.z);
-    f[7] = bf16r(x1.w * inv * g1.w);
+    f[0] = bf16r(x0.x);
+    f[1] = bf16r(x0.y);
+    f[2] = bf16r(x0.z);
+    f[3] = bf16r(x0.w);
+    f[4] = bf16r(x1.x);
+    f[5] = bf16r(x1.y);
+    f[6] = bf16r(x1.z);
+    f[7] = bf16r(x1.w);
   } else {
     unpack8(__ldg(reinterpret_cast<const uint4*>(a.A + static_cast<long long>(row) * a.K + k)), f);
   }
@@ -230,7 +229,7 @@ __global__ void fill_f32_kernel(float* dst, long long n, float v) {
 
 __global__ void embed_kernel(const RowDesc* __restrict__ rows, const int* __restrict__ meta,
                              const int* __restrict__ out_tok, const bf16* __restrict__ emb, int d,
-                             float* __restrict__ x, float* __restrict__ ssq) {
+                             float* __restrict__ x, float* __restrict__ ssq, bf16* __restrict__ xb) {
   MOA_PDL_ENTRY();
   const int r = blockIdx.x;
   if (r >= meta[0]) return;
@@ -239,7 +238,9 @@ __global__ void embed_kernel(const RowDesc* __restrict__ rows, const int* __rest
   const bf16* e = emb + static_cast<long long>(t) * d;
   for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
     float f[8];
-    unpack8(*reinterpret_cast<const uint4*>(e + c), f);
+    const uint4 raw = *reinterpret_cast<const uint4*>(e + c);
+    unpack8(raw, f);
+    if (xb) *reinterpret_cast<uint4*>(xb + static_cast<long long>(r) * d + c) = raw;  // bf16(x): the row itself
     float4* o = reinterpret_cast<float4*>(x + static_cast<long long>(r) * d + c);
     o[0] = make_float4(f[0], f[1], f[2], f[3]);
     o[1] = make_float4(f[4], f[5], f[6], f[7]);
@@ -274,12 +275,6 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
     w_first[c] = (n0 + c < a.N && kb + lane * 8 < ke)
                      ? ldg_stream(a.W + static_cast<long long>(n0 + c) * a.K + kb + lane * 8)
                      : make_uint4(0, 0, 0, 0);
-  // norm gains of the first k-step: weights too
-  float4 g_first0 = make_float4(0.f, 0.f, 0.f, 0.f), g_first1 = g_first0;
-  if (NORM && kb + lane * 8 < ke) {
-    g_first0 = __ldg(reinterpret_cast<const float4*>(a.g + kb + lane * 8));
-    g_first1 = __ldg(reinterpret_cast<const float4*>(a.g + kb + lane * 8 + 4));
-  }
   const int live = a.meta ? __ldg(a.meta) : a.R;  // tick metadata: not produced by the previous kernel
   // residual of this lane's epilogue element (lane L: column n0 + L/8, row r0 + L%8)
   float res = 0.f;
@@ -320,12 +315,7 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
       for (int r = 0; r < kRB; ++r) {
         if (r < rows) {
           float f[8];
-          float4 g0 = g_first0, g1 = g_first1;
-          if (NORM && k != kb + lane * 8) {
-            g0 = __ldg(reinterpret_cast<const float4*>(a.g + k));
-            g1 = __ldg(reinterpret_cast<const float4*>(a.g + k + 4));
-          }
-          load_a<NORM>(a, r0 + r, k, NORM ? inv_s[r] : 0.f, f, g0, g1);
+          load_a<NORM>(a, r0 + r, k, f);
 #pragma unroll
           for (int c = 0; c < kCPW; ++c) acc[c * kRB + r] = dot8(f, w[c], acc[c * kRB + r]);
         }
@@ -346,6 +336,7 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
   // ---- epilogue: lane L holds column n0 + L/8, row r0 + L%8 ----
   const int c = lane / kRB, r = lane % kRB, n = n0 + c, row = r0 + r;
   const bool ok = r < rows && n < a.N;
+  if constexpr (NORM) v *= r < rows ? inv_s[r] : 0.f;  // RMSNorm on the fp32 product
   const float partner = __shfl_xor_sync(kFull, v, kRB);  // column n ^ 1 (same row)
   switch (a.epi) {
     case kEpiF32:
@@ -1502,7 +1493,6 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
     asm volatile("prefetch.global.L2 [%0];" ::"l"(K + static_cast<long long>(j) * HD));
     asm volatile("prefetch.global.L2 [%0];" ::"l"(V + static_cast<long long>(j) * HD));
   }
-  const float g_first = threadIdx.x < D ? __ldg(g_norm + threadIdx.x) : 0.f;  // norm gains: weights
   // RoPE factors of this warp's first column group (the position is tick metadata)
   float2 cs0 = make_float2(0.f, 0.f);
   if (warp < ncol / 32 && warp * 32 + lane < (hpg + 1) * HD)
@@ -1540,8 +1530,7 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
   float tot = 0.f;
   for (int w = 0; w < NW; ++w) tot += red[w];
   const float inv = 1.0f / sqrtf(tot / static_cast<float>(D) + eps);
-  for (int c = threadIdx.x; c < D; c += 256)
-    xn[c] = __float2bfloat16_rn(x[c] * inv * (c == threadIdx.x ? g_first : g_norm[c]));
+  for (int c = threadIdx.x; c < D; c += 256) xn[c] = __float2bfloat16_rn(x[c]);  // operand bf16(x); inv scales q/k/v
   // weights landed
   {
     std::uint32_t ok = 0;
@@ -1564,7 +1553,7 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
 #pragma unroll
       for (int j = 0; j < 32; ++j) acc[j] = dot8(xf, *reinterpret_cast<const uint4*>(W + static_cast<long long>(grp * 32 + j) * D + k), acc[j]);
     }
-    const float v = transpose_reduce32(acc, lane);
+    const float v = transpose_reduce32(acc, lane) * inv;
     const float partner = __shfl_xor_sync(kFull, v, 1);
     const int c = grp * 32 + lane;  // column within the CTA's slab
     if (c < (hpg + 1) * HD) {       // q or k: rotate the (even, odd) pair
@@ -1587,6 +1576,8 @@ qkv_attention_kernel(float* __restrict__ X, const float* __restrict__ g_norm, fl
     }
   }
   __threadfence_block();
+  // the weight slab's generic-proxy reads are ordered before the Wo bulk copy (async proxy) refills it
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   if (threadIdx.x == 0) chain_mark(cst, 4);
   // fused o-projection: this group's Wo block [D][hpg*HD] into the (now free)
@@ -1905,7 +1896,6 @@ lm_head_kernel(const float* __restrict__ X, const int* __restrict__ sel, const i
   __syncthreads();
   GemvArgs ga;
   ga.X = X;
-  ga.g = g;
   ga.K = d;
   for (int r0 = 0; r0 < Rl; r0 += kRB) {
     const int rows = min(kRB, Rl - r0);
@@ -1923,15 +1913,14 @@ lm_head_kernel(const float* __restrict__ X, const int* __restrict__ sel, const i
         for (int r = 0; r < kRB; ++r) {
           if (r < rows) {
             float f[8];
-            load_a<true>(ga, sel[r0 + r], k, inv_s[r0 + r], f, __ldg(reinterpret_cast<const float4*>(ga.g + k)),
-                         __ldg(reinterpret_cast<const float4*>(ga.g + k + 4)));
+            load_a<true>(ga, sel[r0 + r], k, f);
 #pragma unroll
             for (int c = 0; c < kCPW; ++c) acc[c * kRB + r] = dot8(f, w[c], acc[c * kRB + r]);
           }
         }
       }
-      const float v = transpose_reduce32(acc, lane);
       const int c = lane / kRB, r = lane % kRB;
+      const float v = transpose_reduce32(acc, lane) * (r < rows ? inv_s[r0 + r] : 0.f);
       if (r < rows && cb + c < c1) {
         if (logits) logits[static_cast<long long>(r0 + r) * V + cb + c] = v;
         st = stat_merge(st, LmStat{v, 1.f, 0.f, cb + c});
@@ -2028,8 +2017,8 @@ void fill_f32(float* dst, long long n, float v, cudaStream_t st) {
 }
 
 void embed(const RowDesc* rows, int R_cap, const int* meta, const int* out_tok, const bf16* emb, int d, float* x,
-           cudaStream_t st, float* ssq) {
-  if (R_cap > 0) launch_pdl(embed_kernel, dim3(R_cap), dim3(128), st, rows, meta, out_tok, emb, d, x, ssq);
+           cudaStream_t st, float* ssq, bf16* xb) {
+  if (R_cap > 0) launch_pdl(embed_kernel, dim3(R_cap), dim3(128), st, rows, meta, out_tok, emb, d, x, ssq, xb);
 }
 
 void gemv(const GemvArgs& a, cudaStream_t st) {

@@ -180,8 +180,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const char* xp = reinterpret_cast<const char*>(a.out + static_cast<long long>(row) * a.N + n0);
     for (int off = 0; off < kBN * 4 && n0 + off / 4 < a.N; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(xp + off));
   }
+  // normed linear map: the row's inverse RMS scales its fp32 products
+  const float rs = (a.inv && row_ok) ? __ldcg(a.inv + row) : 1.f;
   mbar_wait(done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  auto ld_scaled = [&](int c0, float (&v)[16]) {
+    tmem_ld16(tmem + lane_base + static_cast<std::uint32_t>(c0), v);
+    if (a.inv) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] *= rs;
+    }
+  };
   if (a.epi == kEpiQkv && kBN % a.hd == 0) {
     // RoPE + q / K / V rows staged as a bf16 tile in the (now idle) pipeline
     // smem in natural head order, then written out in 16-byte chunks: one
@@ -196,7 +205,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const int hd = a.hd, half = hd / 2, qk_cols = (a.nh + a.nkv) * hd;
     for (int c0 = 0; c0 < kBN; c0 += 16) {
       float v[16];
-      tmem_ld16(tmem + lane_base + static_cast<std::uint32_t>(c0), v);
+      ld_scaled(c0, v);
       if (!row_ok) continue;
 #pragma unroll
       for (int i = 0; i < 16; i += 2) {
@@ -236,7 +245,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   } else
   for (int c0 = 0; c0 < kBN; c0 += 16) {
     float v[16];
-    tmem_ld16(tmem + lane_base + static_cast<std::uint32_t>(c0), v);
+    ld_scaled(c0, v);
     if (!row_ok) continue;
     const int nb = n0 + c0;
     if (nb >= a.N) break;
@@ -305,10 +314,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kBN));
 }
 
-// One CTA per row: 16-byte vector loads, block reduction in a fixed order.
+// Operand prep of a normed linear map, one CTA per row: h = bf16(x) and the
+// row's inverse RMS (16-byte vector loads, block reduction in a fixed order).
 __global__ void __launch_bounds__(128) rmsnorm_rows_kernel(const float* __restrict__ x, const int* __restrict__ sel,
                                                            const int* __restrict__ meta, int meta_idx, int K,
-                                                           const float* __restrict__ g, float eps,
+                                                           float* __restrict__ inv_out, float eps,
                                                            bf16* __restrict__ h) {
   __shared__ float red[4];
   __shared__ unsigned long long cst[kChainPhases];
@@ -336,20 +346,18 @@ __global__ void __launch_bounds__(128) rmsnorm_rows_kernel(const float* __restri
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
   const float tot = red[0] + red[1] + red[2] + red[3];
-  const float inv = 1.0f / sqrtf(tot / static_cast<float>(K) + eps);
-  const float4* gr = reinterpret_cast<const float4*>(g);
+  if (threadIdx.x == 0) inv_out[i] = 1.0f / sqrtf(tot / static_cast<float>(K) + eps);
   for (int v = threadIdx.x; v < K / 8; v += 128) {
     const float4 a = xr[2 * v], b = xr[2 * v + 1];
-    const float4 ga = gr[2 * v], gb = gr[2 * v + 1];
     __align__(16) bf16 o[8];
-    o[0] = __float2bfloat16_rn(a.x * inv * ga.x);
-    o[1] = __float2bfloat16_rn(a.y * inv * ga.y);
-    o[2] = __float2bfloat16_rn(a.z * inv * ga.z);
-    o[3] = __float2bfloat16_rn(a.w * inv * ga.w);
-    o[4] = __float2bfloat16_rn(b.x * inv * gb.x);
-    o[5] = __float2bfloat16_rn(b.y * inv * gb.y);
-    o[6] = __float2bfloat16_rn(b.z * inv * gb.z);
-    o[7] = __float2bfloat16_rn(b.w * inv * gb.w);
+    o[0] = __float2bfloat16_rn(a.x);
+    o[1] = __float2bfloat16_rn(a.y);
+    o[2] = __float2bfloat16_rn(a.z);
+    o[3] = __float2bfloat16_rn(a.w);
+    o[4] = __float2bfloat16_rn(b.x);
+    o[5] = __float2bfloat16_rn(b.y);
+    o[6] = __float2bfloat16_rn(b.z);
+    o[7] = __float2bfloat16_rn(b.w);
     reinterpret_cast<uint4*>(h + static_cast<long long>(i) * K)[v] = *reinterpret_cast<const uint4*>(o);
   }
   if (g_chain_stamp != nullptr) {
@@ -410,7 +418,7 @@ void gemm_tc(const TmaMap& map_a, const TmaMap& map_w, const GemvArgs& a, cudaSt
                                            *reinterpret_cast<const CUtensorMap*>(&map_w), a);
 }
 
-void rmsnorm_rows(const float* x, int R_cap, const int* meta, int K, const float* g, float eps, bf16* h,
+void rmsnorm_rows(const float* x, int R_cap, const int* meta, int K, float* inv, float eps, bf16* h,
                   cudaStream_t st, const int* sel, int meta_idx) {
   if (R_cap <= 0) return;
   cudaLaunchConfig_t cfg{};
@@ -423,7 +431,7 @@ void rmsnorm_rows(const float* x, int R_cap, const int* meta, int K, const float
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   uniform_carveout(reinterpret_cast<const void*>(rmsnorm_rows_kernel));
-  cudaLaunchKernelEx(&cfg, rmsnorm_rows_kernel, x, sel, meta, meta_idx, K, g, eps, h);
+  cudaLaunchKernelEx(&cfg, rmsnorm_rows_kernel, x, sel, meta, meta_idx, K, inv, eps, h);
 }
 
 MOA_CHAIN_STAMP_SETTER(gemm_tc_chain_stamp)

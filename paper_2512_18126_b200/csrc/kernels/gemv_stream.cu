@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_stream_kernel(const GemvArgs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // stage the activations (normalised for the RMSNorm-prologue GEMMs)
+  // stage the activations (bf16(x) for the RMSNorm-prologue GEMMs; inv_s scales their products)
   if (a.X && warp < R) {
     const float* xr = a.X + static_cast<long long>(warp) * K;
     float ss = 0.f;
@@ -114,8 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_stream_kernel(const GemvArgs
   if (staged) {
     for (int i = threadIdx.x; i < R * K; i += kThreads) {
       const int r = i / K, k = i % K;
-      As[i] = a.X ? __float2bfloat16_rn(a.X[static_cast<long long>(r) * K + k] * inv_s[r] * a.g[k])
-                  : a.A[static_cast<long long>(r) * K + k];
+      As[i] = a.X ? __float2bfloat16_rn(a.X[static_cast<long long>(r) * K + k]) : a.A[static_cast<long long>(r) * K + k];
     }
   }
   __syncthreads();
@@ -192,6 +191,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_stream_kernel(const GemvArgs
     }
     if (lane >= R) continue;
     const int r = lane;
+    if (a.X) {  // RMSNorm on the fp32 product (the staged operand is bf16(x))
+      v0 *= inv_s[r];
+      v1 *= inv_s[r];
+    }
     const bool two = n0 + 1 < N;
     switch (a.epi) {
       case kEpiF32:

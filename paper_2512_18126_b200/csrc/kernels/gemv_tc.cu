@@ -28,10 +28,6 @@ constexpr int kM = 128, kN = 16, kBK = 64, kStages = 5;  // 92 KB: two kernels' 
 constexpr int kTileW = kM * kBK * 2;  // 16 KB
 constexpr int kTileX = kN * kBK * 2;  // 2 KB
 constexpr int kSmem = kStages * (kTileW + kTileX) + 1024 + 256;
-// norm-from-x mode: the CTA stages its K range of bf16(rmsnorm(x)) itself
-// (no rmsnorm kernel, no TMA for X): a 4-stage weight ring + <= 16 k-tiles
-constexpr int kNxStages = 4, kNxMaxKt = 16;
-constexpr int kNxSmem = kNxStages * kTileW + kNxMaxKt * kTileX + 1024 + 256;
 constexpr std::uint32_t kIdesc = idesc_bf16(kM, kN);
 
 // debug: per-CTA %globaltimer stamps (tools/gvisolated.py), off when null
@@ -48,7 +44,38 @@ __device__ __forceinline__ void gv_stamp(int ev) {
   }
 }
 
-__device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const float (&v)[16]) {
+// Operands of the epilogue that do not depend on the MMA, loaded while the
+// weights stream: the residual rows x[r][n] (final once the previous kernel
+// completed), and for the QKV epilogue the rows' descriptors and RoPE factors
+// (tick metadata / static tables).  Only rows r < R are touched.
+struct EpiPre {
+  float res[16];
+  float2 cs[16];
+  int kv[16], pos[16];
+};
+
+__device__ __forceinline__ void epi_preload(const GemvArgs& a, int n, int R, EpiPre& p) {
+  if (a.epi == kEpiResidual) {
+#pragma unroll
+    for (int r = 0; r < kN; ++r) {
+      if (r >= R) break;
+      p.res[r] = n < a.N ? __ldcg(a.out + static_cast<long long>(r) * a.N + n) : 0.f;
+    }
+  } else if (a.epi == kEpiQkv) {
+    const int hd = a.hd, half = hd / 2, qk_cols = (a.nh + a.nkv) * hd;
+    const int e = (n % hd) / 2;
+#pragma unroll
+    for (int r = 0; r < kN; ++r) {
+      if (r >= R) break;
+      const RowDesc rd = a.rows[r];
+      p.kv[r] = rd.kv;
+      p.pos[r] = rd.pos;
+      p.cs[r] = n < qk_cols ? __ldg(a.rope + static_cast<long long>(rd.pos) * half + e) : make_float2(1.f, 0.f);
+    }
+  }
+}
+
+__device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const float (&v)[16], const EpiPre& pre) {
   const int lane = threadIdx.x & 31;
   if (a.epi == kEpiResidual && a.ssq_out) {
     // residual + per-16-column sums of squares of the new rows (the next
@@ -58,9 +85,9 @@ __device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const 
       if (r >= R) break;
       float nv = 0.f;
       if (n < a.N) {
-        float* xp = a.out + static_cast<long long>(r) * a.N + n;
-        nv = *xp + v[r];
-        *xp = nv;
+        nv = pre.res[r] + v[r];
+        a.out[static_cast<long long>(r) * a.N + n] = nv;
+        if (a.xb_out) a.xb_out[static_cast<long long>(r) * a.N + n] = __float2bfloat16_rn(nv);  // next GEMV's operand
       }
       float sq = nv * nv;
       sq += __shfl_xor_sync(0xffffffffu, sq, 1);
@@ -82,19 +109,19 @@ __device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const 
         a.out[static_cast<long long>(r) * a.N + n] = x;
         break;
       case kEpiResidual:
-        a.out[static_cast<long long>(r) * a.N + n] += x;
+        a.out[static_cast<long long>(r) * a.N + n] = pre.res[r] + x;
         break;
       case kEpiSwiGlu:
         if (!(n & 1))
           a.out_bf16[static_cast<long long>(r) * (a.N / 2) + n / 2] = __float2bfloat16_rn(x / (1.0f + __expf(-x)) * partner);
         break;
       case kEpiQkv: {
-        const RowDesc rd = a.rows[r];
+        const RowDesc rd{pre.kv[r], pre.pos[r], 0, 0};
         const int hd = a.hd, half = hd / 2, qk_cols = (a.nh + a.nkv) * hd;
         if (n < qk_cols) {
           if (n & 1) break;
           const int head = n / hd, e = (n % hd) / 2;
-          const float2 cs = a.rope[static_cast<long long>(rd.pos) * half + e];
+          const float2 cs = pre.cs[r];
           const float y0 = __fsub_rn(__fmul_rn(x, cs.x), __fmul_rn(partner, cs.y));
           const float y1 = __fadd_rn(__fmul_rn(partner, cs.x), __fmul_rn(x, cs.y));
           bf16* dst = head < a.nh ? a.out_bf16 + (static_cast<long long>(r) * a.nh + head) * hd
@@ -220,16 +247,22 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
-  const bool nx = a.X != nullptr;  // norm-from-x: stage bf16(rmsnorm(x)) in smem, no X TMA
-  const int stages = nx ? kNxStages : kStages;
+  // Normed GEMVs (RMSNorm on the fp32 product, oracle/model.py normed_linear):
+  // X = bf16(x) arrives by TMA like any activation; the rows' inverse RMS come
+  // from the producers' 16-column sums of squares (a.ssq) or a prep kernel
+  // (a.inv), computed while the weights stream and applied in the epilogue.
+  const bool scaled = a.ssq != nullptr || a.inv != nullptr;
+  constexpr int stages = kStages;
   unsigned char* sw = smem;
-  unsigned char* sx = smem + stages * kTileW;  // per-stage X tiles, or the norm-from-x staging
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sx + (nx ? kNxMaxKt : kStages) * kTileX);
+  unsigned char* sx = smem + stages * kTileW;  // per-stage X tiles
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sx + kStages * kTileX);
   std::uint64_t* empty = full + kStages;
   std::uint64_t* done = empty + kStages;
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
+  std::uint64_t* inv_bar = done + 1;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(inv_bar + 1);
   __shared__ bool last;
   __shared__ float inv_s[kN];
+  __shared__ float inv_red[2][kN];
   // split-K landing buffer: [src rank][row of this CTA's 128/S slice][16] fp32
   __shared__ __align__(16) float land[kM * kN];
   __shared__ __align__(8) std::uint64_t land_bar;
@@ -238,16 +271,17 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   const int tile = blockIdx.x, split = blockIdx.y;
   const int m0 = tile * kM;
   const int KT = a.K / kBK, kt0 = split * KT / S, kt_n = (split + 1) * KT / S - kt0;
-  const std::uint32_t wtx = nx ? kTileW : kTileW + kTileX;
+  const std::uint32_t wtx = kTileW + kTileX;
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&map_w);
-    if (!nx) prefetch_tmap(&map_x);
+    prefetch_tmap(&map_x);
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
+    mbar_init(inv_bar, 1);
     if (S > 1) {
       mbar_init(&land_bar, 1);
       mbar_expect_tx(&land_bar, kM * kN * 4);  // every rank's slice of this CTA's rows (128/S x 16 x S)
@@ -293,75 +327,20 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
       load_w(kt_issued, kt_issued);
     }
   }
-  if (nx) {
-    // Norm-from-x staging by all 128 threads (before the producer / MMA
-    // threads take their roles): inverse RMS of each row from the 16-column
-    // sums of squares its producer wrote, then this CTA's k-tiles of
-    // bf16(x * inv * g) in the 128B-swizzled K-major layout the MMA reads.
-    pdl_wait();
-    const int groups = a.K / 16;
-    {
-      const int r = threadIdx.x >> 3, j = threadIdx.x & 7;  // 8 threads per row
-      float ss = 0.f;
-      if (r < R)
-        for (int gidx = j; gidx < groups; gidx += 8) ss += __ldcg(a.ssq + static_cast<long long>(r) * groups + gidx);
-      ss += __shfl_xor_sync(0xffffffffu, ss, 1);
-      ss += __shfl_xor_sync(0xffffffffu, ss, 2);
-      ss += __shfl_xor_sync(0xffffffffu, ss, 4);
-      if (j == 0 && r < kN) inv_s[r] = r < R ? 1.0f / sqrtf(ss / static_cast<float>(a.K) + a.eps) : 0.f;
-    }
-    __syncthreads();
-    const int nchunk = kt_n * R * 8;  // (k-tile, row, 16-byte chunk); rows >= R feed ignored columns
-    for (int c0 = 0; c0 < nchunk; c0 += 128 * 8) {
-      float4 xa[8], xb[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int ch = c0 + u * 128 + threadIdx.x;
-        if (ch >= nchunk) continue;
-        const int t = ch / (R * 8), r = (ch >> 3) % R, cc = ch & 7;
-        const float4* xp = reinterpret_cast<const float4*>(a.X + static_cast<long long>(r) * a.K + (kt0 + t) * kBK + cc * 8);
-        xa[u] = __ldg(xp);
-        xb[u] = __ldg(xp + 1);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int ch = c0 + u * 128 + threadIdx.x;
-        if (ch >= nchunk) continue;
-        const int t = ch / (R * 8), r = (ch >> 3) % R, cc = ch & 7;
-        const int col = (kt0 + t) * kBK + cc * 8;
-        const float4 g0 = __ldg(reinterpret_cast<const float4*>(a.g + col));
-        const float4 g1 = __ldg(reinterpret_cast<const float4*>(a.g + col + 4));
-        const float iv = inv_s[r];
-        __align__(16) bf16 o8[8];
-        o8[0] = __float2bfloat16_rn(xa[u].x * iv * g0.x);
-        o8[1] = __float2bfloat16_rn(xa[u].y * iv * g0.y);
-        o8[2] = __float2bfloat16_rn(xa[u].z * iv * g0.z);
-        o8[3] = __float2bfloat16_rn(xa[u].w * iv * g0.w);
-        o8[4] = __float2bfloat16_rn(xb[u].x * iv * g1.x);
-        o8[5] = __float2bfloat16_rn(xb[u].y * iv * g1.y);
-        o8[6] = __float2bfloat16_rn(xb[u].z * iv * g1.z);
-        o8[7] = __float2bfloat16_rn(xb[u].w * iv * g1.w);
-        *reinterpret_cast<uint4*>(sx + t * kTileX + r * 128 + ((cc ^ (r & 7)) * 16)) = *reinterpret_cast<const uint4*>(o8);
-      }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-  }
-
   if (warp == 0 && lane == 0) {
-    // TMA producer (the rest of the weight stream; activations by TMA unless nx)
+    // TMA producer (the rest of the weight stream; activations after the PDL wait)
     int kt = kt_issued;
-    if (!nx) {
-      pdl_wait();
-      for (int j = 0; j < kt; ++j) tma_load_2d(sx + j * kTileX, &map_x, &full[j], (kt0 + j) * kBK, 0);
-    }
+    pdl_wait();
+    for (int j = 0; j < kt; ++j) tma_load_2d(sx + j * kTileX, &map_x, &full[j], (kt0 + j) * kBK, 0);
     for (; kt < kt_n; ++kt) {
       const int s = kt % stages;
       mbar_wait(&empty[s], ((kt / stages) - 1) & 1);
       mbar_expect_tx(&full[s], wtx);
       load_w(s, kt);
-      if (!nx) tma_load_2d(sx + s * kTileX, &map_x, &full[s], (kt0 + kt) * kBK, 0);
+      tma_load_2d(sx + s * kTileX, &map_x, &full[s], (kt0 + kt) * kBK, 0);
     }
+    // this CTA's weight stream is issued: its share of the next kernel's weights into L2
+    l2_prefetch_share(a.pf_base, a.pf_bytes, blockIdx.x + gridDim.x * blockIdx.y, gridDim.x * gridDim.y);
   } else if (warp == 1 && lane == 0) {
     for (int kt = 0; kt < kt_n; ++kt) {
       const int s = kt % stages;
@@ -369,7 +348,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
       if (kt == 0) gv_stamp(2);
       if (kt == 0) chain_mark(cst, 4);
       tc_fence_after();
-      const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + (nx ? kt : s) * kTileX);
+      const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + s * kTileX);
 #pragma unroll
       for (int k = 0; k < kBK / 16; ++k) umma_bf16(tmem, umma_desc(w0 + k * 32), umma_desc(x0 + k * 32), kIdesc, (kt | k) ? 1u : 0u);
       umma_commit(&empty[s]);
@@ -379,18 +358,60 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   __syncwarp();
   pdl_wait();  // every epilogue thread reads the previous kernel's outputs (rows, residual)
   if (threadIdx.x == 64) chain_mark(cst, 1);
+  // this thread's epilogue row: its TMEM lane, or with split-K its reduced row
+  const int row = warp * 32 + lane;
+  const int per = kM / S;
+  const int n_epi = S == 1 ? m0 + row : (row < per ? m0 + split * per + row : a.N);
+  EpiPre pre;
+  if (a.epi != kEpiLmStats) epi_preload(a, n_epi, R, pre);
+  if (scaled && warp >= 2) {
+    // warps 2-3 (idle while the weights stream): each live row's inverse RMS,
+    // from the producers' sums of squares (one float4 per thread per row, in a
+    // fixed order) or from the prep kernel's values
+    const int t = threadIdx.x - 64;
+    if (a.ssq) {
+      const int g4 = a.K / 64;  // float4 groups of 16-column partials per row (K <= 4096: <= 64)
+      float4 b[kN];
+#pragma unroll
+      for (int r = 0; r < kN; ++r)
+        b[r] = (r < R && t < g4) ? __ldcg(reinterpret_cast<const float4*>(a.ssq + static_cast<long long>(r) * (a.K / 16)) + t)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < kN; ++r) {
+        if (r >= R) break;
+        float v = (b[r].x + b[r].y) + (b[r].z + b[r].w);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) inv_red[warp - 2][r] = v;
+      }
+      asm volatile("bar.sync 2, 64;" ::: "memory");
+      if (t < kN) inv_s[t] = t < R ? 1.0f / sqrtf((inv_red[0][t] + inv_red[1][t]) / static_cast<float>(a.K) + a.eps) : 0.f;
+    } else if (t < kN) {
+      inv_s[t] = t < R ? __ldcg(a.inv + t) : 0.f;
+    }
+    asm volatile("bar.sync 2, 64;" ::: "memory");
+    if (t == 0) mbar_arrive(inv_bar);
+  }
   mbar_wait(done, 0);
   tc_fence_after();
   if (threadIdx.x == 0) gv_stamp(3);
   if (threadIdx.x == 64) chain_mark(cst, 3);
 
-  const int row = warp * 32 + lane, n = m0 + row;
+  const int n = m0 + row;
   float v[16];
   tmem_ld16(tmem + (static_cast<std::uint32_t>(warp * 32) << 16), v);
+  if (scaled) mbar_wait(inv_bar, 0);
+  auto scale_rows = [&](float (&u)[16]) {
+    if (!scaled) return;
+#pragma unroll
+    for (int r = 0; r < kN; ++r) u[r] *= inv_s[r];
+  };
   if (a.epi == kEpiLmStats) {
+    scale_rows(v);
     lm_stats_epilogue(a, n, R, v, tile, gridDim.x);  // S == 1 for the LM head
   } else if (S == 1) {
-    epilogue(a, n, R, v);
+    scale_rows(v);
+    epilogue(a, n, R, v, pre);
   } else {
     // Split-K inside a thread-block cluster (the S CTAs of this weight tile):
     // CTA q reduces weight rows [q*128/S, (q+1)*128/S).  Every CTA pushes the
@@ -399,7 +420,6 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     // waits only for its own data -- no cluster-wide barrier, no remote loads
     // -- then sums the S partials in rank order (deterministic) and runs the
     // epilogue of its rows.
-    const int per = kM / S;
     const int q = row / per, rq = row % per;
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every landing barrier is initialised
     {
@@ -434,7 +454,8 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
         }
       if (threadIdx.x == 0) gv_stamp(6);
       if (threadIdx.x == 0) chain_mark(cst, 6);
-      epilogue(a, mine ? m0 + wr : a.N, R, v);
+      scale_rows(v);
+      epilogue(a, mine ? m0 + wr : a.N, R, v, pre);
     }
   }
   tc_fence_before();
@@ -594,7 +615,8 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
     pdl_wait();
     if (threadIdx.x == 64) chain_mark(cst, 1);
     if (fold) {
-      // stage bf16(rmsnorm(x[sel[r]]) * g) for every k-tile (128B-swizzled K-major)
+      // stage bf16(x[sel[r]]) for every k-tile (128B-swizzled K-major); the
+      // rows' inverse RMS scale the logits (RMSNorm on the fp32 product)
       const int et0 = threadIdx.x - 64;
       {
         const int r = et0 >> 3, j = et0 & 7;  // 8 threads per row
@@ -621,25 +643,26 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
         const int col = t * kBK + cc * 8;
         const float* xr = a.X + static_cast<long long>(__ldg(a.sel + r)) * a.K + col;
         const float4 x0 = __ldg(reinterpret_cast<const float4*>(xr)), x1 = __ldg(reinterpret_cast<const float4*>(xr + 4));
-        const float4 one = make_float4(1.f, 1.f, 1.f, 1.f);  // a.g == nullptr: unit gains
-        const float4 g0 = a.g ? __ldg(reinterpret_cast<const float4*>(a.g + col)) : one;
-        const float4 g1 = a.g ? __ldg(reinterpret_cast<const float4*>(a.g + col + 4)) : one;
-        const float iv = inv_s[r];
         __align__(16) bf16 o8[8];
-        o8[0] = __float2bfloat16_rn(x0.x * iv * g0.x);
-        o8[1] = __float2bfloat16_rn(x0.y * iv * g0.y);
-        o8[2] = __float2bfloat16_rn(x0.z * iv * g0.z);
-        o8[3] = __float2bfloat16_rn(x0.w * iv * g0.w);
-        o8[4] = __float2bfloat16_rn(x1.x * iv * g1.x);
-        o8[5] = __float2bfloat16_rn(x1.y * iv * g1.y);
-        o8[6] = __float2bfloat16_rn(x1.z * iv * g1.z);
-        o8[7] = __float2bfloat16_rn(x1.w * iv * g1.w);
+        o8[0] = __float2bfloat16_rn(x0.x);
+        o8[1] = __float2bfloat16_rn(x0.y);
+        o8[2] = __float2bfloat16_rn(x0.z);
+        o8[3] = __float2bfloat16_rn(x0.w);
+        o8[4] = __float2bfloat16_rn(x1.x);
+        o8[5] = __float2bfloat16_rn(x1.y);
+        o8[6] = __float2bfloat16_rn(x1.z);
+        o8[7] = __float2bfloat16_rn(x1.w);
         *reinterpret_cast<uint4*>(sx + t * kTileX + r * 128 + ((cc ^ (r & 7)) * 16)) = *reinterpret_cast<const uint4*>(o8);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (et0 == 0) mbar_arrive(xrdy);
       if (et0 == 0) chain_mark(cst, 3);
+    } else {
+      // operand rows prepared by the prep kernel (bf16(x) by TMA), their inverse RMS in a.inv
+      const int et0 = threadIdx.x - 64;
+      if (et0 < kN) inv_s[et0] = et0 < R ? (a.inv ? __ldcg(a.inv + et0) : 1.f) : 0.f;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
     }
     const int quarter = warp & 3;
     const int et = threadIdx.x - 64;  // 0..127
@@ -659,6 +682,9 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
         for (int u = 0; u < 4; ++u)
           v[u] = t + u < t1 ? tmem_ld1(tq + static_cast<std::uint32_t>((t + u - t0) * kN + r)) : 0.f;
         tmem_ld_wait();
+        const float iv = inv_s[r];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] *= iv;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int n = (t + u) * kM + quarter * 32 + lane;
@@ -789,9 +815,8 @@ long long gemv_tc_ws_floats(int N, int K) {
 }
 
 bool gemv_tc_norm_supported(const GemvArgs& a) {
-  const int S = gemv_tc_splits(a.N, a.K, a.epi);
-  const int KT = a.K / kBK;
-  return gemv_tc_supported(a) && (KT + S - 1) / S <= kNxMaxKt && a.K % 16 == 0 && a.ssq != nullptr;
+  // inverse RMS from 16-column partials: one float4 of them per thread of two warps
+  return gemv_tc_supported(a) && a.K % 64 == 0 && a.K <= 64 * 64;
 }
 
 bool gemv_tc_supported(const GemvArgs& a) {
@@ -801,7 +826,7 @@ bool gemv_tc_supported(const GemvArgs& a) {
 void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float* ws, int* cnt, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem > kNxSmem ? kSmem : kNxSmem);
+    cudaFuncSetAttribute(gemv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     uniform_carveout(reinterpret_cast<const void*>(gemv_tc_kernel));
     attr = true;
   }
@@ -809,7 +834,7 @@ void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float*
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((a.N + kM - 1) / kM, S);
   cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = a.X ? kNxSmem : kSmem;
+  cfg.dynamicSmemBytes = kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
   int na = 0;

@@ -59,9 +59,10 @@ void noop_chain_link(int* p, int ctas, cudaStream_t st);
 // captured CUDA graph per (rows, context) bucket serves every tick:
 // meta[0] = live rows R, meta[1] = logits rows Rl, meta[2] = max position.
 // Grids are sized for the bucket caps; CTAs past the live counts exit.
-// ssq (optional): per-16-column sums of squares of the rows [R][d/16]
+// ssq / xb (optional): per-16-column sums of squares of the rows [R][d/16]
+// and their bf16 copy [R][d] (the first normed GEMV's operand)
 void embed(const RowDesc* rows, int R_cap, const int* meta, const int* out_tok, const bf16* emb, int d, float* x,
-           cudaStream_t st, float* ssq = nullptr);
+           cudaStream_t st, float* ssq = nullptr, bf16* xb = nullptr);
 
 // Fused skinny GEMM  y[r][n] = sum_k A[r][k] W[n][k]  for decode/incremental
 // rows.  A is either bf16 activations or, with `norm`, the fp32 residual rows
@@ -71,8 +72,10 @@ enum Epi : int { kEpiF32 = 0, kEpiResidual = 1, kEpiSwiGlu = 2, kEpiQkv = 3, kEp
 struct LmStat;
 struct GemvArgs {
   const bf16* A = nullptr;   // [R][K] bf16 (when X == nullptr)
-  const float* X = nullptr;  // [R][K] fp32 residual rows (norm prologue)
-  const float* g = nullptr;  // norm gains [K]
+  // Normed linear maps (RMSNorm with unit gains, applied to the fp32 product:
+  // y = (bf16(x) W^T) * inv_rms(x), oracle/model.py normed_linear):
+  const float* X = nullptr;  // [R][K] fp32 residual rows: operand bf16(x), inverse RMS computed in-kernel
+  const float* inv = nullptr;  // or: A = bf16(x) rows and their inverse RMS [R] (prep kernel)
   float eps = 1e-5f;
   int R = 0, N = 0, K = 0;    // R: row cap (grid); live rows = meta ? meta[0] : R
   const int* meta = nullptr;
@@ -95,10 +98,12 @@ struct GemvArgs {
   float* out_lp = nullptr;
   float* out_ent = nullptr;
   float* logits = nullptr;  // optional fp32 [rows][N]
-  // norm-from-x (gemv_tc): per-16-column sums of squares of the X rows [R][K/16]
+  // or (gemv_tc): A = bf16(x) rows and their per-16-column sums of squares [R][K/16]
   const float* ssq = nullptr;
   // kEpiResidual: also write the new rows' per-16-column sums of squares [R][N/16]
+  // and their bf16 copy [R][N] (the next normed GEMV's operand)
   float* ssq_out = nullptr;
+  bf16* xb_out = nullptr;
   // lm_head_tc with X (norm folded in): the residual rows to normalise, selected by sel[i]
   const int* sel = nullptr;
   // kEpiResidual (SIMT gemv): the residual rows were last written at least two
@@ -108,6 +113,11 @@ struct GemvArgs {
   // (each weight byte is read once per forward; the activations, KV and
   // partials the chain re-reads keep the L2)
   bool evict_first = false;
+  // gemv_tc: once this CTA has issued its last weight load, prefetch its share
+  // of [pf_base, pf_base + pf_bytes) into L2 (the next kernel's weights), so
+  // HBM keeps streaming through this kernel's tail and the next one's start
+  const void* pf_base = nullptr;
+  long long pf_bytes = 0;
 };
 void gemv(const GemvArgs& a, cudaStream_t st);  // dispatches to gemv_stream for large matrices
 // HBM-streaming variant (gemv_stream.cu): persistent CTAs, cp.async.bulk ring.
@@ -121,12 +131,13 @@ struct alignas(64) TmaMap {
 };
 bool make_tmap_bf16(TmaMap* out, const bf16* base, long long rows, long long cols, int box_rows);
 bool gemm_tc_supported(int N, int K);
-// Same epilogues as gemv; A comes from map_a (bf16 rows, already normalised
-// where the GEMV path would normalise on the fly).
+// Same epilogues as gemv; A comes from map_a (bf16 rows; for a normed map
+// A = bf16(x) and a.inv holds the rows' inverse RMS, applied to the products).
 void gemm_tc(const TmaMap& map_a, const TmaMap& map_w, const GemvArgs& a, cudaStream_t st);
-// h[i] = bf16(rmsnorm(x[sel ? sel[i] : i]) * g) for i < meta[meta_idx] (same
-// rounding as the gemv prologue); one CTA per row, 16-byte vectors.
-void rmsnorm_rows(const float* x, int R_cap, const int* meta, int K, const float* g, float eps, bf16* h,
+// Operand prep of a normed linear map: h[i] = bf16(x[r]) and inv[i] =
+// 1 / sqrt(mean(x[r]^2) + eps), r = sel ? sel[i] : i, for i < meta[meta_idx];
+// one CTA per row, 16-byte vectors.
+void rmsnorm_rows(const float* x, int R_cap, const int* meta, int K, float* inv, float eps, bf16* h,
                   cudaStream_t st, const int* sel = nullptr, int meta_idx = 0);
 constexpr int kTcMinRows = 17;  // ticks with more rows than the swap-AB GEMV holds use the tcgen05 GEMM (M = 128 tiles)
 
@@ -191,9 +202,12 @@ void attention_decode_tma(const TmaMap& kmap, const TmaMap& vmap, const bf16* q,
 // split's boxes through a TMA ring.  Same maps and pool contract as above.
 int attention_decode_cluster_splits(int rcap, int nkv, int nbox_cap);
 bool attention_decode_cluster_supported(int nh, int nkv, int hd);
+// pf_base / pf_bytes: prefetched into L2 by the grid's CTAs at their start
+// (the o-projection's weights: attention leaves HBM mostly idle).
 void attention_decode_cluster(const TmaMap& kmap, const TmaMap& vmap, const bf16* q, const RowDesc* rows, int R_cap,
                               int ns, const int* meta, int nh, int nkv, int hd, long long kv_stride,
-                              long long layer_off, int max_ctx, bf16* o, cudaStream_t st, bool skip_runs = false);
+                              long long layer_off, int max_ctx, bf16* o, cudaStream_t st, bool skip_runs = false,
+                              const void* pf_base = nullptr, long long pf_bytes = 0);
 
 // Prefill ticks (rows of long same-agent runs): CTA = 64 consecutive rows x q
 // head, keys streamed through smem once per same-agent segment; rows alone in
