@@ -41,8 +41,9 @@ def run_config(cfg: dict) -> RunConfig:
 def models_of(cfg: dict, max_ctx: int = 4096) -> dict:
     out = {}
     for tag, m in cfg["models"].items():
-        key = (tag, m["shape"], m.get("seed", 0), max_ctx)
+        over = {k: v for k, v in m.items() if k not in ("shape", "seed")}  # e.g. n_layers: the shape's first layers
+        key = (tag, m["shape"], m.get("seed", 0), max_ctx, tuple(sorted(over.items())))
         if key not in _MODEL_CACHE:
-            _MODEL_CACHE[key] = CpuModel(make_spec(tag, m["shape"], seed=m.get("seed", 0)), max_ctx)
+            _MODEL_CACHE[key] = CpuModel(make_spec(tag, m["shape"], seed=m.get("seed", 0), **over), max_ctx)
         out[tag] = _MODEL_CACHE[key]
     return out

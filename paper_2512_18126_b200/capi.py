@@ -593,7 +593,9 @@ def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16
         counts[cfg["embed_model"]] += 1
     tags = list(cfg["models"])
     specs = [model_spec(tag, cfg["models"][tag]["shape"], cfg["models"][tag].get("seed", 0),
-                        max_agents=max(1, counts[tag] * concurrency)) for tag in tags]
+                        max_agents=max(1, counts[tag] * concurrency),
+                        **{k: v for k, v in cfg["models"][tag].items() if k not in ("shape", "seed")})
+             for tag in tags]
     out_max = max(x if isinstance(x, int) else x[1] for x in cfg["out_len"])
     if max_ctx is None:
         prompt_max = max(cfg["query_tokens"] + cfg["leaf_prefix_tokens"],

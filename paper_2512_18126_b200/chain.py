@@ -36,6 +36,8 @@ def _name(tag):
         return "attention"
     if tag >> 16 == 7:
         return "rmsnorm"
+    if tag == 0x80001:
+        return "attn_prefill_tc"
     return hex(tag)
 
 

@@ -69,7 +69,14 @@ C1H = dict(copy.deepcopy(C1U), name="C1H", provider="hidden", embed_model="embed
            models=dict(leaf=dict(shape="tiny", seed=1), agg=dict(shape="tiny", seed=2), embed=dict(shape="tiny", seed=7)),
            workload="C1U with the hidden-state embedding provider (tiny embedding model, h = 256)")
 
-CONFIGS = {c["name"]: c for c in (C0, C1, C1U, C1H, C2, C3, C4_TREE, C4_DENSE)}
+# ... at a 1B-class embedding width (the first 2 layers of the `1b` shape,
+# h = d_model = 2048 > completion length: the n x n cross-Gram FCS route)
+C1H1B = dict(copy.deepcopy(C1H), name="C1H1B",
+             models=dict(leaf=dict(shape="tiny", seed=1), agg=dict(shape="tiny", seed=2),
+                         embed=dict(shape="1b", seed=7, n_layers=2)),
+             workload="C1U with the hidden-state provider at 1B width (h = 2048, n x n FCS route)")
+
+CONFIGS = {c["name"]: c for c in (C0, C1, C1U, C1H, C1H1B, C2, C3, C4_TREE, C4_DENSE)}
 
 
 def agent_tag(cfg: dict, layer: int, position: int) -> str:

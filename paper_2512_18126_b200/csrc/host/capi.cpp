@@ -996,10 +996,24 @@ int moa_k_attention(uintptr_t q, uintptr_t rows, int R, uintptr_t meta, int nh, 
     auto* op = reinterpret_cast<moa::k::bf16*>(out);
     const bool tma = (prefill & 2) != 0;  // bit 1: the TMA-staged per-row kernel
     const bool cluster = (prefill & 4) != 0;  // bit 2: the cluster-split kernel, splits = bits 8-15 (0: heuristic)
+    const bool pf_tc = (prefill & 8) != 0;    // bit 3 (with bit 0): the runs by the tcgen05 prefill kernel
+    const bool runs_only = (prefill & 16) != 0;  // bit 4 (with bit 0): no per-row kernel (timing the runs)
     const int ns_req = (prefill >> 8) & 0xff;
     prefill &= 1;
-    if (prefill) moa::k::attention_prefill(qp, rp, R, mp, nh, nkv, hd, kp, vp, kv_stride, 0, max_ctx, op, st);
-    if (cluster) {
+    if (prefill && pf_tc) {
+      if (!moa::k::attention_prefill_tc_supported(nh, nkv, hd)) throw moa::ValidationError("attention: tcgen05 prefill shape");
+      const long long pool_rows = static_cast<long long>(slots) * kv_stride / hd;
+      moa::k::TmaMap qm, km, vm;
+      if (!moa::k::make_tmap_q3d(&qm, qp, R, nh, hd, nh / nkv) || !moa::k::make_tmap_bf16(&km, kp, pool_rows, hd, 64) ||
+          !moa::k::make_tmap_bf16(&vm, vp, pool_rows, hd, 64))
+        throw moa::DeviceError("attention: TMA map creation failed");
+      moa::k::attention_prefill_tc(qm, km, vm, rp, R, mp, nh, nkv, hd, kv_stride, 0, max_ctx, op, st);
+    } else if (prefill) {
+      moa::k::attention_prefill(qp, rp, R, mp, nh, nkv, hd, kp, vp, kv_stride, 0, max_ctx, op, st);
+    }
+    if (prefill && runs_only) {
+      MOA_CUDA(cudaStreamSynchronize(st));
+    } else if (cluster) {
       const long long pool_rows = static_cast<long long>(slots) * kv_stride / hd;
       moa::k::TmaMap km, vm;
       if (!moa::k::make_tmap_bf16(&km, kp, pool_rows, hd, 64) || !moa::k::make_tmap_bf16(&vm, vp, pool_rows, hd, 64))
@@ -1091,6 +1105,7 @@ int moa_k_chain_stamp(uintptr_t buf) {
     moa::k::gemv_tc_chain_stamp(reinterpret_cast<unsigned long long*>(buf));
     moa::k::gemm_tc_chain_stamp(reinterpret_cast<unsigned long long*>(buf));
     moa::k::attn_decode_chain_stamp(reinterpret_cast<unsigned long long*>(buf));
+    moa::k::attn_prefill_tc_chain_stamp(reinterpret_cast<unsigned long long*>(buf));
   });
 }
 

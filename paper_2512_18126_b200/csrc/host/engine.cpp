@@ -149,6 +149,8 @@ void GpuEngine::add_agent(const AgentId& id, int model, int owner) {
   order_.push_back(id);
 }
 
+void GpuEngine::set_chunk_dests(const AgentId& id, std::uint64_t ranks) { req(id).dests = ranks; }
+
 // Literal token ids index the model's embedding table on the device: reject
 // anything outside [0, vocab) (negative ids are the engine's own symbolic
 // references to decoded tokens, created only by the host orchestrator).
@@ -477,11 +479,16 @@ void GpuEngine::step() {
   // launch (no host decision can change them: callbacks fire only on chunk /
   // completion events, which the run ends on).
   int K = 1;
-  if (in_run_ && max_run_ > 1 && world() == 1 && !tracing_ && !probing_ && !opt_.keep_logits && !plan.empty()) {
+  // With several ranks every rank computes the same K from the replicated
+  // plan (remote agents' rows included: they bound the run by their chunk
+  // events too), so runs end on the ticks whose hand-offs all ranks issue;
+  // a rank whose own rows cannot run (workspace) falls back to single ticks,
+  // which changes no tick number or event.
+  if (in_run_ && max_run_ > 1 && !tracing_ && !probing_ && !opt_.keep_logits && !plan.empty()) {
     K = max_run_;
     for (const Plan& p : plan) {
       const Req& r = *p.r;
-      if (p.kind != Decode || !r.local) {
+      if (p.kind != Decode) {
         K = 1;
         break;
       }
@@ -598,10 +605,11 @@ void GpuEngine::step() {
       for (int p = 0; p < world(); ++p) {
         if (p == rank()) continue;
         if (r.local) {
+          if (!((r.dests >> p) & 1)) continue;  // this rank needs no copy of the chunk
           comm_->send_i32(out_tok_ + off, cnt, p, stream_);
           comm_->send_f32(out_lp_ + off, cnt, p, stream_);
           comm_->send_f32(out_ent_ + off, cnt, p, stream_);
-        } else if (p == r.owner) {
+        } else if (p == r.owner && ((r.dests >> rank()) & 1)) {
           comm_->recv_i32(out_tok_ + off, cnt, p, stream_);
           comm_->recv_f32(out_lp_ + off, cnt, p, stream_);
           comm_->recv_f32(out_ent_ + off, cnt, p, stream_);

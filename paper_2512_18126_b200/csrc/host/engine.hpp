@@ -76,6 +76,10 @@ class GpuEngine {
   // Tree-partitioned serving: chunks of an agent's output are sent by its
   // owner to every other rank (NCCL P2P) into the same output-cache slots.
   void attach_comm(std::unique_ptr<PeerComm> comm);
+  // Ranks (bit mask) that receive the agent's chunks; default every rank.  The
+  // caller narrows it to the ranks that consume them (identically on every
+  // rank: sender and receivers must agree).
+  void set_chunk_dests(const AgentId& id, std::uint64_t ranks);
   int rank() const { return comm_ ? comm_->rank() : 0; }
   int world() const { return comm_ ? comm_->world() : 1; }
   bool is_local(const AgentId& id) const { return req(id).local; }
@@ -158,6 +162,7 @@ class GpuEngine {
     AgentId id;
     int model = 0, slot = 0, kv = 0, owner = 0;
     bool local = true;
+    std::uint64_t dests = ~0ULL;  // ranks receiving this agent's chunks
     TokenSeq prompt;
     int prefilled = 0, max_computed = 0;
     std::uint64_t gen = 0;

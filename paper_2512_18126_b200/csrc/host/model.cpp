@@ -195,6 +195,10 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   // decode ticks: L2 prefetch of the next kernel's weights (bit 0: attention
   // -> Wo, bit 1: down -> next layer's Wqkv); MOA_L2_PREFETCH=<mask>
   if (const char* e = std::getenv("MOA_L2_PREFETCH")) l2pf_ = std::atoi(e);
+  // prompt-prefill ticks: the tcgen05 attention (MOA_PREFILL_TC=0: the mma.sync kernel)
+  pf_tc_ = kv_maps_ok_ && k::attention_prefill_tc_supported(s.n_heads, s.n_kv_heads, static_cast<int>(hd)) &&
+           k::make_tmap_q3d(&qmap3_, q_, max_rows, s.n_heads, static_cast<int>(hd), s.n_heads / s.n_kv_heads);
+  if (const char* e = std::getenv("MOA_PREFILL_TC")) pf_tc_ = pf_tc_ && e[0] != '0';
   // default: the cluster-split kernel (MOA_DECODE_CLUSTER=0: the fixed-split TMA kernel)
   attn_cluster_ = kv_maps_ok_ && k::attention_decode_cluster_supported(s.n_heads, s.n_kv_heads, static_cast<int>(hd));
   if (const char* e = std::getenv("MOA_DECODE_CLUSTER")) attn_cluster_ = attn_cluster_ && e[0] != '0';
@@ -457,7 +461,12 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       const double run_rows = Rv - static_cast<double>(live_.singles);
       probe_begin(KernelProbes::AttnPrefill, 4.0 * live_.run_keys * nkv * hd + 4.0 * run_rows * nh * hd,
                   4.0 * static_cast<double>(live_.run_pairs) * nh * hd);
-      k::attention_prefill(q_, buf_.rows, rcap, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_, st);
+      if (pf_tc_)
+        k::attention_prefill_tc(qmap3_, kmap_, vmap_, buf_.rows, rcap, meta, nh, nkv, hd, kv_stride_, loff, max_ctx_,
+                                h_, st);
+      else
+        k::attention_prefill(q_, buf_.rows, rcap, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_,
+                             st);
       probe_end();
     }
     if (!prefill || singles) {

@@ -159,6 +159,8 @@ class DeviceModel {
   k::TmaMap kmap_, vmap_;  // K / V pools as [rows][hd], 64-row boxes (fused QKV + attention, hd 64)
   k::bf16* wo_blk_ = nullptr;  // [L][nkv][D][hpg*hd]: Wo regrouped for the fused o-projection
   bool kv_maps_ok_ = false;
+  k::TmaMap qmap3_;     // q [rows][nh][hd] as a 3-D map (GQA-group boxes) for the tcgen05 prefill attention
+  bool pf_tc_ = false;  // prompt-prefill attention on tcgen05 (attn_prefill_tc.cu)
   bool attn_tma_ = false;  // decode rows: TMA-staged attention (attn_decode.cu)
   bool attn_cluster_ = false;  // decode rows: cluster-split TMA-ring attention (attn_decode.cu, default)
   int split_keys_ = 512;   // keys per attention CTA (sizes the graphs' split buckets)

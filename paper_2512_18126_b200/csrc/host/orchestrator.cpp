@@ -190,6 +190,19 @@ struct Request {
         }
       }
 
+    // Tree-partitioned serving without an early-exit gate: an agent's chunks
+    // go only to the ranks of its consumers (their slot plans prefill them)
+    // and to rank 0 (which resolves the request's outputs).  With the gate
+    // every rank evaluates it on every completion, so chunks go everywhere.
+    if (eng.world() > 1 && !(cfg.early_exit && topo.depth() > 1)) {
+      std::map<AgentId, std::uint64_t> dests;
+      for (const auto& layer : topo.layers())
+        for (const AgentId& a : layer) dests[a] |= 1ULL;
+      for (const auto& layer : topo.layers())
+        for (const AgentId& c : layer)
+          for (const AgentId& p : topo.precursors(c)) dests[p] |= 1ULL << owner.at(c);
+      for (const auto& [a, m] : dests) eng.set_chunk_dests(id(a), m);
+    }
     // exit groups (orchestrator.cpp:193-220)
     if (!(cfg.early_exit && topo.depth() > 1)) return;
     std::vector<std::vector<AgentId>> sets;

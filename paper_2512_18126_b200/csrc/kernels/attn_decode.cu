@@ -15,6 +15,7 @@
 // Algorithmic bytes per (row, kv head): (pos + 1) * hd * 2 (K) * 2 (V).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <set>
 
 #include "kernels.cuh"
@@ -323,45 +324,33 @@ attention_decode_tma_kernel(const __grid_constant__ CUtensorMap kmap, const __gr
 // of mma.sync m16n8k16 tiles) with an online softmax across boxes, so loads
 // overlap compute and a CTA holds only STG boxes.  Partials are combined
 // without global memory: each CTA folds its warps (fixed order) into
-// (max, sum, o) in shared memory, and after one cluster barrier CTA s reads
-// every rank's partial over DSMEM for its slice of the outputs and combines
-// them in rank order (deterministic for given shapes).  NS = 8 for every row
+// (max, sum, o) and pushes each slice of o, with every head's (max, sum), into
+// the owning rank's landing buffer with st.async (DSMEM stores completing on
+// the owner's mbarrier); CTA s waits only for its own slice and combines the
+// ranks in rank order (deterministic for given shapes).  NS = 8 for every row
 // (a row's splits depend only on its context length: batch invariant); two
 // ring stages per CTA suffice with 8 kv heads x 8 splits per row in flight
 // and leave room on the SM for the next GEMV's CTAs (PDL prologue).
-template <int HD>
+template <int HD, int STG_ = (HD == 128 ? 2 : 3)>
 struct DecCl {
-  static constexpr int STG = HD == 128 ? 2 : 3;    // ring stages (64-key boxes of K and V)
+  static constexpr int STG = STG_;                 // ring stages (64-key boxes of K and V)
   static constexpr int SUB = HD / 64;              // 128-byte column subtiles per key row
   static constexpr int BOX = 64 * HD * 2;          // bytes of one K (or V) box
   static constexpr int STAGE = 2 * BOX;
   static constexpr int QB = 16 * HD * 2;
   static constexpr int WO = 4 * 16 * HD * 4;       // warp partials (reuse the ring)
-  static constexpr int PART = 16 * (HD + 2) * 4;   // CTA partial: [16][HD] o, then m[16], l[16]
-  static_assert(WO + PART <= STG * STAGE, "partials fit in the ring");
+  static_assert(WO <= STG * STAGE, "warp partials fit in the ring");
   static constexpr int SMEM = 1024 + STG * STAGE + QB + 2 * STG * 8;
 };
 
-__device__ __forceinline__ void cluster_arrive_wait() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ float dsmem_ldf(const float* local, int rank) {
-  std::uint32_t a;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(local)), "r"(rank));
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
-  return v;
-}
-
-template <int HD>
+template <int HD, int STG_>
 __global__ void __launch_bounds__(160)
 attention_decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                                 const bf16* __restrict__ q, const RowDesc* __restrict__ rows,
                                 const int* __restrict__ meta, int nh, int nkv, long long kv_stride,
                                 long long layer_off, int max_ctx, bf16* __restrict__ o, int skip_runs,
                                 const void* pf_base, long long pf_bytes) {
-  using C = DecCl<HD>;
+  using C = DecCl<HD, STG_>;
   constexpr int KSTEPS = HD / 16, NT = HD / 8, RB = HD * 2, STG = C::STG;
   extern __shared__ unsigned char dc_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(dc_raw) + 1023) &
@@ -371,10 +360,12 @@ attention_decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap, const 
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(Qs + C::QB);
   std::uint64_t* empty = full + STG;
   float* wo = reinterpret_cast<float*>(ring);  // after the box loop: [4 warps][16][HD]
-  float* po = reinterpret_cast<float*>(ring + C::WO);  // CTA partial o [16][HD], m [16], l [16]
-  float* pm = po + 16 * HD;
-  float* pl = pm + 16;
   __shared__ float wm[4][16], wl[4][16];
+  // partials pushed here by every rank of the cluster (st.async): this CTA's
+  // slice of the outputs [NS][chunk] and every rank's (max, sum) per q head
+  __shared__ __align__(16) float land_o[8 * 256];
+  __shared__ __align__(16) float land_ml[8 * 16 * 2];
+  __shared__ __align__(8) std::uint64_t land_bar;
   __shared__ int first_new_s;
   __shared__ unsigned long long cst[kChainPhases];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -424,10 +415,15 @@ attention_decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap, const 
         mbar_init(&full[i], 1);
         mbar_init(&empty[i], 4);
       }
+      mbar_init(&land_bar, 1);
+      const int chunk = hpg * HD / NS;
+      mbar_expect_tx(&land_bar, static_cast<std::uint32_t>(NS * (chunk * 4 + hpg * 8)));
       mbar_fence_init();
     }
   }
   __syncthreads();
+  // this CTA's landing barrier is armed (peers wait for it before pushing)
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   if (warp == 4) {
     if (lane == 0) {
       prefetch_tmap(&kmap);
@@ -560,6 +556,7 @@ attention_decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap, const 
     l_b += __shfl_xor_sync(kAll, l_b, 2);
   }
   __syncthreads();  // every box consumed: the ring is free for the partials
+  if (threadIdx.x == 0) chain_mark(cst, 4);
   if (warp < 4) {
     if (t4 == 0) {
       wm[warp][g8] = m_a;
@@ -575,48 +572,63 @@ attention_decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap, const 
     }
   }
   __syncthreads();
-  // this CTA's partial over its boxes: warps folded in a fixed order
-  if (threadIdx.x < 16) {
-    const int h = threadIdx.x;
+  // This CTA's partial over its boxes (warps folded in a fixed order), pushed
+  // straight into the owners' landing buffers: rank q owns output elements
+  // [q * chunk, (q + 1) * chunk) of the group's hpg x HD outputs.
+  const int chunk = hpg * HD / NS;
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every landing barrier is armed
+  if (threadIdx.x == 0) chain_mark(cst, 5);
+  for (int t = threadIdx.x; t < hpg * HD / 4; t += blockDim.x) {
+    const int e0 = 4 * t, h = e0 / HD, e = e0 % HD;
+    float M = -1e30f;
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, wm[w][h]);
+    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int w = 0; w < 4; ++w)
+      if (wl[w][h] != 0.f) {
+        const float c = exp2f(wm[w][h] - M);
+        const float4 x = *reinterpret_cast<const float4*>(wo + (w * 16 + h) * HD + e);
+        val.x += c * x.x;
+        val.y += c * x.y;
+        val.z += c * x.z;
+        val.w += c * x.w;
+      }
+    const int q = e0 / chunk, off = e0 % chunk;
+    std::uint32_t dst, bar;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(smem_u32(land_o + s * chunk + off)), "r"(q));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(smem_u32(&land_bar)), "r"(q));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst),
+                 "f"(val.x), "f"(val.y), "f"(val.z), "f"(val.w), "r"(bar)
+                 : "memory");
+  }
+  for (int t = threadIdx.x; t < NS * hpg; t += blockDim.x) {
+    const int q = t / hpg, h = t % hpg;
     float M = -1e30f;
     for (int w = 0; w < 4; ++w) M = fmaxf(M, wm[w][h]);
     float L = 0.f;
     for (int w = 0; w < 4; ++w) L += wl[w][h] == 0.f ? 0.f : exp2f(wm[w][h] - M) * wl[w][h];
-    pm[h] = M;
-    pl[h] = L;
+    std::uint32_t dst, bar;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(smem_u32(land_ml + (s * hpg + h) * 2)), "r"(q));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(smem_u32(&land_bar)), "r"(q));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(dst),
+                 "f"(M), "f"(L), "r"(bar)
+                 : "memory");
   }
-  for (int i = threadIdx.x; i < hpg * HD; i += blockDim.x) {
-    const int h = i / HD, e = i % HD;
+  // rank s combines its slice over all ranks, in rank order
+  mbar_wait(&land_bar, 0);
+  for (int i = threadIdx.x; i < chunk; i += blockDim.x) {
+    const int e = s * chunk + i, h = e / HD;
     float M = -1e30f;
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, wm[w][h]);
-    float val = 0.f;
-    for (int w = 0; w < 4; ++w)
-      if (wl[w][h] != 0.f) val += exp2f(wm[w][h] - M) * wo[(w * 16 + h) * HD + e];
-    po[h * HD + e] = val;
-  }
-  cluster_arrive_wait();  // every rank's partial is visible
-  // rank s combines its slice of the (q head, column) outputs over all ranks, in rank order
-  for (int i = s * blockDim.x + threadIdx.x; i < hpg * HD; i += NS * blockDim.x) {
-    const int h = i / HD, e = i % HD;
-    float mt[8], lt[8], ot[8];
-    float M = -1e30f;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      mt[t] = t < NS ? dsmem_ldf(pm + h, t) : -1e30f;
-      lt[t] = t < NS ? dsmem_ldf(pl + h, t) : 0.f;
-      ot[t] = t < NS ? dsmem_ldf(po + h * HD + e, t) : 0.f;
-      M = fmaxf(M, mt[t]);
-    }
+    for (int t = 0; t < NS; ++t) M = fmaxf(M, land_ml[(t * hpg + h) * 2]);
     float L = 0.f, val = 0.f;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const float w = lt[t] == 0.f ? 0.f : exp2f(mt[t] - M);
-      L += w * lt[t];
-      val += w * ot[t];
+    for (int t = 0; t < NS; ++t) {
+      const float lt = land_ml[(t * hpg + h) * 2 + 1];
+      const float w = lt == 0.f ? 0.f : exp2f(land_ml[(t * hpg + h) * 2] - M);
+      L += w * lt;
+      val += w * land_o[t * chunk + i];
     }
-    o[(static_cast<long long>(r) * nh + g * hpg + h) * HD + e] = __float2bfloat16_rn(val / L);
+    o[(static_cast<long long>(r) * nh + g * hpg) * HD + e] = __float2bfloat16_rn(val / L);
   }
-  cluster_arrive_wait();  // no CTA leaves while a peer may still read its partial
+  __syncthreads();
   if (threadIdx.x == 0) {
     chain_mark(cst, 2);
     chain_flush(cst, (6u << 16) | 1u);
@@ -708,10 +720,16 @@ void attention_decode_cluster(const TmaMap& kmap, const TmaMap& vmap, const bf16
                        *reinterpret_cast<const CUtensorMap*>(&vmap), q, rows, meta, nh, nkv, kv_stride, layer_off,
                        max_ctx, o, skip_runs ? 1 : 0, pf_base, pf_bytes);
   };
-  if (hd == 128)
-    go(attention_decode_cluster_kernel<128>, DecCl<128>::SMEM);
+  static const int stg = [] {  // MOA_ATTN_STAGES=3: a 3-stage ring for hd 128 (A/B)
+    const char* e = std::getenv("MOA_ATTN_STAGES");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (hd == 128 && stg == 3)
+    go(attention_decode_cluster_kernel<128, 3>, DecCl<128, 3>::SMEM);
+  else if (hd == 128)
+    go(attention_decode_cluster_kernel<128, 2>, DecCl<128, 2>::SMEM);
   else
-    go(attention_decode_cluster_kernel<64>, DecCl<64>::SMEM);
+    go(attention_decode_cluster_kernel<64, 3>, DecCl<64, 3>::SMEM);
 }
 
 }  // namespace moa::k

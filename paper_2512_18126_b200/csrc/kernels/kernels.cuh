@@ -48,6 +48,7 @@ void forward_chain_stamp(unsigned long long* buf);
 void gemv_tc_chain_stamp(unsigned long long* buf);
 void gemm_tc_chain_stamp(unsigned long long* buf);
 void attn_decode_chain_stamp(unsigned long long* buf);
+void attn_prefill_tc_chain_stamp(unsigned long long* buf);
 
 void init_uniform_rows(bf16* dst, long long rows, long long cols, std::uint64_t base, float scale, int map,
                        int hd, cudaStream_t st);
@@ -215,6 +216,17 @@ void attention_decode_cluster(const TmaMap& kmap, const TmaMap& vmap, const bf16
 void attention_prefill(const bf16* q, const RowDesc* rows, int R_cap, const int* meta, int nh, int nkv, int hd,
                        const bf16* kpool, const bf16* vpool, long long kv_stride, long long layer_off, int max_ctx,
                        bf16* o, cudaStream_t st);
+
+// Prompt-prefill attention on tcgen05 (attn_prefill_tc.cu): CTA = kv head x
+// 128 / hpg tick rows (M = 128 (row, q head) pairs of the GQA group), S and O
+// accumulated in TMEM, K / V blocks by TMA.  qmap: make_tmap_q3d over q
+// [rows][nh][hd]; kmap / vmap as for attention_decode_tma.  Rows alone in
+// their run are skipped (pair with the per-row kernel, skip_runs = true).
+bool make_tmap_q3d(TmaMap* out, const bf16* q, long long rows, int nh, int hd, int hpg);
+bool attention_prefill_tc_supported(int nh, int nkv, int hd);
+void attention_prefill_tc(const TmaMap& qmap, const TmaMap& kmap, const TmaMap& vmap, const RowDesc* rows, int R_cap,
+                          const int* meta, int nh, int nkv, int hd, long long kv_stride, long long layer_off,
+                          int max_ctx, bf16* o, cudaStream_t st);
 
 // Decode ticks of small agents (every row the only row of its agent):
 // RMSNorm + QKV + RoPE + KV append + attention in one launch, CTA = (row, kv

@@ -211,7 +211,8 @@ def test_attention_kernels_match_torch(torch_cuda, nh, nkv, hd, max_ctx):
             ref[i, h] = torch.softmax(sc, -1) @ V[kv, kh, :pos + 1]
     # mode bit 0: tiled prefill kernel + per-row kernel for the rows alone in their run
     # bit 1: the per-row kernel is the TMA-staged one; bit 2: the cluster-split kernel, bits 8-15 its splits
-    for mode in (1, 0, 3, 2, 5, 4, 4 | (1 << 8), 4 | (2 << 8), 4 | (8 << 8), 5 | (8 << 8)):
+    # bit 3 (with bit 0): the runs by the tcgen05 prefill kernel
+    for mode in (1, 0, 3, 2, 5, 4, 4 | (1 << 8), 4 | (2 << 8), 4 | (8 << 8), 5 | (8 << 8), 13, 9):
         out = torch.zeros(R, nh, hd, dtype=torch.bfloat16, device="cuda")
         capi.check(capi.lib().moa_k_attention(q.data_ptr(), rd.data_ptr(), R, meta.data_ptr(), nh, nkv, hd,
                                               kpool.data_ptr(), vpool.data_ptr(), kv_stride, max_ctx, out.data_ptr(),
@@ -654,14 +655,17 @@ def test_certain_exit_prunes_unfinished_members(scope, groups):
         assert g["agents"][n]["output_tokens"] < 96
 
 
-def test_hidden_state_provider():
+@pytest.mark.parametrize("name", ["C1H", "C1H1B"])
+def test_hidden_state_provider(name):
     """Hidden-state embedding provider: the early-exit
     agreement is computed on the final hidden states of a separate embedding
     model run over each completion on the GPU.  The oracle recomputes every
     evaluation with its CPU model on the GPU's completions: q agrees to 2e-3
     (fp32 hidden states through different accumulation orders), and every
-    exit decision whose margin |q - draw| exceeds that tolerance is identical."""
-    cfg = CONFIGS["C1H"]
+    exit decision whose margin |q - draw| exceeds that tolerance is identical.
+    C1H1B runs the provider at a 1B-class width (h = 2048 > n: the n x n
+    cross-Gram route of the FCS)."""
+    cfg = CONFIGS[name]
     g = _gpu_query(cfg, 3)
     o = _replay(cfg, g, 3)
     evald = [e for e in g["metricq"] if e["evaluated"]]

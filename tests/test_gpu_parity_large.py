@@ -135,7 +135,8 @@ def test_c2_full_tree_matches_oracle():
             if (tag == "leaf") != name.startswith("1:"):
                 continue
             chk = check_agent(model, ga["prompt"], ga["output"], ga["logprobs"], gpu_logits=logits[name])
-            assert chk["mismatches"] == [] and chk["lp_ok"], (name, chk)
+            assert chk["mismatches"] == [] and chk["lp_ok"], (name, chk["max_logit_err"], chk["max_lp_err"],
+                                                              chk["checked"], chk["mismatches"])
             checked += chk["checked"]
             total += len(ga["output"])
             per[name] = (chk["checked"], round(chk["max_logit_err"], 4))

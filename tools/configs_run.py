@@ -4,11 +4,15 @@ the 8B decode forward rate.  Prints one JSON line per config."""
 import json
 import sys
 import time
-sys.path.insert(0, '/root/repo')
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
 from paper_2512_18126_b200 import capi
 from paper_2512_18126_b200.configs import CONFIGS
 
-peak = json.load(open('/root/repo/MEASURED_PEAKS.json'))['hbm_gbs'] if __import__('os').path.exists('/root/repo/MEASURED_PEAKS.json') else 6544.3
+PEAKS = ROOT / 'MEASURED_PEAKS.json'
+peak = json.load(open(PEAKS))['hbm_gbs'] if PEAKS.exists() else 6544.3
 names = sys.argv[1:] or ['C4-tree', 'C4-dense', 'C3']
 for name in names:
     cfg = dict(CONFIGS[name])
