@@ -61,7 +61,8 @@ def parse(argv=None):
     ap.add_argument("--profile-only", action="store_true", help="run steps without JSON (for ncu)")
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the secondary configs (C1 with early exit, C2 at 512 tokens) reported beside the headline")
-    ap.add_argument("--timeline", action="store_true", help="in-graph tick timeline (chain stamps) of one request")
+    ap.add_argument("--no-timeline", action="store_true",
+                    help="skip the in-graph tick timeline (chain stamps) of one extra request")
     ap.add_argument("--concurrency", default="4,8",
                     help="continuous-batching sweep on C1 reported beside the headline (comma list; '' to skip)")
     ap.add_argument("--dry-run", action="store_true",
@@ -180,6 +181,33 @@ def roofline(probes, hbm, tf, src, cfg_name, prefill=False):
     a = v["bytes"] / s / 1e9
     return {"bound": "hbm", "achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm,
             "bytes_per_launch": v["bytes"] / v["launches"], **common}
+
+
+def in_graph_roofline(tl, cfg, hbm):
+    """The dominant decode kernel inside the graphs, with PDL overlap: from the
+    chain-stamp timeline of the request's last phase (the root decoding alone,
+    one row), each launch's incremental time (its last CTA's end minus the
+    previous launch's) against its algorithmic bytes."""
+    from paper_2512_18126_b200.configs import agent_tag
+    if not tl or "kernels" not in tl:
+        return None
+    depth = len(cfg["topology"]["widths"])
+    shape = cfg["models"][agent_tag(cfg, depth, 0)]["shape"]
+    sp = {"tiny": (256, 1024), "1b": (2048, 8192), "8b": (4096, 14336)}[shape]
+    D, F = sp
+    ks = tl["kernels"]
+    inc = [ks[0]["end_us"] - ks[0]["start_us"]] + [ks[i]["end_us"] - ks[i - 1]["end_us"] for i in range(1, len(ks))]
+    gu = [t for k, t in zip(ks, inc) if k["kernel"].startswith("gemv_tc(swiglu")]
+    if not gu:
+        return None
+    us = statistics.median(gu)
+    byts = 2.0 * (2 * F) * D + 4.0 * D + 2.0 * F  # weights + one row in / out
+    a = byts / (us * 1e-6) / 1e9
+    return {"bound": "hbm", "kernel": "gate_up", "rows": 1, "achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm,
+            "bytes_per_launch": byts, "incremental_us": us, "launches": len(gu),
+            "tick_us": tl.get("tick_us"),
+            "source": "per-CTA %globaltimer stamps of one request's root-decode ticks (graphs and PDL as in the "
+                      "timed region): launch end minus the previous launch's end"}
 
 
 def probe_requests(eng, qc, samples):
@@ -514,7 +542,7 @@ def main():
     npr = max(1, min(args.probe_steps, args.steps))
     probes, n_ee_launches = probe_requests(eng, qc, [sample_of(i) for i in range(npr)])
     timeline = None
-    if rank == 0 and args.timeline:
+    if rank == 0 and not args.no_timeline:
         from paper_2512_18126_b200 import chain
         try:
             timeline = chain.request_timeline(eng, qc, sample_of(0))
@@ -557,6 +585,9 @@ def main():
     }
     if timeline:
         line["tick_timeline"] = timeline
+        rig = in_graph_roofline(timeline, cfg, hbm)
+        if rig:
+            line["roofline_in_graph"] = rig
     eng.close()  # the headline engine; the extra measurements build their own
     if not args.no_secondary and world == 1:
         sec = []

@@ -44,7 +44,9 @@ GpuEngine::GpuEngine(std::vector<ModelSpec> models, std::vector<int> agents_per_
   MOA_CUDA(cudaMemsetAsync(out_tok_, 0, sizeof(int) * nout, stream_));
   if (opt_.keep_logits) {
     MOA_CUDA(cudaMalloc(&logits_, sizeof(float) * nout * logits_v_));
-    MOA_CUDA(cudaMalloc(&logits_scratch_, sizeof(float) * static_cast<long long>(max_slots_) * logits_v_));
+    // one scratch region per model: forwards of different models run side by side on their own streams
+    MOA_CUDA(cudaMalloc(&logits_scratch_,
+                        sizeof(float) * static_cast<long long>(models.size()) * max_slots_ * logits_v_));
   }
   ring_bytes_ = sizeof(k::RowDesc) * (opt_.max_rows + max_slots_) + sizeof(int) * (2 * max_slots_ + 3) + 16;
   for (const auto& dm : models_) ring_bytes_ = std::max(ring_bytes_, DeviceModel::kMaxRun * dm->run_stride());
@@ -338,14 +340,16 @@ void GpuEngine::upload_and_forward(int m, const std::vector<k::RowDesc>& rows, c
     MOA_CUDA(cudaMemcpyAsync(dm.buffers().sel, s.host, sb + rb, cudaMemcpyHostToDevice, st));
     MOA_CUDA(cudaEventRecord(s.done, st));
   }
-  float* logits = (opt_.keep_logits && !lsel.empty()) ? logits_scratch_ : nullptr;
+  float* logits = (opt_.keep_logits && !lsel.empty())
+                      ? logits_scratch_ + static_cast<long long>(m) * max_slots_ * logits_v_
+                      : nullptr;
   dm.forward(static_cast<int>(rows.size()), static_cast<int>(lsel.size()), max_pos, ts, out_tok_, out_tok_,
              out_lp_, out_ent_, logits, st, distinct, prefill, singles > 0);
   if (logits) {  // debug path: scatter each logits row to its (slot, k) home
     const long long V = dm.spec().vocab;
     for (std::size_t i = 0; i < lsel.size(); ++i)
       MOA_CUDA(cudaMemcpyAsync(logits_ + static_cast<long long>(lout[i]) * logits_v_,
-                               logits_scratch_ + static_cast<long long>(i) * V, sizeof(float) * V,
+                               logits + static_cast<long long>(i) * V, sizeof(float) * V,
                                cudaMemcpyDeviceToDevice, st));
   }
   if (async_upload_) MOA_CUDA(cudaEventRecord(blob_free_[2 * static_cast<std::size_t>(m) + static_cast<std::size_t>(b)], st));

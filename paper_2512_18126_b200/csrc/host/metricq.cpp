@@ -70,6 +70,7 @@ GpuMetricQ::GpuMetricQ(int hidden, std::uint64_t seed, double tau, bool include_
   MOA_CUDA(cudaMalloc(&d_emb_, sizeof(double) * static_cast<long long>(max_tokens) * hidden));
   cross_ = hidden > max_tokens;
   if (const char* e = std::getenv("MOA_FCS_ROUTE")) cross_ = std::string(e) == "nn";  // force one route (tests)
+  if (const char* e = std::getenv("MOA_EE_FUSED")) fused_ = std::string(e) != "0";    // A/B: the 5-launch path
   if (cross_) {
     MOA_CUDA(cudaMalloc(&d_hat_, sizeof(double) * static_cast<long long>(max_members) * max_tokens * hidden));
     MOA_CUDA(cudaMalloc(&d_nv_, sizeof(int) * max_members));
@@ -93,6 +94,13 @@ GpuMetricQ::~GpuMetricQ() {
 QualityScore GpuMetricQ::add_completion(const int* d_tok, const float* d_lp, long long base, int n) {
   if (n <= 0) throw ValidationError("logprobs: need at least one token");
   if (n > max_tokens_) throw ValidationError("metricq: completion longer than the evaluator capacity");
+  if (!cross_ && fused_ && k::ee_fused_mock_supported(hidden_, completions())) {
+    // the whole evaluation in one launch; one synchronisation for its result
+    const int m = completions();
+    if (m >= max_members_) throw ValidationError("metricq: exit group capacity exceeded");
+    k::ee_fused_mock(d_tok, d_lp, base, n, hidden_, seed_, 1e-12, d_corrs_, m, d_out_, st_);
+    return finish(nullptr, 0, n, nullptr, true);
+  }
   k::ee_mock_embed(d_tok, base, n, hidden_, seed_, d_emb_, st_);
   return finish(d_lp, base, n);
 }
@@ -116,13 +124,15 @@ QualityScore GpuMetricQ::add_completion_conf(double c, int n) {
   return finish(nullptr, 0, n, &c);
 }
 
-QualityScore GpuMetricQ::finish(const float* d_lp, long long base, int n, const double* conf) {
+QualityScore GpuMetricQ::finish(const float* d_lp, long long base, int n, const double* conf, bool computed) {
   const int m = completions();
   if (m >= max_members_) throw ValidationError("metricq: exit group capacity exceeded");
   const long long hh = static_cast<long long>(hidden_) * hidden_;
-  if (!conf) k::ee_confidence(d_lp + base, n, d_out_, st_);
+  if (!conf && !computed) k::ee_confidence(d_lp + base, n, d_out_, st_);
   const int nout = cross_ ? 2 + m : 1 + m;  // C, FCS numerators (+ the self term on the n x n route)
-  if (cross_) {
+  if (computed) {
+    // d_out_ already holds C and the FCS row (ee_fused_mock)
+  } else if (cross_) {
     const long long stride = static_cast<long long>(max_tokens_) * hidden_;
     double* hat = d_hat_ + stride * m;
     k::ee_colnorm(d_emb_, n, hidden_, 1e-12, hat, st_);

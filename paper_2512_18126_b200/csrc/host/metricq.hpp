@@ -78,7 +78,7 @@ class GpuMetricQ {
   }
 
  private:
-  QualityScore finish(const float* d_lp, long long base, int n, const double* conf = nullptr);
+  QualityScore finish(const float* d_lp, long long base, int n, const double* conf = nullptr, bool computed = false);
   QualityScore current() const;
   int hidden_;
   std::uint64_t seed_;
@@ -95,6 +95,7 @@ class GpuMetricQ {
   std::vector<double> sim_;  // n x n
   // n x n route (hidden_ > max_tokens_)
   bool cross_ = false;
+  bool fused_ = true;  // mock provider, h x h route: one launch per evaluation (ee_fused_mock)
   double* d_hat_ = nullptr;   // [max_members][max_tokens][h] column-normalised rows
   int* d_nv_ = nullptr;       // [max_members] rows per stored completion
   double* d_part_ = nullptr;  // per-tile partial sums of squares

@@ -202,6 +202,143 @@ __global__ void sum_parts_kernel(const double* __restrict__ part, int tiles, dou
   }
 }
 
+// One launch for a whole mock-provider evaluation on the h x h route (h <=
+// 128, <= 16 stored members): confidence (warp 31, sequential fp64 sum), the
+// MockProvider rows hashed 32 at a time into shared memory (bit-exact with
+// mock_embed_kernel), the Gram's upper triangle accumulated in registers
+// (each entry sequential in r, as gram_kernel), the correlation (written to
+// corrs[m]) and its Frobenius cosine against every stored member (fixed
+// thread -> entry map and reduction tree: deterministic).  out[0] = C,
+// out[1 + k] = FCS(new, member k).
+constexpr int kEeThreads = 1024, kEeWorkers = 992, kEeRows = 32, kEeMaxM = 16, kEeMaxH = 128;
+constexpr int kEeMaxE = kEeMaxH * (kEeMaxH + 1) / 2;
+constexpr int kEePer = (kEeMaxE + kEeWorkers - 1) / kEeWorkers;  // entries per worker thread
+
+__global__ void __launch_bounds__(kEeThreads, 1)
+ee_fused_mock_kernel(const int* __restrict__ out_tok, const float* __restrict__ lp, long long base, int n, int h,
+                     std::uint64_t seed, double eps, double* __restrict__ corrs, int m, double* __restrict__ out) {
+  extern __shared__ double ee_sm[];
+  double* rows = ee_sm;                                // [kEeRows][h]
+  double* diag = rows + kEeRows * h;                   // [h]
+  double* mean = diag + h;                             // [kEeRows]
+  std::uint32_t* pairs = reinterpret_cast<std::uint32_t*>(mean + kEeRows);  // [E]: i << 16 | j
+  __shared__ double red[kEeWorkers / 32][2 * kEeMaxM + 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int E = h * (h + 1) / 2;
+  const long long hh = static_cast<long long>(h) * h;
+  if (warp == kEeWorkers / 32) {  // confidence C = exp(mean logprob), sequential as the reference
+    if (lane == 0) {
+      double sacc = 0.0;
+      for (int i = 0; i < n; ++i) sacc += static_cast<double>(lp[base + i]);
+      out[0] = exp(sacc / static_cast<double>(n));
+    }
+    return;
+  }
+  for (int e = tid; e < E; e += kEeWorkers) {  // upper-triangle entry table
+    int i = 0, rem = e;
+    while (rem >= h - i) {
+      rem -= h - i;
+      ++i;
+    }
+    pairs[e] = (static_cast<std::uint32_t>(i) << 16) | static_cast<std::uint32_t>(i + rem);
+  }
+  double acc[kEePer];
+#pragma unroll
+  for (int k = 0; k < kEePer; ++k) acc[k] = 0.0;
+  asm volatile("bar.sync 1, %0;" ::"n"(kEeWorkers) : "memory");
+  for (int r0 = 0; r0 < n; r0 += kEeRows) {
+    const int rc = min(kEeRows, n - r0);
+    for (int idx = tid; idx < rc * h; idx += kEeWorkers) {
+      const int r = idx / h, c = idx % h;
+      const std::uint64_t tok = static_cast<std::uint64_t>(static_cast<std::int64_t>(out_tok[base + r0 + r]));
+      const std::uint64_t row_seed = hash_combine(hash_combine(seed, tok), static_cast<std::uint64_t>(r0 + r));
+      const std::uint64_t bits = mix64(hash_combine(row_seed, static_cast<std::uint64_t>(c)));
+      const double u = static_cast<double>(bits >> 11) * 0x1.0p-53;
+      rows[r * h + c] = __dsub_rn(__dmul_rn(2.0, u), 1.0);
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kEeWorkers) : "memory");
+    if (tid < rc) {  // sequential row mean (embedding.cpp:104-108)
+      double sm = 0.0;
+      for (int c = 0; c < h; ++c) sm += rows[tid * h + c];
+      mean[tid] = sm / static_cast<double>(h);
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kEeWorkers) : "memory");
+    for (int idx = tid; idx < rc * h; idx += kEeWorkers) rows[idx] = rows[idx] - mean[idx / h];
+    asm volatile("bar.sync 1, %0;" ::"n"(kEeWorkers) : "memory");
+#pragma unroll
+    for (int k = 0; k < kEePer; ++k) {
+      const int e = tid + k * kEeWorkers;
+      if (e >= E) break;
+      const int i = pairs[e] >> 16, j = pairs[e] & 0xffff;
+      double a = acc[k];
+      for (int r = 0; r < rc; ++r) a = __dadd_rn(a, __dmul_rn(rows[r * h + i], rows[r * h + j]));
+      acc[k] = a;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kEeWorkers) : "memory");
+  }
+#pragma unroll
+  for (int k = 0; k < kEePer; ++k) {
+    const int e = tid + k * kEeWorkers;
+    if (e < E && (pairs[e] >> 16) == (pairs[e] & 0xffff)) diag[pairs[e] >> 16] = acc[k];
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kEeWorkers) : "memory");
+  // correlation (metricq.cpp:32-53, upper triangle mirrored) and the FCS sums
+  double dot[kEeMaxM], nv[kEeMaxM], nu = 0.0;
+#pragma unroll
+  for (int k = 0; k < kEeMaxM; ++k) dot[k] = nv[k] = 0.0;
+  double* cnew = corrs + hh * m;
+#pragma unroll
+  for (int k = 0; k < kEePer; ++k) {
+    const int e = tid + k * kEeWorkers;
+    if (e >= E) break;
+    const int i = pairs[e] >> 16, j = pairs[e] & 0xffff;
+    const double gi = diag[i], gj = diag[j];
+    double v = 0.0;
+    if (gi > eps && gj > eps) v = i == j ? 1.0 : acc[k] / sqrt(gi * gj);
+    cnew[static_cast<long long>(i) * h + j] = v;
+    cnew[static_cast<long long>(j) * h + i] = v;
+    const double w = i == j ? 1.0 : 2.0;  // symmetric: off-diagonal entries count twice
+    nu = fma(w * v, v, nu);
+#pragma unroll
+    for (int q = 0; q < kEeMaxM; ++q) {
+      if (q >= m) break;
+      const double b = corrs[hh * q + static_cast<long long>(i) * h + j];
+      dot[q] = fma(w * v, b, dot[q]);
+      nv[q] = fma(w * b, b, nv[q]);
+    }
+  }
+  // reduction: warp shuffles, then warps in order
+#pragma unroll
+  for (int o = 16; o; o >>= 1) nu += __shfl_xor_sync(0xffffffffu, nu, o);
+#pragma unroll
+  for (int q = 0; q < kEeMaxM; ++q) {
+    if (q >= m) break;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      dot[q] += __shfl_xor_sync(0xffffffffu, dot[q], o);
+      nv[q] += __shfl_xor_sync(0xffffffffu, nv[q], o);
+    }
+  }
+  if (lane == 0) {
+    red[warp][2 * kEeMaxM] = nu;
+    for (int q = 0; q < m; ++q) {
+      red[warp][q] = dot[q];
+      red[warp][kEeMaxM + q] = nv[q];
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kEeWorkers) : "memory");
+  if (tid < m) {
+    double d = 0.0, a = 0.0, b = 0.0;
+    for (int w = 0; w < kEeWorkers / 32; ++w) {
+      d += red[w][tid];
+      a += red[w][2 * kEeMaxM];
+      b += red[w][kEeMaxM + tid];
+    }
+    const double su = sqrt(a), sv = sqrt(b);
+    out[1 + tid] = (su == 0.0 || sv == 0.0) ? 0.0 : d / (su * sv);
+  }
+}
+
 }  // namespace
 
 void ee_colnorm(const double* emb, int n, int h, double eps, double* ahat, cudaStream_t st) {
@@ -270,6 +407,21 @@ void ee_corr(const double* emb, int n, int h, double eps, double* gram, double* 
 
 void ee_fcs(const double* corr_new, const double* corrs, int m, int h, double* sim, cudaStream_t st) {
   if (m > 0) fcs_kernel<<<m, 256, 0, st>>>(corr_new, corrs, h, sim);
+}
+
+
+bool ee_fused_mock_supported(int h, int m) { return h <= kEeMaxH && m <= kEeMaxM; }
+
+void ee_fused_mock(const int* out_tok, const float* lp, long long base, int n, int h, std::uint64_t seed, double eps,
+                   double* corrs, int m, double* out, cudaStream_t st) {
+  const int E = h * (h + 1) / 2;
+  const int smem = static_cast<int>((kEeRows * h + h + kEeRows) * sizeof(double) + E * sizeof(std::uint32_t));
+  static int attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(ee_fused_mock_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = smem;
+  }
+  ee_fused_mock_kernel<<<1, kEeThreads, smem, st>>>(out_tok, lp, base, n, h, seed, eps, corrs, m, out);
 }
 
 }  // namespace moa::k

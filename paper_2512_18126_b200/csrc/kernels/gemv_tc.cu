@@ -339,8 +339,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
       load_w(s, kt);
       tma_load_2d(sx + s * kTileX, &map_x, &full[s], (kt0 + kt) * kBK, 0);
     }
-    // this CTA's weight stream is issued: its share of the next kernel's weights into L2
-    l2_prefetch_share(a.pf_base, a.pf_bytes, blockIdx.x + gridDim.x * blockIdx.y, gridDim.x * gridDim.y);
+
   } else if (warp == 1 && lane == 0) {
     for (int kt = 0; kt < kt_n; ++kt) {
       const int s = kt % stages;
@@ -394,6 +393,10 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   }
   mbar_wait(done, 0);
   tc_fence_after();
+  // this CTA's weights are consumed: while its reduction / epilogue, the grid
+  // boundary and the next kernel's start leave HBM idle, pull this CTA's share
+  // of the next kernel's weights into L2
+  if (threadIdx.x == 0) l2_prefetch_share(a.pf_base, a.pf_bytes, blockIdx.x + gridDim.x * blockIdx.y, gridDim.x * gridDim.y);
   if (threadIdx.x == 0) gv_stamp(3);
   if (threadIdx.x == 64) chain_mark(cst, 3);
 

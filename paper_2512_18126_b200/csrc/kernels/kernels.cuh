@@ -114,9 +114,10 @@ struct GemvArgs {
   // (each weight byte is read once per forward; the activations, KV and
   // partials the chain re-reads keep the L2)
   bool evict_first = false;
-  // gemv_tc: once this CTA has issued its last weight load, prefetch its share
-  // of [pf_base, pf_base + pf_bytes) into L2 (the next kernel's weights), so
-  // HBM keeps streaming through this kernel's tail and the next one's start
+  // gemv_tc: once this CTA's MMAs are done (its weights consumed), prefetch
+  // its share of [pf_base, pf_base + pf_bytes) into L2 (the next kernel's
+  // weights), so HBM keeps streaming through this kernel's tail and the next
+  // one's start
   const void* pf_base = nullptr;
   long long pf_bytes = 0;
 };
@@ -280,5 +281,11 @@ void ee_cross_sumsq(const double* ahat, int n, const double* stored, const int* 
                     long long stride, int m, int h, double* part, double* out, cudaStream_t st);
 // sim[j] = frob_cos_sim_corr(corr_new, corrs[j]) for j < m (metricq.cpp:55-64).
 void ee_fcs(const double* corr_new, const double* corrs, int m, int h, double* sim, cudaStream_t st);
+// One launch per mock-provider evaluation on the h x h route (h <= 128, m <= 16
+// stored members): out[0] = C from the device logprobs, the new correlation into
+// corrs[m], out[1 + k] = FCS against member k.
+bool ee_fused_mock_supported(int h, int m);
+void ee_fused_mock(const int* out_tok, const float* lp, long long base, int n, int h, std::uint64_t seed, double eps,
+                   double* corrs, int m, double* out, cudaStream_t st);
 
 }  // namespace moa::k

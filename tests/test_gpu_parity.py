@@ -397,7 +397,14 @@ _SEQ = dict(C1U, name="C1U-seq", mode="sequential-pd")
                                         (_SEQ, 4), (_HETERO, 1)],
                          ids=lambda v: v["name"] if isinstance(v, dict) else str(v))
 def test_run_query_replay_and_numerics(cfg, sample):
-    g = _gpu_query(cfg, sample)
+    eng, qc = capi.engine_for(cfg, keep_logits=True)
+    try:
+        g = eng.run_query(qc, sample=sample)
+        logits = {name: np.stack([eng.read_logits(tuple(int(x) for x in name.split(":")), k)
+                                  for k in range(len(ga["output"]))]) if ga["output"] else None
+                  for name, ga in g["agents"].items()}
+    finally:
+        eng.close()
     o = _replay(cfg, g, sample)
     # 1. orchestration parity, bit-exact: prompts, schedule, EE decisions
     for name, oa in o["agents"].items():
@@ -427,12 +434,14 @@ def test_run_query_replay_and_numerics(cfg, sample):
         tag = cfg["assign"][min(int(name[0]) - 1, len(cfg["assign"]) - 1)]
         tag = tag[int(name.split(":")[1]) % len(tag)]
         mm = cfg["models"][tag]
-        chk = check_agent(_cpu_model(tag, mm["shape"], mm["seed"]), ga["prompt"], ga["output"], ga["logprobs"])
+        chk = check_agent(_cpu_model(tag, mm["shape"], mm["seed"]), ga["prompt"], ga["output"], ga["logprobs"],
+                          gpu_logits=logits[name])
         assert chk["mismatches"] == [], (name, chk)
         assert chk["lp_ok"], (name, chk)
         checked += chk["checked"]
     outputs = sum(len(ga["output"]) for ga in g["agents"].values())
-    assert checked >= 0.6 * outputs, (checked, outputs)  # token-only bound 2*LOGIT_ATOL: ~60-65% decisive
+    # measured per-logit errors (pairwise bound): a token is unchecked only at a genuine near-tie
+    assert checked >= 0.8 * outputs, (checked, outputs)
 
 
 @pytest.mark.parametrize("sample", [0, 1, 2, 3])
