@@ -192,9 +192,6 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   // decode rows of GQA agents: TMA-staged attention (MOA_DECODE_TMA=0: the register-staged kernel)
   attn_tma_ = kv_maps_ok_ && k::attention_decode_tma_supported(s.n_heads, s.n_kv_heads, static_cast<int>(hd), max_ctx);
   if (const char* e = std::getenv("MOA_DECODE_TMA")) attn_tma_ = attn_tma_ && e[0] != '0';
-  // decode ticks: L2 prefetch of the next kernel's weights (bit 0: attention
-  // -> Wo, bit 1: down -> next layer's Wqkv); MOA_L2_PREFETCH=<mask>
-  if (const char* e = std::getenv("MOA_L2_PREFETCH")) l2pf_ = std::atoi(e);
   // prompt-prefill ticks: the tcgen05 attention (MOA_PREFILL_TC=0: the mma.sync kernel)
   pf_tc_ = kv_maps_ok_ && k::attention_prefill_tc_supported(s.n_heads, s.n_kv_heads, static_cast<int>(hd)) &&
            k::make_tmap_q3d(&qmap3_, q_, max_rows, s.n_heads, static_cast<int>(hd), s.n_heads / s.n_kv_heads);
@@ -476,9 +473,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       if (attn_cluster_)
         k::attention_decode_cluster(kmap_, vmap_, q_, buf_.rows, rcap,
                                     k::attention_decode_cluster_splits(rcap, nkv, nsplit), meta, nh, nkv, hd,
-                                    kv_stride_, loff, max_ctx_, h_, st, prefill,
-                                    (swap_ab && (l2pf_ & 1)) ? static_cast<const void*>(L.wo) : nullptr,
-                                    2LL * D * nh * hd);
+                                    kv_stride_, loff, max_ctx_, h_, st, prefill);
       else if (attn_tma_)
         k::attention_decode_tma(kmap_, vmap_, q_, buf_.rows, rcap, nsplit, meta, nh, nkv, hd, kv_stride_, loff,
                                 max_ctx_, h_, attn_ws_, attn_cnt_, st, prefill);
@@ -534,10 +529,6 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     dn.out = x_;
     dn.res_early = true;  // x was written by the o-projection, two kernels back
     if (norm_fold) dn.ssq_out = ssq_, dn.xb_out = hn_;
-    if (swap_ab && (l2pf_ & 2) && l + 1 < s.n_layers) {  // the next layer's Wqkv into L2 through this tail
-      dn.pf_base = layers_[static_cast<std::size_t>(l + 1)].wqkv;
-      dn.pf_bytes = 2LL * s.qkv_cols() * D;
-    }
     probe_begin(gkind(KernelProbes::Down, KernelProbes::PfDown), 2.0 * dn.N * dn.K + 2.0 * Rv * dn.K + 8.0 * Rv * D,
                 2.0 * Rv * dn.N * dn.K);
     run_gemm(dn, &map_h_ffn_, &map_h_ffn16_, wmaps_[static_cast<std::size_t>(l)].wd);

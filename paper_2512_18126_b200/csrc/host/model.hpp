@@ -145,7 +145,6 @@ class DeviceModel {
   bool nfold_ok_ = false, use_nfold_ = true;
   float* ssq_ = nullptr;
   float* inv_ = nullptr;  // prep launches: the rows' inverse RMS [max_rows]
-  int l2pf_ = 0;          // decode: L2 prefetch of the next kernel's weights (mask, MOA_L2_PREFETCH)
   int lm_grid_ = 148;  // persistent LM head: one CTA per SM
   // decode GEMVs stream their weights with an L2 evict-first hint
   // (MOA_EVICT_FIRST=0: off; measured -3.5..-6% per 1B / 8B decode tick)

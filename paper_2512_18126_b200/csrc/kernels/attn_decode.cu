@@ -348,8 +348,7 @@ __global__ void __launch_bounds__(160)
 attention_decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                                 const bf16* __restrict__ q, const RowDesc* __restrict__ rows,
                                 const int* __restrict__ meta, int nh, int nkv, long long kv_stride,
-                                long long layer_off, int max_ctx, bf16* __restrict__ o, int skip_runs,
-                                const void* pf_base, long long pf_bytes) {
+                                long long layer_off, int max_ctx, bf16* __restrict__ o, int skip_runs) {
   using C = DecCl<HD, STG_>;
   constexpr int KSTEPS = HD / 16, NT = HD / 8, RB = HD * 2, STG = C::STG;
   extern __shared__ unsigned char dc_raw[];
@@ -371,10 +370,6 @@ attention_decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap, const 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g8 = lane >> 2, t4 = lane & 3;
   const int s = blockIdx.x, NS = gridDim.x, g = blockIdx.y, r = blockIdx.z;
-  // every CTA of the grid (live or not) prefetches its share of the next
-  // kernel's weights into L2 first: this kernel leaves HBM mostly idle
-  if (threadIdx.x == 32 * 4)
-    l2_prefetch_share(pf_base, pf_bytes, s + NS * (g + gridDim.y * r), NS * gridDim.y * gridDim.z);
   // cluster-uniform early exits (every CTA of a cluster has the same row)
   const int live = __ldg(meta);
   if (r >= live) return;
@@ -693,8 +688,7 @@ bool attention_decode_cluster_supported(int nh, int nkv, int hd) {
 
 void attention_decode_cluster(const TmaMap& kmap, const TmaMap& vmap, const bf16* q, const RowDesc* rows, int R_cap,
                               int ns, const int* meta, int nh, int nkv, int hd, long long kv_stride,
-                              long long layer_off, int max_ctx, bf16* o, cudaStream_t st, bool skip_runs,
-                              const void* pf_base, long long pf_bytes) {
+                              long long layer_off, int max_ctx, bf16* o, cudaStream_t st, bool skip_runs) {
   if (R_cap <= 0) return;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ns, nkv, R_cap);
@@ -718,7 +712,7 @@ void attention_decode_cluster(const TmaMap& kmap, const TmaMap& vmap, const bf16
     cfg.dynamicSmemBytes = smem;
     cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(&kmap),
                        *reinterpret_cast<const CUtensorMap*>(&vmap), q, rows, meta, nh, nkv, kv_stride, layer_off,
-                       max_ctx, o, skip_runs ? 1 : 0, pf_base, pf_bytes);
+                       max_ctx, o, skip_runs ? 1 : 0);
   };
   static const int stg = [] {  // MOA_ATTN_STAGES=3: a 3-stage ring for hd 128 (A/B)
     const char* e = std::getenv("MOA_ATTN_STAGES");

@@ -114,12 +114,6 @@ struct GemvArgs {
   // (each weight byte is read once per forward; the activations, KV and
   // partials the chain re-reads keep the L2)
   bool evict_first = false;
-  // gemv_tc: once this CTA's MMAs are done (its weights consumed), prefetch
-  // its share of [pf_base, pf_base + pf_bytes) into L2 (the next kernel's
-  // weights), so HBM keeps streaming through this kernel's tail and the next
-  // one's start
-  const void* pf_base = nullptr;
-  long long pf_bytes = 0;
 };
 void gemv(const GemvArgs& a, cudaStream_t st);  // dispatches to gemv_stream for large matrices
 // HBM-streaming variant (gemv_stream.cu): persistent CTAs, cp.async.bulk ring.
@@ -204,12 +198,9 @@ void attention_decode_tma(const TmaMap& kmap, const TmaMap& vmap, const bf16* q,
 // split's boxes through a TMA ring.  Same maps and pool contract as above.
 int attention_decode_cluster_splits(int rcap, int nkv, int nbox_cap);
 bool attention_decode_cluster_supported(int nh, int nkv, int hd);
-// pf_base / pf_bytes: prefetched into L2 by the grid's CTAs at their start
-// (the o-projection's weights: attention leaves HBM mostly idle).
 void attention_decode_cluster(const TmaMap& kmap, const TmaMap& vmap, const bf16* q, const RowDesc* rows, int R_cap,
                               int ns, const int* meta, int nh, int nkv, int hd, long long kv_stride,
-                              long long layer_off, int max_ctx, bf16* o, cudaStream_t st, bool skip_runs = false,
-                              const void* pf_base = nullptr, long long pf_bytes = 0);
+                              long long layer_off, int max_ctx, bf16* o, cudaStream_t st, bool skip_runs = false);
 
 // Prefill ticks (rows of long same-agent runs): CTA = 64 consecutive rows x q
 // head, keys streamed through smem once per same-agent segment; rows alone in

@@ -133,21 +133,6 @@ __device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// L2 prefetch of part `part` of `nparts` equal shares of [base, base + bytes)
-// (the next kernel's weights), issued by one thread as bulk prefetches.
-__device__ __forceinline__ void l2_prefetch_share(const void* base, long long bytes, int part, int nparts) {
-  if (base == nullptr || bytes <= 0) return;
-  const long long per = ((bytes + nparts - 1) / nparts + 15) & ~15LL;
-  long long b = per * part;
-  const long long e = b + per < bytes ? b + per : bytes;
-  const char* p = static_cast<const char*>(base);
-  for (; b < e; b += 65536) {
-    const long long n = e - b < 65536 ? e - b : 65536;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + b), "r"(static_cast<std::uint32_t>(n & ~15LL))
-                 : "memory");
-  }
-}
-
 // Programmatic dependent launch: release dependents early / wait for the
 // producer grid's memory before touching its outputs.
 __device__ __forceinline__ void pdl_launch_dependents() {
