@@ -177,6 +177,11 @@ typedef struct {
    * the request, between engine ticks, once per early-exit evaluation. */
   int (*embed_fn)(void* user, const int32_t* tokens, int n, int hidden, double* out);
   void* embed_user;
+  /* OutputLenDist::Empirical (agent.hpp:40-103): out_values_len[l] > 0 makes
+   * layer l's output length a uniform draw from the next out_values_len[l]
+   * entries of out_values (layers concatenated); NULL / 0 = out_lo..out_hi. */
+  const int* out_values;
+  const int* out_values_len;
 } moa_run_config;
 
 typedef struct {

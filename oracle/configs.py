@@ -25,7 +25,7 @@ def run_config(cfg: dict) -> RunConfig:
             cyc = cfg["assign"][min(a[0] - 1, len(cfg["assign"]) - 1)]
             assign[a] = cyc[a[1] % len(cyc)]
             ol = cfg["out_len"][min(a[0] - 1, len(cfg["out_len"]) - 1)]
-            out_len[a] = tuple(ol) if isinstance(ol, (list, tuple)) else int(ol)
+            out_len[a] = dict(ol) if isinstance(ol, dict) else tuple(ol) if isinstance(ol, (list, tuple)) else int(ol)
     keys = ("mode", "early_exit", "exit_scope", "tau", "include_diagonal", "chunk_size", "seed",
             "query_tokens", "leaf_prefix_tokens", "agg_prefix_tokens", "separator_tokens",
             "suffix_tokens", "hidden", "provider_seed")

@@ -28,7 +28,7 @@ class RunConfig:
     """orchestrator.hpp:23-53 (+ model assignment, which replaces rates)."""
     topology: Topology
     assign: dict  # agent -> model tag
-    out_len: dict  # agent -> fixed output length, or (lo, hi) uniform
+    out_len: dict  # agent -> fixed output length, (lo, hi) uniform, or {"values": [...]} empirical
     mode: str = "incremental-overlap"
     early_exit: bool = False
     exit_scope: str = "cluster"
@@ -61,14 +61,32 @@ class RunConfig:
             raise ValidationError("run.force_q: must be in [0, 1]")
         if self.mode not in MODES:
             raise ValidationError(f"mode: unknown '{self.mode}'")
+        for a, spec in self.out_len.items():
+            if isinstance(spec, dict) and (not spec["values"] or min(spec["values"]) < 0):
+                raise ValidationError(f"run: empirical output lengths need values >= 0 for agent {aid(a)}")
+            if self.early_exit and out_len_min(spec) < 1:  # orchestrator.cpp:42-60
+                raise ValidationError(f"run: early exit needs output_len >= 1 for agent {aid(a)}")
 
 
 def sample_out_len(spec, ss, a):
-    """OutputLenDist::sample with RngStream::derive(ss, "outlen:l:p") (agent.hpp:88-99)."""
+    """OutputLenDist::sample with RngStream::derive(ss, "outlen:l:p") (agent.hpp:88-99):
+    int = Fixed, (lo, hi) = Uniform, {"values": [...]} = Empirical (uniform over
+    the support: values[next_int(0, size - 1)])."""
     if isinstance(spec, int):
         return spec
+    if isinstance(spec, dict):
+        v = spec["values"]
+        return v[RngStream.derive_from(ss, "outlen:" + aid(a)).next_int(0, len(v) - 1)]
     lo, hi = spec
     return RngStream.derive_from(ss, "outlen:" + aid(a)).next_int(lo, hi)
+
+
+def out_len_min(spec):
+    if isinstance(spec, int):
+        return spec
+    if isinstance(spec, dict):
+        return min(spec["values"])
+    return spec[0]
 
 
 class Driver:

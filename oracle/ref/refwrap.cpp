@@ -365,6 +365,21 @@ json cmd_rng(const json& req) {
   return out;
 }
 
+// OutputLenDist::sample (agent.hpp:88-99) on RngStream::derive(seed, "outlen:" + agent)
+json cmd_outlen(const json& req) {
+  const std::uint64_t seed = req.value("seed", std::uint64_t{0});
+  const std::string agent = req.value("agent", std::string("1:0"));
+  const json& d = req.at("dist");
+  OutputLenDist dist;
+  const std::string kind = d.at("kind").get<std::string>();
+  if (kind == "fixed") dist = OutputLenDist::fixed_len(d.at("n").get<int>());
+  else if (kind == "uniform") dist = OutputLenDist::uniform(d.at("lo").get<int>(), d.at("hi").get<int>());
+  else dist = OutputLenDist::empirical(d.at("values").get<std::vector<int>>());
+  dist.validate("outlen");
+  RngStream rng = RngStream::derive(seed, "outlen:" + agent);
+  return json{{"n", dist.sample(rng)}};
+}
+
 thread_local std::string g_out;
 
 }  // namespace
@@ -382,6 +397,7 @@ extern "C" const char* moaref_call(const char* request) {
     else if (cmd == "time_run_query") out = cmd_time_run_query(req);
     else if (cmd == "rng") out = cmd_rng(req);
     else if (cmd == "summarize") out = cmd_summarize(req);
+    else if (cmd == "outlen") out = cmd_outlen(req);
     else out = json{{"error", "unknown"}, {"what", cmd}};
   } catch (const ValidationError& e) {
     out = json{{"error", "ValidationError"}, {"what", e.what()}};

@@ -79,7 +79,8 @@ class RunConfigC(C.Structure):
                 ("seed", C.c_uint64), ("query_tokens", C.c_int), ("leaf_prefix_tokens", C.c_int),
                 ("agg_prefix_tokens", C.c_int), ("separator_tokens", C.c_int), ("suffix_tokens", C.c_int),
                 ("hidden", C.c_int), ("provider_seed", C.c_uint64), ("embed_model", C.c_int),
-                ("embed_fn", EMBED_FN), ("embed_user", C.c_void_p)]
+                ("embed_fn", EMBED_FN), ("embed_user", C.c_void_p),
+                ("out_values", _P(C.c_int)), ("out_values_len", _P(C.c_int))]
 
 
 class RunSummary(C.Structure):
@@ -538,13 +539,19 @@ class QueryConfig:
             else:
                 sizes = [b for l, b in enumerate(t["branching"]) for _ in range(widths[l + 1])]
             cs = arr(sizes)
-        cyc, clen, lo, hi = [], [], [], []
+        cyc, clen, lo, hi, vals, vlen = [], [], [], [], [], []
         for l in range(L):
             c = cfg["assign"][min(l, len(cfg["assign"]) - 1)]
             cyc += [model_index[x] for x in c]
             clen.append(len(c))
             ol = cfg["out_len"][min(l, len(cfg["out_len"]) - 1)]
-            a, b = (ol, ol) if isinstance(ol, int) else tuple(ol)
+            if isinstance(ol, dict):  # OutputLenDist::Empirical
+                a = b = 0
+                vals += list(ol["values"])
+                vlen.append(len(ol["values"]))
+            else:
+                a, b = (ol, ol) if isinstance(ol, int) else tuple(ol)
+                vlen.append(0)
             lo.append(a)
             hi.append(b)
         fq = cfg.get("force_q")
@@ -558,7 +565,8 @@ class QueryConfig:
             agg_prefix_tokens=cfg["agg_prefix_tokens"], separator_tokens=cfg["separator_tokens"],
             suffix_tokens=cfg["suffix_tokens"], hidden=cfg.get("hidden", 64),
             provider_seed=cfg.get("provider_seed", 0),
-            embed_model=model_index[cfg["embed_model"]] if cfg.get("provider", "mock") == "hidden" else -1)
+            embed_model=model_index[cfg["embed_model"]] if cfg.get("provider", "mock") == "hidden" else -1,
+            out_values=arr(vals) if vals else None, out_values_len=arr(vlen))
         if embed is not None:
             import numpy as np
             codes = {v: k for k, v in _PROVIDER_KINDS.items()}
@@ -596,7 +604,8 @@ def engine_for(cfg: dict, device=0, keep_logits=False, max_ctx=None, max_rows=16
                         max_agents=max(1, counts[tag] * concurrency),
                         **{k: v for k, v in cfg["models"][tag].items() if k not in ("shape", "seed")})
              for tag in tags]
-    out_max = max(x if isinstance(x, int) else x[1] for x in cfg["out_len"])
+    out_max = max(x if isinstance(x, int) else max(x["values"]) if isinstance(x, dict) else x[1]
+                  for x in cfg["out_len"])
     if max_ctx is None:
         prompt_max = max(cfg["query_tokens"] + cfg["leaf_prefix_tokens"],
                          cfg["agg_prefix_tokens"] + cfg["suffix_tokens"]

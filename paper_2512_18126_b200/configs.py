@@ -33,6 +33,10 @@ C0 = dict(
 C1 = dict(copy.deepcopy(C0), name="C1", early_exit=True,
           workload="tree 4-2-1, tiny agents, greedy 64 tokens, adaptive early exit (cluster scope, tau 0.7)")
 
+# OutputLenDist::Empirical (agent.hpp:40-103): leaf lengths drawn from a support
+C1E = dict(copy.deepcopy(C0), name="C1E", early_exit=True, out_len=[{"values": [24, 40, 72, 96]}, 64, 64],
+           workload="C1 with empirical leaf output lengths {24, 40, 72, 96}")
+
 # EE parity variant: uneven leaf lengths (test_orchestrator.cpp:32-57 style) so
 # exits actually prune still-decoding siblings.
 C1U = dict(copy.deepcopy(C1), name="C1U", out_len=[[24, 96], 64, 64],
@@ -76,7 +80,7 @@ C1H1B = dict(copy.deepcopy(C1H), name="C1H1B",
                          embed=dict(shape="1b", seed=7, n_layers=2)),
              workload="C1U with the hidden-state provider at 1B width (h = 2048, n x n FCS route)")
 
-CONFIGS = {c["name"]: c for c in (C0, C1, C1U, C1H, C1H1B, C2, C3, C4_TREE, C4_DENSE)}
+CONFIGS = {c["name"]: c for c in (C0, C1, C1E, C1U, C1H, C1H1B, C2, C3, C4_TREE, C4_DENSE)}
 
 
 def agent_tag(cfg: dict, layer: int, position: int) -> str:

@@ -101,16 +101,25 @@ moa::RunConfig run_config_of(const moa_run_config* c) {
   need(c->cycle_len, "cycle_len");
   need(c->out_lo, "out_lo");
   need(c->out_hi, "out_hi");
-  std::vector<int> off(static_cast<std::size_t>(c->n_layers) + 1, 0);
+  std::vector<int> off(static_cast<std::size_t>(c->n_layers) + 1, 0), voff(off);
   for (int l = 0; l < c->n_layers; ++l) {
     if (c->cycle_len[l] <= 0) throw moa::ValidationError("config: assignment cycle must not be empty");
     off[static_cast<std::size_t>(l) + 1] = off[static_cast<std::size_t>(l)] + c->cycle_len[l];
+    const int nv = c->out_values_len ? c->out_values_len[l] : 0;
+    if (nv < 0) throw moa::ValidationError("config: out_values_len must be >= 0");
+    if (nv > 0) need(c->out_values, "out_values");
+    voff[static_cast<std::size_t>(l) + 1] = voff[static_cast<std::size_t>(l)] + nv;
   }
   for (const auto& layer : cfg.topology.layers())
     for (const auto& a : layer) {
       const int l = a.layer - 1;
       cfg.model_of[a] = c->model_cycle[off[static_cast<std::size_t>(l)] + a.position % c->cycle_len[l]];
-      cfg.out_len[a] = moa::OutLen{c->out_lo[l], c->out_hi[l]};
+      moa::OutLen ol{c->out_lo[l], c->out_hi[l], {}};
+      const int nv = c->out_values_len ? c->out_values_len[l] : 0;
+      if (nv > 0)
+        ol.values.assign(c->out_values + voff[static_cast<std::size_t>(l)],
+                         c->out_values + voff[static_cast<std::size_t>(l)] + nv);
+      cfg.out_len[a] = std::move(ol);
     }
   switch (c->mode) {
     case MOA_MODE_SEQUENTIAL_PD: cfg.mode = moa::ScheduleMode::SequentialPd; break;

@@ -1,5 +1,7 @@
 #include "orchestrator.hpp"
 
+#include <algorithm>
+
 #include <chrono>
 
 namespace moa {
@@ -19,9 +21,27 @@ void RunConfig::validate() const {  // orchestrator.cpp:21-62
       if (!model_of.count(a)) throw ValidationError("run: no model assigned to agent " + a.str());
       auto it = out_len.find(a);
       if (it == out_len.end()) throw ValidationError("run: no output length for agent " + a.str());
-      if (it->second.lo < 0 || it->second.hi < it->second.lo)
+      const OutLen& ol = it->second;
+      if (ol.values.empty() && (ol.lo < 0 || ol.hi < ol.lo))
         throw ValidationError("run: output length needs 0 <= min <= max for agent " + a.str());
+      for (int v : ol.values)
+        if (v < 0) throw ValidationError("run: empirical output lengths must be >= 0 for agent " + a.str());
+      // quality scores need at least one token of logprobs per output (orchestrator.cpp:42-60)
+      if (early_exit && ol.min() < 1)
+        throw ValidationError("run: early exit needs output_len >= 1 for agent " + a.str());
     }
+}
+
+int OutLen::min() const { return values.empty() ? lo : *std::min_element(values.begin(), values.end()); }
+
+int OutLen::sample(std::uint64_t ss, const AgentId& a) const {
+  if (!values.empty()) {
+    rng::Stream s = rng::Stream::derive(ss, "outlen:" + a.str());
+    return values[static_cast<std::size_t>(s.next_int(0, static_cast<std::int64_t>(values.size()) - 1))];
+  }
+  if (hi == lo) return lo;  // Fixed (a Uniform of one value draws the same)
+  rng::Stream s = rng::Stream::derive(ss, "outlen:" + a.str());
+  return static_cast<int>(s.next_int(lo, hi));
 }
 
 std::map<AgentId, int> tree_placement(const Topology& topo, int world) {
@@ -167,12 +187,7 @@ struct Request {
     int max_out = 0;
     for (const auto& layer : topo.layers())
       for (const AgentId& a : layer) {
-        const OutLen ol = cfg.out_len.at(a);
-        int n = ol.lo;
-        if (ol.hi != ol.lo) {
-          rng::Stream s = rng::Stream::derive(ss, "outlen:" + a.str());
-          n = static_cast<int>(s.next_int(ol.lo, ol.hi));
-        }
+        const int n = cfg.out_len.at(a).sample(ss, a);
         max_out = std::max(max_out, n);
         if (topo.precursors(a).empty()) {
           TokenSeq prompt = rng::synth_tokens(ss, "leaf_prefix:" + a.str(), cfg.leaf_prefix_tokens);

@@ -20,8 +20,11 @@ namespace moa {
 enum class ScheduleMode { SequentialPd, DpOnly, DpChunkedPrefill, IncrementalOverlap };  // pdsim.hpp:38
 enum class ExitScope { Cluster, Layer };                                                   // orchestrator.hpp:17
 
-struct OutLen {
-  int lo = 64, hi = 64;  // fixed when lo == hi, else uniform (agent.hpp:40-103)
+struct OutLen {             // OutputLenDist (agent.hpp:40-103)
+  int lo = 64, hi = 64;      // Fixed when lo == hi, else Uniform [lo, hi]
+  std::vector<int> values;   // Empirical when non-empty: uniform over this support
+  int min() const;
+  int sample(std::uint64_t ss, const AgentId& a) const;  // RngStream::derive(ss, "outlen:" + a)
 };
 
 struct RunConfig {  // orchestrator.hpp:23-53 (+ model per agent, which replaces rates)

@@ -1,210 +1,79 @@
 // Prefill GEMM on the 5th-generation tensor cores (sm_100a):
 //   Y[M][N] = A[M][K] . W[N][K]^T, bf16 operands, fp32 accumulation in TMEM.
 //
-// One CTA per 128 x 128 output tile, 4 warps:
-//   warp 0 / lane 0  TMA producer: A and W k-tiles (64 x 128, SWIZZLE_128B)
-//                    into a 4-stage shared-memory ring, mbarrier complete_tx;
-//   warp 1 / lane 0  MMA issuer: tcgen05.mma.cta_group::1.kind::f16
-//                    (M=128, N=128, K=16) x 4 per k-tile, tcgen05.commit
-//                    frees the stage;
-//   all 4 warps      epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes
-//                    32w..32w+31 = rows), then the same epilogues as the GEMV
-//                    path (RoPE + KV append, residual add, SwiGLU, fp32 store).
+// Two kernels, one epilogue (RoPE + KV append / residual add / SwiGLU / fp32,
+// normed maps scaled by the rows' inverse RMS):
+//  * gemm_tc_kernel -- one CTA per 128 x 128 output tile, 4 warps (warp 0:
+//    TMA producer, warp 1: MMA issuer, all four: epilogue), 3-stage ring, two
+//    CTAs per SM so one's epilogue overlaps the other's main loop.  Used for
+//    the chunked-prefill ticks (M <= 512 rows): N / 128 CTAs stream the
+//    weights.
+//  * gemm_tc_persistent_kernel -- prompt-prefill ticks (M > 512): one CTA per
+//    SM loops over 128 x 256 tiles (M-fastest order: concurrent CTAs share a
+//    weight tile in L2); warp 0 streams A and W k-tiles through a 3-stage
+//    ring, warp 1 issues tcgen05.mma (M 128, N 256) into one of two TMEM
+//    accumulators (2 x 256 columns), warps 2-5 run the epilogue of tile i
+//    while the tensor core computes tile i + 1.
 // With N along TMEM columns each thread holds consecutive columns of its row,
 // so RoPE pairs and gate/up pairs (adjacent device columns) sit in one thread.
 #include <cuda.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
+#include "tc_common.cuh"
 #include "stamp.cuh"
 
 namespace moa::k {
 
 namespace {
 
-// 128 x 128 tiles, 3 stages so two CTAs fit per SM and one CTA's epilogue
-// overlaps the other's main loop (measured: C3 prefill GEMMs 252 -> 205 ms;
-// 128 x 256 tiles with 2 stages lose on the small prefills of C1 / C2)
+using namespace tc;
+
 constexpr int kBM = 128, kBN = 128, kBK = 64, kStages = 3;
 constexpr int kTileA = kBM * kBK * 2;  // 16 KB
 constexpr int kTileB = kBN * kBK * 2;  // 16 KB
 constexpr int kSmem = kStages * (kTileA + kTileB) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr std::uint32_t kIdesc = idesc_bf16(kBM, kBN);
 
-__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
-  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
-}
+// persistent kernel: 128 x 256 tiles, 3 stages (+ a 32 KB epilogue staging tile), 2 TMEM accumulators
+constexpr int kPN = 256, kPStages = 3;
+constexpr int kPTileB = kPN * kBK * 2;  // 32 KB
+constexpr int kPStage = kTileA + kPTileB;
+constexpr int kPStaging = kBM * kBN * 2;  // 32 KB: a 128 x 128 bf16 half-tile (QKV epilogue)
+constexpr int kPSmem = kPStages * kPStage + kPStaging + 1024 + 256;
+constexpr std::uint32_t kPIdesc = idesc_bf16(kBM, kPN);
+constexpr int kPMinRows = 512;  // rows above which the persistent kernel runs
 
-__device__ __forceinline__ void mbar_init(std::uint64_t* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes));
-}
-
-__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity));
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int x, int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
-      : "memory");
-}
-
-// K-major, SWIZZLE_128B shared-memory matrix descriptor: 8-row groups of
-// 128-byte rows, SBO = 1024 B, LBO unused (1), version 1 (sm100), layout 2.
-__device__ __forceinline__ std::uint64_t umma_desc(std::uint32_t saddr) {
-  std::uint64_t d = 0;
-  d |= static_cast<std::uint64_t>((saddr & 0x3FFFF) >> 4);
-  d |= static_cast<std::uint64_t>(1) << 16;
-  d |= static_cast<std::uint64_t>(1024 >> 4) << 32;
-  d |= static_cast<std::uint64_t>(1) << 46;
-  d |= static_cast<std::uint64_t>(2) << 61;
-  return d;
-}
-
-// kind::f16 instruction descriptor: F32 accumulate, BF16 A/B, K-major both.
-constexpr std::uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<std::uint32_t>(kBN >> 3) << 17) |
-                                 (static_cast<std::uint32_t>(kBM >> 4) << 24);
-
-__device__ __forceinline__ void umma_f16(std::uint32_t tmem_d, std::uint64_t da, std::uint64_t db, std::uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
-}
-
-__device__ __forceinline__ void umma_commit(std::uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, float (&v)[16]) {
-  std::uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__global__ void __launch_bounds__(128, 2)
-gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_w, const GemvArgs a) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
-  unsigned char* sa = smem;
-  unsigned char* sb = smem + kStages * kTileA;
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sb + kStages * kTileB);
-  std::uint64_t* empty = full + kStages;
-  std::uint64_t* done = empty + kStages;
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * kBN;
-  const int live = a.meta ? __ldg(a.meta) : a.R;
-  if (m0 >= live) return;  // uniform: the whole tile is past the live rows
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(done, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(kBN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const std::uint32_t tmem = *tmem_slot;
-  const int kt_n = a.K / kBK;
-
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer ----
-    for (int kt = 0; kt < kt_n; ++kt) {
-      const int s = kt % kStages;
-      if (kt >= kStages) mbar_wait(&empty[s], ((kt / kStages) - 1) & 1);
-      mbar_expect_tx(&full[s], kTileA + kTileB);
-      tma_load_2d(sa + s * kTileA, &map_a, &full[s], kt * kBK, m0);
-      tma_load_2d(sb + s * kTileB, &map_w, &full[s], kt * kBK, n0);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer ----
-    for (int kt = 0; kt < kt_n; ++kt) {
-      const int s = kt % kStages;
-      mbar_wait(&full[s], (kt / kStages) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const std::uint32_t a0 = smem_u32(sa + s * kTileA), b0 = smem_u32(sb + s * kTileB);
-#pragma unroll
-      for (int k = 0; k < kBK / 16; ++k)  // K advance inside the 128-byte swizzle atom: +32 bytes
-        umma_f16(tmem, umma_desc(a0 + k * 32), umma_desc(b0 + k * 32), (kt | k) ? 1u : 0u);
-      umma_commit(&empty[s]);
-    }
-    umma_commit(done);
-  }
-  __syncwarp();
-  // ---- epilogue: thread = row m0 + 32*warp + lane; 16 columns per tcgen05.ld ----
-  const int row = m0 + warp * 32 + lane;
-  const bool row_ok = row < live;
-  const std::uint32_t lane_base = static_cast<std::uint32_t>(warp * 32) << 16;
-  RowDesc rd{};
-  if (row_ok && a.epi == kEpiQkv) {
-    // while the main loop runs: this row's descriptor and its RoPE table row
-    // into L1 (the epilogue reads one cos/sin pair per column pair)
-    rd = a.rows[row];
-    const char* rp = reinterpret_cast<const char*>(a.rope + static_cast<long long>(rd.pos) * (a.hd / 2));
-    for (int off = 0; off < a.hd * 4; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + off));
-  }
-  if (row_ok && a.epi == kEpiResidual) {  // the tile's residual row segment into L1 while the main loop runs
-    const char* xp = reinterpret_cast<const char*>(a.out + static_cast<long long>(row) * a.N + n0);
-    for (int off = 0; off < kBN * 4 && n0 + off / 4 < a.N; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(xp + off));
-  }
-  // normed linear map: the row's inverse RMS scales its fp32 products
-  const float rs = (a.inv && row_ok) ? __ldcg(a.inv + row) : 1.f;
-  mbar_wait(done, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+// Epilogue of one 128-row x 128-column block of the output: `tc` = TMEM
+// address of this thread's lane and the block's first column, (row, n0) the
+// output coordinates, `et` the thread's index among the 128 epilogue threads
+// and `sync` a barrier over them; `st` is 32 KB of staging smem (QKV).
+template <typename Sync>
+__device__ __forceinline__ void block_epilogue(const GemvArgs& a, std::uint32_t tc, int row, bool row_ok, int live,
+                                               int m0, int n0, int et, const RowDesc& rd, float rs, bf16* st,
+                                               RowDesc* rds, Sync sync) {
   auto ld_scaled = [&](int c0, float (&v)[16]) {
-    tmem_ld16(tmem + lane_base + static_cast<std::uint32_t>(c0), v);
+    tmem_ld16(tc + static_cast<std::uint32_t>(c0), v);
     if (a.inv) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] *= rs;
     }
   };
+  const int lr = row - m0;  // block-local row
   if (a.epi == kEpiQkv && kBN % a.hd == 0) {
-    // RoPE + q / K / V rows staged as a bf16 tile in the (now idle) pipeline
-    // smem in natural head order, then written out in 16-byte chunks: one
-    // head row (hd x 2 bytes) per destination, instead of one 2-byte store per
-    // element scattered over q and the KV pool
-    bf16* st = reinterpret_cast<bf16*>(smem);  // [kBM][kBN], 16-byte chunks XOR-ed with row % 16
-    // (a warp's threads are 32 rows writing the same column: without the
-    // swizzle every store of a warp hits one bank)
+    // RoPE + q / K / V rows staged as a bf16 tile in smem in natural head
+    // order, then written out in 16-byte chunks: one head row (hd x 2 bytes)
+    // per destination, instead of one 2-byte store per element scattered over
+    // q and the KV pool (16-byte chunks XOR-ed with row % 16: a warp's threads
+    // are 32 rows writing the same column)
     auto sti = [](int rr, int cc) { return rr * kBN + ((((cc >> 3) ^ (rr & 15))) << 3) + (cc & 7); };
-    __shared__ RowDesc rds[kBM];
-    rds[warp * 32 + lane] = rd;
+    rds[lr] = rd;
     const int hd = a.hd, half = hd / 2, qk_cols = (a.nh + a.nkv) * hd;
     for (int c0 = 0; c0 < kBN; c0 += 16) {
       float v[16];
+      __syncwarp();  // tcgen05.ld is warp-collective
       ld_scaled(c0, v);
       if (!row_ok) continue;
 #pragma unroll
@@ -214,18 +83,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
           const int e = (n % hd) / 2, hb = cl - (n % hd);  // tile-local head start
           const float2 cs = a.rope[static_cast<long long>(rd.pos) * half + e];
           const float x0 = v[i], x1 = v[i + 1];
-          st[sti(warp * 32 + lane, hb + e)] = __float2bfloat16_rn(__fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y)));
-          st[sti(warp * 32 + lane, hb + e + half)] =
-              __float2bfloat16_rn(__fadd_rn(__fmul_rn(x1, cs.x), __fmul_rn(x0, cs.y)));
+          st[sti(lr, hb + e)] = __float2bfloat16_rn(__fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y)));
+          st[sti(lr, hb + e + half)] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(x1, cs.x), __fmul_rn(x0, cs.y)));
         } else {
-          st[sti(warp * 32 + lane, cl)] = __float2bfloat16_rn(v[i]);
-          st[sti(warp * 32 + lane, cl + 1)] = __float2bfloat16_rn(v[i + 1]);
+          st[sti(lr, cl)] = __float2bfloat16_rn(v[i]);
+          st[sti(lr, cl + 1)] = __float2bfloat16_rn(v[i + 1]);
         }
       }
     }
-    __syncthreads();
+    sync();
     const int cpr = kBN / 8;  // 16-byte chunks per tile row
-    for (int c = threadIdx.x; c < kBM * cpr; c += 128) {
+    for (int c = et; c < kBM * cpr; c += 128) {
       const int rl = c / cpr, ch = c % cpr, r = m0 + rl;
       const int n = n0 + ch * 8;
       if (r >= live || n >= a.N) continue;
@@ -242,9 +110,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
               (static_cast<long long>(head - a.nh - a.nkv) * a.max_ctx + d.pos) * hd + e;
       *reinterpret_cast<uint4*>(dst) = val;
     }
-  } else
+    sync();  // staging and rds are reused by the next block
+    return;
+  }
   for (int c0 = 0; c0 < kBN; c0 += 16) {
     float v[16];
+    __syncwarp();  // tcgen05.ld is warp-collective
     ld_scaled(c0, v);
     if (!row_ok) continue;
     const int nb = n0 + c0;
@@ -280,7 +151,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             *reinterpret_cast<const uint4*>(o8);
         break;
       }
-      case kEpiQkv: {
+      case kEpiQkv: {  // head dim not dividing the block: per-element RoPE stores
         const int hd = a.hd, half = hd / 2;
         const int qk_cols = (a.nh + a.nkv) * hd;
 #pragma unroll
@@ -309,9 +180,194 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       }
     }
   }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(128, 2)
+gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_w, const GemvArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  unsigned char* sa = smem;
+  unsigned char* sb = smem + kStages * kTileA;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sb + kStages * kTileB);
+  std::uint64_t* empty = full + kStages;
+  std::uint64_t* done = empty + kStages;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
+  __shared__ RowDesc rds[kBM];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * kBN;
+  const int live = a.meta ? __ldg(a.meta) : a.R;
+  if (m0 >= live) return;  // uniform: the whole tile is past the live rows
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&map_a);
+    prefetch_tmap(&map_w);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    mbar_fence_init();
+  }
+  if (warp == 0) tmem_alloc<kBN>(tmem_slot);
+  tc_fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kBN));
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+  const int kt_n = a.K / kBK;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    for (int kt = 0; kt < kt_n; ++kt) {
+      const int s = kt % kStages;
+      if (kt >= kStages) mbar_wait(&empty[s], ((kt / kStages) - 1) & 1);
+      mbar_expect_tx(&full[s], kTileA + kTileB);
+      tma_load_2d(sa + s * kTileA, &map_a, &full[s], kt * kBK, m0);
+      tma_load_2d(sb + s * kTileB, &map_w, &full[s], kt * kBK, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer ----
+    for (int kt = 0; kt < kt_n; ++kt) {
+      const int s = kt % kStages;
+      mbar_wait(&full[s], (kt / kStages) & 1);
+      tc_fence_after();
+      const std::uint32_t a0 = smem_u32(sa + s * kTileA), b0 = smem_u32(sb + s * kTileB);
+#pragma unroll
+      for (int k = 0; k < kBK / 16; ++k)  // K advance inside the 128-byte swizzle atom: +32 bytes
+        umma_bf16(tmem, umma_desc(a0 + k * 32), umma_desc(b0 + k * 32), kIdesc, (kt | k) ? 1u : 0u);
+      umma_commit(&empty[s]);
+    }
+    umma_commit(done);
+  }
+  __syncwarp();
+  // ---- epilogue: thread = row m0 + 32*warp + lane; 16 columns per tcgen05.ld ----
+  const int row = m0 + warp * 32 + lane;
+  const bool row_ok = row < live;
+  RowDesc rd{};
+  if (row_ok && a.epi == kEpiQkv) {
+    // while the main loop runs: this row's descriptor and its RoPE table row
+    // into L1 (the epilogue reads one cos/sin pair per column pair)
+    rd = a.rows[row];
+    const char* rp = reinterpret_cast<const char*>(a.rope + static_cast<long long>(rd.pos) * (a.hd / 2));
+    for (int off = 0; off < a.hd * 4; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + off));
+  }
+  if (row_ok && a.epi == kEpiResidual) {  // the tile's residual row segment into L1 while the main loop runs
+    const char* xp = reinterpret_cast<const char*>(a.out + static_cast<long long>(row) * a.N + n0);
+    for (int off = 0; off < kBN * 4 && n0 + off / 4 < a.N; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(xp + off));
+  }
+  // normed linear map: the row's inverse RMS scales its fp32 products
+  const float rs = (a.inv && row_ok) ? __ldcg(a.inv + row) : 1.f;
+  mbar_wait(done, 0);
+  tc_fence_after();
+  // the QKV staging tile reuses the (now idle) pipeline smem
+  block_epilogue(a, tmem + (static_cast<std::uint32_t>(warp * 32) << 16), row, row_ok, live, m0, n0, threadIdx.x, rd, rs,
+                 reinterpret_cast<bf16*>(smem), rds, [] { __syncthreads(); });
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<kBN>(tmem);
+}
+
+// Persistent prompt-prefill GEMM: one CTA per SM, tiles t = blockIdx.x,
+// blockIdx.x + gridDim.x, ... in M-fastest order over 128 x 256 tiles.
+__global__ void __launch_bounds__(192, 1)
+gemm_tc_persistent_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_w,
+                          const GemvArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  unsigned char* ring = smem;                                   // [kPStages][A 16 KB | W 32 KB]
+  bf16* staging = reinterpret_cast<bf16*>(smem + kPStages * kPStage);
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + kPStages * kPStage + kPStaging);
+  std::uint64_t* empty = full + kPStages;
+  std::uint64_t* acc_full = empty + kPStages;  // [2]: tile's accumulator complete
+  std::uint64_t* acc_free = acc_full + 2;      // [2]: epilogue done reading it
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(acc_free + 2);
+  __shared__ RowDesc rds[kBM];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int live = a.meta ? __ldg(a.meta) : a.R;
+  const int mt = (live + kBM - 1) / kBM, nt = (a.N + kPN - 1) / kPN;
+  const int tiles = mt * nt, kt_n = a.K / kBK;
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&map_a);
+    prefetch_tmap(&map_w);
+    for (int s = 0; s < kPStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_free[b], 128);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer: every tile's k-tiles through one ring ----
+      int q = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t % mt) * kBM, n0 = (t / mt) * kPN;
+        for (int kt = 0; kt < kt_n; ++kt, ++q) {
+          const int s = q % kPStages;
+          if (q >= kPStages) mbar_wait(&empty[s], ((q / kPStages) - 1) & 1);
+          unsigned char* st = ring + s * kPStage;
+          mbar_expect_tx(&full[s], kPStage);
+          tma_load_2d(st, &map_a, &full[s], kt * kBK, m0);
+          tma_load_2d(st + kTileA, &map_w, &full[s], kt * kBK, n0);
+          tma_load_2d(st + kTileA + kPTileB / 2, &map_w, &full[s], kt * kBK, n0 + kPN / 2);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer: tile i into accumulator i % 2 ----
+      int q = 0, i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const int b = i & 1;
+        if (i >= 2) mbar_wait(&acc_free[b], ((i >> 1) - 1) & 1);
+        tc_fence_after();
+        const std::uint32_t acc = tmem + b * kPN;
+        for (int kt = 0; kt < kt_n; ++kt, ++q) {
+          const int s = q % kPStages;
+          mbar_wait(&full[s], (q / kPStages) & 1);
+          tc_fence_after();
+          const std::uint32_t a0 = smem_u32(ring + s * kPStage), b0 = a0 + kTileA;
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_bf16(acc, umma_desc(a0 + k * 32), umma_desc(b0 + k * 32), kPIdesc, (kt | k) ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&acc_full[b]);
+      }
+    }
+  } else {
+    // ---- epilogue warps 2-5: TMEM lane quarter = warp % 4 ----
+    const int quarter = warp & 3, et = threadIdx.x - 64;
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int m0 = (t % mt) * kBM, n0 = (t / mt) * kPN;
+      const int row = m0 + quarter * 32 + lane;
+      const bool row_ok = row < live;
+      const RowDesc rd = (row_ok && a.epi == kEpiQkv) ? a.rows[row] : RowDesc{};
+      const float rs = (a.inv && row_ok) ? __ldcg(a.inv + row) : 1.f;
+      mbar_wait(&acc_full[b], (i >> 1) & 1);
+      __syncwarp();
+      tc_fence_after();
+      const std::uint32_t tc = tmem + (static_cast<std::uint32_t>(quarter * 32) << 16) + b * kPN;
+      for (int h = 0; h < kPN / kBN; ++h)
+        block_epilogue(a, tc + h * kBN, row, row_ok, live, m0, n0 + h * kBN, et, rd, rs, staging, rds,
+                       [] { asm volatile("bar.sync 1, 128;" ::: "memory"); });
+      tc_fence_before();
+      mbar_arrive(&acc_free[b]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
 // Operand prep of a normed linear map, one CTA per row: h = bf16(x) and the
@@ -407,6 +463,26 @@ bool gemm_tc_supported(int N, int K) { return N % kBN == 0 && K % kBK == 0; }
 
 void gemm_tc(const TmaMap& map_a, const TmaMap& map_w, const GemvArgs& a, cudaStream_t st) {
   if (a.R <= 0) return;
+  static const bool persistent_on = [] {  // MOA_GEMM_PERSISTENT=0: the tile kernel for every M (A/B)
+    const char* e = std::getenv("MOA_GEMM_PERSISTENT");
+    return !(e && e[0] == '0');
+  }();
+  if (persistent_on && a.R > kPMinRows && a.N % kPN == 0) {
+    static bool pattr = false;
+    static int sms = 148;
+    if (!pattr) {
+      cudaFuncSetAttribute(gemm_tc_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem);
+      uniform_carveout(reinterpret_cast<const void*>(gemm_tc_persistent_kernel));
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      pattr = true;
+    }
+    const int tiles = ((a.R + kBM - 1) / kBM) * (a.N / kPN);  // the row cap: live rows decide on the device
+    gemm_tc_persistent_kernel<<<tiles < sms ? tiles : sms, 192, kPSmem, st>>>(
+        *reinterpret_cast<const CUtensorMap*>(&map_a), *reinterpret_cast<const CUtensorMap*>(&map_w), a);
+    return;
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);

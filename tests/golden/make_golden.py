@@ -203,7 +203,23 @@ def gen_summary():
     dump("summary.json", cases)
 
 
+def gen_outlen():
+    """OutputLenDist::sample for every kind (agent.hpp:40-103), as run_query
+    draws it (RngStream::derive(sample seed, "outlen:<agent>"))."""
+    dists = [dict(kind="fixed", n=64), dict(kind="uniform", lo=24, hi=96), dict(kind="uniform", lo=7, hi=7),
+             dict(kind="empirical", values=[16, 40, 24]), dict(kind="empirical", values=[5]),
+             dict(kind="empirical", values=[1, 2, 3, 5, 8, 13, 21, 34])]
+    cases = []
+    for d in dists:
+        for seed in (0, 3, 2**63 + 11):
+            for agent in ("1:0", "1:3", "2:1"):
+                cases.append(dict(dist=d, seed=seed, agent=agent,
+                                  n=ref({"cmd": "outlen", "seed": seed, "agent": agent, "dist": d})["n"]))
+    dump("outlen.json", cases)
+
+
 if __name__ == "__main__":
+    gen_outlen()
     gen_rng()
     gen_topology()
     gen_slotplan()

@@ -393,7 +393,8 @@ _CHUNKED = dict(C1U, name="C1U-chunked", mode="dp-chunked-prefill")
 _SEQ = dict(C1U, name="C1U-seq", mode="sequential-pd")
 
 
-@pytest.mark.parametrize("cfg,sample", [(C0, 0), (C1, 0), (C1, 5), (C1U, 0), (C1U, 3), (_DENSE_EE, 1), (_CHUNKED, 2),
+@pytest.mark.parametrize("cfg,sample", [(C0, 0), (C1, 0), (C1, 5), (C1U, 0), (C1U, 3), (CONFIGS["C1E"], 2),
+                                        (_DENSE_EE, 1), (_CHUNKED, 2),
                                         (_SEQ, 4), (_HETERO, 1)],
                          ids=lambda v: v["name"] if isinstance(v, dict) else str(v))
 def test_run_query_replay_and_numerics(cfg, sample):
