@@ -546,8 +546,11 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
         return !(e && e[0] == '0');
       }();
       if (lm_fold) {
-        // the LM head normalises its selected rows itself (no rmsnorm launch)
+        // the LM head normalises its selected rows itself (no rmsnorm launch);
+        // on decode ticks from the last residual GEMV's bf16 copy of x and its
+        // sums of squares
         lm.X = x_;
+        if (norm_fold) lm.ssq = ssq_;
         lm.eps = eps;
         lm.sel = buf_.sel;
       } else {

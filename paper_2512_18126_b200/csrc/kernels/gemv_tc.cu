@@ -606,19 +606,42 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
     if (threadIdx.x == 64) chain_mark(cst, 1);
     if (fold) {
       // stage bf16(x[sel[r]]) for every k-tile (128B-swizzled K-major); the
-      // rows' inverse RMS scale the logits (RMSNorm on the fp32 product)
+      // rows' inverse RMS scale the logits (RMSNorm on the fp32 product).
+      // With the producer's bf16 copy of x and its 16-column sums of squares
+      // (a.A, a.ssq: decode ticks) both are plain loads; else from fp32 x.
+      // Every thread issues all its loads of a batch before using them.
       const int et0 = threadIdx.x - 64;
+      const bool xb = a.A != nullptr && a.ssq != nullptr;
+      __shared__ int sel_s[kN];
+      if (et0 < kN) sel_s[et0] = et0 < R ? __ldg(a.sel + et0) : 0;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
       {
         const int r = et0 >> 3, j = et0 & 7;  // 8 threads per row
         float ss = 0.f;
         if (r < R) {
-          const float* xr = a.X + static_cast<long long>(__ldg(a.sel + r)) * a.K;
-          for (int k = j * 4; k < a.K; k += 32) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(xr + k));
-            ss = fmaf(v.x, v.x, ss);
-            ss = fmaf(v.y, v.y, ss);
-            ss = fmaf(v.z, v.z, ss);
-            ss = fmaf(v.w, v.w, ss);
+          if (xb) {  // K / 16 partials per row: K / 128 float4 per thread
+            const float4* pr = reinterpret_cast<const float4*>(a.ssq + static_cast<long long>(sel_s[r]) * (a.K / 16));
+            float4 b[8];
+            for (int q0 = j; q0 < a.K / 64; q0 += 64) {
+#pragma unroll
+              for (int u = 0; u < 8; ++u) b[u] = q0 + 8 * u < a.K / 64 ? __ldcg(pr + q0 + 8 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) ss += (b[u].x + b[u].y) + (b[u].z + b[u].w);
+            }
+          } else {
+            const float4* xr = reinterpret_cast<const float4*>(a.X + static_cast<long long>(sel_s[r]) * a.K);
+            float4 b[8];
+            for (int q0 = j; q0 < a.K / 4; q0 += 64) {
+#pragma unroll
+              for (int u = 0; u < 8; ++u) b[u] = q0 + 8 * u < a.K / 4 ? __ldg(xr + q0 + 8 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                ss = fmaf(b[u].x, b[u].x, ss);
+                ss = fmaf(b[u].y, b[u].y, ss);
+                ss = fmaf(b[u].z, b[u].z, ss);
+                ss = fmaf(b[u].w, b[u].w, ss);
+              }
+            }
           }
         }
         ss += __shfl_xor_sync(0xffffffffu, ss, 1);
@@ -626,23 +649,42 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
         ss += __shfl_xor_sync(0xffffffffu, ss, 4);
         if (j == 0 && r < kN) inv_s[r] = r < R ? 1.0f / sqrtf(ss / static_cast<float>(a.K) + a.eps) : 0.f;
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      const int nchunk = KT * R * 8;
-      for (int ch = et0; ch < nchunk; ch += 128) {
-        const int t = ch / (R * 8), r = (ch >> 3) % R, cc = ch & 7;
-        const int col = t * kBK + cc * 8;
-        const float* xr = a.X + static_cast<long long>(__ldg(a.sel + r)) * a.K + col;
-        const float4 x0 = __ldg(reinterpret_cast<const float4*>(xr)), x1 = __ldg(reinterpret_cast<const float4*>(xr + 4));
-        __align__(16) bf16 o8[8];
-        o8[0] = __float2bfloat16_rn(x0.x);
-        o8[1] = __float2bfloat16_rn(x0.y);
-        o8[2] = __float2bfloat16_rn(x0.z);
-        o8[3] = __float2bfloat16_rn(x0.w);
-        o8[4] = __float2bfloat16_rn(x1.x);
-        o8[5] = __float2bfloat16_rn(x1.y);
-        o8[6] = __float2bfloat16_rn(x1.z);
-        o8[7] = __float2bfloat16_rn(x1.w);
-        *reinterpret_cast<uint4*>(sx + t * kTileX + r * 128 + ((cc ^ (r & 7)) * 16)) = *reinterpret_cast<const uint4*>(o8);
+      const int nchunk = KT * R * 8;  // (k-tile, row, 16-byte chunk of 8 elements)
+      for (int c0 = et0; c0 < nchunk; c0 += 128 * 8) {
+        uint4 raw[8];
+        float4 xa[8], xc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int ch = c0 + 128 * u;
+          if (ch >= nchunk) continue;
+          const int t = ch / (R * 8), r = (ch >> 3) % R, cc = ch & 7;
+          const long long off = static_cast<long long>(sel_s[r]) * a.K + t * kBK + cc * 8;
+          if (xb) {
+            raw[u] = __ldcg(reinterpret_cast<const uint4*>(a.A + off));
+          } else {
+            xa[u] = __ldg(reinterpret_cast<const float4*>(a.X + off));
+            xc[u] = __ldg(reinterpret_cast<const float4*>(a.X + off + 4));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int ch = c0 + 128 * u;
+          if (ch >= nchunk) continue;
+          const int t = ch / (R * 8), r = (ch >> 3) % R, cc = ch & 7;
+          if (!xb) {
+            __align__(16) bf16 o8[8];
+            o8[0] = __float2bfloat16_rn(xa[u].x);
+            o8[1] = __float2bfloat16_rn(xa[u].y);
+            o8[2] = __float2bfloat16_rn(xa[u].z);
+            o8[3] = __float2bfloat16_rn(xa[u].w);
+            o8[4] = __float2bfloat16_rn(xc[u].x);
+            o8[5] = __float2bfloat16_rn(xc[u].y);
+            o8[6] = __float2bfloat16_rn(xc[u].z);
+            o8[7] = __float2bfloat16_rn(xc[u].w);
+            raw[u] = *reinterpret_cast<const uint4*>(o8);
+          }
+          *reinterpret_cast<uint4*>(sx + t * kTileX + r * 128 + ((cc ^ (r & 7)) * 16)) = raw[u];
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("bar.sync 1, 128;" ::: "memory");
