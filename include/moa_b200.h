@@ -383,7 +383,6 @@ int moa_k_attention(uintptr_t q, uintptr_t rows, int R, uintptr_t meta, int nh, 
                     uintptr_t vpool, long long kv_stride, int max_ctx, uintptr_t out, int prefill, uintptr_t stream,
                     int slots);
 int moa_k_noop(uintptr_t p, int ctas, uintptr_t stream); /* trivial PDL kernel: launch-chain cost probe */
-int moa_k_debug_trace(uintptr_t buf); /* debug: gemv_tc per-CTA clock stamps, 0 = off */
 int moa_k_chain_stamp(uintptr_t buf); /* debug: decode-chain per-CTA globaltimer stamps (stamp.cuh), 0 = off */
 int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
 /* Hash-uniform weight init of a logical [rows][cols] tensor into a device row

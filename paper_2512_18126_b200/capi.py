@@ -159,7 +159,6 @@ _SIGS = {
     "moa_loopback_destroy": ([C.c_void_p], C.c_int),
     "moa_engine_attach_loopback": ([C.c_void_p, C.c_void_p, C.c_int], C.c_int),
     "moa_placement": ([C.c_int, C.c_int, _P(C.c_int), _P(C.c_int), C.c_int, _P(C.c_int)], C.c_int),
-    "moa_k_debug_trace": ([C.c_size_t], C.c_int),
     "moa_k_noop": ([C.c_size_t, C.c_int, C.c_size_t], C.c_int),
     "moa_k_chain_stamp": ([C.c_size_t], C.c_int),
     "moa_engine_probe": ([C.c_void_p, C.c_int], C.c_int),

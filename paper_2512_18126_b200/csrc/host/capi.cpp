@@ -1102,12 +1102,6 @@ int moa_k_noop(uintptr_t p, int ctas, uintptr_t stream) {
   return guard([&] { moa::k::noop_chain_link(reinterpret_cast<int*>(p), ctas, reinterpret_cast<cudaStream_t>(stream)); });
 }
 
-int moa_k_debug_trace(uintptr_t buf) {
-  return guard([&] { moa::k::gemv_tc_debug_trace(reinterpret_cast<unsigned long long*>(buf)); });
-}
-
-
-
 int moa_k_chain_stamp(uintptr_t buf) {
   return guard([&] {
     moa::k::forward_chain_stamp(reinterpret_cast<unsigned long long*>(buf));

@@ -32,20 +32,6 @@ constexpr int kTileX = kN * kBK * 2;  // 2 KB
 constexpr int kSmem = kStages * (kTileW + kTileX) + 1024 + 256;
 constexpr std::uint32_t kIdesc = idesc_bf16(kM, kN);
 
-// debug: per-CTA %globaltimer stamps (tools/gvisolated.py), off when null
-__device__ unsigned long long* g_gv_trace = nullptr;
-__device__ __forceinline__ void gv_stamp(int ev) {
-  if (g_gv_trace) {
-    unsigned long long t;
-    unsigned smid;
-    t = clock64();
-    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    const long long cta = blockIdx.y * gridDim.x + blockIdx.x;
-    g_gv_trace[cta * 8 + ev] = t;
-    g_gv_trace[cta * 8 + 7] = smid;
-  }
-}
-
 // Operands of the epilogue that do not depend on the MMA, loaded while the
 // weights stream: the residual rows x[r][n] (final once the previous kernel
 // completed), and for the QKV epilogue the rows' descriptors and RoPE factors
@@ -56,12 +42,21 @@ struct EpiPre {
   int kv[16], pos[16];
 };
 
+// The loads are pinned here (an empty asm consumes each value): without it the
+// compiler sinks them to their use in the epilogue, putting the L2 round
+// trips back on the critical path (measured: 2.4 us of RoPE epilogue per 8B
+// QKV launch).
 __device__ __forceinline__ void epi_preload(const GemvArgs& a, int n, int R, EpiPre& p) {
   if (a.epi == kEpiResidual) {
 #pragma unroll
     for (int r = 0; r < kN; ++r) {
       if (r >= R) break;
       p.res[r] = n < a.N ? __ldcg(a.out + static_cast<long long>(r) * a.N + n) : 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < kN; ++r) {
+      if (r >= R) break;
+      asm volatile("" ::"f"(p.res[r]));
     }
   } else if (a.epi == kEpiQkv) {
     const int hd = a.hd, half = hd / 2, qk_cols = (a.nh + a.nkv) * hd;
@@ -73,6 +68,11 @@ __device__ __forceinline__ void epi_preload(const GemvArgs& a, int n, int R, Epi
       p.kv[r] = rd.kv;
       p.pos[r] = rd.pos;
       p.cs[r] = n < qk_cols ? __ldg(a.rope + static_cast<long long>(rd.pos) * half + e) : make_float2(1.f, 0.f);
+    }
+#pragma unroll
+    for (int r = 0; r < kN; ++r) {
+      if (r >= R) break;
+      asm volatile("" ::"f"(p.cs[r].x), "f"(p.cs[r].y), "r"(p.kv[r]), "r"(p.pos[r]));
     }
   }
 }
@@ -279,7 +279,6 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     }
     mbar_fence_init();
   }
-  if (threadIdx.x == 0) gv_stamp(0);
   __shared__ unsigned long long cst[kChainPhases];
   const unsigned stag = (5u << 16) | (static_cast<unsigned>(a.epi) << 12) | ((a.K >> 4) & 0xfff);
   if (threadIdx.x == 0) {
@@ -297,7 +296,6 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const std::uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) gv_stamp(1);
   // split-K: announce this CTA's landing barrier as initialised (waited on
   // just before the partials are pushed, long after)
   if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
@@ -335,7 +333,6 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     for (int kt = 0; kt < kt_n; ++kt) {
       const int s = kt % stages;
       mbar_wait(&full[s], (kt / stages) & 1);
-      if (kt == 0) gv_stamp(2);
       if (kt == 0) chain_mark(cst, 4);
       tc_fence_after();
       const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + s * kTileX);
@@ -384,7 +381,6 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   }
   mbar_wait(done, 0);
   tc_fence_after();
-  if (threadIdx.x == 0) gv_stamp(3);
   if (threadIdx.x == 64) chain_mark(cst, 3);
 
   const int n = m0 + row;
@@ -422,7 +418,6 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
             "f"(v[4 * i]), "f"(v[4 * i + 1]), "f"(v[4 * i + 2]), "f"(v[4 * i + 3]), "r"(bar)
             : "memory");
     }
-    if (threadIdx.x == 0) gv_stamp(5);
     if (threadIdx.x == 0) chain_mark(cst, 5);
     if (warp * 32 < per) {  // warps holding at least one reduced row (whole warps: the epilogue shuffles)
       mbar_wait(&land_bar, 0);
@@ -442,15 +437,14 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
             v[4 * i + 3] += t.w;
           }
         }
-      if (threadIdx.x == 0) gv_stamp(6);
       if (threadIdx.x == 0) chain_mark(cst, 6);
       scale_rows(v);
       epilogue(a, mine ? m0 + wr : a.N, R, v, pre);
     }
   }
+  if (threadIdx.x == 0) chain_mark(cst, 7);  // this thread's epilogue done
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) gv_stamp(4);
   if (threadIdx.x == 0) {
     chain_mark(cst, 2);
     chain_flush(cst, stag);
@@ -522,7 +516,6 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
   const LmStat none{-INFINITY, 0.f, 0.f, 0x7fffffff};
 
   pdl_launch_dependents();
-  if (threadIdx.x == 0) gv_stamp(0);
   if (threadIdx.x == 0) {
     prefetch_tmap(&map_w);
     if (!fold) prefetch_tmap(&map_x);
@@ -585,7 +578,6 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
         for (int kt = 0; kt < KT; ++kt, ++q) {
           const int s = q % stages;
           mbar_wait(&full[s], (q / stages) & 1);
-          if (q == 0) gv_stamp(1);
           tc_fence_after();
           const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + (fold ? kt : s) * kTileX);
 #pragma unroll
@@ -596,7 +588,6 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
         umma_commit(&accf[j]);
       }
       chain_mark(cst, 7);
-      gv_stamp(2);
     }
     __syncwarp();
   } else {
@@ -742,13 +733,11 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
       __stcg(reinterpret_cast<float4*>(part + static_cast<long long>(et) * G + c),
              make_float4(st.m, st.s, st.t, __int_as_float(st.idx)));
     }
-    if (et == 0) gv_stamp(3);
     asm volatile("bar.sync 1, 128;" ::: "memory");
     if (et == 0) {
       unsigned prev;
       asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(cnt) : "memory");
       last = prev == static_cast<unsigned>(G - 1);
-      gv_stamp(4);
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");
     if (last) {
@@ -779,7 +768,6 @@ lm_head_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_consta
         }
       }
       if (et == 0) __stcg(cnt, 0);
-      if (et == 0) gv_stamp(5);
       if (et == 0) chain_mark(cst, 6);
     }
     if (et == 0) {
@@ -829,7 +817,6 @@ void lm_head_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, LmS
 }
 
 MOA_CHAIN_STAMP_SETTER(gemv_tc_chain_stamp)
-void gemv_tc_debug_trace(unsigned long long* buf) { cudaMemcpyToSymbol(g_gv_trace, &buf, sizeof(buf)); }
 
 // K splits per weight tile: as many as keep the grid within one CTA per SM
 // (148), at least 4 k-tiles per split (uneven splits allowed; the partials

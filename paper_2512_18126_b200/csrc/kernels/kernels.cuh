@@ -151,7 +151,6 @@ bool gemv_tc_norm_supported(const GemvArgs& a);
 int gemv_tc_splits(int N, int K, int epi);
 long long gemv_tc_ws_floats(int N, int K);
 void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float* ws, int* cnt, cudaStream_t st);
-void gemv_tc_debug_trace(unsigned long long* buf);
 // Persistent LM head with fused greedy statistics (epi kEpiLmStats args): one
 // CTA per SM over contiguous vocab tiles; part >= 16 * grid LmStat, cnt one
 // int zero-initialised once.  With a.X set (and a.sel, a.g, a.eps) the CTA

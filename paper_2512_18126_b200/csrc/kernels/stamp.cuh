@@ -7,7 +7,9 @@
 
 namespace moa::k {
 namespace {
-__device__ unsigned long long* g_chain_stamp = nullptr;
+// in constant memory: the "stamps off" test on every chain_mark is a
+// constant-cache hit, not a global load on the kernel's critical path
+__constant__ unsigned long long* g_chain_stamp = nullptr;
 constexpr unsigned long long kChainStampCap = 1ull << 25;
 constexpr int kChainPhases = 8;
 
