@@ -183,29 +183,23 @@ def roofline(probes, hbm, tf, src, cfg_name, prefill=False):
             "bytes_per_launch": v["bytes"] / v["launches"], **common}
 
 
-def in_graph_roofline(tl, cfg, hbm):
-    """The dominant decode kernel inside the graphs, with PDL overlap: from the
-    chain-stamp timeline of the request's last phase (the root decoding alone,
-    one row), each launch's incremental time (its last CTA's end minus the
-    previous launch's) against its algorithmic bytes."""
+def in_graph_roofline(gu, cfg, hbm):
+    """The dominant decode kernel inside the graphs, with PDL overlap: per-CTA
+    %globaltimer stamps of one request, the gate/up launches of its last phase
+    (the root decoding alone, one row): each launch's incremental time (its
+    last CTA's end minus the previous launch's end) against its algorithmic
+    bytes."""
     from paper_2512_18126_b200.configs import agent_tag
-    if not tl or "kernels" not in tl:
+    if not gu:
         return None
     depth = len(cfg["topology"]["widths"])
     shape = cfg["models"][agent_tag(cfg, depth, 0)]["shape"]
-    sp = {"tiny": (256, 1024), "1b": (2048, 8192), "8b": (4096, 14336)}[shape]
-    D, F = sp
-    ks = tl["kernels"]
-    inc = [ks[0]["end_us"] - ks[0]["start_us"]] + [ks[i]["end_us"] - ks[i - 1]["end_us"] for i in range(1, len(ks))]
-    gu = [t for k, t in zip(ks, inc) if k["kernel"].startswith("gemv_tc(swiglu")]
-    if not gu:
-        return None
+    D, F = {"tiny": (256, 1024), "1b": (2048, 8192), "8b": (4096, 14336)}[shape]
     us = statistics.median(gu)
     byts = 2.0 * (2 * F) * D + 4.0 * D + 2.0 * F  # weights + one row in / out
     a = byts / (us * 1e-6) / 1e9
     return {"bound": "hbm", "kernel": "gate_up", "rows": 1, "achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm,
             "bytes_per_launch": byts, "incremental_us": us, "launches": len(gu),
-            "tick_us": tl.get("tick_us"),
             "source": "per-CTA %globaltimer stamps of one request's root-decode ticks (graphs and PDL as in the "
                       "timed region): launch end minus the previous launch's end"}
 
@@ -541,11 +535,16 @@ def main():
     # the same requests replay (graphs bypassed during this pass only)
     npr = max(1, min(args.probe_steps, args.steps))
     probes, n_ee_launches = probe_requests(eng, qc, [sample_of(i) for i in range(npr)])
-    timeline = None
+    timeline, gu_inc = None, []
     if rank == 0 and not args.no_timeline:
         from paper_2512_18126_b200 import chain
         try:
-            timeline = chain.request_timeline(eng, qc, sample_of(0))
+            recs, e2e_st = chain.collect(eng, qc, sample_of(0))
+            timeline = chain.timeline(chain.ticks(recs))
+            from paper_2512_18126_b200.configs import agent_tag
+            root_shape = cfg["models"][agent_tag(cfg, len(cfg["topology"]["widths"]), 0)]["shape"]
+            d_root = {"tiny": 256, "1b": 2048, "8b": 4096}[root_shape]
+            gu_inc = chain.launch_increments(recs, f"gemv_tc(swiglu,K={d_root})")
         except Exception as e:  # diagnostics only
             timeline = {"error": str(e)}
     dev_ms_max, e2e_ms_max, toks_all, e2e_toks_all = reduce_over_ranks(pg, "cuda", dev_ms, e2e_s * 1e3, toks, toks,
@@ -585,9 +584,9 @@ def main():
     }
     if timeline:
         line["tick_timeline"] = timeline
-        rig = in_graph_roofline(timeline, cfg, hbm)
-        if rig:
-            line["roofline_in_graph"] = rig
+    rig = in_graph_roofline(gu_inc, cfg, hbm)
+    if rig:
+        line["roofline_in_graph"] = rig
     eng.close()  # the headline engine; the extra measurements build their own
     if not args.no_secondary and world == 1:
         sec = []

@@ -129,3 +129,28 @@ def request_timeline(eng, qc, sample=0, first_frac=0.75):
     if tl is not None:
         tl["stamped_request_e2e_ms"] = round(e2e, 3)
     return tl
+
+
+def launch_increments(records, prefix, last_frac=0.25, gap_ns=8000):
+    """In-graph time of each launch of the kernels named `prefix...` in the
+    last `last_frac` of the request: its last CTA's end minus the previous
+    launch's (any kernel's) end -- the launch's share of the serial chain,
+    programmatic-dependent-launch overlap included.  Returns microseconds."""
+    tag, phase, t = records[:, 0], records[:, 1], records[:, 3]
+    inst = []  # (end, is_target)
+    for tg in np.unique(tag):
+        e = np.sort(t[(tag == tg) & (phase == 0)])
+        if len(e) == 0:
+            continue
+        ends = np.sort(t[(tag == tg) & (phase == 2)])
+        starts = [g.min() for g in np.split(e, np.where(np.diff(e) > gap_ns)[0] + 1)] + [np.inf]
+        target = _name(int(tg)).startswith(prefix)
+        for j in range(len(starts) - 1):
+            w = ends[(ends >= starts[j]) & (ends < starts[j + 1])]
+            if len(w):
+                inst.append((int(w.max()), target))
+    inst.sort()
+    if len(inst) < 3:
+        return []
+    t0 = inst[0][0] + (inst[-1][0] - inst[0][0]) * (1.0 - last_frac)
+    return [(inst[i][0] - inst[i - 1][0]) / 1e3 for i in range(1, len(inst)) if inst[i][1] and inst[i][0] >= t0]
