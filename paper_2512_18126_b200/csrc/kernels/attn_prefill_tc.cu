@@ -121,7 +121,12 @@ attention_prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __gr
   unsigned char* Qs = sm;                        // [SUB][128 rows][128 B]
   unsigned char* ring = Qs + C::QB;              // [STG][K: SUB x 64 keys x 128 B | V: same]
   unsigned char* Ps = ring + STG * C::STAGE;     // [2][128 rows][64 keys] bf16, 128B-swizzled
-  __shared__ __align__(8) std::uint64_t full[STG], empty[STG], q_full, s_full[2], s_free[2], p_full, o_done[2];
+  // p_full alternates by item parity: the softmax warps may finish item i + 1
+  // before the MMA thread observes item i's arrival (no rescale to wait for),
+  // and a single barrier two phases ahead would alias the parity the MMA
+  // thread waits on (a deadlock seen when other streams' kernels slow the
+  // MMA thread down).  Every other barrier is bounded to one phase ahead.
+  __shared__ __align__(8) std::uint64_t full[STG], empty[STG], q_full, s_full[2], s_free[2], p_full[2], o_done[2];
   __shared__ std::uint32_t tmem_slot;
   __shared__ RowDesc rd_s[128];
   __shared__ int seg_b[129], seg_e[128], seg_of[128];
@@ -173,7 +178,8 @@ attention_prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __gr
     mbar_init(&s_full[1], 1);
     mbar_init(&s_free[0], 128);
     mbar_init(&s_free[1], 128);
-    mbar_init(&p_full, 128);
+    mbar_init(&p_full[0], 128);
+    mbar_init(&p_full[1], 128);
     mbar_init(&o_done[0], 1);
     mbar_init(&o_done[1], 1);
     mbar_fence_init();
@@ -234,7 +240,7 @@ attention_prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __gr
       issue_s(0);
       for (int i = 0; i < nitems; ++i) {
         if (i + 1 < nitems) issue_s(i + 1);
-        mbar_wait(&p_full, i & 1);  // P_i written, O rescaled
+        mbar_wait(&p_full[i & 1], (i >> 1) & 1);  // P_i written, O rescaled
         tc_fence_after();
         const int st = i % STG;
         const std::uint32_t v_u = smem_u32(ring + st * C::STAGE + SUB * C::KVCH);
@@ -331,7 +337,7 @@ attention_prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __gr
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
       tc_fence_before();
-      mbar_arrive(&p_full);
+      mbar_arrive(&p_full[i & 1]);
     }
     if (nitems > 0) {
       mbar_wait(&o_done[(nitems - 1) & 1], ((nitems - 1) >> 1) & 1);
