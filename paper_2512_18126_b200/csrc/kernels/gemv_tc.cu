@@ -824,8 +824,12 @@ MOA_CHAIN_STAMP_SETTER(gemv_tc_chain_stamp)
 int gemv_tc_splits(int N, int K, int epi) {
   const int tiles = (N + kM - 1) / kM, kts = K / kBK;
   if (epi == kEpiLmStats) return 1;
+  static const int max_ctas = [] {  // MOA_GEMV_MAX_CTAS (A/B): cap on tiles x splits
+    const char* e = std::getenv("MOA_GEMV_MAX_CTAS");
+    return e ? std::atoi(e) : 2 * 148;
+  }();
   int S = 1;  // power of two <= 8 (one cluster per tile), >= 4 k-tiles per split, <= 2 CTAs per SM
-  while (S < 8 && tiles * S * 2 <= 2 * 148 && kts / (S * 2) >= 4) S *= 2;
+  while (S < 8 && tiles * S * 2 <= max_ctas && kts / (S * 2) >= 4) S *= 2;
   return S;
 }
 

@@ -17,7 +17,7 @@ $L --launch-skip 600 -c 200 --log-file $O/launches_1b_r4.csv python tools/fwdben
 $F -k regex:gemv_tc_kernel --launch-skip 130 -c 3 -o $O/ncu_8b_gemv python tools/fwdbench.py 8b 4 2048 8 > /dev/null 2>&1
 $F -k regex:attention_decode_cluster --launch-skip 40 -c 1 -o $O/ncu_8b_attn_decode python tools/fwdbench.py 8b 4 2048 8 > /dev/null 2>&1
 $F -k regex:lm_head_tc --launch-skip 2 -c 1 -o $O/ncu_8b_lm_head python tools/fwdbench.py 8b 4 2048 8 > /dev/null 2>&1
-$F -k regex:gemm_tc_kernel --launch-skip 2 -c 2 -o $O/ncu_8b_gemm python tools/fwdbench.py 8b 4 2048 8 > /dev/null 2>&1
+$F -k regex:gemm_tc_persistent --launch-skip 2 -c 1 -o $O/ncu_8b_gemm_persistent python tools/fwdbench.py 8b 4 2048 4 > /dev/null 2>&1
 $F -k regex:attention_prefill_tc --launch-skip 0 -c 1 -o $O/ncu_8b_attn_prefill_tc python tools/fwdbench.py 8b 4 2048 8 > /dev/null 2>&1
 $F -k regex:gemv_tc_kernel --launch-skip 66 -c 4 -o $O/ncu_1b_gemv python tools/fwdbench.py 1b 4 2048 8 > /dev/null 2>&1
 ls -la $O
