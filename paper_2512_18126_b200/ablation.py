@@ -65,6 +65,7 @@ def run_ablation(base: dict, samples: int = 8, device: int = 0) -> list[dict]:
         rows.append({"setting": name, "samples": samples, "mean_e2e_ms": statistics.fmean(e2e),
                      "p50_e2e_ms": _pct(e2e, 0.5), "p95_e2e_ms": _pct(e2e, 0.95),
                      "normalized_mean": statistics.fmean(e / b for e, b in zip(e2e, base_e2e)),
+                     "mean_tokens": statistics.fmean(t for _, t in lat),
                      "tokens_per_s": sum(t for _, t in lat) / (sum(e2e) / 1e3)})
     return rows
 
@@ -90,6 +91,7 @@ def main():
     ap.add_argument("--json", default=None)
     ap.add_argument("--out", type=int, default=None, help="override output tokens per agent")
     ap.add_argument("--query-tokens", type=int, default=None, help="override the shared query length")
+    ap.add_argument("--no-second-layer", action="store_true", help="skip the second-layer schedule study")
     args = ap.parse_args()
     base = dict(CONFIGS[args.base])
     if args.out:
@@ -97,10 +99,10 @@ def main():
     if args.query_tokens:
         base["query_tokens"] = args.query_tokens
     out = {"base": args.base, "overrides": {"out": args.out, "query_tokens": args.query_tokens}, "ablation": run_ablation(base, args.samples),
-           "second_layer": run_second_layer_study(base, samples=args.samples)}
+           "second_layer": [] if args.no_second_layer else run_second_layer_study(base, samples=args.samples)}
     for r in out["ablation"]:
         print(f"{r['setting']:18s} mean {r['mean_e2e_ms']:8.2f} ms  p50 {r['p50_e2e_ms']:8.2f}  p95 {r['p95_e2e_ms']:8.2f}"
-              f"  normalized {r['normalized_mean']:.3f}  {r['tokens_per_s']:.0f} tok/s")
+              f"  normalized {r['normalized_mean']:.3f}  {r['mean_tokens']:.0f} tokens  {r['tokens_per_s']:.0f} tok/s")
     for r in out["second_layer"]:
         print(f"{r['mode']:20s} mean {r['mean_e2e_ms']:8.2f} ms  normalized {r['normalized_vs_sequential']:.3f}")
     if args.json:

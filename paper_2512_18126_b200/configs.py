@@ -60,6 +60,23 @@ C3 = dict(
     query_tokens=1984,
 )
 
+# The reference preset's scenario (config.cpp:182-240) at model scale: a 9-3-1
+# tree whose leaves cycle three profiles (here 1B, 1B, 8B) with outputs
+# ~U(192, 768) (the preset's U(256, 1024), scaled so the all-to-all
+# aggregators' 9-output prompts fit the 8192-token context), aggregators with
+# fixed 256-token outputs, adaptive early exit at cluster scope.  The
+# ablation's paper-scale base (ablation.py --base C5).
+C5 = dict(
+    copy.deepcopy(C0), name="C5",
+    workload="reference-preset analogue: tree 9-3-1, leaves 1B/1B/8B ~U(192,768), 1B aggregators 256, early exit",
+    topology=dict(kind="tree", widths=[9, 3, 1], branching=[3, 3]),
+    models=dict(fast=dict(shape="1b", seed=1), medium=dict(shape="1b", seed=4), slow=dict(shape="8b", seed=3),
+                agg=dict(shape="1b", seed=2)),
+    assign=[["fast", "medium", "slow"], ["agg"], ["agg"]],
+    out_len=[[192, 768], 256, 256],
+    early_exit=True,
+)
+
 C4_TREE = dict(copy.deepcopy(C0), name="C4-tree", workload="tree 9-3-1 (13 tiny agents)",
                topology=dict(kind="tree", widths=[9, 3, 1], branching=[3, 3]))
 C4_DENSE = dict(copy.deepcopy(C0), name="C4-dense", workload="all-to-all 6-6-1 (13 tiny agents)",
@@ -80,7 +97,7 @@ C1H1B = dict(copy.deepcopy(C1H), name="C1H1B",
                          embed=dict(shape="1b", seed=7, n_layers=2)),
              workload="C1U with the hidden-state provider at 1B width (h = 2048, n x n FCS route)")
 
-CONFIGS = {c["name"]: c for c in (C0, C1, C1E, C1U, C1H, C1H1B, C2, C3, C4_TREE, C4_DENSE)}
+CONFIGS = {c["name"]: c for c in (C0, C1, C1E, C1U, C1H, C1H1B, C2, C3, C4_TREE, C4_DENSE, C5)}
 
 
 def agent_tag(cfg: dict, layer: int, position: int) -> str:

@@ -121,7 +121,7 @@ def test_slotplan_matches_reference(golden):
             capi.lib().moa_slotplan_free(h)
 
 
-@pytest.mark.parametrize("name", ["C0", "C1", "C1U", "C2", "C3", "C4-tree", "C4-dense"])
+@pytest.mark.parametrize("name", ["C0", "C1", "C1U", "C2", "C3", "C4-tree", "C4-dense", "C5"])
 def test_query_config_marshalling(name):
     from paper_2512_18126_b200.configs import CONFIGS
     cfg = CONFIGS[name]
