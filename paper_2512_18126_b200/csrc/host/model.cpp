@@ -276,6 +276,18 @@ KernelProbes::~KernelProbes() {
 }
 
 namespace {
+// Smallest row-count bucket a tick graph is captured for (MOA_RCAP_MIN):
+// exact power-of-two buckets keep the decode attention's grid (rows x kv
+// heads x splits) free of dead CTAs, whose late scheduling would hold back
+// the dependent launch of the o-projection (measured: -1.3 us per 8B layer).
+int rcap_min() {
+  static const int v = [] {
+    const char* e = std::getenv("MOA_RCAP_MIN");
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  return v;
+}
+
 int pow2_at_least(int v, int lo) {
   int p = lo;
   while (p < v) p <<= 1;
@@ -294,7 +306,7 @@ void DeviceModel::forward(int R, int Rl, int max_pos, const TickStats& ts, const
   if (Rl > max_lrows_ || Rl > k::kLmMaxRows) throw RunError("model " + spec_.tag + ": logits rows exceed workspace");
   if (max_pos >= max_ctx_) throw RunError("model " + spec_.tag + ": position exceeds max_ctx");
   // bucket caps: one graph serves every tick whose live counts fit them
-  const int rcap = std::min(pow2_at_least(R, 8), max_rows_);
+  const int rcap = std::min(pow2_at_least(R, rcap_min()), max_rows_);
   const int ks = split_keys_;
   const int nsplit = pow2_at_least((max_pos + ks) / ks, 1);
   if (!use_graphs_ || probes_) {
@@ -327,7 +339,7 @@ void DeviceModel::forward_run(int K, int R, int max_pos, const int* out_tok_read
   if (K < 2 || K > kMaxRun || !runs_supported()) throw RunError("model " + spec_.tag + ": invalid decode run");
   if (R <= 0 || R > max_lrows_ || R > k::kLmMaxRows) throw RunError("model " + spec_.tag + ": run rows exceed workspace");
   if (max_pos >= max_ctx_) throw RunError("model " + spec_.tag + ": position exceeds max_ctx");
-  const int rcap = std::min(pow2_at_least(R, 8), max_rows_);
+  const int rcap = std::min(pow2_at_least(R, rcap_min()), max_rows_);
   const int ks = split_keys_;
   const int nsplit = pow2_at_least((max_pos + ks) / ks, 1);  // the last tick's: a cap for the earlier ones
   const auto key = std::make_tuple(rcap, nsplit, 1 | (use_tc_ ? 2 : 0) | 8 | (parity << 4),
