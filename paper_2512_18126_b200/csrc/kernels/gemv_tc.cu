@@ -13,6 +13,7 @@
 // RoPE / gate-up partners are adjacent weight rows = adjacent lanes.
 #include <cstdio>
 #include <cstdlib>
+#include <set>
 
 #include "kernels.cuh"
 #include "tc_common.cuh"
@@ -46,23 +47,24 @@ struct EpiPre {
 // compiler sinks them to their use in the epilogue, putting the L2 round
 // trips back on the critical path (measured: 2.4 us of RoPE epilogue per 8B
 // QKV launch).
+template <int EPI, int NR>
 __device__ __forceinline__ void epi_preload(const GemvArgs& a, int n, int R, EpiPre& p) {
-  if (a.epi == kEpiResidual) {
+  if (EPI == kEpiResidual) {
 #pragma unroll
-    for (int r = 0; r < kN; ++r) {
+    for (int r = 0; r < NR; ++r) {
       if (r >= R) break;
       p.res[r] = n < a.N ? __ldcg(a.out + static_cast<long long>(r) * a.N + n) : 0.f;
     }
 #pragma unroll
-    for (int r = 0; r < kN; ++r) {
+    for (int r = 0; r < NR; ++r) {
       if (r >= R) break;
       asm volatile("" ::"f"(p.res[r]));
     }
-  } else if (a.epi == kEpiQkv) {
+  } else if (EPI == kEpiQkv) {
     const int hd = a.hd, half = hd / 2, qk_cols = (a.nh + a.nkv) * hd;
     const int e = (n % hd) / 2;
 #pragma unroll
-    for (int r = 0; r < kN; ++r) {
+    for (int r = 0; r < NR; ++r) {
       if (r >= R) break;
       const RowDesc rd = a.rows[r];
       p.kv[r] = rd.kv;
@@ -70,20 +72,21 @@ __device__ __forceinline__ void epi_preload(const GemvArgs& a, int n, int R, Epi
       p.cs[r] = n < qk_cols ? __ldg(a.rope + static_cast<long long>(rd.pos) * half + e) : make_float2(1.f, 0.f);
     }
 #pragma unroll
-    for (int r = 0; r < kN; ++r) {
+    for (int r = 0; r < NR; ++r) {
       if (r >= R) break;
       asm volatile("" ::"f"(p.cs[r].x), "f"(p.cs[r].y), "r"(p.kv[r]), "r"(p.pos[r]));
     }
   }
 }
 
+template <int EPI, int NR>
 __device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const float (&v)[16], const EpiPre& pre) {
   const int lane = threadIdx.x & 31;
-  if (a.epi == kEpiResidual && a.ssq_out) {
+  if (EPI == kEpiResidual && a.ssq_out) {
     // residual + per-16-column sums of squares of the new rows (the next
     // RMSNorm's statistics; 16 consecutive lanes = 16 consecutive columns)
 #pragma unroll
-    for (int r = 0; r < kN; ++r) {
+    for (int r = 0; r < NR; ++r) {
       if (r >= R) break;
       float nv = 0.f;
       if (n < a.N) {
@@ -101,12 +104,12 @@ __device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const 
     return;
   }
 #pragma unroll
-  for (int r = 0; r < kN; ++r) {
+  for (int r = 0; r < NR; ++r) {
     if (r >= R) break;  // R is CTA-uniform
     const float x = v[r];
     const float partner = __shfl_xor_sync(0xffffffffu, x, 1);  // weight row n ^ 1
     if (n >= a.N) continue;
-    switch (a.epi) {
+    switch (EPI) {
       case kEpiF32:
         a.out[static_cast<long long>(r) * a.N + n] = x;
         break;
@@ -233,6 +236,7 @@ __device__ void lm_stats_epilogue(const GemvArgs& a, int n, int R, const float (
   if (threadIdx.x == 0) *a.lm_cnt = 0;
 }
 
+template <int EPI, int NR>
 __global__ void __launch_bounds__(128)
 gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, const GemvArgs a,
                int S, float* __restrict__ ws, int* __restrict__ cnt) {
@@ -280,7 +284,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     mbar_fence_init();
   }
   __shared__ unsigned long long cst[kChainPhases];
-  const unsigned stag = (5u << 16) | (static_cast<unsigned>(a.epi) << 12) | ((a.K >> 4) & 0xfff);
+  const unsigned stag = (5u << 16) | (static_cast<unsigned>(EPI) << 12) | ((a.K >> 4) & 0xfff);
   if (threadIdx.x == 0) {
     chain_reset(cst);
     chain_mark(cst, 0);
@@ -350,7 +354,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   const int per = kM / S;
   const int n_epi = S == 1 ? m0 + row : (row < per ? m0 + split * per + row : a.N);
   EpiPre pre;
-  if (a.epi != kEpiLmStats) epi_preload(a, n_epi, R, pre);
+  if (EPI != kEpiLmStats) epi_preload<EPI, NR>(a, n_epi, R, pre);
   if (scaled && warp >= 2) {
     // warps 2-3 (idle while the weights stream): each live row's inverse RMS,
     // from the producers' sums of squares (one float4 per thread per row, in a
@@ -358,13 +362,13 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     const int t = threadIdx.x - 64;
     if (a.ssq) {
       const int g4 = a.K / 64;  // float4 groups of 16-column partials per row (K <= 4096: <= 64)
-      float4 b[kN];
+      float4 b[NR];
 #pragma unroll
-      for (int r = 0; r < kN; ++r)
+      for (int r = 0; r < NR; ++r)
         b[r] = (r < R && t < g4) ? __ldcg(reinterpret_cast<const float4*>(a.ssq + static_cast<long long>(r) * (a.K / 16)) + t)
                                  : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int r = 0; r < kN; ++r) {
+      for (int r = 0; r < NR; ++r) {
         if (r >= R) break;
         float v = (b[r].x + b[r].y) + (b[r].z + b[r].w);
 #pragma unroll
@@ -390,14 +394,14 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   auto scale_rows = [&](float (&u)[16]) {
     if (!scaled) return;
 #pragma unroll
-    for (int r = 0; r < kN; ++r) u[r] *= inv_s[r];
+    for (int r = 0; r < NR; ++r) u[r] *= inv_s[r];
   };
-  if (a.epi == kEpiLmStats) {
+  if (EPI == kEpiLmStats) {
     scale_rows(v);
     lm_stats_epilogue(a, n, R, v, tile, gridDim.x);  // S == 1 for the LM head
   } else if (S == 1) {
     scale_rows(v);
-    epilogue(a, n, R, v, pre);
+    epilogue<EPI, NR>(a, n, R, v, pre);
   } else {
     // Split-K inside a thread-block cluster (the S CTAs of this weight tile):
     // CTA q reduces weight rows [q*128/S, (q+1)*128/S).  Every CTA pushes the
@@ -439,7 +443,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
         }
       if (threadIdx.x == 0) chain_mark(cst, 6);
       scale_rows(v);
-      epilogue(a, mine ? m0 + wr : a.N, R, v, pre);
+      epilogue<EPI, NR>(a, mine ? m0 + wr : a.N, R, v, pre);
     }
   }
   if (threadIdx.x == 0) chain_mark(cst, 7);  // this thread's epilogue done
@@ -846,12 +850,30 @@ bool gemv_tc_supported(const GemvArgs& a) {
   return a.R <= kN && a.K % kBK == 0 && a.N % 2 == 0 && static_cast<long long>(a.N) * a.K >= (2LL << 20);
 }
 
+// One kernel per (epilogue, row bucket): the epilogue and its per-row loops
+// are compiled for the bucket's row count only, so each launch runs a small,
+// branch-free instruction stream (the generic kernel's qkv epilogue took
+// ~1.3 us longer than the residual one at the same work, in every launch).
+template <int EPI>
+static void (*gemv_tc_pick(int R))(CUtensorMap, CUtensorMap, GemvArgs, int, float*, int*) {
+  if (R <= 4) return gemv_tc_kernel<EPI, 4>;
+  if (R <= 8) return gemv_tc_kernel<EPI, 8>;
+  return gemv_tc_kernel<EPI, 16>;
+}
+
 void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float* ws, int* cnt, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    uniform_carveout(reinterpret_cast<const void*>(gemv_tc_kernel));
-    attr = true;
+  void (*kern)(CUtensorMap, CUtensorMap, GemvArgs, int, float*, int*) = nullptr;
+  switch (a.epi) {
+    case kEpiF32: kern = gemv_tc_pick<kEpiF32>(a.R); break;
+    case kEpiResidual: kern = gemv_tc_pick<kEpiResidual>(a.R); break;
+    case kEpiSwiGlu: kern = gemv_tc_pick<kEpiSwiGlu>(a.R); break;
+    case kEpiQkv: kern = gemv_tc_pick<kEpiQkv>(a.R); break;
+    default: kern = gemv_tc_pick<kEpiLmStats>(a.R); break;
+  }
+  static std::set<const void*> attr;
+  if (attr.insert(reinterpret_cast<const void*>(kern)).second) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    uniform_carveout(reinterpret_cast<const void*>(kern));
   }
   const int S = gemv_tc_splits(a.N, a.K, a.epi);
   cudaLaunchConfig_t cfg{};
@@ -875,7 +897,7 @@ void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float*
   }
   cfg.attrs = attrs;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, gemv_tc_kernel, *reinterpret_cast<const CUtensorMap*>(&map_w),
+  cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(&map_w),
                      *reinterpret_cast<const CUtensorMap*>(&map_x), a, S, ws, cnt);
 }
 
