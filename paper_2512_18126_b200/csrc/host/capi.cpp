@@ -1120,12 +1120,13 @@ int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, 
     a.K = K;
     a.epi = moa::k::kEpiF32;
     a.out = reinterpret_cast<float*>(out);
-    if (R <= 0 || R > moa::k::kGemvTcRows || K % 64 || N % 2)
-      throw moa::ValidationError("gemv_tc: needs 1 <= R <= 16, K % 64 == 0, even N");
+    if (R <= 0 || R > moa::k::kGemvTcWideRows || K % 64 || N % 2)
+      throw moa::ValidationError("gemv_tc: needs 1 <= R <= 32, K % 64 == 0, even N");
+    // A holds 16 rows (R <= 16) or 32 (the wide variant), the activation tile's box
+    const int arows = R > moa::k::kGemvTcRows ? moa::k::kGemvTcWideRows : moa::k::kGemvTcRows;
     moa::k::TmaMap mw, mx;
     if (!moa::k::make_tmap_bf16(&mw, reinterpret_cast<const moa::k::bf16*>(W), N, K, 128) ||
-        !moa::k::make_tmap_bf16(&mx, reinterpret_cast<const moa::k::bf16*>(A), moa::k::kGemvTcRows, K,
-                                moa::k::kGemvTcRows))
+        !moa::k::make_tmap_bf16(&mx, reinterpret_cast<const moa::k::bf16*>(A), arows, K, arows))
       throw moa::DeviceError("gemv_tc: cuTensorMapEncodeTiled failed");
     static float* ws = nullptr;
     static int* cnt = nullptr;

@@ -162,7 +162,10 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
            k::make_tmap_bf16(&map_h_ffn_, h_, max_rows, s.ffn, 128) &&
            k::make_tmap_bf16(&map_hn16_, hn_, max_rows, D, k::kGemvTcRows) &&
            k::make_tmap_bf16(&map_h_attn16_, h_, max_rows, static_cast<long long>(s.n_heads) * hd, k::kGemvTcRows) &&
-           k::make_tmap_bf16(&map_h_ffn16_, h_, max_rows, s.ffn, k::kGemvTcRows);
+           k::make_tmap_bf16(&map_h_ffn16_, h_, max_rows, s.ffn, k::kGemvTcRows) &&
+           k::make_tmap_bf16(&map_hn32_, hn_, max_rows, D, k::kGemvTcWideRows) &&
+           k::make_tmap_bf16(&map_h_attn32_, h_, max_rows, static_cast<long long>(s.n_heads) * hd, k::kGemvTcWideRows) &&
+           k::make_tmap_bf16(&map_h_ffn32_, h_, max_rows, s.ffn, k::kGemvTcWideRows);
   long long ws = 0;
   for (auto [n, kk] : {std::pair<int, int>{s.qkv_cols(), s.d}, {s.d, s.n_heads * s.head_dim}, {2 * s.ffn, s.d},
                        {s.d, s.ffn}})
@@ -205,7 +208,7 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   if (const char* e = std::getenv("MOA_QKV_ATTN")) use_qkv_attn_ = std::string(e) != "0";
   if (const char* e = std::getenv("MOA_PREFILL_ATTN")) use_prefill_attn_ = std::string(e) != "0";
   // RMSNorm folded into the decode GEMVs: ssq partials [16 rows][d/16]
-  dev_alloc(&ssq_, static_cast<long long>(k::kGemvTcRows) * (D / 16));
+  dev_alloc(&ssq_, static_cast<long long>(k::kGemvTcWideRows) * (D / 16));
   dev_alloc(&inv_, static_cast<long long>(max_rows));
   {
     k::GemvArgs q1, g1, o1, d1;
@@ -375,7 +378,10 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   // tensor-core path for row buckets >= kTcMinRows (prefill-heavy ticks)
   const bool tc = use_tc_ && tc_ok_ && rcap >= k::kTcMinRows;
   // decode ticks of large models: swap-AB tensor-core GEMV (pure weight stream)
-  const bool swap_ab = use_tc_ && tc_ok_ && rcap <= k::kGemvTcRows;
+  // (17..32 rows -- incremental-prefill chunks: its wide, N = 32 variant)
+  const bool swap_ab = use_tc_ && tc_ok_ && rcap <= k::kGemvTcWideRows;
+  const bool wide = rcap > k::kGemvTcRows;
+  auto xmap = [&](const k::TmaMap& m16, const k::TmaMap& m32) { return wide ? &m32 : &m16; };
   // decode ticks: RMSNorm folded into the swap-AB GEMV when every normed
   // GEMV of the model qualifies (the residual producers then write ssq)
   const bool norm_fold = swap_ab && nfold_ok_ && use_nfold_;
@@ -390,7 +396,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       g.X = nullptr;
       g.A = hn_;
       g.ssq = ssq_;
-      k::gemv_tc(map_w, map_hn16_, g, gv_ws_, gv_cnt_, st);
+      k::gemv_tc(map_w, *xmap(map_hn16_, map_hn32_), g, gv_ws_, gv_cnt_, st);
       return;
     }
     if (g.X) {  // prep launch: bf16(x) and the rows' inverse RMS, then TMA-load the operand
@@ -399,7 +405,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       g.A = hn_;
       g.inv = inv_;
       map_a = &map_hn_;
-      map_a16 = &map_hn16_;
+      map_a16 = xmap(map_hn16_, map_hn32_);
     }
     if (dec_tc)
       k::gemv_tc(map_w, *map_a16, g, gv_ws_, gv_cnt_, st);
@@ -511,7 +517,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     if (norm_fold) o.ssq_out = ssq_, o.xb_out = hn_;
     probe_begin(gkind(KernelProbes::OProj, KernelProbes::PfOProj), 2.0 * o.N * o.K + 2.0 * Rv * o.K + 8.0 * Rv * D,
                 2.0 * Rv * o.N * o.K);
-    run_gemm(o, &map_h_attn_, &map_h_attn16_, wmaps_[static_cast<std::size_t>(l)].wo);
+    run_gemm(o, &map_h_attn_, xmap(map_h_attn16_, map_h_attn32_), wmaps_[static_cast<std::size_t>(l)].wo);
     probe_end();
     }
     // a = silu(gate) * up over rmsnorm(x)
@@ -543,7 +549,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     if (norm_fold) dn.ssq_out = ssq_, dn.xb_out = hn_;
     probe_begin(gkind(KernelProbes::Down, KernelProbes::PfDown), 2.0 * dn.N * dn.K + 2.0 * Rv * dn.K + 8.0 * Rv * D,
                 2.0 * Rv * dn.N * dn.K);
-    run_gemm(dn, &map_h_ffn_, &map_h_ffn16_, wmaps_[static_cast<std::size_t>(l)].wd);
+    run_gemm(dn, &map_h_ffn_, xmap(map_h_ffn16_, map_h_ffn32_), wmaps_[static_cast<std::size_t>(l)].wd);
     probe_end();
   }
   if (with_logits) {

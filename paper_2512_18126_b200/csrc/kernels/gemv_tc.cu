@@ -32,6 +32,16 @@ constexpr int kTileW = kM * kBK * 2;  // 16 KB
 constexpr int kTileX = kN * kBK * 2;  // 2 KB
 constexpr int kSmem = kStages * (kTileW + kTileX) + 1024 + 256;
 constexpr std::uint32_t kIdesc = idesc_bf16(kM, kN);
+// Wide variant for ticks of 17..32 rows (incremental-prefill chunks): the
+// same weight stream against a 32-row activation tile (MMA N = 32), a 4-stage
+// ring so two CTAs still fit an SM next to the 16 KB split-K landing buffer.
+template <int NC>
+struct GvCfg {
+  static constexpr int stages = NC == 16 ? kStages : 4;
+  static constexpr int tile_x = NC * kBK * 2;
+  static constexpr int smem = stages * (kTileW + tile_x) + 1024 + 256;
+  static constexpr std::uint32_t idesc = idesc_bf16(kM, NC);
+};
 
 // Operands of the epilogue that do not depend on the MMA, loaded while the
 // weights stream: the residual rows x[r][n] (final once the previous kernel
@@ -48,16 +58,17 @@ struct EpiPre {
 // trips back on the critical path (measured: 2.4 us of RoPE epilogue per 8B
 // QKV launch).
 template <int EPI, int NR>
-__device__ __forceinline__ void epi_preload(const GemvArgs& a, int n, int R, EpiPre& p) {
+__device__ __forceinline__ void epi_preload(const GemvArgs& a, int n, int R, EpiPre& p, int rb = 0) {
+  // rows rb .. rb + NR - 1 (NR <= 16) of the tick
   if (EPI == kEpiResidual) {
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      if (r >= R) break;
-      p.res[r] = n < a.N ? __ldcg(a.out + static_cast<long long>(r) * a.N + n) : 0.f;
+      if (rb + r >= R) break;
+      p.res[r] = n < a.N ? __ldcg(a.out + static_cast<long long>(rb + r) * a.N + n) : 0.f;
     }
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      if (r >= R) break;
+      if (rb + r >= R) break;
       asm volatile("" ::"f"(p.res[r]));
     }
   } else if (EPI == kEpiQkv) {
@@ -65,60 +76,61 @@ __device__ __forceinline__ void epi_preload(const GemvArgs& a, int n, int R, Epi
     const int e = (n % hd) / 2;
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      if (r >= R) break;
-      const RowDesc rd = a.rows[r];
+      if (rb + r >= R) break;
+      const RowDesc rd = a.rows[rb + r];
       p.kv[r] = rd.kv;
       p.pos[r] = rd.pos;
       p.cs[r] = n < qk_cols ? __ldg(a.rope + static_cast<long long>(rd.pos) * half + e) : make_float2(1.f, 0.f);
     }
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      if (r >= R) break;
+      if (rb + r >= R) break;
       asm volatile("" ::"f"(p.cs[r].x), "f"(p.cs[r].y), "r"(p.kv[r]), "r"(p.pos[r]));
     }
   }
 }
 
 template <int EPI, int NR>
-__device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const float (&v)[16], const EpiPre& pre) {
+__device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const float (&v)[16], const EpiPre& pre, int rb = 0) {
+  // v[r], pre.*[r]: row rb + r of the tick
   const int lane = threadIdx.x & 31;
   if (EPI == kEpiResidual && a.ssq_out) {
     // residual + per-16-column sums of squares of the new rows (the next
     // RMSNorm's statistics; 16 consecutive lanes = 16 consecutive columns)
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      if (r >= R) break;
+      if (rb + r >= R) break;
       float nv = 0.f;
       if (n < a.N) {
         nv = pre.res[r] + v[r];
-        a.out[static_cast<long long>(r) * a.N + n] = nv;
-        if (a.xb_out) a.xb_out[static_cast<long long>(r) * a.N + n] = __float2bfloat16_rn(nv);  // next GEMV's operand
+        a.out[static_cast<long long>(rb + r) * a.N + n] = nv;
+        if (a.xb_out) a.xb_out[static_cast<long long>(rb + r) * a.N + n] = __float2bfloat16_rn(nv);  // next GEMV's operand
       }
       float sq = nv * nv;
       sq += __shfl_xor_sync(0xffffffffu, sq, 1);
       sq += __shfl_xor_sync(0xffffffffu, sq, 2);
       sq += __shfl_xor_sync(0xffffffffu, sq, 4);
       sq += __shfl_xor_sync(0xffffffffu, sq, 8);
-      if ((lane & 15) == 0 && n < a.N) a.ssq_out[static_cast<long long>(r) * (a.N / 16) + n / 16] = sq;
+      if ((lane & 15) == 0 && n < a.N) a.ssq_out[static_cast<long long>(rb + r) * (a.N / 16) + n / 16] = sq;
     }
     return;
   }
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
-    if (r >= R) break;  // R is CTA-uniform
+    if (rb + r >= R) break;  // R is CTA-uniform
     const float x = v[r];
     const float partner = __shfl_xor_sync(0xffffffffu, x, 1);  // weight row n ^ 1
     if (n >= a.N) continue;
     switch (EPI) {
       case kEpiF32:
-        a.out[static_cast<long long>(r) * a.N + n] = x;
+        a.out[static_cast<long long>(rb + r) * a.N + n] = x;
         break;
       case kEpiResidual:
-        a.out[static_cast<long long>(r) * a.N + n] = pre.res[r] + x;
+        a.out[static_cast<long long>(rb + r) * a.N + n] = pre.res[r] + x;
         break;
       case kEpiSwiGlu:
         if (!(n & 1))
-          a.out_bf16[static_cast<long long>(r) * (a.N / 2) + n / 2] = __float2bfloat16_rn(x / (1.0f + __expf(-x)) * partner);
+          a.out_bf16[static_cast<long long>(rb + r) * (a.N / 2) + n / 2] = __float2bfloat16_rn(x / (1.0f + __expf(-x)) * partner);
         break;
       case kEpiQkv: {
         const RowDesc rd{pre.kv[r], pre.pos[r], 0, 0};
@@ -129,7 +141,7 @@ __device__ __forceinline__ void epilogue(const GemvArgs& a, int n, int R, const 
           const float2 cs = pre.cs[r];
           const float y0 = __fsub_rn(__fmul_rn(x, cs.x), __fmul_rn(partner, cs.y));
           const float y1 = __fadd_rn(__fmul_rn(partner, cs.x), __fmul_rn(x, cs.y));
-          bf16* dst = head < a.nh ? a.out_bf16 + (static_cast<long long>(r) * a.nh + head) * hd
+          bf16* dst = head < a.nh ? a.out_bf16 + (static_cast<long long>(rb + r) * a.nh + head) * hd
                                   : a.kpool + rd.kv * a.kv_stride + a.layer_off +
                                         (static_cast<long long>(head - a.nh) * a.max_ctx + rd.pos) * hd;
           dst[e] = __float2bfloat16_rn(y0);
@@ -236,7 +248,7 @@ __device__ void lm_stats_epilogue(const GemvArgs& a, int n, int R, const float (
   if (threadIdx.x == 0) *a.lm_cnt = 0;
 }
 
-template <int EPI, int NR>
+template <int EPI, int NR, int NC>
 __global__ void __launch_bounds__(128)
 gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, const GemvArgs a,
                int S, float* __restrict__ ws, int* __restrict__ cnt) {
@@ -248,18 +260,19 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   // from the producers' 16-column sums of squares (a.ssq) or a prep kernel
   // (a.inv), computed while the weights stream and applied in the epilogue.
   const bool scaled = a.ssq != nullptr || a.inv != nullptr;
-  constexpr int stages = kStages;
+  using G = GvCfg<NC>;
+  constexpr int stages = G::stages, kTileX = G::tile_x;
   unsigned char* sw = smem;
   unsigned char* sx = smem + stages * kTileW;  // per-stage X tiles
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sx + kStages * kTileX);
-  std::uint64_t* empty = full + kStages;
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sx + stages * kTileX);
+  std::uint64_t* empty = full + stages;
   std::uint64_t* done = empty + kStages;
   std::uint64_t* inv_bar = done + 1;
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(inv_bar + 1);
-  __shared__ float inv_s[kN];
-  __shared__ float inv_red[2][kN];
-  // split-K landing buffer: [src rank][row of this CTA's 128/S slice][16] fp32
-  __shared__ __align__(16) float land[kM * kN];
+  __shared__ float inv_s[NC];
+  __shared__ float inv_red[2][NC];
+  // split-K landing buffer: [src rank][row of this CTA's 128/S slice][NC] fp32
+  __shared__ __align__(16) float land[kM * NC];
   __shared__ __align__(8) std::uint64_t land_bar;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -279,7 +292,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     mbar_init(inv_bar, 1);
     if (S > 1) {
       mbar_init(&land_bar, 1);
-      mbar_expect_tx(&land_bar, kM * kN * 4);  // every rank's slice of this CTA's rows (128/S x 16 x S)
+      mbar_expect_tx(&land_bar, kM * NC * 4);  // every rank's slice of this CTA's rows (128/S x 16 x S)
     }
     mbar_fence_init();
   }
@@ -341,7 +354,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
       tc_fence_after();
       const std::uint32_t w0 = smem_u32(sw + s * kTileW), x0 = smem_u32(sx + s * kTileX);
 #pragma unroll
-      for (int k = 0; k < kBK / 16; ++k) umma_bf16(tmem, umma_desc(w0 + k * 32), umma_desc(x0 + k * 32), kIdesc, (kt | k) ? 1u : 0u);
+      for (int k = 0; k < kBK / 16; ++k) umma_bf16(tmem, umma_desc(w0 + k * 32), umma_desc(x0 + k * 32), G::idesc, (kt | k) ? 1u : 0u);
       umma_commit(&empty[s]);
     }
     umma_commit(done);
@@ -354,7 +367,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   const int per = kM / S;
   const int n_epi = S == 1 ? m0 + row : (row < per ? m0 + split * per + row : a.N);
   EpiPre pre;
-  if (EPI != kEpiLmStats) epi_preload<EPI, NR>(a, n_epi, R, pre);
+  if (EPI != kEpiLmStats) epi_preload<EPI, NR < 16 ? NR : 16>(a, n_epi, R, pre);
   if (scaled && warp >= 2) {
     // warps 2-3 (idle while the weights stream): each live row's inverse RMS,
     // from the producers' sums of squares (one float4 per thread per row, in a
@@ -362,22 +375,27 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     const int t = threadIdx.x - 64;
     if (a.ssq) {
       const int g4 = a.K / 64;  // float4 groups of 16-column partials per row (K <= 4096: <= 64)
-      float4 b[NR];
 #pragma unroll
-      for (int r = 0; r < NR; ++r)
-        b[r] = (r < R && t < g4) ? __ldcg(reinterpret_cast<const float4*>(a.ssq + static_cast<long long>(r) * (a.K / 16)) + t)
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int r0 = 0; r0 < NR; r0 += 16) {  // batches of <= 16 rows: all loads of a batch in flight
+        constexpr int NB = NR < 16 ? NR : 16;
+        float4 b[NB];
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        if (r >= R) break;
-        float v = (b[r].x + b[r].y) + (b[r].z + b[r].w);
+        for (int r = 0; r < NB; ++r)
+          b[r] = (r0 + r < R && t < g4)
+                     ? __ldcg(reinterpret_cast<const float4*>(a.ssq + static_cast<long long>(r0 + r) * (a.K / 16)) + t)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) inv_red[warp - 2][r] = v;
+        for (int r = 0; r < NB; ++r) {
+          if (r0 + r >= R) break;
+          float v = (b[r].x + b[r].y) + (b[r].z + b[r].w);
+#pragma unroll
+          for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == 0) inv_red[warp - 2][r0 + r] = v;
+        }
       }
       asm volatile("bar.sync 2, 64;" ::: "memory");
-      if (t < kN) inv_s[t] = t < R ? 1.0f / sqrtf((inv_red[0][t] + inv_red[1][t]) / static_cast<float>(a.K) + a.eps) : 0.f;
-    } else if (t < kN) {
+      if (t < NC) inv_s[t] = t < R ? 1.0f / sqrtf((inv_red[0][t] + inv_red[1][t]) / static_cast<float>(a.K) + a.eps) : 0.f;
+    } else if (t < NC) {
       inv_s[t] = t < R ? __ldcg(a.inv + t) : 0.f;
     }
     asm volatile("bar.sync 2, 64;" ::: "memory");
@@ -388,20 +406,38 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   if (threadIdx.x == 64) chain_mark(cst, 3);
 
   const int n = m0 + row;
-  float v[16];
-  tmem_ld16(tmem + (static_cast<std::uint32_t>(warp * 32) << 16), v);
+  constexpr int NH = NC / 16;  // 16-column halves of the accumulator
+  float v[NH][16];
+#pragma unroll
+  for (int h = 0; h < NH; ++h) tmem_ld16(tmem + (static_cast<std::uint32_t>(warp * 32) << 16) + 16 * h, v[h]);
   if (scaled) mbar_wait(inv_bar, 0);
-  auto scale_rows = [&](float (&u)[16]) {
+  auto scale_rows = [&](float (&u)[16], int rb) {
     if (!scaled) return;
 #pragma unroll
-    for (int r = 0; r < NR; ++r) u[r] *= inv_s[r];
+    for (int r = 0; r < 16; ++r) u[r] *= inv_s[rb + r];
   };
-  if (EPI == kEpiLmStats) {
-    scale_rows(v);
-    lm_stats_epilogue(a, n, R, v, tile, gridDim.x);  // S == 1 for the LM head
+  // rows of the second half: their epilogue operands are loaded now (the
+  // first half's were preloaded while the weights streamed)
+  auto run_epilogue = [&](int n_row) {
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      if (16 * h >= R) break;
+      scale_rows(v[h], 16 * h);
+      if (h == 0) {
+        epilogue<EPI, NR < 16 ? NR : 16>(a, n_row, R, v[0], pre, 0);
+      } else {
+        EpiPre pre1;
+        epi_preload<EPI, 16>(a, n_row, R, pre1, 16);
+        epilogue<EPI, 16>(a, n_row, R, v[h], pre1, 16);
+      }
+    }
+  };
+  if constexpr (EPI == kEpiLmStats) {
+    static_assert(NC == 16, "LM statistics: 16 rows");
+    scale_rows(v[0], 0);
+    lm_stats_epilogue(a, n, R, v[0], tile, gridDim.x);  // S == 1 for the LM head
   } else if (S == 1) {
-    scale_rows(v);
-    epilogue<EPI, NR>(a, n, R, v, pre);
+    run_epilogue(n);
   } else {
     // Split-K inside a thread-block cluster (the S CTAs of this weight tile):
     // CTA q reduces weight rows [q*128/S, (q+1)*128/S).  Every CTA pushes the
@@ -413,14 +449,17 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     const int q = row / per, rq = row % per;
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every landing barrier is initialised
     {
-      const std::uint32_t dst = dsmem_addr(smem_u32(land + (split * per + rq) * kN), q);
+      const std::uint32_t dst = dsmem_addr(smem_u32(land + (split * per + rq) * NC), q);
       const std::uint32_t bar = dsmem_addr(smem_u32(&land_bar), q);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        asm volatile(
-            "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst + 16 * i),
-            "f"(v[4 * i]), "f"(v[4 * i + 1]), "f"(v[4 * i + 2]), "f"(v[4 * i + 3]), "r"(bar)
-            : "memory");
+      for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          asm volatile(
+              "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                  dst + 64 * h + 16 * i),
+              "f"(v[h][4 * i]), "f"(v[h][4 * i + 1]), "f"(v[h][4 * i + 2]), "f"(v[h][4 * i + 3]), "r"(bar)
+              : "memory");
     }
     if (threadIdx.x == 0) chain_mark(cst, 5);
     if (warp * 32 < per) {  // warps holding at least one reduced row (whole warps: the epilogue shuffles)
@@ -428,22 +467,25 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
       const bool mine = row < per;
       const int wr = split * per + (mine ? row : 0);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[h][i] = 0.f;
       if (mine)
         for (int src = 0; src < S; ++src) {
-          const float4* p = reinterpret_cast<const float4*>(land + (src * per + row) * kN);
+          const float4* p = reinterpret_cast<const float4*>(land + (src * per + row) * NC);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float4 t = p[i];
-            v[4 * i] += t.x;
-            v[4 * i + 1] += t.y;
-            v[4 * i + 2] += t.z;
-            v[4 * i + 3] += t.w;
-          }
+          for (int h = 0; h < NH; ++h)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float4 t = p[4 * h + i];
+              v[h][4 * i] += t.x;
+              v[h][4 * i + 1] += t.y;
+              v[h][4 * i + 2] += t.z;
+              v[h][4 * i + 3] += t.w;
+            }
         }
       if (threadIdx.x == 0) chain_mark(cst, 6);
-      scale_rows(v);
-      epilogue<EPI, NR>(a, mine ? m0 + wr : a.N, R, v, pre);
+      run_epilogue(mine ? m0 + wr : a.N);
     }
   }
   if (threadIdx.x == 0) chain_mark(cst, 7);  // this thread's epilogue done
@@ -847,7 +889,8 @@ bool gemv_tc_norm_supported(const GemvArgs& a) {
 }
 
 bool gemv_tc_supported(const GemvArgs& a) {
-  return a.R <= kN && a.K % kBK == 0 && a.N % 2 == 0 && static_cast<long long>(a.N) * a.K >= (2LL << 20);
+  return a.R <= kGemvTcWideRows && (a.R <= kN || a.epi != kEpiLmStats) && a.K % kBK == 0 && a.N % 2 == 0 &&
+         static_cast<long long>(a.N) * a.K >= (2LL << 20);
 }
 
 // One kernel per (epilogue, row bucket): the epilogue and its per-row loops
@@ -856,9 +899,11 @@ bool gemv_tc_supported(const GemvArgs& a) {
 // ~1.3 us longer than the residual one at the same work, in every launch).
 template <int EPI>
 static void (*gemv_tc_pick(int R))(CUtensorMap, CUtensorMap, GemvArgs, int, float*, int*) {
-  if (R <= 4) return gemv_tc_kernel<EPI, 4>;
-  if (R <= 8) return gemv_tc_kernel<EPI, 8>;
-  return gemv_tc_kernel<EPI, 16>;
+  if (R <= 4) return gemv_tc_kernel<EPI, 4, 16>;
+  if (R <= 8) return gemv_tc_kernel<EPI, 8, 16>;
+  if (R <= 16 || EPI == kEpiLmStats) return gemv_tc_kernel<EPI, 16, 16>;
+  if constexpr (EPI != kEpiLmStats) return gemv_tc_kernel<EPI, 32, 32>;
+  return nullptr;
 }
 
 void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float* ws, int* cnt, cudaStream_t st) {
@@ -870,16 +915,17 @@ void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float*
     case kEpiQkv: kern = gemv_tc_pick<kEpiQkv>(a.R); break;
     default: kern = gemv_tc_pick<kEpiLmStats>(a.R); break;
   }
+  const int smem = a.R > kN ? GvCfg<32>::smem : GvCfg<16>::smem;
   static std::set<const void*> attr;
   if (attr.insert(reinterpret_cast<const void*>(kern)).second) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     uniform_carveout(reinterpret_cast<const void*>(kern));
   }
   const int S = gemv_tc_splits(a.N, a.K, a.epi);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((a.N + kM - 1) / kM, S);
   cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = kSmem;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
   int na = 0;

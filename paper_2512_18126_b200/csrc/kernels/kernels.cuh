@@ -144,6 +144,8 @@ constexpr int kTcMinRows = 17;  // ticks with more rows than the swap-AB GEMV ho
 // programmatic dependent launch: weight tiles stream before the previous
 // kernel has finished.
 constexpr int kGemvTcRows = 16;
+// ... and its wide variant (MMA N = 32) for ticks of 17..32 rows (incremental-prefill chunks)
+constexpr int kGemvTcWideRows = 32;
 bool gemv_tc_supported(const GemvArgs& a);
 // gemv_tc with X = fp32 residual rows normalised in-kernel (a.X, a.g, a.eps,
 // a.ssq): no separate rmsnorm launch

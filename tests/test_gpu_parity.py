@@ -109,12 +109,14 @@ def test_gemm_tc_vs_torch_fp32(torch_cuda, M, N, K):
 
 
 @pytest.mark.parametrize("R,N,K", [(1, 3072, 2048), (8, 16384, 2048), (16, 2048, 8192), (3, 50000, 2048),
-                                   (5, 6144, 4096)])
+                                   (5, 6144, 4096), (17, 3072, 2048), (24, 6144, 4096), (32, 4096, 14336),
+                                   (32, 28672, 4096)])
 def test_gemv_tc_vs_torch_fp32(torch_cuda, R, N, K):
-    """Swap-AB tensor-core decode GEMV (split-K, last-arriver epilogue)."""
+    """Swap-AB tensor-core decode GEMV (cluster split-K); 17..32 rows: its
+    wide (MMA N = 32) variant for incremental-prefill chunks."""
     torch = torch_cuda
     g = torch.Generator(device="cuda").manual_seed(R + N + K)
-    A = torch.randn(16, K, device="cuda", generator=g).to(torch.bfloat16)
+    A = torch.randn(16 if R <= 16 else 32, K, device="cuda", generator=g).to(torch.bfloat16)
     W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
     out = torch.full((R, N), float("nan"), device="cuda")
     for _ in range(2):  # second call re-uses the zeroed split counters
