@@ -1008,6 +1008,7 @@ int moa_k_attention(uintptr_t q, uintptr_t rows, int R, uintptr_t meta, int nh, 
     const bool pf_tc = (prefill & 8) != 0;    // bit 3 (with bit 0): the runs by the tcgen05 prefill kernel
     const bool runs_only = (prefill & 16) != 0;  // bit 4 (with bit 0): no per-row kernel (timing the runs)
     const int ns_req = (prefill >> 8) & 0xff;
+    const int ks_req = std::max(1, (prefill >> 16) & 0xff);  // bits 16-23: key splits of the tcgen05 prefill kernel
     prefill &= 1;
     if (prefill && pf_tc) {
       if (!moa::k::attention_prefill_tc_supported(nh, nkv, hd)) throw moa::ValidationError("attention: tcgen05 prefill shape");
@@ -1016,7 +1017,12 @@ int moa_k_attention(uintptr_t q, uintptr_t rows, int R, uintptr_t meta, int nh, 
       if (!moa::k::make_tmap_q3d(&qm, qp, R, nh, hd, nh / nkv) || !moa::k::make_tmap_bf16(&km, kp, pool_rows, hd, 64) ||
           !moa::k::make_tmap_bf16(&vm, vp, pool_rows, hd, 64))
         throw moa::DeviceError("attention: TMA map creation failed");
-      moa::k::attention_prefill_tc(qm, km, vm, rp, R, mp, nh, nkv, hd, kv_stride, 0, max_ctx, op, st);
+      static float* pws = nullptr;
+      if (ks_req > 1 && !pws) MOA_CUDA(cudaMalloc(&pws, sizeof(float) * moa::k::attention_prefill_tc_ws_floats(128)));
+      const int P = 128 / (nh / nkv);
+      if (ks_req > 8 || (R + P - 1) / P * nkv * ks_req > moa::k::kPfTcMaxCtas)
+        throw moa::ValidationError("attention: key splits exceed the workspace");
+      moa::k::attention_prefill_tc(qm, km, vm, rp, R, mp, nh, nkv, hd, kv_stride, 0, max_ctx, op, st, ks_req, pws);
     } else if (prefill) {
       moa::k::attention_prefill(qp, rp, R, mp, nh, nkv, hd, kp, vp, kv_stride, 0, max_ctx, op, st);
     }
@@ -1121,9 +1127,9 @@ int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, 
     a.epi = moa::k::kEpiF32;
     a.out = reinterpret_cast<float*>(out);
     if (R <= 0 || R > moa::k::kGemvTcWideRows || K % 64 || N % 2)
-      throw moa::ValidationError("gemv_tc: needs 1 <= R <= 32, K % 64 == 0, even N");
-    // A holds 16 rows (R <= 16) or 32 (the wide variant), the activation tile's box
-    const int arows = R > moa::k::kGemvTcRows ? moa::k::kGemvTcWideRows : moa::k::kGemvTcRows;
+      throw moa::ValidationError("gemv_tc: needs 1 <= R <= 64, K % 64 == 0, even N");
+    // A holds 16, 32 or 64 rows (R <= 16 / 32 / 64), the activation tile's box
+    const int arows = moa::k::gemv_tc_box_rows(R);
     moa::k::TmaMap mw, mx;
     if (!moa::k::make_tmap_bf16(&mw, reinterpret_cast<const moa::k::bf16*>(W), N, K, 128) ||
         !moa::k::make_tmap_bf16(&mx, reinterpret_cast<const moa::k::bf16*>(A), arows, K, arows))

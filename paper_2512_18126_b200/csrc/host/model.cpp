@@ -163,9 +163,12 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
            k::make_tmap_bf16(&map_hn16_, hn_, max_rows, D, k::kGemvTcRows) &&
            k::make_tmap_bf16(&map_h_attn16_, h_, max_rows, static_cast<long long>(s.n_heads) * hd, k::kGemvTcRows) &&
            k::make_tmap_bf16(&map_h_ffn16_, h_, max_rows, s.ffn, k::kGemvTcRows) &&
-           k::make_tmap_bf16(&map_hn32_, hn_, max_rows, D, k::kGemvTcWideRows) &&
-           k::make_tmap_bf16(&map_h_attn32_, h_, max_rows, static_cast<long long>(s.n_heads) * hd, k::kGemvTcWideRows) &&
-           k::make_tmap_bf16(&map_h_ffn32_, h_, max_rows, s.ffn, k::kGemvTcWideRows);
+           k::make_tmap_bf16(&map_hn32_, hn_, max_rows, D, k::kGemvTcMidRows) &&
+           k::make_tmap_bf16(&map_h_attn32_, h_, max_rows, static_cast<long long>(s.n_heads) * hd, k::kGemvTcMidRows) &&
+           k::make_tmap_bf16(&map_h_ffn32_, h_, max_rows, s.ffn, k::kGemvTcMidRows) &&
+           k::make_tmap_bf16(&map_hn64_, hn_, max_rows, D, k::kGemvTcWideRows) &&
+           k::make_tmap_bf16(&map_h_attn64_, h_, max_rows, static_cast<long long>(s.n_heads) * hd, k::kGemvTcWideRows) &&
+           k::make_tmap_bf16(&map_h_ffn64_, h_, max_rows, s.ffn, k::kGemvTcWideRows);
   long long ws = 0;
   for (auto [n, kk] : {std::pair<int, int>{s.qkv_cols(), s.d}, {s.d, s.n_heads * s.head_dim}, {2 * s.ffn, s.d},
                        {s.d, s.ffn}})
@@ -199,6 +202,9 @@ DeviceModel::DeviceModel(const ModelSpec& spec, int max_agents, int max_ctx, int
   pf_tc_ = kv_maps_ok_ && k::attention_prefill_tc_supported(s.n_heads, s.n_kv_heads, static_cast<int>(hd)) &&
            k::make_tmap_q3d(&qmap3_, q_, max_rows, s.n_heads, static_cast<int>(hd), s.n_heads / s.n_kv_heads);
   if (const char* e = std::getenv("MOA_PREFILL_TC")) pf_tc_ = pf_tc_ && e[0] != '0';
+  if (pf_tc_) {  // key-split partials of the prefill attention (chunk ticks)
+    dev_alloc(&pf_ws_, k::attention_prefill_tc_ws_floats(static_cast<int>(hd)));
+  }
   // default: the cluster-split kernel (MOA_DECODE_CLUSTER=0: the fixed-split TMA kernel)
   attn_cluster_ = kv_maps_ok_ && k::attention_decode_cluster_supported(s.n_heads, s.n_kv_heads, static_cast<int>(hd));
   if (const char* e = std::getenv("MOA_DECODE_CLUSTER")) attn_cluster_ = attn_cluster_ && e[0] != '0';
@@ -247,7 +253,7 @@ DeviceModel::~DeviceModel() {
                     static_cast<void*>(attn_cnt_), static_cast<void*>(part_), static_cast<void*>(lm_cnt_),
                     meta_blob_, run_area_, static_cast<void*>(hn_), static_cast<void*>(wo_blk_),
                     static_cast<void*>(gv_ws_), static_cast<void*>(gv_cnt_), static_cast<void*>(ssq_),
-                    static_cast<void*>(inv_)})
+                    static_cast<void*>(inv_), static_cast<void*>(pf_ws_)})
     if (ptr) cudaFree(ptr);
 }
 
@@ -378,10 +384,17 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   // tensor-core path for row buckets >= kTcMinRows (prefill-heavy ticks)
   const bool tc = use_tc_ && tc_ok_ && rcap >= k::kTcMinRows;
   // decode ticks of large models: swap-AB tensor-core GEMV (pure weight stream)
-  // (17..32 rows -- incremental-prefill chunks: its wide, N = 32 variant)
-  const bool swap_ab = use_tc_ && tc_ok_ && rcap <= k::kGemvTcWideRows;
-  const bool wide = rcap > k::kGemvTcRows;
-  auto xmap = [&](const k::TmaMap& m16, const k::TmaMap& m32) { return wide ? &m32 : &m16; };
+  // (17..64 rows -- incremental-prefill chunks: its wide, N = 32 / 64 variants;
+  // MOA_GEMV_MAX_ROWS caps the rows it takes, A/B against the 128-row GEMM tiles)
+  static const int gemv_max_rows = [] {
+    const char* e = std::getenv("MOA_GEMV_MAX_ROWS");
+    return e ? std::max(k::kGemvTcRows, std::min(k::kGemvTcWideRows, std::atoi(e))) : k::kGemvTcWideRows;
+  }();
+  const bool swap_ab = use_tc_ && tc_ok_ && rcap <= gemv_max_rows;
+  const int box = k::gemv_tc_box_rows(rcap);
+  auto xmap = [&](const k::TmaMap& m16, const k::TmaMap& m32, const k::TmaMap& m64) {
+    return box == k::kGemvTcRows ? &m16 : box == k::kGemvTcMidRows ? &m32 : &m64;
+  };
   // decode ticks: RMSNorm folded into the swap-AB GEMV when every normed
   // GEMV of the model qualifies (the residual producers then write ssq)
   const bool norm_fold = swap_ab && nfold_ok_ && use_nfold_;
@@ -396,7 +409,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       g.X = nullptr;
       g.A = hn_;
       g.ssq = ssq_;
-      k::gemv_tc(map_w, *xmap(map_hn16_, map_hn32_), g, gv_ws_, gv_cnt_, st);
+      k::gemv_tc(map_w, *xmap(map_hn16_, map_hn32_, map_hn64_), g, gv_ws_, gv_cnt_, st);
       return;
     }
     if (g.X) {  // prep launch: bf16(x) and the rows' inverse RMS, then TMA-load the operand
@@ -405,7 +418,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
       g.A = hn_;
       g.inv = inv_;
       map_a = &map_hn_;
-      map_a16 = xmap(map_hn16_, map_hn32_);
+      map_a16 = xmap(map_hn16_, map_hn32_, map_hn64_);
     }
     if (dec_tc)
       k::gemv_tc(map_w, *map_a16, g, gv_ws_, gv_cnt_, st);
@@ -427,6 +440,9 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
   // append + attention in one launch per layer
   const bool qkv_attn = use_tc_ && use_qkv_attn_ && qkv_attn_ok_ && distinct && rcap <= k::kGemvTcRows;
   const bool fuse_o = qkv_attn && wo_blk_ != nullptr;
+  // key splits of the tcgen05 prefill attention (chunk ticks: few row blocks);
+  // nsplit bounds the tick's 64-key blocks
+  const int pf_ks = pf_tc_ && pf_ws_ ? k::attention_prefill_tc_splits(rcap, nh, nkv, nsplit * split_keys_ / 64) : 1;
   if (!qkv_attn) {  // (the fused QKV + attention kernel gathers layer 0's embeddings itself)
   probe_begin(KernelProbes::Embed, 6.0 * live_R_ * D);
   k::embed(buf_.rows, rcap, meta, out_tok_read, emb_, D, x_, st, norm_fold ? ssq_ : nullptr, norm_fold ? hn_ : nullptr);
@@ -478,7 +494,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
                   4.0 * static_cast<double>(live_.run_pairs) * nh * hd);
       if (pf_tc_)
         k::attention_prefill_tc(qmap3_, kmap_, vmap_, buf_.rows, rcap, meta, nh, nkv, hd, kv_stride_, loff, max_ctx_,
-                                h_, st);
+                                h_, st, pf_ks, pf_ws_);
       else
         k::attention_prefill(q_, buf_.rows, rcap, meta, nh, nkv, hd, kpool_, vpool_, kv_stride_, loff, max_ctx_, h_,
                              st);
@@ -517,7 +533,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     if (norm_fold) o.ssq_out = ssq_, o.xb_out = hn_;
     probe_begin(gkind(KernelProbes::OProj, KernelProbes::PfOProj), 2.0 * o.N * o.K + 2.0 * Rv * o.K + 8.0 * Rv * D,
                 2.0 * Rv * o.N * o.K);
-    run_gemm(o, &map_h_attn_, xmap(map_h_attn16_, map_h_attn32_), wmaps_[static_cast<std::size_t>(l)].wo);
+    run_gemm(o, &map_h_attn_, xmap(map_h_attn16_, map_h_attn32_, map_h_attn64_), wmaps_[static_cast<std::size_t>(l)].wo);
     probe_end();
     }
     // a = silu(gate) * up over rmsnorm(x)
@@ -549,7 +565,7 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     if (norm_fold) dn.ssq_out = ssq_, dn.xb_out = hn_;
     probe_begin(gkind(KernelProbes::Down, KernelProbes::PfDown), 2.0 * dn.N * dn.K + 2.0 * Rv * dn.K + 8.0 * Rv * D,
                 2.0 * Rv * dn.N * dn.K);
-    run_gemm(dn, &map_h_ffn_, xmap(map_h_ffn16_, map_h_ffn32_), wmaps_[static_cast<std::size_t>(l)].wd);
+    run_gemm(dn, &map_h_ffn_, xmap(map_h_ffn16_, map_h_ffn32_, map_h_ffn64_), wmaps_[static_cast<std::size_t>(l)].wd);
     probe_end();
   }
   if (with_logits) {

@@ -165,7 +165,9 @@ class DeviceModel {
   int split_keys_ = 512;   // keys per attention CTA (sizes the graphs' split buckets)
   k::TmaMap map_hn_, map_h_attn_, map_h_ffn_;        // A operands, 128-row boxes (prefill)
   k::TmaMap map_hn16_, map_h_attn16_, map_h_ffn16_;  // 16-row boxes (decode, swap-AB)
-  k::TmaMap map_hn32_, map_h_attn32_, map_h_ffn32_;  // 32-row boxes (its wide variant)
+  k::TmaMap map_hn32_, map_h_attn32_, map_h_ffn32_;  // 32-row boxes (its wide variants)
+  k::TmaMap map_hn64_, map_h_attn64_, map_h_ffn64_;  // 64-row boxes
+  float* pf_ws_ = nullptr;  // key-split partials of the tcgen05 prefill attention
   float* gv_ws_ = nullptr;                           // gemv_tc split-K partials
   int* gv_cnt_ = nullptr;
   k::bf16* hn_ = nullptr;                      // normalised rows for the tensor-core path

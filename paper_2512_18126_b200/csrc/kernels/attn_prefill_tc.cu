@@ -18,6 +18,15 @@
 // per-row kernel; a row block spanning several agents' runs loops over the
 // runs, each run's K / V streamed once (rows of other runs see p = 0).
 //
+// Key splits (incremental-prefill chunks: a tick of a few 32-row runs is only
+// nkv x (rows / P) CTAs): grid.z = KS CTAs share a row block and form a
+// thread-block cluster, each streaming a contiguous slice of every run's key
+// blocks; each writes its rows' unnormalised O with the running reference m
+// and the sum l (fp32) to a workspace (L2), and after one cluster barrier CTA
+// s combines rows [s * 128 / KS, (s + 1) * 128 / KS) of the block from the KS
+// partials in split order (O = sum 2^(m_s - M) O_s, l likewise; deterministic
+// for a given tick shape).
+//
 // Algorithmic work per run of n rows ending at position p: causal
 // Q.K^T and P.V over keys [0, p]: 4 * hd * (sum over rows of (pos + 1)) flops
 // per q head; bytes: the run's keys once per kv head (K and V).
@@ -112,7 +121,7 @@ __global__ void __launch_bounds__(192, 1)
 attention_prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                             const __grid_constant__ CUtensorMap vmap, const RowDesc* __restrict__ rows,
                             const int* __restrict__ meta, int nh, int nkv, long long kv_stride, long long layer_off,
-                            int max_ctx, bf16* __restrict__ o) {
+                            int max_ctx, bf16* __restrict__ o, float* __restrict__ ws) {
   using C = PfTc<HD>;
   constexpr int STG = C::STG, SUB = C::SUB;
   extern __shared__ unsigned char pt_raw[];
@@ -130,11 +139,13 @@ attention_prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __gr
   __shared__ std::uint32_t tmem_slot;
   __shared__ RowDesc rd_s[128];
   __shared__ int seg_b[129], seg_e[128], seg_of[128];
-  __shared__ int nseg_s, nitems_s, nblk_s[128];
+  __shared__ int nseg_s, nitems_s, nblk_s[128], blk0_s[128];
   __shared__ unsigned long long cst[kChainPhases];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hpg = nh / nkv, P = 128 / hpg;
   const int b0 = blockIdx.x * P, g = blockIdx.y;
+  const int KS = gridDim.z, split = blockIdx.z;
+  const long long cl_blk = static_cast<long long>(blockIdx.x) * nkv + g;  // workspace slot of this row block
   const int live = __ldg(meta);
   if (b0 >= live) return;
   const int nb = min(P, live - b0);
@@ -163,7 +174,9 @@ attention_prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __gr
       seg_b[m] = a;
       seg_e[m] = b;
       for (int i = a; i < b; ++i) seg_of[i] = m;
-      nblk_s[m] = rd_s[b - 1].pos / C::KB + 1;  // keys [0, last position of the run]
+      const int tot = rd_s[b - 1].pos / C::KB + 1;  // keys [0, last position of the run]
+      blk0_s[m] = split * tot / KS;  // this split's slice of them
+      nblk_s[m] = (split + 1) * tot / KS - blk0_s[m];
       items += nblk_s[m];
       ++m;
     }
@@ -207,7 +220,7 @@ attention_prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __gr
         if (i >= STG) mbar_wait(&empty[st], ((i / STG) - 1) & 1);
         const RowDesc& r0 = rd_s[seg_b[sg]];
         const int row0 = static_cast<int>((r0.kv * kv_stride + layer_off) / HD + static_cast<long long>(g) * max_ctx) +
-                         j * C::KB;
+                         (blk0_s[sg] + j) * C::KB;
         mbar_expect_tx(&full[st], C::STAGE);
         unsigned char* kd = ring + st * C::STAGE;
 #pragma unroll
@@ -275,7 +288,7 @@ attention_prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __gr
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&s_free[sb]);
-      const int kb = j * C::KB;
+      const int kb = (blk0_s[sg] + j) * C::KB;
       const bool in = sg == my_seg;
       // causal mask only on blocks that reach past some row's position
       float mx = -INFINITY;
@@ -339,7 +352,33 @@ attention_prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __gr
       tc_fence_before();
       mbar_arrive(&p_full[i & 1]);
     }
-    if (nitems > 0) {
+    if (KS > 1) {
+      // key split: this row's partial (O relative to m, m, l) to the
+      // workspace; combined below, after the cluster barrier
+      float* wp = ws + ((cl_blk * KS + split) * 128 + row) * (HD + 4);
+      if (nitems > 0) {
+        mbar_wait(&o_done[(nitems - 1) & 1], ((nitems - 1) >> 1) & 1);
+        __syncwarp();
+        tc_fence_after();
+      }
+#pragma unroll
+      for (int c = 0; c < HD / 16; ++c) {
+        float ov[16];
+        if (nitems > 0) {
+          __syncwarp();
+          tmem_ld16_nw(tO + c * 16, ov);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) ov[k] = 0.f;
+        }
+        float4* d4 = reinterpret_cast<float4*>(wp + c * 16);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) __stcg(d4 + k, make_float4(ov[4 * k], ov[4 * k + 1], ov[4 * k + 2], ov[4 * k + 3]));
+      }
+      __stcg(reinterpret_cast<float4*>(wp + HD), make_float4(m, l, 0.f, 0.f));
+    }
+    if (KS == 1 && nitems > 0) {
       mbar_wait(&o_done[(nitems - 1) & 1], ((nitems - 1) >> 1) & 1);
       __syncwarp();
       tc_fence_after();
@@ -365,6 +404,49 @@ attention_prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __gr
   }
   tc_fence_before();
   __syncthreads();
+  if (KS > 1) {
+    // The KS CTAs of this row block form a cluster: once every partial is
+    // written, CTA s combines rows [s * 128 / KS, (s + 1) * 128 / KS) of the
+    // block, one float4 of a row's output per thread-item, summing the
+    // partials in split order.
+    __threadfence();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    const int per = 128 / KS;
+    const long long sstr = 128LL * (HD + 4);
+    const float* base = ws + cl_blk * KS * sstr;
+    for (int it = threadIdx.x; it < per * (HD / 4); it += blockDim.x) {
+      const int r = split * per + it / (HD / 4), c4 = it % (HD / 4);
+      const int pl = r / hpg, head = r % hpg;
+      if (pl >= nb || seg_of[pl] < 0) continue;
+      const float* rb = base + static_cast<long long>(r) * (HD + 4);
+      float2 ml[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        ml[q] = q < KS ? __ldcg(reinterpret_cast<const float2*>(rb + q * sstr + HD)) : make_float2(-1e30f, 0.f);
+      float4 t[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        t[q] = q < KS ? __ldcg(reinterpret_cast<const float4*>(rb + q * sstr) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float M = -1e30f;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) M = fmaxf(M, ml[q].x);
+      float lt = 0.f;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (q >= KS) break;
+        const float sc = ex2(ml[q].x - M);
+        lt += sc * ml[q].y;
+        acc.x += sc * t[q].x;
+        acc.y += sc * t[q].y;
+        acc.z += sc * t[q].z;
+        acc.w += sc * t[q].w;
+      }
+      const float inv = 1.0f / lt;
+      bf16* dst = o + (static_cast<long long>(b0 + pl) * nh + g * hpg + head) * HD + 4 * c4;
+      *reinterpret_cast<uint2*>(dst) = make_uint2(pack2(acc.x * inv, acc.y * inv), pack2(acc.z * inv, acc.w * inv));
+    }
+  }
   if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem);
   if (threadIdx.x == 0) {
     chain_mark(cst, 2);
@@ -397,24 +479,57 @@ bool make_tmap_q3d(TmaMap* out, const bf16* q, long long rows, int nh, int hd, i
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Key splits per row block: only when the tick's grid (row blocks x kv heads)
+// leaves most SMs idle, at least 2 key blocks per split, <= 8 splits (one
+// portable cluster) and <=
+// kPfTcMaxCtas CTAs in all (the workspace bound).
+int attention_prefill_tc_splits(int R_cap, int nh, int nkv, int nblocks) {
+  static const int cap = [] {  // MOA_PF_KSPLIT (A/B): max splits, 1 = off
+    const char* e = std::getenv("MOA_PF_KSPLIT");
+    return e ? std::max(1, std::min(8, std::atoi(e))) : 8;
+  }();
+  const int P = 128 / (nh / nkv);
+  const int base = (R_cap + P - 1) / P * nkv;
+  int KS = 1;
+  while (KS * 2 <= cap && base * KS * 2 <= kPfTcMaxCtas && nblocks / (KS * 2) >= 2) KS *= 2;
+  return KS;
+}
+
+long long attention_prefill_tc_ws_floats(int hd) { return static_cast<long long>(kPfTcMaxCtas) * 128 * (hd + 4); }
+
 bool attention_prefill_tc_supported(int nh, int nkv, int hd) {
   return (hd == 64 || hd == 128) && nh % nkv == 0 && 128 % (nh / nkv) == 0 && nh / nkv <= 16;
 }
 
 void attention_prefill_tc(const TmaMap& qmap, const TmaMap& kmap, const TmaMap& vmap, const RowDesc* rows, int R_cap,
                           const int* meta, int nh, int nkv, int hd, long long kv_stride, long long layer_off,
-                          int max_ctx, bf16* o, cudaStream_t st) {
+                          int max_ctx, bf16* o, cudaStream_t st, int KS, float* ws) {
   if (R_cap <= 0) return;
   const int P = 128 / (nh / nkv);
+  if (KS < 1 || KS > 8 || (KS > 1 && ((R_cap + P - 1) / P * nkv * KS > kPfTcMaxCtas || !ws))) {
+    std::fprintf(stderr, "attention_prefill_tc: %d key splits exceed the workspace\n", KS);
+    std::abort();
+  }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((R_cap + P - 1) / P, nkv);
+  cfg.gridDim = dim3((R_cap + P - 1) / P, nkv, KS);
   cfg.blockDim = dim3(192);
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (KS > 1) {  // the KS key splits of a row block: one cluster
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 1;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = KS;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = na;
   auto go = [&](auto kern, int smem) {
     static std::set<const void*> attr;
     if (attr.insert(reinterpret_cast<const void*>(kern)).second) {
@@ -424,7 +539,7 @@ void attention_prefill_tc(const TmaMap& qmap, const TmaMap& kmap, const TmaMap& 
     cfg.dynamicSmemBytes = smem;
     cudaLaunchKernelEx(&cfg, kern, *reinterpret_cast<const CUtensorMap*>(&qmap),
                        *reinterpret_cast<const CUtensorMap*>(&kmap), *reinterpret_cast<const CUtensorMap*>(&vmap),
-                       rows, meta, nh, nkv, kv_stride, layer_off, max_ctx, o);
+                       rows, meta, nh, nkv, kv_stride, layer_off, max_ctx, o, ws);
   };
   if (hd == 128)
     go(attention_prefill_tc_kernel<128>, PfTc<128>::SMEM);

@@ -32,12 +32,14 @@ constexpr int kTileW = kM * kBK * 2;  // 16 KB
 constexpr int kTileX = kN * kBK * 2;  // 2 KB
 constexpr int kSmem = kStages * (kTileW + kTileX) + 1024 + 256;
 constexpr std::uint32_t kIdesc = idesc_bf16(kM, kN);
-// Wide variant for ticks of 17..32 rows (incremental-prefill chunks): the
-// same weight stream against a 32-row activation tile (MMA N = 32), a 4-stage
-// ring so two CTAs still fit an SM next to the 16 KB split-K landing buffer.
+// Wide variants for ticks of 17..32 / 33..64 rows (incremental-prefill
+// chunks): the same weight stream against a 32- / 64-row activation tile (MMA
+// N = 32 / 64), a 4- / 3-stage ring so two CTAs still fit an SM next to the
+// 16 / 32 KB split-K landing buffer.
 template <int NC>
 struct GvCfg {
-  static constexpr int stages = NC == 16 ? kStages : 4;
+  static constexpr int stages = NC == 16 ? kStages : NC == 32 ? 4 : 3;
+  static constexpr int tmem_cols = NC < 32 ? 32 : NC;
   static constexpr int tile_x = NC * kBK * 2;
   static constexpr int smem = stages * (kTileW + tile_x) + 1024 + 256;
   static constexpr std::uint32_t idesc = idesc_bf16(kM, NC);
@@ -308,7 +310,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   // reading its outputs.  Grids are sized to one CTA per SM, so this grid and
   // the next fit side by side.
   pdl_launch_dependents();
-  if (warp == 0) tmem_alloc<32>(tmem_slot);
+  if (warp == 0) tmem_alloc<G::tmem_cols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -416,8 +418,8 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
 #pragma unroll
     for (int r = 0; r < 16; ++r) u[r] *= inv_s[rb + r];
   };
-  // rows of the second half: their epilogue operands are loaded now (the
-  // first half's were preloaded while the weights streamed)
+  // rows past the first 16: their epilogue operands are loaded now (the
+  // first 16 rows' were preloaded while the weights streamed)
   auto run_epilogue = [&](int n_row) {
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
@@ -427,8 +429,8 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
         epilogue<EPI, NR < 16 ? NR : 16>(a, n_row, R, v[0], pre, 0);
       } else {
         EpiPre pre1;
-        epi_preload<EPI, 16>(a, n_row, R, pre1, 16);
-        epilogue<EPI, 16>(a, n_row, R, v[h], pre1, 16);
+        epi_preload<EPI, 16>(a, n_row, R, pre1, 16 * h);
+        epilogue<EPI, 16>(a, n_row, R, v[h], pre1, 16 * h);
       }
     }
   };
@@ -495,7 +497,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     chain_mark(cst, 2);
     chain_flush(cst, stag);
   }
-  if (warp == 0) tmem_dealloc<32>(tmem);
+  if (warp == 0) tmem_dealloc<G::tmem_cols>(tmem);
 }
 
 
@@ -902,7 +904,10 @@ static void (*gemv_tc_pick(int R))(CUtensorMap, CUtensorMap, GemvArgs, int, floa
   if (R <= 4) return gemv_tc_kernel<EPI, 4, 16>;
   if (R <= 8) return gemv_tc_kernel<EPI, 8, 16>;
   if (R <= 16 || EPI == kEpiLmStats) return gemv_tc_kernel<EPI, 16, 16>;
-  if constexpr (EPI != kEpiLmStats) return gemv_tc_kernel<EPI, 32, 32>;
+  if constexpr (EPI != kEpiLmStats) {
+    if (R <= kGemvTcMidRows) return gemv_tc_kernel<EPI, 32, 32>;
+    return gemv_tc_kernel<EPI, 64, 64>;
+  }
   return nullptr;
 }
 
@@ -915,7 +920,8 @@ void gemv_tc(const TmaMap& map_w, const TmaMap& map_x, const GemvArgs& a, float*
     case kEpiQkv: kern = gemv_tc_pick<kEpiQkv>(a.R); break;
     default: kern = gemv_tc_pick<kEpiLmStats>(a.R); break;
   }
-  const int smem = a.R > kN ? GvCfg<32>::smem : GvCfg<16>::smem;
+  const int box = gemv_tc_box_rows(a.R);
+  const int smem = box == 16 ? GvCfg<16>::smem : box == 32 ? GvCfg<32>::smem : GvCfg<64>::smem;
   static std::set<const void*> attr;
   if (attr.insert(reinterpret_cast<const void*>(kern)).second) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

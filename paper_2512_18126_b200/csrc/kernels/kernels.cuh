@@ -144,8 +144,12 @@ constexpr int kTcMinRows = 17;  // ticks with more rows than the swap-AB GEMV ho
 // programmatic dependent launch: weight tiles stream before the previous
 // kernel has finished.
 constexpr int kGemvTcRows = 16;
-// ... and its wide variant (MMA N = 32) for ticks of 17..32 rows (incremental-prefill chunks)
-constexpr int kGemvTcWideRows = 32;
+// ... and its wide variants (MMA N = 32 / 64) for ticks of 17..32 / 33..64 rows
+// (incremental-prefill chunks: one or two 32-token chunks of a model per tick)
+constexpr int kGemvTcMidRows = 32;
+constexpr int kGemvTcWideRows = 64;
+// rows of the activation tile (the TMA box) the swap-AB GEMV uses for R rows
+constexpr int gemv_tc_box_rows(int R) { return R <= kGemvTcRows ? kGemvTcRows : R <= kGemvTcMidRows ? kGemvTcMidRows : kGemvTcWideRows; }
 bool gemv_tc_supported(const GemvArgs& a);
 // gemv_tc with X = fp32 residual rows normalised in-kernel (a.X, a.g, a.eps,
 // a.ssq): no separate rmsnorm launch
@@ -216,10 +220,15 @@ void attention_prefill(const bf16* q, const RowDesc* rows, int R_cap, const int*
 // [rows][nh][hd]; kmap / vmap as for attention_decode_tma.  Rows alone in
 // their run are skipped (pair with the per-row kernel, skip_runs = true).
 bool make_tmap_q3d(TmaMap* out, const bf16* q, long long rows, int nh, int hd, int hpg);
+// Key splits (KS <= 8): grid.z = KS CTAs per row block (one cluster), fp32
+// partials through ws (attention_prefill_tc_ws_floats).
 bool attention_prefill_tc_supported(int nh, int nkv, int hd);
+constexpr int kPfTcMaxCtas = 2 * 148;  // key-split grids: at most two CTAs per SM
+int attention_prefill_tc_splits(int R_cap, int nh, int nkv, int nblocks);
+long long attention_prefill_tc_ws_floats(int hd);
 void attention_prefill_tc(const TmaMap& qmap, const TmaMap& kmap, const TmaMap& vmap, const RowDesc* rows, int R_cap,
                           const int* meta, int nh, int nkv, int hd, long long kv_stride, long long layer_off,
-                          int max_ctx, bf16* o, cudaStream_t st);
+                          int max_ctx, bf16* o, cudaStream_t st, int KS = 1, float* ws = nullptr);
 
 // Decode ticks of small agents (every row the only row of its agent):
 // RMSNorm + QKV + RoPE + KV append + attention in one launch, CTA = (row, kv

@@ -110,13 +110,14 @@ def test_gemm_tc_vs_torch_fp32(torch_cuda, M, N, K):
 
 @pytest.mark.parametrize("R,N,K", [(1, 3072, 2048), (8, 16384, 2048), (16, 2048, 8192), (3, 50000, 2048),
                                    (5, 6144, 4096), (17, 3072, 2048), (24, 6144, 4096), (32, 4096, 14336),
-                                   (32, 28672, 4096)])
+                                   (32, 28672, 4096), (33, 3072, 2048), (48, 6144, 4096), (64, 4096, 14336),
+                                   (64, 28672, 4096), (40, 2048, 8192)])
 def test_gemv_tc_vs_torch_fp32(torch_cuda, R, N, K):
-    """Swap-AB tensor-core decode GEMV (cluster split-K); 17..32 rows: its
-    wide (MMA N = 32) variant for incremental-prefill chunks."""
+    """Swap-AB tensor-core decode GEMV (cluster split-K); 17..32 / 33..64
+    rows: its wide (MMA N = 32 / 64) variants for incremental-prefill chunks."""
     torch = torch_cuda
     g = torch.Generator(device="cuda").manual_seed(R + N + K)
-    A = torch.randn(16 if R <= 16 else 32, K, device="cuda", generator=g).to(torch.bfloat16)
+    A = torch.randn(16 if R <= 16 else 32 if R <= 32 else 64, K, device="cuda", generator=g).to(torch.bfloat16)
     W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
     out = torch.full((R, N), float("nan"), device="cuda")
     for _ in range(2):  # second call re-uses the zeroed split counters
@@ -214,7 +215,11 @@ def test_attention_kernels_match_torch(torch_cuda, nh, nkv, hd, max_ctx):
     # mode bit 0: tiled prefill kernel + per-row kernel for the rows alone in their run
     # bit 1: the per-row kernel is the TMA-staged one; bit 2: the cluster-split kernel, bits 8-15 its splits
     # bit 3 (with bit 0): the runs by the tcgen05 prefill kernel
-    for mode in (1, 0, 3, 2, 5, 4, 4 | (1 << 8), 4 | (2 << 8), 4 | (8 << 8), 5 | (8 << 8), 13, 9):
+    # bits 16-23 (with bits 0 and 3): key splits of the tcgen05 prefill kernel
+    P = 128 // (nh // nkv)
+    ks_ok = [ks for ks in (2, 4, 8) if -(-R // P) * nkv * ks <= 296]
+    for mode in (1, 0, 3, 2, 5, 4, 4 | (1 << 8), 4 | (2 << 8), 4 | (8 << 8), 5 | (8 << 8), 13, 9) + \
+            tuple(9 | (ks << 16) for ks in ks_ok) + tuple(13 | (ks << 16) for ks in ks_ok):
         out = torch.zeros(R, nh, hd, dtype=torch.bfloat16, device="cuda")
         capi.check(capi.lib().moa_k_attention(q.data_ptr(), rd.data_ptr(), R, meta.data_ptr(), nh, nkv, hd,
                                               kpool.data_ptr(), vpool.data_ptr(), kv_stride, max_ctx, out.data_ptr(),
@@ -222,6 +227,46 @@ def test_attention_kernels_match_torch(torch_cuda, nh, nkv, hd, max_ctx):
         torch.cuda.synchronize()
         err = float((out.float() - ref).abs().max())
         assert err < 2e-2, (mode, err)
+
+
+@pytest.mark.parametrize("nh,nkv,hd", [(32, 8, 128), (32, 8, 64)])
+def test_prefill_attention_key_splits_on_chunk_ticks(torch_cuda, nh, nkv, hd):
+    """Incremental-prefill chunk ticks (a few 32-row runs deep into the
+    context, plus a decode row): the tcgen05 prefill attention with its keys
+    split over 1..8 CTAs per row block against fp32 torch; every split count
+    within bf16 rounding of the unsplit kernel."""
+    torch = torch_cuda
+    max_ctx = 4096
+    g = torch.Generator(device="cpu").manual_seed(11 + hd)
+    slots = 3
+    kv_stride = nkv * max_ctx * hd
+    kpool = (torch.randn(slots * kv_stride, generator=g) * 0.5).to(torch.bfloat16).cuda()
+    vpool = torch.randn(slots * kv_stride, generator=g).to(torch.bfloat16).cuda()
+    rows = [(0, p) for p in range(2300, 2332)] + [(1, p) for p in range(1000, 1032)] + [(2, 3000)]
+    R = len(rows)
+    q = torch.randn(R, nh, hd, generator=g).to(torch.bfloat16).cuda()
+    rd = torch.tensor([[kv, pos, 0, 0] for kv, pos in rows], dtype=torch.int32).cuda()
+    meta = torch.tensor([R, 0, max(p for _, p in rows)], dtype=torch.int32).cuda()
+    K = kpool.float().view(slots, nkv, max_ctx, hd)
+    V = vpool.float().view(slots, nkv, max_ctx, hd)
+    ref = torch.empty(R, nh, hd, device="cuda")
+    for i, (kv, pos) in enumerate(rows):
+        kh = torch.arange(nh, device="cuda") // (nh // nkv)
+        sc = torch.einsum("hd,hkd->hk", q[i].float(), K[kv, kh, :pos + 1]) / math.sqrt(hd)
+        ref[i] = torch.einsum("hk,hkd->hd", torch.softmax(sc, -1), V[kv, kh, :pos + 1])
+    outs = {}
+    for ks in (1, 2, 4, 8):
+        out = torch.zeros(R, nh, hd, dtype=torch.bfloat16, device="cuda")
+        for _ in range(2):
+            capi.check(capi.lib().moa_k_attention(q.data_ptr(), rd.data_ptr(), R, meta.data_ptr(), nh, nkv, hd,
+                                                  kpool.data_ptr(), vpool.data_ptr(), kv_stride, max_ctx,
+                                                  out.data_ptr(), 13 | (ks << 16), 0, slots))
+        torch.cuda.synchronize()
+        err = float((out.float() - ref).abs().max())
+        assert err < 2e-2, (ks, err)
+        outs[ks] = out.float()
+    for ks in (2, 4, 8):
+        assert float((outs[ks] - outs[1]).abs().max()) < 2e-2, ks
 
 
 def test_single_agent_decode_matches_oracle():
