@@ -61,34 +61,31 @@ struct EpiPre {
 // QKV launch).
 template <int EPI, int NR>
 __device__ __forceinline__ void epi_preload(const GemvArgs& a, int n, int R, EpiPre& p, int rb = 0) {
-  // rows rb .. rb + NR - 1 (NR <= 16) of the tick
+  // rows rb .. rb + NR - 1 (NR <= 16) of the tick; predicated loads (no early
+  // exit), so every row's load is in flight at once: one L2 round trip per
+  // chunk instead of one (two for the QKV RoPE factors) per row -- the wide
+  // variants run this on their critical path for the rows past the first 16
   if (EPI == kEpiResidual) {
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      if (rb + r >= R) break;
-      p.res[r] = n < a.N ? __ldcg(a.out + static_cast<long long>(rb + r) * a.N + n) : 0.f;
-    }
+    for (int r = 0; r < NR; ++r)
+      p.res[r] = (rb + r < R && n < a.N) ? __ldcg(a.out + static_cast<long long>(rb + r) * a.N + n) : 0.f;
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      if (rb + r >= R) break;
-      asm volatile("" ::"f"(p.res[r]));
-    }
+    for (int r = 0; r < NR; ++r) asm volatile("" ::"f"(p.res[r]));
   } else if (EPI == kEpiQkv) {
     const int hd = a.hd, half = hd / 2, qk_cols = (a.nh + a.nkv) * hd;
     const int e = (n % hd) / 2;
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      if (rb + r >= R) break;
-      const RowDesc rd = a.rows[rb + r];
-      p.kv[r] = rd.kv;
-      p.pos[r] = rd.pos;
-      p.cs[r] = n < qk_cols ? __ldg(a.rope + static_cast<long long>(rd.pos) * half + e) : make_float2(1.f, 0.f);
+      const int2 kp = rb + r < R ? *reinterpret_cast<const int2*>(a.rows + rb + r) : make_int2(0, 0);
+      p.kv[r] = kp.x;
+      p.pos[r] = kp.y;
     }
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      if (rb + r >= R) break;
-      asm volatile("" ::"f"(p.cs[r].x), "f"(p.cs[r].y), "r"(p.kv[r]), "r"(p.pos[r]));
-    }
+    for (int r = 0; r < NR; ++r)
+      p.cs[r] = (rb + r < R && n < qk_cols) ? __ldg(a.rope + static_cast<long long>(p.pos[r]) * half + e)
+                                             : make_float2(1.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) asm volatile("" ::"f"(p.cs[r].x), "f"(p.cs[r].y), "r"(p.kv[r]), "r"(p.pos[r]));
   }
 }
 
@@ -418,19 +415,30 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
 #pragma unroll
     for (int r = 0; r < 16; ++r) u[r] *= inv_s[rb + r];
   };
-  // rows past the first 16: their epilogue operands are loaded now (the
-  // first 16 rows' were preloaded while the weights streamed)
+  // Wide variants: the 16-row chunks in a rolled loop, the epilogue operands
+  // of rows past the first 16 loaded per chunk (the first 16 rows' were
+  // preloaded while the weights streamed).  Unrolled, the 64-row QKV epilogue
+  // was ~20k instructions run once from a cold instruction cache (ncu: 57% of
+  // the warps' samples at the final barrier waiting on it, 76 us per 8B launch).
   auto run_epilogue = [&](int n_row) {
+    if constexpr (NH == 1) {
+      scale_rows(v[0], 0);
+      epilogue<EPI, NR < 16 ? NR : 16>(a, n_row, R, v[0], pre, 0);
+    } else {
+      // one copy of the 16-row epilogue, cold once, then warm
+#pragma unroll 1
+      for (int h = 0; h < NH; ++h) {
+        if (16 * h >= R) break;
+        float u[16];
 #pragma unroll
-    for (int h = 0; h < NH; ++h) {
-      if (16 * h >= R) break;
-      scale_rows(v[h], 16 * h);
-      if (h == 0) {
-        epilogue<EPI, NR < 16 ? NR : 16>(a, n_row, R, v[0], pre, 0);
-      } else {
-        EpiPre pre1;
-        epi_preload<EPI, 16>(a, n_row, R, pre1, 16 * h);
-        epilogue<EPI, 16>(a, n_row, R, v[h], pre1, 16 * h);
+        for (int hh = 0; hh < NH; ++hh)
+          if (hh == h)
+#pragma unroll
+            for (int r = 0; r < 16; ++r) u[r] = v[hh][r];
+        scale_rows(u, 16 * h);
+        EpiPre p1 = pre;
+        if (h > 0) epi_preload<EPI, 16>(a, n_row, R, p1, 16 * h);
+        epilogue<EPI, 16>(a, n_row, R, u, p1, 16 * h);
       }
     }
   };
@@ -438,9 +446,12 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     static_assert(NC == 16, "LM statistics: 16 rows");
     scale_rows(v[0], 0);
     lm_stats_epilogue(a, n, R, v[0], tile, gridDim.x);  // S == 1 for the LM head
-  } else if (S == 1) {
-    run_epilogue(n);
   } else {
+  // one call site of the (inlined) epilogue: run by every thread (S == 1) or
+  // by the warps holding reduced rows (split-K)
+  int n_run = n;
+  bool run = true;
+  if (S > 1) {
     // Split-K inside a thread-block cluster (the S CTAs of this weight tile):
     // CTA q reduces weight rows [q*128/S, (q+1)*128/S).  Every CTA pushes the
     // partial rows owned by q straight into q's landing buffer with st.async
@@ -487,8 +498,12 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
             }
         }
       if (threadIdx.x == 0) chain_mark(cst, 6);
-      run_epilogue(mine ? m0 + wr : a.N);
+      n_run = mine ? m0 + wr : a.N;
+    } else {
+      run = false;
     }
+  }
+  if (run) run_epilogue(n_run);
   }
   if (threadIdx.x == 0) chain_mark(cst, 7);  // this thread's epilogue done
   tc_fence_before();
