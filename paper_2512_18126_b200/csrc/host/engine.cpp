@@ -58,10 +58,23 @@ GpuEngine::GpuEngine(std::vector<ModelSpec> models, std::vector<int> agents_per_
   }
   MOA_CUDA(cudaEventCreate(&start_ev_));
   MOA_CUDA(cudaEventCreateWithFlags(&tick_fork_, cudaEventDisableTiming));
+  // Per-model forward streams, equal priorities by default.  MOA_STREAM_PRIO
+  // (A/B): 1 = the model with the largest weight stream gets the highest
+  // priority (its chain is the longest of a fanned-out tick), 2 = every other
+  // model does.  Measured on C3's leaf ticks (8B + 1B): 1 is 6% slower (p50
+  // 3.59 vs 3.39 ms).
+  int prio_lo = 0, prio_hi = 0;
+  MOA_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  double big = 0.0;
+  for (const auto& dm : models_) big = std::max(big, dm->spec().weight_bytes());
+  int prio_mode = 0;
+  if (const char* e = std::getenv("MOA_STREAM_PRIO")) prio_mode = std::atoi(e);
   for (std::size_t m = 0; m < models_.size(); ++m) {
     cudaStream_t s2;
     cudaEvent_t e2;
-    MOA_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    const bool is_big = models_[m]->spec().weight_bytes() >= big;
+    const bool first = models_.size() > 1 && ((prio_mode == 1 && is_big) || (prio_mode == 2 && !is_big));
+    MOA_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, first ? prio_hi : prio_lo));
     MOA_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
     mstreams_.push_back(s2);
     mdone_.push_back(e2);

@@ -475,7 +475,42 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
               : "memory");
     }
     if (threadIdx.x == 0) chain_mark(cst, 5);
-    if (warp * 32 < per) {  // warps holding at least one reduced row (whole warps: the epilogue shuffles)
+    if constexpr (NH > 1) {
+      // Wide variants: the reduced rows' epilogues are spread over all four
+      // warps as units of (32 reduced rows, one 16-column chunk): with one
+      // warp per CTA holding reduced rows, the 64-row QKV epilogue ran ~5.7k
+      // dependent instructions on a single warp (ncu: the other warps' samples
+      // at the final barrier, 57% of the kernel).  Same split order, same sums.
+      mbar_wait(&land_bar, 0);
+      const int units = (per + 31) / 32 * NH;
+#pragma unroll 1
+      for (int un = warp; un < units; un += 4) {
+        const int h = un % NH, rr = un / NH * 32 + lane;
+        if (16 * h >= R) continue;  // warp-uniform
+        const bool mine = rr < per;
+        float u[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) u[i] = 0.f;
+        if (mine)
+          for (int src = 0; src < S; ++src) {
+            const float4* p = reinterpret_cast<const float4*>(land + (src * per + rr) * NC + 16 * h);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float4 t = p[i];
+              u[4 * i] += t.x;
+              u[4 * i + 1] += t.y;
+              u[4 * i + 2] += t.z;
+              u[4 * i + 3] += t.w;
+            }
+          }
+        const int nn = mine ? m0 + split * per + rr : a.N;
+        scale_rows(u, 16 * h);
+        EpiPre p1;
+        epi_preload<EPI, 16>(a, nn, R, p1, 16 * h);
+        epilogue<EPI, 16>(a, nn, R, u, p1, 16 * h);
+      }
+      run = false;
+    } else if (warp * 32 < per) {  // warps holding at least one reduced row (whole warps: the epilogue shuffles)
       mbar_wait(&land_bar, 0);
       const bool mine = row < per;
       const int wr = split * per + (mine ? row : 0);
