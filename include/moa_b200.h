@@ -378,14 +378,16 @@ int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, 
  * the per-row kernel is the TMA-staged one (attn_decode.cu) instead of the register-staged one; bit 2: the
  * cluster-split kernel (attn_decode.cu) with (prefill >> 8) & 0xff splits (0: the engine's heuristic); bit 3
  * (with bit 0): the runs by the tcgen05 prefill kernel (attn_prefill_tc.cu) instead of the mma.sync one; bit 4
- * (with bit 0): no per-row kernel (rows alone in their run left untouched: timing the prefill kernels). */
+ * (with bit 0): no per-row kernel (rows alone in their run left untouched: timing the prefill kernels);
+ * (prefill >> 16) & 0xff (with bits 0 and 3): key splits of the tcgen05 prefill kernel, 1..8 (0: 1), at most
+ * 296 CTAs in all (row blocks x kv heads x splits). */
 int moa_k_attention(uintptr_t q, uintptr_t rows, int R, uintptr_t meta, int nh, int nkv, int hd, uintptr_t kpool,
                     uintptr_t vpool, long long kv_stride, int max_ctx, uintptr_t out, int prefill, uintptr_t stream,
                     int slots);
 int moa_k_noop(uintptr_t p, int ctas, uintptr_t stream); /* trivial PDL kernel: launch-chain cost probe */
 int moa_k_chain_stamp(uintptr_t buf); /* debug: decode-chain per-CTA globaltimer stamps (stamp.cuh), 0 = off */
-/* Swap-AB tensor-core GEMV out[R][N] = A[:R] . W^T, fp32 out; A holds 16 rows (R <= 16) or 32 (17 <= R <= 32,
- * the wide variant the engine runs for incremental-prefill chunks). */
+/* Swap-AB tensor-core GEMV out[R][N] = A[:R] . W^T, fp32 out; A holds 16 rows (R <= 16), 32 (17 <= R <= 32)
+ * or 64 (33 <= R <= 64: the wide variants the engine runs for incremental-prefill chunks). */
 int moa_k_gemv_tc(uintptr_t A, int R, uintptr_t W, int N, int K, uintptr_t out, uintptr_t stream);
 /* Hash-uniform weight init of a logical [rows][cols] tensor into a device row
  * layout (0 identity, 1 RoPE-pair interleave per hd rows, 2 even rows, 3 odd rows). */
