@@ -96,6 +96,42 @@ def test_layer1_residual_after_prefill_and_decode(shape, seed):
         assert err <= RESID_RTOL, (shape, what, err)
 
 
+@pytest.mark.parametrize("shape,seed", [("8b", 3), ("1b", 1)])
+def test_layer1_residual_on_chunk_ticks(shape, seed):
+    """Incremental-prefill chunk ticks deep into a 2048-token context (the
+    successor side of the pipelined overlap): 64- and 48-row ticks (the MMA
+    N = 64 swap-AB GEMVs), 32- and 20-row ticks (N = 32), their runs through
+    the key-split tcgen05 prefill attention -- each chunk's layer-1 residual
+    rows elementwise against the oracle's layer output."""
+    P, chunks = 2048, [64, 48, 32, 20, 64]
+    prompt = synth_tokens(13, "chunks", P + sum(chunks))
+    eng = capi.Engine([capi.model_spec("big", shape, seed, max_agents=1, n_layers=1)],
+                      max_ctx=len(prompt) + 64, max_out=8)
+    got = []
+    try:
+        a = (2, 0)
+        eng.add_agent(a, 0)
+        eng.prefill_only(a, 0, prompt[:P])
+        eng.step()
+        pos = P
+        for c in chunks:
+            eng.prefill_only(a, pos, prompt[pos:pos + c])
+            eng.step()
+            got.append(eng.read_residual(0, c))
+            pos += c
+    finally:
+        eng.close()
+    m = _cpu("big", shape, seed, n_layers=1)
+    kv = m.new_kv()
+    ref = m.layers([(kv, i, t) for i, t in enumerate(prompt)])
+    pos = P
+    for c, g in zip(chunks, got):
+        want = ref[pos:pos + c]
+        err = float(np.abs(g - want).max()) / float(np.sqrt(np.mean(want.astype(np.float64) ** 2)))
+        assert err <= RESID_RTOL, (shape, c, err)
+        pos += c
+
+
 def test_8b_width_agent_2k_prompt():
     """2-layer 8B-width agent: 2048-token prompt (tcgen05 prefill + tiled
     attention), 48 greedy tokens (norm-unfolded swap-AB decode chain, GQA
