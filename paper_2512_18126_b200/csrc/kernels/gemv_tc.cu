@@ -447,98 +447,98 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     scale_rows(v[0], 0);
     lm_stats_epilogue(a, n, R, v[0], tile, gridDim.x);  // S == 1 for the LM head
   } else {
-  // one call site of the (inlined) epilogue: run by every thread (S == 1) or
-  // by the warps holding reduced rows (split-K)
-  int n_run = n;
-  bool run = true;
-  if (S > 1) {
-    // Split-K inside a thread-block cluster (the S CTAs of this weight tile):
-    // CTA q reduces weight rows [q*128/S, (q+1)*128/S).  Every CTA pushes the
-    // partial rows owned by q straight into q's landing buffer with st.async
-    // (DSMEM stores that complete transactions on q's mbarrier), so a reducer
-    // waits only for its own data -- no cluster-wide barrier, no remote loads
-    // -- then sums the S partials in rank order (deterministic) and runs the
-    // epilogue of its rows.
-    const int q = row / per, rq = row % per;
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every landing barrier is initialised
-    {
-      const std::uint32_t dst = dsmem_addr(smem_u32(land + (split * per + rq) * NC), q);
-      const std::uint32_t bar = dsmem_addr(smem_u32(&land_bar), q);
-#pragma unroll
-      for (int h = 0; h < NH; ++h)
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          asm volatile(
-              "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
-                  dst + 64 * h + 16 * i),
-              "f"(v[h][4 * i]), "f"(v[h][4 * i + 1]), "f"(v[h][4 * i + 2]), "f"(v[h][4 * i + 3]), "r"(bar)
-              : "memory");
-    }
-    if (threadIdx.x == 0) chain_mark(cst, 5);
-    if constexpr (NH > 1) {
-      // Wide variants: the reduced rows' epilogues are spread over all four
-      // warps as units of (32 reduced rows, one 16-column chunk): with one
-      // warp per CTA holding reduced rows, the 64-row QKV epilogue ran ~5.7k
-      // dependent instructions on a single warp (ncu: the other warps' samples
-      // at the final barrier, 57% of the kernel).  Same split order, same sums.
-      mbar_wait(&land_bar, 0);
-      const int units = (per + 31) / 32 * NH;
-#pragma unroll 1
-      for (int un = warp; un < units; un += 4) {
-        const int h = un % NH, rr = un / NH * 32 + lane;
-        if (16 * h >= R) continue;  // warp-uniform
-        const bool mine = rr < per;
-        float u[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) u[i] = 0.f;
+    // one call site of the (inlined) epilogue: run by every thread (S == 1) or
+    // by the warps holding reduced rows (split-K)
+    int n_run = n;
+    bool run = true;
+    if (S > 1) {
+      // Split-K inside a thread-block cluster (the S CTAs of this weight tile):
+      // CTA q reduces weight rows [q*128/S, (q+1)*128/S).  Every CTA pushes the
+      // partial rows owned by q straight into q's landing buffer with st.async
+      // (DSMEM stores that complete transactions on q's mbarrier), so a reducer
+      // waits only for its own data -- no cluster-wide barrier, no remote loads
+      // -- then sums the S partials in rank order (deterministic) and runs the
+      // epilogue of its rows.
+      const int q = row / per, rq = row % per;
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every landing barrier is initialised
+      {
+        const std::uint32_t dst = dsmem_addr(smem_u32(land + (split * per + rq) * NC), q);
+        const std::uint32_t bar = dsmem_addr(smem_u32(&land_bar), q);
+  #pragma unroll
+        for (int h = 0; h < NH; ++h)
+  #pragma unroll
+          for (int i = 0; i < 4; ++i)
+            asm volatile(
+                "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                    dst + 64 * h + 16 * i),
+                "f"(v[h][4 * i]), "f"(v[h][4 * i + 1]), "f"(v[h][4 * i + 2]), "f"(v[h][4 * i + 3]), "r"(bar)
+                : "memory");
+      }
+      if (threadIdx.x == 0) chain_mark(cst, 5);
+      if constexpr (NH > 1) {
+        // Wide variants: the reduced rows' epilogues are spread over all four
+        // warps as units of (32 reduced rows, one 16-column chunk): with one
+        // warp per CTA holding reduced rows, the 64-row QKV epilogue ran ~5.7k
+        // dependent instructions on a single warp (ncu: the other warps' samples
+        // at the final barrier, 57% of the kernel).  Same split order, same sums.
+        mbar_wait(&land_bar, 0);
+        const int units = (per + 31) / 32 * NH;
+  #pragma unroll 1
+        for (int un = warp; un < units; un += 4) {
+          const int h = un % NH, rr = un / NH * 32 + lane;
+          if (16 * h >= R) continue;  // warp-uniform
+          const bool mine = rr < per;
+          float u[16];
+  #pragma unroll
+          for (int i = 0; i < 16; ++i) u[i] = 0.f;
+          if (mine)
+            for (int src = 0; src < S; ++src) {
+              const float4* p = reinterpret_cast<const float4*>(land + (src * per + rr) * NC + 16 * h);
+  #pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float4 t = p[i];
+                u[4 * i] += t.x;
+                u[4 * i + 1] += t.y;
+                u[4 * i + 2] += t.z;
+                u[4 * i + 3] += t.w;
+              }
+            }
+          const int nn = mine ? m0 + split * per + rr : a.N;
+          scale_rows(u, 16 * h);
+          EpiPre p1;
+          epi_preload<EPI, 16>(a, nn, R, p1, 16 * h);
+          epilogue<EPI, 16>(a, nn, R, u, p1, 16 * h);
+        }
+        run = false;
+      } else if (warp * 32 < per) {  // warps holding at least one reduced row (whole warps: the epilogue shuffles)
+        mbar_wait(&land_bar, 0);
+        const bool mine = row < per;
+        const int wr = split * per + (mine ? row : 0);
+  #pragma unroll
+        for (int h = 0; h < NH; ++h)
+  #pragma unroll
+          for (int i = 0; i < 16; ++i) v[h][i] = 0.f;
         if (mine)
           for (int src = 0; src < S; ++src) {
-            const float4* p = reinterpret_cast<const float4*>(land + (src * per + rr) * NC + 16 * h);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float4 t = p[i];
-              u[4 * i] += t.x;
-              u[4 * i + 1] += t.y;
-              u[4 * i + 2] += t.z;
-              u[4 * i + 3] += t.w;
-            }
+            const float4* p = reinterpret_cast<const float4*>(land + (src * per + row) * NC);
+  #pragma unroll
+            for (int h = 0; h < NH; ++h)
+  #pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float4 t = p[4 * h + i];
+                v[h][4 * i] += t.x;
+                v[h][4 * i + 1] += t.y;
+                v[h][4 * i + 2] += t.z;
+                v[h][4 * i + 3] += t.w;
+              }
           }
-        const int nn = mine ? m0 + split * per + rr : a.N;
-        scale_rows(u, 16 * h);
-        EpiPre p1;
-        epi_preload<EPI, 16>(a, nn, R, p1, 16 * h);
-        epilogue<EPI, 16>(a, nn, R, u, p1, 16 * h);
+        if (threadIdx.x == 0) chain_mark(cst, 6);
+        n_run = mine ? m0 + wr : a.N;
+      } else {
+        run = false;
       }
-      run = false;
-    } else if (warp * 32 < per) {  // warps holding at least one reduced row (whole warps: the epilogue shuffles)
-      mbar_wait(&land_bar, 0);
-      const bool mine = row < per;
-      const int wr = split * per + (mine ? row : 0);
-#pragma unroll
-      for (int h = 0; h < NH; ++h)
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[h][i] = 0.f;
-      if (mine)
-        for (int src = 0; src < S; ++src) {
-          const float4* p = reinterpret_cast<const float4*>(land + (src * per + row) * NC);
-#pragma unroll
-          for (int h = 0; h < NH; ++h)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float4 t = p[4 * h + i];
-              v[h][4 * i] += t.x;
-              v[h][4 * i + 1] += t.y;
-              v[h][4 * i + 2] += t.z;
-              v[h][4 * i + 3] += t.w;
-            }
-        }
-      if (threadIdx.x == 0) chain_mark(cst, 6);
-      n_run = mine ? m0 + wr : a.N;
-    } else {
-      run = false;
     }
-  }
-  if (run) run_epilogue(n_run);
+    if (run) run_epilogue(n_run);
   }
   if (threadIdx.x == 0) chain_mark(cst, 7);  // this thread's epilogue done
   tc_fence_before();
