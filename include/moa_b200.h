@@ -376,7 +376,7 @@ int moa_k_gemm_tc(uintptr_t A, int M, uintptr_t W, int N, int K, uintptr_t out, 
  * q[R][nh][hd] bf16, rows = moa row descriptors {kv, pos, tok, out}, meta[0] = live rows.  prefill bit 0:
  * the tiled prefill kernel (rows in same-agent runs) + the per-row kernel for rows alone in their run; bit 1:
  * the per-row kernel is the TMA-staged one (attn_decode.cu) instead of the register-staged one; bit 2: the
- * cluster-split kernel (attn_decode.cu) with (prefill >> 8) & 0xff splits (0: the engine's heuristic); bit 3
+ * cluster-split kernel (attn_decode.cu) with (prefill >> 8) & 0xff splits (1..16; 0: the engine's choice); bit 3
  * (with bit 0): the runs by the tcgen05 prefill kernel (attn_prefill_tc.cu) instead of the mma.sync one; bit 4
  * (with bit 0): no per-row kernel (rows alone in their run left untouched: timing the prefill kernels);
  * (prefill >> 16) & 0xff (with bits 0 and 3): key splits of the tcgen05 prefill kernel, 1..8 (0: 1), at most

@@ -1033,7 +1033,7 @@ int moa_k_attention(uintptr_t q, uintptr_t rows, int R, uintptr_t meta, int nh, 
       moa::k::TmaMap km, vm;
       if (!moa::k::make_tmap_bf16(&km, kp, pool_rows, hd, 64) || !moa::k::make_tmap_bf16(&vm, vp, pool_rows, hd, 64))
         throw moa::DeviceError("attention: TMA map creation failed");
-      if (ns_req > 8 || (ns_req & (ns_req - 1))) throw moa::ValidationError("attention: splits must be 1, 2, 4 or 8");
+      if (ns_req > 16 || (ns_req & (ns_req - 1))) throw moa::ValidationError("attention: splits must be 1, 2, 4, 8 or 16");
       const int ns = ns_req ? ns_req : moa::k::attention_decode_cluster_splits(R, nkv, (max_ctx + 63) / 64);
       moa::k::attention_decode_cluster(km, vm, qp, rp, R, ns, mp, nh, nkv, hd, kv_stride, 0, max_ctx, op, st,
                                        prefill != 0);

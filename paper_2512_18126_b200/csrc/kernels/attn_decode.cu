@@ -363,7 +363,7 @@ attention_decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap, const 
   // partials pushed here by every rank of the cluster (st.async): this CTA's
   // slice of the outputs [NS][chunk] and every rank's (max, sum) per q head
   __shared__ __align__(16) float land_o[8 * 256];
-  __shared__ __align__(16) float land_ml[8 * 16 * 2];
+  __shared__ __align__(16) float land_ml[16 * 16 * 2];
   __shared__ __align__(8) std::uint64_t land_bar;
   __shared__ int first_new_s;
   __shared__ unsigned long long cst[kChainPhases];
@@ -679,7 +679,11 @@ int attention_decode_cluster_splits(int rcap, int nkv, int nbox_cap) {
   // only on its own context length, never on the tick's row count -- schedule
   // modes that batch rows differently decode identical tokens.
   (void)rcap, (void)nkv, (void)nbox_cap;
-  return 8;
+  static const int ns = [] {  // MOA_ATTN_SPLITS (A/B): 8 (portable cluster) or 16 (non-portable)
+    const char* e = std::getenv("MOA_ATTN_SPLITS");
+    return e && std::atoi(e) == 16 ? 16 : 8;
+  }();
+  return ns;
 }
 
 bool attention_decode_cluster_supported(int nh, int nkv, int hd) {
@@ -707,6 +711,7 @@ void attention_decode_cluster(const TmaMap& kmap, const TmaMap& vmap, const bf16
     static std::set<const void*> attr;
     if (attr.insert(reinterpret_cast<const void*>(kern)).second) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       uniform_carveout(reinterpret_cast<const void*>(kern));
     }
     cfg.dynamicSmemBytes = smem;

@@ -218,7 +218,7 @@ def test_attention_kernels_match_torch(torch_cuda, nh, nkv, hd, max_ctx):
     # bits 16-23 (with bits 0 and 3): key splits of the tcgen05 prefill kernel
     P = 128 // (nh // nkv)
     ks_ok = [ks for ks in (2, 4, 8) if -(-R // P) * nkv * ks <= 296]
-    for mode in (1, 0, 3, 2, 5, 4, 4 | (1 << 8), 4 | (2 << 8), 4 | (8 << 8), 5 | (8 << 8), 13, 9) + \
+    for mode in (1, 0, 3, 2, 5, 4, 4 | (1 << 8), 4 | (2 << 8), 4 | (8 << 8), 5 | (8 << 8), 4 | (16 << 8), 13, 9) + \
             tuple(9 | (ks << 16) for ks in ks_ok) + tuple(13 | (ks << 16) for ks in ks_ok):
         out = torch.zeros(R, nh, hd, dtype=torch.bfloat16, device="cuda")
         capi.check(capi.lib().moa_k_attention(q.data_ptr(), rd.data_ptr(), R, meta.data_ptr(), nh, nkv, hd,
