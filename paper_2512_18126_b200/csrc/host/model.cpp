@@ -425,13 +425,15 @@ void DeviceModel::launch(int rcap, int nsplit, bool with_logits, const int* out_
     else
       k::gemm_tc(*map_a, map_w, g, st);
   };
-  // probes: decode-regime launches (rows <= 16) and prefill-regime ones
+  // probes: weight-streaming launches (decode and chunk-tick GEMVs) and prefill-regime ones
   // (tcgen05 GEMM / tiled attention) are separate kinds; bytes are the
   // launch's algorithmic (unique) bytes, flops its dense flops
   auto probe_begin = [&](int kind, double bytes, double flops = 0.0) {
     if (probes_) probes_->begin(kind, bytes, st, flops);
   };
-  auto gkind = [&](int dec, int pf) { return tc ? pf : dec; };
+  // (the wide swap-AB GEMVs of 17..64-row chunk ticks stream the weights like
+  // decode: HBM-bound kinds; the prefill kinds are the tcgen05 GEMM launches)
+  auto gkind = [&](int dec, int pf) { return tc && !swap_ab ? pf : dec; };
   const double Rv = live_R_;
   auto probe_end = [&]() {
     if (probes_) probes_->end(st);
